@@ -1,0 +1,203 @@
+"""Graphs of the BASELINE.json configurations and the SPEC desk-scale corpus
+(oracle side; test infrastructure only).  The C++ library builds the same
+graphs independently (ac_graph_block); tests compare the two documents.
+
+Kernel-granularity node kinds; weights use the nn.Linear
+layout W[out, in].  Block maths = SURVEY §8(c) O1; AlphaFold triangle
+attention follows AF2 supplement Alg. 13 (starting node) / Alg. 14 (ending
+node) — DESIGN.md reading R16.
+"""
+from __future__ import annotations
+
+import math
+
+from .graph import Builder, Graph
+
+
+def transformer(N, d, h, f=0, causal=False, dtype="bf16", attn_only=False, name="transformer",
+                eps=1e-5) -> Graph:
+    """Pre-LN block: a = LN1(x); q,k,v = a W + b; softmax(q k^T / sqrt(dh)) v;
+    x1 = x + o Wo + bo; (y = x1 + GELU(LN2(x1) W1 + b1) W2 + b2)."""
+    dh = d // h
+    B = Builder(name, dtype)
+    B.input("x", (N, d))
+    B.weight("ln1_g", (d,), "ln_gamma", d)
+    B.weight("ln1_b", (d,), "ln_beta", d)
+    for nm in ("q", "k", "v", "o"):
+        B.weight(f"w{nm}", (d, d), "matrix", d)
+        B.weight(f"b{nm}", (d,), "bias", d)
+    if not attn_only:
+        B.weight("ln2_g", (d,), "ln_gamma", d)
+        B.weight("ln2_b", (d,), "ln_beta", d)
+        B.weight("w1", (f, d), "matrix", d)
+        B.weight("b1", (f,), "bias", d)
+        B.weight("w2", (d, f), "matrix", f)
+        B.weight("b2", (d,), "bias", f)
+    B.op("layernorm", ["x", "ln1_g", "ln1_b"], "a", nid="ln1", naxes=1, eps=eps)
+    B.op("linear", ["a", "wq", "bq"], "q", nid="proj_q", kin=1, out=[h, dh], act="none", trans=0,
+         swap=0, bias=1, res=0)
+    B.op("linear", ["a", "wk", "bk"], "k", nid="proj_k", kin=1, out=[h, dh], act="none", trans=0,
+         swap=0, bias=1, res=0)
+    B.op("linear", ["a", "wv", "bv"], "vt", nid="proj_v", kin=1, out=[h, dh], act="none", trans=1,
+         swap=0, bias=1, res=0)
+    B.op("attn_scores", ["q", "k"], "s", nid="scores", scale=1.0 / math.sqrt(dh), causal=int(causal))
+    B.op("softmax", ["s"], "p", nid="softmax", dim=2)
+    B.op("attn_pv", ["p", "vt"], "o", nid="pv")
+    B.op("linear", ["o", "wo", "bo", "x"], "x1", nid="proj_o", kin=2, out=[d], act="none", trans=0,
+         swap=0, bias=1, res=1)
+    if attn_only:
+        B.output("x1")
+        return B.build()
+    B.op("layernorm", ["x1", "ln2_g", "ln2_b"], "c", nid="ln2", naxes=1, eps=eps)
+    B.op("linear", ["c", "w1", "b1"], "hid", nid="ffn1", kin=1, out=[f], act="gelu", trans=0, swap=0,
+         bias=1, res=0)
+    B.op("linear", ["hid", "w2", "b2", "x1"], "y", nid="ffn2", kin=1, out=[d], act="none", trans=0,
+         swap=0, bias=1, res=1)
+    B.output("y")
+    return B.build()
+
+
+def _tri_weights(B: Builder, pre: str, cz: int, H: int, c: int):
+    for nm, shp, role, fan in (("ln_g", (cz,), "ln_gamma", cz), ("ln_b", (cz,), "ln_beta", cz),
+                               ("wb", (H, cz), "matrix", cz), ("wq", (H * c, cz), "matrix", cz),
+                               ("wk", (H * c, cz), "matrix", cz), ("wv", (H * c, cz), "matrix", cz),
+                               ("wg", (H * c, cz), "matrix", cz), ("bg", (H * c,), "bias", cz),
+                               ("wo", (cz, H * c), "matrix", H * c), ("bo", (cz,), "bias", H * c)):
+        B.weight(pre + nm, shp, role, fan)
+
+
+def _tri_attention(B: Builder, z: str, pre: str, N: int, cz: int, H: int, c: int, ending: int,
+                   out: str, eps=1e-5):
+    zn, b, q, k, vt, g = (pre + s for s in ("zn", "bias", "q", "k", "vt", "g"))
+    B.op("layernorm", [z, pre + "ln_g", pre + "ln_b"], zn, nid=pre + "ln", naxes=1, eps=eps)
+    B.op("linear", [zn, pre + "wb"], b, nid=pre + "proj_b", kin=1, out=[H], act="none", trans=1,
+         swap=0, bias=0, res=0)
+    B.op("linear", [zn, pre + "wq"], q, nid=pre + "proj_q", kin=1, out=[H, c], act="none", trans=0,
+         swap=0, bias=0, res=0)
+    B.op("linear", [zn, pre + "wk"], k, nid=pre + "proj_k", kin=1, out=[H, c], act="none", trans=0,
+         swap=0, bias=0, res=0)
+    B.op("linear", [zn, pre + "wv"], vt, nid=pre + "proj_v", kin=1, out=[H, c], act="none", trans=1,
+         swap=int(ending), bias=0, res=0)
+    B.op("linear", [zn, pre + "wg", pre + "bg"], g, nid=pre + "proj_g", kin=1, out=[H, c],
+         act="sigmoid", trans=0, swap=0, bias=1, res=0)
+    B.op("tri_scores", [q, k, b], pre + "s", nid=pre + "scores", scale=1.0 / math.sqrt(c),
+         ending=int(ending))
+    B.op("softmax", [pre + "s"], pre + "p", nid=pre + "softmax", dim=3)
+    B.op("tri_pv", [pre + "p", vt, g], pre + "o", nid=pre + "pv", ending=int(ending))
+    B.op("linear", [pre + "o", pre + "wo", pre + "bo", z], out, nid=pre + "proj_o", kin=2, out=[cz],
+         act="none", trans=0, swap=0, bias=1, res=1)
+
+
+def tri_attn_pair(N, cz=128, H=4, c=32, dtype="bf16", name="af_pair") -> Graph:
+    """Triangle attention around the starting node (rows, Alg. 13) followed by
+    the ending node (columns, Alg. 14), each with its residual add."""
+    B = Builder(name, dtype)
+    B.input("z", (N, N, cz))
+    _tri_weights(B, "row_", cz, H, c)
+    _tri_weights(B, "col_", cz, H, c)
+    _tri_attention(B, "z", "row_", N, cz, H, c, 0, "z1")
+    _tri_attention(B, "z1", "col_", N, cz, H, c, 1, "z2")
+    B.output("z2")
+    return B.build()
+
+
+CONFIGS = {
+    # BASELINE.json configs[0..4]
+    "tiny": dict(kind="transformer", N=256, d=64, h=2, f=256, causal=False, dtype="f32"),
+    "gpt": dict(kind="transformer", N=16384, d=1024, h=16, f=4096, causal=True, dtype="bf16"),
+    "vit": dict(kind="transformer", N=65536, d=1024, h=16, f=4096, causal=False, dtype="bf16"),
+    "af": dict(kind="tri_attn_pair", N=1024, d=128, h=4, f=32, causal=False, dtype="bf16"),
+    "unet": dict(kind="attn_only", N=16384, d=640, h=10, f=0, causal=False, dtype="bf16"),
+    "unet_h8": dict(kind="attn_only", N=16384, d=640, h=8, f=0, causal=False, dtype="bf16"),
+}
+
+
+def block(kind, N, d, h, f=0, causal=False, dtype="bf16", name=None) -> Graph:
+    if kind == "transformer":
+        return transformer(N, d, h, f, causal, dtype, False, name or "transformer")
+    if kind == "attn_only":
+        return transformer(N, d, h, 0, causal, dtype, True, name or "attn_only")
+    if kind == "tri_attn_pair":
+        return tri_attn_pair(N, d, h, f, dtype, name or "af_pair")
+    raise ValueError(kind)
+
+
+def config(name: str, **over) -> Graph:
+    c = dict(CONFIGS[name])
+    c.update(over)
+    return block(c["kind"], c["N"], c["d"], c["h"], c["f"], c["causal"], c["dtype"], name)
+
+
+# ----------------------------------------------------------- SPEC corpus
+def corpus(name: str, seq=64, d=32, dtype="f64") -> Graph:
+    """Desk-scale graphs from SPEC's primitive op set (mlp, attention,
+    transformer2, alphafold_like_2d)."""
+    B = Builder(name, dtype)
+    if name == "mlp":
+        B.input("x", (seq, d))
+        B.weight("w1", (d, 4 * d), "matrix", d)
+        B.weight("w2", (4 * d, d), "matrix", 4 * d)
+        B.op("matmul", ["x", "w1"], "h1")
+        B.op("relu", ["h1"], "h2")
+        B.op("matmul", ["h2", "w2"], "y")
+        B.output("y")
+    elif name == "attention":
+        B.input("x", (seq, d))
+        for w in ("wq", "wk", "wv", "wo"):
+            B.weight(w, (d, d), "matrix", d)
+        B.weight("scale", (1,), "bias", 1)
+        _spec_attn(B, "x", "", "y")
+        B.output("y")
+    elif name == "transformer2":
+        B.input("x", (seq, d))
+        cur = "x"
+        for blk in range(2):
+            p = f"b{blk}_"
+            B.weight(p + "g1", (d,), "ln_gamma", d)
+            B.weight(p + "be1", (d,), "ln_beta", d)
+            for w in ("wq", "wk", "wv", "wo"):
+                B.weight(p + w, (d, d), "matrix", d)
+            B.weight(p + "scale", (1,), "bias", 1)
+            B.weight(p + "g2", (d,), "ln_gamma", d)
+            B.weight(p + "be2", (d,), "ln_beta", d)
+            B.weight(p + "w1", (d, 2 * d), "matrix", d)
+            B.weight(p + "w2", (2 * d, d), "matrix", 2 * d)
+            B.op("layernorm", [cur, p + "g1", p + "be1"], p + "a", naxes=1, eps=1e-5)
+            _spec_attn(B, p + "a", p, p + "att")
+            B.op("add", [cur, p + "att"], p + "x1")
+            B.op("layernorm", [p + "x1", p + "g2", p + "be2"], p + "c", naxes=1, eps=1e-5)
+            B.op("matmul", [p + "c", p + "w1"], p + "h")
+            B.op("gelu", [p + "h"], p + "hg")
+            B.op("matmul", [p + "hg", p + "w2"], p + "m")
+            B.op("add", [p + "x1", p + "m"], p + "out")
+            cur = p + "out"
+        B.output(cur)
+    elif name == "alphafold_like_2d":
+        L = seq
+        B.input("z", (L, L, d))
+        B.weight("w1", (d, d), "matrix", d)
+        B.weight("w2", (d, d), "matrix", d)
+        B.op("matmul", ["z", "w1"], "u")
+        B.op("softmax", ["u"], "r", dim=1)
+        B.op("mul", ["r", "z"], "rz")
+        B.op("add", ["z", "rz"], "z1")
+        B.op("matmul", ["z1", "w2"], "w")
+        B.op("softmax", ["w"], "cc", dim=0)
+        B.op("mul", ["cc", "z1"], "cz")
+        B.op("add", ["z1", "cz"], "z2")
+        B.output("z2")
+    else:
+        raise ValueError(f"unknown corpus {name}")
+    return B.build()
+
+
+def _spec_attn(B: Builder, x, p, out):
+    B.op("matmul", [x, p + "wq"], p + "q")
+    B.op("matmul", [x, p + "wk"], p + "k")
+    B.op("matmul", [x, p + "wv"], p + "v")
+    B.op("transpose", [p + "k"], p + "kt", perm=[1, 0])
+    B.op("matmul", [p + "q", p + "kt"], p + "s")
+    B.op("mul", [p + "s", p + "scale"], p + "ss")
+    B.op("softmax", [p + "ss"], p + "pr", dim=1)
+    B.op("matmul", [p + "pr", p + "v"], p + "o")
+    B.op("matmul", [p + "o", p + "wo"], out)

@@ -1,0 +1,203 @@
+"""Pins for the oracle's block maths (SURVEY §8(c) c.3 "O1 block forward").
+
+Each pin comes from outside the oracle: torch.nn.functional in fp64 (library
+routines), closed forms and the paper's/SPEC's worked examples."""
+import math
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+from oracle import executor, graph, ops, workloads
+from oracle.graph import Builder, GraphError
+import synth
+
+
+def _values(g, seed=0):
+    return {t: s.value for t, s in synth.make_inputs(g.input_specs(), seed).items()}
+
+
+def _torch_transformer(v, N, d, h, causal, attn_only):
+    """Same block through torch.nn.functional (fp64 CPU): layer_norm, linear,
+    scaled_dot_product_attention, gelu(approximate='none')."""
+    T = {k: torch.from_numpy(np.asarray(a, dtype=np.float64)) for k, a in v.items()}
+    dh = d // h
+    x = T["x"]
+    a = F.layer_norm(x, (d,), T["ln1_g"], T["ln1_b"], eps=1e-5)
+    q = F.linear(a, T["wq"], T["bq"]).view(N, h, dh).transpose(0, 1)
+    k = F.linear(a, T["wk"], T["bk"]).view(N, h, dh).transpose(0, 1)
+    vv = F.linear(a, T["wv"], T["bv"]).view(N, h, dh).transpose(0, 1)
+    with torch.nn.attention.sdpa_kernel(torch.nn.attention.SDPBackend.MATH):
+        o = F.scaled_dot_product_attention(q[None], k[None], vv[None], is_causal=causal)[0]
+    o = o.transpose(0, 1).reshape(N, d)
+    x1 = x + F.linear(o, T["wo"], T["bo"])
+    if attn_only:
+        return x1.numpy()
+    c = F.layer_norm(x1, (d,), T["ln2_g"], T["ln2_b"], eps=1e-5)
+    hid = F.gelu(F.linear(c, T["w1"], T["b1"]), approximate="none")
+    return (x1 + F.linear(hid, T["w2"], T["b2"])).numpy()
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("attn_only", [False, True])
+def test_transformer_matches_torch_functional(causal, attn_only):
+    N, d, h, f = 48, 32, 4, 64
+    g = workloads.block("attn_only" if attn_only else "transformer", N, d, h, f, causal, "f64")
+    v = _values(g)
+    ours = executor.run(g, v)[g.outputs[0]]
+    ref = _torch_transformer(v, N, d, h, causal, attn_only)
+    np.testing.assert_allclose(ours, ref, rtol=0, atol=1e-12)
+
+
+def _torch_tri_attention(z, W, ending):
+    """AF2 Alg. 13 (starting node) / Alg. 14 (ending node) via torch einsum."""
+    T = {k: torch.from_numpy(np.asarray(a, dtype=np.float64)) for k, a in W.items()}
+    z = torch.from_numpy(z)
+    N, _, cz = z.shape
+    H = T["wb"].shape[0]
+    c = T["wq"].shape[0] // H
+    zn = F.layer_norm(z, (cz,), T["ln_g"], T["ln_b"], eps=1e-5)
+    q = (zn @ T["wq"].T).view(N, N, H, c)
+    k = (zn @ T["wk"].T).view(N, N, H, c)
+    v = (zn @ T["wv"].T).view(N, N, H, c)
+    b = zn @ T["wb"].T                                   # [N, N, H] : b[j,k,h]
+    g = torch.sigmoid(zn @ T["wg"].T + T["bg"]).view(N, N, H, c)
+    if not ending:   # a_ijk = softmax_k(q_ij . k_ik / sqrt c + b_jk)
+        logits = torch.einsum("ijhc,ikhc->ihjk", q, k) / math.sqrt(c) + b.permute(2, 0, 1)[None]
+        a = torch.softmax(logits, dim=-1)
+        o = torch.einsum("ihjk,ikhc->ijhc", a, v)
+    else:            # a_ijk = softmax_k(q_ij . k_kj / sqrt c + b_ki)
+        logits = torch.einsum("ijhc,kjhc->jhik", q, k) / math.sqrt(c) + b.permute(2, 1, 0)[None]
+        a = torch.softmax(logits, dim=-1)
+        o = torch.einsum("jhik,kjhc->ijhc", a, v)
+    o = g * o
+    return (z + o.reshape(N, N, H * c) @ T["wo"].T + T["bo"]).numpy()
+
+
+def test_triangle_attention_matches_af2_algorithms():
+    N, cz, H, c = 12, 16, 2, 8
+    g = workloads.tri_attn_pair(N, cz, H, c, "f64")
+    v = _values(g, 3)
+    env = executor.run(g, v, keep_all=True)
+    rw = {k[4:]: v[k] for k in v if k.startswith("row_")}
+    cw = {k[4:]: v[k] for k in v if k.startswith("col_")}
+    z1 = _torch_tri_attention(v["z"], rw, ending=False)
+    np.testing.assert_allclose(env["z1"], z1, rtol=0, atol=1e-12)
+    z2 = _torch_tri_attention(z1, cw, ending=True)
+    np.testing.assert_allclose(env["z2"], z2, rtol=0, atol=1e-12)
+
+
+def test_ending_node_is_starting_node_on_transpose():
+    """Alg. 14 on z equals Alg. 13 on z^T, transposed back (AF2 construction)."""
+    N, cz, H, c = 10, 8, 2, 4
+    g = workloads.tri_attn_pair(N, cz, H, c, "f64")
+    v = _values(g, 5)
+    env = executor.run(g, v, keep_all=True)
+    # run the row block with the column weights on z1^T
+    gr = workloads.tri_attn_pair(N, cz, H, c, "f64")
+    v2 = dict(v)
+    v2["z"] = np.ascontiguousarray(np.transpose(env["z1"], (1, 0, 2)))
+    for k in list(v):
+        if k.startswith("col_"):
+            v2["row_" + k[4:]] = v[k]
+    env2 = executor.run(gr, v2, keep_all=True)
+    np.testing.assert_allclose(np.transpose(env2["z1"], (1, 0, 2)), env["z2"], rtol=0, atol=1e-12)
+
+
+def _attn_graph(N, h, dh, causal):
+    B = Builder("a", "f64")
+    B.input("q", (N, h, dh))
+    B.input("k", (N, h, dh))
+    B.input("vt", (h, dh, N))
+    B.op("attn_scores", ["q", "k"], "s", scale=1.0 / math.sqrt(dh), causal=int(causal))
+    B.op("softmax", ["s"], "p", dim=2)
+    B.op("attn_pv", ["p", "vt"], "o")
+    B.output("o")
+    return B.build()
+
+
+def test_closed_forms_attention():
+    N, h, dh = 7, 2, 3
+    rng = np.random.default_rng(0)
+    vt = rng.standard_normal((h, dh, N))
+    g = _attn_graph(N, h, dh, False)
+    z = np.zeros((N, h, dh))
+    o = executor.run(g, {"q": z, "k": z, "vt": vt})["o"]     # uniform softmax -> mean of v
+    np.testing.assert_allclose(o, np.broadcast_to(vt.mean(axis=2)[None], (N, h, dh)), atol=1e-15)
+    gc = _attn_graph(N, h, dh, True)
+    q = rng.standard_normal((N, h, dh))
+    k = rng.standard_normal((N, h, dh))
+    o = executor.run(gc, {"q": q, "k": k, "vt": vt})["o"]
+    np.testing.assert_allclose(o[0], vt[:, :, 0], atol=1e-15)  # causal row 0 attends to key 0 only
+    g1 = _attn_graph(1, h, dh, False)                          # single key -> o = v
+    o = executor.run(g1, {"q": q[:1], "k": k[:1], "vt": vt[:, :, :1]})["o"]
+    np.testing.assert_allclose(o[0], vt[:, :, 0], atol=1e-15)
+
+
+def test_closed_forms_elementwise():
+    assert ops.evaluate("relu", {}, [np.array([-1.0, 2.0])]).tolist() == [0.0, 2.0]
+    assert ops.evaluate("softmax", {"dim": 0}, [np.array([0.0, 0.0])]).tolist() == [0.5, 0.5]
+    m = np.array([[1.0, 2.0], [3.0, 4.0]])
+    assert ops.evaluate("matmul", {}, [m, np.eye(2)]).tolist() == m.tolist()
+    assert ops.evaluate("gelu", {}, [np.array([0.0])])[0] == 0.0
+    beta = np.array([0.3, -0.2, 0.1])
+    y = ops.evaluate("layernorm", {"naxes": 1, "eps": 1e-5},
+                     [np.full((2, 3), 7.0), np.array([2.0, 3.0, 4.0]), beta])
+    np.testing.assert_array_equal(y, np.broadcast_to(beta, (2, 3)))   # LN of a constant row -> beta
+    # GELU(x) -> x for large x, -> 0 for very negative x; GELU(1) = Phi(1)
+    assert abs(ops.evaluate("gelu", {}, [np.array([1.0])])[0] - 0.8413447460685429) < 1e-15
+
+
+def test_exact_mode_equals_fast_mode():
+    g = workloads.block("transformer", 32, 16, 2, 32, True, "f64")
+    v = _values(g, 7)
+    a = executor.run(g, v)["y"]
+    with ops.exact_order():
+        b = executor.run(g, v)["y"]
+    np.testing.assert_allclose(a, b, rtol=0, atol=1e-12)
+
+
+def test_mirror_rounding_is_bf16():
+    x = np.array([1.0 + 2 ** -9, 1.0 + 3 * 2 ** -9, -3.14159, 65504.0])
+    r = executor.round_bf16(x)
+    # ties to even at 1 + 2^-8 spacing
+    assert r[0] == 1.0 and r[1] == 1.0 + 2 ** -7
+    assert abs(r[2] - -3.140625) == 0
+
+
+# ---------------------------------------------------------------- SPEC graph_ir examples
+def test_spec_infer_shapes_and_flops():
+    assert ops.shape("matmul", {}, [(2, 3), (3, 4)]) == (2, 4)
+    assert ops.flops("matmul", {}, [(2, 3), (3, 4)], (2, 4)) == 48
+    assert ops.shape("reshape", {"shape": [3, 4]}, [(2, 6)]) == (3, 4)
+    with pytest.raises(ValueError, match="inner dimension mismatch"):
+        ops.shape("matmul", {}, [(2, 3), (4, 5)])
+    assert ops.flops("relu", {}, [(4, 4)], (4, 4)) == 16
+    assert ops.flops("transpose", {"perm": [1, 0]}, [(3, 5)], (5, 3)) == 0
+    assert graph.TensorMeta("t", "f32", (3, 4)).strides == (4, 1)
+
+
+def test_spec_load_graph_examples():
+    doc = "autochunk-graph 1\ntensor x f32 2,3\ntensor y f32 2,3\ninput x\nnode r relu x y\noutput y\n"
+    g = graph.load_graph(doc)
+    assert len([n for n in g.nodes if n.kind == "relu"]) == 1 and len(g.tensors) == 2
+    with pytest.raises(GraphError, match="unknown tensor id"):
+        graph.load_graph(doc.replace("node r relu x y", "node r relu t9 y"))
+    cyc = ("autochunk-graph 1\ntensor x f32 2\ntensor a f32 2\ntensor b f32 2\ninput x\n"
+           "node A add x,b a\nnode B relu a b\noutput b\n")
+    with pytest.raises(GraphError, match="cycle|order"):
+        graph.load_graph(cyc)
+    bad = doc.replace("node r relu x y", "node r transpose x y perm=0,0")
+    with pytest.raises(GraphError, match="bijection"):
+        graph.load_graph(bad)
+
+
+@pytest.mark.parametrize("name", ["tiny", "gpt", "vit", "af", "unet", "unet_h8"])
+def test_document_round_trip(name):
+    g = workloads.config(name)
+    doc = graph.serialize(g)
+    g2 = graph.load_graph(doc)
+    assert graph.serialize(g2) == doc
+    graph.infer_shapes(g2)
+    assert graph.serialize(g2) == doc
