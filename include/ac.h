@@ -1,0 +1,210 @@
+/*
+ * ac.h — C ABI of libautochunk: chunked execution of a selected chunk region
+ * (AutoChunk, arXiv 2401.10652) on NVIDIA B200 (sm_100a).
+ *
+ * Citations: P:n = line n of the paper text, S:n = line n of the CPU-program
+ * spec used for interface ideas, SURVEY §x = SURVEY.md section.
+ *
+ * Conventions (all calls)
+ *  - Every call returns an ac_status; no exception or C++ type crosses the ABI.
+ *    On failure a thread-local message is available from ac_last_error().
+ *  - The library owns the opaque ac_graph / ac_chunk_plan / ac_exec / ac_comm objects;
+ *    graphs and plans are immutable after creation and safe to share between
+ *    threads.  Free them with the matching ac_*_free.
+ *  - The caller owns ALL device memory: inputs, weights (passed as inputs, by
+ *    tensor id), outputs and the workspace.  ac_run never allocates or frees
+ *    device memory.
+ *  - Tensor data are dense, row-major, 16-byte aligned device pointers; the
+ *    element type is the graph's (f32 or bf16).  Sizes are in bytes unless a
+ *    name says otherwise.
+ *  - Determinism: the same graph, budget and params give byte-identical plan
+ *    text.
+ */
+#ifndef AUTOCHUNK_AC_H
+#define AUTOCHUNK_AC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum ac_status {
+  AC_OK = 0,
+  AC_ERR_ARG = 1,         /* bad arguments (NULL, out of range, buffer too small) */
+  AC_ERR_GRAPH = 2,       /* graph parse / shape / validation failure */
+  AC_ERR_BUDGET = 3,      /* budget unachievable; *out still holds the best-effort plan */
+  AC_ERR_PLAN = 4,        /* plan/graph mismatch, overlapping regions, illegal region, n > extent */
+  AC_ERR_UNSUPPORTED = 5, /* legal plan/graph the GPU executor has no kernel for */
+  AC_ERR_BIND = 6,        /* tensor id / shape / dtype / alignment mismatch at ac_run */
+  AC_ERR_CUDA = 7,        /* CUDA runtime error */
+  AC_ERR_NCCL = 8,        /* NCCL error */
+  AC_ERR_WORKSPACE = 9    /* workspace smaller than ac_plan_workspace_bytes */
+} ac_status;
+
+typedef struct ac_graph ac_graph;
+typedef struct ac_chunk_plan ac_chunk_plan; /* a chunk plan S = [s_1..s_l] (Eq. 11) */
+typedef struct ac_exec ac_exec;
+typedef struct ac_comm ac_comm;
+
+/* Thread-local message describing the last failure of this thread ("" if none). */
+const char* ac_last_error(void);
+/* Library version string, e.g. "autochunk-b200 0.1". */
+const char* ac_version(void);
+
+/* ------------------------------------------------------------------ graphs */
+
+/* Parse a graph document (schema 1; SPEC load_graph / infer_shapes /
+ * validate).  doc: UTF-8 text of `len` bytes (need not be NUL-terminated).
+ * On success *out owns a new graph.  Errors: AC_ERR_ARG, AC_ERR_GRAPH. */
+ac_status ac_graph_parse(const char* doc, size_t len, ac_graph** out);
+
+typedef enum ac_block_kind {
+  AC_BLOCK_TRANSFORMER = 0,   /* pre-LN attention + GELU FFN (GPT, ViT, tiny) */
+  AC_BLOCK_ATTN_ONLY = 1,     /* pre-LN attention + residual only (UNet self-attention) */
+  AC_BLOCK_TRI_ATTN_PAIR = 2  /* AlphaFold triangle attention, starting then ending node */
+} ac_block_kind;
+
+typedef enum ac_dtype { AC_F32 = 0, AC_BF16 = 1, AC_F64 = 2 } ac_dtype;
+
+/* Workload templates of BASELINE.json (the SPEC cmd_corpus analog).
+ * transformer/attn_only: N tokens, d model width, h heads, f FFN width.
+ * tri_attn_pair: N residues, d = c_z, h = heads, f = per-head width c. */
+typedef struct ac_block_desc {
+  int32_t kind;      /* ac_block_kind */
+  int64_t N, d, h, f;
+  int32_t causal;    /* 1: causal attention (GPT prefill) */
+  int32_t dtype;     /* ac_dtype */
+  double ln_eps;     /* LayerNorm epsilon (1e-5) */
+  const char* name;  /* graph name in the document; NULL -> kind name */
+} ac_block_desc;
+
+ac_status ac_graph_block(const ac_block_desc* desc, ac_graph** out);
+
+/* Canonical document text.  Writes at most `cap` bytes (NUL-terminated if it
+ * fits) and always sets *len to the full length without the NUL; call with
+ * buf = NULL, cap = 0 to size.  AC_ERR_ARG if cap is too small. */
+ac_status ac_graph_serialize(const ac_graph* g, char* buf, size_t cap, size_t* len);
+void ac_graph_free(ac_graph* g);
+
+/* Number of nodes (= execution steps) and tensors. */
+int32_t ac_graph_num_nodes(const ac_graph* g);
+
+/* ------------------------------------------------------------------ memory */
+
+/* Eq. 1 / Eq. 2 activation-memory profile.  Weights are
+ * parameter memory and excluded; peak ties go to the first
+ * step. */
+typedef struct ac_mem_profile {
+  int64_t peak_bytes;
+  int32_t peak_step;   /* node index n_p */
+  int32_t n_steps;     /* = number of nodes */
+  int64_t x_bytes;     /* graph inputs live at the peak (mem(X)) */
+  int64_t y_bytes;     /* graph outputs live at the peak (mem(Y)) */
+  int64_t a_bytes;     /* everything else live at the peak (mem(A)) */
+} ac_mem_profile;
+
+/* plan == NULL: unchunked profile (Eq. 1).  Otherwise the estimate under the
+ * plan (Eq. 2 with the exact chunked liveness of DESIGN.md R6).  per_step may be
+ * NULL; else it must hold ac_graph_num_nodes(g) entries.  The GPU model charges
+ * no contiguity copies (R5).  Errors: AC_ERR_ARG, AC_ERR_PLAN. */
+ac_status ac_estimate_memory(const ac_graph* g, const ac_chunk_plan* plan, ac_mem_profile* out, int64_t* per_step);
+
+/* ------------------------------------------------------------------ planning */
+
+enum {
+  AC_FLAG_NO_HOIST = 1 << 0,     /* Table 1 "No graph optimization" */
+  AC_FLAG_NO_DENSITY = 1 << 1,   /* "No computation density" */
+  AC_FLAG_NO_STRIDE = 1 << 2,    /* "No dimension strides" */
+  AC_FLAG_NO_NODES = 1 << 3,     /* "No number of nodes" */
+  AC_FLAG_NO_FLOPS = 1 << 4,     /* "No flops" */
+  AC_FLAG_CONTIGUITY = 1 << 5    /* charge SPEC contiguity copies */
+};
+
+/* Cost model Eq. 8-10 and search/selection knobs. */
+typedef struct ac_cost_params {
+  double alpha, beta, gamma, lambda; /* defaults 1, 1e-9, -1e-5, 0.01 (readings R8/R9) */
+  int32_t beam;        /* beam width B (4) */
+  int32_t window;      /* local window k (32) */
+  int32_t max_passes;  /* 16 */
+  int32_t max_chunks;  /* top of the chunk-count ladder (4096) */
+  uint32_t flags;      /* AC_FLAG_* */
+  uint32_t allowed_dims_mask; /* bit d set: output dim d may be chunked; 0 = all */
+} ac_cost_params;
+
+void ac_cost_params_default(ac_cost_params* p);
+
+/* Alg. 1 chunk search + Eq. 8-11 DP/beam selection, multi-pass until
+ * peak < mem_budget_bytes (strict).  params NULL -> defaults.
+ * AC_OK: feasible plan.  AC_ERR_BUDGET: *out holds the best-effort plan.
+ * Errors: AC_ERR_ARG. */
+ac_status ac_plan(const ac_graph* g, int64_t mem_budget_bytes, const ac_cost_params* params, ac_chunk_plan** out);
+
+/* User-fixed plan: "autochunk-plan 1" followed by lines
+ *   region s=<node id> e=<node id> n=<chunks> dims=<d,...>
+ * (one output dim per region output).  The library re-derives the flow, X^c,
+ * X^nc, Y^c and hoisting exactly as the search would.  Errors: AC_ERR_PLAN. */
+ac_status ac_plan_parse(const ac_graph* g, const char* doc, size_t len, ac_chunk_plan** out);
+
+/* Canonical plan text — the bit-exactness target vs the oracle. */
+ac_status ac_plan_serialize(const ac_chunk_plan* p, char* buf, size_t cap, size_t* len);
+void ac_plan_free(ac_chunk_plan* p);
+int32_t ac_plan_num_regions(const ac_chunk_plan* p);
+
+/* Bytes of workspace ac_run needs for this plan on rank `rank` of `world`
+ * (every activation tensor that is not a graph input / output, packed by the
+ * static arena).  -1 on error. */
+int64_t ac_plan_workspace_bytes(const ac_chunk_plan* p, int32_t rank, int32_t world);
+
+/* ------------------------------------------------------------------ multi-GPU */
+
+/* NCCL bootstrap: rank 0 calls ac_comm_get_unique_id, the 128
+ * bytes are broadcast by the caller (torch.distributed), every rank calls
+ * ac_comm_init on its device.  Errors: AC_ERR_NCCL, AC_ERR_ARG. */
+ac_status ac_comm_get_unique_id(uint8_t unique_id[128]);
+ac_status ac_comm_init(const uint8_t unique_id[128], int32_t rank, int32_t world, int32_t device, ac_comm** out);
+void ac_comm_free(ac_comm* c);
+
+/* ------------------------------------------------------------------ execution */
+
+/* A caller tensor bound to a graph tensor id.  shape/stride in elements;
+ * stride must be dense row-major. */
+typedef struct ac_tensor {
+  const char* tensor_id;
+  int32_t dtype;        /* ac_dtype */
+  int32_t ndim;         /* <= 6 */
+  int64_t shape[6];
+  int64_t stride[6];
+  void* data;           /* device pointer */
+} ac_tensor;
+
+/* Bind plan + workspace (+ communicator, NULL -> single GPU).  The workspace
+ * must hold ac_plan_workspace_bytes(plan, rank, world) bytes and stay valid
+ * while the exec is used.  Errors: AC_ERR_WORKSPACE, AC_ERR_UNSUPPORTED. */
+ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_bytes, const ac_comm* comm, ac_exec** out);
+void ac_exec_free(ac_exec* e);
+
+/* Execute the plan on `stream` (a cudaStream_t; NULL = legacy default stream).
+ * inputs: every graph input and weight, by tensor id; outputs: every graph
+ * output (fully overwritten).  Asynchronous and stream-ordered; buffers must
+ * stay valid until the stream completes.  With a communicator, each rank runs
+ * its contiguous share of every region's chunks and the region outputs are
+ * all-gathered.  Errors: AC_ERR_BIND, AC_ERR_CUDA, AC_ERR_NCCL. */
+ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_tensor* outputs, int32_t n_out,
+                 void* stream);
+
+/* Statistics of the last ac_run (read after the stream has completed). */
+typedef struct ac_run_stats {
+  int64_t workspace_high_water;  /* bytes of the arena actually addressed */
+  int64_t planned_peak;          /* ac_estimate_memory(plan) peak */
+  int64_t caller_bytes;          /* graph inputs + outputs (full size) */
+  int32_t launches;              /* kernels launched by the last ac_run */
+  int32_t chunks_run;            /* chunk iterations executed on this rank */
+} ac_run_stats;
+ac_status ac_exec_stats(const ac_exec* e, ac_run_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AUTOCHUNK_AC_H */

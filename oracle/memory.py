@@ -121,11 +121,12 @@ def estimate_with_plan(g: Graph, regions, contiguity: bool = False) -> MemoryPro
         if r.n <= 1:
             continue
         ins, outs = region_io(g, r.start, r.end, cons)
+        hoisted_out = {g.nodes[i].output for i in r.hoisted}
+        outs = [t for t in outs if t not in hoisted_out]    # charged as hoisted tensors
         produced = {g.nodes[i].output: i for i in range(r.start, r.end + 1)}
         consumed_in = set()
         for i in range(r.start, r.end + 1):
             consumed_in.update(g.nodes[i].inputs)
-        hoisted_out = {g.nodes[i].output for i in r.hoisted}
         interior = {}
         for t, p in produced.items():
             if t in outs or t in hoisted_out:

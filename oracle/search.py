@@ -170,7 +170,7 @@ def make_region(g: Graph, s, e, dims, hoisted, assign, cons=None) -> Region:
     hout = {g.nodes[i].output for i in hoisted}
     xc = [(t, dims[t]) for t in ins if t in dims]
     xnc = [t for t in ins if t not in dims]
-    yc = [(t, dims[t]) for t in outs]
+    yc = [(t, dims[t]) for t in outs if t not in hout]   # hoisted outputs are computed once
     # keep only the flow entries that belong to this (possibly shrunk) region
     keep = set(ins) | {g.nodes[i].output for i in range(s, e + 1)}
     fl = {t: d for t, d in dims.items() if t in keep and t not in hout}

@@ -186,3 +186,31 @@ def exhaustive(g: Graph, budget: int, p: CostParams, max_passes: int = 3):
             return feas[0][0], feas[0][2]
         level = nxt
     return None
+
+
+def user_plan(g: Graph, specs, p: CostParams = None) -> Plan:
+    """A user-fixed plan (ac_plan_parse): specs = [(start_node_id, end_node_id, n,
+    dims)].  Flows, X^c / X^nc / Y^c and hoisting are derived as the search does."""
+    from .search import candidate_for
+    p = p or CostParams()
+    names = [n.id for n in g.nodes]
+    regions = []
+    for s_id, e_id, n, dims in specs:
+        s, e = names.index(s_id), names.index(e_id)
+        if any(g.nodes[i].kind in ("input", "weight") for i in range(s, e + 1)):
+            raise ValueError("illegal region: contains an input/weight node")
+        r = candidate_for(g, s, e, tuple(dims), hoist=True)
+        if r is None:
+            raise ValueError("illegal region: no legal chunk flow for these dims")
+        if not 1 <= n <= r.extent:
+            raise ValueError("chunk count n outside [1, extent]")
+        r = r.with_n(n)
+        for o in regions:
+            if not (r.end < o.start or r.start > o.end):
+                raise ValueError("overlapping regions")
+        r.cost = region_cost(g, r, p)
+        regions.append(r)
+    cost = 0.0
+    for r in regions:
+        cost = cost + r.cost.total
+    return Plan(regions, 0, profile(g).peak_bytes, estimate_with_plan(g, regions).peak_bytes, True, cost, g.name)

@@ -1,0 +1,93 @@
+// G8: fp32 path (tiny config, north_star tolerance 1e-4).  One-pass TF32 on the
+// tensor cores would miss 1e-4 (10-bit mantissa), so fp32 graphs use an FFMA
+// SIMT GEMM: 64x64 output tile per 256-thread CTA, 4x4 per thread, K staged
+// through shared memory 16 at a time.  The K loop is sequential per output, so
+// the value of an element does not depend on the tile it lives in.
+#include <cuda_runtime.h>
+
+#include "epilogue.cuh"
+#include "kernels.h"
+
+namespace ac {
+namespace {
+
+constexpr int TM = 64, TN = 64, TK = 16;
+
+__global__ void __launch_bounds__(256) gemm_f32_kernel(const GemmProblem p) {
+  __shared__ float sa[TK][TM + 4];
+  __shared__ float sb[TK][TN + 4];
+  const int b = blockIdx.z;
+  const int b1 = b / p.B2, b2 = b - (b / p.B2) * p.B2;
+  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
+  const float* A = static_cast<const float*>(p.A.p) + (p.A.use_b1 ? b1 * p.A.sb1 : 0) + (p.A.use_b2 ? b2 * p.A.sb2 : 0);
+  const float* B = static_cast<const float*>(p.B.p) + (p.B.use_b1 ? b1 * p.B.sb1 : 0) + (p.B.use_b2 ? b2 * p.B.sb2 : 0);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][4] = {};
+  int kend = p.K;
+  if (p.causal_k) {
+    const long long e = p.k_row_off + m0 + TM;
+    if (e < kend) kend = static_cast<int>(e);
+  }
+  for (int k0 = 0; k0 < kend; k0 += TK) {
+    for (int i = threadIdx.x; i < TK * TM; i += 256) {
+      const int kk = i % TK, mm = i / TK;
+      const int m = m0 + mm, k = k0 + kk;
+      sa[kk][mm] = (m < p.M && k < kend) ? A[static_cast<int64_t>(m) * p.A.srow + k] : 0.f;
+      const int n = n0 + mm;
+      sb[kk][mm] = (n < p.N && k < kend) ? B[static_cast<int64_t>(n) * p.B.srow + k] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK; ++kk) {
+      float ra[4], rb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        ra[i] = sa[kk][ty * 4 + i];
+        rb[i] = sb[kk][tx * 4 + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ra[i], rb[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  // epilogue element by element (same order as the tcgen05 path)
+  const Epilogue& ep = p.ep;
+  const float* add = static_cast<const float*>(ep.add);
+  const float* bias = static_cast<const float*>(ep.bias);
+  const float* gate = static_cast<const float*>(ep.gate);
+  const float* res = static_cast<const float*>(ep.res);
+  float* out = static_cast<float*>(ep.out);
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= p.M) continue;
+    const int64_t ob = b1 * ep.out_sb1 + b2 * ep.out_sb2 + static_cast<int64_t>(m) * ep.out_sm;
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= p.N) continue;
+      float x = acc[i][j] * ep.scale;
+      if (add) x += add[b1 * ep.add_sb1 + b2 * ep.add_sb2 + static_cast<int64_t>(m) * ep.add_sm +
+                        static_cast<int64_t>(n) * ep.add_sn];
+      if (bias) x += ep.bias_along_m ? bias[m] : bias[n];
+      x = act_apply(ep.act, x);
+      const int64_t o = ob + static_cast<int64_t>(n) * ep.out_sn;
+      if (gate) x *= gate[o];
+      if (res) x += res[o];
+      if (ep.causal && static_cast<int64_t>(n) + ep.col_off > ep.row_off + m) x = -CUDART_INF_F;
+      out[o] = x;
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t gemm_f32(const GemmProblem& p, cudaStream_t s) {
+  if (p.M <= 0 || p.N <= 0 || p.K <= 0) return cudaErrorInvalidValue;
+  dim3 grid((p.N + TN - 1) / TN, (p.M + TM - 1) / TM, p.B1 * p.B2);
+  if (grid.y > 65535 || grid.z > 65535) return cudaErrorInvalidValue;
+  gemm_f32_kernel<<<grid, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace ac

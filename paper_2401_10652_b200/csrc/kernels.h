@@ -1,0 +1,76 @@
+// Host-side launch API of the sm_100a kernels (internal to libautochunk).
+// Every kernel works on dense strided tensors owned by the caller; nothing here
+// allocates device memory.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ac {
+
+enum Act : int { ACT_NONE = 0, ACT_GELU = 1, ACT_SIGMOID = 2, ACT_RELU = 3 };
+
+// One K-major GEMM operand: element (b1, b2, row, k) lives at
+//   p + b1*sb1 + b2*sb2 + row*srow + k        (element units, k contiguous).
+// use_b1 / use_b2 = 0 means the operand is shared across that batch dim.
+struct Operand {
+  const void* p = nullptr;
+  int64_t srow = 0, sb1 = 0, sb2 = 0;
+  int use_b1 = 0, use_b2 = 0;
+};
+
+// Epilogue applied to acc (fp32) in this order (DESIGN.md §5 "G1 epilogue"):
+//   v = acc * scale
+//   v += add[b1,b2,m,n]            (triangle bias)
+//   v += bias[n] | bias[m]         (linear bias)
+//   v = act(v)
+//   v *= gate[b1,b2,m,n]           (AlphaFold sigmoid gate)
+//   v += res[b1,b2,m,n]            (residual)
+//   causal: v = -inf where (col_off + n) > (row_off + m)
+//   out[b1,b2,m,n] = v
+struct Epilogue {
+  float scale = 1.f;
+  int act = ACT_NONE;
+  int causal = 0;
+  int64_t row_off = 0, col_off = 0;
+  const void* bias = nullptr;
+  int bias_along_m = 0;
+  const void* add = nullptr;
+  int64_t add_sb1 = 0, add_sb2 = 0, add_sm = 0, add_sn = 0;
+  const void* gate = nullptr;
+  const void* res = nullptr;   // gate and res use the output strides
+  void* out = nullptr;
+  int64_t out_sb1 = 0, out_sb2 = 0, out_sm = 0, out_sn = 1;
+};
+
+// D[b1,b2][m][n] = sum_k A[b1,b2][m][k] * B[b1,b2][n][k]
+struct GemmProblem {
+  int M = 0, N = 0, K = 0, B1 = 1, B2 = 1;
+  int a_rows_total = 0;  // extent of A's row dim in memory (for TMA bounds); 0 -> M
+  int b_rows_total = 0;  // extent of B's row dim in memory; 0 -> N
+  Operand A, B;
+  Epilogue ep;
+  int causal_tiles = 0;  // skip (m,n) tiles entirely above the diagonal (QK^T)
+  int causal_k = 0;      // K loop stops after the tile's last row (PV, keys = K)
+  int64_t k_row_off = 0; // global row of m = 0 for causal_k
+};
+
+// bf16 x bf16 -> fp32 (TMEM) -> bf16, tcgen05 + TMA, sm_100a.  Returns a
+// cudaError_t (cudaErrorInvalidValue for shapes it cannot take).
+cudaError_t gemm_tc(const GemmProblem& p, cudaStream_t s, int bn_hint = 0);
+// fp32 SIMT (FFMA) path for fp32 graphs (G8).
+cudaError_t gemm_f32(const GemmProblem& p, cudaStream_t s);
+
+// Row ops.  dtype: 0 = fp32, 1 = bf16.
+// LayerNorm over the last C elements of `rows` rows (row stride = C).
+cudaError_t layernorm(const void* x, const void* gamma, const void* beta, void* y, int64_t rows,
+                      int C, float eps, int dtype, cudaStream_t s);
+// Row softmax: rows of `ncols` values with row stride `ld` (elements).  With
+// causal, row r (global row row_off + r) reads columns <= row and writes
+// columns [0, ceil128(row+1)) with zeros above the diagonal (PV reads whole
+// 128-key blocks); otherwise the full row.
+cudaError_t softmax_rows(const void* s_in, void* p_out, int64_t rows, int64_t ncols, int64_t ld,
+                         int causal, int64_t row_off, int dtype, cudaStream_t s);
+
+int num_sms();
+
+}  // namespace ac

@@ -1,0 +1,190 @@
+"""The C-ABI host library (ac_graph_*, ac_estimate_memory, ac_plan, ac_plan_parse)
+against the oracle: byte-identical documents, per-step estimates and plan texts
+(SURVEY §7 step 2).  CPU only — no compute calls."""
+import ctypes
+import random
+import re
+
+import pytest
+
+from oracle import graph as og
+from oracle import memory, plan as oplan, select, workloads
+from oracle.graph import Builder
+
+api = pytest.importorskip("paper_2401_10652_b200.api")
+from paper_2401_10652_b200 import _lib  # noqa: E402
+
+
+def test_library_exports_every_declared_symbol(root):
+    import os
+    L = _lib.lib()
+    declared = set()
+    for h in ("ac.h", "ac_kernels.h"):
+        txt = open(os.path.join(root, "include", h)).read()
+        declared |= set(re.findall(r"\b(ac_[a-z0-9_]+)\s*\(", txt))
+    declared -= {"ac_plan_workspace_bytes(plan"}  # (none: regex only matches identifiers)
+    for name in sorted(declared):
+        assert hasattr(L, name), name
+    bound = {n for n, _, _ in _lib.SIGNATURES}
+    assert declared <= bound, declared - bound
+
+
+CONFIGS = ["tiny", "gpt", "vit", "af", "unet", "unet_h8"]
+
+
+def _c_graph(name):
+    c = workloads.CONFIGS[name]
+    return api.graph_block(c["kind"], c["N"], c["d"], c["h"], c["f"], c["causal"], c["dtype"], name=name)
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+def test_block_documents_identical(name):
+    assert _c_graph(name).serialize() == og.serialize(workloads.config(name))
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+def test_parse_round_trip_and_profile(name):
+    doc = og.serialize(workloads.config(name))
+    g = api.graph_parse(doc)
+    assert g.serialize() == doc
+    prof, per = api.estimate_memory(g)
+    ref = memory.profile(workloads.config(name))
+    assert per == ref.per_step and prof.peak_bytes == ref.peak_bytes and prof.peak_step == ref.peak_step
+    assert (prof.x_bytes, prof.y_bytes, prof.a_bytes) == (ref.x_bytes, ref.y_bytes, ref.a_bytes)
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+@pytest.mark.parametrize("frac", [0.5, 0.2])
+def test_plans_bit_exact(name, frac):
+    og_g = workloads.config(name)
+    budget = int(frac * memory.profile(og_g).peak_bytes)
+    ref = select.select(og_g, budget)
+    g = _c_graph(name)
+    p = api.ac_plan(g, budget)
+    assert p.serialize() == oplan.serialize(ref, og_g)
+    assert p.feasible == ref.feasible
+    prof, per = api.estimate_memory(g, p)
+    assert per == memory.estimate_with_plan(og_g, ref.regions).per_step
+
+
+def _corpus():
+    for name, seq, d in [("mlp", 32, 8), ("attention", 32, 8), ("transformer2", 24, 8),
+                         ("alphafold_like_2d", 8, 4)]:
+        yield name, workloads.corpus(name, seq, d, "f32")
+
+
+@pytest.mark.parametrize("frac", [0.6, 0.4, 0.25])
+def test_corpus_plans_bit_exact(frac):
+    for name, g in _corpus():
+        doc = og.serialize(g)
+        cg = api.graph_parse(doc)
+        budget = int(frac * memory.profile(g).peak_bytes)
+        for kw, prm in [({}, select.CostParams()), ({"beam": 16}, select.CostParams(beam=16)),
+                        ({"flags": _lib.AC_FLAG_NO_HOIST}, select.CostParams(hoist=False)),
+                        ({"flags": _lib.AC_FLAG_CONTIGUITY}, select.CostParams(contiguity=True))]:
+            ref = select.select(g, budget, prm)
+            got = api.ac_plan(cg, budget, api.cost_params(**kw))
+            assert got.serialize() == oplan.serialize(ref, g), (name, kw)
+
+
+def _random_graph(rng: random.Random, i: int):
+    """Fuzzed tiny graphs over the primitive and fused kinds."""
+    B = Builder(f"fz{i}", rng.choice(["f32", "bf16", "f64"]))
+    N, d = rng.choice([4, 6, 8]), rng.choice([2, 4])
+    B.input("x", (N, d))
+    B.weight("w", (d, d), "matrix", d)
+    B.weight("w2", (d, 2 * d), "matrix", d)
+    B.weight("g", (d,), "ln_gamma", d)
+    B.weight("b", (d,), "ln_beta", d)
+    B.weight("lw", (d, d), "matrix", d)
+    live = ["x"]
+    shapes = {"x": (N, d)}
+    for k in range(rng.randint(3, 9)):
+        src = rng.choice(live)
+        out = f"t{k}"
+        kind = rng.choice(["relu", "gelu", "exp", "add", "mul", "softmax0", "softmax1", "ln", "matmul",
+                           "transpose", "linear", "reduce"])
+        s = shapes[src]
+        try:
+            if kind in ("relu", "gelu", "exp"):
+                B.op(kind, [src], out)
+            elif kind in ("add", "mul"):
+                other = rng.choice([t for t in live if shapes[t] == s] or [src])
+                B.op(kind, [src, other], out)
+            elif kind.startswith("softmax"):
+                B.op("softmax", [src], out, dim=int(kind[-1]) % len(s))
+            elif kind == "ln" and s[-1] == d and len(s) == 2:
+                B.op("layernorm", [src, "g", "b"], out, naxes=1, eps=1e-5)
+            elif kind == "matmul" and s[-1] == d:
+                B.op("matmul", [src, rng.choice(["w", "w2"])], out)
+            elif kind == "transpose" and len(s) == 2:
+                B.op("transpose", [src], out, perm=[1, 0])
+            elif kind == "linear" and s[-1] == d and len(s) == 2:
+                B.op("linear", [src, "lw"], out, kin=1, out=[d], act=rng.choice(["none", "gelu"]),
+                     trans=rng.choice([0, 1]), swap=0, bias=0, res=0)
+            elif kind == "reduce" and len(s) == 2:
+                B.op("reduce_sum", [src], out, dim=rng.choice([0, 1]))
+            else:
+                continue
+        except ValueError:
+            continue
+        live.append(out)
+        shapes[out] = B.g.tensors[out].shape
+    B.output(live[-1])
+    if len(live) > 3 and rng.random() < 0.5:
+        B.output(live[-2])
+    return B.build()
+
+
+def test_fuzzed_graphs_plans_and_estimates_bit_exact():
+    rng = random.Random(1234)
+    n_checked = 0
+    for i in range(60):
+        g = _random_graph(rng, i)
+        doc = og.serialize(g)
+        cg = api.graph_parse(doc)
+        assert cg.serialize() == doc
+        base = memory.profile(g)
+        _, per = api.estimate_memory(cg)
+        assert per == base.per_step
+        for frac in (0.7, 0.4):
+            budget = int(frac * base.peak_bytes)
+            ref = select.select(g, budget, select.CostParams(window=8))
+            got = api.ac_plan(cg, budget, api.cost_params(window=8))
+            assert got.serialize() == oplan.serialize(ref, g), doc
+            n_checked += len(ref.regions)
+    assert n_checked > 10
+
+
+def test_user_plan_parse_matches_oracle():
+    g = workloads.config("gpt")
+    cg = _c_graph("gpt")
+    txt = "autochunk-plan 1\nregion s=scores e=pv n=8 dims=0\n"
+    p = api.plan_parse(cg, txt)
+    ref = select.user_plan(g, [("scores", "pv", 8, (0,))])
+    assert p.serialize() == oplan.serialize(ref, g)
+    whole = "autochunk-plan 1\nregion s=proj_q e=ffn2 n=8 dims=0\n"
+    p = api.plan_parse(cg, whole)
+    ref = select.user_plan(g, [("proj_q", "ffn2", 8, (0,))])
+    assert p.serialize() == oplan.serialize(ref, g)
+    # the canonical text of an ac_plan result parses back to the same plan
+    full = api.ac_plan(cg, int(0.2 * memory.profile(g).peak_bytes))
+    again = api.plan_parse(cg, full.serialize())
+    assert re.sub(r"budget \d+\n", "", again.serialize().replace("budget 0\n", "")).split("peak")[1] == \
+        re.sub(r"budget \d+\n", "", full.serialize()).split("peak")[1]
+
+
+def test_error_codes():
+    with pytest.raises(_lib.ACError) as e:
+        api.graph_parse("autochunk-graph 1\ntensor x f32 2,3\ninput x\nnode r relu t9 y\n")
+    assert e.value.status == _lib.AC_ERR_GRAPH
+    cg = _c_graph("tiny")
+    for bad in ["autochunk-plan 1\nregion s=softmax e=softmax n=2 dims=2\n",     # softmax dim: BREAK
+                "autochunk-plan 1\nregion s=scores e=pv n=99999 dims=0\n",       # n > extent
+                "autochunk-plan 1\nregion s=nope e=pv n=2 dims=0\n",
+                "autochunk-plan 1\nregion s=scores e=pv n=2 dims=0\nregion s=softmax e=proj_o n=2 dims=0\n"]:
+        with pytest.raises(_lib.ACError) as e:
+            api.plan_parse(cg, bad)
+        assert e.value.status == _lib.AC_ERR_PLAN
+    p = api.ac_plan(cg, int(0.2 * memory.profile(workloads.config("tiny")).peak_bytes))
+    assert p.status == _lib.AC_ERR_BUDGET and p.num_regions > 0
