@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""Benchmark of the AutoChunk hot path: one block forward under the plan that
+ac_plan selects for BASELINE.json's GPT config at a 20 % activation budget
+(configs[1]), executed chunk by chunk by libautochunk's sm_100a kernels.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config gpt|vit|unet|af|tiny]
+
+Prints ONE JSON line (rank 0).  A step = one pass of the whole hot path (LN1,
+Q/K/V projections, the chunk loop of QK^T -> softmax -> PV, out-projection,
+LN2, FFN1+GELU, FFN2) over one synthetic sequence resident in HBM.  `value` is
+tokens/s over all ranks (device time, max over ranks); `e2e` is the same metric
+through ac_run with the input copied from pinned host memory and the output
+copied back inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tokens/s and peak activation bytes vs unchunked (speed loss %) at 1/2/4/8 B200"
+WORKLOADS = {
+    "gpt": "GPT-style decoder block, seq 16384, hidden 1024, 16 heads, FFN 4096, causal, bf16, "
+           "budget = 20% of unchunked activation (BASELINE.json configs[1])",
+    "vit": "ViT-Large encoder block, 65536 tokens, hidden 1024, 16 heads, FFN 4096, bf16, budget 20%",
+    "unet": "UNet self-attention, 16384 tokens, hidden 640, 10 heads, bf16, budget 20%",
+    "af": "AlphaFold triangle attention pair (rows then columns), N_res 1024, c_z 128, 4 heads, c 32, bf16, "
+          "budget 20% (tokens = pair positions N_res^2)",
+    "tiny": "tiny attention+MLP block, seq 256, hidden 64, 2 heads, fp32, chunk 32 along seq",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=list(WORKLOADS), default="gpt")
+    ap.add_argument("--budget-frac", type=float, default=0.2)
+    ap.add_argument("--plan", default=None, help="user plan text (ac_plan_parse) instead of ac_plan")
+    ap.add_argument("--no-unchunked", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ workload
+def oracle_graph(name):
+    from oracle import workloads
+    return workloads.config(name)
+
+
+def tokens_per_step(name, og):
+    x = og.tensors[og.inputs[0]]
+    return x.shape[0] * x.shape[1] if name == "af" else x.shape[0]
+
+
+def device_inputs(og, torch):
+    import numpy as np
+    import synth
+    samples = synth.make_inputs(og.input_specs(), 0)
+    dev = {}
+    for t, s in samples.items():
+        if s.dtype == "bf16":
+            dev[t] = torch.from_numpy(s.storage.astype(np.int16)).view(torch.bfloat16).cuda()
+        else:
+            dev[t] = torch.from_numpy(np.ascontiguousarray(s.storage)).cuda()
+    return samples, dev
+
+
+# ------------------------------------------------------------------ roofline bookkeeping
+def algorithmic(og, plan_regions, node_id, peaks):
+    """Algorithmic work of one node summed over one step, per DESIGN.md §7:
+    bytes that must cross HBM (reads of inputs + writes of outputs, only the
+    causal lower triangle for S/P) for HBM-bound kinds, FLOPs for GEMMs."""
+    n = next(x for x in og.nodes if x.id == node_id)
+    T = og.tensors
+    esz = T[n.output].esize
+    if n.kind == "softmax":
+        sh = T[n.inputs[0]].shape
+        causal = any(x.kind == "attn_scores" and x.output == n.inputs[0] and x.attrs.get("causal", 0)
+                     for x in og.nodes)
+        if causal:          # rows i read i+1 scores, write up to the 128-block end
+            h, N, M = sh
+            rd = h * N * (N + 1) // 2
+            wr = h * sum(min(M, (i // 128 + 1) * 128) for i in range(N))
+            return "hbm", (rd + wr) * esz
+        el = 1
+        for s in sh:
+            el *= s
+        return "hbm", 2 * el * esz
+    if n.kind in ("attn_scores", "attn_pv", "tri_scores", "tri_pv"):
+        from oracle import ops
+        fl = ops.flops(n.kind, n.attrs, [T[t].shape for t in n.inputs], T[n.output].shape)
+        if n.kind == "attn_scores" and n.attrs.get("causal", 0) or n.kind == "attn_pv" and any(
+                x.kind == "attn_scores" and x.attrs.get("causal", 0) for x in og.nodes):
+            N = T[n.output].shape[1] if n.kind == "attn_scores" else T[n.output].shape[0]
+            fl = fl * (N + 1) // (2 * N)
+        # S / P are N x N-sized: memory-bound at dh <= 80 (AI ~ 63 flop/B < ridge 251)
+        if n.kind in ("attn_scores", "tri_scores"):
+            by = T[n.output].bytes
+        else:
+            by = T[n.inputs[0]].bytes
+        if n.kind in ("attn_scores", "attn_pv") and "causal" in str(n.attrs) or (
+                n.kind == "attn_pv" and any(x.kind == "attn_scores" and x.attrs.get("causal", 0) for x in og.nodes)):
+            by = by // 2
+        return "hbm", by
+    if n.kind == "linear":
+        from oracle import ops
+        fl = ops.flops(n.kind, n.attrs, [T[t].shape for t in n.inputs], T[n.output].shape)
+        return "tensor", fl
+    if n.kind == "layernorm":
+        return "hbm", 2 * T[n.output].bytes
+    return "hbm", T[n.output].bytes
+
+
+def cpu_baseline(name, og, samples, budget_s=20.0):
+    """The oracle as it stands on this host: sampled output rows of the block
+    (K/V of all rows + R query rows), rows/s."""
+    import numpy as np
+    from oracle import blocks, executor
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    vals = {t: s.value for t, s in samples.items()}
+    if name in ("gpt", "vit", "unet", "tiny"):
+        N = og.tensors["x"].shape[0]
+        rows = np.arange(0, N, max(1, N // 32))[:32]
+        t0 = time.perf_counter()
+        blocks.transformer_rows(og, vals, rows)
+        dt = time.perf_counter() - t0
+        return {"value": len(rows) / dt, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                "sample": f"{len(rows)} output rows of the {name} block incl. LN1/K/V of all {N} rows "
+                          f"(fp64 numpy, {dt:.1f} s)"}
+    if name == "af":
+        from oracle import workloads
+        small = workloads.tri_attn_pair(128, 128, 4, 32, "bf16", name="af_sample")
+        import synth
+        v = {t: s.value for t, s in synth.make_inputs(small.input_specs(), 0).items()}
+        t0 = time.perf_counter()
+        executor.run(small, v)
+        dt = time.perf_counter() - t0
+        return {"value": 128 * 128 / dt, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                "sample": f"full AF triangle-attention pair at N_res=128 (fp64 numpy, {dt:.1f} s)"}
+    return None
+
+
+# ------------------------------------------------------------------ reference arm
+def reference_arm(args):
+    """The oracle timed as the base contract's reference arm."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+    import synth
+    from oracle import blocks
+    og = oracle_graph(args.config)
+    samples = synth.make_inputs(og.input_specs(), 0)
+    vals = {t: s.value for t, s in samples.items()}
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    N = og.tensors[og.inputs[0]].shape[0]
+    R = 16
+    times = []
+    for k in range(args.warmup + args.steps):
+        rows = (np.arange(R) * (N // R) + k) % N
+        t0 = time.perf_counter()
+        if args.config == "af":
+            from oracle import executor, workloads
+            small = workloads.tri_attn_pair(64, 128, 4, 32, "bf16", name="af_sample")
+            executor.run(small, {t: s.value for t, s in synth.make_inputs(small.input_specs(), 0).items()})
+        else:
+            blocks.transformer_rows(og, vals, rows)
+        if k >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    units = 64 * 64 if args.config == "af" else R
+    tot = sum(times)
+    value = units * len(times) / tot
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": WORKLOADS[args.config], "sample": f"{units} output rows per step"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{units} sampled output rows per step (incl. full K/V)"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    import torch
+    import torch.distributed as dist
+
+    from oracle import graph as og_graph
+    from paper_2401_10652_b200 import api
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    og = oracle_graph(args.config)
+    cg = api.graph_parse(og_graph.serialize(og))
+    prof0, _ = api.estimate_memory(cg)
+    budget = int(args.budget_frac * prof0.peak_bytes)
+    if args.plan:
+        plan = api.plan_parse(cg, args.plan)
+    elif args.config == "tiny":
+        plan = api.plan_parse(cg, "autochunk-plan 1\nregion s=scores e=pv n=8 dims=0\n")
+    else:
+        plan = api.ac_plan(cg, budget)
+    profp, _ = api.estimate_memory(cg, plan)
+    comm = None
+    if world > 1:
+        uid = [api.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = api.Comm(uid[0], rank, world, local)
+    samples, dev = device_inputs(og, torch)
+    s = torch.cuda.current_stream()
+    ws = torch.empty(max(plan.workspace_bytes(), 16), dtype=torch.uint8, device="cuda")
+    TD = {"bf16": torch.bfloat16, "f32": torch.float32}
+    outs = {o: torch.empty(og.tensors[o].shape, dtype=TD[og.tensors[o].dtype], device="cuda") for o in og.outputs}
+    ins = {t: dev[t] for t in og.inputs + og.weights}
+    ex = api.Exec(plan, ws, comm)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+
+    def timed(exe, inputs, outputs, K, W, profile=False, pre=None, post=None):
+        for _ in range(W):
+            exe.run(inputs, outputs)
+        exe.set_profiling(profile)
+        torch.cuda.synchronize()
+        barrier()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        kt = {}
+        for k in range(K):
+            flush.fill_(k & 0xFF)                      # L2 flushed between timed iterations
+            evs[k][0].record(s)
+            if pre:
+                pre()
+            exe.run(inputs, outputs)
+            if post:
+                post()
+            evs[k][1].record(s)
+            if profile:
+                for node, kind, ms, n in exe.kernel_times():
+                    a = kt.setdefault(node, [kind, 0.0, 0])
+                    a[1] += ms
+                    a[2] += n
+        torch.cuda.synchronize()
+        barrier()
+        exe.set_profiling(False)
+        tot = sum(a.elapsed_time(b) for a, b in evs)
+        if world > 1:
+            t = torch.tensor([tot], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tot = t.item()
+        return tot, kt
+
+    peaks, peak_src = load_peaks()
+    units = tokens_per_step(args.config, og)
+    with ClockSampler(local) as clk:
+        tot_ms, kt = timed(ex, ins, outs, args.steps, args.warmup, profile=True)
+    st = ex.stats()
+    clocks = clk.summary()
+    value = units * args.steps / (tot_ms / 1e3)
+    ms_step = tot_ms / args.steps
+
+    # dominant kernel roofline (device time share inside the timed steps)
+    roof = None
+    shares = {}
+    if kt:
+        total_k = sum(v[1] for v in kt.values())
+        dom = max(kt.items(), key=lambda kv: kv[1][1])
+        node, (kind, ms, nl) = dom
+        bound, work = algorithmic(og, None, node, peaks)
+        per_launch_ms = ms / nl
+        launches_per_step = nl / args.steps
+        work_per_launch = work / launches_per_step
+        if bound == "hbm":
+            ach = work_per_launch / (per_launch_ms / 1e3) / 1e9
+            pk = peaks["hbm_gbs"]
+            unit = "GB/s"
+        else:
+            ach = work_per_launch / (per_launch_ms / 1e3) / 1e12
+            pk = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+            unit = "TFLOP/s"
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+        if os.path.exists(tf):
+            traffic = json.load(open(tf)).get(node)
+        roof = {"bound": bound, "achieved": round(ach, 1), "peak": pk, "unit": unit, "frac": round(ach / pk, 4),
+                "traffic": traffic, "kernel": f"{node} ({kind})", "launches_per_step": launches_per_step,
+                "share_of_step": round(ms / total_k, 4), "peak_source": peak_src}
+        shares = {k: {"kind": v[0], "ms_per_step": round(v[1] / args.steps, 4), "launches_per_step": v[2] / args.steps}
+                  for k, v in sorted(kt.items(), key=lambda kv: -kv[1][1])}
+
+    # same kernels, unchunked (speed loss) — when it fits
+    unchunked = None
+    if not args.no_unchunked and not args.profile:
+        try:
+            up = api.plan_parse(cg, "autochunk-plan 1\n")
+            need = up.workspace_bytes()
+            free, _ = torch.cuda.mem_get_info()
+            if need + (1 << 30) < free:
+                wsu = torch.empty(need, dtype=torch.uint8, device="cuda")
+                exu = api.Exec(up, wsu, comm)
+                tu, _ = timed(exu, ins, outs, max(3, args.steps // 2), 2)
+                vu = units * max(3, args.steps // 2) / (tu / 1e3)
+                unchunked = {"value": vu, "ms_per_step": tu / max(3, args.steps // 2),
+                             "speed_loss": 1.0 - value / vu, "workspace_bytes": need}
+                del exu, wsu
+            else:
+                unchunked = {"value": None, "speed_loss": None, "note": f"unchunked OOM (needs {need} B)"}
+        except Exception as e:  # pragma: no cover
+            unchunked = {"error": str(e)}
+        torch.cuda.empty_cache()
+
+    # end to end: pinned host input -> device, ac_run, output -> pinned host
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        xin = og.inputs[0]
+        yout = og.outputs[0]
+        hx = torch.empty_like(dev[xin], device="cpu").pin_memory()
+        hx.copy_(dev[xin].cpu())
+        hy = torch.empty_like(outs[yout], device="cpu").pin_memory()
+        dx = torch.empty_like(dev[xin])
+        ins2 = dict(ins)
+        ins2[xin] = dx
+        te, _ = timed(ex, ins2, outs, args.steps, 1, pre=lambda: dx.copy_(hx, non_blocking=True),
+                      post=lambda: hy.copy_(outs[yout], non_blocking=True))
+        e2e = {"value": units * args.steps / (te / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": hx.numel() * hx.element_size(),
+               "d2h_bytes_per_step": hy.numel() * hy.element_size()}
+
+    if rank != 0:
+        return 0
+    cpu = None
+    if not args.no_cpu and not args.profile:
+        try:
+            cpu = cpu_baseline(args.config, og, samples)
+        except Exception as e:  # pragma: no cover
+            cpu = {"error": str(e)}
+    plan_txt = plan.serialize().splitlines()
+    regions = [ln.split(" flow=")[0] for ln in plan_txt if ln.startswith("region")]
+    caller = sum(og.tensors[t].bytes for t in og.inputs + og.outputs)
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16" if og.tensors[og.inputs[0]].dtype == "bf16" else "f32",
+        "data": "synthetic (seeded PCG64, DESIGN.md §4)",
+        "config": {"workload": WORKLOADS[args.config], "plan": regions, "parallelism": f"chunk-split x{world}",
+                   "l2": "flushed between timed steps (256 MiB write)"},
+        "peak_activation_bytes": {"planned": profp.peak_bytes, "unchunked": prof0.peak_bytes,
+                                  "reduction": round(1 - profp.peak_bytes / prof0.peak_bytes, 4),
+                                  "budget": budget, "arena_bytes": st.workspace_high_water,
+                                  "arena_plus_caller": st.workspace_high_water + caller},
+        "unchunked": unchunked, "roofline": roof, "stages": shares, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": st.launches * args.steps, "clocks": clocks,
+        "paper": {"claim": ">80% activation reduction at <10% speed loss; <10% loss at 20% memory",
+                  "hardware": "A100 80GB, PyTorch (P:336)"},
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -157,6 +157,13 @@ int32_t ac_plan_num_regions(const ac_chunk_plan* p);
  * static arena).  -1 on error. */
 int64_t ac_plan_workspace_bytes(const ac_chunk_plan* p, int32_t rank, int32_t world);
 
+/* Chunks [*c0, *c1) of region `region` (commit order) that rank `rank` of
+ * `world` executes: floor(rank n / world) .. floor((rank+1) n / world)
+ * (SURVEY §8(e)).  Also reports the region's chunk_len and extent.
+ * Errors: AC_ERR_ARG. */
+ac_status ac_plan_rank_chunks(const ac_chunk_plan* p, int32_t region, int32_t rank, int32_t world, int64_t* c0,
+                              int64_t* c1, int64_t* chunk_len, int64_t* extent);
+
 /* ------------------------------------------------------------------ multi-GPU */
 
 /* NCCL bootstrap: rank 0 calls ac_comm_get_unique_id, the 128
@@ -203,6 +210,21 @@ typedef struct ac_run_stats {
   int32_t chunks_run;            /* chunk iterations executed on this rank */
 } ac_run_stats;
 ac_status ac_exec_stats(const ac_exec* e, ac_run_stats* out);
+
+/* Per-stage timing: while profiling is on, ac_run brackets every kernel
+ * launch with CUDA events on the run stream (a few microseconds of host time
+ * per launch, no device synchronisation).  ac_exec_kernel_times synchronises
+ * on the last event and returns, per graph node (chunk iterations summed), the
+ * total device milliseconds and launch count of the last ac_run.  *n is set to
+ * the number of entries available; at most `cap` are written. */
+typedef struct ac_kernel_time {
+  char node[48];     /* graph node id */
+  char kind[16];     /* node kind */
+  double ms;
+  int32_t launches;
+} ac_kernel_time;
+ac_status ac_exec_set_profiling(ac_exec* e, int32_t on);
+ac_status ac_exec_kernel_times(const ac_exec* e, ac_kernel_time* out, int32_t cap, int32_t* n);
 
 #ifdef __cplusplus
 }

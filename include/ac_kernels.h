@@ -49,10 +49,12 @@ ac_status ac_kernel_gemm(const ac_gemm_desc* d, void* stream);
 ac_status ac_kernel_layernorm(const void* x, const void* gamma, const void* beta, void* y, int64_t rows,
                               int32_t C, float eps, int32_t dtype, void* stream);
 
-/* Row softmax (stable), rows of ncols with row stride ld; causal per
- * ac::softmax_rows (row r is global row row_off + r). */
+/* Row softmax (stable), rows of ncols with row stride ld.  causal: row r is
+ * query row R = row_off + (r % group) (group = rows per head, 0 = no wrap); it
+ * reads columns <= R and writes columns < ceil128(R+1), zeros above the
+ * diagonal. */
 ac_status ac_kernel_softmax(const void* s, void* p, int64_t rows, int64_t ncols, int64_t ld, int32_t causal,
-                            int64_t row_off, int32_t dtype, void* stream);
+                            int64_t row_off, int64_t group, int32_t dtype, void* stream);
 
 #ifdef __cplusplus
 }

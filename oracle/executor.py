@@ -82,9 +82,15 @@ def _last_use(g: Graph):
     return last
 
 
-def tracked_run(g: Graph, values: dict, regions=(), mirror=False, contiguity=False):
+def tracked_run(g: Graph, values: dict, regions=(), mirror=False, contiguity=False, chunk_ranges=None):
     """Execute (chunked if regions are given) while measuring the live activation
-    bytes at every step from real buffers.  Returns (outputs, per_step)."""
+    bytes at every step from real buffers.  Returns (outputs, per_step).
+    chunk_ranges: optional {region index: (c0, c1)} — only those chunks run (one
+    rank's share); Y^c slabs of other chunks stay zero."""
+    ranges = {}
+    for k, r in enumerate(regions):
+        if r.n > 1 and chunk_ranges is not None and k in chunk_ranges:
+            ranges[id(r)] = chunk_ranges[k]
     regions = [r for r in regions if r.n > 1]
     esz = {t: g.tensors[t].esize for t in g.tensors}
     wset = set(g.weights)
@@ -101,7 +107,8 @@ def tracked_run(g: Graph, values: dict, regions=(), mirror=False, contiguity=Fal
         n = g.nodes[i]
         if i in at:
             r = at[i]
-            _tracked_region(g, r, env, tr, per_step, esz, wset, last, mirror, contiguity)
+            _tracked_region(g, r, env, tr, per_step, esz, wset, last, mirror, contiguity,
+                            ranges.get(id(r), (0, r.n)))
             # free everything whose last use was inside the region
             for t in list(tr.live):
                 if isinstance(t, str) and last.get(t, -1) <= r.end:
@@ -122,7 +129,7 @@ def tracked_run(g: Graph, values: dict, regions=(), mirror=False, contiguity=Fal
     return {o: env[o] for o in g.outputs}, per_step
 
 
-def _tracked_region(g, r, env, tr, per_step, esz, wset, last, mirror, contiguity):
+def _tracked_region(g, r, env, tr, per_step, esz, wset, last, mirror, contiguity, crange=None):
     from .memory import contiguity_cost
     E, n = r.extent, r.n
     L = -(-E // n)
@@ -147,7 +154,8 @@ def _tracked_region(g, r, env, tr, per_step, esz, wset, last, mirror, contiguity
             for t in g.nodes[k].inputs:
                 if t in produced:
                     ilast[t] = k
-    for c in range(n):
+    c0, c1 = crange if crange is not None else (0, n)
+    for c in range(c0, c1):
         off = c * L
         ln = min(L, E - off)
         if ln <= 0:
@@ -189,6 +197,6 @@ def _tracked_region(g, r, env, tr, per_step, esz, wset, last, mirror, contiguity
             tr.free(("ctg",))
 
 
-def run_chunked(g: Graph, values: dict, regions, mirror: bool = False) -> dict:
-    outs, _ = tracked_run(g, values, regions, mirror)
+def run_chunked(g: Graph, values: dict, regions, mirror: bool = False, chunk_ranges=None) -> dict:
+    outs, _ = tracked_run(g, values, regions, mirror, chunk_ranges=chunk_ranges)
     return outs

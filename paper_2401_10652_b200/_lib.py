@@ -53,6 +53,10 @@ class RunStats(C.Structure):
                 ("launches", C.c_int32), ("chunks_run", C.c_int32)]
 
 
+class KernelTime(C.Structure):
+    _fields_ = [("node", C.c_char * 48), ("kind", C.c_char * 16), ("ms", C.c_double), ("launches", C.c_int32)]
+
+
 class GemmDesc(C.Structure):
     _fields_ = [("dtype", C.c_int32), ("M", C.c_int32), ("N", C.c_int32), ("K", C.c_int32),
                 ("B1", C.c_int32), ("B2", C.c_int32),
@@ -89,6 +93,8 @@ SIGNATURES = [
     ("ac_plan_free", None, [P]),
     ("ac_plan_num_regions", C.c_int32, [P]),
     ("ac_plan_workspace_bytes", C.c_int64, [P, C.c_int32, C.c_int32]),
+    ("ac_plan_rank_chunks", C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("ac_comm_get_unique_id", C.c_int, [C.c_char_p]),
     ("ac_comm_init", C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(P)]),
     ("ac_comm_free", None, [P]),
@@ -96,9 +102,12 @@ SIGNATURES = [
     ("ac_exec_free", None, [P]),
     ("ac_run", C.c_int, [P, C.POINTER(Tensor), C.c_int32, C.POINTER(Tensor), C.c_int32, P]),
     ("ac_exec_stats", C.c_int, [P, C.POINTER(RunStats)]),
+    ("ac_exec_set_profiling", C.c_int, [P, C.c_int32]),
+    ("ac_exec_kernel_times", C.c_int, [P, C.POINTER(KernelTime), C.c_int32, C.POINTER(C.c_int32)]),
     ("ac_kernel_gemm", C.c_int, [C.POINTER(GemmDesc), P]),
     ("ac_kernel_layernorm", C.c_int, [P, P, P, P, C.c_int64, C.c_int32, C.c_float, C.c_int32, P]),
-    ("ac_kernel_softmax", C.c_int, [P, P, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int64, C.c_int32, P]),
+    ("ac_kernel_softmax", C.c_int, [P, P, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int64, C.c_int64,
+                                    C.c_int32, P]),
 ]
 
 _lib = None

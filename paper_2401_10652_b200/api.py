@@ -91,6 +91,13 @@ class Plan:
     def num_regions(self) -> int:
         return lib().ac_plan_num_regions(self._h)
 
+    def rank_chunks(self, region: int, rank: int, world: int):
+        """(c0, c1, chunk_len, extent): the chunks of `region` that `rank` runs."""
+        a, b, ln, ext = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().ac_plan_rank_chunks(self._h, region, rank, world, C.byref(a), C.byref(b), C.byref(ln),
+                                        C.byref(ext)))
+        return a.value, b.value, ln.value, ext.value
+
     def workspace_bytes(self, rank: int = 0, world: int = 1) -> int:
         v = lib().ac_plan_workspace_bytes(self._h, rank, world)
         if v < 0:
@@ -128,3 +135,94 @@ def estimate_memory(g: Graph, plan: Plan | None = None):
     arr = (C.c_int64 * max(n, 1))()
     check(lib().ac_estimate_memory(g.handle, plan.handle if plan is not None else None, C.byref(prof), arr))
     return prof, list(arr)[:n]
+
+
+class Comm:
+    """NCCL communicator (ac_comm_*); `unique_id` is broadcast by the caller."""
+
+    def __init__(self, unique_id: bytes, rank: int, world: int, device: int):
+        out = C.c_void_p()
+        check(lib().ac_comm_init(unique_id, rank, world, device, C.byref(out)))
+        self._h = out
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().ac_comm_get_unique_id(buf))
+        return buf.raw
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().ac_comm_free(self._h)
+            self._h = None
+
+
+_TORCH_DT = None
+
+
+def _dtype_code(t) -> int:
+    import torch
+    return {torch.float32: L.AC_F32, torch.bfloat16: L.AC_BF16, torch.float64: L.AC_F64}[t.dtype]
+
+
+def _tensor(tid: str, t, keep: list) -> L.Tensor:
+    b = tid.encode()
+    keep.append(b)
+    at = L.Tensor()
+    at.tensor_id = b
+    at.dtype = _dtype_code(t)
+    at.ndim = t.dim()
+    for i in range(t.dim()):
+        at.shape[i] = t.shape[i]
+        at.stride[i] = t.stride(i)
+    at.data = t.data_ptr()
+    return at
+
+
+class Exec:
+    """ac_exec_create / ac_run / ac_exec_stats.  `workspace` is a caller-owned
+    device tensor of at least plan.workspace_bytes() bytes."""
+
+    def __init__(self, plan: Plan, workspace, comm: Comm | None = None):
+        out = C.c_void_p()
+        nbytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+        ptr = None if workspace is None else workspace.data_ptr()
+        check(lib().ac_exec_create(plan.handle, ptr, nbytes, comm.handle if comm else None, C.byref(out)))
+        self._h = out
+        self.plan, self.workspace, self.comm = plan, workspace, comm
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().ac_exec_free(self._h)
+            self._h = None
+
+    def run(self, inputs: dict, outputs: dict, stream=None):
+        import torch
+        keep = []
+        ins = [_tensor(k, v, keep) for k, v in inputs.items()]
+        outs = [_tensor(k, v, keep) for k, v in outputs.items()]
+        ia = (L.Tensor * max(len(ins), 1))(*ins)
+        oa = (L.Tensor * max(len(outs), 1))(*outs)
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        check(lib().ac_run(self._h, ia, len(ins), oa, len(outs), C.c_void_p(stream.cuda_stream)))
+
+    def stats(self) -> L.RunStats:
+        s = L.RunStats()
+        check(lib().ac_exec_stats(self._h, C.byref(s)))
+        return s
+
+    def set_profiling(self, on: bool = True):
+        check(lib().ac_exec_set_profiling(self._h, int(on)))
+
+    def kernel_times(self) -> list:
+        """[(node id, kind, total ms, launches)] of the last run (profiling on)."""
+        n = C.c_int32()
+        check(lib().ac_exec_kernel_times(self._h, None, 0, C.byref(n)))
+        arr = (L.KernelTime * max(n.value, 1))()
+        check(lib().ac_exec_kernel_times(self._h, arr, n.value, C.byref(n)))
+        return [(a.node.decode(), a.kind.decode(), a.ms, a.launches) for a in arr[: n.value]]

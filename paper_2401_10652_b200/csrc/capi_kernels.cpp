@@ -24,6 +24,11 @@ extern "C" ac_status ac_kernel_gemm(const ac_gemm_desc* d, void* stream) {
   e.add = d->add; e.add_sb1 = d->add_sb1; e.add_sb2 = d->add_sb2; e.add_sm = d->add_sm; e.add_sn = d->add_sn;
   e.gate = d->gate; e.res = d->res;
   e.out = d->out; e.out_sb1 = d->out_sb1; e.out_sb2 = d->out_sb2; e.out_sm = d->out_sm; e.out_sn = d->out_sn;
+  // gate and residual share the output layout at this entry point
+  e.gate_sb1 = e.res_sb1 = d->out_sb1;
+  e.gate_sb2 = e.res_sb2 = d->out_sb2;
+  e.gate_sm = e.res_sm = d->out_sm;
+  e.gate_sn = e.res_sn = d->out_sn;
   cudaError_t err;
   if (d->dtype == 1) err = gemm_tc(p, static_cast<cudaStream_t>(stream), d->bn);
   else if (d->dtype == 0) err = gemm_f32(p, static_cast<cudaStream_t>(stream));
@@ -38,7 +43,8 @@ extern "C" ac_status ac_kernel_layernorm(const void* x, const void* gamma, const
 }
 
 extern "C" ac_status ac_kernel_softmax(const void* s, void* p, int64_t rows, int64_t ncols, int64_t ld,
-                                       int32_t causal, int64_t row_off, int32_t dtype, void* stream) {
-  return cuda_status(softmax_rows(s, p, rows, ncols, ld, causal, row_off, dtype, static_cast<cudaStream_t>(stream)),
+                                       int32_t causal, int64_t row_off, int64_t group, int32_t dtype, void* stream) {
+  return cuda_status(softmax_rows(s, p, rows, ncols, ld, group * ld, ld, group * ld, causal, row_off, group, dtype,
+                                  static_cast<cudaStream_t>(stream)),
                      "ac_kernel_softmax");
 }

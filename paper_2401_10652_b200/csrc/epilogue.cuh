@@ -1,6 +1,6 @@
 // Shared GEMM epilogue (DESIGN.md §5 G1): applied per output element in fp32,
-// rounded once at the store.  Used by the tcgen05 path (T = bf16) and the SIMT
-// fp32 path (T = float).
+// rounded once at the store.  Used by the tcgen05 path (T = bf16); the SIMT
+// fp32 path applies the same order inline.
 #pragma once
 #include <cuda_bf16.h>
 #include <math_constants.h>
@@ -30,59 +30,129 @@ __device__ __forceinline__ float act_apply(int act, float v) {
   return v;
 }
 
-// Process 32 consecutive columns n0..n0+31 of row m (vals: fp32 accumulators).
-// Columns >= N and rows >= M are not stored.
+// v = acc*scale (+add) (+bias) -> act (*gate) (+res), causal -> -inf.  o = output offset.
 template <typename T>
-__device__ __forceinline__ void epilogue_row32(const Epilogue& ep, int M, int N, int b1, int b2,
-                                               int m, int n0, float (&v)[32]) {
-  if (m >= M) return;
-  const int64_t ob = static_cast<int64_t>(b1) * ep.out_sb1 + static_cast<int64_t>(b2) * ep.out_sb2 +
-                     static_cast<int64_t>(m) * ep.out_sm;
-  const bool full = (n0 + 32 <= N);
-  const T* add = static_cast<const T*>(ep.add);
-  const T* bias = static_cast<const T*>(ep.bias);
-  const T* gate = static_cast<const T*>(ep.gate);
-  const T* res = static_cast<const T*>(ep.res);
+__device__ __forceinline__ float epi_value(const Epilogue& ep, int b1, int b2, int m, int n, float acc, int64_t o) {
+  float x = acc * ep.scale;
+  if (ep.add)
+    x += to_f<T>(static_cast<const T*>(ep.add)[static_cast<int64_t>(b1) * ep.add_sb1 +
+                                               static_cast<int64_t>(b2) * ep.add_sb2 +
+                                               static_cast<int64_t>(m) * ep.add_sm + static_cast<int64_t>(n) * ep.add_sn]);
+  if (ep.bias) x += to_f<T>(static_cast<const T*>(ep.bias)[ep.bias_along_m ? m : n]);
+  x = act_apply(ep.act, x);
+  (void)o;
+  if (ep.gate)
+    x *= to_f<T>(static_cast<const T*>(ep.gate)[static_cast<int64_t>(b1) * ep.gate_sb1 +
+                                                static_cast<int64_t>(b2) * ep.gate_sb2 +
+                                                static_cast<int64_t>(m) * ep.gate_sm +
+                                                static_cast<int64_t>(n) * ep.gate_sn]);
+  if (ep.res)
+    x += to_f<T>(static_cast<const T*>(ep.res)[static_cast<int64_t>(b1) * ep.res_sb1 +
+                                               static_cast<int64_t>(b2) * ep.res_sb2 +
+                                               static_cast<int64_t>(m) * ep.res_sm + static_cast<int64_t>(n) * ep.res_sn]);
+  if (ep.causal && static_cast<int64_t>(n) + ep.col_off > ep.row_off + m) x = -CUDART_INF_F;
+  return x;
+}
+
+// Two adjacent columns n, n+1 of row m (a lane's share of a coalesced row segment).
+template <typename T>
+__device__ __forceinline__ void epilogue_pair(const Epilogue& ep, int N, int b1, int b2, int m, int n, float a0,
+                                              float a1) {
+  if (n >= N) return;
+  const int64_t o = static_cast<int64_t>(b1) * ep.out_sb1 + static_cast<int64_t>(b2) * ep.out_sb2 +
+                    static_cast<int64_t>(m) * ep.out_sm + static_cast<int64_t>(n) * ep.out_sn;
   T* out = static_cast<T*>(ep.out);
-  const int64_t ab = add ? (static_cast<int64_t>(b1) * ep.add_sb1 +
-                            static_cast<int64_t>(b2) * ep.add_sb2 + static_cast<int64_t>(m) * ep.add_sm)
-                         : 0;
-  const float bm = (bias && ep.bias_along_m) ? to_f<T>(bias[m]) : 0.f;
-  const int64_t lim = static_cast<int64_t>(ep.row_off) + m - ep.col_off;  // causal: n > lim masked
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const int n = n0 + j;
-    if (!full && n >= N) break;
-    float x = v[j] * ep.scale;
-    if (add) x += to_f<T>(add[ab + static_cast<int64_t>(n) * ep.add_sn]);
-    if (bias) x += ep.bias_along_m ? bm : to_f<T>(bias[n]);
-    x = act_apply(ep.act, x);
-    const int64_t o = ob + static_cast<int64_t>(n) * ep.out_sn;
-    if (gate) x *= to_f<T>(gate[o]);
-    if (res) x += to_f<T>(res[o]);
-    if (ep.causal && n > lim) x = -CUDART_INF_F;
-    v[j] = x;
+  const float x0 = epi_value<T>(ep, b1, b2, m, n, a0, o);
+  if (n + 1 >= N) {
+    out[o] = from_f<T>(x0);
+    return;
   }
-  if (full && ep.out_sn == 1 && sizeof(T) == 2 && ((ob + n0) % 8) == 0) {
-    uint4* dst = reinterpret_cast<uint4*>(out + ob + n0);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t w[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        __nv_bfloat162 h = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
-        w[e] = *reinterpret_cast<uint32_t*>(&h);
-      }
-      dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int n = n0 + j;
-      if (!full && n >= N) break;
-      out[ob + static_cast<int64_t>(n) * ep.out_sn] = from_f<T>(v[j]);
+  const float x1 = epi_value<T>(ep, b1, b2, m, n + 1, a1, o + ep.out_sn);
+  if constexpr (sizeof(T) == 2) {
+    if (ep.out_sn == 1 && (o & 1) == 0) {
+      *reinterpret_cast<__nv_bfloat162*>(out + o) = __floats2bfloat162_rn(x0, x1);
+      return;
     }
   }
+  out[o] = from_f<T>(x0);
+  out[o + ep.out_sn] = from_f<T>(x1);
+}
+
+__device__ __forceinline__ void bf16x8_to_f(const uint4& u, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+// Eight consecutive columns n..n+7 of row m, bf16, all aux tensors n-contiguous
+// and 16-byte aligned (checked on the host): one 16-byte load per aux tensor and
+// one 16-byte store.  Same operation order as epi_value.
+__device__ __forceinline__ void epilogue8(const Epilogue& ep, int b1, int b2, int m, int n, float (&x)[8]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] *= ep.scale;
+  float a[8];
+  if (ep.add) {
+    const int64_t o = static_cast<int64_t>(b1) * ep.add_sb1 + static_cast<int64_t>(b2) * ep.add_sb2 +
+                      static_cast<int64_t>(m) * ep.add_sm + n;
+    bf16x8_to_f(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(ep.add) + o), a);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] += a[i];
+  }
+  if (ep.bias) {
+    const __nv_bfloat16* b = static_cast<const __nv_bfloat16*>(ep.bias);
+    if (ep.bias_along_m) {
+      const float bm = __bfloat162float(b[m]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] += bm;
+    } else {
+      bf16x8_to_f(*reinterpret_cast<const uint4*>(b + n), a);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] += a[i];
+    }
+  }
+  if (ep.act != ACT_NONE) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = act_apply(ep.act, x[i]);
+  }
+  if (ep.gate) {
+    const int64_t o = static_cast<int64_t>(b1) * ep.gate_sb1 + static_cast<int64_t>(b2) * ep.gate_sb2 +
+                      static_cast<int64_t>(m) * ep.gate_sm + n;
+    bf16x8_to_f(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(ep.gate) + o), a);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] *= a[i];
+  }
+  if (ep.res) {
+    const int64_t o = static_cast<int64_t>(b1) * ep.res_sb1 + static_cast<int64_t>(b2) * ep.res_sb2 +
+                      static_cast<int64_t>(m) * ep.res_sm + n;
+    bf16x8_to_f(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(ep.res) + o), a);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] += a[i];
+  }
+  if (ep.causal) {
+    const int64_t lim = ep.row_off + m - ep.col_off - n;  // column n+i masked when i > lim
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i > lim) x[i] = -CUDART_INF_F;
+  }
+  uint4 w;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(x[2 * i], x[2 * i + 1]);
+  const int64_t o = static_cast<int64_t>(b1) * ep.out_sb1 + static_cast<int64_t>(b2) * ep.out_sb2 +
+                    static_cast<int64_t>(m) * ep.out_sm + n;
+  *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + o) = w;
+}
+
+template <typename T>
+__device__ __forceinline__ void epilogue_one(const Epilogue& ep, int N, int b1, int b2, int m, int n, float a0) {
+  if (n >= N) return;
+  const int64_t o = static_cast<int64_t>(b1) * ep.out_sb1 + static_cast<int64_t>(b2) * ep.out_sb2 +
+                    static_cast<int64_t>(m) * ep.out_sm + static_cast<int64_t>(n) * ep.out_sn;
+  static_cast<T*>(ep.out)[o] = from_f<T>(epi_value<T>(ep, b1, b2, m, n, a0, o));
 }
 
 }  // namespace ac

@@ -1,0 +1,726 @@
+// L2 executor: plan -> static workspace arena + chunk-loop schedule -> sm_100a
+// kernels.
+//
+// * Arena: every activation that is not a graph input/weight/output lives in
+//   the caller's workspace at a static offset.  Live intervals follow the same
+//   chunked-liveness model as the estimator (R6): region inputs are
+//   held to region end, Y^c is allocated at region start, hoisted tensors live
+//   across the region, interior flow tensors get ONE chunk-sized scratch buffer
+//   that every chunk reuses.  Offsets are assigned first-fit in birth order.
+// * Chunk loop (G6): for each region, hoisted nodes run once, then chunk
+//   c = c0..c1-1 runs the flow nodes on views: X^c / Y^c are the full tensors
+//   narrowed along their chunk dim (pointer offset, same strides; TMA reads the
+//   strided slice, so no contiguity copy, R5), interior tensors are the scratch
+//   buffer narrowed to the chunk's length.  Y^c slices are written in place.
+// * Multi-GPU (§8(e)): rank r runs chunks [floor(r n / W), floor((r+1) n / W))
+//   and the Y^c slabs are exchanged with NCCL broadcasts from their owners.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <set>
+#include <string>
+#include <unordered_map>
+
+#include "comm.h"
+#include "errors.h"
+#include "handles.h"
+#include "kernels.h"
+
+using namespace ac;
+
+namespace ac {
+
+struct ArenaSlot {
+  int64_t offset = -1;  // -1: caller-owned
+  int64_t bytes = 0;
+  int birth = 0, death = 0;
+};
+
+struct Arena {
+  std::vector<ArenaSlot> slot;  // per tensor
+  int64_t size = 0;
+  int64_t live_peak = 0;        // max over steps of the bytes live in the arena
+};
+
+struct View {
+  char* p = nullptr;
+  int nd = 0;
+  int64_t sh[8] = {0};
+  int64_t st[8] = {0};
+};
+
+}  // namespace ac
+
+struct ac_exec {
+  std::shared_ptr<const Graph> g;
+  Plan plan;
+  Arena arena;
+  char* ws = nullptr;
+  int64_t ws_bytes = 0;
+  const ac_comm* comm = nullptr;
+  int rank = 0, world = 1;
+  DT dt = DT::BF16;
+  std::vector<int> region_of;          // node -> region index or -1
+  std::vector<char> causal_fast;       // per node: member of an aligned causal chain
+  std::vector<int> chain_rows_dim;     // per node: output dim holding query rows (-1 none)
+  mutable ac_run_stats stats{};
+  // profiling: event pairs per launch of the last run
+  bool profiling = false;
+  mutable std::vector<cudaEvent_t> ev_pool;
+  mutable std::vector<int> ev_node;    // node of launch k (events 2k, 2k+1)
+  ~ac_exec() {
+    for (auto ev : ev_pool) cudaEventDestroy(ev);
+  }
+};
+
+namespace {
+
+bool is_caller(const Graph& g, int t) { return g.is_input[t] || g.is_weight[t] || g.is_output[t]; }
+
+Arena build_arena(const Graph& g, const Plan& plan) {
+  const int T = static_cast<int>(g.tensors.size());
+  const int S = static_cast<int>(g.nodes.size());
+  Arena A;
+  A.slot.assign(T, ArenaSlot{});
+  std::vector<int> birth(T, 0), death(T, 0);
+  for (int i = 0; i < S; ++i) {
+    const int b = g.nodes[i].source() ? 0 : i;
+    birth[g.nodes[i].output] = b;
+    death[g.nodes[i].output] = b;
+  }
+  for (int i = 0; i < S; ++i)
+    for (int t : g.nodes[i].inputs) death[t] = std::max(death[t], i);
+  for (int o : g.outputs) death[o] = S - 1;
+  std::vector<int64_t> bytes(T);
+  for (int t = 0; t < T; ++t) bytes[t] = g.tensors[t].bytes();
+  for (const Region& r : plan.regions) {
+    if (r.n <= 1) continue;
+    std::vector<int> ins, outs;
+    region_io(g, r.start, r.end, ins, outs);
+    std::set<int> hout;
+    for (int i : r.hoisted) hout.insert(g.nodes[i].output);
+    for (int t : ins) death[t] = std::max(death[t], r.end);
+    for (auto& y : r.yc) birth[y.first] = std::min(birth[y.first], r.start);
+    for (int t : hout) {
+      birth[t] = r.start;
+      death[t] = std::max(death[t], r.end);
+    }
+    std::set<int> ycs;
+    for (auto& y : r.yc) ycs.insert(y.first);
+    for (int i = r.start; i <= r.end; ++i) {
+      const int t = g.nodes[i].output;
+      if (ycs.count(t) || hout.count(t)) continue;
+      bool out = g.is_output[t] != 0;
+      for (int c : g.consumers[t]) out = out || c > r.end;
+      if (out) continue;
+      const int d = r.dim_of(t);
+      if (d >= 0) {
+        const int64_t E = g.tensors[t].shape[d];
+        bytes[t] = bytes[t] / E * ((E + r.n - 1) / r.n);
+      }
+      int lastc = i;
+      for (int c : g.consumers[t])
+        if (c >= r.start && c <= r.end) lastc = std::max(lastc, c);
+      death[t] = lastc;
+    }
+  }
+  std::vector<int> order;
+  for (int t = 0; t < T; ++t)
+    if (!is_caller(g, t)) order.push_back(t);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return birth[a] < birth[b]; });
+  std::vector<int> placed;
+  for (int t : order) {
+    const int64_t sz = (bytes[t] + 255) / 256 * 256;
+    // first fit among the address ranges of time-overlapping placed tensors
+    std::vector<std::pair<int64_t, int64_t>> busy;
+    for (int u : placed)
+      if (!(death[u] < birth[t] || death[t] < birth[u]))
+        busy.push_back({A.slot[u].offset, A.slot[u].offset + (A.slot[u].bytes + 255) / 256 * 256});
+    std::sort(busy.begin(), busy.end());
+    int64_t off = 0;
+    for (auto& bz : busy) {
+      if (off + sz <= bz.first) break;
+      off = std::max(off, bz.second);
+    }
+    A.slot[t] = ArenaSlot{off, bytes[t], birth[t], death[t]};
+    A.size = std::max(A.size, off + sz);
+    placed.push_back(t);
+  }
+  for (int s = 0; s < S; ++s) {
+    int64_t live = 0;
+    for (int t : order)
+      if (A.slot[t].birth <= s && s <= A.slot[t].death) live += A.slot[t].bytes;
+    A.live_peak = std::max(A.live_peak, live);
+  }
+  return A;
+}
+
+bool gpu_kind(const std::string& k) {
+  return k == "layernorm" || k == "linear" || k == "attn_scores" || k == "softmax" || k == "attn_pv" ||
+         k == "tri_scores" || k == "tri_pv";
+}
+
+View full_view(const TensorMeta& tm, void* p) {
+  View v;
+  v.p = static_cast<char*>(p);
+  v.nd = static_cast<int>(tm.shape.size());
+  auto st = tm.strides();
+  for (int i = 0; i < v.nd; ++i) {
+    v.sh[i] = tm.shape[i];
+    v.st[i] = st[i];
+  }
+  return v;
+}
+
+View narrow(View v, int d, int64_t off, int64_t len, int esz) {
+  v.p += off * v.st[d] * esz;
+  v.sh[d] = len;
+  return v;
+}
+
+// stride of dims [a, b) collapsed into one index; -1 if not collapsible
+int64_t collapse(const View& v, int a, int b) {
+  if (a >= b) return 1;
+  for (int i = a; i < b - 1; ++i)
+    if (v.st[i] != v.st[i + 1] * v.sh[i + 1]) return -1;
+  return v.st[b - 1];
+}
+int64_t extent(const View& v, int a, int b) {
+  int64_t e = 1;
+  for (int i = a; i < b; ++i) e *= v.sh[i];
+  return e;
+}
+
+struct NodeCtx {
+  int64_t row_off = 0;  // global query-row offset of this view (causal)
+  int64_t col_off = 0;
+  bool fast = false;    // aligned causal chain: skip masked tiles / keys
+};
+
+cudaError_t gemm(DT dt, const GemmProblem& p, cudaStream_t s) {
+  return dt == DT::BF16 ? gemm_tc(p, s) : gemm_f32(p, s);
+}
+
+ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, const NodeCtx& cx, cudaStream_t s);
+
+ac_status launch_node(const ac_exec* e, int i, const std::vector<View>& V, const NodeCtx& cx, cudaStream_t s) {
+  if (!e->profiling) return launch_node_impl(e, i, V, cx, s);
+  const size_t k = e->ev_node.size();
+  while (e->ev_pool.size() < 2 * (k + 1)) {
+    cudaEvent_t ev;
+    if (cudaEventCreate(&ev) != cudaSuccess) return set_error(AC_ERR_CUDA, "cudaEventCreate failed");
+    e->ev_pool.push_back(ev);
+  }
+  cudaEventRecord(e->ev_pool[2 * k], s);
+  ac_status st = launch_node_impl(e, i, V, cx, s);
+  cudaEventRecord(e->ev_pool[2 * k + 1], s);
+  e->ev_node.push_back(i);
+  return st;
+}
+
+ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, const NodeCtx& cx, cudaStream_t s) {
+  const Graph& g = *e->g;
+  const Node& n = g.nodes[i];
+  const int dtc = e->dt == DT::BF16 ? 1 : 0;
+  auto in = [&](int k) -> const View& { return V[n.inputs[k]]; };
+  const View& out = V[n.output];
+  const std::string& k = n.kind;
+  cudaError_t err = cudaSuccess;
+  auto unsup = [&](const char* why) {
+    return set_error(AC_ERR_UNSUPPORTED, "node " + n.id + " (" + k + "): " + why);
+  };
+  if (k == "layernorm") {
+    const View& x = in(0);
+    const int na = static_cast<int>(n.ai("naxes"));
+    const int64_t C = extent(x, x.nd - na, x.nd);
+    if (collapse(x, 0, x.nd) != 1 || collapse(out, 0, out.nd) != 1) return unsup("non-contiguous rows");
+    err = layernorm(x.p, in(1).p, in(2).p, out.p, extent(x, 0, x.nd - na), static_cast<int>(C),
+                    static_cast<float>(n.af("eps", 1e-5)), dtc, s);
+  } else if (k == "softmax") {
+    const View& x = in(0);
+    if (n.ai("dim") != x.nd - 1 || x.st[x.nd - 1] != 1) return unsup("softmax over a non-last dim");
+    // rows = (leading dims) x (second-to-last dim): a group stride and a row stride
+    if (x.nd < 2) return unsup("softmax of a vector");
+    if (out.st[out.nd - 1] != 1) return unsup("softmax output not contiguous");
+    const int64_t ld = x.st[x.nd - 2], ldo = out.st[out.nd - 2];
+    const int64_t group = x.sh[x.nd - 2];
+    const int64_t gst = x.nd >= 3 ? collapse(x, 0, x.nd - 2) : group * ld;
+    const int64_t gsto = out.nd >= 3 ? collapse(out, 0, out.nd - 2) : group * ldo;
+    if (gst < 0 || gsto < 0) return unsup("softmax rows not uniformly strided");
+    const int64_t rows = extent(x, 0, x.nd - 1);
+    err = softmax_rows(x.p, out.p, rows, x.sh[x.nd - 1], ld, gst, ldo, gsto, cx.fast ? 1 : 0, cx.row_off, group,
+                       dtc, s);
+  } else {
+    GemmProblem p;
+    Epilogue& ep = p.ep;
+    ep.out = out.p;
+    if (k == "linear") {
+      const View& a = in(0);
+      const View& w = in(1);
+      const int kin = static_cast<int>(n.ai("kin"));
+      const int nrows = a.nd - kin;
+      const int nout = static_cast<int>(n.av("out").size());
+      const bool trans = n.ai("trans") != 0, swap = n.ai("swap") != 0;
+      const int64_t K = extent(a, nrows, a.nd);
+      if (collapse(a, nrows, a.nd) != 1) return unsup("K dims not contiguous");
+      const int64_t O = w.sh[0];
+      int ia = 2;
+      const void* bias = nullptr;
+      if (n.ai("bias")) bias = in(ia++).p;
+      const View* resv = n.ai("res") ? &in(ia) : nullptr;
+      ep.bias = bias;
+      ep.res = resv ? resv->p : nullptr;
+      const std::string act = n.as("act", "none");
+      ep.act = act == "gelu" ? ACT_GELU : act == "sigmoid" ? ACT_SIGMOID : act == "relu" ? ACT_RELU : ACT_NONE;
+      Operand W;
+      W.p = w.p;
+      W.srow = K;
+      if (!trans) {
+        if (swap) return unsup("swap without trans");
+        const int64_t sa = collapse(a, 0, nrows), so = collapse(out, 0, nrows), sf = collapse(out, nrows, out.nd);
+        const int64_t sr = resv ? collapse(*resv, 0, nrows) : 0;
+        if (sf == 1 && nrows == 2 && (sa < 0 || so < 0 || sr < 0)) {
+          // two row dims that do not collapse (a chunk of a middle dim): batch over the first
+          p.B1 = static_cast<int>(a.sh[0]);
+          p.M = static_cast<int>(a.sh[1]);
+          p.N = static_cast<int>(O);
+          p.K = static_cast<int>(K);
+          p.A.p = a.p; p.A.srow = a.st[1]; p.A.sb1 = a.st[0]; p.A.use_b1 = 1;
+          p.B = W;
+          ep.out_sb1 = out.st[0]; ep.out_sm = out.st[1]; ep.out_sn = 1;
+          if (resv) {
+            ep.res_sb1 = resv->st[0]; ep.res_sm = resv->st[1];
+            ep.res_sn = collapse(*resv, 2, resv->nd);
+            if (ep.res_sn < 0) return unsup("residual not collapsible");
+          }
+          goto launch;
+        }
+        if (sa < 0 || so < 0 || sf != 1) return unsup("rows not collapsible");
+        p.M = static_cast<int>(extent(a, 0, nrows));
+        p.N = static_cast<int>(O);
+        p.K = static_cast<int>(K);
+        p.A.p = a.p;
+        p.A.srow = sa;
+        p.B = W;
+        ep.out_sm = so;
+        ep.out_sn = 1;
+        if (resv) {
+          ep.res_sm = collapse(*resv, 0, nrows);
+          ep.res_sn = collapse(*resv, nrows, resv->nd);
+          if (ep.res_sm < 0 || ep.res_sn < 0) return unsup("residual not collapsible");
+        }
+      } else if (!swap) {
+        const int64_t sa = collapse(a, 0, nrows), sf = collapse(out, 0, nout), so = collapse(out, nout, out.nd);
+        if (sa < 0 || sf < 0 || so != 1) return unsup("rows not collapsible");
+        p.M = static_cast<int>(O);
+        p.N = static_cast<int>(extent(a, 0, nrows));
+        p.K = static_cast<int>(K);
+        p.A = W;
+        p.B.p = a.p;
+        p.B.srow = sa;
+        ep.out_sm = sf;
+        ep.out_sn = 1;
+        ep.bias_along_m = 1;
+        if (resv) {
+          ep.res_sm = collapse(*resv, 0, nout);
+          ep.res_sn = collapse(*resv, nout, resv->nd);
+          if (ep.res_sm < 0 || ep.res_sn < 0) return unsup("residual not collapsible");
+        }
+      } else {
+        if (nrows != 2) return unsup("swap needs two row dims");
+        const int64_t sf = collapse(out, 0, nout);
+        if (sf < 0) return unsup("features not collapsible");
+        p.M = static_cast<int>(O);
+        p.N = static_cast<int>(a.sh[0]);
+        p.B1 = static_cast<int>(a.sh[1]);
+        p.K = static_cast<int>(K);
+        p.A = W;
+        p.B.p = a.p;
+        p.B.srow = a.st[0];
+        p.B.sb1 = a.st[1];
+        p.B.use_b1 = 1;
+        ep.out_sm = sf;
+        ep.out_sb1 = out.st[nout];
+        ep.out_sn = out.st[nout + 1];
+        ep.bias_along_m = 1;
+        if (resv) {
+          ep.res_sm = collapse(*resv, 0, nout);
+          ep.res_sb1 = resv->st[nout];
+          ep.res_sn = resv->st[nout + 1];
+          if (ep.res_sm < 0) return unsup("residual not collapsible");
+        }
+      }
+    } else if (k == "attn_scores") {
+      const View &q = in(0), &kk = in(1);
+      p.M = static_cast<int>(q.sh[0]);
+      p.N = static_cast<int>(kk.sh[0]);
+      p.K = static_cast<int>(q.sh[2]);
+      p.B1 = static_cast<int>(q.sh[1]);
+      if (q.st[2] != 1 || kk.st[2] != 1) return unsup("head dim not contiguous");
+      p.A.p = q.p; p.A.srow = q.st[0]; p.A.sb1 = q.st[1]; p.A.use_b1 = 1;
+      p.B.p = kk.p; p.B.srow = kk.st[0]; p.B.sb1 = kk.st[1]; p.B.use_b1 = 1;
+      ep.out_sb1 = out.st[0]; ep.out_sm = out.st[1]; ep.out_sn = out.st[2];
+      ep.scale = static_cast<float>(n.af("scale", 1.0));
+      if (n.ai("causal")) {
+        ep.causal = 1;
+        ep.row_off = cx.row_off;
+        ep.col_off = cx.col_off;
+        p.causal_tiles = cx.fast ? 1 : 0;
+      }
+    } else if (k == "attn_pv") {
+      const View &pp = in(0), &vt = in(1);
+      p.M = static_cast<int>(pp.sh[1]);
+      p.N = static_cast<int>(vt.sh[1]);
+      p.K = static_cast<int>(pp.sh[2]);
+      p.B1 = static_cast<int>(pp.sh[0]);
+      if (pp.st[2] != 1 || vt.st[2] != 1) return unsup("key dim not contiguous");
+      p.A.p = pp.p; p.A.srow = pp.st[1]; p.A.sb1 = pp.st[0]; p.A.use_b1 = 1;
+      p.B.p = vt.p; p.B.srow = vt.st[1]; p.B.sb1 = vt.st[0]; p.B.use_b1 = 1;
+      ep.out_sb1 = out.st[1]; ep.out_sm = out.st[0]; ep.out_sn = out.st[2];
+      if (cx.fast) {
+        p.causal_k = 1;
+        p.k_row_off = cx.row_off;
+      }
+    } else if (k == "tri_scores") {
+      const View &q = in(0), &kk = in(1), &b = in(2);
+      const bool end = n.ai("ending") != 0;
+      if (q.st[3] != 1 || kk.st[3] != 1) return unsup("c not contiguous");
+      p.K = static_cast<int>(q.sh[3]);
+      p.B2 = static_cast<int>(q.sh[2]);
+      ep.scale = static_cast<float>(n.af("scale", 1.0));
+      ep.add = b.p;
+      ep.add_sb2 = b.st[0];
+      ep.out_sb1 = out.st[0]; ep.out_sb2 = out.st[1]; ep.out_sm = out.st[2]; ep.out_sn = out.st[3];
+      if (!end) {  // s[i,h,j,k]: batch (i,h), rows j, cols k
+        p.B1 = static_cast<int>(q.sh[0]);
+        p.M = static_cast<int>(q.sh[1]);
+        p.N = static_cast<int>(kk.sh[1]);
+        p.A.p = q.p; p.A.srow = q.st[1]; p.A.sb1 = q.st[0]; p.A.sb2 = q.st[2];
+        p.B.p = kk.p; p.B.srow = kk.st[1]; p.B.sb1 = kk.st[0]; p.B.sb2 = kk.st[2];
+        ep.add_sm = b.st[1]; ep.add_sn = b.st[2];
+      } else {     // s[j,h,i,k]: batch (j,h), rows i, cols k
+        p.B1 = static_cast<int>(q.sh[1]);
+        p.M = static_cast<int>(q.sh[0]);
+        p.N = static_cast<int>(kk.sh[0]);
+        p.A.p = q.p; p.A.srow = q.st[0]; p.A.sb1 = q.st[1]; p.A.sb2 = q.st[2];
+        p.B.p = kk.p; p.B.srow = kk.st[0]; p.B.sb1 = kk.st[1]; p.B.sb2 = kk.st[2];
+        ep.add_sm = b.st[2]; ep.add_sn = b.st[1];
+      }
+      p.A.use_b1 = p.A.use_b2 = p.B.use_b1 = p.B.use_b2 = 1;
+    } else if (k == "tri_pv") {
+      const View &pp = in(0), &vt = in(1), &gt = in(2);
+      const bool end = n.ai("ending") != 0;
+      if (pp.st[3] != 1 || vt.st[3] != 1) return unsup("key dim not contiguous");
+      p.B1 = static_cast<int>(pp.sh[0]);
+      p.B2 = static_cast<int>(pp.sh[1]);
+      p.M = static_cast<int>(pp.sh[2]);
+      p.N = static_cast<int>(vt.sh[1]);
+      p.K = static_cast<int>(pp.sh[3]);
+      p.A.p = pp.p; p.A.srow = pp.st[2]; p.A.sb1 = pp.st[0]; p.A.sb2 = pp.st[1];
+      p.B.p = vt.p; p.B.srow = vt.st[1]; p.B.sb1 = vt.st[2]; p.B.sb2 = vt.st[0];
+      p.A.use_b1 = p.A.use_b2 = p.B.use_b1 = p.B.use_b2 = 1;
+      ep.gate = gt.p;
+      if (!end) {  // o[i,j,h,c]: b1=i, b2=h, m=j
+        ep.out_sb1 = out.st[0]; ep.out_sb2 = out.st[2]; ep.out_sm = out.st[1]; ep.out_sn = out.st[3];
+        ep.gate_sb1 = gt.st[0]; ep.gate_sb2 = gt.st[2]; ep.gate_sm = gt.st[1]; ep.gate_sn = gt.st[3];
+      } else {     // o[i,j,h,c]: b1=j, b2=h, m=i
+        ep.out_sb1 = out.st[1]; ep.out_sb2 = out.st[2]; ep.out_sm = out.st[0]; ep.out_sn = out.st[3];
+        ep.gate_sb1 = gt.st[1]; ep.gate_sb2 = gt.st[2]; ep.gate_sm = gt.st[0]; ep.gate_sn = gt.st[3];
+      }
+    } else {
+      return unsup("no GPU kernel for this kind");
+    }
+  launch:
+    err = gemm(e->dt, p, s);
+  }
+  e->stats.launches += 1;
+  return cuda_status(err, ("node " + n.id).c_str());
+}
+
+// query-row dim of a node's output in an attention chain (causal offsets)
+int rows_dim(const Node& n) {
+  if (n.kind == "attn_scores" || n.kind == "softmax") return 1;
+  if (n.kind == "attn_pv") return 0;
+  return -1;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t ac_plan_workspace_bytes(const ac_chunk_plan* p, int32_t rank, int32_t world) {
+  if (!p || world < 1 || rank < 0 || rank >= world) {
+    set_error(AC_ERR_ARG, "ac_plan_workspace_bytes: bad arguments");
+    return -1;
+  }
+  return build_arena(*p->g, p->plan).size;
+}
+
+ac_status ac_plan_rank_chunks(const ac_chunk_plan* p, int32_t region, int32_t rank, int32_t world, int64_t* c0,
+                              int64_t* c1, int64_t* chunk_len, int64_t* extent) {
+  if (!p || !c0 || !c1 || world < 1 || rank < 0 || rank >= world || region < 0 ||
+      region >= static_cast<int32_t>(p->plan.regions.size()))
+    return set_error(AC_ERR_ARG, "ac_plan_rank_chunks: bad arguments");
+  const Region& R = p->plan.regions[region];
+  *c0 = chunk_begin(rank, R.n, world);
+  *c1 = chunk_begin(rank + 1, R.n, world);
+  if (chunk_len) *chunk_len = R.chunk_len();
+  if (extent) *extent = R.extent;
+  return AC_OK;
+}
+
+ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_bytes, const ac_comm* comm,
+                         ac_exec** out) {
+  if (!plan || !out) return set_error(AC_ERR_ARG, "ac_exec_create: NULL argument");
+  *out = nullptr;
+  const Graph& g = *plan->g;
+  std::unique_ptr<ac_exec> e(new ac_exec);
+  e->g = plan->g;
+  e->plan = plan->plan;
+  e->arena = build_arena(g, plan->plan);
+  if (ws_bytes < e->arena.size || (e->arena.size > 0 && !workspace))
+    return set_error(AC_ERR_WORKSPACE, "workspace of " + std::to_string(ws_bytes) + " bytes < required " +
+                                           std::to_string(e->arena.size));
+  e->ws = static_cast<char*>(workspace);
+  e->ws_bytes = ws_bytes;
+  e->comm = comm;
+  if (comm) {
+    e->rank = comm_rank(comm);
+    e->world = comm_world(comm);
+  }
+  // one element type for the whole graph (f32 -> SIMT path, bf16 -> tcgen05 path)
+  e->dt = g.tensors.empty() ? DT::BF16 : g.tensors[0].dtype;
+  for (auto& t : g.tensors)
+    if (t.dtype != e->dt || t.dtype == DT::F64)
+      return set_error(AC_ERR_UNSUPPORTED, "GPU executor needs one dtype (f32 or bf16) for every tensor");
+  for (auto& n : g.nodes)
+    if (!n.source() && !gpu_kind(n.kind))
+      return set_error(AC_ERR_UNSUPPORTED, "no GPU kernel for node " + n.id + " (" + n.kind + ")");
+  const int S = static_cast<int>(g.nodes.size());
+  e->region_of.assign(S, -1);
+  for (size_t r = 0; r < e->plan.regions.size(); ++r)
+    for (int i = e->plan.regions[r].start; i <= e->plan.regions[r].end; ++i) e->region_of[i] = static_cast<int>(r);
+  // aligned causal chains: attn_scores(causal) -> softmax -> attn_pv, S and P used
+  // only inside the chain, never chunked along keys, chunk starts multiples of 128
+  e->causal_fast.assign(S, 0);
+  e->chain_rows_dim.assign(S, -1);
+  for (int i = 0; i < S; ++i) {
+    const Node& n = g.nodes[i];
+    if (n.kind != "attn_scores" || !n.ai("causal")) continue;
+    const int s_t = n.output;
+    if (g.is_output[s_t] || g.consumers[s_t].size() != 1) continue;
+    const int sm = g.consumers[s_t][0];
+    if (g.nodes[sm].kind != "softmax" || g.nodes[sm].ai("dim") != 2) continue;
+    const int p_t = g.nodes[sm].output;
+    if (g.is_output[p_t] || g.consumers[p_t].size() != 1) continue;
+    const int pv = g.consumers[p_t][0];
+    if (g.nodes[pv].kind != "attn_pv" || g.nodes[pv].inputs[0] != p_t) continue;
+    bool ok = true;
+    for (int node : {i, sm, pv}) {
+      const int r = e->region_of[node];
+      if (r < 0) continue;
+      const Region& R = e->plan.regions[r];
+      if (R.n <= 1) continue;
+      const int d = R.dim_of(g.nodes[node].output);
+      if (d < 0) continue;  // hoisted
+      if (d == rows_dim(g.nodes[node])) {
+        if (R.chunk_len() % 128 != 0) ok = false;
+      } else if (!(g.nodes[node].kind != "attn_pv" && d == 0) && !(g.nodes[node].kind == "attn_pv" && d == 1)) {
+        ok = false;  // keys or head-dim chunking: use the generic masked path
+      }
+    }
+    if (!ok) continue;
+    for (int node : {i, sm, pv}) e->causal_fast[node] = 1;
+  }
+  for (int i = 0; i < S; ++i) e->chain_rows_dim[i] = rows_dim(g.nodes[i]);
+  *out = e.release();
+  return AC_OK;
+}
+
+void ac_exec_free(ac_exec* e) { delete e; }
+
+ac_status ac_exec_set_profiling(ac_exec* e, int32_t on) {
+  if (!e) return set_error(AC_ERR_ARG, "ac_exec_set_profiling: NULL exec");
+  e->profiling = on != 0;
+  e->ev_node.clear();
+  return AC_OK;
+}
+
+ac_status ac_exec_kernel_times(const ac_exec* e, ac_kernel_time* out, int32_t cap, int32_t* n) {
+  if (!e || !n) return set_error(AC_ERR_ARG, "ac_exec_kernel_times: NULL argument");
+  const Graph& g = *e->g;
+  std::vector<int> order;
+  std::unordered_map<int, std::pair<double, int>> acc;
+  if (!e->ev_node.empty() && cudaEventSynchronize(e->ev_pool[2 * e->ev_node.size() - 1]) != cudaSuccess)
+    return set_error(AC_ERR_CUDA, "cudaEventSynchronize failed");
+  for (size_t k = 0; k < e->ev_node.size(); ++k) {
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, e->ev_pool[2 * k], e->ev_pool[2 * k + 1]) != cudaSuccess)
+      return set_error(AC_ERR_CUDA, "cudaEventElapsedTime failed");
+    const int node = e->ev_node[k];
+    if (!acc.count(node)) order.push_back(node);
+    acc[node].first += ms;
+    acc[node].second += 1;
+  }
+  *n = static_cast<int32_t>(order.size());
+  for (int32_t j = 0; j < cap && j < *n; ++j) {
+    const Node& nd = g.nodes[order[j]];
+    memset(&out[j], 0, sizeof(ac_kernel_time));
+    strncpy(out[j].node, nd.id.c_str(), sizeof(out[j].node) - 1);
+    strncpy(out[j].kind, nd.kind.c_str(), sizeof(out[j].kind) - 1);
+    out[j].ms = acc[order[j]].first;
+    out[j].launches = acc[order[j]].second;
+  }
+  return AC_OK;
+}
+
+ac_status ac_exec_stats(const ac_exec* e, ac_run_stats* out) {
+  if (!e || !out) return set_error(AC_ERR_ARG, "ac_exec_stats: NULL argument");
+  *out = e->stats;
+  return AC_OK;
+}
+
+ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_tensor* outputs, int32_t n_out,
+                 void* stream) {
+  if (!e) return set_error(AC_ERR_ARG, "ac_run: NULL exec");
+  const Graph& g = *e->g;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int T = static_cast<int>(g.tensors.size());
+  const int esz = dt_size(e->dt);
+  std::vector<View> full(T);
+  std::vector<char> bound(T, 0);
+  auto bind = [&](const ac_tensor& at) -> ac_status {
+    if (!at.tensor_id) return set_error(AC_ERR_BIND, "tensor without id");
+    auto it = g.tindex.find(at.tensor_id);
+    if (it == g.tindex.end()) return set_error(AC_ERR_BIND, std::string("unknown tensor id ") + at.tensor_id);
+    const int t = it->second;
+    const TensorMeta& tm = g.tensors[t];
+    if (!is_caller(g, t)) return set_error(AC_ERR_BIND, "tensor " + tm.id + " is not a graph input/weight/output");
+    if (at.dtype != static_cast<int>(tm.dtype)) return set_error(AC_ERR_BIND, "dtype mismatch for " + tm.id);
+    if (at.ndim != static_cast<int>(tm.shape.size())) return set_error(AC_ERR_BIND, "rank mismatch for " + tm.id);
+    auto st = tm.strides();
+    for (int d = 0; d < at.ndim; ++d) {
+      if (at.shape[d] != tm.shape[d]) return set_error(AC_ERR_BIND, "shape mismatch for " + tm.id);
+      if (at.stride[d] != st[d]) return set_error(AC_ERR_BIND, "non-dense strides for " + tm.id);
+    }
+    if (!at.data || (reinterpret_cast<uintptr_t>(at.data) & 15))
+      return set_error(AC_ERR_BIND, "data of " + tm.id + " must be a 16-byte aligned device pointer");
+    full[t] = full_view(tm, at.data);
+    bound[t] = 1;
+    return AC_OK;
+  };
+  for (int i = 0; i < n_in; ++i) {
+    ac_status st = bind(inputs[i]);
+    if (st != AC_OK) return st;
+  }
+  for (int i = 0; i < n_out; ++i) {
+    ac_status st = bind(outputs[i]);
+    if (st != AC_OK) return st;
+  }
+  for (int t = 0; t < T; ++t) {
+    if (is_caller(g, t)) {
+      if (!bound[t]) return set_error(AC_ERR_BIND, "graph tensor " + g.tensors[t].id + " not bound");
+    } else {
+      full[t] = full_view(g.tensors[t], e->ws + e->arena.slot[t].offset);
+    }
+  }
+  e->stats = ac_run_stats{};
+  e->ev_node.clear();
+  e->stats.workspace_high_water = e->arena.size;
+  e->stats.planned_peak = estimate(g, e->plan.regions, false).peak;
+  for (int t = 0; t < T; ++t)
+    if (g.is_input[t] || g.is_output[t]) e->stats.caller_bytes += g.tensors[t].bytes();
+
+  const int S = static_cast<int>(g.nodes.size());
+  int i = 0;
+  while (i < S) {
+    const Node& n = g.nodes[i];
+    if (n.source()) {
+      ++i;
+      continue;
+    }
+    const int r = e->region_of[i];
+    if (r < 0 || e->plan.regions[r].n <= 1) {
+      NodeCtx cx;
+      cx.fast = e->causal_fast[i] != 0;
+      ac_status st = launch_node(e, i, full, cx, s);
+      if (st != AC_OK) return st;
+      ++i;
+      continue;
+    }
+    const Region& R = e->plan.regions[r];
+    for (int h : R.hoisted) {
+      NodeCtx cx;
+      cx.fast = e->causal_fast[h] != 0;
+      ac_status st = launch_node(e, h, full, cx, s);
+      if (st != AC_OK) return st;
+    }
+    const int64_t L = R.chunk_len();
+    const int64_t c0 = chunk_begin(e->rank, R.n, e->world);
+    const int64_t c1 = chunk_begin(e->rank + 1, R.n, e->world);
+    std::set<int> hs(R.hoisted.begin(), R.hoisted.end());
+    std::set<int> ycs;
+    for (auto& y : R.yc) ycs.insert(y.first);
+    std::vector<char> produced(T, 0);
+    for (int j = R.start; j <= R.end; ++j) produced[g.nodes[j].output] = 1;
+    for (int64_t c = c0; c < c1; ++c) {
+      const int64_t off = c * L;
+      const int64_t len = std::min(L, R.extent - off);
+      if (len <= 0) break;
+      std::vector<View> V = full;
+      for (auto& fd : R.dims) {
+        const int t = fd.first, d = fd.second;
+        if (produced[t] && !ycs.count(t)) {
+          // interior flow tensor: the chunk scratch, dense for chunk length L
+          TensorMeta sm = g.tensors[t];
+          sm.shape[d] = L;
+          V[t] = narrow(full_view(sm, e->ws + e->arena.slot[t].offset), d, 0, len, esz);
+        } else {
+          V[t] = narrow(full[t], d, off, len, esz);
+        }
+      }
+      for (int j = R.start; j <= R.end; ++j) {
+        if (hs.count(j)) continue;
+        const Node& nj = g.nodes[j];
+        // consumers taking a region input whole keep the full view
+        std::vector<View> VV;
+        const std::vector<View>* use = &V;
+        auto res_dims = [&]() {
+          std::vector<std::vector<int64_t>> in;
+          for (int t : nj.inputs) in.push_back(g.tensors[t].shape);
+          return op_propagate(nj.kind, nj, in, g.tensors[nj.output].shape, R.dim_of(nj.output));
+        }();
+        for (size_t q = 0; q < nj.inputs.size(); ++q) {
+          const int t = nj.inputs[q];
+          if (res_dims[q] < 0 && !produced[t] && R.dim_of(t) >= 0) {
+            if (use == &V) {
+              VV = V;
+              use = &VV;
+            }
+            VV[t] = full[t];
+          }
+        }
+        NodeCtx cx;
+        cx.fast = e->causal_fast[j] != 0;
+        const int d = R.dim_of(nj.output);
+        if (d >= 0 && d == e->chain_rows_dim[j]) cx.row_off = off;
+        ac_status st = launch_node(e, j, *use, cx, s);
+        if (st != AC_OK) return st;
+      }
+      e->stats.chunks_run += 1;
+    }
+    if (e->world > 1) {
+      for (auto& y : R.yc) {
+        ac_status st = comm_gather_slabs(e->comm, full[y.first].p, g.tensors[y.first].shape, y.second, esz,
+                                         R.extent, L, R.n, s);
+        if (st != AC_OK) return st;
+      }
+    }
+    i = R.end + 1;
+  }
+  return cuda_status(cudaGetLastError(), "ac_run");
+}
+
+}  // extern "C"

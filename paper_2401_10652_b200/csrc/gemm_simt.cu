@@ -72,8 +72,10 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(const GemmProblem p) {
       if (bias) x += ep.bias_along_m ? bias[m] : bias[n];
       x = act_apply(ep.act, x);
       const int64_t o = ob + static_cast<int64_t>(n) * ep.out_sn;
-      if (gate) x *= gate[o];
-      if (res) x += res[o];
+      if (gate) x *= gate[b1 * ep.gate_sb1 + b2 * ep.gate_sb2 + static_cast<int64_t>(m) * ep.gate_sm +
+                          static_cast<int64_t>(n) * ep.gate_sn];
+      if (res) x += res[b1 * ep.res_sb1 + b2 * ep.res_sb2 + static_cast<int64_t>(m) * ep.res_sm +
+                        static_cast<int64_t>(n) * ep.res_sn];
       if (ep.causal && static_cast<int64_t>(n) + ep.col_off > ep.row_off + m) x = -CUDART_INF_F;
       out[o] = x;
     }

@@ -34,6 +34,8 @@ constexpr int MAX_MT = 2048;
 struct alignas(64) GemmArgs {
   CUtensorMap ta;
   CUtensorMap tb;
+  CUtensorMap tout;  // output map for the TMA-store epilogue (tma_store = 1)
+  int tma_store;
   Epilogue ep;
   int M, N, K, B1, B2;
   int a_b1, a_b2, b_b1, b_b2;
@@ -42,16 +44,24 @@ struct alignas(64) GemmArgs {
   int MT, NT;
   int tiles_per_batch_dense;
   int total_tiles_dense;
+  int vec;  // 1: 8-wide vectorised epilogue (16-byte aux loads / stores) is legal
 };
+
+// epilogue staging: per epilogue warp a [32 rows][PITCH] fp32 slab; PITCH = 68
+// keeps rows 16-byte aligned (float4 row writes are conflict-free per phase)
+constexpr int PITCH = 68;
+constexpr int EPI_BYTES = 4 * 32 * PITCH * 4;
 
 template <int BN>
 struct Cfg {
-  static constexpr int STAGES = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
+  static constexpr int STAGES = BN >= 256 ? 3 : (BN >= 128 ? 5 : 7);
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int SW = BN >= 64 ? 64 : 32;  // epilogue slab width (columns)
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
-  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * (A_BYTES + B_BYTES) + 256 /*barriers*/ +
+  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * (A_BYTES + B_BYTES) + EPI_BYTES + 256 /*barriers*/ +
                               (MAX_MT + 1) * 4;
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
 __device__ __forceinline__ void decode_tile(const GemmArgs& a, const int* prefix, int tpb, int t,
@@ -88,7 +98,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  float* sEpi = reinterpret_cast<float*>(sB + C::STAGES * C::B_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES + EPI_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -203,32 +214,139 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
-    const int row = quarter * 32 + lane;
+    // Each warp owns TMEM lanes (= tile rows) 32*quarter .. +31.  Per slab of SW
+    // columns: tcgen05.ld (thread = row) -> fp32 staging in smem -> read back
+    // transposed (lane = column pair) so that aux loads and output stores are
+    // coalesced along n.
+    const int quarter = warp & 3;
+    float* stage = sEpi + quarter * 32 * PITCH;
+    constexpr int SW = C::SW;
     int acc = 0;
+    int sbuf = 0;
     uint32_t aphase = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       int b1, b2, mt, nt, kbn;
       decode_tile(a, prefix, tpb, t, b1, b2, mt, nt, kbn);
       ptx::mbar_wait(&tfull[acc], aphase);
       ptx::tc_fence_after();
-      const int m = mt * BM + row;
+      const int m0 = mt * BM + quarter * 32;
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c * 32, r);
-        ptx::tmem_ld_wait();
-        float v[32];
+      for (int c = 0; c < BN / SW; ++c) {
+        const int n0 = nt * BN + c * SW;
+        if constexpr (SW == 64) {
+          if (a.tma_store) {
+            // lean path (no aux tensors): scale (+ causal) in registers, bf16 pack,
+            // 128B-swizzled staging, one TMA tensor store per warp and slab
+            uint32_t r[32], r2[32];
+            ptx::tmem_ld32(tbase + c * SW, r);
+            ptx::tmem_ld32(tbase + c * SW + 32, r2);
+            ptx::tmem_ld_wait();
+            if (c == BN / SW - 1) {
+              ptx::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            }
+            const float sc = a.ep.scale;
+            const long long lim = a.ep.causal ? (a.ep.row_off + (m0 + lane) - a.ep.col_off - n0) : (1ll << 40);
+            uint32_t pk[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if (nt * BN + c * 32 < a.N)
-          epilogue_row32<__nv_bfloat16>(a.ep, a.M, a.N, b1, b2, m, nt * BN + c * 32, v);
+            for (int j = 0; j < 16; ++j) {
+              float x0 = __uint_as_float(r[2 * j]) * sc, x1 = __uint_as_float(r[2 * j + 1]) * sc;
+              float y0 = __uint_as_float(r2[2 * j]) * sc, y1 = __uint_as_float(r2[2 * j + 1]) * sc;
+              if (2 * j > lim) x0 = -CUDART_INF_F;
+              if (2 * j + 1 > lim) x1 = -CUDART_INF_F;
+              if (32 + 2 * j > lim) y0 = -CUDART_INF_F;
+              if (33 + 2 * j > lim) y1 = -CUDART_INF_F;
+              __nv_bfloat162 hx = __floats2bfloat162_rn(x0, x1), hy = __floats2bfloat162_rn(y0, y1);
+              pk[j] = *reinterpret_cast<uint32_t*>(&hx);
+              pk[16 + j] = *reinterpret_cast<uint32_t*>(&hy);
+            }
+            uint8_t* sb = reinterpret_cast<uint8_t*>(sEpi) + quarter * 8192 + sbuf * 4096;
+            if (lane == 0) ptx::bulk_wait_read<1>();  // the store issued two slabs ago has read its buffer
+            __syncwarp();
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+              const uint32_t addr = ptx::smem_u32(sb + lane * 128 + ((ch ^ (lane & 7)) * 16));
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[4 * ch]),
+                           "r"(pk[4 * ch + 1]), "r"(pk[4 * ch + 2]), "r"(pk[4 * ch + 3])
+                           : "memory");
+            }
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              ptx::tma_store_4d(&a.tout, sb, n0, m0, b1, b2);
+              ptx::bulk_commit();
+            }
+            sbuf ^= 1;
+            continue;
+          }
+        }
+        uint32_t r[32];
+        ptx::tmem_ld32(tbase + c * SW, r);
+        if constexpr (SW == 64) {
+          uint32_t r2[32];
+          ptx::tmem_ld32(tbase + c * SW + 32, r2);
+          ptx::tmem_ld_wait();
+          float4* dst = reinterpret_cast<float4*>(stage + lane * PITCH);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                 __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+            dst[8 + j] = make_float4(__uint_as_float(r2[4 * j]), __uint_as_float(r2[4 * j + 1]),
+                                     __uint_as_float(r2[4 * j + 2]), __uint_as_float(r2[4 * j + 3]));
+          }
+        } else {
+          ptx::tmem_ld_wait();
+          float4* dst = reinterpret_cast<float4*>(stage + lane * PITCH);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                 __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+        }
+        if (c == BN / SW - 1) {  // accumulator fully read: hand TMEM back to the MMA warp
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+        }
+        __syncwarp();
+        if (n0 < a.N) {
+          const int rows = min(32, a.M - m0);
+          if (a.vec) {
+            // 8 consecutive columns per lane: SW/8 lanes cover a row segment, 32/(SW/8) rows per pass
+            constexpr int LPR = SW / 8;
+            constexpr int RPI = 32 / LPR;
+            const int sub = lane / LPR, seg = lane % LPR;
+            const int n = n0 + seg * 8;
+#pragma unroll 2
+            for (int rr = 0; rr < 32; rr += RPI) {
+              const int r = rr + sub;
+              if (r < rows && n < a.N) {
+                const float4* src = reinterpret_cast<const float4*>(stage + r * PITCH + seg * 8);
+                const float4 u0 = src[0], u1 = src[1];
+                float v8[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+                epilogue8(a.ep, b1, b2, m0 + r, n, v8);
+              }
+            }
+          } else {
+#pragma unroll 4
+            for (int rr = 0; rr < rows; ++rr) {
+              if constexpr (SW == 64) {
+                const float2 v = reinterpret_cast<const float2*>(stage + rr * PITCH)[lane];
+                epilogue_pair<__nv_bfloat16>(a.ep, a.N, b1, b2, m0 + rr, n0 + 2 * lane, v.x, v.y);
+              } else {
+                const float v = stage[rr * PITCH + lane];
+                epilogue_one<__nv_bfloat16>(a.ep, a.N, b1, b2, m0 + rr, n0 + lane, v);
+              }
+            }
+          }
+        }
+        __syncwarp();
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
+    if (lane == 0) ptx::bulk_wait_read<0>();  // staging buffers must outlive the TMA stores' reads
+    __syncwarp();
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -297,6 +415,36 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   a.MT = (p.M + BM - 1) / BM;
   a.NT = (p.N + BN - 1) / BN;
   if (a.MT > MAX_MT) return cudaErrorInvalidValue;
+  {
+    // vectorised epilogue: n-contiguous 16-byte aligned output / aux rows, N % 8 == 0
+    const Epilogue& e = p.ep;
+    auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+    auto m8 = [](int64_t v) { return v % 8 == 0; };
+    bool v = p.N % 8 == 0 && e.out_sn == 1 && al(e.out) && m8(e.out_sm) && m8(e.out_sb1) && m8(e.out_sb2);
+    if (e.add) v = v && e.add_sn == 1 && al(e.add) && m8(e.add_sm) && m8(e.add_sb1) && m8(e.add_sb2);
+    if (e.gate) v = v && e.gate_sn == 1 && al(e.gate) && m8(e.gate_sm) && m8(e.gate_sb1) && m8(e.gate_sb2);
+    if (e.res) v = v && e.res_sn == 1 && al(e.res) && m8(e.res_sm) && m8(e.res_sb1) && m8(e.res_sb2);
+    if (e.bias && !e.bias_along_m) v = v && al(e.bias);
+    a.vec = v ? 1 : 0;
+    // TMA-store epilogue: no aux tensors, identity activation, 64-column slabs
+    if (BN >= 64 && v && !e.add && !e.bias && !e.gate && !e.res && e.act == ACT_NONE) {
+      EncodeTiledFn enc = get_encode();
+      cuuint64_t dims[4] = {static_cast<cuuint64_t>(p.N), static_cast<cuuint64_t>(p.M),
+                            static_cast<cuuint64_t>(p.B1), static_cast<cuuint64_t>(p.B2)};
+      const int64_t big = ((e.out_sm * p.M + 8) * 2 + 15) / 16 * 16;
+      cuuint64_t strides[3] = {static_cast<cuuint64_t>(e.out_sm * 2),
+                               static_cast<cuuint64_t>(p.B1 > 1 ? e.out_sb1 * 2 : big),
+                               static_cast<cuuint64_t>(p.B2 > 1 ? e.out_sb2 * 2 : big)};
+      cuuint32_t box[4] = {64, 32, 1, 1};
+      cuuint32_t es[4] = {1, 1, 1, 1};
+      bool ok = enc && strides[0] > 0 && strides[1] > 0 && strides[2] > 0;
+      if (ok)
+        ok = enc(&a.tout, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, e.out, dims, strides, box, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+      a.tma_store = ok ? 1 : 0;
+    }
+  }
   a.tiles_per_batch_dense = a.MT * a.NT;
   a.total_tiles_dense = a.tiles_per_batch_dense * p.B1 * p.B2;
   int grid = a.total_tiles_dense;

@@ -37,7 +37,9 @@ struct Epilogue {
   const void* add = nullptr;
   int64_t add_sb1 = 0, add_sb2 = 0, add_sm = 0, add_sn = 0;
   const void* gate = nullptr;
-  const void* res = nullptr;   // gate and res use the output strides
+  int64_t gate_sb1 = 0, gate_sb2 = 0, gate_sm = 0, gate_sn = 1;
+  const void* res = nullptr;
+  int64_t res_sb1 = 0, res_sb2 = 0, res_sm = 0, res_sn = 1;
   void* out = nullptr;
   int64_t out_sb1 = 0, out_sb2 = 0, out_sm = 0, out_sn = 1;
 };
@@ -65,11 +67,14 @@ cudaError_t gemm_f32(const GemmProblem& p, cudaStream_t s);
 cudaError_t layernorm(const void* x, const void* gamma, const void* beta, void* y, int64_t rows,
                       int C, float eps, int dtype, cudaStream_t s);
 // Row softmax: rows of `ncols` values with row stride `ld` (elements).  With
-// causal, row r (global row row_off + r) reads columns <= row and writes
-// columns [0, ceil128(row+1)) with zeros above the diagonal (PV reads whole
-// 128-key blocks); otherwise the full row.
-cudaError_t softmax_rows(const void* s_in, void* p_out, int64_t rows, int64_t ncols, int64_t ld,
-                         int causal, int64_t row_off, int dtype, cudaStream_t s);
+// causal, row r is query row R = row_off + (r % group) (rows of several heads
+// are stacked); it reads columns <= R and writes columns [0, ceil128(R+1)) with
+// zeros above the diagonal (the causal PV reads whole 128-key blocks);
+// otherwise the full row.  Input row r lives at (r / group) * gstride + (r % group) * ld
+// (group = 0: r * ld); output rows likewise with gstrideo / ldo.
+cudaError_t softmax_rows(const void* s_in, void* p_out, int64_t rows, int64_t ncols, int64_t ld, int64_t gstride,
+                         int64_t ldo, int64_t gstrideo, int causal, int64_t row_off, int64_t group, int dtype,
+                         cudaStream_t s);
 
 int num_sms();
 

@@ -52,7 +52,7 @@ def layernorm(x, gamma, beta, y, eps=1e-5, stream=None):
     return y
 
 
-def softmax(s, p, rows, ncols, ld, causal=0, row_off=0, stream=None):
-    check(lib().ac_kernel_softmax(_ptr(s), _ptr(p), rows, ncols, ld, causal, row_off, _DT[s.dtype],
+def softmax(s, p, rows, ncols, ld, causal=0, row_off=0, group=0, stream=None):
+    check(lib().ac_kernel_softmax(_ptr(s), _ptr(p), rows, ncols, ld, causal, row_off, group, _DT[s.dtype],
                                   _stream(stream)))
     return p

@@ -1,0 +1,119 @@
+"""GPU path (ac_run through the C ABI) vs the fp64 oracle, element by element.
+Tolerances (north_star): fp32 path 1e-4, bf16 path 2e-2, normwise max relative
+error per output tensor (R18)."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import blocks, executor, memory, select, workloads  # noqa: E402
+
+TOL = {"f32": 1e-4, "bf16": 2e-2}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+
+
+def _gu():
+    import gpu_util
+    return gpu_util
+
+
+def _check_all_plans(og, plans, seed=0):
+    gu = _gu()
+    from paper_2401_10652_b200 import api
+    cg = gu.c_graph(og)
+    vals, dev = gu.make_values(og, seed)
+    ref = executor.run(og, vals)
+    base, _ = gu.run(cg, gu.empty_plan(cg), og, dev)
+    dt = og.tensors[og.outputs[0]].dtype
+    for o in og.outputs:
+        assert gu.rel_err(base[o], ref[o]) < TOL[dt], ("unchunked", o)
+    for txt in plans:
+        plan = api.plan_parse(cg, txt) if isinstance(txt, str) else txt
+        got, ex = gu.run(cg, plan, og, dev)
+        torch.cuda.synchronize()
+        for o in og.outputs:
+            err = gu.rel_err(got[o], ref[o])
+            assert err < TOL[dt], (txt, o, err)
+            # chunked == unchunked bitwise: tiles never depend on the chunking
+            assert torch.equal(got[o], base[o]), (txt, o)
+        st = ex.stats()
+        assert st.launches > 0 and st.chunks_run >= 1
+    return cg
+
+
+def test_tiny_fp32_forced_chunk32():
+    og = workloads.config("tiny")
+    _check_all_plans(og, [
+        "autochunk-plan 1\nregion s=scores e=pv n=8 dims=0\n",      # attention region, chunk_len 32
+        "autochunk-plan 1\nregion s=proj_q e=ffn2 n=8 dims=0\n",    # whole block on rows
+        "autochunk-plan 1\nregion s=scores e=pv n=32 dims=0\n",     # reading R1 alternative (len 8)
+        "autochunk-plan 1\nregion s=scores e=pv n=2 dims=1\n",      # heads
+        "autochunk-plan 1\nregion s=ln2 e=ffn2 n=7 dims=0\n",       # ragged FFN chunks
+    ])
+
+
+def test_tiny_fp32_ac_plan_best_effort():
+    gu = _gu()
+    from paper_2401_10652_b200 import api
+    og = workloads.config("tiny")
+    cg = gu.c_graph(og)
+    plan = api.ac_plan(cg, int(0.2 * memory.profile(og).peak_bytes))
+    assert not plan.feasible
+    _check_all_plans(og, [plan])
+
+
+@pytest.mark.parametrize("N,causal", [(1024, True), (1024 + 96, True), (768, False)])
+def test_small_gpt_bf16(N, causal):
+    og = workloads.block("transformer", N, 256, 4, 1024, causal, "bf16", name="gpt_small")
+    _check_all_plans(og, [
+        "autochunk-plan 1\nregion s=scores e=pv n=4 dims=0\n",
+        "autochunk-plan 1\nregion s=scores e=pv n=3 dims=0\n",      # ragged chunks (unaligned: masked path)
+        "autochunk-plan 1\nregion s=proj_q e=ffn2 n=4 dims=0\n",
+    ])
+
+
+def test_small_unet_bf16():
+    og = workloads.block("attn_only", 512, 640, 10, 0, False, "bf16", name="unet_small")
+    _check_all_plans(og, ["autochunk-plan 1\nregion s=scores e=pv n=4 dims=0\n",
+                          "autochunk-plan 1\nregion s=scores e=pv n=8 dims=0\n"])
+
+
+def test_small_af_bf16():
+    og = workloads.tri_attn_pair(64, 128, 4, 32, "bf16", name="af_small")
+    plan = select.select(og, int(0.2 * memory.profile(og).peak_bytes))
+    gu = _gu()
+    from paper_2401_10652_b200 import api
+    cg = gu.c_graph(og)
+    p = api.ac_plan(cg, int(0.2 * memory.profile(og).peak_bytes))
+    assert p.num_regions == len(plan.regions)
+    _check_all_plans(og, [p,
+                          "autochunk-plan 1\nregion s=row_scores e=row_pv n=4 dims=0\n"
+                          "region s=col_scores e=col_pv n=4 dims=1\n"])
+
+
+def test_gpt_full_size_sampled_rows():
+    """BASELINE configs[1] at full size, the plan ac_plan picks at 20 %, in the
+    launch configuration bench.py times; sampled rows vs the oracle."""
+    gu = _gu()
+    from paper_2401_10652_b200 import api
+    og = workloads.config("gpt")
+    cg = gu.c_graph(og)
+    budget = int(0.2 * memory.profile(og).peak_bytes)
+    plan = api.ac_plan(cg, budget)
+    vals, dev = gu.make_values(og, 0)
+    got, ex = gu.run(cg, plan, og, dev)
+    torch.cuda.synchronize()
+    rows = blocks.sample_rows(16384, 2048, 48)
+    ref = blocks.transformer_rows(og, vals, rows)
+    err = gu.rel_err(got["y"][torch.from_numpy(rows).cuda()], ref["y"])
+    assert err < 2e-2, err
+    st = ex.stats()
+    assert st.planned_peak < budget
+    # arena high-water + caller-held tensors live at the peak == planned peak (no fragmentation)
+    assert st.workspace_high_water + 2 * 16384 * 1024 * 2 >= st.planned_peak

@@ -201,3 +201,17 @@ def test_document_round_trip(name):
     assert graph.serialize(g2) == doc
     graph.infer_shapes(g2)
     assert graph.serialize(g2) == doc
+
+
+def test_sampled_rows_equal_full_run():
+    """oracle.blocks.transformer_rows (full-size parity helper) == executor.run rows."""
+    from oracle import blocks
+    for causal, kind in ((True, "transformer"), (False, "attn_only")):
+        g = workloads.block(kind, 64, 32, 4, 64, causal, "f64")
+        v = _values(g, 9)
+        env = executor.run(g, v, keep_all=True)
+        rows = blocks.sample_rows(64, 16, 8)
+        got = blocks.transformer_rows(g, v, rows)
+        out = "y" if kind == "transformer" else "x1"
+        np.testing.assert_allclose(got[out], env[out][rows], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(got["o"], env["o"][rows], rtol=0, atol=1e-12)
