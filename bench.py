@@ -108,20 +108,38 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ workload
+# BASELINE.json configs as ac_graph_block descriptors (kind, N, d, h, f, causal, dtype)
+BLOCKS = {
+    "tiny": ("transformer", 256, 64, 2, 256, False, "f32"),
+    "gpt": ("transformer", 16384, 1024, 16, 4096, True, "bf16"),
+    "vit": ("transformer", 65536, 1024, 16, 4096, False, "bf16"),
+    "af": ("tri_attn_pair", 1024, 128, 4, 32, False, "bf16"),
+    "unet": ("attn_only", 16384, 640, 10, 0, False, "bf16"),
+}
+
+
+def c_graph(name):
+    """The workload graph, built by libautochunk (ac_graph_block), and its document."""
+    from paper_2401_10652_b200 import api, graphdoc
+    kind, N, d, h, f, causal, dt = BLOCKS[name]
+    cg = api.graph_block(kind, N, d, h, f, causal, dt, name=name)
+    return cg, graphdoc.parse(cg.serialize())
+
+
 def oracle_graph(name):
     from oracle import workloads
     return workloads.config(name)
 
 
-def tokens_per_step(name, og):
-    x = og.tensors[og.inputs[0]]
-    return x.shape[0] * x.shape[1] if name == "af" else x.shape[0]
+def tokens_per_step(name, doc):
+    shp = doc.tensors[doc.inputs[0]][1]
+    return shp[0] * shp[1] if name == "af" else shp[0]
 
 
-def device_inputs(og, torch):
+def device_inputs(doc, torch):
     import numpy as np
     import synth
-    samples = synth.make_inputs(og.input_specs(), 0)
+    samples = synth.make_inputs(doc.input_specs(), 0)
     dev = {}
     for t, s in samples.items():
         if s.dtype == "bf16":
@@ -132,49 +150,48 @@ def device_inputs(og, torch):
 
 
 # ------------------------------------------------------------------ roofline bookkeeping
-def algorithmic(og, plan_regions, node_id, peaks):
-    """Algorithmic work of one node summed over one step, per DESIGN.md §7:
-    bytes that must cross HBM (reads of inputs + writes of outputs, only the
-    causal lower triangle for S/P) for HBM-bound kinds, FLOPs for GEMMs."""
-    n = next(x for x in og.nodes if x.id == node_id)
-    T = og.tensors
-    esz = T[n.output].esize
-    if n.kind == "softmax":
-        sh = T[n.inputs[0]].shape
-        causal = any(x.kind == "attn_scores" and x.output == n.inputs[0] and x.attrs.get("causal", 0)
-                     for x in og.nodes)
-        if causal:          # rows i read i+1 scores, write up to the 128-block end
-            h, N, M = sh
-            rd = h * N * (N + 1) // 2
-            wr = h * sum(min(M, (i // 128 + 1) * 128) for i in range(N))
-            return "hbm", (rd + wr) * esz
-        el = 1
-        for s in sh:
-            el *= s
-        return "hbm", 2 * el * esz
-    if n.kind in ("attn_scores", "attn_pv", "tri_scores", "tri_pv"):
-        from oracle import ops
-        fl = ops.flops(n.kind, n.attrs, [T[t].shape for t in n.inputs], T[n.output].shape)
-        if n.kind == "attn_scores" and n.attrs.get("causal", 0) or n.kind == "attn_pv" and any(
-                x.kind == "attn_scores" and x.attrs.get("causal", 0) for x in og.nodes):
-            N = T[n.output].shape[1] if n.kind == "attn_scores" else T[n.output].shape[0]
-            fl = fl * (N + 1) // (2 * N)
-        # S / P are N x N-sized: memory-bound at dh <= 80 (AI ~ 63 flop/B < ridge 251)
-        if n.kind in ("attn_scores", "tri_scores"):
-            by = T[n.output].bytes
-        else:
-            by = T[n.inputs[0]].bytes
-        if n.kind in ("attn_scores", "attn_pv") and "causal" in str(n.attrs) or (
-                n.kind == "attn_pv" and any(x.kind == "attn_scores" and x.attrs.get("causal", 0) for x in og.nodes)):
-            by = by // 2
-        return "hbm", by
-    if n.kind == "linear":
-        from oracle import ops
-        fl = ops.flops(n.kind, n.attrs, [T[t].shape for t in n.inputs], T[n.output].shape)
-        return "tensor", fl
-    if n.kind == "layernorm":
-        return "hbm", 2 * T[n.output].bytes
-    return "hbm", T[n.output].bytes
+def _prod(xs):
+    p = 1
+    for x in xs:
+        p *= x
+    return p
+
+
+def algorithmic(doc, node_id):
+    """Algorithmic work of one node summed over one step.
+    HBM-bound kinds: the bytes the operation must move — inputs read once,
+    outputs written once, and for a causal score matrix only its lower triangle
+    (j <= i).  GEMM-shaped linears: 2*M*N*K FLOPs."""
+    nid, kind, ins, out, attrs = doc.node(node_id)
+    B = doc.nbytes
+    causal_scores = {o for (_, k, _, o, a) in doc.nodes if k == "attn_scores" and a.get("causal") == "1"}
+    causal_p = {o for (_, k, i, o, _) in doc.nodes if k == "softmax" and i[0] in causal_scores}
+    if kind == "linear":
+        a_shape = doc.tensors[ins[0]][1]
+        kin = int(attrs["kin"])
+        R, K = _prod(a_shape[: len(a_shape) - kin]), _prod(a_shape[len(a_shape) - kin:])
+        O = doc.tensors[ins[1]][1][0]
+        return "tensor", 2 * R * K * O
+    if kind == "attn_scores":
+        h, N, M = doc.tensors[out][1]
+        esz = B(out) // (h * N * M)
+        s = h * N * (N + 1) // 2 * esz if out in causal_scores else B(out)
+        return "hbm", s + B(ins[0]) + B(ins[1])
+    if kind == "softmax":
+        if out in causal_p:
+            h, N, M = doc.tensors[out][1]
+            esz = B(out) // (h * N * M)
+            return "hbm", 2 * h * N * (N + 1) // 2 * esz
+        return "hbm", B(ins[0]) + B(out)
+    if kind == "attn_pv":
+        p = B(ins[0])
+        if ins[0] in causal_p:
+            h, N, M = doc.tensors[ins[0]][1]
+            p = h * N * (N + 1) // 2 * (p // (h * N * M))
+        return "hbm", p + B(ins[1]) + B(out)
+    if kind in ("tri_scores", "tri_pv", "layernorm"):
+        return "hbm", sum(B(t) for t in ins) + B(out)
+    return "hbm", B(out)
 
 
 def cpu_baseline(name, og, samples, budget_s=20.0):
@@ -256,7 +273,6 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from oracle import graph as og_graph
     from paper_2401_10652_b200 import api
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -270,8 +286,7 @@ def main():
         if world > 1:
             dist.barrier()
 
-    og = oracle_graph(args.config)
-    cg = api.graph_parse(og_graph.serialize(og))
+    cg, doc = c_graph(args.config)
     prof0, _ = api.estimate_memory(cg)
     budget = int(args.budget_frac * prof0.peak_bytes)
     if args.plan:
@@ -286,12 +301,12 @@ def main():
         uid = [api.Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = api.Comm(uid[0], rank, world, local)
-    samples, dev = device_inputs(og, torch)
+    samples, dev = device_inputs(doc, torch)
     s = torch.cuda.current_stream()
     ws = torch.empty(max(plan.workspace_bytes(), 16), dtype=torch.uint8, device="cuda")
     TD = {"bf16": torch.bfloat16, "f32": torch.float32}
-    outs = {o: torch.empty(og.tensors[o].shape, dtype=TD[og.tensors[o].dtype], device="cuda") for o in og.outputs}
-    ins = {t: dev[t] for t in og.inputs + og.weights}
+    outs = {o: torch.empty(doc.tensors[o][1], dtype=TD[doc.tensors[o][0]], device="cuda") for o in doc.outputs}
+    ins = {t: dev[t] for t in doc.order}
     ex = api.Exec(plan, ws, comm)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
 
@@ -328,7 +343,7 @@ def main():
         return tot, kt
 
     peaks, peak_src = load_peaks()
-    units = tokens_per_step(args.config, og)
+    units = tokens_per_step(args.config, doc)
     with ClockSampler(local) as clk:
         tot_ms, kt = timed(ex, ins, outs, args.steps, args.warmup, profile=True)
     st = ex.stats()
@@ -343,7 +358,7 @@ def main():
         total_k = sum(v[1] for v in kt.values())
         dom = max(kt.items(), key=lambda kv: kv[1][1])
         node, (kind, ms, nl) = dom
-        bound, work = algorithmic(og, None, node, peaks)
+        bound, work = algorithmic(doc, node)
         per_launch_ms = ms / nl
         launches_per_step = nl / args.steps
         work_per_launch = work / launches_per_step
@@ -389,8 +404,8 @@ def main():
     # end to end: pinned host input -> device, ac_run, output -> pinned host
     e2e = None
     if not args.no_e2e and not args.profile:
-        xin = og.inputs[0]
-        yout = og.outputs[0]
+        xin = doc.inputs[0]
+        yout = doc.outputs[0]
         hx = torch.empty_like(dev[xin], device="cpu").pin_memory()
         hx.copy_(dev[xin].cpu())
         hy = torch.empty_like(outs[yout], device="cpu").pin_memory()
@@ -408,16 +423,16 @@ def main():
     cpu = None
     if not args.no_cpu and not args.profile:
         try:
-            cpu = cpu_baseline(args.config, og, samples)
+            cpu = cpu_baseline(args.config, oracle_graph(args.config), samples)
         except Exception as e:  # pragma: no cover
             cpu = {"error": str(e)}
     plan_txt = plan.serialize().splitlines()
     regions = [ln.split(" flow=")[0] for ln in plan_txt if ln.startswith("region")]
-    caller = sum(og.tensors[t].bytes for t in og.inputs + og.outputs)
+    caller = sum(doc.nbytes(t) for t in doc.inputs + doc.outputs)
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "bf16" if og.tensors[og.inputs[0]].dtype == "bf16" else "f32",
+        "vs_baseline": None, "dtype": doc.tensors[doc.inputs[0]][0],
         "data": "synthetic (seeded PCG64, DESIGN.md §4)",
         "config": {"workload": WORKLOADS[args.config], "plan": regions, "parallelism": f"chunk-split x{world}",
                    "l2": "flushed between timed steps (256 MiB write)"},

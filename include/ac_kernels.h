@@ -41,6 +41,7 @@ typedef struct ac_gemm_desc {
   const void* res;
   void* out; int64_t out_sb1, out_sb2, out_sm, out_sn;
   int32_t bn;                /* tcgen05 N tile (32/64/128/256), 0 = auto */
+  int32_t ksplit;            /* split K over a cluster of this many CTAs (BN = 64 only), <= 1 = off */
 } ac_gemm_desc;
 
 ac_status ac_kernel_gemm(const ac_gemm_desc* d, void* stream);

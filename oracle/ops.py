@@ -267,7 +267,8 @@ def shape(kind: str, attrs: dict, ins) -> tuple:
             raise ValueError("tri_scores rank")
         I, J, H, c = q
         if attrs.get("ending", 0):
-            if k[1:] != (J, H, c) or b != (H, k[0], I):
+            # bias given as bT[h, i, k] = b_ki (the projection writes it transposed)
+            if k[1:] != (J, H, c) or b != (H, I, k[0]):
                 raise ValueError("tri_scores(ending) shape mismatch")
             return (J, H, I, k[0])
         if (k[0], k[2], k[3]) != (I, H, c) or b != (H, J, k[1]):
@@ -397,7 +398,7 @@ def propagate(kind: str, attrs: dict, ins, out, d: int):
         return [[1, NC], [0, 0], [NC, 1]][d]
     if kind == "tri_scores":
         if attrs.get("ending", 0):
-            return [[1, 1, NC], [2, 2, 0], [0, NC, 2], [NC, 0, 1]][d]
+            return [[1, 1, NC], [2, 2, 0], [0, NC, 1], [NC, 0, 2]][d]
         return [[0, 0, NC], [2, 2, 0], [1, NC, 1], [NC, 1, 2]][d]
     if kind == "tri_pv":
         if attrs.get("ending", 0):
@@ -478,7 +479,7 @@ def evaluate(kind: str, attrs: dict, vals, ctx=None) -> np.ndarray:
         if attrs.get("ending", 0):
             Q = np.transpose(q, (1, 2, 0, 3))   # [J,H,I,c]
             Kk = np.transpose(k, (1, 2, 0, 3))  # [J,H,K,c]
-            return _bdot(Q, Kk) * sc + np.transpose(b, (0, 2, 1))[None]
+            return _bdot(Q, Kk) * sc + b[None]            # b = bT[h, i, k] = b_ki
         Q = np.transpose(q, (0, 2, 1, 3))       # [I,H,J,c]
         Kk = np.transpose(k, (0, 2, 1, 3))      # [I,H,K,c]
         return _bdot(Q, Kk) * sc + b[None]

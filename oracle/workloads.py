@@ -70,8 +70,10 @@ def _tri_attention(B: Builder, z: str, pre: str, N: int, cz: int, H: int, c: int
                    out: str, eps=1e-5):
     zn, b, q, k, vt, g = (pre + s for s in ("zn", "bias", "q", "k", "vt", "g"))
     B.op("layernorm", [z, pre + "ln_g", pre + "ln_b"], zn, nid=pre + "ln", naxes=1, eps=eps)
+    # ending node: the bias is used as b_ki (Alg. 14), written transposed (swap) so the
+    # scores epilogue reads it contiguously along the key index
     B.op("linear", [zn, pre + "wb"], b, nid=pre + "proj_b", kin=1, out=[H], act="none", trans=1,
-         swap=0, bias=0, res=0)
+         swap=int(ending), bias=0, res=0)
     B.op("linear", [zn, pre + "wq"], q, nid=pre + "proj_q", kin=1, out=[H, c], act="none", trans=0,
          swap=0, bias=0, res=0)
     B.op("linear", [zn, pre + "wk"], k, nid=pre + "proj_k", kin=1, out=[H, c], act="none", trans=0,

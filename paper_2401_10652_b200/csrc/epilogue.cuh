@@ -23,9 +23,30 @@ __device__ __forceinline__ float from_f<float>(float v) { return v; }
 template <>
 __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
+// Branch-free erf for the GELU epilogue: erfc(|z|) = t exp(-z^2 + P(t)),
+// t = 1 / (1 + |z|/2) (Chebyshev fit, Numerical Recipes 6.2; fractional error of
+// erfc < 1.2e-7), so |erf error| < 1.2e-7 everywhere — below fp32 GELU rounding
+// at the bf16 / fp32 outputs.  One MUFU reciprocal + one MUFU exp, no branches
+// (CUDA's erff has a data-dependent branch that serialises the epilogue).
+__device__ __forceinline__ float erf_fast(float z) {
+  const float a = fabsf(z);
+  const float t = __frcp_rn(fmaf(0.5f, a, 1.f));
+  float p = fmaf(t, 0.17087277f, -0.82215223f);
+  p = fmaf(t, p, 1.48851587f);
+  p = fmaf(t, p, -1.13520398f);
+  p = fmaf(t, p, 0.27886807f);
+  p = fmaf(t, p, -0.18628806f);
+  p = fmaf(t, p, 0.09678418f);
+  p = fmaf(t, p, 0.37409196f);
+  p = fmaf(t, p, 1.00002368f);
+  p = fmaf(t, p, -1.26551223f);
+  const float erfc = t * __expf(fmaf(-a, a, p));
+  return copysignf(1.f - erfc, z);
+}
+
 __device__ __forceinline__ float act_apply(int act, float v) {
-  if (act == ACT_GELU) return 0.5f * v * (1.f + erff(v * 0.70710678118654752f));
-  if (act == ACT_SIGMOID) return 1.f / (1.f + expf(-v));
+  if (act == ACT_GELU) return 0.5f * v * (1.f + erf_fast(v * 0.70710678118654752f));
+  if (act == ACT_SIGMOID) return __frcp_rn(1.f + __expf(-v));
   if (act == ACT_RELU) return fmaxf(v, 0.f);
   return v;
 }
@@ -134,6 +155,71 @@ __device__ __forceinline__ void epilogue8(const Epilogue& ep, int b1, int b2, in
   }
   if (ep.causal) {
     const int64_t lim = ep.row_off + m - ep.col_off - n;  // column n+i masked when i > lim
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i > lim) x[i] = -CUDART_INF_F;
+  }
+  uint4 w;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(x[2 * i], x[2 * i + 1]);
+  const int64_t o = static_cast<int64_t>(b1) * ep.out_sb1 + static_cast<int64_t>(b2) * ep.out_sb2 +
+                    static_cast<int64_t>(m) * ep.out_sm + n;
+  *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + o) = w;
+}
+
+// Operands of epilogue8p loaded ahead of time (several rows in flight).
+struct Aux8 {
+  uint4 add, gate, res;
+  float bias_m;
+};
+
+__device__ __forceinline__ void load_aux8(const Epilogue& ep, int b1, int b2, int m, int n, Aux8& x) {
+  if (ep.add)
+    x.add = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(ep.add) + static_cast<int64_t>(b1) * ep.add_sb1 +
+                                            static_cast<int64_t>(b2) * ep.add_sb2 + static_cast<int64_t>(m) * ep.add_sm + n);
+  if (ep.gate)
+    x.gate = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(ep.gate) +
+                                             static_cast<int64_t>(b1) * ep.gate_sb1 + static_cast<int64_t>(b2) * ep.gate_sb2 +
+                                             static_cast<int64_t>(m) * ep.gate_sm + n);
+  if (ep.res)
+    x.res = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(ep.res) + static_cast<int64_t>(b1) * ep.res_sb1 +
+                                            static_cast<int64_t>(b2) * ep.res_sb2 + static_cast<int64_t>(m) * ep.res_sm + n);
+  if (ep.bias && ep.bias_along_m) x.bias_m = __bfloat162float(static_cast<const __nv_bfloat16*>(ep.bias)[m]);
+}
+
+// epilogue8 with the aux operands preloaded; bias_n = the column bias of this
+// lane's 8 columns (loaded once per slab).  Same operation order as epi_value.
+__device__ __forceinline__ void epilogue8p(const Epilogue& ep, int b1, int b2, int m, int n, float (&x)[8],
+                                           const Aux8& aux, const float (&bias_n)[8]) {
+  float a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] *= ep.scale;
+  if (ep.add) {
+    bf16x8_to_f(aux.add, a);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] += a[i];
+  }
+  if (ep.bias) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] += ep.bias_along_m ? aux.bias_m : bias_n[i];
+  }
+  if (ep.act != ACT_NONE) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = act_apply(ep.act, x[i]);
+  }
+  if (ep.gate) {
+    bf16x8_to_f(aux.gate, a);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] *= a[i];
+  }
+  if (ep.res) {
+    bf16x8_to_f(aux.res, a);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] += a[i];
+  }
+  if (ep.causal) {
+    const int64_t lim = ep.row_off + m - ep.col_off - n;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
       if (i > lim) x[i] = -CUDART_INF_F;

@@ -383,6 +383,9 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         p.causal_k = 1;
         p.k_row_off = cx.row_off;
       }
+      // few (head x 128-row) tiles per chunk and a long key loop: split K over a
+      // 4-CTA cluster (depends on the key count only, so chunking never changes it)
+      if (p.N <= 64 && p.K >= 2048) p.ksplit = 4;
     } else if (k == "tri_scores") {
       const View &q = in(0), &kk = in(1), &b = in(2);
       const bool end = n.ai("ending") != 0;
@@ -406,7 +409,7 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         p.N = static_cast<int>(kk.sh[0]);
         p.A.p = q.p; p.A.srow = q.st[0]; p.A.sb1 = q.st[1]; p.A.sb2 = q.st[2];
         p.B.p = kk.p; p.B.srow = kk.st[0]; p.B.sb1 = kk.st[1]; p.B.sb2 = kk.st[2];
-        ep.add_sm = b.st[2]; ep.add_sn = b.st[1];
+        ep.add_sm = b.st[1]; ep.add_sn = b.st[2];  // bT[h, i, k]
       }
       p.A.use_b1 = p.A.use_b2 = p.B.use_b1 = p.B.use_b2 = 1;
     } else if (k == "tri_pv") {

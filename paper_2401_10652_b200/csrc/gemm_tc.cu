@@ -28,7 +28,8 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int NUM_THREADS = 192;
+constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, alternating 64-column slabs
+constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr int MAX_MT = 2048;
 
 struct alignas(64) GemmArgs {
@@ -45,16 +46,17 @@ struct alignas(64) GemmArgs {
   int tiles_per_batch_dense;
   int total_tiles_dense;
   int vec;  // 1: 8-wide vectorised epilogue (16-byte aux loads / stores) is legal
+  int ks;   // cluster split-K factor (1 = none)
 };
 
 // epilogue staging: per epilogue warp a [32 rows][PITCH] fp32 slab; PITCH = 68
 // keeps rows 16-byte aligned (float4 row writes are conflict-free per phase)
 constexpr int PITCH = 68;
-constexpr int EPI_BYTES = 4 * 32 * PITCH * 4;
+constexpr int EPI_BYTES = EPI_WARPS * 32 * PITCH * 4;
 
 template <int BN>
 struct Cfg {
-  static constexpr int STAGES = BN >= 256 ? 3 : (BN >= 128 ? 5 : 7);
+  static constexpr int STAGES = BN >= 256 ? 3 : (BN >= 128 ? 4 : 5);
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int SW = BN >= 64 ? 64 : 32;  // epilogue slab width (columns)
@@ -104,10 +106,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* part_full = full + 16;   // split-K: leader waits for the other ranks' partials
+  uint64_t* part_empty = full + 20;  // split-K: ranks wait for the leader to have read them
   int* prefix = reinterpret_cast<int*>(full + 32);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int ks = a.ks;
+  const uint32_t crank = ks > 1 ? ptx::cluster_rank() : 0;
+  const int cid = blockIdx.x / ks, ncl = gridDim.x / ks;
 
   // --- tile table for causal QK^T: live n-tiles per m-tile, prefix-summed
   int tpb = a.tiles_per_batch_dense;
@@ -150,13 +157,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], 4);
+      ptx::mbar_init(&tempty[s], EPI_WARPS);
+    }
+    for (int q = 0; q < 4; ++q) {
+      ptx::mbar_init(&part_full[q], 32 * (ks > 1 ? ks - 1 : 1));
+      ptx::mbar_init(&part_empty[q], 32);
     }
     ptx::fence_barrier_init();
   }
   if (warp == 1) ptx::tmem_alloc<C::TMEM_COLS>(tmem_holder);
   ptx::tc_fence_before();
   __syncthreads();
+  if (ks > 1) ptx::cluster_sync();  // remote barriers initialised before any remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
@@ -165,12 +177,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = cid; t < total; t += ncl) {
         int b1, b2, mt, nt, kbn;
         decode_tile(a, prefix, tpb, t, b1, b2, mt, nt, kbn);
         const int ac2 = a.a_b1 ? b1 : 0, ac3 = a.a_b2 ? b2 : 0;
         const int bc2 = a.b_b1 ? b1 : 0, bc3 = a.b_b2 ? b2 : 0;
-        for (int kb = 0; kb < kbn; ++kb) {
+        const int klo = kbn * static_cast<int>(crank) / ks, khi = kbn * (static_cast<int>(crank) + 1) / ks;
+        for (int kb = klo; kb < khi; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
           ptx::tma_load_4d(sA + stage * C::A_BYTES, &a.ta, &full[stage], kb * BK, mt * BM, ac2, ac3);
@@ -186,13 +199,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     uint32_t phase = 0;
     int acc = 0;
     uint32_t aphase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int t = cid; t < total; t += ncl) {
       int b1, b2, mt, nt, kbn;
       decode_tile(a, prefix, tpb, t, b1, b2, mt, nt, kbn);
       ptx::mbar_wait(&tempty[acc], aphase ^ 1);
       ptx::tc_fence_after();
       const uint32_t d = tmem_base + acc * BN;
-      for (int kb = 0; kb < kbn; ++kb) {
+      const int klo = kbn * static_cast<int>(crank) / ks, khi = kbn * (static_cast<int>(crank) + 1) / ks;
+      for (int kb = klo; kb < khi; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
         if (lane == 0) {
@@ -201,7 +215,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             ptx::mma_bf16(d, ptx::sdesc_sw128(sa + k * 32), ptx::sdesc_sw128(sb + k * 32), IDESC,
-                          (kb | k) != 0);
+                          (kb != klo || k != 0) ? 1u : 0u);
           }
           ptx::mma_commit(&empty[stage]);  // slot free once these MMAs have read smem
         }
@@ -218,21 +232,103 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     // columns: tcgen05.ld (thread = row) -> fp32 staging in smem -> read back
     // transposed (lane = column pair) so that aux loads and output stores are
     // coalesced along n.
-    const int quarter = warp & 3;
-    float* stage = sEpi + quarter * 32 * PITCH;
+    const int ew = warp - 2;       // epilogue warp 0..7
+    const int quarter = warp & 3;  // TMEM lane quarter (hardware: warp w reads lanes 32*(w%4)..)
+    const int half = ew >> 2;      // which alternate slabs this warp handles
+    float* stage = sEpi + ew * 32 * PITCH;
     constexpr int SW = C::SW;
+    constexpr int NSLAB = BN / SW;
     int acc = 0;
     int sbuf = 0;
     uint32_t aphase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    uint32_t pf_phase = 0, pe_phase = 0;  // split-K barrier phases
+    for (int t = cid; t < total; t += ncl) {
       int b1, b2, mt, nt, kbn;
       decode_tile(a, prefix, tpb, t, b1, b2, mt, nt, kbn);
       ptx::mbar_wait(&tfull[acc], aphase);
       ptx::tc_fence_after();
+      if (half >= NSLAB) {  // narrow tile: nothing for this warp, but keep the tempty count
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+        continue;
+      }
       const int m0 = mt * BM + quarter * 32;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
+      if constexpr (BN == 64) {
+        if (ks > 1) {
+          // ---- split-K: every rank stages its fp32 partial; the leader (rank 0)
+          // sums rank 0 + 1 + ... + ks-1 through DSMEM and runs the epilogue
+          const int klo = kbn * static_cast<int>(crank) / ks, khi = kbn * (static_cast<int>(crank) + 1) / ks;
+          if (crank != 0) ptx::mbar_wait_cluster(&part_empty[quarter], pe_phase ^ 1);
+          uint32_t r[32], r2[32];
+          if (khi > klo) {
+            ptx::tmem_ld32(tbase, r);
+            ptx::tmem_ld32(tbase + 32, r2);
+            ptx::tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[j] = r2[j] = 0u;
+          }
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+          float4* dst = reinterpret_cast<float4*>(stage + lane * PITCH);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                 __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+            dst[8 + j] = make_float4(__uint_as_float(r2[4 * j]), __uint_as_float(r2[4 * j + 1]),
+                                     __uint_as_float(r2[4 * j + 2]), __uint_as_float(r2[4 * j + 3]));
+          }
+          if (crank != 0) {
+            // every lane publishes its own row (release at cluster scope)
+            ptx::mbar_arrive_remote(ptx::map_remote(ptx::smem_u32(&part_full[quarter]), 0));
+            pe_phase ^= 1;
+          } else {
+            ptx::mbar_wait_cluster(&part_full[quarter], pf_phase);
+            pf_phase ^= 1;
+            __syncwarp();
+            const int rows = min(32, a.M - m0);
+            const int sub = lane / 8, seg = lane % 8;
+            const int n = nt * BN + seg * 8;
+            const bool col_ok = n < a.N;
+            float bias_n[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (a.ep.bias && !a.ep.bias_along_m && col_ok)
+              bf16x8_to_f(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.ep.bias) + n), bias_n);
+#pragma unroll 2
+            for (int it = 0; it < 8; ++it) {
+              const int rr = it * 4 + sub;
+              if (rr < rows && col_ok) {
+                Aux8 aux;
+                load_aux8(a.ep, b1, b2, m0 + rr, n, aux);
+                const float* own = stage + rr * PITCH + seg * 8;
+                const float4 u0 = reinterpret_cast<const float4*>(own)[0];
+                const float4 u1 = reinterpret_cast<const float4*>(own)[1];
+                float v8[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+                const uint32_t la = ptx::smem_u32(own);
+                for (int q = 1; q < ks; ++q) {
+                  const uint32_t ra = ptx::map_remote(la, static_cast<uint32_t>(q));
+                  const float4 w0 = ptx::ld_remote_f4(ra), w1 = ptx::ld_remote_f4(ra + 16);
+                  v8[0] += w0.x; v8[1] += w0.y; v8[2] += w0.z; v8[3] += w0.w;
+                  v8[4] += w1.x; v8[5] += w1.y; v8[6] += w1.z; v8[7] += w1.w;
+                }
+                epilogue8p(a.ep, b1, b2, m0 + rr, n, v8, aux, bias_n);
+              }
+            }
+            // let the other ranks overwrite their staging (each lane releases its reads)
+            for (int q = 1; q < ks; ++q)
+              ptx::mbar_arrive_remote(ptx::map_remote(ptx::smem_u32(&part_empty[quarter]), static_cast<uint32_t>(q)));
+          }
+          __syncwarp();
+          if (++acc == 2) { acc = 0; aphase ^= 1; }
+          continue;
+        }
+      }
 #pragma unroll 1
-      for (int c = 0; c < BN / SW; ++c) {
+      for (int c = half; c < NSLAB; c += 2) {
+        const bool last = c + 2 >= NSLAB;
         const int n0 = nt * BN + c * SW;
         if constexpr (SW == 64) {
           if (a.tma_store) {
@@ -242,7 +338,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
             ptx::tmem_ld32(tbase + c * SW, r);
             ptx::tmem_ld32(tbase + c * SW + 32, r2);
             ptx::tmem_ld_wait();
-            if (c == BN / SW - 1) {
+            if (last) {
               ptx::tc_fence_before();
               __syncwarp();
               if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
@@ -262,7 +358,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
               pk[j] = *reinterpret_cast<uint32_t*>(&hx);
               pk[16 + j] = *reinterpret_cast<uint32_t*>(&hy);
             }
-            uint8_t* sb = reinterpret_cast<uint8_t*>(sEpi) + quarter * 8192 + sbuf * 4096;
+            uint8_t* sb = reinterpret_cast<uint8_t*>(sEpi) + ew * 8192 + sbuf * 4096;
             if (lane == 0) ptx::bulk_wait_read<1>();  // the store issued two slabs ago has read its buffer
             __syncwarp();
 #pragma unroll
@@ -304,7 +400,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
             dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
                                  __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
         }
-        if (c == BN / SW - 1) {  // accumulator fully read: hand TMEM back to the MMA warp
+        if (last) {  // this warp's share of the accumulator is read: release TMEM
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
@@ -316,16 +412,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
             // 8 consecutive columns per lane: SW/8 lanes cover a row segment, 32/(SW/8) rows per pass
             constexpr int LPR = SW / 8;
             constexpr int RPI = 32 / LPR;
+            constexpr int NIT = 32 / RPI;     // row passes per slab
+            constexpr int BATCH = 4;          // rows whose aux loads are in flight together
             const int sub = lane / LPR, seg = lane % LPR;
             const int n = n0 + seg * 8;
-#pragma unroll 2
-            for (int rr = 0; rr < 32; rr += RPI) {
-              const int r = rr + sub;
-              if (r < rows && n < a.N) {
-                const float4* src = reinterpret_cast<const float4*>(stage + r * PITCH + seg * 8);
-                const float4 u0 = src[0], u1 = src[1];
-                float v8[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
-                epilogue8(a.ep, b1, b2, m0 + r, n, v8);
+            const bool col_ok = n < a.N;
+            float bias_n[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (a.ep.bias && !a.ep.bias_along_m && col_ok)
+              bf16x8_to_f(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.ep.bias) + n), bias_n);
+#pragma unroll
+            for (int it0 = 0; it0 < NIT; it0 += BATCH) {
+              Aux8 aux[BATCH];
+#pragma unroll
+              for (int q = 0; q < BATCH; ++q) {
+                const int r = (it0 + q) * RPI + sub;
+                if (r < rows && col_ok) load_aux8(a.ep, b1, b2, m0 + r, n, aux[q]);
+              }
+#pragma unroll
+              for (int q = 0; q < BATCH; ++q) {
+                const int r = (it0 + q) * RPI + sub;
+                if (r < rows && col_ok) {
+                  const float4* src = reinterpret_cast<const float4*>(stage + r * PITCH + seg * 8);
+                  const float4 u0 = src[0], u1 = src[1];
+                  float v8[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+                  epilogue8p(a.ep, b1, b2, m0 + r, n, v8, aux[q], bias_n);
+                }
               }
             }
           } else {
@@ -350,6 +461,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (ks > 1) ptx::cluster_sync();  // the leader has finished reading our staging
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
@@ -414,7 +526,7 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   a.causal_tiles = p.causal_tiles; a.causal_k = p.causal_k; a.k_row_off = p.k_row_off;
   a.MT = (p.M + BM - 1) / BM;
   a.NT = (p.N + BN - 1) / BN;
-  if (a.MT > MAX_MT) return cudaErrorInvalidValue;
+  if (p.causal_tiles && a.MT > MAX_MT) return cudaErrorInvalidValue;  // prefix table size
   {
     // vectorised epilogue: n-contiguous 16-byte aligned output / aux rows, N % 8 == 0
     const Epilogue& e = p.ep;
@@ -447,12 +559,30 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   }
   a.tiles_per_batch_dense = a.MT * a.NT;
   a.total_tiles_dense = a.tiles_per_batch_dense * p.B1 * p.B2;
-  int grid = a.total_tiles_dense;
+  a.ks = (BN == 64 && a.vec && p.ksplit > 1) ? (p.ksplit > 8 ? 8 : p.ksplit) : 1;
+  if (a.ks > 1) a.tma_store = 0;
   const int sms = num_sms();
-  if (grid > sms) grid = sms;
-  if (grid < 1) grid = 1;
-  gemm_tc_kernel<BN><<<grid, NUM_THREADS, C::SMEM, s>>>(a);
-  return cudaGetLastError();
+  int grid = a.total_tiles_dense * a.ks;
+  const int cap = (sms / a.ks) * a.ks;
+  if (grid > cap) grid = cap;
+  if (grid < a.ks) grid = a.ks;
+  if (a.ks == 1) {
+    gemm_tc_kernel<BN><<<grid, NUM_THREADS, C::SMEM, s>>>(a);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute lattr[1];
+  lattr[0].id = cudaLaunchAttributeClusterDimension;
+  lattr[0].val.clusterDim.x = a.ks;
+  lattr[0].val.clusterDim.y = 1;
+  lattr[0].val.clusterDim.z = 1;
+  cfg.attrs = lattr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN>, a);
 }
 
 }  // namespace

@@ -241,7 +241,8 @@ Shape op_shape(const std::string& k, const Node& n, const std::vector<Shape>& in
     if (q.size() != 4 || kk.size() != 4 || b.size() != 3) fail("tri_scores rank");
     int64_t I = q[0], J = q[1], H = q[2], c = q[3];
     if (n.ai("ending")) {
-      if (kk[1] != J || kk[2] != H || kk[3] != c || b != Shape{H, kk[0], I}) fail("tri_scores(ending) shape mismatch");
+      // bias given transposed: bT[h, i, k] = b_ki (Alg. 14)
+      if (kk[1] != J || kk[2] != H || kk[3] != c || b != Shape{H, I, kk[0]}) fail("tri_scores(ending) shape mismatch");
       return {J, H, I, kk[0]};
     }
     if (kk[0] != I || kk[2] != H || kk[3] != c || b != Shape{H, J, kk[1]}) fail("tri_scores shape mismatch");
@@ -346,7 +347,7 @@ std::vector<int> op_propagate(const std::string& k, const Node& n, const std::ve
   }
   if (k == "tri_scores") {
     static const int e0[4][3] = {{0, 0, NC}, {2, 2, 0}, {1, NC, 1}, {NC, 1, 2}};
-    static const int e1[4][3] = {{1, 1, NC}, {2, 2, 0}, {0, NC, 2}, {NC, 0, 1}};
+    static const int e1[4][3] = {{1, 1, NC}, {2, 2, 0}, {0, NC, 1}, {NC, 0, 2}};
     const int(*t)[3] = n.ai("ending") ? e1 : e0;
     return {t[d][0], t[d][1], t[d][2]};
   }
@@ -762,7 +763,8 @@ void tri_weights(GB& b, const std::string& pre, int64_t cz, int64_t H, int64_t c
 void tri_attention(GB& b, const std::string& z, const std::string& pre, int64_t cz, int64_t H, int64_t c, int ending,
                    const std::string& out, double eps) {
   b.op(pre + "ln", "layernorm", {z, pre + "ln_g", pre + "ln_b"}, pre + "zn", {{"naxes", GB::I(1)}, {"eps", GB::F(eps)}});
-  b.linear(pre + "proj_b", {pre + "zn", pre + "wb"}, pre + "bias", 1, {H}, "none", 1, 0, 0, 0);
+  // ending node: bias written transposed (bT[h,i,k] = b_ki) so it is k-contiguous
+  b.linear(pre + "proj_b", {pre + "zn", pre + "wb"}, pre + "bias", 1, {H}, "none", 1, ending, 0, 0);
   b.linear(pre + "proj_q", {pre + "zn", pre + "wq"}, pre + "q", 1, {H, c}, "none", 0, 0, 0, 0);
   b.linear(pre + "proj_k", {pre + "zn", pre + "wk"}, pre + "k", 1, {H, c}, "none", 0, 0, 0, 0);
   b.linear(pre + "proj_v", {pre + "zn", pre + "wv"}, pre + "vt", 1, {H, c}, "none", 1, ending, 0, 0);

@@ -54,6 +54,11 @@ struct GemmProblem {
   int causal_tiles = 0;  // skip (m,n) tiles entirely above the diagonal (QK^T)
   int causal_k = 0;      // K loop stops after the tile's last row (PV, keys = K)
   int64_t k_row_off = 0; // global row of m = 0 for causal_k
+  // split-K across a thread-block cluster (tcgen05 path, BN = 64): the KS CTAs of
+  // a cluster take contiguous K ranges of the same tile and the leader sums the
+  // fp32 partials through distributed shared memory in rank order (deterministic;
+  // the split depends only on the tile's K range, never on the chunking)
+  int ksplit = 1;
 };
 
 // bf16 x bf16 -> fp32 (TMEM) -> bf16, tcgen05 + TMA, sm_100a.  Returns a

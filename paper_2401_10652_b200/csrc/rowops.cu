@@ -181,21 +181,39 @@ __global__ void __launch_bounds__(SMX_THREADS) softmax_bulk_kernel(
   __shared__ float red[2][SMX_THREADS / 32];
   uint8_t* buf0 = sm + 128;
   const int tid = threadIdx.x;
-  auto row_geom = [&](int64_t r, int64_t& sof, int64_t& pof, int64_t& valid, int64_t& wend) {
-    sof = group > 0 ? (r / group) * gstride + (r % group) * ld : r * ld;
-    pof = group > 0 ? (r / group) * gstrideo + (r % group) * ldo : r * ldo;
-    valid = ncols;
-    wend = ncols;
-    if (causal) {
-      const int64_t R = row_off + (group > 0 ? r % group : r);
-      valid = R + 1 < ncols ? R + 1 : ncols;
-      const int64_t k = ((R >> 7) + 1) << 7;
-      wend = k < ncols ? k : ncols;
+  if (group <= 0) group = rows;
+  // row r = gq * group + gr, tracked incrementally (no 64-bit division per row)
+  struct Pos {
+    int64_t gq, gr;
+  };
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  const int64_t sq = stride / group, sr = stride % group;
+  auto advance = [&](Pos& p, int64_t times) {
+    for (int64_t t = 0; t < times; ++t) {
+      p.gq += sq;
+      p.gr += sr;
+      if (p.gr >= group) {
+        p.gr -= group;
+        p.gq += 1;
+      }
     }
   };
-  auto issue = [&](int64_t r, int b) {
-    int64_t sof, pof, valid, wend;
-    row_geom(r, sof, pof, valid, wend);
+  auto row_geom = [&](const Pos& p, int64_t& sof, int64_t& pof, int& valid, int& wend) {
+    sof = p.gq * gstride + p.gr * ld;
+    pof = p.gq * gstrideo + p.gr * ldo;
+    valid = static_cast<int>(ncols);
+    wend = static_cast<int>(ncols);
+    if (causal) {
+      const int64_t R = row_off + p.gr;
+      valid = static_cast<int>(R + 1 < ncols ? R + 1 : ncols);
+      const int64_t k = ((R >> 7) + 1) << 7;
+      wend = static_cast<int>(k < ncols ? k : ncols);
+    }
+  };
+  auto issue = [&](const Pos& pr, int b) {
+    int64_t sof, pof;
+    int valid, wend;
+    row_geom(pr, sof, pof, valid, wend);
     const uint32_t bytes = static_cast<uint32_t>(((valid * 2 + 15) / 16) * 16);
     const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[b]));
     const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(buf0 + b * cap_bytes));
@@ -210,13 +228,19 @@ __global__ void __launch_bounds__(SMX_THREADS) softmax_bulk_kernel(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int64_t first = blockIdx.x, stride = gridDim.x;
-  if (tid == 0)
-    for (int b = 0; b < SMX_NBUF - 1; ++b)
-      if (first + b * stride < rows) issue(first + b * stride, b);
+  Pos cur{first / group, first % group};
+  Pos ahead = cur;  // thread 0: the row NBUF-1 iterations ahead
+  if (tid == 0) {
+    Pos q = cur;
+    for (int b = 0; b < SMX_NBUF - 1; ++b) {
+      if (first + b * stride < rows) issue(q, b);
+      advance(q, 1);
+    }
+    ahead = q;
+  }
   constexpr float L2E = 1.4426950408889634f;
   int64_t j = 0;
-  for (int64_t r = first; r < rows; r += stride, ++j) {
+  for (int64_t r = first; r < rows; r += stride, ++j, advance(cur, 1)) {
     const int b = static_cast<int>(j % SMX_NBUF);
     const uint32_t par = static_cast<uint32_t>((j / SMX_NBUF) & 1);
     if (tid == 0) {
@@ -224,10 +248,12 @@ __global__ void __launch_bounds__(SMX_THREADS) softmax_bulk_kernel(
       // the buffer was read through the generic proxy last iteration; order those
       // reads before the async-proxy (TMA) write that refills it
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      if (rn < rows) issue(rn, static_cast<int>((j + SMX_NBUF - 1) % SMX_NBUF));
+      if (rn < rows) issue(ahead, static_cast<int>((j + SMX_NBUF - 1) % SMX_NBUF));
+      advance(ahead, 1);
     }
-    int64_t sof, pof, valid, wend;
-    row_geom(r, sof, pof, valid, wend);
+    int64_t sof, pof;
+    int valid, wend;
+    row_geom(cur, sof, pof, valid, wend);
     {
       const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[b]));
       asm volatile(
@@ -236,20 +262,25 @@ __global__ void __launch_bounds__(SMX_THREADS) softmax_bulk_kernel(
           : "memory");
     }
     const uint4* row = reinterpret_cast<const uint4*>(buf0 + b * cap_bytes);
-    const int64_t nv = (valid + 7) / 8;
+    const int nfull = valid >> 3, tail = valid & 7, nv = nfull + (tail ? 1 : 0);
     float mx = -CUDART_INF_F;
-    for (int64_t v = tid; v < nv; v += SMX_THREADS) {
-      float f[8];
-      Vec<__nv_bfloat16> q;
-      q.raw = row[v];
-      q.to_float(f);
-      if ((v + 1) * 8 <= valid) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) mx = fmaxf(mx, f[e]);
-      } else {
+    {
+      __nv_bfloat162 m2 = __float2bfloat162_rn(-CUDART_INF_F);
+      for (int v = tid; v < nfull; v += SMX_THREADS) {
+        const uint4 u = row[v];
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+        m2 = __hmax2(m2, __hmax2(__hmax2(h[0], h[1]), __hmax2(h[2], h[3])));
+      }
+      const float2 mf = __bfloat1622float2(m2);
+      mx = fmaxf(mf.x, mf.y);
+      if (tail && tid == (nfull % SMX_THREADS)) {
+        float f[8];
+        Vec<__nv_bfloat16> q;
+        q.raw = row[nfull];
+        q.to_float(f);
 #pragma unroll
         for (int e = 0; e < 8; ++e)
-          if (v * 8 + e < valid) mx = fmaxf(mx, f[e]);
+          if (e < tail) mx = fmaxf(mx, f[e]);
       }
     }
     mx = warp_max(mx);
@@ -259,20 +290,35 @@ __global__ void __launch_bounds__(SMX_THREADS) softmax_bulk_kernel(
 #pragma unroll
     for (int i = 1; i < SMX_THREADS / 32; ++i) mx = fmaxf(mx, red[0][i]);
     const float mxl = mx * L2E;
+    // pass 2: e = exp(s - m) once per element; the sum uses the fp32 e, the row
+    // buffer is overwritten in place with bf16(e) for the normalising pass
     float sum = 0.f;
-    for (int64_t v = tid; v < nv; v += SMX_THREADS) {
+    uint4* rowm = const_cast<uint4*>(row);
+    for (int v = tid; v < nfull; v += SMX_THREADS) {
       float f[8];
       Vec<__nv_bfloat16> q;
       q.raw = row[v];
       q.to_float(f);
-      if ((v + 1) * 8 <= valid) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) sum += ex2(fmaf(f[e], L2E, -mxl));
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if (v * 8 + e < valid) sum += ex2(fmaf(f[e], L2E, -mxl));
+      for (int e = 0; e < 8; ++e) {
+        f[e] = ex2(fmaf(f[e], L2E, -mxl));
+        sum += f[e];
       }
+      q.from_float(f);
+      rowm[v] = q.raw;
+    }
+    if (tail && tid == (nfull % SMX_THREADS)) {
+      float f[8];
+      Vec<__nv_bfloat16> q;
+      q.raw = row[nfull];
+      q.to_float(f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        f[e] = e < tail ? ex2(fmaf(f[e], L2E, -mxl)) : 0.f;
+        sum += f[e];
+      }
+      q.from_float(f);
+      rowm[nfull] = q.raw;
     }
     sum = warp_sum(sum);
     if ((tid & 31) == 0) red[1][tid >> 5] = sum;
@@ -282,22 +328,140 @@ __global__ void __launch_bounds__(SMX_THREADS) softmax_bulk_kernel(
     for (int i = 0; i < SMX_THREADS / 32; ++i) sum += red[1][i];
     const float inv = 1.f / sum;
     uint4* out = reinterpret_cast<uint4*>(p + pof);
-    const int64_t nw = (wend + 7) / 8;
-    for (int64_t v = tid; v < nw; v += SMX_THREADS) {
-      float f[8];
-      if (v < nv) {
+    const int nw = (wend + 7) >> 3;
+    for (int v = tid; v < nw; v += SMX_THREADS) {
+      uint4 w = make_uint4(0, 0, 0, 0);
+      if (v < nv) {  // e (bf16, zero beyond the valid prefix) * 1/l
+        float f[8];
         Vec<__nv_bfloat16> q;
         q.raw = row[v];
         q.to_float(f);
-      }
 #pragma unroll
-      for (int e = 0; e < 8; ++e) f[e] = (v * 8 + e < valid) ? ex2(fmaf(f[e], L2E, -mxl)) * inv : 0.f;
-      Vec<__nv_bfloat16> o;
-      o.from_float(f);
-      out[v] = o.raw;
+        for (int e = 0; e < 8; ++e) f[e] *= inv;
+        q.from_float(f);
+        w = q.raw;
+      }
+      out[v] = w;
     }
     __syncthreads();  // buffer b and red[] free for reuse
   }
+}
+
+// ---------------------------------------------------------------- long rows (> 32768 columns)
+// Streaming two-read softmax: pass 1 keeps a per-thread online (max, sum) while
+// streaming the row with several 16-byte loads in flight, the block combines
+// them; pass 2 re-reads the row (mostly L2 hits: the rows in flight fit in L2)
+// and writes p.  Rows stay out of registers and shared memory, so any length works.
+constexpr int STR_THREADS = 512;
+constexpr int STR_UNROLL = 4;
+
+__global__ void __launch_bounds__(STR_THREADS) softmax_stream_kernel(
+    const __nv_bfloat16* __restrict__ s, __nv_bfloat16* __restrict__ p, int64_t rows, int64_t ncols, int64_t ld,
+    int causal, int64_t row_off, int64_t group, int64_t gstride, int64_t ldo, int64_t gstrideo) {
+  __shared__ float red_m[STR_THREADS / 32], red_l[STR_THREADS / 32];
+  const int tid = threadIdx.x;
+  if (group <= 0) group = rows;
+  constexpr float L2E = 1.4426950408889634f;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int64_t gq = r / group, gr = r % group;
+    const uint4* row = reinterpret_cast<const uint4*>(s + gq * gstride + gr * ld);
+    uint4* out = reinterpret_cast<uint4*>(p + gq * gstrideo + gr * ldo);
+    int64_t valid = ncols, wend = ncols;
+    if (causal) {
+      const int64_t R = row_off + gr;
+      valid = R + 1 < ncols ? R + 1 : ncols;
+      const int64_t k = ((R >> 7) + 1) << 7;
+      wend = k < ncols ? k : ncols;
+    }
+    const int nv = static_cast<int>((valid + 7) >> 3);
+    float m = -CUDART_INF_F, l = 0.f;
+    for (int v0 = tid; v0 < nv; v0 += STR_THREADS * STR_UNROLL) {
+      uint4 u[STR_UNROLL];
+#pragma unroll
+      for (int k = 0; k < STR_UNROLL; ++k) {
+        const int v = v0 + k * STR_THREADS;
+        if (v < nv) u[k] = row[v];
+      }
+#pragma unroll
+      for (int k = 0; k < STR_UNROLL; ++k) {
+        const int v = v0 + k * STR_THREADS;
+        if (v >= nv) break;
+        float f[8];
+        Vec<__nv_bfloat16> q;
+        q.raw = u[k];
+        q.to_float(f);
+        float vm = -CUDART_INF_F;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (static_cast<int64_t>(v) * 8 + e >= valid) f[e] = -CUDART_INF_F;
+          vm = fmaxf(vm, f[e]);
+        }
+        if (vm > m) {
+          l *= ex2((m - vm) * L2E);
+          m = vm;
+        }
+        const float ml = m * L2E;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) l += ex2(fmaf(f[e], L2E, -ml));
+      }
+    }
+    // combine (m, l) across the block
+    float mw = warp_max(m);
+    float lw = l * (m == -CUDART_INF_F ? 0.f : ex2((m - mw) * L2E));
+    lw = warp_sum(lw);
+    if ((tid & 31) == 0) {
+      red_m[tid >> 5] = mw;
+      red_l[tid >> 5] = lw;
+    }
+    __syncthreads();
+    float M = red_m[0];
+#pragma unroll
+    for (int i = 1; i < STR_THREADS / 32; ++i) M = fmaxf(M, red_m[i]);
+    float Lsum = 0.f;
+#pragma unroll
+    for (int i = 0; i < STR_THREADS / 32; ++i)
+      Lsum += red_m[i] == -CUDART_INF_F ? 0.f : red_l[i] * ex2((red_m[i] - M) * L2E);
+    const float inv = 1.f / Lsum, ML = M * L2E;
+    const int nw = static_cast<int>((wend + 7) >> 3);
+    for (int v0 = tid; v0 < nw; v0 += STR_THREADS * STR_UNROLL) {
+      uint4 u[STR_UNROLL];
+#pragma unroll
+      for (int k = 0; k < STR_UNROLL; ++k) {
+        const int v = v0 + k * STR_THREADS;
+        if (v < nv) u[k] = row[v];
+      }
+#pragma unroll
+      for (int k = 0; k < STR_UNROLL; ++k) {
+        const int v = v0 + k * STR_THREADS;
+        if (v >= nw) break;
+        uint4 w = make_uint4(0, 0, 0, 0);
+        if (v < nv) {
+          float f[8];
+          Vec<__nv_bfloat16> q;
+          q.raw = u[k];
+          q.to_float(f);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            f[e] = static_cast<int64_t>(v) * 8 + e < valid ? ex2(fmaf(f[e], L2E, -ML)) * inv : 0.f;
+          q.from_float(f);
+          w = q.raw;
+        }
+        out[v] = w;
+      }
+    }
+    __syncthreads();  // red_* reused by the next row
+  }
+}
+
+cudaError_t launch_softmax_stream(const void* s, void* p, int64_t rows, int64_t ncols, int64_t ld, int causal,
+                                  int64_t row_off, int64_t group, int64_t gstride, int64_t ldo, int64_t gstrideo,
+                                  cudaStream_t st) {
+  int64_t grid = static_cast<int64_t>(num_sms()) * 4;
+  if (grid > rows) grid = rows;
+  softmax_stream_kernel<<<static_cast<unsigned>(grid), STR_THREADS, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(s), static_cast<__nv_bfloat16*>(p), rows, ncols, ld, causal, row_off, group,
+      gstride, ldo, gstrideo);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_softmax_bulk(const void* s, void* p, int64_t rows, int64_t ncols, int64_t ld, int causal,
@@ -330,6 +494,8 @@ cudaError_t softmax_dispatch(const void* s, void* p, int64_t rows, int64_t ncols
   const int64_t vecs = (ncols + VN - 1) / VN;
   if (sizeof(T) == 2 && ncols > 2048 && ncols <= 32768 && (reinterpret_cast<uintptr_t>(s) & 15) == 0)
     return launch_softmax_bulk(s, p, rows, ncols, ld, causal, row_off, group, gstride, ldo, gstrideo, st);
+  if (sizeof(T) == 2 && ncols > 32768)
+    return launch_softmax_stream(s, p, rows, ncols, ld, causal, row_off, group, gstride, ldo, gstrideo, st);
   if (vecs <= 32 * 1) return launch_softmax<T, 32, 1>(s, p, rows, ncols, ld, causal, row_off, group, gstride, ldo, gstrideo, st);
   if (vecs <= 32 * 2) return launch_softmax<T, 32, 2>(s, p, rows, ncols, ld, causal, row_off, group, gstride, ldo, gstrideo, st);
   if (vecs <= 32 * 4) return launch_softmax<T, 32, 4>(s, p, rows, ncols, ld, causal, row_off, group, gstride, ldo, gstrideo, st);

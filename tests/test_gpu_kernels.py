@@ -89,6 +89,30 @@ def test_gemm_tc_pv_causal_k(K):
     assert _rel(o, ref) < 1e-2
 
 
+@pytest.mark.parametrize("ks,causal", [(2, 0), (4, 0), (4, 1), (8, 1)])
+def test_gemm_tc_cluster_split_k(K, ks, causal):
+    """PV with split-K over a thread-block cluster (DSMEM reduction): equal to the
+    fp32 reference, deterministic run to run, and the causal K loop respected."""
+    torch.manual_seed(7)
+    N, h, dh, rows, row_off = 4096, 3, 64, 640, (1024 if causal else 0)
+    p = torch.rand(h, rows, N, device="cuda")
+    if causal:
+        i = torch.arange(rows, device="cuda")[:, None] + row_off
+        j = torch.arange(N, device="cuda")[None, :]
+        p = torch.where((j <= i)[None], p, torch.zeros_like(p))
+    p = p.bfloat16()
+    vt = torch.randn(h, dh, N, device="cuda").bfloat16()
+    outs = []
+    for _ in range(2):
+        o = torch.empty(rows, h, dh, device="cuda", dtype=torch.bfloat16)
+        K.gemm(p, N, vt, N, o, rows, dh, N, B1=h, a_sb=(rows * N, 0), a_use=(1, 0), b_sb=(dh * N, 0),
+               b_use=(1, 0), out_s=(dh, 0, h * dh, 1), causal_k=causal, k_row_off=row_off, ksplit=ks)
+        outs.append(o)
+    ref = torch.einsum("hij,hcj->ihc", p.float(), vt.float())
+    assert _rel(outs[0], ref) < 1e-2
+    assert torch.equal(outs[0], outs[1])
+
+
 def test_gemm_f32_path(K):
     torch.manual_seed(4)
     M, N, Kd = 100, 70, 33
