@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    ap.add_argument("--sweep", action="store_true", help="also sweep the attention chunk length 64..4096")
     return ap.parse_args()
 
 
@@ -418,6 +419,23 @@ def main():
                "h2d_bytes_per_step": hx.numel() * hx.element_size(),
                "d2h_bytes_per_step": hy.numel() * hy.element_size()}
 
+    # chunk-length sweep of the attention region (BASELINE.json configs[4]: UNet 64..4096)
+    sweep = None
+    if args.sweep and not args.profile:
+        sweep = []
+        N = doc.tensors[doc.inputs[0]][1][0]
+        for L in (64, 128, 256, 512, 1024, 2048, 4096):
+            n = -(-N // L)
+            sp = api.plan_parse(cg, f"autochunk-plan 1\nregion s=scores e=pv n={n} dims=0\n")
+            pr, _ = api.estimate_memory(cg, sp)
+            wss = torch.empty(max(sp.workspace_bytes(), 16), dtype=torch.uint8, device="cuda")
+            exs = api.Exec(sp, wss, comm)
+            ts, _ = timed(exs, ins, outs, max(2, args.steps // 2), 1)
+            sweep.append({"chunk_len": L, "n": n, "tokens_per_s": units * max(2, args.steps // 2) / (ts / 1e3),
+                          "planned_peak": pr.peak_bytes, "peak_frac": pr.peak_bytes / prof0.peak_bytes})
+            del exs, wss
+        torch.cuda.empty_cache()
+
     if rank != 0:
         return 0
     cpu = None
@@ -441,6 +459,7 @@ def main():
                                   "budget": budget, "arena_bytes": st.workspace_high_water,
                                   "arena_plus_caller": st.workspace_high_water + caller},
         "unchunked": unchunked, "roofline": roof, "stages": shares, "cpu_baseline": cpu, "e2e": e2e,
+        **({"chunk_sweep": sweep} if sweep else {}),
         "gpu_launches": st.launches * args.steps, "clocks": clocks,
         "paper": {"claim": ">80% activation reduction at <10% speed loss; <10% loss at 20% memory",
                   "hardware": "A100 80GB, PyTorch (P:336)"},

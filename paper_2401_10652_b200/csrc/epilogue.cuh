@@ -233,6 +233,78 @@ __device__ __forceinline__ void epilogue8p(const Epilogue& ep, int b1, int b2, i
   *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + o) = w;
 }
 
+__device__ __forceinline__ void load32_bf16(const __nv_bfloat16* p, float (&f)[32]) {
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+  uint4 u[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) u[i] = q[i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float g[8];
+    bf16x8_to_f(u[i], g);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[8 * i + e] = g[e];
+  }
+}
+
+// Thread-per-row epilogue of 32 consecutive accumulator columns n..n+31 of row m
+// (all aux tensors n-contiguous and 16-byte aligned, checked on the host); the
+// result is packed to 16 bf16x2 words.  Same operation order as epi_value.
+__device__ __forceinline__ void epilogue_row32(const Epilogue& ep, int b1, int b2, int m, int n, bool mvalid,
+                                               const uint32_t (&r)[32], uint32_t (&pk)[16]) {
+  float x[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(r[j]) * ep.scale;
+  float a[32];
+  if (ep.add && mvalid) {
+    load32_bf16(static_cast<const __nv_bfloat16*>(ep.add) + static_cast<int64_t>(b1) * ep.add_sb1 +
+                    static_cast<int64_t>(b2) * ep.add_sb2 + static_cast<int64_t>(m) * ep.add_sm + n,
+                a);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] += a[j];
+  }
+  if (ep.bias) {
+    if (ep.bias_along_m) {
+      const float bm = mvalid ? __bfloat162float(static_cast<const __nv_bfloat16*>(ep.bias)[m]) : 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j] += bm;
+    } else {
+      load32_bf16(static_cast<const __nv_bfloat16*>(ep.bias) + n, a);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j] += a[j];
+    }
+  }
+  if (ep.act != ACT_NONE) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = act_apply(ep.act, x[j]);
+  }
+  if (ep.gate && mvalid) {
+    load32_bf16(static_cast<const __nv_bfloat16*>(ep.gate) + static_cast<int64_t>(b1) * ep.gate_sb1 +
+                    static_cast<int64_t>(b2) * ep.gate_sb2 + static_cast<int64_t>(m) * ep.gate_sm + n,
+                a);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] *= a[j];
+  }
+  if (ep.res && mvalid) {
+    load32_bf16(static_cast<const __nv_bfloat16*>(ep.res) + static_cast<int64_t>(b1) * ep.res_sb1 +
+                    static_cast<int64_t>(b2) * ep.res_sb2 + static_cast<int64_t>(m) * ep.res_sm + n,
+                a);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] += a[j];
+  }
+  if (ep.causal) {
+    const int64_t lim = ep.row_off + m - ep.col_off - n;  // column n+j masked when j > lim
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j > lim) x[j] = -CUDART_INF_F;
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(x[2 * j], x[2 * j + 1]);
+    pk[j] = *reinterpret_cast<uint32_t*>(&h);
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ void epilogue_one(const Epilogue& ep, int N, int b1, int b2, int m, int n, float a0) {
   if (n >= N) return;

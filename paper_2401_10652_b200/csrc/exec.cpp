@@ -383,9 +383,8 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         p.causal_k = 1;
         p.k_row_off = cx.row_off;
       }
-      // few (head x 128-row) tiles per chunk and a long key loop: split K over a
-      // 4-CTA cluster (depends on the key count only, so chunking never changes it)
-      if (p.N <= 64 && p.K >= 2048) p.ksplit = 4;
+      // Cluster split-K (ac_gemm_desc.ksplit) exists but measured slower than one
+      // CTA per tile for these shapes (DSMEM reduction latency), so it stays off.
     } else if (k == "tri_scores") {
       const View &q = in(0), &kk = in(1), &b = in(2);
       const bool end = n.ai("ending") != 0;

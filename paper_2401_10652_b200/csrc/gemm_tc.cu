@@ -47,6 +47,7 @@ struct alignas(64) GemmArgs {
   int total_tiles_dense;
   int vec;  // 1: 8-wide vectorised epilogue (16-byte aux loads / stores) is legal
   int ks;   // cluster split-K factor (1 = none)
+  int lean; // TMA-store epilogue without aux tensors / activation (scale and causal only)
 };
 
 // epilogue staging: per epilogue warp a [32 rows][PITCH] fp32 slab; PITCH = 68
@@ -332,41 +333,69 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         const int n0 = nt * BN + c * SW;
         if constexpr (SW == 64) {
           if (a.tma_store) {
-            // lean path (no aux tensors): scale (+ causal) in registers, bf16 pack,
-            // 128B-swizzled staging, one TMA tensor store per warp and slab
-            uint32_t r[32], r2[32];
-            ptx::tmem_ld32(tbase + c * SW, r);
-            ptx::tmem_ld32(tbase + c * SW + 32, r2);
-            ptx::tmem_ld_wait();
-            if (last) {
-              ptx::tc_fence_before();
-              __syncwarp();
-              if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-            }
-            const float sc = a.ep.scale;
-            const long long lim = a.ep.causal ? (a.ep.row_off + (m0 + lane) - a.ep.col_off - n0) : (1ll << 40);
-            uint32_t pk[32];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              float x0 = __uint_as_float(r[2 * j]) * sc, x1 = __uint_as_float(r[2 * j + 1]) * sc;
-              float y0 = __uint_as_float(r2[2 * j]) * sc, y1 = __uint_as_float(r2[2 * j + 1]) * sc;
-              if (2 * j > lim) x0 = -CUDART_INF_F;
-              if (2 * j + 1 > lim) x1 = -CUDART_INF_F;
-              if (32 + 2 * j > lim) y0 = -CUDART_INF_F;
-              if (33 + 2 * j > lim) y1 = -CUDART_INF_F;
-              __nv_bfloat162 hx = __floats2bfloat162_rn(x0, x1), hy = __floats2bfloat162_rn(y0, y1);
-              pk[j] = *reinterpret_cast<uint32_t*>(&hx);
-              pk[16 + j] = *reinterpret_cast<uint32_t*>(&hy);
-            }
+            // row-oriented path: thread = output row; the epilogue (scale, bias,
+            // triangle bias, activation, gate, residual, causal) runs in registers
+            // with each thread reading its row's contiguous aux segments, then bf16
+            // pack, 128B-swizzled staging, one TMA tensor store per warp and slab
             uint8_t* sb = reinterpret_cast<uint8_t*>(sEpi) + ew * 8192 + sbuf * 4096;
             if (lane == 0) ptx::bulk_wait_read<1>();  // the store issued two slabs ago has read its buffer
             __syncwarp();
+            const int m = m0 + lane;
+            const bool mvalid = m < a.M;
+            if (a.lean) {
+              // scale (+ causal) only: both TMEM loads in flight, no aux traffic
+              uint32_t r[32], r2[32];
+              ptx::tmem_ld32(tbase + c * SW, r);
+              ptx::tmem_ld32(tbase + c * SW + 32, r2);
+              ptx::tmem_ld_wait();
+              if (last) {
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+              }
+              const float sc = a.ep.scale;
+              const long long lim = a.ep.causal ? (a.ep.row_off + m - a.ep.col_off - n0) : (1ll << 40);
+              uint32_t pk[32];
 #pragma unroll
-            for (int ch = 0; ch < 8; ++ch) {
-              const uint32_t addr = ptx::smem_u32(sb + lane * 128 + ((ch ^ (lane & 7)) * 16));
-              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[4 * ch]),
-                           "r"(pk[4 * ch + 1]), "r"(pk[4 * ch + 2]), "r"(pk[4 * ch + 3])
-                           : "memory");
+              for (int j = 0; j < 16; ++j) {
+                float x0 = __uint_as_float(r[2 * j]) * sc, x1 = __uint_as_float(r[2 * j + 1]) * sc;
+                float y0 = __uint_as_float(r2[2 * j]) * sc, y1 = __uint_as_float(r2[2 * j + 1]) * sc;
+                if (2 * j > lim) x0 = -CUDART_INF_F;
+                if (2 * j + 1 > lim) x1 = -CUDART_INF_F;
+                if (32 + 2 * j > lim) y0 = -CUDART_INF_F;
+                if (33 + 2 * j > lim) y1 = -CUDART_INF_F;
+                __nv_bfloat162 hx = __floats2bfloat162_rn(x0, x1), hy = __floats2bfloat162_rn(y0, y1);
+                pk[j] = *reinterpret_cast<uint32_t*>(&hx);
+                pk[16 + j] = *reinterpret_cast<uint32_t*>(&hy);
+              }
+#pragma unroll
+              for (int ch = 0; ch < 8; ++ch) {
+                const uint32_t addr = ptx::smem_u32(sb + lane * 128 + ((ch ^ (lane & 7)) * 16));
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[4 * ch]),
+                             "r"(pk[4 * ch + 1]), "r"(pk[4 * ch + 2]), "r"(pk[4 * ch + 3])
+                             : "memory");
+              }
+            } else
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              uint32_t r[32];
+              ptx::tmem_ld32(tbase + c * SW + hh * 32, r);
+              ptx::tmem_ld_wait();
+              if (hh == 1 && last) {
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+              }
+              uint32_t pk[16];
+              epilogue_row32(a.ep, b1, b2, m, n0 + hh * 32, mvalid, r, pk);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int ch = hh * 4 + q;
+                const uint32_t addr = ptx::smem_u32(sb + lane * 128 + ((ch ^ (lane & 7)) * 16));
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[4 * q]),
+                             "r"(pk[4 * q + 1]), "r"(pk[4 * q + 2]), "r"(pk[4 * q + 3])
+                             : "memory");
+              }
             }
             ptx::fence_proxy_async_smem();
             __syncwarp();
@@ -538,8 +567,8 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
     if (e.res) v = v && e.res_sn == 1 && al(e.res) && m8(e.res_sm) && m8(e.res_sb1) && m8(e.res_sb2);
     if (e.bias && !e.bias_along_m) v = v && al(e.bias);
     a.vec = v ? 1 : 0;
-    // TMA-store epilogue: no aux tensors, identity activation, 64-column slabs
-    if (BN >= 64 && v && !e.add && !e.bias && !e.gate && !e.res && e.act == ACT_NONE) {
+    // row-oriented TMA-store epilogue: 64-column slabs, n-contiguous aligned output and aux
+    if (BN >= 64 && v) {
       EncodeTiledFn enc = get_encode();
       cuuint64_t dims[4] = {static_cast<cuuint64_t>(p.N), static_cast<cuuint64_t>(p.M),
                             static_cast<cuuint64_t>(p.B1), static_cast<cuuint64_t>(p.B2)};
@@ -555,6 +584,7 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
       a.tma_store = ok ? 1 : 0;
+      a.lean = (!e.add && !e.bias && !e.gate && !e.res && e.act == ACT_NONE) ? 1 : 0;
     }
   }
   a.tiles_per_batch_dense = a.MT * a.NT;

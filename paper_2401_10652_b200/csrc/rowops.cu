@@ -173,9 +173,11 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-__global__ void __launch_bounds__(SMX_THREADS) softmax_bulk_kernel(
+template <int TH>
+__global__ void __launch_bounds__(TH) softmax_bulk_kernel(
     const __nv_bfloat16* __restrict__ s, __nv_bfloat16* __restrict__ p, int64_t rows, int64_t ncols, int64_t ld,
     int causal, int64_t row_off, int64_t group, int64_t gstride, int64_t ldo, int64_t gstrideo, int64_t cap_bytes) {
+  constexpr int SMX_THREADS = TH;  // threads per row (CTA), sized to the launch's longest valid row
   extern __shared__ __align__(128) uint8_t sm[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm);
   __shared__ float red[2][SMX_THREADS / 32];
@@ -467,22 +469,42 @@ cudaError_t launch_softmax_stream(const void* s, void* p, int64_t rows, int64_t 
 cudaError_t launch_softmax_bulk(const void* s, void* p, int64_t rows, int64_t ncols, int64_t ld, int causal,
                                 int64_t row_off, int64_t group, int64_t gstride, int64_t ldo, int64_t gstrideo,
                                 cudaStream_t st) {
-  const int64_t cap = ((ncols * 2 + 127) / 128) * 128;
-  const int smem = static_cast<int>(128 + SMX_NBUF * cap);
-  static int attr_set = 0;
-  if (attr_set < smem) {
-    cudaError_t e = cudaFuncSetAttribute(softmax_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = 200 * 1024;
+  // a causal launch never reads beyond its last row's diagonal: size the row
+  // buffers (and the CTA) by the longest valid prefix, so early chunks get many
+  // small CTAs per SM (more rows in flight) instead of a few half-empty ones
+  int64_t maxv = ncols;
+  if (causal) {
+    const int64_t last = row_off + (group > 0 ? group : rows);
+    if (last < maxv) maxv = last;
   }
+  const int64_t cap = ((maxv * 2 + 127) / 128) * 128;
+  const int smem = static_cast<int>(128 + SMX_NBUF * cap);
+  static bool attr_set = false;
+  if (!attr_set) {
+    for (auto fn : {softmax_bulk_kernel<128>, softmax_bulk_kernel<256>, softmax_bulk_kernel<512>}) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      if (e != cudaSuccess) return e;
+    }
+    attr_set = true;
+  }
+  const int th = maxv >= 8192 ? 512 : (maxv >= 2048 ? 256 : 128);
   int per_sm = (220 * 1024) / smem;
-  if (per_sm > 4) per_sm = 4;
+  if (per_sm > 2048 / th) per_sm = 2048 / th;
   if (per_sm < 1) return cudaErrorInvalidValue;
   int64_t grid = static_cast<int64_t>(num_sms()) * per_sm;
   if (grid > rows) grid = rows;
-  softmax_bulk_kernel<<<static_cast<unsigned>(grid), SMX_THREADS, smem, st>>>(
-      static_cast<const __nv_bfloat16*>(s), static_cast<__nv_bfloat16*>(p), rows, ncols, ld, causal, row_off, group,
-      gstride, ldo, gstrideo, cap);
+  auto S = static_cast<const __nv_bfloat16*>(s);
+  auto P = static_cast<__nv_bfloat16*>(p);
+  const unsigned g = static_cast<unsigned>(grid);
+  if (th == 512)
+    softmax_bulk_kernel<512><<<g, 512, smem, st>>>(S, P, rows, ncols, ld, causal, row_off, group, gstride, ldo,
+                                                    gstrideo, cap);
+  else if (th == 256)
+    softmax_bulk_kernel<256><<<g, 256, smem, st>>>(S, P, rows, ncols, ld, causal, row_off, group, gstride, ldo,
+                                                    gstrideo, cap);
+  else
+    softmax_bulk_kernel<128><<<g, 128, smem, st>>>(S, P, rows, ncols, ld, causal, row_off, group, gstride, ldo,
+                                                    gstrideo, cap);
   return cudaGetLastError();
 }
 
