@@ -26,7 +26,10 @@ class Graph:
 
     def __del__(self):
         if getattr(self, "_h", None) and self._h.value:
-            lib().ac_graph_free(self._h)
+            try:
+                lib().ac_graph_free(self._h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self._h = None
 
     @property
@@ -69,7 +72,10 @@ class Plan:
 
     def __del__(self):
         if getattr(self, "_h", None) and self._h.value:
-            lib().ac_plan_free(self._h)
+            try:
+                lib().ac_plan_free(self._h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self._h = None
 
     @property
@@ -197,7 +203,10 @@ class Exec:
 
     def __del__(self):
         if getattr(self, "_h", None) and self._h.value:
-            lib().ac_exec_free(self._h)
+            try:
+                lib().ac_exec_free(self._h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self._h = None
 
     def run(self, inputs: dict, outputs: dict, stream=None):

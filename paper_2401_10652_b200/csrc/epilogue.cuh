@@ -233,11 +233,13 @@ __device__ __forceinline__ void epilogue8p(const Epilogue& ep, int b1, int b2, i
   *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + o) = w;
 }
 
-__device__ __forceinline__ void load32_bf16(const __nv_bfloat16* p, float (&f)[32]) {
+// 32 consecutive bf16 -> fp32; only the 8-element groups below `nvalid` are
+// read (columns past N are never touched; the vec path guarantees N % 8 == 0)
+__device__ __forceinline__ void load32_bf16(const __nv_bfloat16* p, float (&f)[32], int nvalid = 32) {
   const uint4* q = reinterpret_cast<const uint4*>(p);
   uint4 u[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) u[i] = q[i];
+  for (int i = 0; i < 4; ++i) u[i] = 8 * i < nvalid ? q[i] : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     float g[8];
@@ -251,7 +253,7 @@ __device__ __forceinline__ void load32_bf16(const __nv_bfloat16* p, float (&f)[3
 // (all aux tensors n-contiguous and 16-byte aligned, checked on the host); the
 // result is packed to 16 bf16x2 words.  Same operation order as epi_value.
 __device__ __forceinline__ void epilogue_row32(const Epilogue& ep, int b1, int b2, int m, int n, bool mvalid,
-                                               const uint32_t (&r)[32], uint32_t (&pk)[16]) {
+                                               const uint32_t (&r)[32], uint32_t (&pk)[16], int nvalid) {
   float x[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(r[j]) * ep.scale;
@@ -259,7 +261,7 @@ __device__ __forceinline__ void epilogue_row32(const Epilogue& ep, int b1, int b
   if (ep.add && mvalid) {
     load32_bf16(static_cast<const __nv_bfloat16*>(ep.add) + static_cast<int64_t>(b1) * ep.add_sb1 +
                     static_cast<int64_t>(b2) * ep.add_sb2 + static_cast<int64_t>(m) * ep.add_sm + n,
-                a);
+                a, nvalid);
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] += a[j];
   }
@@ -269,7 +271,7 @@ __device__ __forceinline__ void epilogue_row32(const Epilogue& ep, int b1, int b
 #pragma unroll
       for (int j = 0; j < 32; ++j) x[j] += bm;
     } else {
-      load32_bf16(static_cast<const __nv_bfloat16*>(ep.bias) + n, a);
+      load32_bf16(static_cast<const __nv_bfloat16*>(ep.bias) + n, a, nvalid);
 #pragma unroll
       for (int j = 0; j < 32; ++j) x[j] += a[j];
     }
@@ -281,14 +283,14 @@ __device__ __forceinline__ void epilogue_row32(const Epilogue& ep, int b1, int b
   if (ep.gate && mvalid) {
     load32_bf16(static_cast<const __nv_bfloat16*>(ep.gate) + static_cast<int64_t>(b1) * ep.gate_sb1 +
                     static_cast<int64_t>(b2) * ep.gate_sb2 + static_cast<int64_t>(m) * ep.gate_sm + n,
-                a);
+                a, nvalid);
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] *= a[j];
   }
   if (ep.res && mvalid) {
     load32_bf16(static_cast<const __nv_bfloat16*>(ep.res) + static_cast<int64_t>(b1) * ep.res_sb1 +
                     static_cast<int64_t>(b2) * ep.res_sb2 + static_cast<int64_t>(m) * ep.res_sm + n,
-                a);
+                a, nvalid);
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] += a[j];
   }

@@ -65,6 +65,10 @@ struct ac_exec {
   std::vector<int> region_of;          // node -> region index or -1
   std::vector<char> causal_fast;       // per node: member of an aligned causal chain
   std::vector<int> chain_rows_dim;     // per node: output dim holding query rows (-1 none)
+  // fused softmax chains (f2): per node 0 none, 1 scores (writes stats), 2 softmax
+  // (not launched), 3 PV (normalises S in smem); fuse_s / fuse_p: the chain's S and P tensors
+  std::vector<char> fuse_role;
+  std::vector<int> fuse_s, fuse_p;
   mutable ac_run_stats stats{};
   // profiling: event pairs per launch of the last run
   bool profiling = false;
@@ -78,6 +82,55 @@ struct ac_exec {
 namespace {
 
 bool is_caller(const Graph& g, int t) { return g.is_input[t] || g.is_weight[t] || g.is_output[t]; }
+
+int region_index(const Plan& plan, int node) {
+  for (size_t r = 0; r < plan.regions.size(); ++r)
+    if (plan.regions[r].n > 1 && node >= plan.regions[r].start && node <= plan.regions[r].end)
+      return static_cast<int>(r);
+  return -1;
+}
+
+// attn_scores -> softmax(last dim) -> attn_pv chains whose softmax normalisation is
+// fused into PV's operand path (NEXT f2): S consumed only by the
+// softmax, P only by the PV, bf16, head dim <= 64, all three nodes executed in the
+// same chunk context.  P is then never written; its (still allocated) buffer holds
+// the per-slab softmax statistics.  AC_FUSE_SOFTMAX=0 disables it.
+struct Chain {
+  int scores, softmax, pv;
+};
+std::vector<Chain> fused_chains(const Graph& g, const Plan& plan) {
+  std::vector<Chain> out;
+  const char* env = getenv("AC_FUSE_SOFTMAX");
+  if (env && env[0] == '0') return out;
+  for (int i = 0; i < static_cast<int>(g.nodes.size()); ++i) {
+    const Node& n = g.nodes[i];
+    if (n.kind != "attn_scores") continue;
+    const int s_t = n.output;
+    if (g.tensors[s_t].dtype != DT::BF16 || g.is_output[s_t] || g.consumers[s_t].size() != 1) continue;
+    const int sm = g.consumers[s_t][0];
+    if (g.nodes[sm].kind != "softmax" || g.nodes[sm].ai("dim") != 2) continue;
+    const int p_t = g.nodes[sm].output;
+    if (g.is_output[p_t] || g.consumers[p_t].size() != 1) continue;
+    const int pv = g.consumers[p_t][0];
+    if (g.nodes[pv].kind != "attn_pv" || g.nodes[pv].inputs[0] != p_t) continue;
+    // PV on the BN = 64 tile (32 < head dim <= 64); scores on the lean TMA-store path
+    const int64_t dh = g.tensors[g.nodes[pv].output].shape[2], nk = g.tensors[s_t].shape[2];
+    if (dh <= 32 || dh > 64 || nk < 64 || nk % 8 != 0) continue;
+    const int ri = region_index(plan, i), rs = region_index(plan, sm), rp = region_index(plan, pv);
+    if (ri != rs || rs != rp) continue;
+    if (ri >= 0) {
+      const Region& R = plan.regions[ri];
+      bool hoisted = false;
+      for (int h : R.hoisted) hoisted = hoisted || h == i || h == sm || h == pv;
+      if (hoisted) continue;
+      // S and P must be chunked along the same dim (heads or query rows), never keys
+      const int ds = R.dim_of(s_t), dp = R.dim_of(p_t);
+      if (ds != dp || ds == 2) continue;
+    }
+    out.push_back({i, sm, pv});
+  }
+  return out;
+}
 
 Arena build_arena(const Graph& g, const Plan& plan) {
   const int T = static_cast<int>(g.tensors.size());
@@ -125,6 +178,16 @@ Arena build_arena(const Graph& g, const Plan& plan) {
         if (c >= r.start && c <= r.end) lastc = std::max(lastc, c);
       death[t] = lastc;
     }
+  }
+  // fused chains: S stays live until the PV reads it; P's buffer shrinks to the
+  // softmax statistics (float2 per row and 64-key slab), written by the scores step
+  for (const Chain& c : fused_chains(g, plan)) {
+    const int s_t = g.nodes[c.scores].output, p_t = g.nodes[c.softmax].output;
+    const int64_t nk = g.tensors[p_t].shape[2];
+    const int64_t rows = bytes[p_t] / (nk * dt_size(g.tensors[p_t].dtype));
+    bytes[p_t] = rows * ((nk + 63) / 64) * 8;
+    birth[p_t] = std::min(birth[p_t], c.scores);
+    death[s_t] = std::max(death[s_t], c.pv);
   }
   std::vector<int> order;
   for (int t = 0; t < T; ++t)
@@ -238,6 +301,13 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
     if (collapse(x, 0, x.nd) != 1 || collapse(out, 0, out.nd) != 1) return unsup("non-contiguous rows");
     err = layernorm(x.p, in(1).p, in(2).p, out.p, extent(x, 0, x.nd - na), static_cast<int>(C),
                     static_cast<float>(n.af("eps", 1e-5)), dtc, s);
+  } else if (k == "softmax" && e->fuse_role[i] == 2) {
+    // fused chain: the softmax node only combines the slab statistics the scores
+    // step left in P's buffer into per-slab factors; the PV applies them
+    const View& x = in(0);  // S view [H, M, Nk] of this launch
+    const int64_t ns = (x.sh[2] + 63) / 64;
+    err = softmax_stats_combine(reinterpret_cast<float2*>(out.p), x.sh[0], x.sh[1], static_cast<int>(ns),
+                                x.sh[1] * ns, x.sh[1], cx.fast ? 1 : 0, cx.row_off, s);
   } else if (k == "softmax") {
     const View& x = in(0);
     if (n.ai("dim") != x.nd - 1 || x.st[x.nd - 1] != 1) return unsup("softmax over a non-last dim");
@@ -369,8 +439,18 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         ep.col_off = cx.col_off;
         p.causal_tiles = cx.fast ? 1 : 0;
       }
+      if (e->fuse_role[i] == 1) {
+        // per-(row, 64-key slab) softmax partials into the chain's P buffer
+        const int64_t ns = (p.N + 63) / 64;
+        ep.stats = reinterpret_cast<float2*>(V[e->fuse_p[i]].p);
+        ep.stats_ss = p.M;
+        ep.stats_sb1 = static_cast<int64_t>(p.M) * ns;
+      }
     } else if (k == "attn_pv") {
-      const View &pp = in(0), &vt = in(1);
+      // fused chain: A is the raw scores S, normalised in shared memory with the
+      // statistics the scores step left in P's buffer
+      const bool fz = e->fuse_role[i] == 3;
+      const View &pp = fz ? V[e->fuse_s[i]] : in(0), &vt = in(1);
       p.M = static_cast<int>(pp.sh[1]);
       p.N = static_cast<int>(vt.sh[1]);
       p.K = static_cast<int>(pp.sh[2]);
@@ -382,6 +462,12 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
       if (cx.fast) {
         p.causal_k = 1;
         p.k_row_off = cx.row_off;
+      }
+      if (fz) {
+        const int64_t ns = (p.K + 63) / 64;
+        p.fuse_stats = reinterpret_cast<const float2*>(in(0).p);
+        p.fuse_ss = p.M;
+        p.fuse_sb1 = static_cast<int64_t>(p.M) * ns;
       }
       // Cluster split-K (ac_gemm_desc.ksplit) exists but measured slower than one
       // CTA per tile for these shapes (DSMEM reduction latency), so it stays off.
@@ -537,6 +623,21 @@ ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_
     for (int node : {i, sm, pv}) e->causal_fast[node] = 1;
   }
   for (int i = 0; i < S; ++i) e->chain_rows_dim[i] = rows_dim(g.nodes[i]);
+  e->fuse_role.assign(S, 0);
+  e->fuse_s.assign(S, -1);
+  e->fuse_p.assign(S, -1);
+  if (e->dt == DT::BF16) {
+    for (const Chain& c : fused_chains(g, e->plan)) {
+      e->fuse_role[c.scores] = 1;
+      e->fuse_role[c.softmax] = 2;
+      e->fuse_role[c.pv] = 3;
+      const int s_t = g.nodes[c.scores].output, p_t = g.nodes[c.softmax].output;
+      for (int node : {c.scores, c.softmax, c.pv}) {
+        e->fuse_s[node] = s_t;
+        e->fuse_p[node] = p_t;
+      }
+    }
+  }
   *out = e.release();
   return AC_OK;
 }

@@ -48,6 +48,9 @@ struct alignas(64) GemmArgs {
   int vec;  // 1: 8-wide vectorised epilogue (16-byte aux loads / stores) is legal
   int ks;   // cluster split-K factor (1 = none)
   int lean; // TMA-store epilogue without aux tensors / activation (scale and causal only)
+  int fuse; // fused softmax-normalised A operand (PV of the f2 path)
+  const float2* fstats;
+  long long fst_sb1, fst_ss;
 };
 
 // epilogue staging: per epilogue warp a [32 rows][PITCH] fp32 slab; PITCH = 68
@@ -94,7 +97,10 @@ __device__ __forceinline__ void decode_tile(const GemmArgs& a, const int* prefix
   kb = (kend + BK - 1) / BK;
 }
 
-template <int BN>
+// MODE: 0 generic; 1 f2 scores (QK^T -> e = exp(s - m_slab) + slab statistics,
+// lean TMA-store epilogue only); 2 f2 PV (A tile e rescaled to P in shared
+// memory by all epilogue warps, which also run the output epilogue)
+template <int BN, int MODE>
 __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_constant__ GemmArgs a) {
   using C = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -109,11 +115,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
   uint64_t* part_full = full + 16;   // split-K: leader waits for the other ranks' partials
   uint64_t* part_empty = full + 20;  // split-K: ranks wait for the leader to have read them
+  uint64_t* ready = full + 24;       // fused softmax: A tile transformed S -> P (<= 5 stages)
   int* prefix = reinterpret_cast<int*>(full + 32);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int ks = a.ks;
+  const int ks = MODE == 0 ? a.ks : 1;
   const uint32_t crank = ks > 1 ? ptx::cluster_rank() : 0;
   const int cid = blockIdx.x / ks, ncl = gridDim.x / ks;
 
@@ -160,6 +167,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       ptx::mbar_init(&tfull[s], 1);
       ptx::mbar_init(&tempty[s], EPI_WARPS);
     }
+    for (int s = 0; s < C::STAGES && s < 8; ++s) ptx::mbar_init(&ready[s], 32 * EPI_WARPS);
     for (int q = 0; q < 4; ++q) {
       ptx::mbar_init(&part_full[q], 32 * (ks > 1 ? ks - 1 : 1));
       ptx::mbar_init(&part_empty[q], 32);
@@ -208,7 +216,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       const uint32_t d = tmem_base + acc * BN;
       const int klo = kbn * static_cast<int>(crank) / ks, khi = kbn * (static_cast<int>(crank) + 1) / ks;
       for (int kb = klo; kb < khi; ++kb) {
-        ptx::mbar_wait(&full[stage], phase);
+        ptx::mbar_wait(MODE == 2 ? &ready[stage] : &full[stage], phase);
         ptx::tc_fence_after();
         if (lane == 0) {
           const uint32_t sa = ptx::smem_u32(sA + stage * C::A_BYTES);
@@ -243,6 +251,89 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     int sbuf = 0;
     uint32_t aphase = 0;
     uint32_t pf_phase = 0, pe_phase = 0;  // split-K barrier phases
+    if constexpr (MODE == 2) {
+      // ---- f2 PV: thread = A-tile row (TMEM lane quarter x lane), half = which
+      // four of the row's eight 16-byte chunks.  Rescale the stored
+      // e = exp(s - m_slab) in place to P = e * f_slab, f_slab = exp(m_slab - m_row)
+      // / l_row left in the statistics by the combine step (prefetched 8 slabs
+      // ahead); keys >= K are TMA zero-fill (e = 0), rows past M get f = 0.  After
+      // the tile's last k-block the same warps run the output epilogue.
+      const int r = quarter * 32 + lane;
+      int st = 0;
+      uint32_t ph = 0;
+      for (int t = cid; t < total; t += ncl) {
+        int b1, b2, mt, nt, kbn;
+        decode_tile(a, prefix, tpb, t, b1, b2, mt, nt, kbn);
+        const int m = mt * BM + r;
+        const bool mv = m < a.M;
+        const float* fp = reinterpret_cast<const float*>(a.fstats + static_cast<long long>(b1) * a.fst_sb1 + (mv ? m : 0));
+        const long long fs = 2 * a.fst_ss;
+        float fr[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) fr[j] = (mv && j < kbn) ? __ldg(fp + j * fs) : 0.f;
+        for (int kb0 = 0; kb0 < kbn; kb0 += 8) {
+          float nx[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) nx[j] = (mv && kb0 + 8 + j < kbn) ? __ldg(fp + (kb0 + 8 + j) * fs) : 0.f;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (kb0 + j < kbn) {
+              const float f = fr[j];
+              ptx::mbar_wait(&full[st], ph);
+              uint8_t* row = sA + st * C::A_BYTES + r * 128;
+#pragma unroll
+              for (int q4 = 0; q4 < 4; ++q4) {
+                // same factor for every element: walk physical chunks in swizzled
+                // order so 8 consecutive rows hit all 32 banks
+                const int ch = half * 4 + q4;
+                const uint32_t addr = ptx::smem_u32(row + ((ch ^ (r & 7)) * 16));
+                uint32_t w0, w1, w2, w3;
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                             : "r"(addr));
+                uint32_t w[4] = {w0, w1, w2, w3};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const float2 e = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[q]));
+                  __nv_bfloat162 h = __floats2bfloat162_rn(e.x * f, e.y * f);
+                  w[q] = *reinterpret_cast<uint32_t*>(&h);
+                }
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(w[0]), "r"(w[1]),
+                             "r"(w[2]), "r"(w[3])
+                             : "memory");
+              }
+              ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+              ptx::mbar_arrive(&ready[st]);
+              if (++st == C::STAGES) { st = 0; ph ^= 1; }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) fr[j] = nx[j];
+        }
+        // output epilogue: this thread's row, columns half*32 .. +31
+        ptx::mbar_wait(&tfull[acc], aphase);
+        ptx::tc_fence_after();
+        uint32_t rr[32];
+        ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + half * 32, rr);
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+        const int n = nt * BN + half * 32;
+        if (mv && n < a.N) {
+          uint32_t pk[16];
+          epilogue_row32(a.ep, b1, b2, m, n, true, rr, pk, a.N - n);
+          uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.ep.out) +
+                                              static_cast<long long>(b1) * a.ep.out_sb1 +
+                                              static_cast<long long>(b2) * a.ep.out_sb2 +
+                                              static_cast<long long>(m) * a.ep.out_sm + n);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (8 * q < a.N - n) o[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        }
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+    } else
     for (int t = cid; t < total; t += ncl) {
       int b1, b2, mt, nt, kbn;
       decode_tile(a, prefix, tpb, t, b1, b2, mt, nt, kbn);
@@ -332,7 +423,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         const bool last = c + 2 >= NSLAB;
         const int n0 = nt * BN + c * SW;
         if constexpr (SW == 64) {
-          if (a.tma_store) {
+          if (MODE == 1 || a.tma_store) {
             // row-oriented path: thread = output row; the epilogue (scale, bias,
             // triangle bias, activation, gate, residual, causal) runs in registers
             // with each thread reading its row's contiguous aux segments, then bf16
@@ -342,7 +433,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
             __syncwarp();
             const int m = m0 + lane;
             const bool mvalid = m < a.M;
-            if (a.lean) {
+            if (MODE == 1 || a.lean) {
               // scale (+ causal) only: both TMEM loads in flight, no aux traffic
               uint32_t r[32], r2[32];
               ptx::tmem_ld32(tbase + c * SW, r);
@@ -353,20 +444,61 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
               }
-              const float sc = a.ep.scale;
-              const long long lim = a.ep.causal ? (a.ep.row_off + m - a.ep.col_off - n0) : (1ll << 40);
+              long long lim = a.ep.causal ? (a.ep.row_off + m - a.ep.col_off - n0) : (1ll << 40);
+              if (lim > a.N - 1 - n0) lim = a.N - 1 - n0;  // columns past N: masked (clipped by the store)
               uint32_t pk[32];
+              if constexpr (MODE == 1) {
+                // f2 scores: the slab's scores in the log2 domain, x = acc * scale * log2(e)
+                // (scale > 0, so the max is taken on the raw accumulator); stored
+                // e = bf16(2^(x - m2)), statistics (m2 = max x, l = sum of e in fp32)
+                constexpr float L2E = 1.4426950408889634f;
+                const float cl = a.ep.scale * L2E;
+                float v[64];
 #pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                float x0 = __uint_as_float(r[2 * j]) * sc, x1 = __uint_as_float(r[2 * j + 1]) * sc;
-                float y0 = __uint_as_float(r2[2 * j]) * sc, y1 = __uint_as_float(r2[2 * j + 1]) * sc;
-                if (2 * j > lim) x0 = -CUDART_INF_F;
-                if (2 * j + 1 > lim) x1 = -CUDART_INF_F;
-                if (32 + 2 * j > lim) y0 = -CUDART_INF_F;
-                if (33 + 2 * j > lim) y1 = -CUDART_INF_F;
-                __nv_bfloat162 hx = __floats2bfloat162_rn(x0, x1), hy = __floats2bfloat162_rn(y0, y1);
-                pk[j] = *reinterpret_cast<uint32_t*>(&hx);
-                pk[16 + j] = *reinterpret_cast<uint32_t*>(&hy);
+                for (int j = 0; j < 32; ++j) {
+                  v[j] = __uint_as_float(r[j]);
+                  v[32 + j] = __uint_as_float(r2[j]);
+                }
+                if (lim < 63) {  // diagonal / ragged slab only
+#pragma unroll
+                  for (int j = 0; j < 64; ++j)
+                    if (j > lim) v[j] = -CUDART_INF_F;
+                }
+                float mx0 = v[0], mx1 = v[1], mx2 = v[2], mx3 = v[3];
+#pragma unroll
+                for (int j = 4; j < 64; j += 4) {
+                  mx0 = fmaxf(mx0, v[j]); mx1 = fmaxf(mx1, v[j + 1]);
+                  mx2 = fmaxf(mx2, v[j + 2]); mx3 = fmaxf(mx3, v[j + 3]);
+                }
+                const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+                const float m2 = mx * cl;
+                const float mref = mx == -CUDART_INF_F ? 0.f : m2;
+                float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                  const float e0 = ptx::ex2(fmaf(v[2 * j], cl, -mref)), e1 = ptx::ex2(fmaf(v[2 * j + 1], cl, -mref));
+                  l0 += e0;
+                  l1 += e1;
+                  __nv_bfloat162 h = __floats2bfloat162_rn(e0, e1);
+                  pk[j] = *reinterpret_cast<uint32_t*>(&h);
+                }
+                if (mvalid && n0 < a.N)
+                  a.ep.stats[static_cast<long long>(b1) * a.ep.stats_sb1 + static_cast<long long>(n0 / 64) * a.ep.stats_ss +
+                             m] = make_float2(m2, l0 + l1);
+              } else {
+                const float sc = a.ep.scale;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                  float x0 = __uint_as_float(r[2 * j]) * sc, x1 = __uint_as_float(r[2 * j + 1]) * sc;
+                  float y0 = __uint_as_float(r2[2 * j]) * sc, y1 = __uint_as_float(r2[2 * j + 1]) * sc;
+                  if (2 * j > lim) x0 = -CUDART_INF_F;
+                  if (2 * j + 1 > lim) x1 = -CUDART_INF_F;
+                  if (32 + 2 * j > lim) y0 = -CUDART_INF_F;
+                  if (33 + 2 * j > lim) y1 = -CUDART_INF_F;
+                  __nv_bfloat162 hx = __floats2bfloat162_rn(x0, x1), hy = __floats2bfloat162_rn(y0, y1);
+                  pk[j] = *reinterpret_cast<uint32_t*>(&hx);
+                  pk[16 + j] = *reinterpret_cast<uint32_t*>(&hy);
+                }
               }
 #pragma unroll
               for (int ch = 0; ch < 8; ++ch) {
@@ -387,7 +519,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
                 if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
               }
               uint32_t pk[16];
-              epilogue_row32(a.ep, b1, b2, m, n0 + hh * 32, mvalid, r, pk);
+              epilogue_row32(a.ep, b1, b2, m, n0 + hh * 32, mvalid, r, pk, a.N - (n0 + hh * 32));
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 const int ch = hh * 4 + q;
@@ -536,12 +668,12 @@ bool make_map(CUtensorMap* m, const Operand& op, int K, int rows, int B1, int B2
   return r == CUDA_SUCCESS;
 }
 
-template <int BN>
+template <int BN, int MODE>
 cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   using C = Cfg<BN>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -589,7 +721,15 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   }
   a.tiles_per_batch_dense = a.MT * a.NT;
   a.total_tiles_dense = a.tiles_per_batch_dense * p.B1 * p.B2;
-  a.ks = (BN == 64 && a.vec && p.ksplit > 1) ? (p.ksplit > 8 ? 8 : p.ksplit) : 1;
+  // f2 modes: scores need the lean TMA-store epilogue and a positive scale; PV the
+  // 64-wide tile with an n-contiguous aligned output
+  if (MODE == 1 && !(a.tma_store && a.lean && p.ep.scale > 0.f)) return cudaErrorInvalidValue;
+  if (MODE == 2 && !(BN == 64 && a.vec)) return cudaErrorInvalidValue;
+  a.fuse = MODE == 2 ? 1 : 0;
+  a.fstats = p.fuse_stats;
+  a.fst_sb1 = p.fuse_sb1;
+  a.fst_ss = p.fuse_ss;
+  a.ks = (MODE == 0 && BN == 64 && a.vec && p.ksplit > 1) ? (p.ksplit > 8 ? 8 : p.ksplit) : 1;
   if (a.ks > 1) a.tma_store = 0;
   const int sms = num_sms();
   int grid = a.total_tiles_dense * a.ks;
@@ -597,7 +737,7 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   if (grid > cap) grid = cap;
   if (grid < a.ks) grid = a.ks;
   if (a.ks == 1) {
-    gemm_tc_kernel<BN><<<grid, NUM_THREADS, C::SMEM, s>>>(a);
+    gemm_tc_kernel<BN, MODE><<<grid, NUM_THREADS, C::SMEM, s>>>(a);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -612,7 +752,7 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   lattr[0].val.clusterDim.z = 1;
   cfg.attrs = lattr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN>, a);
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, MODE>, a);
 }
 
 }  // namespace
@@ -632,11 +772,20 @@ cudaError_t gemm_tc(const GemmProblem& p, cudaStream_t s, int bn_hint) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0 || p.B1 <= 0 || p.B2 <= 0) return cudaErrorInvalidValue;
   int bn = bn_hint;
   if (bn == 0) bn = p.N <= 32 ? 32 : p.N <= 64 ? 64 : p.N <= 128 ? 128 : 256;
+  if (p.fuse_stats) return bn == 64 ? launch<64, 2>(p, s) : cudaErrorInvalidValue;
+  if (p.ep.stats) {
+    switch (bn) {
+      case 64: return launch<64, 1>(p, s);
+      case 128: return launch<128, 1>(p, s);
+      case 256: return launch<256, 1>(p, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (bn) {
-    case 32: return launch<32>(p, s);
-    case 64: return launch<64>(p, s);
-    case 128: return launch<128>(p, s);
-    case 256: return launch<256>(p, s);
+    case 32: return launch<32, 0>(p, s);
+    case 64: return launch<64, 0>(p, s);
+    case 128: return launch<128, 0>(p, s);
+    case 256: return launch<256, 0>(p, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -42,6 +42,13 @@ struct Epilogue {
   int64_t res_sb1 = 0, res_sb2 = 0, res_sm = 0, res_sn = 1;
   void* out = nullptr;
   int64_t out_sb1 = 0, out_sb2 = 0, out_sm = 0, out_sn = 1;
+  // fused softmax (NEXT f2), QK^T lean epilogue only (scale > 0): with stats
+  // non-null the score is taken in the log2 domain, x = acc * scale * log2(e)
+  // (fp32, never rounded), the stored value is e = bf16(2^(x - m2)) with m2 the
+  // slab max, and stats[b1*stats_sb1 + (n/64)*stats_ss + m] = (m2, fp32 sum of e)
+  // per (b1, 64-column slab, row) - slab-major so a warp's 32 rows write 256 B
+  float2* stats = nullptr;
+  int64_t stats_sb1 = 0, stats_ss = 0;
 };
 
 // D[b1,b2][m][n] = sum_k A[b1,b2][m][k] * B[b1,b2][n][k]
@@ -59,6 +66,13 @@ struct GemmProblem {
   // fp32 partials through distributed shared memory in rank order (deterministic;
   // the split depends only on the tile's K range, never on the chunking)
   int ksplit = 1;
+  // fused softmax-normalised PV (NEXT f2): A holds e = exp(s - m_slab) written by
+  // the QK^T epilogue (Epilogue::stats); each 128 x 64 A tile (one slab) is
+  // rescaled in shared memory to P = e * exp(m_slab - m_row) / l_row (row (m, l)
+  // combined from the slab statistics over the tile's key range) before the MMA
+  // reads it, so P is never written to HBM.  BN = 64 only; layout as Epilogue::stats.
+  const float2* fuse_stats = nullptr;
+  int64_t fuse_sb1 = 0, fuse_ss = 0;
 };
 
 // bf16 x bf16 -> fp32 (TMEM) -> bf16, tcgen05 + TMA, sm_100a.  Returns a
@@ -80,6 +94,14 @@ cudaError_t layernorm(const void* x, const void* gamma, const void* beta, void* 
 cudaError_t softmax_rows(const void* s_in, void* p_out, int64_t rows, int64_t ncols, int64_t ld, int64_t gstride,
                          int64_t ldo, int64_t gstrideo, int causal, int64_t row_off, int64_t group, int dtype,
                          cudaStream_t s);
+
+// f2 statistics combine (the softmax node of a fused chain), log2 domain: for each of the
+// B1 x M rows, fold the slab statistics (m_s, l_s) at stats[b1*sb1 + s*ss + m]
+// into the row's (m, l) and overwrite every m_s with f_s = 2^(m_s - m) / l
+// (0 for empty slabs).  causal: only the slabs below the row's 128-row tile end
+// (row_off + (m/128 + 1)*128) are read and written - the causal PV reads no others.
+cudaError_t softmax_stats_combine(float2* stats, int64_t B1, int64_t M, int ns, int64_t sb1, int64_t ss, int causal,
+                                  int64_t row_off, cudaStream_t s);
 
 int num_sms();
 

@@ -59,6 +59,11 @@ __device__ __forceinline__ float warp_sum(float v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 // ------------------------------------------------------------------ softmax
 // THREADS threads per row (32 or 256), VPT 16-byte vectors per thread.
@@ -611,7 +616,65 @@ cudaError_t layernorm_dispatch(const void* x, const void* g, const void* b, void
   return cudaGetLastError();
 }
 
+// f2 statistics combine: 32 rows x 8 slab groups per 256-thread block.  The
+// slab statistics are in the log2 domain (m2 = max of s*log2(e), l = sum of
+// 2^(x - m2)).  Thread (g, r) folds slabs s = g, g+8, ... of row r online, the 8
+// partials meet in shared memory in a fixed order, then every slab's m2 is
+// replaced by its factor f_s = 2^(m2_s - M) / L.
+__global__ void __launch_bounds__(256) stats_combine_kernel(float2* __restrict__ st, int64_t B1, int64_t M, int ns,
+                                                           int64_t sb1, int64_t ss, int causal, int64_t row_off) {
+  __shared__ float2 part[8][33];
+  const int r = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 32 + r;
+  const bool valid = row < B1 * M;
+  const int64_t b1 = valid ? row / M : 0, m = valid ? row - b1 * M : 0;
+  int lim = ns;
+  if (causal) {  // slabs the causal PV tile of this row reads (its 128-row tile's key end)
+    const int64_t kend = row_off + (m / 128 + 1) * 128;
+    const int64_t sl = (kend + 63) / 64;
+    if (sl < lim) lim = static_cast<int>(sl);
+  }
+  float2* p = st + b1 * sb1 + m;
+  float mx = -INFINITY, l = 0.f;
+  if (valid)
+    for (int s = g; s < lim; s += 8) {
+      const float2 v = p[s * ss];
+      if (v.x == -INFINITY) continue;
+      if (v.x > mx) {
+        l = l * ex2f(mx - v.x) + v.y;
+        mx = v.x;
+      } else {
+        l += v.y * ex2f(v.x - mx);
+      }
+    }
+  part[g][r] = make_float2(mx, l);
+  __syncthreads();
+  float M_ = -INFINITY;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) M_ = fmaxf(M_, part[q][r].x);
+  float L = 0.f;
+  if (M_ != -INFINITY) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (part[q][r].x != -INFINITY) L += part[q][r].y * ex2f(part[q][r].x - M_);
+  }
+  if (!valid) return;
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  for (int s = g; s < lim; s += 8) {
+    const float ms = p[s * ss].x;
+    p[s * ss].x = (ms == -INFINITY || inv == 0.f) ? 0.f : ex2f(ms - M_) * inv;
+  }
+}
+
 }  // namespace
+
+cudaError_t softmax_stats_combine(float2* stats, int64_t B1, int64_t M, int ns, int64_t sb1, int64_t ss, int causal,
+                                  int64_t row_off, cudaStream_t st) {
+  if (B1 * M <= 0) return cudaSuccess;
+  const int64_t blocks = (B1 * M + 31) / 32;
+  stats_combine_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(stats, B1, M, ns, sb1, ss, causal, row_off);
+  return cudaGetLastError();
+}
 
 cudaError_t softmax_rows(const void* s_in, void* p_out, int64_t rows, int64_t ncols, int64_t ld, int64_t gstride,
                          int64_t ldo, int64_t gstrideo, int causal, int64_t row_off, int64_t group, int dtype,

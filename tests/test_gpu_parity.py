@@ -115,5 +115,34 @@ def test_gpt_full_size_sampled_rows():
     assert err < 2e-2, err
     st = ex.stats()
     assert st.planned_peak < budget
-    # arena high-water + caller-held tensors live at the peak == planned peak (no fragmentation)
-    assert st.workspace_high_water + 2 * 16384 * 1024 * 2 >= st.planned_peak
+    # arena high-water + caller-held tensors live at the peak fit the planned peak (no
+    # fragmentation; with the fused softmax chain P shrinks to its statistics)
+    assert st.workspace_high_water + 2 * 16384 * 1024 * 2 <= st.planned_peak
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_fused_softmax_pv_vs_unfused(monkeypatch, causal):
+    """NEXT f2: scores -> softmax -> PV with the normalisation folded into the PV
+    operand path (AC_FUSE_SOFTMAX=1, default) against the three-kernel path
+    (AC_FUSE_SOFTMAX=0): both within the bf16 tolerance of the oracle, same launch
+    count (the softmax launch becomes the statistics combine), smaller workspace."""
+    gu = _gu()
+    from paper_2401_10652_b200 import api
+    og = workloads.block("transformer", 1024 + 96, 256, 4, 1024, causal, "bf16", name="gpt_small")
+    cg = gu.c_graph(og)
+    vals, dev = gu.make_values(og, 3)
+    ref = executor.run(og, vals)
+    txt = "autochunk-plan 1\nregion s=scores e=pv n=4 dims=0\n"
+    res = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("AC_FUSE_SOFTMAX", flag)
+        plan = api.plan_parse(cg, txt)
+        got, ex = gu.run(cg, plan, og, dev)
+        torch.cuda.synchronize()
+        res[flag] = (got["y"], ex.stats(), plan.workspace_bytes())
+        assert gu.rel_err(got["y"], ref["y"]) < TOL["bf16"], flag
+    (y0, s0, w0), (y1, s1, w1) = res["0"], res["1"]
+    assert s1.launches == s0.launches
+    assert w1 < w0
+    # same bf16 P rounding point, different exp/sum order: close, not bitwise
+    assert gu.rel_err(y1, y0.double().cpu().numpy()) < 1e-2

@@ -1,0 +1,62 @@
+"""compute-sanitizer memcheck over small runs of every kernel path, with the
+PyTorch caching allocator off so each tensor is its own allocation and any
+read or write past a tensor's end is reported (e.g. aux loads of a ragged last
+column tile).  GPU only."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import sys
+sys.path[:0] = [%(root)r, %(root)r + "/tests"]
+import torch
+import gpu_util as gu
+from oracle import workloads
+from paper_2401_10652_b200 import api, kernels as K
+
+torch.manual_seed(0)
+# ragged N (640 = 2.5 x 256-column tiles) with bias + residual: the row epilogue
+M, N, Kd = 300, 640, 256
+a = torch.randn(M, Kd, device="cuda").bfloat16()
+w = torch.randn(N, Kd, device="cuda").bfloat16()
+bias = torch.randn(N, device="cuda").bfloat16()
+res = torch.randn(M, N, device="cuda").bfloat16()
+out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+K.gemm(a, Kd, w, Kd, out, M, N, Kd, out_s=(0, 0, N, 1), bias=bias, act=1, res=res)
+torch.cuda.synchronize()
+for og, txt in [
+    (workloads.block("attn_only", 640, 640, 10, 0, False, "bf16", name="u"),
+     "autochunk-plan 1\nregion s=scores e=pv n=3 dims=0\n"),
+    (workloads.block("transformer", 1024 + 96, 256, 4, 1024, True, "bf16", name="g"),
+     "autochunk-plan 1\nregion s=scores e=pv n=4 dims=0\n"),
+    (workloads.block("transformer", 1024, 256, 4, 1024, True, "bf16", name="g2"),
+     "autochunk-plan 1\nregion s=proj_q e=ffn2 n=4 dims=0\n"),
+    (workloads.tri_attn_pair(48, 128, 4, 32, "bf16", name="af"),
+     "autochunk-plan 1\nregion s=row_scores e=row_pv n=4 dims=0\n"),
+]:
+    cg = gu.c_graph(og)
+    vals, dev = gu.make_values(og, 0)
+    for t in [txt, "autochunk-plan 1\n"]:
+        gu.run(cg, api.plan_parse(cg, t), og, dev)
+        torch.cuda.synchronize()
+print("SANITIZER-RUN-OK")
+"""
+
+
+def test_memcheck_clean(tmp_path):
+    san = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(san):
+        pytest.skip("compute-sanitizer not found")
+    script = tmp_path / "run.py"
+    script.write_text(SCRIPT % {"root": ROOT})
+    env = dict(os.environ, PYTORCH_NO_CUDA_MEMORY_CACHING="1")
+    r = subprocess.run([san, "--tool", "memcheck", "--error-exitcode", "3", "--print-limit", "10",
+                        sys.executable, str(script)], capture_output=True, text=True, env=env, timeout=900)
+    assert r.returncode == 0 and "SANITIZER-RUN-OK" in r.stdout, (r.stdout[-3000:], r.stderr[-3000:])
