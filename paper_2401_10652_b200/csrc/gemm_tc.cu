@@ -16,6 +16,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "epilogue.cuh"
@@ -29,7 +31,6 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, alternating 64-column slabs
-constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr int MAX_MT = 2048;
 
 struct alignas(64) GemmArgs {
@@ -56,16 +57,21 @@ struct alignas(64) GemmArgs {
 // epilogue staging: per epilogue warp a [32 rows][PITCH] fp32 slab; PITCH = 68
 // keeps rows 16-byte aligned (float4 row writes are conflict-free per phase)
 constexpr int PITCH = 68;
-constexpr int EPI_BYTES = EPI_WARPS * 32 * PITCH * 4;
 
-template <int BN>
+template <int BN, int MODE>
 struct Cfg {
-  static constexpr int STAGES = BN >= 256 ? 3 : (BN >= 128 ? 4 : 5);
+  // f2 scores (MODE 1): 16 epilogue warps (one 64-column slab each at BN = 256,
+  // <= 112 registers) with a single 4 KB bf16 staging box per warp; K = head dim
+  // is one or two k-blocks, so two smem stages suffice
+  static constexpr int EPI = MODE == 1 ? 16 : EPI_WARPS;
+  static constexpr int THREADS = 64 + 32 * EPI;
+  static constexpr int EPI_BYTES = MODE == 1 ? EPI * 4096 : EPI_WARPS * 32 * PITCH * 4;
+  static constexpr int STAGES = MODE == 1 ? 2 : (BN >= 256 ? 3 : (BN >= 128 ? 4 : 5));
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int SW = BN >= 64 ? 64 : 32;  // epilogue slab width (columns)
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
-  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * (A_BYTES + B_BYTES) + EPI_BYTES + 256 /*barriers*/ +
+  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * (A_BYTES + B_BYTES) + EPI_BYTES + 512 /*barriers*/ +
                               (MAX_MT + 1) * 4;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
@@ -101,14 +107,14 @@ __device__ __forceinline__ void decode_tile(const GemmArgs& a, const int* prefix
 // lean TMA-store epilogue only); 2 f2 PV (A tile e rescaled to P in shared
 // memory by all epilogue warps, which also run the output epilogue)
 template <int BN, int MODE>
-__global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_constant__ GemmArgs a) {
-  using C = Cfg<BN>;
+__global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(const __grid_constant__ GemmArgs a) {
+  using C = Cfg<BN, MODE>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
   float* sEpi = reinterpret_cast<float*>(sB + C::STAGES * C::B_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES + EPI_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES + C::EPI_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -127,7 +133,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   // --- tile table for causal QK^T: live n-tiles per m-tile, prefix-summed
   int tpb = a.tiles_per_batch_dense;
   if (a.causal_tiles) {
-    for (int mt = threadIdx.x; mt < a.MT; mt += NUM_THREADS) {
+    for (int mt = threadIdx.x; mt < a.MT; mt += C::THREADS) {
       long long maxrow = static_cast<long long>(mt) * BM + BM - 1;
       if (maxrow > a.M - 1) maxrow = a.M - 1;
       const long long lastcol = a.ep.row_off + maxrow - a.ep.col_off;
@@ -165,9 +171,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], EPI_WARPS);
+      ptx::mbar_init(&tempty[s], C::EPI);
     }
-    for (int s = 0; s < C::STAGES && s < 8; ++s) ptx::mbar_init(&ready[s], 32 * EPI_WARPS);
+    for (int s = 0; s < C::STAGES && s < 8; ++s) ptx::mbar_init(&ready[s], 32 * C::EPI);
     for (int q = 0; q < 4; ++q) {
       ptx::mbar_init(&part_full[q], 32 * (ks > 1 ? ks - 1 : 1));
       ptx::mbar_init(&part_empty[q], 32);
@@ -278,7 +284,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             if (kb0 + j < kbn) {
-              const float f = fr[j];
+              const __nv_bfloat162 f2 = __float2bfloat162_rn(fr[j]);
               ptx::mbar_wait(&full[st], ph);
               uint8_t* row = sA + st * C::A_BYTES + r * 128;
 #pragma unroll
@@ -293,9 +299,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
                              : "r"(addr));
                 uint32_t w[4] = {w0, w1, w2, w3};
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const float2 e = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[q]));
-                  __nv_bfloat162 h = __floats2bfloat162_rn(e.x * f, e.y * f);
+                for (int q = 0; q < 4; ++q) {  // P = bf16(e * bf16(f)): one packed multiply per pair
+                  __nv_bfloat162 h = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&w[q]), f2);
                   w[q] = *reinterpret_cast<uint32_t*>(&h);
                 }
                 asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(w[0]), "r"(w[1]),
@@ -419,11 +424,100 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         }
       }
 #pragma unroll 1
-      for (int c = half; c < NSLAB; c += 2) {
-        const bool last = c + 2 >= NSLAB;
+      for (int c = half; c < NSLAB; c += C::EPI / 4) {
+        const bool last = c + C::EPI / 4 >= NSLAB;
         const int n0 = nt * BN + c * SW;
+        if constexpr (MODE == 1) {
+          // ---- f2 scores, one 64-column slab: x = acc * scale * log2(e) (fp32,
+          // scale > 0 so the max is taken on the raw accumulator); the slab max m2,
+          // stored e = bf16(2^(x - m2)), statistics (m2, fp32 sum of e).  Two TMEM
+          // passes (max, then exponentials) keep 32 accumulators live at a time.
+          constexpr float L2E = 1.4426950408889634f;
+          uint8_t* sb = reinterpret_cast<uint8_t*>(sEpi) + ew * 4096;
+          if (lane == 0) ptx::bulk_wait_read<0>();  // previous store has read the staging box
+          __syncwarp();
+          const int m = m0 + lane;
+          const bool mvalid = m < a.M;
+          long long lim = a.ep.causal ? (a.ep.row_off + m - a.ep.col_off - n0) : (1ll << 40);
+          if (lim > a.N - 1 - n0) lim = a.N - 1 - n0;  // columns past N are masked (and clipped by the store)
+          const uint32_t ta = tbase + c * SW;
+          const float cl = a.ep.scale * L2E;
+          uint32_t r[32];
+          float mx = -CUDART_INF_F;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            ptx::tmem_ld32(ta + hh * 32, r);
+            ptx::tmem_ld_wait();
+            float q0 = -CUDART_INF_F, q1 = -CUDART_INF_F, q2 = -CUDART_INF_F, q3 = -CUDART_INF_F;
+            if (lim >= hh * 32 + 31) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                q0 = fmaxf(q0, __uint_as_float(r[j])); q1 = fmaxf(q1, __uint_as_float(r[j + 1]));
+                q2 = fmaxf(q2, __uint_as_float(r[j + 2])); q3 = fmaxf(q3, __uint_as_float(r[j + 3]));
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (hh * 32 + j <= lim) q0 = fmaxf(q0, __uint_as_float(r[j]));
+            }
+            mx = fmaxf(mx, fmaxf(fmaxf(q0, q1), fmaxf(q2, q3)));
+          }
+          const float m2 = mx * cl;
+          const float mref = mx == -CUDART_INF_F ? 0.f : m2;
+          float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            ptx::tmem_ld32(ta + hh * 32, r);
+            ptx::tmem_ld_wait();
+            if (hh == 1 && last) {
+              ptx::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            }
+            uint32_t pk[16];
+            if (lim >= hh * 32 + 31) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const float e0 = ptx::ex2(fmaf(__uint_as_float(r[2 * j]), cl, -mref));
+                const float e1 = ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), cl, -mref));
+                l0 += e0;
+                l1 += e1;
+                __nv_bfloat162 h = __floats2bfloat162_rn(e0, e1);
+                pk[j] = *reinterpret_cast<uint32_t*>(&h);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const float e0 = hh * 32 + 2 * j <= lim ? ptx::ex2(fmaf(__uint_as_float(r[2 * j]), cl, -mref)) : 0.f;
+                const float e1 = hh * 32 + 2 * j + 1 <= lim ? ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), cl, -mref)) : 0.f;
+                l0 += e0;
+                l1 += e1;
+                __nv_bfloat162 h = __floats2bfloat162_rn(e0, e1);
+                pk[j] = *reinterpret_cast<uint32_t*>(&h);
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int ch = hh * 4 + q;
+              const uint32_t addr = ptx::smem_u32(sb + lane * 128 + ((ch ^ (lane & 7)) * 16));
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[4 * q]),
+                           "r"(pk[4 * q + 1]), "r"(pk[4 * q + 2]), "r"(pk[4 * q + 3])
+                           : "memory");
+            }
+          }
+          if (mvalid && n0 < a.N)
+            a.ep.stats[static_cast<long long>(b1) * a.ep.stats_sb1 + static_cast<long long>(n0 / 64) * a.ep.stats_ss +
+                       m] = make_float2(m2, l0 + l1);
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_4d(&a.tout, sb, n0, m0, b1, b2);
+            ptx::bulk_commit();
+          }
+          continue;
+        }
         if constexpr (SW == 64) {
-          if (MODE == 1 || a.tma_store) {
+          if (a.tma_store) {
             // row-oriented path: thread = output row; the epilogue (scale, bias,
             // triangle bias, activation, gate, residual, causal) runs in registers
             // with each thread reading its row's contiguous aux segments, then bf16
@@ -433,7 +527,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
             __syncwarp();
             const int m = m0 + lane;
             const bool mvalid = m < a.M;
-            if (MODE == 1 || a.lean) {
+            if (a.lean) {
               // scale (+ causal) only: both TMEM loads in flight, no aux traffic
               uint32_t r[32], r2[32];
               ptx::tmem_ld32(tbase + c * SW, r);
@@ -447,58 +541,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
               long long lim = a.ep.causal ? (a.ep.row_off + m - a.ep.col_off - n0) : (1ll << 40);
               if (lim > a.N - 1 - n0) lim = a.N - 1 - n0;  // columns past N: masked (clipped by the store)
               uint32_t pk[32];
-              if constexpr (MODE == 1) {
-                // f2 scores: the slab's scores in the log2 domain, x = acc * scale * log2(e)
-                // (scale > 0, so the max is taken on the raw accumulator); stored
-                // e = bf16(2^(x - m2)), statistics (m2 = max x, l = sum of e in fp32)
-                constexpr float L2E = 1.4426950408889634f;
-                const float cl = a.ep.scale * L2E;
-                float v[64];
+              const float sc = a.ep.scale;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                  v[j] = __uint_as_float(r[j]);
-                  v[32 + j] = __uint_as_float(r2[j]);
-                }
-                if (lim < 63) {  // diagonal / ragged slab only
-#pragma unroll
-                  for (int j = 0; j < 64; ++j)
-                    if (j > lim) v[j] = -CUDART_INF_F;
-                }
-                float mx0 = v[0], mx1 = v[1], mx2 = v[2], mx3 = v[3];
-#pragma unroll
-                for (int j = 4; j < 64; j += 4) {
-                  mx0 = fmaxf(mx0, v[j]); mx1 = fmaxf(mx1, v[j + 1]);
-                  mx2 = fmaxf(mx2, v[j + 2]); mx3 = fmaxf(mx3, v[j + 3]);
-                }
-                const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
-                const float m2 = mx * cl;
-                const float mref = mx == -CUDART_INF_F ? 0.f : m2;
-                float l0 = 0.f, l1 = 0.f;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                  const float e0 = ptx::ex2(fmaf(v[2 * j], cl, -mref)), e1 = ptx::ex2(fmaf(v[2 * j + 1], cl, -mref));
-                  l0 += e0;
-                  l1 += e1;
-                  __nv_bfloat162 h = __floats2bfloat162_rn(e0, e1);
-                  pk[j] = *reinterpret_cast<uint32_t*>(&h);
-                }
-                if (mvalid && n0 < a.N)
-                  a.ep.stats[static_cast<long long>(b1) * a.ep.stats_sb1 + static_cast<long long>(n0 / 64) * a.ep.stats_ss +
-                             m] = make_float2(m2, l0 + l1);
-              } else {
-                const float sc = a.ep.scale;
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                  float x0 = __uint_as_float(r[2 * j]) * sc, x1 = __uint_as_float(r[2 * j + 1]) * sc;
-                  float y0 = __uint_as_float(r2[2 * j]) * sc, y1 = __uint_as_float(r2[2 * j + 1]) * sc;
-                  if (2 * j > lim) x0 = -CUDART_INF_F;
-                  if (2 * j + 1 > lim) x1 = -CUDART_INF_F;
-                  if (32 + 2 * j > lim) y0 = -CUDART_INF_F;
-                  if (33 + 2 * j > lim) y1 = -CUDART_INF_F;
-                  __nv_bfloat162 hx = __floats2bfloat162_rn(x0, x1), hy = __floats2bfloat162_rn(y0, y1);
-                  pk[j] = *reinterpret_cast<uint32_t*>(&hx);
-                  pk[16 + j] = *reinterpret_cast<uint32_t*>(&hy);
-                }
+              for (int j = 0; j < 16; ++j) {
+                float x0 = __uint_as_float(r[2 * j]) * sc, x1 = __uint_as_float(r[2 * j + 1]) * sc;
+                float y0 = __uint_as_float(r2[2 * j]) * sc, y1 = __uint_as_float(r2[2 * j + 1]) * sc;
+                if (2 * j > lim) x0 = -CUDART_INF_F;
+                if (2 * j + 1 > lim) x1 = -CUDART_INF_F;
+                if (32 + 2 * j > lim) y0 = -CUDART_INF_F;
+                if (33 + 2 * j > lim) y1 = -CUDART_INF_F;
+                __nv_bfloat162 hx = __floats2bfloat162_rn(x0, x1), hy = __floats2bfloat162_rn(y0, y1);
+                pk[j] = *reinterpret_cast<uint32_t*>(&hx);
+                pk[16 + j] = *reinterpret_cast<uint32_t*>(&hy);
               }
 #pragma unroll
               for (int ch = 0; ch < 8; ++ch) {
@@ -670,7 +724,7 @@ bool make_map(CUtensorMap* m, const Operand& op, int K, int rows, int B1, int B2
 
 template <int BN, int MODE>
 cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, MODE>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -737,12 +791,12 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   if (grid > cap) grid = cap;
   if (grid < a.ks) grid = a.ks;
   if (a.ks == 1) {
-    gemm_tc_kernel<BN, MODE><<<grid, NUM_THREADS, C::SMEM, s>>>(a);
+    gemm_tc_kernel<BN, MODE><<<grid, C::THREADS, C::SMEM, s>>>(a);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.blockDim = dim3(C::THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute lattr[1];

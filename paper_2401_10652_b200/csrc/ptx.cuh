@@ -182,6 +182,13 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x on a bf16x2 pair (one MUFU op for both halves)
+__device__ __forceinline__ uint32_t ex2_bf16x2(uint32_t x) {
+  uint32_t y;
+  asm("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
 __device__ __forceinline__ uint32_t elect_one() {
   uint32_t pred = 0;
   asm volatile(
