@@ -83,6 +83,14 @@ namespace {
 
 bool is_caller(const Graph& g, int t) { return g.is_input[t] || g.is_weight[t] || g.is_output[t]; }
 
+// fixed split-K of the fused PV (AC_PV_SPLITK=1): correct and chunk-invariant but
+// measured slower than one unit per tile (the per-SM streaming rate, not the wave
+// count, bounds the chunked PV), so it is opt-in
+bool pv_splitk() {
+  const char* v = getenv("AC_PV_SPLITK");
+  return v && v[0] == '1';
+}
+
 int region_index(const Plan& plan, int node) {
   for (size_t r = 0; r < plan.regions.size(); ++r)
     if (plan.regions[r].n > 1 && node >= plan.regions[r].start && node <= plan.regions[r].end)
@@ -130,6 +138,31 @@ std::vector<Chain> fused_chains(const Graph& g, const Plan& plan) {
     out.push_back({i, sm, pv});
   }
   return out;
+}
+
+// P's buffer in a fused chain (per launch of B1 heads x M rows x nk keys):
+// [slab statistics, float2 per (b1, 64-key slab, row)] [split-K partials of the
+// PV, fp32 128 x 64 per (tile, granule)] [split-K tile counters, int per tile].
+// The granule is SK_GK k-blocks = 4096 keys at fixed key positions.
+constexpr int SK_GK = 64;
+struct F2Layout {
+  int64_t stats = 0, part = 0, cnt = 0, total = 0;
+  int64_t ncnt = 0;
+};
+// S of a fused chain is stored as pre-swizzled e-tiles (GemmProblem::etile):
+// 16 KB per (head, 128-row tile, 64-key block)
+int64_t etile_bytes(int64_t B1, int64_t M, int64_t nk) { return B1 * ((M + 127) / 128) * ((nk + 63) / 64) * 16384; }
+
+F2Layout f2_layout(int64_t B1, int64_t M, int64_t nk) {
+  F2Layout L;
+  const int64_t ns = (nk + 63) / 64, mt = (M + 127) / 128, ng = pv_splitk() ? (ns + SK_GK - 1) / SK_GK : 1;
+  auto al = [](int64_t v) { return (v + 255) / 256 * 256; };
+  L.stats = 0;
+  L.part = al(B1 * ns * M * 8);
+  L.cnt = L.part + (ng > 1 ? al(B1 * mt * ng * 128 * 64 * 4) : 0);
+  L.ncnt = ng > 1 ? B1 * mt : 0;
+  L.total = L.cnt + al(L.ncnt * 4);
+  return L;
 }
 
 Arena build_arena(const Graph& g, const Plan& plan) {
@@ -183,9 +216,15 @@ Arena build_arena(const Graph& g, const Plan& plan) {
   // softmax statistics (float2 per row and 64-key slab), written by the scores step
   for (const Chain& c : fused_chains(g, plan)) {
     const int s_t = g.nodes[c.scores].output, p_t = g.nodes[c.softmax].output;
-    const int64_t nk = g.tensors[p_t].shape[2];
-    const int64_t rows = bytes[p_t] / (nk * dt_size(g.tensors[p_t].dtype));
-    bytes[p_t] = rows * ((nk + 63) / 64) * 8;
+    std::vector<int64_t> sh = g.tensors[p_t].shape;  // [H, M, nk], chunk-reduced inside a region
+    const int r = region_index(plan, c.softmax);
+    if (r >= 0) {
+      const Region& R = plan.regions[r];
+      const int d = R.dim_of(p_t);
+      if (d >= 0) sh[d] = (sh[d] + R.n - 1) / R.n;
+    }
+    bytes[p_t] = f2_layout(sh[0], sh[1], sh[2]).total;
+    bytes[s_t] = etile_bytes(sh[0], sh[1], sh[2]);
     birth[p_t] = std::min(birth[p_t], c.scores);
     death[s_t] = std::max(death[s_t], c.pv);
   }
@@ -306,8 +345,10 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
     // step left in P's buffer into per-slab factors; the PV applies them
     const View& x = in(0);  // S view [H, M, Nk] of this launch
     const int64_t ns = (x.sh[2] + 63) / 64;
+    const F2Layout L = f2_layout(x.sh[0], x.sh[1], x.sh[2]);
     err = softmax_stats_combine(reinterpret_cast<float2*>(out.p), x.sh[0], x.sh[1], static_cast<int>(ns),
-                                x.sh[1] * ns, x.sh[1], cx.fast ? 1 : 0, cx.row_off, s);
+                                x.sh[1] * ns, x.sh[1], cx.fast ? 1 : 0, cx.row_off,
+                                reinterpret_cast<int*>(out.p + L.cnt), L.ncnt, s);
   } else if (k == "softmax") {
     const View& x = in(0);
     if (n.ai("dim") != x.nd - 1 || x.st[x.nd - 1] != 1) return unsup("softmax over a non-last dim");
@@ -443,6 +484,7 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         // per-(row, 64-key slab) softmax partials into the chain's P buffer
         const int64_t ns = (p.N + 63) / 64;
         ep.stats = reinterpret_cast<float2*>(V[e->fuse_p[i]].p);
+        p.etile = out.p;
         ep.stats_ss = p.M;
         ep.stats_sb1 = static_cast<int64_t>(p.M) * ns;
       }
@@ -468,6 +510,13 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         p.fuse_stats = reinterpret_cast<const float2*>(in(0).p);
         p.fuse_ss = p.M;
         p.fuse_sb1 = static_cast<int64_t>(p.M) * ns;
+        const F2Layout L = f2_layout(p.B1, p.M, p.K);
+        p.etile = pp.p;
+        if (L.ncnt > 0) {
+          p.sk_gk = SK_GK;
+          p.sk_part = reinterpret_cast<float*>(in(0).p + L.part);
+          p.sk_cnt = reinterpret_cast<int*>(in(0).p + L.cnt);
+        }
       }
       // Cluster split-K (ac_gemm_desc.ksplit) exists but measured slower than one
       // CTA per tile for these shapes (DSMEM reduction latency), so it stays off.

@@ -52,6 +52,15 @@ struct alignas(64) GemmArgs {
   int fuse; // fused softmax-normalised A operand (PV of the f2 path)
   const float2* fstats;
   long long fst_sb1, fst_ss;
+  // MODE 2 fixed split-K: K cut into granules of skgk k-blocks at fixed key
+  // positions; one work unit per (tile, granule); multi-granule tiles leave fp32
+  // partials in skpart and the last unit to finish sums them in granule order
+  int skgk, skng;
+  float* skpart;
+  int* skcnt;
+  int dbg;  // experiments (AC_DBG): bit0 = MODE 2 transform skipped
+  char* etile;  // f2 pre-swizzled e tiles (GemmProblem::etile), null = tensor path
+  int e_nkb;    // k-blocks per e-tile row
 };
 
 // epilogue staging: per epilogue warp a [32 rows][PITCH] fp32 slab; PITCH = 68
@@ -64,15 +73,20 @@ struct Cfg {
   // <= 112 registers) with a single 4 KB bf16 staging box per warp; K = head dim
   // is one or two k-blocks, so two smem stages suffice
   static constexpr int EPI = MODE == 1 ? 16 : EPI_WARPS;
-  static constexpr int THREADS = 64 + 32 * EPI;
-  static constexpr int EPI_BYTES = MODE == 1 ? EPI * 4096 : EPI_WARPS * 32 * PITCH * 4;
-  static constexpr int STAGES = MODE == 1 ? 2 : (BN >= 256 ? 3 : (BN >= 128 ? 4 : 5));
+  // f2 PV (MODE 2): the EPI warps transform A tiles; XEPI more warps (one per
+  // TMEM lane quarter) run the output epilogue so the transform never stalls
+  static constexpr int XEPI = MODE == 2 ? 4 : 0;
+  static constexpr int THREADS = 64 + 32 * (EPI + XEPI);
+  // f2 PV (MODE 2) stages no output in smem: its ring is 8 deep (one CTA must keep
+  // ~8 x 24 KB of A/B tiles in flight to stream at full speed when few CTAs remain)
+  static constexpr int EPI_BYTES = MODE == 1 ? EPI * 4096 : MODE == 2 ? 0 : EPI_WARPS * 32 * PITCH * 4;
+  static constexpr int STAGES = MODE == 1 ? 2 : MODE == 2 ? 8 : (BN >= 256 ? 3 : (BN >= 128 ? 4 : 5));
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int SW = BN >= 64 ? 64 : 32;  // epilogue slab width (columns)
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
   static constexpr int SMEM = 1024 /*align slack*/ + STAGES * (A_BYTES + B_BYTES) + EPI_BYTES + 512 /*barriers*/ +
-                              (MAX_MT + 1) * 4;
+                              (MAX_MT + 1) * 4 + 16;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
@@ -103,6 +117,45 @@ __device__ __forceinline__ void decode_tile(const GemmArgs& a, const int* prefix
   kb = (kend + BK - 1) / BK;
 }
 
+// MODE 2 work units: (tile, granule) pairs, tile order as decode_tile (one n-tile,
+// heaviest m-tiles first under causal_k).  prefix[r] = first unit of the r-th
+// tile of a batch (causal_k), else ng = skng units per tile.
+__device__ __forceinline__ void decode_unit(const GemmArgs& a, const int* prefix, int upb, int u, int& b1, int& b2,
+                                            int& mt, int& kbn, int& klo, int& khi, int& g, int& ng, int& tile,
+                                            int& unit0) {
+  const int b = u / upb;
+  const int v = u - b * upb;
+  b1 = b / a.B2;
+  b2 = b - b1 * a.B2;
+  int r;
+  if (a.causal_k) {
+    int lo = 0, hi = a.MT;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (prefix[mid] <= v) lo = mid; else hi = mid;
+    }
+    r = lo;
+    g = v - prefix[r];
+    ng = prefix[r + 1] - prefix[r];
+    mt = a.MT - 1 - r;
+  } else {
+    r = v / a.skng;
+    g = v - r * a.skng;
+    ng = a.skng;
+    mt = r;
+  }
+  int kend = a.K;
+  if (a.causal_k) {
+    const long long e = a.k_row_off + static_cast<long long>(mt + 1) * BM;
+    if (e < kend) kend = static_cast<int>(e);
+  }
+  kbn = (kend + BK - 1) / BK;
+  klo = g * a.skgk;
+  khi = klo + a.skgk < kbn ? klo + a.skgk : kbn;
+  tile = b * a.MT + r;
+  unit0 = u - g;
+}
+
 // MODE: 0 generic; 1 f2 scores (QK^T -> e = exp(s - m_slab) + slab statistics,
 // lean TMA-store epilogue only); 2 f2 PV (A tile e rescaled to P in shared
 // memory by all epilogue warps, which also run the output epilogue)
@@ -119,10 +172,11 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint64_t* part_full = full + 16;   // split-K: leader waits for the other ranks' partials
-  uint64_t* part_empty = full + 20;  // split-K: ranks wait for the leader to have read them
-  uint64_t* ready = full + 24;       // fused softmax: A tile transformed S -> P (<= 5 stages)
-  int* prefix = reinterpret_cast<int*>(full + 32);
+  uint64_t* part_full = tempty + 3;   // split-K: leader waits for the other ranks' partials
+  uint64_t* part_empty = tempty + 7;  // split-K: ranks wait for the leader to have read them
+  uint64_t* ready = tempty + 11;      // fused softmax: A tile transformed S -> P (<= 8 stages)
+  int* prefix = reinterpret_cast<int*>(tempty + 19);  // ends at 2 * STAGES + 21 words <= 512 bytes
+  static_assert(C::STAGES <= 8, "barrier block layout");
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -160,6 +214,27 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
     __syncthreads();
     tpb = prefix[a.MT];
   }
+  if constexpr (MODE == 2) {
+    // units per batch: granules of every m-tile (prefix over the heaviest-first order)
+    if (a.causal_k) {
+      for (int r = threadIdx.x; r < a.MT; r += C::THREADS) {
+        const int mt = a.MT - 1 - r;
+        long long kend = a.k_row_off + static_cast<long long>(mt + 1) * BM;
+        if (kend > a.K) kend = a.K;
+        const int kbn = static_cast<int>((kend + BK - 1) / BK);
+        prefix[r + 1] = (kbn + a.skgk - 1) / a.skgk;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        prefix[0] = 0;
+        for (int r = 0; r < a.MT; ++r) prefix[r + 1] += prefix[r];
+      }
+      __syncthreads();
+      tpb = prefix[a.MT];
+    } else {
+      tpb = a.MT * a.skng;
+    }
+  }
   const int total = tpb * a.B1 * a.B2;
 
   if (warp == 0 && lane == 0) {
@@ -171,9 +246,9 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], C::EPI);
+      ptx::mbar_init(&tempty[s], MODE == 2 ? C::XEPI : C::EPI);
     }
-    for (int s = 0; s < C::STAGES && s < 8; ++s) ptx::mbar_init(&ready[s], 32 * C::EPI);
+    for (int s = 0; s < C::STAGES; ++s) ptx::mbar_init(&ready[s], 32 * C::EPI);
     for (int q = 0; q < 4; ++q) {
       ptx::mbar_init(&part_full[q], 32 * (ks > 1 ? ks - 1 : 1));
       ptx::mbar_init(&part_empty[q], 32);
@@ -193,15 +268,27 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cid; t < total; t += ncl) {
-        int b1, b2, mt, nt, kbn;
-        decode_tile(a, prefix, tpb, t, b1, b2, mt, nt, kbn);
+        int b1, b2, mt, nt = 0, kbn, klo, khi;
+        if constexpr (MODE == 2) {
+          int g, ng, tile, unit0;
+          decode_unit(a, prefix, tpb, t, b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0);
+        } else {
+          decode_tile(a, prefix, tpb, t, b1, b2, mt, nt, kbn);
+          klo = kbn * static_cast<int>(crank) / ks;
+          khi = kbn * (static_cast<int>(crank) + 1) / ks;
+        }
         const int ac2 = a.a_b1 ? b1 : 0, ac3 = a.a_b2 ? b2 : 0;
         const int bc2 = a.b_b1 ? b1 : 0, bc3 = a.b_b2 ? b2 : 0;
-        const int klo = kbn * static_cast<int>(crank) / ks, khi = kbn * (static_cast<int>(crank) + 1) / ks;
+        const char* esrc = MODE == 2 && a.etile
+                               ? a.etile + (static_cast<long long>(b1 * a.B2 + b2) * a.MT + mt) * a.e_nkb * 16384
+                               : nullptr;
         for (int kb = klo; kb < khi; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
-          ptx::tma_load_4d(sA + stage * C::A_BYTES, &a.ta, &full[stage], kb * BK, mt * BM, ac2, ac3);
+          if (MODE == 2 && esrc)
+            ptx::bulk_load(sA + stage * C::A_BYTES, esrc + static_cast<long long>(kb) * 16384, C::A_BYTES, &full[stage]);
+          else
+            ptx::tma_load_4d(sA + stage * C::A_BYTES, &a.ta, &full[stage], kb * BK, mt * BM, ac2, ac3);
           ptx::tma_load_4d(sB + stage * C::B_BYTES, &a.tb, &full[stage], kb * BK, nt * BN, bc2, bc3);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -215,12 +302,18 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
     int acc = 0;
     uint32_t aphase = 0;
     for (int t = cid; t < total; t += ncl) {
-      int b1, b2, mt, nt, kbn;
-      decode_tile(a, prefix, tpb, t, b1, b2, mt, nt, kbn);
+      int b1, b2, mt, nt = 0, kbn, klo, khi;
+      if constexpr (MODE == 2) {
+        int g, ng, tile, unit0;
+        decode_unit(a, prefix, tpb, t, b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0);
+      } else {
+        decode_tile(a, prefix, tpb, t, b1, b2, mt, nt, kbn);
+        klo = kbn * static_cast<int>(crank) / ks;
+        khi = kbn * (static_cast<int>(crank) + 1) / ks;
+      }
       ptx::mbar_wait(&tempty[acc], aphase ^ 1);
       ptx::tc_fence_after();
       const uint32_t d = tmem_base + acc * BN;
-      const int klo = kbn * static_cast<int>(crank) / ks, khi = kbn * (static_cast<int>(crank) + 1) / ks;
       for (int kb = klo; kb < khi; ++kb) {
         ptx::mbar_wait(MODE == 2 ? &ready[stage] : &full[stage], phase);
         ptx::tc_fence_after();
@@ -229,8 +322,9 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
           const uint32_t sb = ptx::smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            ptx::mma_bf16(d, ptx::sdesc_sw128(sa + k * 32), ptx::sdesc_sw128(sb + k * 32), IDESC,
-                          (kb != klo || k != 0) ? 1u : 0u);
+            if (MODE != 2 || !(a.dbg & 4))
+              ptx::mma_bf16(d, ptx::sdesc_sw128(sa + k * 32), ptx::sdesc_sw128(sb + k * 32), IDESC,
+                            (kb != klo || k != 0) ? 1u : 0u);
           }
           ptx::mma_commit(&empty[stage]);  // slot free once these MMAs have read smem
         }
@@ -258,85 +352,144 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
     uint32_t aphase = 0;
     uint32_t pf_phase = 0, pe_phase = 0;  // split-K barrier phases
     if constexpr (MODE == 2) {
-      // ---- f2 PV: thread = A-tile row (TMEM lane quarter x lane), half = which
-      // four of the row's eight 16-byte chunks.  Rescale the stored
-      // e = exp(s - m_slab) in place to P = e * f_slab, f_slab = exp(m_slab - m_row)
-      // / l_row left in the statistics by the combine step (prefetched 8 slabs
-      // ahead); keys >= K are TMA zero-fill (e = 0), rows past M get f = 0.  After
-      // the tile's last k-block the same warps run the output epilogue.
-      const int r = quarter * 32 + lane;
-      int st = 0;
-      uint32_t ph = 0;
-      for (int t = cid; t < total; t += ncl) {
-        int b1, b2, mt, nt, kbn;
-        decode_tile(a, prefix, tpb, t, b1, b2, mt, nt, kbn);
-        const int m = mt * BM + r;
-        const bool mv = m < a.M;
-        const float* fp = reinterpret_cast<const float*>(a.fstats + static_cast<long long>(b1) * a.fst_sb1 + (mv ? m : 0));
-        const long long fs = 2 * a.fst_ss;
-        float fr[8];
+      if (ew < C::EPI) {
+        // ---- f2 PV transform warps: thread = A-tile row (TMEM lane quarter x
+        // lane), half = which four of the row's eight 16-byte chunks.  Rescale the
+        // stored e = 2^(x - m2_slab) in place to P = e * f_slab (f_slab left in the
+        // statistics by the combine step, prefetched 8 slabs ahead); keys >= K are
+        // TMA zero-fill (e = 0), rows past M get f = 0.
+        const int r = quarter * 32 + lane;
+        int st = 0;
+        uint32_t ph = 0;
+        for (int t = cid; t < total; t += ncl) {
+          int b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0;
+          decode_unit(a, prefix, tpb, t, b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0);
+          const int m = mt * BM + r;
+          const bool mv = m < a.M;
+          const float* fp = reinterpret_cast<const float*>(a.fstats + static_cast<long long>(b1) * a.fst_sb1 + (mv ? m : 0));
+          const long long fs = 2 * a.fst_ss;
+          float fr[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) fr[j] = (mv && j < kbn) ? __ldg(fp + j * fs) : 0.f;
-        for (int kb0 = 0; kb0 < kbn; kb0 += 8) {
-          float nx[8];
+          for (int j = 0; j < 8; ++j) fr[j] = (mv && klo + j < khi) ? __ldg(fp + (klo + j) * fs) : 0.f;
+          for (int kb0 = klo; kb0 < khi; kb0 += 8) {
+            float nx[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) nx[j] = (mv && kb0 + 8 + j < kbn) ? __ldg(fp + (kb0 + 8 + j) * fs) : 0.f;
+            for (int j = 0; j < 8; ++j) nx[j] = (mv && kb0 + 8 + j < khi) ? __ldg(fp + (kb0 + 8 + j) * fs) : 0.f;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (kb0 + j < kbn) {
-              const __nv_bfloat162 f2 = __float2bfloat162_rn(fr[j]);
-              ptx::mbar_wait(&full[st], ph);
-              uint8_t* row = sA + st * C::A_BYTES + r * 128;
+            for (int j = 0; j < 8; ++j) {
+              if (kb0 + j < khi) {
+                const __nv_bfloat162 f2 = __float2bfloat162_rn(fr[j]);
+                ptx::mbar_wait(&full[st], ph);
+                uint8_t* row = sA + st * C::A_BYTES + r * 128;
 #pragma unroll
-              for (int q4 = 0; q4 < 4; ++q4) {
-                // same factor for every element: walk physical chunks in swizzled
-                // order so 8 consecutive rows hit all 32 banks
-                const int ch = half * 4 + q4;
-                const uint32_t addr = ptx::smem_u32(row + ((ch ^ (r & 7)) * 16));
-                uint32_t w0, w1, w2, w3;
-                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                             : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
-                             : "r"(addr));
-                uint32_t w[4] = {w0, w1, w2, w3};
+                for (int q4 = 0; q4 < ((a.dbg & 1) ? 0 : 4); ++q4) {
+                  // same factor for every element: walk physical chunks in swizzled
+                  // order so 8 consecutive rows hit all 32 banks
+                  const int ch = half * 4 + q4;
+                  const uint32_t addr = ptx::smem_u32(row + ((ch ^ (r & 7)) * 16));
+                  uint32_t w0, w1, w2, w3;
+                  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                               : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                               : "r"(addr));
+                  uint32_t w[4] = {w0, w1, w2, w3};
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {  // P = bf16(e * bf16(f)): one packed multiply per pair
-                  __nv_bfloat162 h = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&w[q]), f2);
-                  w[q] = *reinterpret_cast<uint32_t*>(&h);
+                  for (int q = 0; q < 4; ++q) {  // P = bf16(e * bf16(f)): one packed multiply per pair
+                    __nv_bfloat162 h = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&w[q]), f2);
+                    w[q] = *reinterpret_cast<uint32_t*>(&h);
+                  }
+                  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(w[0]), "r"(w[1]),
+                               "r"(w[2]), "r"(w[3])
+                               : "memory");
                 }
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(w[0]), "r"(w[1]),
-                             "r"(w[2]), "r"(w[3])
-                             : "memory");
+                if (!(a.dbg & 2)) ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+                ptx::mbar_arrive(&ready[st]);
+                if (++st == C::STAGES) { st = 0; ph ^= 1; }
               }
-              ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
-              ptx::mbar_arrive(&ready[st]);
-              if (++st == C::STAGES) { st = 0; ph ^= 1; }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) fr[j] = nx[j];
+          }
+        }
+      } else {
+        // ---- f2 PV output warps (one per TMEM lane quarter, all 64 columns): the
+        // unit's accumulator -> bf16 output (single-granule tile) or an fp32
+        // partial; the unit that completes a multi-granule tile sums the partials
+        // in granule order (fixed split-K, the same arithmetic however the units
+        // were scheduled or the rows chunked)
+        const int r = quarter * 32 + lane;
+        int* sk_old = prefix + MAX_MT + 1;  // counter value seen by this CTA (broadcast)
+        for (int t = cid; t < total; t += ncl) {
+          int b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0;
+          decode_unit(a, prefix, tpb, t, b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0);
+          const int m = mt * BM + r;
+          const bool mv = m < a.M;
+          ptx::mbar_wait(&tfull[acc], aphase);
+          ptx::tc_fence_after();
+          uint32_t rr[64];
+          {
+            uint32_t (&lo)[32] = *reinterpret_cast<uint32_t(*)[32]>(&rr[0]);
+            uint32_t (&hi)[32] = *reinterpret_cast<uint32_t(*)[32]>(&rr[32]);
+            const uint32_t tb = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
+            ptx::tmem_ld32(tb, lo);
+            ptx::tmem_ld32(tb + 32, hi);
+          }
+          ptx::tmem_ld_wait();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+          if (++acc == 2) { acc = 0; aphase ^= 1; }
+          if (ng > 1) {
+            float* mine = a.skpart + (static_cast<long long>(unit0 + g) * BM + r) * BN;
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              reinterpret_cast<float4*>(mine)[q] = make_float4(__uint_as_float(rr[4 * q]), __uint_as_float(rr[4 * q + 1]),
+                                                               __uint_as_float(rr[4 * q + 2]), __uint_as_float(rr[4 * q + 3]));
+            __threadfence();
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (ew == C::EPI && lane == 0) *sk_old = atomicAdd(a.skcnt + tile, 1);
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const int old = *sk_old;
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // sk_old reusable
+            if (old != ng - 1) continue;
+            __threadfence();
+            const float4* base = reinterpret_cast<const float4*>(a.skpart + (static_cast<long long>(unit0) * BM + r) * BN);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const float4 v = __ldcg(base + q);
+              rr[4 * q] = __float_as_uint(v.x); rr[4 * q + 1] = __float_as_uint(v.y);
+              rr[4 * q + 2] = __float_as_uint(v.z); rr[4 * q + 3] = __float_as_uint(v.w);
+            }
+            for (int gg = 1; gg < ng; ++gg) {
+              const float4* pp = base + static_cast<long long>(gg) * BM * BN / 4;
+#pragma unroll
+              for (int q = 0; q < 16; ++q) {
+                const float4 v = __ldcg(pp + q);
+                rr[4 * q] = __float_as_uint(__uint_as_float(rr[4 * q]) + v.x);
+                rr[4 * q + 1] = __float_as_uint(__uint_as_float(rr[4 * q + 1]) + v.y);
+                rr[4 * q + 2] = __float_as_uint(__uint_as_float(rr[4 * q + 2]) + v.z);
+                rr[4 * q + 3] = __float_as_uint(__uint_as_float(rr[4 * q + 3]) + v.w);
+              }
+            }
+            if (ew == C::EPI && lane == 0) a.skcnt[tile] = 0;  // ready for the next launch
+          }
+          if (mv) {
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const int n = hh * 32;
+              if (n >= a.N) break;
+              uint32_t pk[16];
+              epilogue_row32(a.ep, b1, b2, m, n, true, *reinterpret_cast<const uint32_t(*)[32]>(&rr[hh * 32]), pk,
+                             a.N - n);
+              uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.ep.out) +
+                                                  static_cast<long long>(b1) * a.ep.out_sb1 +
+                                                  static_cast<long long>(b2) * a.ep.out_sb2 +
+                                                  static_cast<long long>(m) * a.ep.out_sm + n);
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (8 * q < a.N - n) o[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
             }
           }
-#pragma unroll
-          for (int j = 0; j < 8; ++j) fr[j] = nx[j];
         }
-        // output epilogue: this thread's row, columns half*32 .. +31
-        ptx::mbar_wait(&tfull[acc], aphase);
-        ptx::tc_fence_after();
-        uint32_t rr[32];
-        ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + half * 32, rr);
-        ptx::tmem_ld_wait();
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-        const int n = nt * BN + half * 32;
-        if (mv && n < a.N) {
-          uint32_t pk[16];
-          epilogue_row32(a.ep, b1, b2, m, n, true, rr, pk, a.N - n);
-          uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.ep.out) +
-                                              static_cast<long long>(b1) * a.ep.out_sb1 +
-                                              static_cast<long long>(b2) * a.ep.out_sb2 +
-                                              static_cast<long long>(m) * a.ep.out_sm + n);
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (8 * q < a.N - n) o[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-        }
-        if (++acc == 2) { acc = 0; aphase ^= 1; }
       }
     } else
     for (int t = cid; t < total; t += ncl) {
@@ -511,7 +664,14 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            ptx::tma_store_4d(&a.tout, sb, n0, m0, b1, b2);
+            if (a.etile) {
+              // (slabs past N would land in the next tile row: not stored)
+              char* dst = a.etile + ((static_cast<long long>(b1 * a.B2 + b2) * a.MT + mt) * a.e_nkb + n0 / 64) * 16384 +
+                          quarter * 4096;
+              if (n0 < a.N) ptx::bulk_store(dst, sb, 4096);
+            } else {
+              ptx::tma_store_4d(&a.tout, sb, n0, m0, b1, b2);
+            }
             ptx::bulk_commit();
           }
           continue;
@@ -733,7 +893,12 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   }
   GemmArgs a;
   memset(&a, 0, sizeof(a));
-  if (!make_map(&a.ta, p.A, p.K, p.a_rows_total ? p.a_rows_total : p.M, p.B1, p.B2, BM)) return cudaErrorInvalidValue;
+  if (!(MODE == 2 && p.etile) &&
+      !make_map(&a.ta, p.A, p.K, p.a_rows_total ? p.a_rows_total : p.M, p.B1, p.B2, BM))
+    return cudaErrorInvalidValue;
+  a.etile = static_cast<char*>(p.etile);
+  a.e_nkb = MODE == 1 ? (p.N + 63) / 64 : (p.K + 63) / 64;
+  if (p.etile && (reinterpret_cast<uintptr_t>(p.etile) & 127)) return cudaErrorInvalidValue;
   if (!make_map(&a.tb, p.B, p.K, p.b_rows_total ? p.b_rows_total : p.N, p.B1, p.B2, BN)) return cudaErrorInvalidValue;
   a.ep = p.ep;
   a.M = p.M; a.N = p.N; a.K = p.K; a.B1 = p.B1; a.B2 = p.B2;
@@ -780,14 +945,38 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   if (MODE == 1 && !(a.tma_store && a.lean && p.ep.scale > 0.f)) return cudaErrorInvalidValue;
   if (MODE == 2 && !(BN == 64 && a.vec)) return cudaErrorInvalidValue;
   a.fuse = MODE == 2 ? 1 : 0;
+  if (MODE == 2) {
+    const int kbn = (p.K + BK - 1) / BK;
+    if (p.sk_part && p.sk_gk > 0 && a.NT == 1) {
+      a.skgk = p.sk_gk;
+      a.skpart = p.sk_part;
+      a.skcnt = p.sk_cnt;
+    } else {
+      a.skgk = kbn;  // one unit per tile
+    }
+    a.skng = (kbn + a.skgk - 1) / a.skgk;
+    if (a.skng > 1 && !a.skcnt) return cudaErrorInvalidValue;
+    if (p.causal_k && a.MT > MAX_MT) return cudaErrorInvalidValue;
+  }
   a.fstats = p.fuse_stats;
   a.fst_sb1 = p.fuse_sb1;
   a.fst_ss = p.fuse_ss;
   a.ks = (MODE == 0 && BN == 64 && a.vec && p.ksplit > 1) ? (p.ksplit > 8 ? 8 : p.ksplit) : 1;
   if (a.ks > 1) a.tma_store = 0;
   const int sms = num_sms();
-  int grid = a.total_tiles_dense * a.ks;
-  const int cap = (sms / a.ks) * a.ks;
+  int grid = a.total_tiles_dense * a.ks * (MODE == 2 ? a.skng : 1);
+  int cap = (sms / a.ks) * a.ks;
+  {
+    static int dbg = -1, dgrid = -1;
+    if (dbg < 0) {
+      const char* v = getenv("AC_DBG");
+      dbg = v ? atoi(v) : 0;
+      v = getenv("AC_DBG_GRID");
+      dgrid = v ? atoi(v) : 0;
+    }
+    a.dbg = dbg;
+    if (MODE == 2 && dgrid > 0 && dgrid < cap) cap = dgrid;
+  }
   if (grid > cap) grid = cap;
   if (grid < a.ks) grid = a.ks;
   if (a.ks == 1) {

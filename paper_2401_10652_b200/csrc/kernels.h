@@ -66,13 +66,29 @@ struct GemmProblem {
   // fp32 partials through distributed shared memory in rank order (deterministic;
   // the split depends only on the tile's K range, never on the chunking)
   int ksplit = 1;
-  // fused softmax-normalised PV (NEXT f2): A holds e = exp(s - m_slab) written by
-  // the QK^T epilogue (Epilogue::stats); each 128 x 64 A tile (one slab) is
-  // rescaled in shared memory to P = e * exp(m_slab - m_row) / l_row (row (m, l)
-  // combined from the slab statistics over the tile's key range) before the MMA
-  // reads it, so P is never written to HBM.  BN = 64 only; layout as Epilogue::stats.
+  // fused softmax-normalised PV (NEXT f2): A holds e = 2^(x - m2_slab) written by
+  // the QK^T epilogue (Epilogue::stats); fuse_stats holds, per (b1, slab, row),
+  // the factor f = 2^(m2_slab - m2_row) / l_row in .x (softmax_stats_combine);
+  // each 128 x 64 A tile (one slab) is rescaled in shared memory to P = e * f
+  // before the MMA reads it, so P is never written to HBM.  BN = 64 only.
   const float2* fuse_stats = nullptr;
   int64_t fuse_sb1 = 0, fuse_ss = 0;
+  // fixed split-K of the fused PV (SURVEY H-g): the key range is cut into
+  // granules of sk_gk k-blocks at fixed key positions (0 = off); one work unit
+  // per (tile, granule) balances the waves, multi-granule tiles leave fp32 partials
+  // (BM x 64 per unit) in sk_part and the unit that completes a tile sums them in
+  // granule order, so the result does not depend on the scheduling or chunking.
+  // sk_cnt: one zero-initialised int per tile (B1*B2*MT), left zero on return.
+  int sk_gk = 0;
+  float* sk_part = nullptr;
+  int* sk_cnt = nullptr;
+  // f2 e-tiles: e = 2^(x - m2) stored as pre-swizzled 16 KB tiles, tile
+  // (b1, mt, kb) = the 128-row x 64-key block exactly as the 128B-swizzled UMMA
+  // operand sits in shared memory, at etile + ((b1 * MT + mt) * NKB + kb) * 16384
+  // (MT = ceil(M / 128), NKB = ceil(keys / 64)).  The QK^T (Epilogue::stats set)
+  // writes it with 4 KB bulk stores instead of its output tensor; the PV
+  // (fuse_stats set) reads its A operand from it with 16 KB bulk loads.
+  void* etile = nullptr;
 };
 
 // bf16 x bf16 -> fp32 (TMEM) -> bf16, tcgen05 + TMA, sm_100a.  Returns a
@@ -100,8 +116,9 @@ cudaError_t softmax_rows(const void* s_in, void* p_out, int64_t rows, int64_t nc
 // into the row's (m, l) and overwrite every m_s with f_s = 2^(m_s - m) / l
 // (0 for empty slabs).  causal: only the slabs below the row's 128-row tile end
 // (row_off + (m/128 + 1)*128) are read and written - the causal PV reads no others.
+// Also zeroes zero[0 .. nzero) (the split-K tile counters of the PV that follows).
 cudaError_t softmax_stats_combine(float2* stats, int64_t B1, int64_t M, int ns, int64_t sb1, int64_t ss, int causal,
-                                  int64_t row_off, cudaStream_t s);
+                                  int64_t row_off, int* zero, int64_t nzero, cudaStream_t s);
 
 int num_sms();
 

@@ -622,8 +622,11 @@ cudaError_t layernorm_dispatch(const void* x, const void* g, const void* b, void
 // partials meet in shared memory in a fixed order, then every slab's m2 is
 // replaced by its factor f_s = 2^(m2_s - M) / L.
 __global__ void __launch_bounds__(256) stats_combine_kernel(float2* __restrict__ st, int64_t B1, int64_t M, int ns,
-                                                           int64_t sb1, int64_t ss, int causal, int64_t row_off) {
+                                                           int64_t sb1, int64_t ss, int causal, int64_t row_off,
+                                                           int* __restrict__ zero, int64_t nzero) {
   __shared__ float2 part[8][33];
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x; i < nzero; i += static_cast<int64_t>(gridDim.x) * 256)
+    zero[i] = 0;  // split-K tile counters of the PV that follows
   const int r = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * 32 + r;
   const bool valid = row < B1 * M;
@@ -669,10 +672,11 @@ __global__ void __launch_bounds__(256) stats_combine_kernel(float2* __restrict__
 }  // namespace
 
 cudaError_t softmax_stats_combine(float2* stats, int64_t B1, int64_t M, int ns, int64_t sb1, int64_t ss, int causal,
-                                  int64_t row_off, cudaStream_t st) {
+                                  int64_t row_off, int* zero, int64_t nzero, cudaStream_t st) {
   if (B1 * M <= 0) return cudaSuccess;
   const int64_t blocks = (B1 * M + 31) / 32;
-  stats_combine_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(stats, B1, M, ns, sb1, ss, causal, row_off);
+  stats_combine_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(stats, B1, M, ns, sb1, ss, causal, row_off,
+                                                                      zero, nzero);
   return cudaGetLastError();
 }
 
