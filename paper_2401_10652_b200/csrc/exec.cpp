@@ -69,6 +69,7 @@ struct ac_exec {
   // (not launched), 3 PV (normalises S in smem); fuse_s / fuse_p: the chain's S and P tensors
   std::vector<char> fuse_role;
   std::vector<int> fuse_s, fuse_p;
+  std::vector<char> fuse_split;        // per node of a fused chain: PV fixed split-K on
   mutable ac_run_stats stats{};
   // profiling: event pairs per launch of the last run
   bool profiling = false;
@@ -83,12 +84,15 @@ namespace {
 
 bool is_caller(const Graph& g, int t) { return g.is_input[t] || g.is_weight[t] || g.is_output[t]; }
 
-// fixed split-K of the fused PV (AC_PV_SPLITK=1): correct and chunk-invariant but
-// measured slower than one unit per tile (the per-SM streaming rate, not the wave
-// count, bounds the chunked PV), so it is opt-in
-bool pv_splitk() {
+// Fixed split-K of the fused PV: on for non-causal chains (uniform tiles, where
+// quarter-tile units taken dynamically shorten the last wave: UNet PV 1.70 -> 1.39 ms),
+// off for causal ones (heaviest-first whole tiles already balance; the partials
+// cost more than they save).  The choice depends only on the graph, never on the
+// chunking, so chunked == unchunked bitwise either way.  AC_PV_SPLITK=0/1 forces it.
+bool pv_splitk(bool causal, int64_t nk) {
   const char* v = getenv("AC_PV_SPLITK");
-  return v && v[0] == '1';
+  if (v && (v[0] == '0' || v[0] == '1')) return v[0] == '1';
+  return !causal && nk >= 4096;  // short rows: one unit per tile is cheaper
 }
 
 int region_index(const Plan& plan, int node) {
@@ -143,24 +147,28 @@ std::vector<Chain> fused_chains(const Graph& g, const Plan& plan) {
 // P's buffer in a fused chain (per launch of B1 heads x M rows x nk keys):
 // [slab statistics, float2 per (b1, 64-key slab, row)] [split-K partials of the
 // PV, fp32 128 x 64 per (tile, granule)] [split-K tile counters, int per tile].
-// The granule is SK_GK k-blocks = 4096 keys at fixed key positions.
-constexpr int SK_GK = 64;
+// The key range is cut into SK_NG granules of sk_gk(nk) k-blocks at fixed key
+// positions (a function of the key count only, so chunk-invariant): four units
+// per tile balance the waves while the fp32 partials stay < 1 % of the e traffic.
+constexpr int SK_NG = 4;
+int64_t sk_gk(int64_t nk) { return ((nk + 63) / 64 + SK_NG - 1) / SK_NG; }
 struct F2Layout {
-  int64_t stats = 0, part = 0, cnt = 0, total = 0;
+  int64_t stats = 0, rowst = 0, part = 0, cnt = 0, total = 0;
   int64_t ncnt = 0;
 };
 // S of a fused chain is stored as pre-swizzled e-tiles (GemmProblem::etile):
 // 16 KB per (head, 128-row tile, 64-key block)
 int64_t etile_bytes(int64_t B1, int64_t M, int64_t nk) { return B1 * ((M + 127) / 128) * ((nk + 63) / 64) * 16384; }
 
-F2Layout f2_layout(int64_t B1, int64_t M, int64_t nk) {
+F2Layout f2_layout(int64_t B1, int64_t M, int64_t nk, bool split) {
   F2Layout L;
-  const int64_t ns = (nk + 63) / 64, mt = (M + 127) / 128, ng = pv_splitk() ? (ns + SK_GK - 1) / SK_GK : 1;
+  const int64_t ns = (nk + 63) / 64, mt = (M + 127) / 128, ng = split ? (ns + sk_gk(nk) - 1) / sk_gk(nk) : 1;
   auto al = [](int64_t v) { return (v + 255) / 256 * 256; };
   L.stats = 0;
-  L.part = al(B1 * ns * M * 8);
+  L.rowst = al(B1 * ns * M * 8);
+  L.part = L.rowst + al(B1 * M * 8);
   L.cnt = L.part + (ng > 1 ? al(B1 * mt * ng * 128 * 64 * 4) : 0);
-  L.ncnt = ng > 1 ? B1 * mt : 0;
+  L.ncnt = 1 + (ng > 1 ? B1 * mt : 0);  // [0]: dynamic unit counter, then one per tile
   L.total = L.cnt + al(L.ncnt * 4);
   return L;
 }
@@ -223,7 +231,7 @@ Arena build_arena(const Graph& g, const Plan& plan) {
       const int d = R.dim_of(p_t);
       if (d >= 0) sh[d] = (sh[d] + R.n - 1) / R.n;
     }
-    bytes[p_t] = f2_layout(sh[0], sh[1], sh[2]).total;
+    bytes[p_t] = f2_layout(sh[0], sh[1], sh[2], pv_splitk(g.nodes[c.scores].ai("causal") != 0, sh[2])).total;
     bytes[s_t] = etile_bytes(sh[0], sh[1], sh[2]);
     birth[p_t] = std::min(birth[p_t], c.scores);
     death[s_t] = std::max(death[s_t], c.pv);
@@ -345,10 +353,11 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
     // step left in P's buffer into per-slab factors; the PV applies them
     const View& x = in(0);  // S view [H, M, Nk] of this launch
     const int64_t ns = (x.sh[2] + 63) / 64;
-    const F2Layout L = f2_layout(x.sh[0], x.sh[1], x.sh[2]);
+    const F2Layout L = f2_layout(x.sh[0], x.sh[1], x.sh[2], e->fuse_split[i] != 0);
     err = softmax_stats_combine(reinterpret_cast<float2*>(out.p), x.sh[0], x.sh[1], static_cast<int>(ns),
                                 x.sh[1] * ns, x.sh[1], cx.fast ? 1 : 0, cx.row_off,
-                                reinterpret_cast<int*>(out.p + L.cnt), L.ncnt, s);
+                                reinterpret_cast<float2*>(out.p + L.rowst), reinterpret_cast<int*>(out.p + L.cnt),
+                                L.ncnt, s);
   } else if (k == "softmax") {
     const View& x = in(0);
     if (n.ai("dim") != x.nd - 1 || x.st[x.nd - 1] != 1) return unsup("softmax over a non-last dim");
@@ -510,12 +519,14 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         p.fuse_stats = reinterpret_cast<const float2*>(in(0).p);
         p.fuse_ss = p.M;
         p.fuse_sb1 = static_cast<int64_t>(p.M) * ns;
-        const F2Layout L = f2_layout(p.B1, p.M, p.K);
+        const F2Layout L = f2_layout(p.B1, p.M, p.K, e->fuse_split[i] != 0);
         p.etile = pp.p;
-        if (L.ncnt > 0) {
-          p.sk_gk = SK_GK;
+        p.sched = reinterpret_cast<int*>(in(0).p + L.cnt);
+        p.fuse_rowst = reinterpret_cast<const float2*>(in(0).p + L.rowst);
+        if (L.ncnt > 1) {
+          p.sk_gk = static_cast<int>(sk_gk(p.K));
           p.sk_part = reinterpret_cast<float*>(in(0).p + L.part);
-          p.sk_cnt = reinterpret_cast<int*>(in(0).p + L.cnt);
+          p.sk_cnt = reinterpret_cast<int*>(in(0).p + L.cnt) + 1;
         }
       }
       // Cluster split-K (ac_gemm_desc.ksplit) exists but measured slower than one
@@ -675,15 +686,19 @@ ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_
   e->fuse_role.assign(S, 0);
   e->fuse_s.assign(S, -1);
   e->fuse_p.assign(S, -1);
+  e->fuse_split.assign(S, 0);
   if (e->dt == DT::BF16) {
     for (const Chain& c : fused_chains(g, e->plan)) {
       e->fuse_role[c.scores] = 1;
       e->fuse_role[c.softmax] = 2;
       e->fuse_role[c.pv] = 3;
       const int s_t = g.nodes[c.scores].output, p_t = g.nodes[c.softmax].output;
+      const bool split =
+          pv_splitk(g.nodes[c.scores].ai("causal") != 0, g.tensors[g.nodes[c.softmax].output].shape[2]);
       for (int node : {c.scores, c.softmax, c.pv}) {
         e->fuse_s[node] = s_t;
         e->fuse_p[node] = p_t;
+        e->fuse_split[node] = split ? 1 : 0;
       }
     }
   }

@@ -16,7 +16,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 #include <cstring>
 #include <mutex>
 
@@ -51,6 +53,7 @@ struct alignas(64) GemmArgs {
   int lean; // TMA-store epilogue without aux tensors / activation (scale and causal only)
   int fuse; // fused softmax-normalised A operand (PV of the f2 path)
   const float2* fstats;
+  const float2* frow;  // MODE 2: (M, 1/L) per (b1, row)
   long long fst_sb1, fst_ss;
   // MODE 2 fixed split-K: K cut into granules of skgk k-blocks at fixed key
   // positions; one work unit per (tile, granule); multi-granule tiles leave fp32
@@ -59,6 +62,8 @@ struct alignas(64) GemmArgs {
   float* skpart;
   int* skcnt;
   int dbg;  // experiments (AC_DBG): bit0 = MODE 2 transform skipped
+  int* sched;  // MODE 2: zero-initialised work counter for dynamic unit scheduling (null = round-robin)
+  unsigned long long* trace;  // debug (AC_TRACE): per unit {cta, t_load0, t_tfull, t_done}
   char* etile;  // f2 pre-swizzled e tiles (GemmProblem::etile), null = tensor path
   int e_nkb;    // k-blocks per e-tile row
 };
@@ -175,7 +180,13 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
   uint64_t* part_full = tempty + 3;   // split-K: leader waits for the other ranks' partials
   uint64_t* part_empty = tempty + 7;  // split-K: ranks wait for the leader to have read them
   uint64_t* ready = tempty + 11;      // fused softmax: A tile transformed S -> P (<= 8 stages)
-  int* prefix = reinterpret_cast<int*>(tempty + 19);  // ends at 2 * STAGES + 21 words <= 512 bytes
+  // MODE 2 unit queue: the producer picks the next work unit (dynamically from the
+  // sched counter when given, else round-robin) and hands it to the other roles
+  // through a 4-deep ring (uq_full: 1 arrival, uq_empty: one per consuming warp)
+  uint64_t* uq_full = tempty + 19;
+  uint64_t* uq_empty = tempty + 23;
+  int* uq_slot = reinterpret_cast<int*>(tempty + 27);
+  int* prefix = reinterpret_cast<int*>(tempty + 29);  // ends at 2 * STAGES + 31 words <= 512 bytes
   static_assert(C::STAGES <= 8, "barrier block layout");
 
   const int warp = threadIdx.x >> 5;
@@ -249,6 +260,10 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
       ptx::mbar_init(&tempty[s], MODE == 2 ? C::XEPI : C::EPI);
     }
     for (int s = 0; s < C::STAGES; ++s) ptx::mbar_init(&ready[s], 32 * C::EPI);
+    for (int s = 0; s < 4; ++s) {
+      ptx::mbar_init(&uq_full[s], 1);
+      ptx::mbar_init(&uq_empty[s], 1 + C::EPI + C::XEPI);
+    }
     for (int q = 0; q < 4; ++q) {
       ptx::mbar_init(&part_full[q], 32 * (ks > 1 ? ks - 1 : 1));
       ptx::mbar_init(&part_empty[q], 32);
@@ -261,13 +276,39 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
   if (ks > 1) ptx::cluster_sync();  // remote barriers initialised before any remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // unit sequence of this CTA: i-th unit (static round-robin, or the MODE 2 queue)
+  auto produce = [&](int i) -> int {  // producer lane only
+    if constexpr (MODE == 2) {
+      const int sl = i & 3;
+      int u = a.sched ? atomicAdd(a.sched, 1) : cid + i * ncl;
+      if (u > total) u = total;
+      ptx::mbar_wait(&uq_empty[sl], ((i >> 2) & 1) ^ 1);
+      *reinterpret_cast<volatile int*>(&uq_slot[sl]) = u;
+      ptx::mbar_arrive(&uq_full[sl]);
+      return u;
+    } else {
+      return cid + i * ncl;
+    }
+  };
+  auto take = [&](int i) -> int {  // whole consuming warp
+    if constexpr (MODE == 2) {
+      const int sl = i & 3;
+      ptx::mbar_wait(&uq_full[sl], (i >> 2) & 1);
+      const int u = *reinterpret_cast<volatile int*>(&uq_slot[sl]);
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(&uq_empty[sl]);
+      return u;
+    } else {
+      return cid + i * ncl;
+    }
+  };
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cid; t < total; t += ncl) {
+      for (int i = 0, t = produce(0); t < total; t = produce(++i)) {
         int b1, b2, mt, nt = 0, kbn, klo, khi;
         if constexpr (MODE == 2) {
           int g, ng, tile, unit0;
@@ -279,6 +320,12 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
         }
         const int ac2 = a.a_b1 ? b1 : 0, ac3 = a.a_b2 ? b2 : 0;
         const int bc2 = a.b_b1 ? b1 : 0, bc3 = a.b_b2 ? b2 : 0;
+        if (MODE == 2 && a.trace) {
+          unsigned long long tnow;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+          a.trace[4 * t] = blockIdx.x;
+          a.trace[4 * t + 1] = tnow;
+        }
         const char* esrc = MODE == 2 && a.etile
                                ? a.etile + (static_cast<long long>(b1 * a.B2 + b2) * a.MT + mt) * a.e_nkb * 16384
                                : nullptr;
@@ -301,7 +348,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
     uint32_t phase = 0;
     int acc = 0;
     uint32_t aphase = 0;
-    for (int t = cid; t < total; t += ncl) {
+    for (int i = 0, t = take(0); t < total; t = take(++i)) {
       int b1, b2, mt, nt = 0, kbn, klo, khi;
       if constexpr (MODE == 2) {
         int g, ng, tile, unit0;
@@ -361,24 +408,26 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
         const int r = quarter * 32 + lane;
         int st = 0;
         uint32_t ph = 0;
-        for (int t = cid; t < total; t += ncl) {
+        for (int i = 0, t = take(0); t < total; t = take(++i)) {
           int b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0;
           decode_unit(a, prefix, tpb, t, b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0);
           const int m = mt * BM + r;
           const bool mv = m < a.M;
           const float* fp = reinterpret_cast<const float*>(a.fstats + static_cast<long long>(b1) * a.fst_sb1 + (mv ? m : 0));
           const long long fs = 2 * a.fst_ss;
+          const float2 rs = mv ? __ldg(a.frow + static_cast<long long>(b1) * a.M + m) : make_float2(0.f, 0.f);
           float fr[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) fr[j] = (mv && klo + j < khi) ? __ldg(fp + (klo + j) * fs) : 0.f;
+          for (int j = 0; j < 8; ++j) fr[j] = (mv && klo + j < khi) ? __ldg(fp + (klo + j) * fs) : -CUDART_INF_F;
           for (int kb0 = klo; kb0 < khi; kb0 += 8) {
             float nx[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) nx[j] = (mv && kb0 + 8 + j < khi) ? __ldg(fp + (kb0 + 8 + j) * fs) : 0.f;
+            for (int j = 0; j < 8; ++j) nx[j] = (mv && kb0 + 8 + j < khi) ? __ldg(fp + (kb0 + 8 + j) * fs) : -CUDART_INF_F;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               if (kb0 + j < khi) {
-                const __nv_bfloat162 f2 = __float2bfloat162_rn(fr[j]);
+                // f = 2^(m2_slab - M) / L (an empty slab has m2 = -inf: f = 0)
+                const __nv_bfloat162 f2 = __float2bfloat162_rn(ptx::ex2(fr[j] - rs.x) * rs.y);
                 ptx::mbar_wait(&full[st], ph);
                 uint8_t* row = sA + st * C::A_BYTES + r * 128;
 #pragma unroll
@@ -418,13 +467,18 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
         // were scheduled or the rows chunked)
         const int r = quarter * 32 + lane;
         int* sk_old = prefix + MAX_MT + 1;  // counter value seen by this CTA (broadcast)
-        for (int t = cid; t < total; t += ncl) {
+        for (int i = 0, t = take(0); t < total; t = take(++i)) {
           int b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0;
           decode_unit(a, prefix, tpb, t, b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0);
           const int m = mt * BM + r;
           const bool mv = m < a.M;
           ptx::mbar_wait(&tfull[acc], aphase);
           ptx::tc_fence_after();
+          if (a.trace && ew == C::EPI && lane == 0) {
+            unsigned long long tnow;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+            a.trace[4 * t + 2] = tnow;
+          }
           uint32_t rr[64];
           {
             uint32_t (&lo)[32] = *reinterpret_cast<uint32_t(*)[32]>(&rr[0]);
@@ -488,6 +542,11 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
               for (int q = 0; q < 4; ++q)
                 if (8 * q < a.N - n) o[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
             }
+          }
+          if (a.trace && ew == C::EPI && lane == 0) {
+            unsigned long long tnow;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+            a.trace[4 * t + 3] = tnow;
           }
         }
       }
@@ -897,6 +956,7 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
       !make_map(&a.ta, p.A, p.K, p.a_rows_total ? p.a_rows_total : p.M, p.B1, p.B2, BM))
     return cudaErrorInvalidValue;
   a.etile = static_cast<char*>(p.etile);
+  a.sched = MODE == 2 ? p.sched : nullptr;
   a.e_nkb = MODE == 1 ? (p.N + 63) / 64 : (p.K + 63) / 64;
   if (p.etile && (reinterpret_cast<uintptr_t>(p.etile) & 127)) return cudaErrorInvalidValue;
   if (!make_map(&a.tb, p.B, p.K, p.b_rows_total ? p.b_rows_total : p.N, p.B1, p.B2, BN)) return cudaErrorInvalidValue;
@@ -961,6 +1021,8 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   a.fstats = p.fuse_stats;
   a.fst_sb1 = p.fuse_sb1;
   a.fst_ss = p.fuse_ss;
+  a.frow = p.fuse_rowst;
+  if (MODE == 2 && !a.frow) return cudaErrorInvalidValue;
   a.ks = (MODE == 0 && BN == 64 && a.vec && p.ksplit > 1) ? (p.ksplit > 8 ? 8 : p.ksplit) : 1;
   if (a.ks > 1) a.tma_store = 0;
   const int sms = num_sms();
@@ -977,10 +1039,33 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
     a.dbg = dbg;
     if (MODE == 2 && dgrid > 0 && dgrid < cap) cap = dgrid;
   }
+  static int trace_on = -1;
+  static unsigned long long* trace_buf = nullptr;
+  static int trace_launch = 0;
+  const long long trace_units = static_cast<long long>(a.total_tiles_dense) * (MODE == 2 ? a.skng : 1);
+  if (trace_on < 0) trace_on = getenv("AC_TRACE") ? 1 : 0;
+  if (MODE == 2 && trace_on) {
+    if (!trace_buf) cudaMalloc(&trace_buf, 8 << 20);
+    if (trace_units * 4 * 8 <= (8 << 20)) {
+      cudaMemsetAsync(trace_buf, 0, trace_units * 32, s);
+      a.trace = trace_buf;
+    }
+  }
   if (grid > cap) grid = cap;
   if (grid < a.ks) grid = a.ks;
   if (a.ks == 1) {
     gemm_tc_kernel<BN, MODE><<<grid, C::THREADS, C::SMEM, s>>>(a);
+    if (a.trace) {  // debug only: dump {cta, t_load0, t_tfull, t_done} per unit
+      std::vector<unsigned long long> h(trace_units * 4);
+      cudaMemcpy(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost);
+      char fn[256];
+      snprintf(fn, sizeof fn, "%s/trace_%03d.txt", getenv("AC_TRACE"), trace_launch++);
+      if (FILE* f = fopen(fn, "w")) {
+        for (long long u = 0; u < trace_units; ++u)
+          fprintf(f, "%lld %llu %llu %llu %llu\n", u, h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]);
+        fclose(f);
+      }
+    }
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};

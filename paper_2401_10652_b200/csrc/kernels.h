@@ -67,12 +67,13 @@ struct GemmProblem {
   // the split depends only on the tile's K range, never on the chunking)
   int ksplit = 1;
   // fused softmax-normalised PV (NEXT f2): A holds e = 2^(x - m2_slab) written by
-  // the QK^T epilogue (Epilogue::stats); fuse_stats holds, per (b1, slab, row),
-  // the factor f = 2^(m2_slab - m2_row) / l_row in .x (softmax_stats_combine);
-  // each 128 x 64 A tile (one slab) is rescaled in shared memory to P = e * f
-  // before the MMA reads it, so P is never written to HBM.  BN = 64 only.
+  // the QK^T epilogue (Epilogue::stats, same layout in fuse_stats); fuse_rowst
+  // holds (M, 1/L) per (b1, row) (softmax_stats_combine); each 128 x 64 A tile
+  // (one slab) is rescaled in shared memory to P = e * 2^(m2_slab - M) / L before
+  // the MMA reads it, so P is never written to HBM.  BN = 64 only.
   const float2* fuse_stats = nullptr;
   int64_t fuse_sb1 = 0, fuse_ss = 0;
+  const float2* fuse_rowst = nullptr;
   // fixed split-K of the fused PV (SURVEY H-g): the key range is cut into
   // granules of sk_gk k-blocks at fixed key positions (0 = off); one work unit
   // per (tile, granule) balances the waves, multi-granule tiles leave fp32 partials
@@ -89,6 +90,9 @@ struct GemmProblem {
   // writes it with 4 KB bulk stores instead of its output tensor; the PV
   // (fuse_stats set) reads its A operand from it with 16 KB bulk loads.
   void* etile = nullptr;
+  // f2 PV: zero-initialised int; CTAs take work units from it dynamically (faster
+  // SMs take more), null = static round-robin.  Results do not depend on it.
+  int* sched = nullptr;
 };
 
 // bf16 x bf16 -> fp32 (TMEM) -> bf16, tcgen05 + TMA, sm_100a.  Returns a
@@ -112,13 +116,13 @@ cudaError_t softmax_rows(const void* s_in, void* p_out, int64_t rows, int64_t nc
                          cudaStream_t s);
 
 // f2 statistics combine (the softmax node of a fused chain), log2 domain: for each of the
-// B1 x M rows, fold the slab statistics (m_s, l_s) at stats[b1*sb1 + s*ss + m]
-// into the row's (m, l) and overwrite every m_s with f_s = 2^(m_s - m) / l
-// (0 for empty slabs).  causal: only the slabs below the row's 128-row tile end
-// (row_off + (m/128 + 1)*128) are read and written - the causal PV reads no others.
-// Also zeroes zero[0 .. nzero) (the split-K tile counters of the PV that follows).
+// B1 x M rows, fold the slab statistics (m2_s, l_s) at stats[b1*sb1 + s*ss + m]
+// into the row's (M, L) and write rowst[b1*M + m] = (M, 1/L) (1/L = 0 for an
+// empty row).  causal: only the slabs below the row's 128-row tile end
+// (row_off + (m/128 + 1)*128) are read - the causal PV reads no others.
+// Also zeroes zero[0 .. nzero) (the PV's unit counter and split-K tile counters).
 cudaError_t softmax_stats_combine(float2* stats, int64_t B1, int64_t M, int ns, int64_t sb1, int64_t ss, int causal,
-                                  int64_t row_off, int* zero, int64_t nzero, cudaStream_t s);
+                                  int64_t row_off, float2* rowst, int* zero, int64_t nzero, cudaStream_t s);
 
 int num_sms();
 

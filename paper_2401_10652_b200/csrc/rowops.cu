@@ -619,11 +619,12 @@ cudaError_t layernorm_dispatch(const void* x, const void* g, const void* b, void
 // f2 statistics combine: 32 rows x 8 slab groups per 256-thread block.  The
 // slab statistics are in the log2 domain (m2 = max of s*log2(e), l = sum of
 // 2^(x - m2)).  Thread (g, r) folds slabs s = g, g+8, ... of row r online, the 8
-// partials meet in shared memory in a fixed order, then every slab's m2 is
-// replaced by its factor f_s = 2^(m2_s - M) / L.
+// partials meet in shared memory in a fixed order and the row's (M, 1/L) is
+// written to rowst (one pass over the slab statistics, which stay as they are).
 __global__ void __launch_bounds__(256) stats_combine_kernel(float2* __restrict__ st, int64_t B1, int64_t M, int ns,
                                                            int64_t sb1, int64_t ss, int causal, int64_t row_off,
-                                                           int* __restrict__ zero, int64_t nzero) {
+                                                           float2* __restrict__ rowst, int* __restrict__ zero,
+                                                           int64_t nzero) {
   __shared__ float2 part[8][33];
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x; i < nzero; i += static_cast<int64_t>(gridDim.x) * 256)
     zero[i] = 0;  // split-K tile counters of the PV that follows
@@ -661,22 +662,19 @@ __global__ void __launch_bounds__(256) stats_combine_kernel(float2* __restrict__
     for (int q = 0; q < 8; ++q)
       if (part[q][r].x != -INFINITY) L += part[q][r].y * ex2f(part[q][r].x - M_);
   }
-  if (!valid) return;
-  const float inv = L > 0.f ? 1.f / L : 0.f;
-  for (int s = g; s < lim; s += 8) {
-    const float ms = p[s * ss].x;
-    p[s * ss].x = (ms == -INFINITY || inv == 0.f) ? 0.f : ex2f(ms - M_) * inv;
-  }
+  if (!valid || g != 0) return;
+  // the PV forms f_s = 2^(m2_s - M) / L itself from (M, 1/L)
+  rowst[b1 * M + m] = make_float2(M_ == -INFINITY ? 0.f : M_, L > 0.f ? 1.f / L : 0.f);
 }
 
 }  // namespace
 
 cudaError_t softmax_stats_combine(float2* stats, int64_t B1, int64_t M, int ns, int64_t sb1, int64_t ss, int causal,
-                                  int64_t row_off, int* zero, int64_t nzero, cudaStream_t st) {
+                                  int64_t row_off, float2* rowst, int* zero, int64_t nzero, cudaStream_t st) {
   if (B1 * M <= 0) return cudaSuccess;
   const int64_t blocks = (B1 * M + 31) / 32;
   stats_combine_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(stats, B1, M, ns, sb1, ss, causal, row_off,
-                                                                      zero, nzero);
+                                                                      rowst, zero, nzero);
   return cudaGetLastError();
 }
 

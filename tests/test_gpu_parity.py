@@ -150,11 +150,11 @@ def test_fused_softmax_pv_vs_unfused(monkeypatch, causal):
 
 @pytest.mark.parametrize("split", ["0", "1"])
 def test_fused_pv_split_k_chunk_invariant(monkeypatch, split):
-    """Fixed split-K of the fused PV (AC_PV_SPLITK=1, keys cut at 4096-key
-    granules): bf16 tolerance vs the oracle and chunked == unchunked bitwise at
-    4608 keys (2 granules), causal and not."""
+    """Fixed split-K of the fused PV (AC_PV_SPLITK=1 forces it on, 0 off; keys cut
+    into 4 granules at fixed positions): bf16 tolerance vs the oracle and chunked ==
+    unchunked bitwise, causal and not."""
     monkeypatch.setenv("AC_PV_SPLITK", split)
     for causal in (True, False):
-        og = workloads.block("attn_only", 4608, 256, 4, 0, causal, "bf16", name="pv_split")
+        og = workloads.block("attn_only", 2048 + 320, 256, 4, 0, causal, "bf16", name="pv_split")
         _check_all_plans(og, ["autochunk-plan 1\nregion s=scores e=pv n=4 dims=0\n",
                               "autochunk-plan 1\nregion s=scores e=pv n=3 dims=0\n"], seed=5)
