@@ -391,10 +391,13 @@ def main():
             if need + (1 << 30) < free:
                 wsu = torch.empty(need, dtype=torch.uint8, device="cuda")
                 exu = api.Exec(up, wsu, comm)
-                tu, _ = timed(exu, ins, outs, max(3, args.steps // 2), 2)
-                vu = units * max(3, args.steps // 2) / (tu / 1e3)
-                unchunked = {"value": vu, "ms_per_step": tu / max(3, args.steps // 2),
-                             "speed_loss": 1.0 - value / vu, "workspace_bytes": need}
+                ku = max(3, args.steps // 2)
+                tu, ktu = timed(exu, ins, outs, ku, 2, profile=True)
+                vu = units * ku / (tu / 1e3)
+                unchunked = {"value": vu, "ms_per_step": tu / ku,
+                             "speed_loss": 1.0 - value / vu, "workspace_bytes": need,
+                             "stages_ms": {k: round(v[1] / ku, 4) for k, v in
+                                           sorted(ktu.items(), key=lambda kv: -kv[1][1])}}
                 del exu, wsu
             else:
                 unchunked = {"value": None, "speed_loss": None, "note": f"unchunked OOM (needs {need} B)"}

@@ -26,11 +26,17 @@ __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return
 // Branch-free erf for the GELU epilogue: erfc(|z|) = t exp(-z^2 + P(t)),
 // t = 1 / (1 + |z|/2) (Chebyshev fit, Numerical Recipes 6.2; fractional error of
 // erfc < 1.2e-7), so |erf error| < 1.2e-7 everywhere — below fp32 GELU rounding
-// at the bf16 / fp32 outputs.  One MUFU reciprocal + one MUFU exp, no branches
+// at the bf16 / fp32 outputs (rcp.approx adds < 2 ulp).  One MUFU reciprocal + one MUFU exp, no branches
 // (CUDA's erff has a data-dependent branch that serialises the epilogue).
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ float erf_fast(float z) {
   const float a = fabsf(z);
-  const float t = __frcp_rn(fmaf(0.5f, a, 1.f));
+  const float t = rcp_approx(fmaf(0.5f, a, 1.f));  // MUFU.RCP, 1 ulp (the IEEE __frcp_rn is a slow sequence)
   float p = fmaf(t, 0.17087277f, -0.82215223f);
   p = fmaf(t, p, 1.48851587f);
   p = fmaf(t, p, -1.13520398f);
@@ -46,7 +52,7 @@ __device__ __forceinline__ float erf_fast(float z) {
 
 __device__ __forceinline__ float act_apply(int act, float v) {
   if (act == ACT_GELU) return 0.5f * v * (1.f + erf_fast(v * 0.70710678118654752f));
-  if (act == ACT_SIGMOID) return __frcp_rn(1.f + __expf(-v));
+  if (act == ACT_SIGMOID) return rcp_approx(1.f + __expf(-v));
   if (act == ACT_RELU) return fmaxf(v, 0.f);
   return v;
 }

@@ -132,6 +132,16 @@ struct TileWalk {
     return a.causal_tiles ? prefix[m + 1] : start + a.NT;
   }
   __device__ __forceinline__ void next(const GemmArgs& a, const int* prefix, int tpb, int t, int ncl) {
+    if (!a.causal_tiles) {
+      // dense tiles: direct decode (stepping m-tile by m-tile costs ncl / NT
+      // iterations per tile, 148 for a one-n-tile GEMM)
+      b = t / tpb;
+      r = t - b * tpb;
+      mt = r / a.NT;
+      lo = mt * a.NT;
+      hi = lo + a.NT;
+      return;
+    }
     if (!started) {
       started = true;
       b = t / tpb;
