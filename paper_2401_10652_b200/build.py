@@ -70,6 +70,8 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
     inc = ["-I" + CSRC, "-I" + os.path.join(ROOT, "include")]
     ninc = _nccl_include()
     defs = []
+    if os.environ.get("AC_DEBUG_HANG"):
+        defs.append("-DAC_DEBUG_HANG=1")
     if ninc:
         inc.append("-I" + ninc)
         defs.append("-DAC_HAVE_NCCL_H=1")

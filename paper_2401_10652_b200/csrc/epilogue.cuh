@@ -50,6 +50,23 @@ __device__ __forceinline__ float erf_fast(float z) {
   return copysignf(1.f - erfc, z);
 }
 
+// Activation over an array with the kind test hoisted out of the element loop: a
+// per-element branch puts every element in its own reconvergence region and
+// serialises the otherwise independent erf chains (measured 2x on FFN1).
+template <int NE>
+__device__ __forceinline__ void act_array(int act, float (&x)[NE]) {
+  if (act == ACT_GELU) {
+#pragma unroll
+    for (int j = 0; j < NE; ++j) x[j] = 0.5f * x[j] * (1.f + erf_fast(x[j] * 0.70710678118654752f));
+  } else if (act == ACT_SIGMOID) {
+#pragma unroll
+    for (int j = 0; j < NE; ++j) x[j] = rcp_approx(1.f + __expf(-x[j]));
+  } else if (act == ACT_RELU) {
+#pragma unroll
+    for (int j = 0; j < NE; ++j) x[j] = fmaxf(x[j], 0.f);
+  }
+}
+
 __device__ __forceinline__ float act_apply(int act, float v) {
   if (act == ACT_GELU) return 0.5f * v * (1.f + erf_fast(v * 0.70710678118654752f));
   if (act == ACT_SIGMOID) return rcp_approx(1.f + __expf(-v));
@@ -141,10 +158,7 @@ __device__ __forceinline__ void epilogue8(const Epilogue& ep, int b1, int b2, in
       for (int i = 0; i < 8; ++i) x[i] += a[i];
     }
   }
-  if (ep.act != ACT_NONE) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = act_apply(ep.act, x[i]);
-  }
+  act_array(ep.act, x);
   if (ep.gate) {
     const int64_t o = static_cast<int64_t>(b1) * ep.gate_sb1 + static_cast<int64_t>(b2) * ep.gate_sb2 +
                       static_cast<int64_t>(m) * ep.gate_sm + n;
@@ -210,10 +224,7 @@ __device__ __forceinline__ void epilogue8p(const Epilogue& ep, int b1, int b2, i
 #pragma unroll
     for (int i = 0; i < 8; ++i) x[i] += ep.bias_along_m ? aux.bias_m : bias_n[i];
   }
-  if (ep.act != ACT_NONE) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = act_apply(ep.act, x[i]);
-  }
+  act_array(ep.act, x);
   if (ep.gate) {
     bf16x8_to_f(aux.gate, a);
 #pragma unroll
@@ -282,10 +293,7 @@ __device__ __forceinline__ void epilogue_row32(const Epilogue& ep, int b1, int b
       for (int j = 0; j < 32; ++j) x[j] += a[j];
     }
   }
-  if (ep.act != ACT_NONE) {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = act_apply(ep.act, x[j]);
-  }
+  act_array(ep.act, x);
   if (ep.gate && mvalid) {
     load32_bf16(static_cast<const __nv_bfloat16*>(ep.gate) + static_cast<int64_t>(b1) * ep.gate_sb1 +
                     static_cast<int64_t>(b2) * ep.gate_sb2 + static_cast<int64_t>(m) * ep.gate_sm + n,

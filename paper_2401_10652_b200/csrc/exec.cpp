@@ -116,18 +116,23 @@ std::vector<Chain> fused_chains(const Graph& g, const Plan& plan) {
   if (env && env[0] == '0') return out;
   for (int i = 0; i < static_cast<int>(g.nodes.size()); ++i) {
     const Node& n = g.nodes[i];
-    if (n.kind != "attn_scores") continue;
+    // attn_scores [H, M, nk] -> softmax -> attn_pv, or the AlphaFold triangle chain
+    // tri_scores [B1, H, M, nk] (+ bias) -> softmax -> tri_pv (gated)
+    const bool tri = n.kind == "tri_scores";
+    if (n.kind != "attn_scores" && !tri) continue;
     const int s_t = n.output;
+    const int kd = static_cast<int>(g.tensors[s_t].shape.size()) - 1;  // key dim of S
     if (g.tensors[s_t].dtype != DT::BF16 || g.is_output[s_t] || g.consumers[s_t].size() != 1) continue;
     const int sm = g.consumers[s_t][0];
-    if (g.nodes[sm].kind != "softmax" || g.nodes[sm].ai("dim") != 2) continue;
+    if (g.nodes[sm].kind != "softmax" || g.nodes[sm].ai("dim") != kd) continue;
     const int p_t = g.nodes[sm].output;
     if (g.is_output[p_t] || g.consumers[p_t].size() != 1) continue;
     const int pv = g.consumers[p_t][0];
-    if (g.nodes[pv].kind != "attn_pv" || g.nodes[pv].inputs[0] != p_t) continue;
-    // PV on the BN = 64 tile (32 < head dim <= 64); scores on the lean TMA-store path
-    const int64_t dh = g.tensors[g.nodes[pv].output].shape[2], nk = g.tensors[s_t].shape[2];
-    if (dh <= 32 || dh > 64 || nk < 64 || nk % 8 != 0) continue;
+    if (g.nodes[pv].kind != (tri ? "tri_pv" : "attn_pv") || g.nodes[pv].inputs[0] != p_t) continue;
+    // PV on the BN = 32 / 64 tile (head dim <= 64); scores on the TMA-store path
+    const std::vector<int64_t>& osh = g.tensors[g.nodes[pv].output].shape;
+    const int64_t dh = osh.back(), nk = g.tensors[s_t].shape[kd];
+    if (dh > 64 || dh % 8 != 0 || nk < 64 || nk % 8 != 0) continue;
     const int ri = region_index(plan, i), rs = region_index(plan, sm), rp = region_index(plan, pv);
     if (ri != rs || rs != rp) continue;
     if (ri >= 0) {
@@ -135,9 +140,9 @@ std::vector<Chain> fused_chains(const Graph& g, const Plan& plan) {
       bool hoisted = false;
       for (int h : R.hoisted) hoisted = hoisted || h == i || h == sm || h == pv;
       if (hoisted) continue;
-      // S and P must be chunked along the same dim (heads or query rows), never keys
+      // S and P must be chunked along the same dim (batch, heads or query rows), never keys
       const int ds = R.dim_of(s_t), dp = R.dim_of(p_t);
-      if (ds != dp || ds == 2) continue;
+      if (ds != dp || ds == kd) continue;
     }
     out.push_back({i, sm, pv});
   }
@@ -224,15 +229,18 @@ Arena build_arena(const Graph& g, const Plan& plan) {
   // softmax statistics (float2 per row and 64-key slab), written by the scores step
   for (const Chain& c : fused_chains(g, plan)) {
     const int s_t = g.nodes[c.scores].output, p_t = g.nodes[c.softmax].output;
-    std::vector<int64_t> sh = g.tensors[p_t].shape;  // [H, M, nk], chunk-reduced inside a region
+    std::vector<int64_t> sh = g.tensors[p_t].shape;  // [(B1,) H, M, nk], chunk-reduced inside a region
     const int r = region_index(plan, c.softmax);
     if (r >= 0) {
       const Region& R = plan.regions[r];
       const int d = R.dim_of(p_t);
       if (d >= 0) sh[d] = (sh[d] + R.n - 1) / R.n;
     }
-    bytes[p_t] = f2_layout(sh[0], sh[1], sh[2], pv_splitk(g.nodes[c.scores].ai("causal") != 0, sh[2])).total;
-    bytes[s_t] = etile_bytes(sh[0], sh[1], sh[2]);
+    int64_t B = 1;
+    for (size_t d = 0; d + 2 < sh.size(); ++d) B *= sh[d];
+    const int64_t M = sh[sh.size() - 2], nk = sh.back();
+    bytes[p_t] = f2_layout(B, M, nk, pv_splitk(g.nodes[c.scores].ai("causal") != 0, nk)).total;
+    bytes[s_t] = etile_bytes(B, M, nk);
     birth[p_t] = std::min(birth[p_t], c.scores);
     death[s_t] = std::max(death[s_t], c.pv);
   }
@@ -351,11 +359,12 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
   } else if (k == "softmax" && e->fuse_role[i] == 2) {
     // fused chain: the softmax node only combines the slab statistics the scores
     // step left in P's buffer into per-slab factors; the PV applies them
-    const View& x = in(0);  // S view [H, M, Nk] of this launch
-    const int64_t ns = (x.sh[2] + 63) / 64;
-    const F2Layout L = f2_layout(x.sh[0], x.sh[1], x.sh[2], e->fuse_split[i] != 0);
-    err = softmax_stats_combine(reinterpret_cast<float2*>(out.p), x.sh[0], x.sh[1], static_cast<int>(ns),
-                                x.sh[1] * ns, x.sh[1], cx.fast ? 1 : 0, cx.row_off,
+    const View& x = in(0);  // S view [(B1,) H, M, Nk] of this launch
+    const int64_t B = extent(x, 0, x.nd - 2), M = x.sh[x.nd - 2], nk = x.sh[x.nd - 1];
+    const int64_t ns = (nk + 63) / 64;
+    const F2Layout L = f2_layout(B, M, nk, e->fuse_split[i] != 0);
+    err = softmax_stats_combine(reinterpret_cast<float2*>(out.p), B, M, static_cast<int>(ns),
+                                M * ns, M, cx.fast ? 1 : 0, cx.row_off,
                                 reinterpret_cast<float2*>(out.p + L.rowst), reinterpret_cast<int*>(out.p + L.cnt),
                                 L.ncnt, s);
   } else if (k == "softmax") {
@@ -557,8 +566,17 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         ep.add_sm = b.st[1]; ep.add_sn = b.st[2];  // bT[h, i, k]
       }
       p.A.use_b1 = p.A.use_b2 = p.B.use_b1 = p.B.use_b2 = 1;
+      if (e->fuse_role[i] == 1) {
+        // fused chain: e-tiles into S's buffer, slab statistics into P's, batch = (b1, h)
+        const int64_t ns = (p.N + 63) / 64;
+        ep.stats = reinterpret_cast<float2*>(V[e->fuse_p[i]].p);
+        p.etile = out.p;
+        ep.stats_ss = p.M;
+        ep.stats_sb1 = static_cast<int64_t>(p.M) * ns;
+      }
     } else if (k == "tri_pv") {
-      const View &pp = in(0), &vt = in(1), &gt = in(2);
+      const bool fz = e->fuse_role[i] == 3;
+      const View &pp = fz ? V[e->fuse_s[i]] : in(0), &vt = in(1), &gt = in(2);
       const bool end = n.ai("ending") != 0;
       if (pp.st[3] != 1 || vt.st[3] != 1) return unsup("key dim not contiguous");
       p.B1 = static_cast<int>(pp.sh[0]);
@@ -576,6 +594,21 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
       } else {     // o[i,j,h,c]: b1=j, b2=h, m=i
         ep.out_sb1 = out.st[1]; ep.out_sb2 = out.st[2]; ep.out_sm = out.st[0]; ep.out_sn = out.st[3];
         ep.gate_sb1 = gt.st[1]; ep.gate_sb2 = gt.st[2]; ep.gate_sm = gt.st[0]; ep.gate_sn = gt.st[3];
+      }
+      if (fz) {
+        const int64_t Bt = static_cast<int64_t>(p.B1) * p.B2, ns = (p.K + 63) / 64;
+        p.fuse_stats = reinterpret_cast<const float2*>(in(0).p);
+        p.fuse_ss = p.M;
+        p.fuse_sb1 = static_cast<int64_t>(p.M) * ns;
+        const F2Layout L = f2_layout(Bt, p.M, p.K, e->fuse_split[i] != 0);
+        p.etile = pp.p;
+        p.sched = reinterpret_cast<int*>(in(0).p + L.cnt);
+        p.fuse_rowst = reinterpret_cast<const float2*>(in(0).p + L.rowst);
+        if (L.ncnt > 1) {
+          p.sk_gk = static_cast<int>(sk_gk(p.K));
+          p.sk_part = reinterpret_cast<float*>(in(0).p + L.part);
+          p.sk_cnt = reinterpret_cast<int*>(in(0).p + L.cnt) + 1;
+        }
       }
     } else {
       return unsup("no GPU kernel for this kind");
@@ -694,7 +727,7 @@ ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_
       e->fuse_role[c.pv] = 3;
       const int s_t = g.nodes[c.scores].output, p_t = g.nodes[c.softmax].output;
       const bool split =
-          pv_splitk(g.nodes[c.scores].ai("causal") != 0, g.tensors[g.nodes[c.softmax].output].shape[2]);
+          pv_splitk(g.nodes[c.scores].ai("causal") != 0, g.tensors[g.nodes[c.softmax].output].shape.back());
       for (int node : {c.scores, c.softmax, c.pv}) {
         e->fuse_s[node] = s_t;
         e->fuse_p[node] = p_t;

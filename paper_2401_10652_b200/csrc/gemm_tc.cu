@@ -39,6 +39,8 @@ struct alignas(64) GemmArgs {
   CUtensorMap ta;
   CUtensorMap tb;
   CUtensorMap tout;  // output map for the TMA-store epilogue (tma_store = 1)
+  CUtensorMap tadd;  // MODE 1: map over the added bias tensor (add_tma = 1), box {64, 32}
+  int add_tma;
   int tma_store;
   Epilogue ep;
   int M, N, K, B1, B2;
@@ -77,21 +79,21 @@ struct Cfg {
   // f2 scores (MODE 1): 16 epilogue warps (one 64-column slab each at BN = 256,
   // <= 112 registers) with a single 4 KB bf16 staging box per warp; K = head dim
   // is one or two k-blocks, so two smem stages suffice
-  static constexpr int EPI = MODE == 1 ? 16 : EPI_WARPS;
+  static constexpr int EPI = (MODE == 1 || MODE == 3) ? 16 : EPI_WARPS;
   // f2 PV (MODE 2): the EPI warps transform A tiles; XEPI more warps (one per
   // TMEM lane quarter) run the output epilogue so the transform never stalls
   static constexpr int XEPI = MODE == 2 ? 4 : 0;
   static constexpr int THREADS = 64 + 32 * (EPI + XEPI);
   // f2 PV (MODE 2) stages no output in smem: its ring is 8 deep (one CTA must keep
   // ~8 x 24 KB of A/B tiles in flight to stream at full speed when few CTAs remain)
-  static constexpr int EPI_BYTES = MODE == 1 ? EPI * 4096 : MODE == 2 ? 0 : EPI_WARPS * 32 * PITCH * 4;
-  static constexpr int STAGES = MODE == 1 ? 2 : MODE == 2 ? 8 : (BN >= 256 ? 3 : (BN >= 128 ? 4 : 5));
+  static constexpr int EPI_BYTES = (MODE == 1 || MODE == 3) ? EPI * 4096 : MODE == 2 ? 0 : EPI_WARPS * 32 * PITCH * 4;
+  static constexpr int STAGES = (MODE == 1 || MODE == 3) ? 2 : MODE == 2 ? 8 : (BN >= 256 ? 3 : (BN >= 128 ? 4 : 5));
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int SW = BN >= 64 ? 64 : 32;  // epilogue slab width (columns)
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
   static constexpr int SMEM = 1024 /*align slack*/ + STAGES * (A_BYTES + B_BYTES) + EPI_BYTES + 512 /*barriers*/ +
-                              (MAX_MT + 1) * 4 + 16;
+                              (MAX_MT + 1) * 4 + 16 + (MODE == 3 ? 16 * 8 + 8 : 0) /*bias-box barriers*/;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
@@ -256,6 +258,8 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
   uint64_t* uq_empty = tempty + 23;
   int* uq_slot = reinterpret_cast<int*>(tempty + 27);
   int* prefix = reinterpret_cast<int*>(tempty + 29);  // ends at 2 * STAGES + 31 words <= 512 bytes
+  // MODE 1 bias boxes: one mbarrier per epilogue warp, after the prefix table
+  uint64_t* bbar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(prefix + MAX_MT + 2) + 7) & ~uintptr_t(7));
   static_assert(C::STAGES <= 8, "barrier block layout");
 
   const int warp = threadIdx.x >> 5;
@@ -316,10 +320,16 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
     }
   }
   const int total = tpb * a.B1 * a.B2;
+#ifdef AC_DEBUG_HANG
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    printf("gemm_tc<%d,%d> enter grid %d M %d N %d K %d B1 %d B2 %d total %d tpb %d etile %p\n", BN, MODE, gridDim.x, a.M,
+           a.N, a.K, a.B1, a.B2, total, tpb, a.etile);
+#endif
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&a.ta);
     ptx::prefetch_tmap(&a.tb);
+    if (MODE == 3) ptx::prefetch_tmap(&a.tadd);
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -329,6 +339,8 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
       ptx::mbar_init(&tempty[s], MODE == 2 ? C::XEPI : C::EPI);
     }
     for (int s = 0; s < C::STAGES; ++s) ptx::mbar_init(&ready[s], 32 * C::EPI);
+    if (MODE == 3)
+      for (int w = 0; w < C::EPI; ++w) ptx::mbar_init(&bbar[w], 1);
     for (int s = 0; s < 4; ++s) {
       ptx::mbar_init(&uq_full[s], 1);
       ptx::mbar_init(&uq_empty[s], 1 + C::EPI + C::XEPI);
@@ -400,11 +412,19 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
         const char* esrc = MODE == 2 && a.etile
                                ? a.etile + (static_cast<long long>(b1 * a.B2 + b2) * a.MT + mt) * a.e_nkb * 16384
                                : nullptr;
+        // e-tile rows past M were never stored (short chunks, ragged tails): load only
+        // the 32-row quarters that hold rows < M (the rest of the stage is stale and
+        // feeds only accumulator rows that are never written out)
+        int ebytes = C::A_BYTES;
+        if (MODE == 2 && esrc) {
+          const int rows = a.M - mt * BM;
+          if (rows < BM) ebytes = ((rows + 31) / 32) * 4096;
+        }
         for (int kb = klo; kb < khi; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          ptx::mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
+          ptx::mbar_expect_tx(&full[stage], ebytes + C::B_BYTES);
           if (MODE == 2 && esrc)
-            ptx::bulk_load(sA + stage * C::A_BYTES, esrc + static_cast<long long>(kb) * 16384, C::A_BYTES, &full[stage]);
+            ptx::bulk_load(sA + stage * C::A_BYTES, esrc + static_cast<long long>(kb) * 16384, ebytes, &full[stage]);
           else
             ptx::tma_load_4d(sA + stage * C::A_BYTES, &a.ta, &full[stage], kb * BK, mt * BM, ac2, ac3);
           ptx::tma_load_4d(sB + stage * C::B_BYTES, &a.tb, &full[stage], kb * BK, nt * BN, bc2, bc3);
@@ -470,6 +490,8 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
     int acc = 0;
     int sbuf = 0;
     uint32_t aphase = 0;
+    uint32_t bphase = 0;  // MODE 3 bias-box barrier phase
+    bool bias_pending = false;  // MODE 3: this warp's next bias box is already in flight
     uint32_t pf_phase = 0, pe_phase = 0;  // split-K barrier phases
     if constexpr (MODE == 2) {
       if (ew < C::EPI) {
@@ -486,9 +508,11 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
           decode_unit(a, prefix, tpb, t, b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0);
           const int m = mt * BM + r;
           const bool mv = m < a.M;
-          const float* fp = reinterpret_cast<const float*>(a.fstats + static_cast<long long>(b1) * a.fst_sb1 + (mv ? m : 0));
+          const bool dead = mt * BM + quarter * 32 >= a.M;  // warp-uniform: rows never loaded
+          const long long bb = static_cast<long long>(b1) * a.B2 + b2;
+          const float* fp = reinterpret_cast<const float*>(a.fstats + bb * a.fst_sb1 + (mv ? m : 0));
           const long long fs = 2 * a.fst_ss;
-          const float2 rs = mv ? __ldg(a.frow + static_cast<long long>(b1) * a.M + m) : make_float2(0.f, 0.f);
+          const float2 rs = mv ? __ldg(a.frow + bb * a.M + m) : make_float2(0.f, 0.f);
           float fr[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) fr[j] = (mv && klo + j < khi) ? __ldg(fp + (klo + j) * fs) : -CUDART_INF_F;
@@ -504,7 +528,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
                 ptx::mbar_wait(&full[st], ph);
                 uint8_t* row = sA + st * C::A_BYTES + r * 128;
 #pragma unroll
-                for (int q4 = 0; q4 < ((a.dbg & 1) ? 0 : 4); ++q4) {
+                for (int q4 = 0; q4 < ((a.dbg & 1) || dead ? 0 : 4); ++q4) {
                   // same factor for every element: walk physical chunks in swizzled
                   // order so 8 consecutive rows hit all 32 banks
                   const int ch = half * 4 + q4;
@@ -558,7 +582,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
             uint32_t (&hi)[32] = *reinterpret_cast<uint32_t(*)[32]>(&rr[32]);
             const uint32_t tb = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
             ptx::tmem_ld32(tb, lo);
-            ptx::tmem_ld32(tb + 32, hi);
+            if constexpr (BN > 32) ptx::tmem_ld32(tb + 32, hi);
           }
           ptx::tmem_ld_wait();
           ptx::tc_fence_before();
@@ -601,7 +625,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
           }
           if (mv) {
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
+            for (int hh = 0; hh < BN / 32; ++hh) {
               const int n = hh * 32;
               if (n >= a.N) break;
               uint32_t pk[16];
@@ -714,27 +738,75 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
       for (int c = half; c < NSLAB; c += C::EPI / 4) {
         const bool last = c + C::EPI / 4 >= NSLAB;
         const int n0 = nt * BN + c * SW;
-        if constexpr (MODE == 1) {
-          // ---- f2 scores, one 64-column slab: x = acc * scale * log2(e) (fp32,
-          // scale > 0 so the max is taken on the raw accumulator); the slab max m2,
-          // stored e = bf16(2^(x - m2)), statistics (m2, fp32 sum of e).  Two TMEM
-          // passes (max, then exponentials) keep 32 accumulators live at a time.
-          constexpr float L2E = 1.4426950408889634f;
+        if constexpr (MODE == 1 || MODE == 3) {
+          // MODE 3 = MODE 1 plus an added bias tensor (the AlphaFold triangle bias,
+          // AF2 Alg. 13 line 5): compiled separately so the plain f2 scores keep
+          // their register budget
+          constexpr bool BIASED = MODE == 3;
           uint8_t* sb = reinterpret_cast<uint8_t*>(sEpi) + ew * 4096;
-          if (lane == 0) ptx::bulk_wait_read<0>();  // previous store has read the staging box
+          if (m0 >= a.M) {  // quarter entirely past M (short chunk): nothing to compute or store
+            if (last) {
+              ptx::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            }
+            continue;
+          }
+          // ---- f2 scores, one 64-column slab: x = acc * scale * log2(e) (fp32,
+          // scale > 0 so the max is taken on the raw accumulator) or, biased,
+          // x = (acc * scale + b) * log2(e); the slab max m2, stored
+          // e = bf16(2^(x - m2)), statistics (m2, fp32 sum of e).  Two TMEM passes
+          // (max, then exponentials) keep 32 accumulators live at a time.
+          constexpr float L2E = 1.4426950408889634f;
+          if (lane == 0) {
+            if (!BIASED || !bias_pending) ptx::bulk_wait_read<0>();  // previous store has read the staging box
+            if (BIASED && !bias_pending) {
+              // the slab's bias box [32 rows x 64 cols] (TMA, 128B-swizzled) lands in the
+              // staging box; rows are read back per thread from shared memory
+              ptx::mbar_expect_tx(&bbar[ew], 4096);
+              ptx::tma_load_4d(sb, &a.tadd, &bbar[ew], n0, m0, a.ep.add_sb1 ? b1 : 0, a.ep.add_sb2 ? b2 : 0);
+            }
+          }
           __syncwarp();
+          if constexpr (BIASED) {
+            ptx::mbar_wait(&bbar[ew], bphase);
+            bphase ^= 1;
+            bias_pending = false;
+          }
           const int m = m0 + lane;
           const bool mvalid = m < a.M;
           long long lim = a.ep.causal ? (a.ep.row_off + m - a.ep.col_off - n0) : (1ll << 40);
           if (lim > a.N - 1 - n0) lim = a.N - 1 - n0;  // columns past N are masked (and clipped by the store)
           const uint32_t ta = tbase + c * SW;
-          const float cl = a.ep.scale * L2E;
+          // biased: registers hold x itself after the add (unit multiplier below)
+          const float cl = BIASED ? 1.f : a.ep.scale * L2E;
+          // x for the 32 columns hh*32.. of this row (biased: bias chunks from the box)
+          auto load_x = [&](int hh, uint32_t (&r)[32]) {
+            ptx::tmem_ld32(ta + hh * 32, r);
+            ptx::tmem_ld_wait();
+            if constexpr (BIASED) {
+              const float sc = a.ep.scale * L2E;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t addr = ptx::smem_u32(sb + lane * 128 + (((hh * 4 + q) ^ (lane & 7)) * 16));
+                uint32_t w[4];
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                             : "r"(addr));
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 bf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+                  r[8 * q + 2 * e] = __float_as_uint(fmaf(__uint_as_float(r[8 * q + 2 * e]), sc, bf.x * L2E));
+                  r[8 * q + 2 * e + 1] = __float_as_uint(fmaf(__uint_as_float(r[8 * q + 2 * e + 1]), sc, bf.y * L2E));
+                }
+              }
+            }
+          };
           uint32_t r[32];
           float mx = -CUDART_INF_F;
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            ptx::tmem_ld32(ta + hh * 32, r);
-            ptx::tmem_ld_wait();
+            load_x(hh, r);
             float q0 = -CUDART_INF_F, q1 = -CUDART_INF_F, q2 = -CUDART_INF_F, q3 = -CUDART_INF_F;
             if (lim >= hh * 32 + 31) {
 #pragma unroll
@@ -754,8 +826,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
           float l0 = 0.f, l1 = 0.f;
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            ptx::tmem_ld32(ta + hh * 32, r);
-            ptx::tmem_ld_wait();
+            load_x(hh, r);
             if (hh == 1 && last) {
               ptx::tc_fence_before();
               __syncwarp();
@@ -783,6 +854,8 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
                 pk[j] = *reinterpret_cast<uint32_t*>(&h);
               }
             }
+            // (biased: this row's bias chunks hh*4.. were read above; the e chunks
+            // overwrite exactly those, in this thread's own row)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               const int ch = hh * 4 + q;
@@ -793,8 +866,8 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
             }
           }
           if (mvalid && n0 < a.N)
-            a.ep.stats[static_cast<long long>(b1) * a.ep.stats_sb1 + static_cast<long long>(n0 / 64) * a.ep.stats_ss +
-                       m] = make_float2(m2, l0 + l1);
+            a.ep.stats[static_cast<long long>(b1 * a.B2 + b2) * a.ep.stats_sb1 +
+                       static_cast<long long>(n0 / 64) * a.ep.stats_ss + m] = make_float2(m2, l0 + l1);
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -802,12 +875,33 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
               // (slabs past N would land in the next tile row: not stored)
               char* dst = a.etile + ((static_cast<long long>(b1 * a.B2 + b2) * a.MT + mt) * a.e_nkb + n0 / 64) * 16384 +
                           quarter * 4096;
-              if (n0 < a.N) ptx::bulk_store(dst, sb, 4096);
+              if (n0 < a.N && m0 < a.M) ptx::bulk_store(dst, sb, 4096);  // quarters past M: never read
             } else {
               ptx::tma_store_4d(&a.tout, sb, n0, m0, b1, b2);
             }
             ptx::bulk_commit();
+            if constexpr (BIASED) {
+              // prefetch the bias box of this warp's slab in the CTA's next tile (same
+              // slab index c) as soon as the store has read the staging box, so its L2
+              // latency overlaps the next accumulator's MMA
+              const int tn = t + ncl;
+              if (tn < total && last) {
+                TileWalk w2 = walk;
+                w2.next(a, prefix, tpb, tn, ncl);
+                int nb1, nb2, nmt, nnt, nkb;
+                w2.get(a, nb1, nb2, nmt, nnt, nkb);
+                const int nm0 = nmt * BM + quarter * 32;
+                if (nm0 < a.M) {
+                  ptx::bulk_wait_read<0>();
+                  ptx::mbar_expect_tx(&bbar[ew], 4096);
+                  ptx::tma_load_4d(sb, &a.tadd, &bbar[ew], nnt * BN + c * SW, nm0, a.ep.add_sb1 ? nb1 : 0,
+                                   a.ep.add_sb2 ? nb2 : 0);
+                  bias_pending = true;
+                }
+              }
+            }
           }
+          if constexpr (BIASED) bias_pending = __shfl_sync(0xffffffffu, bias_pending, 0);
           continue;
         }
         if constexpr (SW == 64) {
@@ -976,6 +1070,9 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
     ptx::tc_fence_after();
     ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
   }
+#ifdef AC_DEBUG_HANG
+  if (blockIdx.x == 0 && threadIdx.x == 0) printf("gemm_tc<%d,%d> exit\n", BN, MODE);
+#endif
 }
 
 // ---------------------------------------------------------------- host side
@@ -1033,7 +1130,7 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
     return cudaErrorInvalidValue;
   a.etile = static_cast<char*>(p.etile);
   a.sched = MODE == 2 ? p.sched : nullptr;
-  a.e_nkb = MODE == 1 ? (p.N + 63) / 64 : (p.K + 63) / 64;
+  a.e_nkb = (MODE == 1 || MODE == 3) ? (p.N + 63) / 64 : (p.K + 63) / 64;
   if (p.etile && (reinterpret_cast<uintptr_t>(p.etile) & 127)) return cudaErrorInvalidValue;
   if (!make_map(&a.tb, p.B, p.K, p.b_rows_total ? p.b_rows_total : p.N, p.B1, p.B2, BN)) return cudaErrorInvalidValue;
   a.ep = p.ep;
@@ -1074,12 +1171,38 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
       a.lean = (!e.add && !e.bias && !e.gate && !e.res && e.act == ACT_NONE) ? 1 : 0;
     }
   }
+  if (MODE == 3 && p.ep.add && p.ep.add_sn == 1) {
+    // bias map {N, M, B1, B2} (a batch dim the bias does not vary over gets extent 1)
+    const Epilogue& e = p.ep;
+    EncodeTiledFn enc = get_encode();
+    const int64_t big = ((e.add_sm * p.M + 8) * 2 + 15) / 16 * 16;
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(p.N), static_cast<cuuint64_t>(p.M),
+                          static_cast<cuuint64_t>(e.add_sb1 ? p.B1 : 1), static_cast<cuuint64_t>(e.add_sb2 ? p.B2 : 1)};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(e.add_sm * 2),
+                             static_cast<cuuint64_t>(e.add_sb1 ? e.add_sb1 * 2 : big),
+                             static_cast<cuuint64_t>(e.add_sb2 ? e.add_sb2 * 2 : big)};
+    bool ok = enc && (reinterpret_cast<uintptr_t>(e.add) & 15) == 0;
+    for (int i = 0; i < 3; ++i) ok = ok && strides[i] % 16 == 0 && strides[i] > 0;
+    cuuint32_t box[4] = {64, 32, 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (ok)
+      ok = enc(&a.tadd, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(e.add), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    a.add_tma = ok ? 1 : 0;
+  }
   a.tiles_per_batch_dense = a.MT * a.NT;
   a.total_tiles_dense = a.tiles_per_batch_dense * p.B1 * p.B2;
   // f2 modes: scores need the lean TMA-store epilogue and a positive scale; PV the
   // 64-wide tile with an n-contiguous aligned output
+  // (MODE 1 may add an n-contiguous bias tensor, the AlphaFold triangle bias)
   if (MODE == 1 && !(a.tma_store && a.lean && p.ep.scale > 0.f)) return cudaErrorInvalidValue;
-  if (MODE == 2 && !(BN == 64 && a.vec)) return cudaErrorInvalidValue;
+  if (MODE == 3) {
+    const Epilogue& e = p.ep;
+    const bool only_add = !e.bias && !e.gate && !e.res && e.act == ACT_NONE && !e.causal && e.add;
+    if (!(a.tma_store && a.add_tma && only_add && p.ep.scale > 0.f)) return cudaErrorInvalidValue;
+  }
+  if (MODE == 2 && !((BN == 64 || BN == 32) && a.vec)) return cudaErrorInvalidValue;
   a.fuse = MODE == 2 ? 1 : 0;
   if (MODE == 2) {
     const int kbn = (p.K + BK - 1) / BK;
@@ -1176,7 +1299,15 @@ cudaError_t gemm_tc(const GemmProblem& p, cudaStream_t s, int bn_hint) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0 || p.B1 <= 0 || p.B2 <= 0) return cudaErrorInvalidValue;
   int bn = bn_hint;
   if (bn == 0) bn = p.N <= 32 ? 32 : p.N <= 64 ? 64 : p.N <= 128 ? 128 : 256;
-  if (p.fuse_stats) return bn == 64 ? launch<64, 2>(p, s) : cudaErrorInvalidValue;
+  if (p.fuse_stats) return p.N <= 32 ? launch<32, 2>(p, s) : bn == 64 ? launch<64, 2>(p, s) : cudaErrorInvalidValue;
+  if (p.ep.stats && p.ep.add) {
+    switch (bn) {
+      case 64: return launch<64, 3>(p, s);
+      case 128: return launch<128, 3>(p, s);
+      case 256: return launch<256, 3>(p, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   if (p.ep.stats) {
     switch (bn) {
       case 64: return launch<64, 1>(p, s);

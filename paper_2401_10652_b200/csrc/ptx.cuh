@@ -3,6 +3,7 @@
 // descriptors.  Bit layouts follow the PTX ISA tcgen05 "matrix descriptor" and
 // "instruction descriptor" tables (kind::f16, K-major, SWIZZLE_128B).
 #pragma once
+#include <cstdio>
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -28,6 +29,29 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifdef AC_DEBUG_HANG
+// debug build (AC_DEBUG_HANG=1 python -m paper_2401_10652_b200.build): a wait that
+// has not completed after ~4 G cycles reports the barrier and traps
+__device__ __noinline__ void mbar_hang(uint64_t* bar, uint32_t parity) {
+  printf("mbar hang: block %d thread %d smem %u parity %u\n", blockIdx.x, threadIdx.x, smem_u32(bar), parity);
+  __trap();
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const long long t0 = clock64();
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (clock64() - t0 > 4000000000ll) mbar_hang(bar, parity);
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -37,6 +61,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity), "r"(0x989680u)  // suspend-time hint: the warp sleeps instead of spinning
       : "memory");
 }
+#endif
 
 // 4-D tiled TMA load into shared memory, completion signalled on `bar`.
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
