@@ -42,6 +42,11 @@ struct Arena {
   std::vector<ArenaSlot> slot;  // per tensor
   int64_t size = 0;
   int64_t live_peak = 0;        // max over steps of the bytes live in the arena
+  // chunk-loop overlap control blocks (fused chains inside a chunked region), after
+  // the tensors: per scores node, offset (-1 none), batches B, chunks n.  Layout in
+  // ints: [epoch: B][tile counters: n][PV unit counters: n][PV done counts: n x B]
+  std::vector<int64_t> ctrl_off;
+  std::vector<int64_t> ctrl_b, ctrl_n;
 };
 
 struct View {
@@ -70,6 +75,7 @@ struct ac_exec {
   std::vector<char> fuse_role;
   std::vector<int> fuse_s, fuse_p;
   std::vector<char> fuse_split;        // per node of a fused chain: PV fixed split-K on
+  std::vector<int> fuse_head;          // per node of a fused chain: its scores node
   mutable ac_run_stats stats{};
   // profiling: event pairs per launch of the last run
   bool profiling = false;
@@ -93,6 +99,14 @@ bool pv_splitk(bool causal, int64_t nk) {
   const char* v = getenv("AC_PV_SPLITK");
   if (v && (v[0] == '0' || v[0] == '1')) return v[0] == '1';
   return !causal && nk >= 4096;  // short rows: one unit per tile is cheaper
+}
+
+// Chunk-loop overlap of fused chains (programmatic dependent launch + per-batch
+// epochs): the next chunk's scores start on SMs the PV's tail frees.
+// AC_OVERLAP=0 disables it (every launch then waits for the previous one).
+bool overlap_enabled() {
+  const char* v = getenv("AC_OVERLAP");
+  return !(v && v[0] == '0');
 }
 
 int region_index(const Plan& plan, int node) {
@@ -272,6 +286,27 @@ Arena build_arena(const Graph& g, const Plan& plan) {
       if (A.slot[t].birth <= s && s <= A.slot[t].death) live += A.slot[t].bytes;
     A.live_peak = std::max(A.live_peak, live);
   }
+  A.ctrl_off.assign(S, -1);
+  A.ctrl_b.assign(S, 0);
+  A.ctrl_n.assign(S, 0);
+  if (overlap_enabled()) {
+    for (const Chain& c : fused_chains(g, plan)) {
+      const int r = region_index(plan, c.scores);
+      if (r < 0 || g.nodes[c.scores].kind != "attn_scores") continue;  // (triangle chains: no overlap yet)
+      // the region must be exactly the chain, so that in the chunk loop the PV of
+      // chunk k is the launch right before the scores of chunk k + 1 (whose inputs
+      // then all predate the region)
+      if (plan.regions[r].start != c.scores || plan.regions[r].end != c.pv) continue;
+      const std::vector<int64_t>& sh = g.tensors[g.nodes[c.scores].output].shape;
+      int64_t B = 1;
+      for (size_t d = 0; d + 2 < sh.size(); ++d) B *= sh[d];
+      const int64_t n = plan.regions[r].n;
+      A.ctrl_off[c.scores] = A.size;
+      A.ctrl_b[c.scores] = B;
+      A.ctrl_n[c.scores] = n;
+      A.size += ((B + 2 * n + n * B) * 4 + 255) / 256 * 256;
+    }
+  }
   return A;
 }
 
@@ -312,6 +347,7 @@ int64_t extent(const View& v, int a, int b) {
 }
 
 struct NodeCtx {
+  int chunk = -1;       // index of the chunk within this rank's chunk loop (-1: none)
   int64_t row_off = 0;  // global query-row offset of this view (causal)
   int64_t col_off = 0;
   bool fast = false;    // aligned causal chain: skip masked tiles / keys
@@ -322,6 +358,32 @@ cudaError_t gemm(DT dt, const GemmProblem& p, cudaStream_t s) {
 }
 
 ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, const NodeCtx& cx, cudaStream_t s);
+
+// Chunk-loop overlap of a fused chain (Arena::ctrl_*): scores of chunk k > 0 start
+// while the PV of chunk k - 1 drains (PDL, no grid wait) and write batch b only once
+// that PV has published epoch k for it; tiles are taken dynamically.  The PV waits
+// for its combine (PDL + griddepcontrol.wait), takes units from its own per-chunk
+// counter and publishes its epochs.
+void chain_overlap(const ac_exec* e, int node, const NodeCtx& cx, GemmProblem& p) {
+  const int h = e->fuse_head[node];
+  const int64_t off = h >= 0 ? e->arena.ctrl_off[h] : -1;
+  if (off < 0 || cx.chunk < 0) return;
+  const int64_t B = e->arena.ctrl_b[h], n = e->arena.ctrl_n[h];
+  int* c = reinterpret_cast<int*>(e->ws + off);
+  const int k = cx.chunk;
+  p.done_epoch = c;
+  if (e->fuse_role[node] == 1) {
+    p.pdl = k > 0 ? 1 : 0;
+    p.dep_epoch = k;
+    p.tsched = c + B + k;
+  } else {
+    p.pdl = 1;
+    p.pdl_wait = 1;
+    p.sched = c + B + n + k;
+    p.done_cnt = c + B + 2 * n + static_cast<int64_t>(k) * B;
+    p.epoch = k;
+  }
+}
 
 ac_status launch_node(const ac_exec* e, int i, const std::vector<View>& V, const NodeCtx& cx, cudaStream_t s) {
   if (!e->profiling) return launch_node_impl(e, i, V, cx, s);
@@ -366,7 +428,7 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
     err = softmax_stats_combine(reinterpret_cast<float2*>(out.p), B, M, static_cast<int>(ns),
                                 M * ns, M, cx.fast ? 1 : 0, cx.row_off,
                                 reinterpret_cast<float2*>(out.p + L.rowst), reinterpret_cast<int*>(out.p + L.cnt),
-                                L.ncnt, s);
+                                L.ncnt, s, cx.chunk >= 0 && e->arena.ctrl_off[e->fuse_head[i]] >= 0 ? 1 : 0);
   } else if (k == "softmax") {
     const View& x = in(0);
     if (n.ai("dim") != x.nd - 1 || x.st[x.nd - 1] != 1) return unsup("softmax over a non-last dim");
@@ -505,6 +567,7 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         p.etile = out.p;
         ep.stats_ss = p.M;
         ep.stats_sb1 = static_cast<int64_t>(p.M) * ns;
+        chain_overlap(e, i, cx, p);
       }
     } else if (k == "attn_pv") {
       // fused chain: A is the raw scores S, normalised in shared memory with the
@@ -537,6 +600,7 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
           p.sk_part = reinterpret_cast<float*>(in(0).p + L.part);
           p.sk_cnt = reinterpret_cast<int*>(in(0).p + L.cnt) + 1;
         }
+        chain_overlap(e, i, cx, p);
       }
       // Cluster split-K (ac_gemm_desc.ksplit) exists but measured slower than one
       // CTA per tile for these shapes (DSMEM reduction latency), so it stays off.
@@ -720,6 +784,7 @@ ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_
   e->fuse_s.assign(S, -1);
   e->fuse_p.assign(S, -1);
   e->fuse_split.assign(S, 0);
+  e->fuse_head.assign(S, -1);
   if (e->dt == DT::BF16) {
     for (const Chain& c : fused_chains(g, e->plan)) {
       e->fuse_role[c.scores] = 1;
@@ -732,6 +797,7 @@ ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_
         e->fuse_s[node] = s_t;
         e->fuse_p[node] = p_t;
         e->fuse_split[node] = split ? 1 : 0;
+        e->fuse_head[node] = c.scores;
       }
     }
   }
@@ -865,6 +931,14 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
     for (auto& y : R.yc) ycs.insert(y.first);
     std::vector<char> produced(T, 0);
     for (int j = R.start; j <= R.end; ++j) produced[g.nodes[j].output] = 1;
+    for (int j = R.start; j <= R.end; ++j) {
+      const int64_t co = e->arena.ctrl_off[j];
+      if (co >= 0) {
+        const int64_t B = e->arena.ctrl_b[j], nn = e->arena.ctrl_n[j];
+        if (cudaMemsetAsync(e->ws + co, 0, (B + 2 * nn + nn * B) * 4, s) != cudaSuccess)
+          return set_error(AC_ERR_CUDA, "cudaMemsetAsync (chunk-loop control block) failed");
+      }
+    }
     for (int64_t c = c0; c < c1; ++c) {
       const int64_t off = c * L;
       const int64_t len = std::min(L, R.extent - off);
@@ -904,6 +978,7 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
         }
         NodeCtx cx;
         cx.fast = e->causal_fast[j] != 0;
+        cx.chunk = static_cast<int>(c - c0);
         const int d = R.dim_of(nj.output);
         if (d >= 0 && d == e->chain_rows_dim[j]) cx.row_off = off;
         ac_status st = launch_node(e, j, *use, cx, s);

@@ -68,6 +68,12 @@ struct alignas(64) GemmArgs {
   unsigned long long* trace;  // debug (AC_TRACE): per unit {cta, t_load0, t_tfull, t_done}
   char* etile;  // f2 pre-swizzled e tiles (GemmProblem::etile), null = tensor path
   int e_nkb;    // k-blocks per e-tile row
+  // chunk-loop overlap (GemmProblem::pdl ...)
+  int pdl_wait;
+  int* done_cnt;
+  int* done_epoch;
+  int epoch, dep_epoch;
+  int* tsched;  // MODE 1 / 3 dynamic tile counter
 };
 
 // epilogue staging: per epilogue warp a [32 rows][PITCH] fp32 slab; PITCH = 68
@@ -134,6 +140,7 @@ struct TileWalk {
     return a.causal_tiles ? prefix[m + 1] : start + a.NT;
   }
   __device__ __forceinline__ void next(const GemmArgs& a, const int* prefix, int tpb, int t, int ncl) {
+    if (a.tsched) started = false;  // dynamic tiles: no fixed stride, decode afresh
     if (!a.causal_tiles) {
       // dense tiles: direct decode (stepping m-tile by m-tile costs ncl / NT
       // iterations per tile, 148 for a one-n-tile GEMM)
@@ -357,11 +364,19 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
   if (ks > 1) ptx::cluster_sync();  // remote barriers initialised before any remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // programmatic dependent launch: the prologue above overlapped the previous
+  // kernel; wait for its results only when this kernel reads them, and let the
+  // next kernel of the chunk loop be scheduled as SMs free up
+  if (a.pdl_wait) ptx::griddep_wait();
+  ptx::griddep_launch();
   // unit sequence of this CTA: i-th unit (static round-robin, or the MODE 2 queue)
+  // unit queue in use: MODE 2 always, MODE 1 / 3 with dynamic tiles
+  const bool uq = MODE == 2 || (MODE != 0 && a.tsched != nullptr);
   auto produce = [&](int i) -> int {  // producer lane only
-    if constexpr (MODE == 2) {
+    if (uq) {
       const int sl = i & 3;
-      int u = a.sched ? atomicAdd(a.sched, 1) : cid + i * ncl;
+      int* sc = MODE == 2 ? a.sched : a.tsched;
+      int u = sc ? atomicAdd(sc, 1) : cid + i * ncl;
       if (u > total) u = total;
       ptx::mbar_wait(&uq_empty[sl], ((i >> 2) & 1) ^ 1);
       *reinterpret_cast<volatile int*>(&uq_slot[sl]) = u;
@@ -372,7 +387,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
     }
   };
   auto take = [&](int i) -> int {  // whole consuming warp
-    if constexpr (MODE == 2) {
+    if (uq) {
       const int sl = i & 3;
       ptx::mbar_wait(&uq_full[sl], (i >> 2) & 1);
       const int u = *reinterpret_cast<volatile int*>(&uq_slot[sl]);
@@ -589,6 +604,12 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
           if (++acc == 2) { acc = 0; aphase ^= 1; }
+          if (a.done_cnt && ew == C::EPI && lane == 0) {
+            // this unit's MMAs are complete, so its e-tiles and statistics have been
+            // read: the unit that completes the batch publishes the chunk epoch
+            const int bb = b1 * a.B2 + b2;
+            if (ptx::atom_add_acqrel_gpu(a.done_cnt + bb, 1) == tpb - 1) ptx::st_release_gpu(a.done_epoch + bb, a.epoch + 1);
+          }
           if (ng > 1) {
             float* mine = a.skpart + (static_cast<long long>(unit0 + g) * BM + r) * BN;
 #pragma unroll
@@ -649,7 +670,8 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
       }
     } else {
     TileWalk walk;
-    for (int t = cid; t < total; t += ncl) {
+    int dep_ok_b = -1;  // MODE 1 / 3: last batch whose predecessor PV is known finished
+    for (int i = 0, t = take(0); t < total; t = take(++i)) {
       int b1, b2, mt, nt, kbn;
       walk.next(a, prefix, tpb, t, ncl);
       walk.get(a, b1, b2, mt, nt, kbn);
@@ -865,6 +887,19 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
                            : "memory");
             }
           }
+          if (a.done_epoch) {
+            // chunk-loop overlap: the previous chunk's PV must have finished reading this
+            // batch's e-tiles and statistics before they are overwritten
+            const int bb = b1 * a.B2 + b2;
+            if (bb != dep_ok_b) {
+              if (lane == 0) {
+                while (ptx::ld_acquire_gpu(a.done_epoch + bb) < a.dep_epoch) __nanosleep(128);
+                ptx::fence_proxy_async_global();
+              }
+              __syncwarp();
+              dep_ok_b = bb;
+            }
+          }
           if (mvalid && n0 < a.N)
             a.ep.stats[static_cast<long long>(b1 * a.B2 + b2) * a.ep.stats_sb1 +
                        static_cast<long long>(n0 / 64) * a.ep.stats_ss + m] = make_float2(m2, l0 + l1);
@@ -885,7 +920,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
               // slab index c) as soon as the store has read the staging box, so its L2
               // latency overlaps the next accumulator's MMA
               const int tn = t + ncl;
-              if (tn < total && last) {
+              if (tn < total && last && !a.tsched) {
                 TileWalk w2 = walk;
                 w2.next(a, prefix, tpb, tn, ncl);
                 int nb1, nb2, nmt, nnt, nkb;
@@ -1217,6 +1252,12 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
     if (a.skng > 1 && !a.skcnt) return cudaErrorInvalidValue;
     if (p.causal_k && a.MT > MAX_MT) return cudaErrorInvalidValue;
   }
+  a.pdl_wait = p.pdl_wait;
+  a.done_cnt = MODE == 2 ? p.done_cnt : nullptr;
+  a.done_epoch = (MODE == 2 && p.done_cnt) || (MODE != 2 && MODE != 0) ? p.done_epoch : nullptr;
+  a.epoch = p.epoch;
+  a.dep_epoch = p.dep_epoch;
+  a.tsched = (MODE == 1 || MODE == 3) ? p.tsched : nullptr;
   a.fstats = p.fuse_stats;
   a.fst_sb1 = p.fuse_sb1;
   a.fst_ss = p.fuse_ss;
@@ -1252,6 +1293,19 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   }
   if (grid > cap) grid = cap;
   if (grid < a.ks) grid = a.ks;
+  if (a.ks == 1 && p.pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(C::THREADS);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute lattr[1];
+    lattr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    lattr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = lattr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, MODE>, a);
+  }
   if (a.ks == 1) {
     gemm_tc_kernel<BN, MODE><<<grid, C::THREADS, C::SMEM, s>>>(a);
     if (a.trace) {  // debug only: dump {cta, t_load0, t_tfull, t_done} per unit

@@ -93,6 +93,21 @@ struct GemmProblem {
   // f2 PV: zero-initialised int; CTAs take work units from it dynamically (faster
   // SMs take more), null = static round-robin.  Results do not depend on it.
   int* sched = nullptr;
+  // Chunk-loop overlap (f2 chains): launched with programmatic
+  // stream serialisation (pdl) so the kernel may start while the previous one
+  // drains; pdl_wait: griddepcontrol.wait before reading the predecessor's output.
+  // MODE 2 (PV) marks a batch finished for chunk `epoch`: done_cnt[b] counts its
+  // units and the unit completing the batch stores epoch + 1 to done_epoch[b]
+  // (release).  MODE 1 (scores of the next chunk) stores nothing of batch b before
+  // done_epoch[b] >= dep_epoch (acquire): the PV of the previous chunk has read
+  // that batch's e-tiles and statistics.  tsched: zero-initialised tile counter
+  // (MODE 1 dynamic tiles, so CTAs that start late on SMs the PV frees take fewer).
+  int pdl = 0, pdl_wait = 0;
+  int* done_cnt = nullptr;
+  int* done_epoch = nullptr;
+  int epoch = 0;
+  int dep_epoch = 0;
+  int* tsched = nullptr;
 };
 
 // bf16 x bf16 -> fp32 (TMEM) -> bf16, tcgen05 + TMA, sm_100a.  Returns a
@@ -122,7 +137,8 @@ cudaError_t softmax_rows(const void* s_in, void* p_out, int64_t rows, int64_t nc
 // (row_off + (m/128 + 1)*128) are read - the causal PV reads no others.
 // Also zeroes zero[0 .. nzero) (the PV's unit counter and split-K tile counters).
 cudaError_t softmax_stats_combine(float2* stats, int64_t B1, int64_t M, int ns, int64_t sb1, int64_t ss, int causal,
-                                  int64_t row_off, float2* rowst, int* zero, int64_t nzero, cudaStream_t s);
+                                  int64_t row_off, float2* rowst, int* zero, int64_t nzero, cudaStream_t s,
+                                  int pdl = 0);
 
 int num_sms();
 

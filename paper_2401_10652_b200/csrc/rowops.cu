@@ -624,8 +624,12 @@ cudaError_t layernorm_dispatch(const void* x, const void* g, const void* b, void
 __global__ void __launch_bounds__(256) stats_combine_kernel(float2* __restrict__ st, int64_t B1, int64_t M, int ns,
                                                            int64_t sb1, int64_t ss, int causal, int64_t row_off,
                                                            float2* __restrict__ rowst, int* __restrict__ zero,
-                                                           int64_t nzero) {
+                                                           int64_t nzero, int pdl) {
   __shared__ float2 part[8][33];
+  if (pdl) {  // chunk-loop overlap: the scores step must be complete and visible
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x; i < nzero; i += static_cast<int64_t>(gridDim.x) * 256)
     zero[i] = 0;  // split-K tile counters of the PV that follows
   const int r = threadIdx.x & 31, g = threadIdx.x >> 5;
@@ -670,11 +674,24 @@ __global__ void __launch_bounds__(256) stats_combine_kernel(float2* __restrict__
 }  // namespace
 
 cudaError_t softmax_stats_combine(float2* stats, int64_t B1, int64_t M, int ns, int64_t sb1, int64_t ss, int causal,
-                                  int64_t row_off, float2* rowst, int* zero, int64_t nzero, cudaStream_t st) {
+                                  int64_t row_off, float2* rowst, int* zero, int64_t nzero, cudaStream_t st, int pdl) {
   if (B1 * M <= 0) return cudaSuccess;
   const int64_t blocks = (B1 * M + 31) / 32;
+  if (pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, stats_combine_kernel, stats, B1, M, ns, sb1, ss, causal, row_off, rowst, zero,
+                              nzero, 1);
+  }
   stats_combine_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(stats, B1, M, ns, sb1, ss, causal, row_off,
-                                                                      rowst, zero, nzero);
+                                                                      rowst, zero, nzero, 0);
   return cudaGetLastError();
 }
 

@@ -14,4 +14,7 @@ for fn in sys.argv[1:]:
               f"  clocks {d.get('clocks')}")
         us = u.get("stages_ms", {})
         for k, v in d.get("stages", {}).items():
+            if not isinstance(v, dict):
+                print(f"   {k} {v}")
+                continue
             print(f"   {k:14s} {v['ms_per_step']:8.4f}  unchunked {us.get(k, float('nan')):8.4f}  x{v['launches_per_step']:.0f}")
