@@ -51,6 +51,15 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
     ap.add_argument("--sweep", action="store_true", help="also sweep the attention chunk length 64..4096")
+    ap.add_argument("--layers", type=int, default=1,
+                    help="stack this many blocks (NEXT f3 multi-block plans; one region per block)")
+    ap.add_argument("--maxlen", action="store_true",
+                    help="NEXT f3: max sequence length whose unchunked / ac_plan peak fits this GPU's free HBM "
+                         "(api.max_length), then run the chunked plan at --maxlen-run tokens")
+    ap.add_argument("--maxlen-run", type=int, default=262144)
+    ap.add_argument("--ablation", action="store_true",
+                    help="also run the paper's Table 1 toggles (P:319-332): ac_plan with each cost term / "
+                         "graph optimisation switched off, at 20/10/5 %% budgets; every distinct plan timed")
     return ap.parse_args()
 
 
@@ -119,17 +128,18 @@ BLOCKS = {
 }
 
 
-def c_graph(name):
+def c_graph(name, layers=1, N=None):
     """The workload graph, built by libautochunk (ac_graph_block), and its document."""
     from paper_2401_10652_b200 import api, graphdoc
-    kind, N, d, h, f, causal, dt = BLOCKS[name]
-    cg = api.graph_block(kind, N, d, h, f, causal, dt, name=name)
+    kind, N0, d, h, f, causal, dt = BLOCKS[name]
+    cg = api.graph_block(kind, N or N0, d, h, f, causal, dt, name=name, layers=layers)
     return cg, graphdoc.parse(cg.serialize())
 
 
-def oracle_graph(name):
+def oracle_graph(name, layers=1):
     from oracle import workloads
-    return workloads.config(name)
+    c = workloads.CONFIGS[name]
+    return workloads.block(c["kind"], c["N"], c["d"], c["h"], c["f"], c["causal"], c["dtype"], name, layers=layers)
 
 
 def tokens_per_step(name, doc):
@@ -266,6 +276,71 @@ def reference_arm(args):
     return 0
 
 
+# ------------------------------------------------------------------ max length (NEXT f3)
+def maxlen_arm(args):
+    """Max inference length on this GPU (SPEC cmd_maxlen S:478-486): the
+    activation budget is the free HBM minus the weights and a 2 GiB margin; the
+    lengths come from the planner's own peak model (api.max_length); the chunked plan
+    is then run at --maxlen-run tokens (past the unchunked maximum) to show it fits."""
+    import torch
+    from paper_2401_10652_b200 import api
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    kind, N0, d, h, f, causal, dt = BLOCKS[args.config]
+    _, doc0 = c_graph(args.config, args.layers)
+    wbytes = sum(doc0.nbytes(w[0]) for w in doc0.weights)
+    free, total = torch.cuda.mem_get_info()
+    budget = free - wbytes - (2 << 30)
+    step = 64 if kind == "tri_attn_pair" else 128
+    cap = (1 << 15) if kind == "tri_attn_pair" else (1 << 23)
+    t0 = time.perf_counter()
+    ml = api.max_length(kind, d, h, f, causal, dt, budget, layers=args.layers, step=step, cap=cap)
+    t_search = time.perf_counter() - t0
+    run = None
+    Nr = min(args.maxlen_run, ml["chunked"]) if ml["chunked"] else 0
+    if Nr and kind != "tri_attn_pair":
+        cg, doc = c_graph(args.config, args.layers, N=Nr)
+        prof0, _ = api.estimate_memory(cg)
+        plan = api.ac_plan(cg, budget)
+        profp, _ = api.estimate_memory(cg, plan)
+        _, dev = device_inputs(doc, torch)
+        TD = {"bf16": torch.bfloat16, "f32": torch.float32}
+        outs = {o: torch.empty(doc.tensors[o][1], dtype=TD[doc.tensors[o][0]], device="cuda") for o in doc.outputs}
+        torch.cuda.synchronize()
+        base = torch.cuda.memory_allocated()
+        torch.cuda.reset_peak_memory_stats()
+        ws = torch.empty(max(plan.workspace_bytes(), 16), dtype=torch.uint8, device="cuda")
+        ex = api.Exec(plan, ws)
+        ins = {t: dev[t] for t in doc.order}
+        ex.run(ins, outs)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        ex.run(ins, outs)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        y = outs[doc.outputs[0]]
+        caller = sum(doc.nbytes(t) for t in doc.inputs + doc.outputs)
+        run = {"tokens": Nr, "plan": [ln.split(" flow=")[0] for ln in plan.serialize().splitlines()
+                                      if ln.startswith("region")],
+               "ms": round(ms, 3), "tokens_per_s": round(Nr / (ms / 1e3), 1),
+               "planned_peak_bytes": profp.peak_bytes, "unchunked_peak_bytes": prof0.peak_bytes,
+               "arena_bytes": ex.stats().workspace_high_water, "arena_plus_caller": ex.stats().workspace_high_water + caller,
+               "torch_peak_delta_bytes": torch.cuda.max_memory_allocated() - base,
+               "output_finite": bool(torch.isfinite(y.float()).all().item())}
+    line = {"metric": "max inference length under this GPU's HBM (P:357-361)", "value": ml["chunked"],
+            "unit": "tokens" if kind != "tri_attn_pair" else "residues", "n_gpus": 1,
+            "higher_is_better": True, "dtype": dt, "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config] + (f", {args.layers} stacked blocks" if args.layers > 1 else ""),
+                       "activation_budget_bytes": budget, "hbm_free_bytes": free, "weights_bytes": wbytes,
+                       "length_step": step, "search_cap": cap},
+            "unchunked_max": ml["unchunked"], "ratio": ml["ratio"], "plan_at_max": ml["plan"],
+            "search_s": round(t_search, 2), "run": run,
+            "paper": {"claim": "11.7x (1D) / 3.2x avg (2D) max-length extension", "hardware": "A100 80GB (P:336)"}}
+    print(json.dumps(line))
+    return 0
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     args = parse()
@@ -287,7 +362,9 @@ def main():
         if world > 1:
             dist.barrier()
 
-    cg, doc = c_graph(args.config)
+    if args.maxlen:
+        return maxlen_arm(args)
+    cg, doc = c_graph(args.config, args.layers)
     prof0, _ = api.estimate_memory(cg)
     budget = int(args.budget_frac * prof0.peak_bytes)
     if args.plan:
@@ -445,12 +522,48 @@ def main():
             del exs, wss
         torch.cuda.empty_cache()
 
+    # Table 1 ablation (NEXT f4): plans under each toggle, each distinct plan timed once
+    ablation = None
+    if args.ablation and not args.profile:
+        import ctypes as C
+        from paper_2401_10652_b200 import _lib as L
+        toggles = [("all strategies", 0), ("no computation density", 2), ("no dimension strides", 4),
+                   ("no number of nodes", 8), ("no flops", 16), ("no graph optimization", 1)]
+        timed_plans = {}
+        ablation = []
+        for frac in (0.2, 0.1, 0.05):
+            for name, flag in toggles:
+                prm = L.CostParams()
+                L.lib().ac_cost_params_default(C.byref(prm))
+                prm.flags = flag
+                ap_ = api.ac_plan(cg, int(frac * prof0.peak_bytes), prm)
+                txt = "\n".join(ln.split(" flow=")[0] for ln in ap_.serialize().splitlines() if ln.startswith("region"))
+                if txt not in timed_plans:
+                    pr_, _ = api.estimate_memory(cg, ap_)
+                    wsa = torch.empty(max(ap_.workspace_bytes(), 16), dtype=torch.uint8, device="cuda")
+                    exa = api.Exec(ap_, wsa, comm)
+                    ka = max(3, args.steps // 2)
+                    ta, _ = timed(exa, ins, outs, ka, 2)
+                    timed_plans[txt] = (units * ka / (ta / 1e3), pr_.peak_bytes / prof0.peak_bytes, ap_.feasible)
+                    del exa, wsa
+                tps, pfrac, feas = timed_plans[txt]
+                ablation.append({"budget_frac": frac, "toggle": name, "plan": txt.splitlines(),
+                                 "feasible": bool(feas), "planned_peak_frac": round(pfrac, 4),
+                                 "tokens_per_s": round(tps, 1)})
+        for frac in (0.2, 0.1, 0.05):
+            ref = [a["tokens_per_s"] for a in ablation if a["budget_frac"] == frac and a["toggle"] == "all strategies"][0]
+            for a in ablation:
+                if a["budget_frac"] == frac:
+                    a["speed_vs_all"] = round(a["tokens_per_s"] / ref, 4)
+        torch.cuda.empty_cache()
+
     if rank != 0:
         return 0
     cpu = None
     if not args.no_cpu and not args.profile:
         try:
-            cpu = cpu_baseline(args.config, oracle_graph(args.config), samples)
+            cpu = (cpu_baseline(args.config, oracle_graph(args.config), samples) if args.layers == 1 else
+                   {"note": "oracle row sampler covers one block; stacks are parity-tested in tests/"})
         except Exception as e:  # pragma: no cover
             cpu = {"error": str(e)}
     plan_txt = plan.serialize().splitlines()
@@ -461,7 +574,8 @@ def main():
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": doc.tensors[doc.inputs[0]][0],
         "data": "synthetic (seeded PCG64, DESIGN.md §4)",
-        "config": {"workload": WORKLOADS[args.config], "plan": regions, "parallelism": f"chunk-split x{world}",
+        "config": {"workload": WORKLOADS[args.config] + (f", {args.layers} stacked blocks" if args.layers > 1 else ""),
+                   "plan": regions, "parallelism": f"chunk-split x{world}",
                    "l2": "flushed between timed steps (256 MiB write)"},
         "peak_activation_bytes": {"planned": profp.peak_bytes, "unchunked": prof0.peak_bytes,
                                   "reduction": round(1 - profp.peak_bytes / prof0.peak_bytes, 4),
@@ -469,6 +583,7 @@ def main():
                                   "arena_plus_caller": st.workspace_high_water + caller},
         "unchunked": unchunked, "roofline": roof, "stages": shares, "cpu_baseline": cpu, "e2e": e2e,
         **({"chunk_sweep": sweep} if sweep else {}),
+        **({"ablation": ablation} if ablation else {}),
         "gpu_launches": st.launches * args.steps, "clocks": clocks,
         "paper": {"claim": ">80% activation reduction at <10% speed loss; <10% loss at 20% memory",
                   "hardware": "A100 80GB, PyTorch (P:336)"},

@@ -78,6 +78,9 @@ typedef struct ac_block_desc {
   int32_t dtype;     /* ac_dtype */
   double ln_eps;     /* LayerNorm epsilon (1e-5) */
   const char* name;  /* graph name in the document; NULL -> kind name */
+  int32_t layers;    /* blocks stacked in sequence (NEXT f3 multi-block plans); 0 or 1 = one
+                        block with the plain ids; L > 1: every id of block i prefixed "L<i>_",
+                        block i + 1 reading block i's output */
 } ac_block_desc;
 
 ac_status ac_graph_block(const ac_block_desc* desc, ac_graph** out);

@@ -14,46 +14,60 @@ import math
 from .graph import Builder, Graph
 
 
-def transformer(N, d, h, f=0, causal=False, dtype="bf16", attn_only=False, name="transformer",
-                eps=1e-5) -> Graph:
-    """Pre-LN block: a = LN1(x); q,k,v = a W + b; softmax(q k^T / sqrt(dh)) v;
-    x1 = x + o Wo + bo; (y = x1 + GELU(LN2(x1) W1 + b1) W2 + b2)."""
+def _transformer_block(B: Builder, d, h, f, causal, attn_only, eps, pre: str, xin: str) -> str:
+    """Pre-LN block reading `xin`: a = LN1(x); q,k,v = a W + b; softmax(q k^T / sqrt(dh)) v;
+    x1 = x + o Wo + bo; (y = x1 + GELU(LN2(x1) W1 + b1) W2 + b2).  Every other id
+    carries the prefix `pre`; returns the output id."""
     dh = d // h
+    P = (lambda s: pre + s)
+    B.weight(P("ln1_g"), (d,), "ln_gamma", d)
+    B.weight(P("ln1_b"), (d,), "ln_beta", d)
+    for nm in ("q", "k", "v", "o"):
+        B.weight(P(f"w{nm}"), (d, d), "matrix", d)
+        B.weight(P(f"b{nm}"), (d,), "bias", d)
+    if not attn_only:
+        B.weight(P("ln2_g"), (d,), "ln_gamma", d)
+        B.weight(P("ln2_b"), (d,), "ln_beta", d)
+        B.weight(P("w1"), (f, d), "matrix", d)
+        B.weight(P("b1"), (f,), "bias", d)
+        B.weight(P("w2"), (d, f), "matrix", f)
+        B.weight(P("b2"), (d,), "bias", f)
+    B.op("layernorm", [xin, P("ln1_g"), P("ln1_b")], P("a"), nid=P("ln1"), naxes=1, eps=eps)
+    B.op("linear", [P("a"), P("wq"), P("bq")], P("q"), nid=P("proj_q"), kin=1, out=[h, dh], act="none",
+         trans=0, swap=0, bias=1, res=0)
+    B.op("linear", [P("a"), P("wk"), P("bk")], P("k"), nid=P("proj_k"), kin=1, out=[h, dh], act="none",
+         trans=0, swap=0, bias=1, res=0)
+    B.op("linear", [P("a"), P("wv"), P("bv")], P("vt"), nid=P("proj_v"), kin=1, out=[h, dh], act="none",
+         trans=1, swap=0, bias=1, res=0)
+    B.op("attn_scores", [P("q"), P("k")], P("s"), nid=P("scores"), scale=1.0 / math.sqrt(dh), causal=int(causal))
+    B.op("softmax", [P("s")], P("p"), nid=P("softmax"), dim=2)
+    B.op("attn_pv", [P("p"), P("vt")], P("o"), nid=P("pv"))
+    B.op("linear", [P("o"), P("wo"), P("bo"), xin], P("x1"), nid=P("proj_o"), kin=2, out=[d], act="none",
+         trans=0, swap=0, bias=1, res=1)
+    if attn_only:
+        return P("x1")
+    B.op("layernorm", [P("x1"), P("ln2_g"), P("ln2_b")], P("c"), nid=P("ln2"), naxes=1, eps=eps)
+    B.op("linear", [P("c"), P("w1"), P("b1")], P("hid"), nid=P("ffn1"), kin=1, out=[f], act="gelu", trans=0,
+         swap=0, bias=1, res=0)
+    B.op("linear", [P("hid"), P("w2"), P("b2"), P("x1")], P("y"), nid=P("ffn2"), kin=1, out=[d], act="none",
+         trans=0, swap=0, bias=1, res=1)
+    return P("y")
+
+
+def _prefix(layers: int, i: int) -> str:
+    """Id prefix of block i in a stack of `layers` blocks (none for a single block)."""
+    return f"L{i}_" if layers > 1 else ""
+
+
+def transformer(N, d, h, f=0, causal=False, dtype="bf16", attn_only=False, name="transformer",
+                eps=1e-5, layers=1) -> Graph:
+    """`layers` pre-LN blocks in sequence (NEXT f3 stacks; one block by default)."""
     B = Builder(name, dtype)
     B.input("x", (N, d))
-    B.weight("ln1_g", (d,), "ln_gamma", d)
-    B.weight("ln1_b", (d,), "ln_beta", d)
-    for nm in ("q", "k", "v", "o"):
-        B.weight(f"w{nm}", (d, d), "matrix", d)
-        B.weight(f"b{nm}", (d,), "bias", d)
-    if not attn_only:
-        B.weight("ln2_g", (d,), "ln_gamma", d)
-        B.weight("ln2_b", (d,), "ln_beta", d)
-        B.weight("w1", (f, d), "matrix", d)
-        B.weight("b1", (f,), "bias", d)
-        B.weight("w2", (d, f), "matrix", f)
-        B.weight("b2", (d,), "bias", f)
-    B.op("layernorm", ["x", "ln1_g", "ln1_b"], "a", nid="ln1", naxes=1, eps=eps)
-    B.op("linear", ["a", "wq", "bq"], "q", nid="proj_q", kin=1, out=[h, dh], act="none", trans=0,
-         swap=0, bias=1, res=0)
-    B.op("linear", ["a", "wk", "bk"], "k", nid="proj_k", kin=1, out=[h, dh], act="none", trans=0,
-         swap=0, bias=1, res=0)
-    B.op("linear", ["a", "wv", "bv"], "vt", nid="proj_v", kin=1, out=[h, dh], act="none", trans=1,
-         swap=0, bias=1, res=0)
-    B.op("attn_scores", ["q", "k"], "s", nid="scores", scale=1.0 / math.sqrt(dh), causal=int(causal))
-    B.op("softmax", ["s"], "p", nid="softmax", dim=2)
-    B.op("attn_pv", ["p", "vt"], "o", nid="pv")
-    B.op("linear", ["o", "wo", "bo", "x"], "x1", nid="proj_o", kin=2, out=[d], act="none", trans=0,
-         swap=0, bias=1, res=1)
-    if attn_only:
-        B.output("x1")
-        return B.build()
-    B.op("layernorm", ["x1", "ln2_g", "ln2_b"], "c", nid="ln2", naxes=1, eps=eps)
-    B.op("linear", ["c", "w1", "b1"], "hid", nid="ffn1", kin=1, out=[f], act="gelu", trans=0, swap=0,
-         bias=1, res=0)
-    B.op("linear", ["hid", "w2", "b2", "x1"], "y", nid="ffn2", kin=1, out=[d], act="none", trans=0,
-         swap=0, bias=1, res=1)
-    B.output("y")
+    x = "x"
+    for i in range(max(1, layers)):
+        x = _transformer_block(B, d, h, f, causal, attn_only, eps, _prefix(layers, i), x)
+    B.output(x)
     return B.build()
 
 
@@ -90,16 +104,21 @@ def _tri_attention(B: Builder, z: str, pre: str, N: int, cz: int, H: int, c: int
          act="none", trans=0, swap=0, bias=1, res=1)
 
 
-def tri_attn_pair(N, cz=128, H=4, c=32, dtype="bf16", name="af_pair") -> Graph:
+def tri_attn_pair(N, cz=128, H=4, c=32, dtype="bf16", name="af_pair", layers=1) -> Graph:
     """Triangle attention around the starting node (rows, Alg. 13) followed by
-    the ending node (columns, Alg. 14), each with its residual add."""
+    the ending node (columns, Alg. 14), each with its residual add; `layers`
+    such pairs in sequence."""
     B = Builder(name, dtype)
     B.input("z", (N, N, cz))
-    _tri_weights(B, "row_", cz, H, c)
-    _tri_weights(B, "col_", cz, H, c)
-    _tri_attention(B, "z", "row_", N, cz, H, c, 0, "z1")
-    _tri_attention(B, "z1", "col_", N, cz, H, c, 1, "z2")
-    B.output("z2")
+    z = "z"
+    for i in range(max(1, layers)):
+        p = _prefix(layers, i)
+        _tri_weights(B, p + "row_", cz, H, c)
+        _tri_weights(B, p + "col_", cz, H, c)
+        _tri_attention(B, z, p + "row_", N, cz, H, c, 0, p + "z1")
+        _tri_attention(B, p + "z1", p + "col_", N, cz, H, c, 1, p + "z2")
+        z = p + "z2"
+    B.output(z)
     return B.build()
 
 
@@ -114,13 +133,13 @@ CONFIGS = {
 }
 
 
-def block(kind, N, d, h, f=0, causal=False, dtype="bf16", name=None) -> Graph:
+def block(kind, N, d, h, f=0, causal=False, dtype="bf16", name=None, layers=1) -> Graph:
     if kind == "transformer":
-        return transformer(N, d, h, f, causal, dtype, False, name or "transformer")
+        return transformer(N, d, h, f, causal, dtype, False, name or "transformer", layers=layers)
     if kind == "attn_only":
-        return transformer(N, d, h, 0, causal, dtype, True, name or "attn_only")
+        return transformer(N, d, h, 0, causal, dtype, True, name or "attn_only", layers=layers)
     if kind == "tri_attn_pair":
-        return tri_attn_pair(N, d, h, f, dtype, name or "af_pair")
+        return tri_attn_pair(N, d, h, f, dtype, name or "af_pair", layers=layers)
     raise ValueError(kind)
 
 

@@ -29,7 +29,8 @@ class ACError(RuntimeError):
 
 class BlockDesc(C.Structure):
     _fields_ = [("kind", C.c_int32), ("N", C.c_int64), ("d", C.c_int64), ("h", C.c_int64), ("f", C.c_int64),
-                ("causal", C.c_int32), ("dtype", C.c_int32), ("ln_eps", C.c_double), ("name", C.c_char_p)]
+                ("causal", C.c_int32), ("dtype", C.c_int32), ("ln_eps", C.c_double), ("name", C.c_char_p),
+                ("layers", C.c_int32)]
 
 
 class MemProfile(C.Structure):

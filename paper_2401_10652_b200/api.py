@@ -56,9 +56,9 @@ def graph_parse(text: str) -> Graph:
 
 
 def graph_block(kind: str, N: int, d: int, h: int, f: int = 0, causal: bool = False, dtype: str = "bf16",
-                ln_eps: float = 1e-5, name: str | None = None) -> Graph:
+                ln_eps: float = 1e-5, name: str | None = None, layers: int = 1) -> Graph:
     desc = L.BlockDesc(KINDS[kind], N, d, h, f, int(causal), DTYPES[dtype], ln_eps,
-                       name.encode() if name else None)
+                       name.encode() if name else None, int(layers))
     out = C.c_void_p()
     check(lib().ac_graph_block(C.byref(desc), C.byref(out)))
     return Graph(out.value)
@@ -235,3 +235,48 @@ class Exec:
         arr = (L.KernelTime * max(n.value, 1))()
         check(lib().ac_exec_kernel_times(self._h, arr, n.value, C.byref(n)))
         return [(a.node.decode(), a.kind.decode(), a.ms, a.launches) for a in arr[: n.value]]
+
+
+def max_length(kind: str, d: int, h: int, f: int, causal: bool, dtype: str, budget: int, layers: int = 1,
+               step: int = 128, cap: int = 1 << 22, params: L.CostParams | None = None) -> dict:
+    """Largest sequence length (multiple of `step`, <= cap) whose unchunked Eq. 1 peak
+    (ac_estimate_memory) and whose ac_plan peak fit `budget` activation bytes, strict
+     - SPEC cmd_maxlen, the paper's max-inference-length extension
+    (P:357-361).  Returns {"unchunked", "chunked", "ratio", "plan"} (plan: ac_plan's
+    regions at the chunked maximum)."""
+    def graph(N):
+        return graph_block(kind, N, d, h, f, causal, dtype, name="maxlen", layers=layers)
+
+    def fits_unchunked(N):
+        prof, _ = estimate_memory(graph(N))
+        return prof.peak_bytes < budget
+
+    def fits_chunked(N):
+        return ac_plan(graph(N), budget, params).feasible
+
+    def largest(fits):
+        if not fits(step):
+            return 0
+        lo, hi = 1, 2  # fits(lo * step) holds; grow hi until it fails or passes the cap
+        while hi * step <= cap and fits(hi * step):
+            lo, hi = hi, 2 * hi
+        if hi * step > cap:
+            top = cap // step
+            if fits(top * step):
+                return top * step
+            hi = top
+        while hi - lo > 1:
+            mid = (lo + hi) // 2
+            if fits(mid * step):
+                lo = mid
+            else:
+                hi = mid
+        return lo * step
+
+    nu = largest(fits_unchunked)
+    nc = largest(fits_chunked)
+    plan = None
+    if nc:
+        p = ac_plan(graph(nc), budget, params)
+        plan = [ln.split(" flow=")[0] for ln in p.serialize().splitlines() if ln.startswith("region")]
+    return {"unchunked": nu, "chunked": nc, "ratio": (nc / nu) if nu else None, "plan": plan}

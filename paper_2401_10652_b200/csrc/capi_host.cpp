@@ -68,8 +68,9 @@ ac_status ac_graph_block(const ac_block_desc* d, ac_graph** out) {
     return set_error(AC_ERR_ARG, "ac_graph_block: sizes must be positive");
   if (d->dtype < 0 || d->dtype > 2) return set_error(AC_ERR_ARG, "ac_graph_block: bad dtype");
   try {
+    if (d->layers < 0 || d->layers > 256) return set_error(AC_ERR_ARG, "ac_graph_block: layers must be 0..256");
     BlockDesc b{d->kind, d->N, d->d, d->h, d->f, d->causal, static_cast<DT>(d->dtype),
-                d->ln_eps > 0 ? d->ln_eps : 1e-5, d->name ? d->name : ""};
+                d->ln_eps > 0 ? d->ln_eps : 1e-5, d->name ? d->name : "", d->layers > 1 ? d->layers : 1};
     *out = new ac_graph{std::make_shared<Graph>(build_block(b))};
     return AC_OK;
   } catch (GraphError& e) {

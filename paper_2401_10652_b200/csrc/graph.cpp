@@ -776,58 +776,74 @@ void tri_attention(GB& b, const std::string& z, const std::string& pre, int64_t 
   b.linear(pre + "proj_o", {pre + "o", pre + "wo", pre + "bo", z}, out, 2, {cz}, "none", 0, 0, 1, 1);
 }
 
+// One pre-LN transformer block reading `xin`, every other id
+// prefixed with `pre`; returns the output tensor id.
+std::string transformer_block(GB& b, const BlockDesc& d, const std::string& pre, const std::string& xin) {
+  const bool attn_only = d.kind == 1;
+  const int64_t D = d.d, h = d.h, f = d.f, dh = D / h;
+  const double eps = d.eps;
+  auto P = [&](const std::string& s) { return pre + s; };
+  b.weight(P("ln1_g"), {D}, "ln_gamma", D);
+  b.weight(P("ln1_b"), {D}, "ln_beta", D);
+  for (const char* nm : {"q", "k", "v", "o"}) {
+    b.weight(P(std::string("w") + nm), {D, D}, "matrix", D);
+    b.weight(P(std::string("b") + nm), {D}, "bias", D);
+  }
+  if (!attn_only) {
+    b.weight(P("ln2_g"), {D}, "ln_gamma", D);
+    b.weight(P("ln2_b"), {D}, "ln_beta", D);
+    b.weight(P("w1"), {f, D}, "matrix", D);
+    b.weight(P("b1"), {f}, "bias", D);
+    b.weight(P("w2"), {D, f}, "matrix", f);
+    b.weight(P("b2"), {D}, "bias", f);
+  }
+  b.op(P("ln1"), "layernorm", {xin, P("ln1_g"), P("ln1_b")}, P("a"), {{"naxes", GB::I(1)}, {"eps", GB::F(eps)}});
+  b.linear(P("proj_q"), {P("a"), P("wq"), P("bq")}, P("q"), 1, {h, dh}, "none", 0, 0, 1, 0);
+  b.linear(P("proj_k"), {P("a"), P("wk"), P("bk")}, P("k"), 1, {h, dh}, "none", 0, 0, 1, 0);
+  b.linear(P("proj_v"), {P("a"), P("wv"), P("bv")}, P("vt"), 1, {h, dh}, "none", 1, 0, 1, 0);
+  b.op(P("scores"), "attn_scores", {P("q"), P("k")}, P("s"),
+       {{"scale", GB::F(1.0 / std::sqrt(static_cast<double>(dh)))}, {"causal", GB::I(d.causal)}});
+  b.op(P("softmax"), "softmax", {P("s")}, P("p"), {{"dim", GB::I(2)}});
+  b.op(P("pv"), "attn_pv", {P("p"), P("vt")}, P("o"), {});
+  b.linear(P("proj_o"), {P("o"), P("wo"), P("bo"), xin}, P("x1"), 2, {D}, "none", 0, 0, 1, 1);
+  if (attn_only) return P("x1");
+  b.op(P("ln2"), "layernorm", {P("x1"), P("ln2_g"), P("ln2_b")}, P("c"), {{"naxes", GB::I(1)}, {"eps", GB::F(eps)}});
+  b.linear(P("ffn1"), {P("c"), P("w1"), P("b1")}, P("hid"), 1, {f}, "gelu", 0, 0, 1, 0);
+  b.linear(P("ffn2"), {P("hid"), P("w2"), P("b2"), P("x1")}, P("y"), 1, {D}, "none", 0, 0, 1, 1);
+  return P("y");
+}
+
 }  // namespace
 
 Graph build_block(const BlockDesc& d) {
   GB b;
   b.dt = d.dtype;
   const double eps = d.eps;
+  const int L = d.layers > 1 ? d.layers : 1;
+  // stacked blocks: block i's ids carry the prefix "L<i>_" (none for a single block)
+  auto pre = [&](int i) { return L > 1 ? "L" + std::to_string(i) + "_" : std::string(); };
   if (d.kind == 0 || d.kind == 1) {
     const bool attn_only = d.kind == 1;
     b.g.name = d.name.empty() ? (attn_only ? "attn_only" : "transformer") : d.name;
-    const int64_t N = d.N, D = d.d, h = d.h, f = d.f, dh = D / h;
-    if (h <= 0 || D % h) fail("d must be a multiple of h");
-    b.input("x", {N, D});
-    b.weight("ln1_g", {D}, "ln_gamma", D);
-    b.weight("ln1_b", {D}, "ln_beta", D);
-    for (const char* nm : {"q", "k", "v", "o"}) {
-      b.weight(std::string("w") + nm, {D, D}, "matrix", D);
-      b.weight(std::string("b") + nm, {D}, "bias", D);
-    }
-    if (!attn_only) {
-      b.weight("ln2_g", {D}, "ln_gamma", D);
-      b.weight("ln2_b", {D}, "ln_beta", D);
-      b.weight("w1", {f, D}, "matrix", D);
-      b.weight("b1", {f}, "bias", D);
-      b.weight("w2", {D, f}, "matrix", f);
-      b.weight("b2", {D}, "bias", f);
-    }
-    b.op("ln1", "layernorm", {"x", "ln1_g", "ln1_b"}, "a", {{"naxes", GB::I(1)}, {"eps", GB::F(eps)}});
-    b.linear("proj_q", {"a", "wq", "bq"}, "q", 1, {h, dh}, "none", 0, 0, 1, 0);
-    b.linear("proj_k", {"a", "wk", "bk"}, "k", 1, {h, dh}, "none", 0, 0, 1, 0);
-    b.linear("proj_v", {"a", "wv", "bv"}, "vt", 1, {h, dh}, "none", 1, 0, 1, 0);
-    b.op("scores", "attn_scores", {"q", "k"}, "s",
-         {{"scale", GB::F(1.0 / std::sqrt(static_cast<double>(dh)))}, {"causal", GB::I(d.causal)}});
-    b.op("softmax", "softmax", {"s"}, "p", {{"dim", GB::I(2)}});
-    b.op("pv", "attn_pv", {"p", "vt"}, "o", {});
-    b.linear("proj_o", {"o", "wo", "bo", "x"}, "x1", 2, {D}, "none", 0, 0, 1, 1);
-    if (attn_only) {
-      b.g.outputs.push_back(b.g.tindex["x1"]);
-    } else {
-      b.op("ln2", "layernorm", {"x1", "ln2_g", "ln2_b"}, "c", {{"naxes", GB::I(1)}, {"eps", GB::F(eps)}});
-      b.linear("ffn1", {"c", "w1", "b1"}, "hid", 1, {f}, "gelu", 0, 0, 1, 0);
-      b.linear("ffn2", {"hid", "w2", "b2", "x1"}, "y", 1, {D}, "none", 0, 0, 1, 1);
-      b.g.outputs.push_back(b.g.tindex["y"]);
-    }
+    if (d.h <= 0 || d.d % d.h) fail("d must be a multiple of h");
+    b.input("x", {d.N, d.d});
+    std::string x = "x";
+    for (int i = 0; i < L; ++i) x = transformer_block(b, d, pre(i), x);
+    b.g.outputs.push_back(b.g.tindex[x]);
   } else if (d.kind == 2) {
     b.g.name = d.name.empty() ? "af_pair" : d.name;
     const int64_t N = d.N, cz = d.d, H = d.h, c = d.f;
     b.input("z", {N, N, cz});
-    tri_weights(b, "row_", cz, H, c);
-    tri_weights(b, "col_", cz, H, c);
-    tri_attention(b, "z", "row_", cz, H, c, 0, "z1", eps);
-    tri_attention(b, "z1", "col_", cz, H, c, 1, "z2", eps);
-    b.g.outputs.push_back(b.g.tindex["z2"]);
+    std::string z = "z";
+    for (int i = 0; i < L; ++i) {
+      const std::string p = pre(i);
+      tri_weights(b, p + "row_", cz, H, c);
+      tri_weights(b, p + "col_", cz, H, c);
+      tri_attention(b, z, p + "row_", cz, H, c, 0, p + "z1", eps);
+      tri_attention(b, p + "z1", p + "col_", cz, H, c, 1, p + "z2", eps);
+      z = p + "z2";
+    }
+    b.g.outputs.push_back(b.g.tindex[z]);
   } else {
     fail("unknown block kind");
   }

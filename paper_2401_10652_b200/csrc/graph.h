@@ -91,6 +91,7 @@ struct BlockDesc {
   DT dtype;
   double eps;
   std::string name;
+  int layers = 1;
 };
 Graph build_block(const BlockDesc& b);
 

@@ -206,3 +206,40 @@ def test_af_fused_softmax_vs_unfused(monkeypatch, nres):
     assert s1.launches == s0.launches
     # (no workspace claim at these sizes: e-tiles pad the rows to 128-row tiles)
     assert gu.rel_err(y1, y0.double().cpu().numpy()) < 1e-2
+
+
+def test_stacked_blocks_multi_region_plan():
+    """NEXT f3: a stack of 3 causal blocks; ac_plan at 20 % and 10 % chunks every
+    block's attention (one region per block, multi-pass DP, P:153; the 10 % plan's
+    32-row chunks take the unaligned masked path); vs the oracle and chunked ==
+    unchunked bitwise."""
+    gu = _gu()
+    from paper_2401_10652_b200 import api
+    og = workloads.transformer(2048, 256, 4, 512, True, "bf16", name="stack", layers=3)
+    cg = gu.c_graph(og)
+    plans = [api.ac_plan(cg, int(fr * memory.profile(og).peak_bytes)) for fr in (0.2, 0.1)]
+    for p in plans:
+        assert p.feasible and p.num_regions >= 3
+    _check_all_plans(og, plans, seed=11)
+
+
+def test_long_sequence_beyond_unchunked_capacity():
+    """NEXT f3: a GPT block at 131072 tokens, whose unchunked activations (> 1 TB)
+    exceed B200 HBM, runs under the plan ac_plan picks for a 96 GiB budget; sampled
+    output rows vs the fp64 oracle."""
+    gu = _gu()
+    from paper_2401_10652_b200 import api
+    N = 131072
+    og = workloads.block("transformer", N, 1024, 16, 4096, True, "bf16", name="gpt_long")
+    assert memory.profile(og).peak_bytes > 200 << 30
+    cg = gu.c_graph(og)
+    plan = api.ac_plan(cg, 96 << 30)
+    assert plan.feasible
+    vals, dev = gu.make_values(og, 0)
+    got, ex = gu.run(cg, plan, og, dev)
+    torch.cuda.synchronize()
+    rows = np.array([0, 1, 4095, 65536, N - 129, N - 1])
+    ref = blocks.transformer_rows(og, vals, rows)
+    err = gu.rel_err(got["y"][torch.from_numpy(rows).cuda()], ref["y"])
+    assert err < 2e-2, err
+    assert ex.stats().planned_peak < 96 << 30

@@ -188,3 +188,58 @@ def test_error_codes():
         assert e.value.status == _lib.AC_ERR_PLAN
     p = api.ac_plan(cg, int(0.2 * memory.profile(workloads.config("tiny")).peak_bytes))
     assert p.status == _lib.AC_ERR_BUDGET and p.num_regions > 0
+
+
+# NEXT f3: stacked blocks (multi-block plans; the DP runs one pass per region as the
+# peak moves from block to block)
+STACKS = [("transformer", 512, 64, 4, 256, True, 3), ("attn_only", 512, 64, 4, 0, False, 2),
+          ("tri_attn_pair", 48, 16, 2, 8, False, 2)]
+
+
+@pytest.mark.parametrize("kind,N,d,h,f,causal,L", STACKS)
+def test_stack_documents_identical(kind, N, d, h, f, causal, L):
+    a = api.graph_block(kind, N, d, h, f, causal, "bf16", name="stack", layers=L).serialize()
+    assert a == og.serialize(workloads.block(kind, N, d, h, f, causal, "bf16", name="stack", layers=L))
+
+
+@pytest.mark.parametrize("kind,N,d,h,f,causal,L", STACKS)
+@pytest.mark.parametrize("frac", [0.5, 0.2, 0.1])
+def test_stack_plans_bit_exact(kind, N, d, h, f, causal, L, frac):
+    og_g = workloads.block(kind, N, d, h, f, causal, "bf16", name="stack", layers=L)
+    budget = int(frac * memory.profile(og_g).peak_bytes)
+    ref = select.select(og_g, budget)
+    g = api.graph_block(kind, N, d, h, f, causal, "bf16", name="stack", layers=L)
+    p = api.ac_plan(g, budget)
+    assert p.serialize() == oplan.serialize(ref, og_g)
+    assert p.feasible == ref.feasible
+    _, per = api.estimate_memory(g, p)
+    assert per == memory.estimate_with_plan(og_g, ref.regions).per_step
+    if ref.feasible and frac <= 0.2:
+        # every block's attention peak had to be chunked: one region per block at least
+        assert p.num_regions >= L
+
+
+# NEXT f3: max inference length under a budget (SPEC cmd_maxlen S:478-486)
+@pytest.mark.parametrize("kind,d,h,f,causal,L,budget,step,cap", [
+    ("transformer", 64, 4, 256, True, 1, 64 << 20, 128, 1 << 20),
+    ("transformer", 64, 4, 256, False, 2, 32 << 20, 128, 1 << 20),
+    ("tri_attn_pair", 16, 2, 8, False, 1, 64 << 20, 8, 1 << 12),
+])
+def test_max_length_matches_oracle(kind, d, h, f, causal, L, budget, step, cap):
+    from oracle import maxlen
+    got = api.max_length(kind, d, h, f, causal, "bf16", budget, layers=L, step=step, cap=cap)
+    ref = maxlen.max_length(kind, d, h, f, causal, "bf16", budget, layers=L, step=step, cap=cap)
+    assert (got["unchunked"], got["chunked"]) == (ref["unchunked"], ref["chunked"])
+    # SPEC AC-4 floors: >= 3x for the 1D attention family, >= 2x for the 2D family
+    assert got["ratio"] >= (2.0 if kind == "tri_attn_pair" else 3.0)
+    # the lengths are maxima: one step more no longer fits
+    g = api.graph_block(kind, got["chunked"] + step, d, h, f, causal, "bf16", name="maxlen", layers=L)
+    assert not api.ac_plan(g, budget).feasible
+    g = api.graph_block(kind, got["unchunked"] + step, d, h, f, causal, "bf16", name="maxlen", layers=L)
+    assert api.estimate_memory(g)[0].peak_bytes >= budget
+
+
+def test_max_length_unbounded_budget_hits_cap():
+    """budget -> infinity: both lengths reach the search cap, ratio 1."""
+    got = api.max_length("transformer", 64, 4, 256, True, "bf16", 1 << 60, step=128, cap=1 << 14)
+    assert got["unchunked"] == got["chunked"] == 1 << 14 and got["ratio"] == 1.0
