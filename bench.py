@@ -34,7 +34,10 @@ WORKLOADS = {
     "af": "AlphaFold triangle attention pair (rows then columns), N_res 1024, c_z 128, 4 heads, c 32, bf16, "
           "budget 20% (tokens = pair positions N_res^2)",
     "tiny": "tiny attention+MLP block, seq 256, hidden 64, 2 heads, fp32, chunk 32 along seq",
+    "gpt_fa": "GPT-style decoder block with fused attention (NEXT f1, P:350-351), seq 16384, hidden 1024, "
+              "16 heads, FFN 4096, causal, bf16, budget 90% of its unchunked activation",
 }
+DEFAULT_BUDGET = {"gpt_fa": 0.9}
 
 
 def parse():
@@ -44,7 +47,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=list(WORKLOADS), default="gpt")
-    ap.add_argument("--budget-frac", type=float, default=0.2)
+    ap.add_argument("--budget-frac", type=float, default=None,
+                    help="activation budget as a fraction of the unchunked peak (default 0.2; gpt_fa 0.9)")
     ap.add_argument("--plan", default=None, help="user plan text (ac_plan_parse) instead of ac_plan")
     ap.add_argument("--no-unchunked", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -125,6 +129,7 @@ BLOCKS = {
     "vit": ("transformer", 65536, 1024, 16, 4096, False, "bf16"),
     "af": ("tri_attn_pair", 1024, 128, 4, 32, False, "bf16"),
     "unet": ("attn_only", 16384, 640, 10, 0, False, "bf16"),
+    "gpt_fa": ("transformer_fa", 16384, 1024, 16, 4096, True, "bf16"),
 }
 
 
@@ -200,6 +205,11 @@ def algorithmic(doc, node_id):
             h, N, M = doc.tensors[ins[0]][1]
             p = h * N * (N + 1) // 2 * (p // (h * N * M))
         return "hbm", p + B(ins[1]) + B(out)
+    if kind == "attn_fused":
+        N, h, dh = doc.tensors[ins[0]][1]
+        Nk = doc.tensors[ins[1]][1][0]
+        pairs = N * (N + 1) // 2 if attrs.get("causal") == "1" else N * Nk
+        return "tensor", 4 * h * dh * pairs
     if kind in ("tri_scores", "tri_pv", "layernorm"):
         return "hbm", sum(B(t) for t in ins) + B(out)
     return "hbm", B(out)
@@ -366,6 +376,8 @@ def main():
         return maxlen_arm(args)
     cg, doc = c_graph(args.config, args.layers)
     prof0, _ = api.estimate_memory(cg)
+    if args.budget_frac is None:
+        args.budget_frac = DEFAULT_BUDGET.get(args.config, 0.2)
     budget = int(args.budget_frac * prof0.peak_bytes)
     if args.plan:
         plan = api.plan_parse(cg, args.plan)
@@ -562,7 +574,8 @@ def main():
     cpu = None
     if not args.no_cpu and not args.profile:
         try:
-            cpu = (cpu_baseline(args.config, oracle_graph(args.config), samples) if args.layers == 1 else
+            base_cfg = "gpt" if args.config == "gpt_fa" else args.config   # same block maths, unfused ids
+            cpu = (cpu_baseline(base_cfg, oracle_graph(base_cfg), samples) if args.layers == 1 else
                    {"note": "oracle row sampler covers one block; stacks are parity-tested in tests/"})
         except Exception as e:  # pragma: no cover
             cpu = {"error": str(e)}

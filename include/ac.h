@@ -63,7 +63,9 @@ ac_status ac_graph_parse(const char* doc, size_t len, ac_graph** out);
 typedef enum ac_block_kind {
   AC_BLOCK_TRANSFORMER = 0,   /* pre-LN attention + GELU FFN (GPT, ViT, tiny) */
   AC_BLOCK_ATTN_ONLY = 1,     /* pre-LN attention + residual only (UNet self-attention) */
-  AC_BLOCK_TRI_ATTN_PAIR = 2  /* AlphaFold triangle attention, starting then ending node */
+  AC_BLOCK_TRI_ATTN_PAIR = 2, /* AlphaFold triangle attention, starting then ending node */
+  AC_BLOCK_TRANSFORMER_FA = 3, /* transformer with attention as one fused kernel (NEXT f1) */
+  AC_BLOCK_ATTN_ONLY_FA = 4    /* attn_only with the fused attention kernel */
 } ac_block_kind;
 
 typedef enum ac_dtype { AC_F32 = 0, AC_BF16 = 1, AC_F64 = 2 } ac_dtype;

@@ -122,7 +122,7 @@ REDUCE = ("reduce_sum", "reduce_mean", "reduce_max")
 SOURCE = ("input", "weight")
 ALL_KINDS = SOURCE + ("matmul",) + ELEMENTWISE2 + UNARY + ("softmax", "layernorm") + REDUCE + (
     "transpose", "reshape", "concat", "slice",
-    "linear", "attn_scores", "attn_pv", "tri_scores", "tri_pv")
+    "linear", "attn_scores", "attn_pv", "tri_scores", "tri_pv", "attn_fused")
 
 # attribute schema: name -> type tag ("int", "float", "ints", "str", "ranges")
 ATTR_SCHEMA = {
@@ -136,13 +136,15 @@ ATTR_SCHEMA = {
     "linear": {"kin": "int", "out": "ints", "act": "str", "trans": "int", "swap": "int",
                "bias": "int", "res": "int"},
     "attn_scores": {"scale": "float", "causal": "int"},
+    "attn_fused": {"scale": "float", "causal": "int"},
     "tri_scores": {"scale": "float", "ending": "int"},
     "tri_pv": {"ending": "int"},
 }
 
 ARITY = {"matmul": (2, 2), "softmax": (1, 1), "layernorm": (3, 3), "transpose": (1, 1),
          "reshape": (1, 1), "concat": (1, 64), "slice": (1, 1), "linear": (2, 4),
-         "attn_scores": (2, 2), "attn_pv": (2, 2), "tri_scores": (3, 3), "tri_pv": (3, 3)}
+         "attn_scores": (2, 2), "attn_pv": (2, 2), "tri_scores": (3, 3), "tri_pv": (3, 3),
+         "attn_fused": (3, 3)}
 for _k in ELEMENTWISE2:
     ARITY[_k] = (2, 2)
 for _k in UNARY + REDUCE:
@@ -261,6 +263,13 @@ def shape(kind: str, attrs: dict, ins) -> tuple:
         if len(p) != 3 or len(vt) != 3 or p[0] != vt[0] or p[2] != vt[2]:
             raise ValueError("attn_pv shape mismatch")
         return (p[1], p[0], vt[1])
+    if kind == "attn_fused":
+        # NEXT f1: attention as one memory-efficient kernel,
+        # o = softmax(q k^T * scale) v with no N x N intermediate
+        q, k, vt = ins
+        if len(q) != 3 or len(k) != 3 or len(vt) != 3 or q[1:] != k[1:] or vt != (k[1], k[2], k[0]):
+            raise ValueError("attn_fused shape mismatch")
+        return q
     if kind == "tri_scores":
         q, k, b = ins
         if len(q) != 4 or len(k) != 4 or len(b) != 3:
@@ -320,6 +329,9 @@ def flops(kind: str, attrs: dict, ins, out) -> int:
     if kind == "attn_pv":
         p = ins[0]
         return 2 * prod(p) * out[2]
+    if kind == "attn_fused":
+        q, k = ins[0], ins[1]
+        return 4 * q[1] * q[0] * k[0] * q[2]   # QK^T + PV of the unfused chain
     if kind == "tri_scores":
         return 2 * ne * ins[0][3] + ne
     if kind == "tri_pv":
@@ -396,6 +408,8 @@ def propagate(kind: str, attrs: dict, ins, out, d: int):
         return [[1, 1], [0, NC], [NC, 0]][d]
     if kind == "attn_pv":
         return [[1, NC], [0, 0], [NC, 1]][d]
+    if kind == "attn_fused":
+        return [[0, NC, NC], [1, 1, 0], [NC, NC, 1]][d]
     if kind == "tri_scores":
         if attrs.get("ending", 0):
             return [[1, 1, NC], [2, 2, 0], [0, NC, 1], [NC, 0, 2]][d]
@@ -473,6 +487,18 @@ def evaluate(kind: str, attrs: dict, vals, ctx=None) -> np.ndarray:
         p, vt = vals
         o = _bdot(p, vt)              # [h, N, dh]
         return np.ascontiguousarray(np.transpose(o, (1, 0, 2)))
+    if kind == "attn_fused":
+        # the unfused chain written out: scores (row offset of a row chunk in ctx,
+        # as for attn_scores' dim 1), softmax over keys, PV
+        q, k, vt = vals
+        c2 = dict(ctx or {})
+        if c2.get("dim") == 0:
+            c2["dim"] = 1        # o's row dim is the scores' row dim
+        elif "dim" in c2:
+            c2.pop("dim")
+        s = evaluate("attn_scores", {"scale": attrs["scale"], "causal": attrs.get("causal", 0)}, [q, k], c2)
+        p = _softmax(s, 2)
+        return evaluate("attn_pv", {}, [p, vt])
     if kind == "tri_scores":
         q, k, b = vals
         sc = attrs["scale"]

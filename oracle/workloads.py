@@ -14,7 +14,7 @@ import math
 from .graph import Builder, Graph
 
 
-def _transformer_block(B: Builder, d, h, f, causal, attn_only, eps, pre: str, xin: str) -> str:
+def _transformer_block(B: Builder, d, h, f, causal, attn_only, eps, pre: str, xin: str, fused=False) -> str:
     """Pre-LN block reading `xin`: a = LN1(x); q,k,v = a W + b; softmax(q k^T / sqrt(dh)) v;
     x1 = x + o Wo + bo; (y = x1 + GELU(LN2(x1) W1 + b1) W2 + b2).  Every other id
     carries the prefix `pre`; returns the output id."""
@@ -39,9 +39,14 @@ def _transformer_block(B: Builder, d, h, f, causal, attn_only, eps, pre: str, xi
          trans=0, swap=0, bias=1, res=0)
     B.op("linear", [P("a"), P("wv"), P("bv")], P("vt"), nid=P("proj_v"), kin=1, out=[h, dh], act="none",
          trans=1, swap=0, bias=1, res=0)
-    B.op("attn_scores", [P("q"), P("k")], P("s"), nid=P("scores"), scale=1.0 / math.sqrt(dh), causal=int(causal))
-    B.op("softmax", [P("s")], P("p"), nid=P("softmax"), dim=2)
-    B.op("attn_pv", [P("p"), P("vt")], P("o"), nid=P("pv"))
+    if fused:  # NEXT f1: memory-efficient attention kernel, no N x N tensor
+        B.op("attn_fused", [P("q"), P("k"), P("vt")], P("o"), nid=P("attn"), scale=1.0 / math.sqrt(dh),
+             causal=int(causal))
+    else:
+        B.op("attn_scores", [P("q"), P("k")], P("s"), nid=P("scores"), scale=1.0 / math.sqrt(dh),
+             causal=int(causal))
+        B.op("softmax", [P("s")], P("p"), nid=P("softmax"), dim=2)
+        B.op("attn_pv", [P("p"), P("vt")], P("o"), nid=P("pv"))
     B.op("linear", [P("o"), P("wo"), P("bo"), xin], P("x1"), nid=P("proj_o"), kin=2, out=[d], act="none",
          trans=0, swap=0, bias=1, res=1)
     if attn_only:
@@ -60,13 +65,14 @@ def _prefix(layers: int, i: int) -> str:
 
 
 def transformer(N, d, h, f=0, causal=False, dtype="bf16", attn_only=False, name="transformer",
-                eps=1e-5, layers=1) -> Graph:
-    """`layers` pre-LN blocks in sequence (NEXT f3 stacks; one block by default)."""
+                eps=1e-5, layers=1, fused=False) -> Graph:
+    """`layers` pre-LN blocks in sequence (NEXT f3 stacks; one block by default);
+    fused: attention as one attn_fused node (NEXT f1)."""
     B = Builder(name, dtype)
     B.input("x", (N, d))
     x = "x"
     for i in range(max(1, layers)):
-        x = _transformer_block(B, d, h, f, causal, attn_only, eps, _prefix(layers, i), x)
+        x = _transformer_block(B, d, h, f, causal, attn_only, eps, _prefix(layers, i), x, fused)
     B.output(x)
     return B.build()
 
@@ -130,6 +136,8 @@ CONFIGS = {
     "af": dict(kind="tri_attn_pair", N=1024, d=128, h=4, f=32, causal=False, dtype="bf16"),
     "unet": dict(kind="attn_only", N=16384, d=640, h=10, f=0, causal=False, dtype="bf16"),
     "unet_h8": dict(kind="attn_only", N=16384, d=640, h=8, f=0, causal=False, dtype="bf16"),
+    # NEXT f1: the GPT block with a fused attention kernel (the paper's second regime)
+    "gpt_fa": dict(kind="transformer_fa", N=16384, d=1024, h=16, f=4096, causal=True, dtype="bf16"),
 }
 
 
@@ -138,6 +146,10 @@ def block(kind, N, d, h, f=0, causal=False, dtype="bf16", name=None, layers=1) -
         return transformer(N, d, h, f, causal, dtype, False, name or "transformer", layers=layers)
     if kind == "attn_only":
         return transformer(N, d, h, 0, causal, dtype, True, name or "attn_only", layers=layers)
+    if kind == "transformer_fa":
+        return transformer(N, d, h, f, causal, dtype, False, name or "transformer_fa", layers=layers, fused=True)
+    if kind == "attn_only_fa":
+        return transformer(N, d, h, 0, causal, dtype, True, name or "attn_only_fa", layers=layers, fused=True)
     if kind == "tri_attn_pair":
         return tri_attn_pair(N, d, h, f, dtype, name or "af_pair", layers=layers)
     raise ValueError(kind)

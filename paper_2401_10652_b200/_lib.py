@@ -17,6 +17,7 @@ STATUS_NAMES = ["AC_OK", "AC_ERR_ARG", "AC_ERR_GRAPH", "AC_ERR_BUDGET", "AC_ERR_
                 "AC_ERR_BIND", "AC_ERR_CUDA", "AC_ERR_NCCL", "AC_ERR_WORKSPACE"]
 AC_F32, AC_BF16, AC_F64 = 0, 1, 2
 AC_BLOCK_TRANSFORMER, AC_BLOCK_ATTN_ONLY, AC_BLOCK_TRI_ATTN_PAIR = 0, 1, 2
+AC_BLOCK_TRANSFORMER_FA, AC_BLOCK_ATTN_ONLY_FA = 3, 4
 AC_FLAG_NO_HOIST, AC_FLAG_NO_DENSITY, AC_FLAG_NO_STRIDE, AC_FLAG_NO_NODES, AC_FLAG_NO_FLOPS, \
     AC_FLAG_CONTIGUITY = 1, 2, 4, 8, 16, 32
 

@@ -17,7 +17,8 @@ from ._lib import check, lib
 
 DTYPES = {"f32": L.AC_F32, "bf16": L.AC_BF16, "f64": L.AC_F64}
 KINDS = {"transformer": L.AC_BLOCK_TRANSFORMER, "attn_only": L.AC_BLOCK_ATTN_ONLY,
-         "tri_attn_pair": L.AC_BLOCK_TRI_ATTN_PAIR}
+         "tri_attn_pair": L.AC_BLOCK_TRI_ATTN_PAIR, "transformer_fa": L.AC_BLOCK_TRANSFORMER_FA,
+         "attn_only_fa": L.AC_BLOCK_ATTN_ONLY_FA}
 
 
 class Graph:

@@ -1,0 +1,380 @@
+// NEXT f1: fused (memory-efficient) attention for sm_100a, o = softmax(q k^T * scale) v
+// with no N x N tensor in HBM (the "fused attention kernel" regime of the paper,
+// P:350-351; the graph node kind attn_fused).  One CTA per SM, persistent over
+// (head, 128-row query tile) work tiles, causal tiles heaviest first.
+//
+//   warp 0     : TMA producer - Q tile once per work tile, K / V^T blocks of 128
+//                keys through a 3-stage ring (128B swizzle)
+//   warp 1     : TMEM allocator + MMA issuer: S_j = Q K_j^T into one of two TMEM
+//                S buffers (M=128, N=128, K=64), O += P_j V_j (M=128, N=64, K=128)
+//                into the TMEM O accumulator; order S_0, S_1, PV_0, S_2, PV_1, ...
+//   warps 2..5 : softmax, thread = query row: online max / sum in the log2 domain
+//                (x = s * scale * log2 e), P_j = 2^(x - m) rounded to bf16 into a
+//                shared-memory A operand (128B-swizzled, two 64-key k-blocks), the
+//                O accumulator rescaled by 2^(m_old - m_new) in TMEM before PV_j,
+//                and at the end o = O / l stored as bf16.
+// Same arithmetic whatever chunk a query row falls in (the key loop and its order
+// depend only on the global row), so chunked == unchunked bitwise.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace ac {
+
+namespace {
+
+constexpr int FA_BM = 128;   // query rows per tile
+constexpr int FA_BN = 128;   // keys per block
+constexpr int FA_DH = 64;    // head dim (one 128-byte swizzle row)
+constexpr int FA_STG = 3;    // K/V ring depth
+constexpr int FA_THREADS = 192;
+constexpr int Q_BYTES = FA_BM * FA_DH * 2;        // 16 KB
+constexpr int K_BYTES = FA_BN * FA_DH * 2;        // 16 KB
+constexpr int V_BYTES = FA_DH * FA_BN * 2;        // 16 KB (two 64-key boxes of 8 KB)
+constexpr int P_BYTES = FA_BM * FA_BN * 2;        // 32 KB (two 64-key k-blocks of 16 KB)
+constexpr int FA_SMEM = 1024 + Q_BYTES + FA_STG * (K_BYTES + V_BYTES) + 2 * P_BYTES + 256;
+
+struct alignas(64) FaArgs {
+  CUtensorMap tq, tk, tv;
+  __nv_bfloat16* out;
+  long long o_srow, o_sh;
+  int M, Nk, H;
+  int MT;
+  int causal;
+  long long row_off;
+  float cl;  // scale * log2(e)
+};
+
+__global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_constant__ FaArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + Q_BYTES;
+  uint8_t* sV = sK + FA_STG * K_BYTES;
+  uint8_t* sP = sV + FA_STG * V_BYTES;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 2 * P_BYTES);
+  uint64_t* q_full = bar;
+  uint64_t* q_empty = bar + 1;
+  uint64_t* kv_full = bar + 2;              // [FA_STG]
+  uint64_t* kv_empty = bar + 2 + FA_STG;    // [FA_STG]
+  uint64_t* s_full = bar + 2 + 2 * FA_STG;  // [2]
+  uint64_t* s_free = s_full + 2;            // [2]
+  uint64_t* p_full = s_full + 4;            // [2]
+  uint64_t* o_done = s_full + 6;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_full + 7);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total = a.H * a.MT;
+  if (threadIdx.x == 0) {
+    ptx::prefetch_tmap(&a.tq);
+    ptx::prefetch_tmap(&a.tk);
+    ptx::prefetch_tmap(&a.tv);
+    ptx::mbar_init(q_full, 1);
+    ptx::mbar_init(q_empty, 1);
+    for (int s = 0; s < FA_STG; ++s) {
+      ptx::mbar_init(&kv_full[s], 1);
+      ptx::mbar_init(&kv_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&s_full[b], 1);
+      ptx::mbar_init(&s_free[b], 4);
+      ptx::mbar_init(&p_full[b], 4);
+    }
+    ptx::mbar_init(o_done, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_holder);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_holder;  // S buffers at columns 0 / 128, O at 256
+
+  // work tile t -> (head, m-tile, key blocks); causal: heaviest (last) m-tiles first
+  auto tile = [&](int t, int& head, int& mt, int& nkb) {
+    const int r = t / a.H;
+    head = t - r * a.H;
+    mt = a.causal ? a.MT - 1 - r : r;
+    long long kend = a.Nk;
+    if (a.causal) {
+      const long long e = a.row_off + static_cast<long long>(mt + 1) * FA_BM;
+      if (e < kend) kend = e;
+    }
+    nkb = static_cast<int>((kend + FA_BN - 1) / FA_BN);
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0, qph = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        int head, mt, nkb;
+        tile(t, head, mt, nkb);
+        ptx::mbar_wait(q_empty, qph ^ 1);
+        qph ^= 1;
+        ptx::mbar_expect_tx(q_full, Q_BYTES);
+        ptx::tma_load_4d(sQ, &a.tq, q_full, 0, mt * FA_BM, head, 0);
+        for (int j = 0; j < nkb; ++j) {
+          ptx::mbar_wait(&kv_empty[st], ph ^ 1);
+          ptx::mbar_expect_tx(&kv_full[st], K_BYTES + V_BYTES);
+          ptx::tma_load_4d(sK + st * K_BYTES, &a.tk, &kv_full[st], 0, j * FA_BN, head, 0);
+          ptx::tma_load_4d(sV + st * V_BYTES, &a.tv, &kv_full[st], j * FA_BN, 0, head, 0);
+          ptx::tma_load_4d(sV + st * V_BYTES + V_BYTES / 2, &a.tv, &kv_full[st], j * FA_BN + 64, 0, head, 0);
+          if (++st == FA_STG) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t IDS = ptx::idesc_bf16(FA_BM, FA_BN);
+    constexpr uint32_t IDO = ptx::idesc_bf16(FA_BM, FA_DH);
+    int st = 0;
+    uint32_t ph = 0, qph = 0;
+    int sidx = 0;  // S blocks issued by this CTA
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int head, mt, nkb;
+      tile(t, head, mt, nkb);
+      ptx::mbar_wait(q_full, qph);
+      qph ^= 1;
+      ptx::tc_fence_after();
+      int pst = st;          // stage of the pending PV
+      int pidx = sidx;       // block index of the pending PV
+      for (int j = 0; j <= nkb; ++j) {
+        if (j < nkb) {
+          const int b = sidx & 1;
+          ptx::mbar_wait(&kv_full[st], ph);
+          ptx::mbar_wait(&s_free[b], ((sidx >> 1) & 1) ^ 1);
+          ptx::tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sa = ptx::smem_u32(sQ), sb = ptx::smem_u32(sK + st * K_BYTES);
+#pragma unroll
+            for (int k = 0; k < FA_DH / 16; ++k)
+              ptx::mma_bf16(tmem + b * FA_BN, ptx::sdesc_sw128(sa + k * 32), ptx::sdesc_sw128(sb + k * 32), IDS,
+                            k ? 1u : 0u);
+            ptx::mma_commit(&s_full[b]);
+            if (j == nkb - 1) ptx::mma_commit(q_empty);  // Q no longer read in this tile
+          }
+          __syncwarp();
+        }
+        if (j >= 1) {
+          // PV of block j - 1 (stage pst, P buffer pidx & 1)
+          const int b = pidx & 1;
+          ptx::mbar_wait(&p_full[b], (pidx >> 1) & 1);
+          ptx::tc_fence_after();
+          if (lane == 0) {
+            const uint32_t pa = ptx::smem_u32(sP + b * P_BYTES), vb = ptx::smem_u32(sV + pst * V_BYTES);
+#pragma unroll
+            for (int k = 0; k < FA_BN / 16; ++k) {
+              const int kb = k >> 2, kk = k & 3;
+              ptx::mma_bf16(tmem + 256, ptx::sdesc_sw128(pa + kb * (P_BYTES / 2) + kk * 32),
+                            ptx::sdesc_sw128(vb + kb * (V_BYTES / 2) + kk * 32), IDO, (j > 1 || k) ? 1u : 0u);
+            }
+            ptx::mma_commit(&kv_empty[pst]);
+            ptx::mma_commit(o_done);
+          }
+          __syncwarp();
+          pidx = sidx;
+          pst = st;
+        }
+        if (j < nkb) {
+          if (j == 0) { pidx = sidx; pst = st; }
+          ++sidx;
+          if (++st == FA_STG) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else {
+    // softmax warps: thread = query row r of the tile (TMEM lane quarter = warp % 4)
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t lrow = static_cast<uint32_t>(quarter * 32) << 16;
+    int sidx = 0;
+    int pv = 0;  // PV completions awaited so far (o_done phase)
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int head, mt, nkb;
+      tile(t, head, mt, nkb);
+      const long long qg = a.row_off + static_cast<long long>(mt) * FA_BM + r;  // global query row
+      float m = -CUDART_INF_F, l = 0.f;
+      for (int j = 0; j < nkb; ++j) {
+        const int b = sidx & 1;
+        ptx::mbar_wait(&s_full[b], (sidx >> 1) & 1);
+        ptx::tc_fence_after();
+        uint32_t s[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ptx::tmem_ld32(tmem + lrow + b * FA_BN + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]));
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&s_free[b]);
+        // mask: causal keys past the row, keys past Nk
+        const long long k0 = static_cast<long long>(j) * FA_BN;
+        long long lim = a.Nk - 1 - k0;  // last valid column of this block
+        if (a.causal && qg - k0 < lim) lim = qg - k0;
+        float mb = -CUDART_INF_F;
+        if (lim >= FA_BN - 1) {
+#pragma unroll
+          for (int c = 0; c < 128; ++c) mb = fmaxf(mb, __uint_as_float(s[c]));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 128; ++c) {
+            if (c > lim) s[c] = __float_as_uint(-CUDART_INF_F);
+            mb = fmaxf(mb, __uint_as_float(s[c]));
+          }
+        }
+        const float m_new = fmaxf(m, mb * a.cl);
+        const float mref = m_new == -CUDART_INF_F ? 0.f : m_new;
+        const float alpha = m == -CUDART_INF_F ? 0.f : ptx::ex2(m - mref);
+        float ls = 0.f;
+        uint32_t pk[64];
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          const float e0 = ptx::ex2(fmaf(__uint_as_float(s[2 * c]), a.cl, -mref));
+          const float e1 = ptx::ex2(fmaf(__uint_as_float(s[2 * c + 1]), a.cl, -mref));
+          ls += e0 + e1;
+          __nv_bfloat162 h = __floats2bfloat162_rn(e0, e1);
+          pk[c] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        l = l * alpha + ls;
+        m = m_new;
+        if (j >= 1) {
+          // PV_{j-1} done: O may be rescaled and P buffer b (last read by PV_{j-2}) rewritten
+          ptx::mbar_wait(o_done, pv & 1);
+          ++pv;
+          ptx::tc_fence_after();
+          uint32_t o[32];
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            ptx::tmem_ld32(tmem + lrow + 256 + h2 * 32, o);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
+            ptx::tmem_st32(tmem + lrow + 256 + h2 * 32, o);
+          }
+          ptx::tmem_st_wait();
+        }
+        uint8_t* pb = sP + b * P_BYTES + r * 128;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {  // 16 chunks of 8 keys: k-block c / 8, chunk c % 8
+          const uint32_t addr = ptx::smem_u32(pb + (c >> 3) * (P_BYTES / 2) + (((c & 7) ^ (r & 7)) * 16));
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[4 * c]), "r"(pk[4 * c + 1]),
+                       "r"(pk[4 * c + 2]), "r"(pk[4 * c + 3])
+                       : "memory");
+        }
+        ptx::fence_proxy_async_smem();  // generic-proxy P writes -> visible to the tensor core
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&p_full[b]);
+        ++sidx;
+      }
+      // epilogue: wait for the last PV, o = O / l
+      ptx::mbar_wait(o_done, pv & 1);
+      ++pv;
+      ptx::tc_fence_after();
+      uint32_t o[64];
+      ptx::tmem_ld32(tmem + lrow + 256, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
+      ptx::tmem_ld32(tmem + lrow + 256 + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
+      ptx::tmem_ld_wait();
+      ptx::tc_fence_before();
+      const int mrow = mt * FA_BM + r;
+      if (mrow < a.M) {
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        uint4* dst = reinterpret_cast<uint4*>(a.out + static_cast<long long>(mrow) * a.o_srow +
+                                              static_cast<long long>(head) * a.o_sh);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 2 * e]) * inv,
+                                                     __uint_as_float(o[8 * c + 2 * e + 1]) * inv);
+            w[e] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          dst[c] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// bf16 map {inner (contiguous), rows, heads, 1} with element strides, box {64, box_rows, 1, 1}
+// (rank 4 to match the 4-D TMA instruction the kernel issues)
+bool map3(CUtensorMap* m, const void* p, long long inner, long long rows, long long heads, long long srow,
+          long long sh, int box_rows) {
+  EncodeFn enc = encode_fn();
+  if (!enc || (reinterpret_cast<uintptr_t>(p) & 15)) return false;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(heads), 1};
+  const long long big = ((sh * heads + srow * rows) * 2 + 15) / 16 * 16;
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(srow * 2), static_cast<cuuint64_t>(sh * 2),
+                           static_cast<cuuint64_t>(big)};
+  if (strides[0] % 16 || strides[1] % 16 || !strides[0] || !strides[1]) return false;
+  cuuint32_t box[4] = {64, static_cast<cuuint32_t>(box_rows), 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(p), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+cudaError_t attn_fused(const AttnFusedProblem& p, cudaStream_t s) {
+  if (p.M <= 0 || p.Nk <= 0 || p.H <= 0) return cudaSuccess;
+  if (p.dh != FA_DH) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  FaArgs a;
+  memset(&a, 0, sizeof(a));
+  // q [M, H, dh] / k [Nk, H, dh]: inner dh; vt [H, dh, Nk]: inner keys, rows dh
+  if (!map3(&a.tq, p.q, FA_DH, p.M, p.H, p.q_srow, p.q_sh, FA_BM) ||
+      !map3(&a.tk, p.k, FA_DH, p.Nk, p.H, p.k_srow, p.k_sh, FA_BN) ||
+      !map3(&a.tv, p.vt, p.Nk, FA_DH, p.H, p.v_sdh, p.v_sh, FA_DH))
+    return cudaErrorInvalidValue;
+  if ((reinterpret_cast<uintptr_t>(p.out) & 15) || p.o_srow % 8 || p.o_sh % 8) return cudaErrorInvalidValue;
+  a.out = static_cast<__nv_bfloat16*>(p.out);
+  a.o_srow = p.o_srow;
+  a.o_sh = p.o_sh;
+  a.M = static_cast<int>(p.M);
+  a.Nk = static_cast<int>(p.Nk);
+  a.H = static_cast<int>(p.H);
+  a.MT = static_cast<int>((p.M + FA_BM - 1) / FA_BM);
+  a.causal = p.causal;
+  a.row_off = p.row_off;
+  a.cl = p.scale * 1.4426950408889634f;
+  const long long tiles = static_cast<long long>(a.H) * a.MT;
+  const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
+  attn_fused_kernel<<<grid, FA_THREADS, FA_SMEM, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace ac

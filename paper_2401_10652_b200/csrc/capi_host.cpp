@@ -64,7 +64,7 @@ ac_status ac_graph_parse(const char* doc, size_t len, ac_graph** out) {
 ac_status ac_graph_block(const ac_block_desc* d, ac_graph** out) {
   if (!d || !out) return set_error(AC_ERR_ARG, "ac_graph_block: NULL argument");
   *out = nullptr;
-  if (d->N < 1 || d->d < 1 || d->h < 1 || (d->kind != AC_BLOCK_ATTN_ONLY && d->f < 1))
+  if (d->N < 1 || d->d < 1 || d->h < 1 || (d->kind != AC_BLOCK_ATTN_ONLY && d->kind != AC_BLOCK_ATTN_ONLY_FA && d->f < 1))
     return set_error(AC_ERR_ARG, "ac_graph_block: sizes must be positive");
   if (d->dtype < 0 || d->dtype > 2) return set_error(AC_ERR_ARG, "ac_graph_block: bad dtype");
   try {

@@ -312,6 +312,7 @@ Arena build_arena(const Graph& g, const Plan& plan) {
 
 bool gpu_kind(const std::string& k) {
   return k == "layernorm" || k == "linear" || k == "attn_scores" || k == "softmax" || k == "attn_pv" ||
+         k == "attn_fused" ||
          k == "tri_scores" || k == "tri_pv";
 }
 
@@ -443,6 +444,23 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
     const int64_t rows = extent(x, 0, x.nd - 1);
     err = softmax_rows(x.p, out.p, rows, x.sh[x.nd - 1], ld, gst, ldo, gsto, cx.fast ? 1 : 0, cx.row_off, group,
                        dtc, s);
+  } else if (k == "attn_fused") {
+    // NEXT f1: one fused attention kernel, no S / P tensors
+    const View &q = in(0), &kk = in(1), &vt = in(2);
+    if (e->dt != DT::BF16) return unsup("fused attention needs bf16");
+    if (q.st[2] != 1 || kk.st[2] != 1 || vt.st[2] != 1 || out.st[2] != 1) return unsup("head dim not contiguous");
+    AttnFusedProblem p;
+    p.q = q.p; p.k = kk.p; p.vt = vt.p; p.out = out.p;
+    p.M = q.sh[0]; p.H = q.sh[1]; p.dh = q.sh[2]; p.Nk = kk.sh[0];
+    p.q_srow = q.st[0]; p.q_sh = q.st[1];
+    p.k_srow = kk.st[0]; p.k_sh = kk.st[1];
+    p.v_sh = vt.st[0]; p.v_sdh = vt.st[1];
+    p.o_srow = out.st[0]; p.o_sh = out.st[1];
+    p.scale = static_cast<float>(n.af("scale", 1.0));
+    p.causal = static_cast<int>(n.ai("causal"));
+    p.row_off = cx.row_off;
+    if (p.dh != 64) return unsup("fused attention kernel takes head dim 64");
+    err = attn_fused(p, s);
   } else {
     GemmProblem p;
     Epilogue& ep = p.ep;
@@ -687,7 +705,7 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
 // query-row dim of a node's output in an attention chain (causal offsets)
 int rows_dim(const Node& n) {
   if (n.kind == "attn_scores" || n.kind == "softmax") return 1;
-  if (n.kind == "attn_pv") return 0;
+  if (n.kind == "attn_pv" || n.kind == "attn_fused") return 0;
   return -1;
 }
 

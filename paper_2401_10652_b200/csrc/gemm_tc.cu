@@ -1352,7 +1352,17 @@ int num_sms() {
 cudaError_t gemm_tc(const GemmProblem& p, cudaStream_t s, int bn_hint) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0 || p.B1 <= 0 || p.B2 <= 0) return cudaErrorInvalidValue;
   int bn = bn_hint;
-  if (bn == 0) bn = p.N <= 32 ? 32 : p.N <= 64 ? 64 : p.N <= 128 ? 128 : 256;
+  if (bn == 0) {
+    bn = p.N <= 32 ? 32 : p.N <= 64 ? 64 : p.N <= 128 ? 128 : 256;
+    if (!p.ep.stats && !p.fuse_stats) {
+      // short-M GEMMs (a row chunk of a linear): narrower tiles until the grid covers
+      // the SMs (M = 1024, N = 1024: 32 tiles at BN = 256, 128 at BN = 64)
+      auto tiles = [&](int b) {
+        return static_cast<long long>((p.M + 127) / 128) * ((p.N + b - 1) / b) * p.B1 * p.B2;
+      };
+      while (bn > 64 && tiles(bn) < num_sms()) bn /= 2;
+    }
+  }
   if (p.fuse_stats) return p.N <= 32 ? launch<32, 2>(p, s) : bn == 64 ? launch<64, 2>(p, s) : cudaErrorInvalidValue;
   if (p.ep.stats && p.ep.add) {
     switch (bn) {

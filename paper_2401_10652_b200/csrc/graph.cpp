@@ -79,6 +79,7 @@ const std::map<std::string, std::map<std::string, Attr::Kind>>& schema() {
        {{"kin", Attr::INT}, {"out", Attr::INTS}, {"act", Attr::STR}, {"trans", Attr::INT}, {"swap", Attr::INT},
         {"bias", Attr::INT}, {"res", Attr::INT}}},
       {"attn_scores", {{"scale", Attr::FLOAT}, {"causal", Attr::INT}}},
+      {"attn_fused", {{"scale", Attr::FLOAT}, {"causal", Attr::INT}}},
       {"tri_scores", {{"scale", Attr::FLOAT}, {"ending", Attr::INT}}},
       {"tri_pv", {{"ending", Attr::INT}}},
   };
@@ -89,7 +90,7 @@ const std::set<std::string>& kinds() {
   static const std::set<std::string> k = {"matmul", "add", "sub", "mul", "div", "relu", "gelu", "exp", "sigmoid",
                                           "softmax", "layernorm", "reduce_sum", "reduce_mean", "reduce_max",
                                           "transpose", "reshape", "concat", "slice", "linear", "attn_scores",
-                                          "attn_pv", "tri_scores", "tri_pv"};
+                                          "attn_pv", "tri_scores", "tri_pv", "attn_fused"};
   return k;
 }
 
@@ -100,7 +101,7 @@ std::pair<int, int> arity(const Node& n) {
     return {a, a};
   }
   if (k == "concat") return {1, 64};
-  if (k == "layernorm" || k == "tri_scores" || k == "tri_pv") return {3, 3};
+  if (k == "layernorm" || k == "tri_scores" || k == "tri_pv" || k == "attn_fused") return {3, 3};
   if (k == "matmul" || is_elem2(k) || k == "attn_scores" || k == "attn_pv") return {2, 2};
   return {1, 1};
 }
@@ -236,6 +237,13 @@ Shape op_shape(const std::string& k, const Node& n, const std::vector<Shape>& in
     if (p.size() != 3 || vt.size() != 3 || p[0] != vt[0] || p[2] != vt[2]) fail("attn_pv shape mismatch");
     return {p[1], p[0], vt[1]};
   }
+  if (k == "attn_fused") {  // NEXT f1: o = softmax(q k^T scale) v in one kernel
+    const Shape &q = in[0], &kk = in[1], &vt = in[2];
+    if (q.size() != 3 || kk.size() != 3 || vt.size() != 3 || q[1] != kk[1] || q[2] != kk[2] || vt[0] != kk[1] ||
+        vt[1] != kk[2] || vt[2] != kk[0])
+      fail("attn_fused shape mismatch");
+    return q;
+  }
   if (k == "tri_scores") {
     const Shape &q = in[0], &kk = in[1], &b = in[2];
     if (q.size() != 4 || kk.size() != 4 || b.size() != 3) fail("tri_scores rank");
@@ -280,6 +288,7 @@ int64_t op_flops(const std::string& k, const Node& n, const std::vector<Shape>& 
   }
   if (k == "attn_scores") return 2 * ne * in[0][2];
   if (k == "attn_pv") return 2 * prod(in[0]) * out[2];
+  if (k == "attn_fused") return 4 * in[0][1] * in[0][0] * in[1][0] * in[0][2];
   if (k == "tri_scores") return 2 * ne * in[0][3] + ne;
   if (k == "tri_pv") return 2 * prod(in[0]) * out[3] + ne;
   fail("unknown op kind " + k);
@@ -344,6 +353,10 @@ std::vector<int> op_propagate(const std::string& k, const Node& n, const std::ve
   if (k == "attn_pv") {
     static const int t[3][2] = {{1, NC}, {0, 0}, {NC, 1}};
     return {t[d][0], t[d][1]};
+  }
+  if (k == "attn_fused") {
+    static const int t[3][3] = {{0, NC, NC}, {1, 1, 0}, {NC, NC, 1}};
+    return {t[d][0], t[d][1], t[d][2]};
   }
   if (k == "tri_scores") {
     static const int e0[4][3] = {{0, 0, NC}, {2, 2, 0}, {1, NC, 1}, {NC, 1, 2}};
@@ -779,7 +792,8 @@ void tri_attention(GB& b, const std::string& z, const std::string& pre, int64_t 
 // One pre-LN transformer block reading `xin`, every other id
 // prefixed with `pre`; returns the output tensor id.
 std::string transformer_block(GB& b, const BlockDesc& d, const std::string& pre, const std::string& xin) {
-  const bool attn_only = d.kind == 1;
+  const bool attn_only = d.kind == 1 || d.kind == 4;
+  const bool fused = d.kind == 3 || d.kind == 4;
   const int64_t D = d.d, h = d.h, f = d.f, dh = D / h;
   const double eps = d.eps;
   auto P = [&](const std::string& s) { return pre + s; };
@@ -801,10 +815,15 @@ std::string transformer_block(GB& b, const BlockDesc& d, const std::string& pre,
   b.linear(P("proj_q"), {P("a"), P("wq"), P("bq")}, P("q"), 1, {h, dh}, "none", 0, 0, 1, 0);
   b.linear(P("proj_k"), {P("a"), P("wk"), P("bk")}, P("k"), 1, {h, dh}, "none", 0, 0, 1, 0);
   b.linear(P("proj_v"), {P("a"), P("wv"), P("bv")}, P("vt"), 1, {h, dh}, "none", 1, 0, 1, 0);
-  b.op(P("scores"), "attn_scores", {P("q"), P("k")}, P("s"),
-       {{"scale", GB::F(1.0 / std::sqrt(static_cast<double>(dh)))}, {"causal", GB::I(d.causal)}});
-  b.op(P("softmax"), "softmax", {P("s")}, P("p"), {{"dim", GB::I(2)}});
-  b.op(P("pv"), "attn_pv", {P("p"), P("vt")}, P("o"), {});
+  if (fused) {  // NEXT f1: memory-efficient attention kernel, no N x N tensor
+    b.op(P("attn"), "attn_fused", {P("q"), P("k"), P("vt")}, P("o"),
+         {{"scale", GB::F(1.0 / std::sqrt(static_cast<double>(dh)))}, {"causal", GB::I(d.causal)}});
+  } else {
+    b.op(P("scores"), "attn_scores", {P("q"), P("k")}, P("s"),
+         {{"scale", GB::F(1.0 / std::sqrt(static_cast<double>(dh)))}, {"causal", GB::I(d.causal)}});
+    b.op(P("softmax"), "softmax", {P("s")}, P("p"), {{"dim", GB::I(2)}});
+    b.op(P("pv"), "attn_pv", {P("p"), P("vt")}, P("o"), {});
+  }
   b.linear(P("proj_o"), {P("o"), P("wo"), P("bo"), xin}, P("x1"), 2, {D}, "none", 0, 0, 1, 1);
   if (attn_only) return P("x1");
   b.op(P("ln2"), "layernorm", {P("x1"), P("ln2_g"), P("ln2_b")}, P("c"), {{"naxes", GB::I(1)}, {"eps", GB::F(eps)}});
@@ -822,9 +841,9 @@ Graph build_block(const BlockDesc& d) {
   const int L = d.layers > 1 ? d.layers : 1;
   // stacked blocks: block i's ids carry the prefix "L<i>_" (none for a single block)
   auto pre = [&](int i) { return L > 1 ? "L" + std::to_string(i) + "_" : std::string(); };
-  if (d.kind == 0 || d.kind == 1) {
-    const bool attn_only = d.kind == 1;
-    b.g.name = d.name.empty() ? (attn_only ? "attn_only" : "transformer") : d.name;
+  if (d.kind == 0 || d.kind == 1 || d.kind == 3 || d.kind == 4) {
+    static const char* names[] = {"transformer", "attn_only", "", "transformer_fa", "attn_only_fa"};
+    b.g.name = d.name.empty() ? names[d.kind] : d.name;
     if (d.h <= 0 || d.d % d.h) fail("d must be a multiple of h");
     b.input("x", {d.N, d.d});
     std::string x = "x";

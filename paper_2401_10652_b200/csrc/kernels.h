@@ -110,6 +110,23 @@ struct GemmProblem {
   int* tsched = nullptr;
 };
 
+// NEXT f1: fused attention o = softmax(q k^T * scale) v, no N x N tensor (attn_fused.cu).
+// q [M, H, dh] (row stride q_srow, head stride q_sh; dh contiguous), k [Nk, H, dh],
+// vt [H, dh, Nk] (keys contiguous), out [M, H, dh]; element strides.  dh = 64.
+// causal: key j > row_off + m masked (row_off = global row of local row 0).
+struct AttnFusedProblem {
+  const void* q = nullptr;
+  const void* k = nullptr;
+  const void* vt = nullptr;
+  void* out = nullptr;
+  int64_t M = 0, Nk = 0, H = 0, dh = 0;
+  int64_t q_srow = 0, q_sh = 0, k_srow = 0, k_sh = 0, v_sh = 0, v_sdh = 0, o_srow = 0, o_sh = 0;
+  float scale = 1.f;
+  int causal = 0;
+  int64_t row_off = 0;
+};
+cudaError_t attn_fused(const AttnFusedProblem& p, cudaStream_t s);
+
 // bf16 x bf16 -> fp32 (TMEM) -> bf16, tcgen05 + TMA, sm_100a.  Returns a
 // cudaError_t (cudaErrorInvalidValue for shapes it cannot take).
 cudaError_t gemm_tc(const GemmProblem& p, cudaStream_t s, int bn_hint = 0);

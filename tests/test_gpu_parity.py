@@ -243,3 +243,34 @@ def test_long_sequence_beyond_unchunked_capacity():
     err = gu.rel_err(got["y"][torch.from_numpy(rows).cuda()], ref["y"])
     assert err < 2e-2, err
     assert ex.stats().planned_peak < 96 << 30
+
+
+@pytest.mark.parametrize("N,causal", [(1024, True), (1024 + 96, True), (768, False), (200, True)])
+def test_fused_attention_block(N, causal):
+    """NEXT f1: the transformer block with attention as one fused kernel (no N x N
+    tensor) vs the fp64 oracle; row-chunked plans (attention and FFN
+    regions, ragged) equal the unchunked run bitwise."""
+    og = workloads.block("transformer_fa", N, 256, 4, 1024, causal, "bf16", name="gpt_fa")
+    _check_all_plans(og, [
+        "autochunk-plan 1\nregion s=attn e=ffn2 n=4 dims=0\n",
+        "autochunk-plan 1\nregion s=ln2 e=ffn2 n=3 dims=0\n",
+        "autochunk-plan 1\nregion s=proj_q e=proj_o n=5 dims=0\n",
+    ], seed=4)
+
+
+def test_fused_attention_regime_plan():
+    """NEXT f1 at the GPT config: ac_plan under a budget below the fused block's
+    unchunked peak chunks the FFN-side intermediates; sampled rows vs the oracle."""
+    gu = _gu()
+    from paper_2401_10652_b200 import api
+    og = workloads.config("gpt_fa")
+    cg = gu.c_graph(og)
+    pk = memory.profile(og).peak_bytes
+    plan = api.ac_plan(cg, int(0.95 * pk))
+    assert plan.feasible and plan.num_regions >= 1
+    vals, dev = gu.make_values(og, 0)
+    got, ex = gu.run(cg, plan, og, dev)
+    torch.cuda.synchronize()
+    rows = blocks.sample_rows(16384, 1024, 24)
+    ref = blocks.transformer_rows(workloads.config("gpt"), vals, rows)
+    assert gu.rel_err(got["y"][torch.from_numpy(rows).cuda()], ref["y"]) < 2e-2
