@@ -215,3 +215,32 @@ def test_sampled_rows_equal_full_run():
         out = "y" if kind == "transformer" else "x1"
         np.testing.assert_allclose(got[out], env[out][rows], rtol=0, atol=1e-12)
         np.testing.assert_allclose(got["o"], env["o"][rows], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("attn_only", [False, True])
+def test_fused_attention_block_matches_torch_functional(causal, attn_only):
+    """NEXT f1: the attn_fused node (one kernel, no N x N tensor) is pinned by the
+    same torch.nn.functional block (SDPA math path) as the unfused chain."""
+    N, d, h, f = 48, 32, 4, 64
+    g = workloads.block("attn_only_fa" if attn_only else "transformer_fa", N, d, h, f, causal, "f64")
+    assert not any(n.kind in ("attn_scores", "softmax", "attn_pv") for n in g.nodes)
+    v = _values(g)
+    ours = executor.run(g, v)[g.outputs[0]]
+    ref = _torch_transformer(v, N, d, h, causal, attn_only)
+    np.testing.assert_allclose(ours, ref, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_fused_attention_chunked_is_exact(causal):
+    """attn_fused chunked along query rows (offset-aware causal mask) or heads
+    reproduces the unchunked node bitwise in exact-order fp64 (Eq. 5)."""
+    from oracle import select
+    g = workloads.block("transformer_fa", 40, 16, 2, 32, causal, "f64")
+    v = _values(g, 3)
+    with ops.exact_order():
+        base = executor.run(g, v)
+        for spec in ([("attn", "attn", 3, [0])], [("attn", "ffn2", 4, [0])], [("attn", "attn", 2, [1])]):
+            plan = select.user_plan(g, spec)
+            got = executor.run_chunked(g, v, plan.regions)
+            np.testing.assert_array_equal(got[g.outputs[0]], base[g.outputs[0]])
