@@ -30,6 +30,12 @@ namespace ac {
 
 namespace {
 
+// f2 scores: exponentials as packed bf16x2 ex2 (one instruction per pair) instead
+// of fp32 ex2 + pack.  Measured slower on B200 (GPT scores 0.94 -> 1.04 ms), so off.
+#ifndef AC_EX2_PACKED
+#define AC_EX2_PACKED 0
+#endif
+
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, alternating 64-column slabs
@@ -858,12 +864,23 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
             if (lim >= hh * 32 + 31) {
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
+#if AC_EX2_PACKED
+                // one MUFU op per pair: e = 2^bf16(x - m2) on bf16x2 (reading R19);
+                // the slab sum adds the stored (rounded) e
+                const __nv_bfloat162 dh = __floats2bfloat162_rn(fmaf(__uint_as_float(r[2 * j]), cl, -mref),
+                                                                fmaf(__uint_as_float(r[2 * j + 1]), cl, -mref));
+                const uint32_t e = ptx::ex2_bf16x2(*reinterpret_cast<const uint32_t*>(&dh));
+                l0 += __uint_as_float(e << 16);
+                l1 += __uint_as_float(e & 0xffff0000u);
+                pk[j] = e;
+#else
                 const float e0 = ptx::ex2(fmaf(__uint_as_float(r[2 * j]), cl, -mref));
                 const float e1 = ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), cl, -mref));
                 l0 += e0;
                 l1 += e1;
                 __nv_bfloat162 h = __floats2bfloat162_rn(e0, e1);
                 pk[j] = *reinterpret_cast<uint32_t*>(&h);
+#endif
               }
             } else {
 #pragma unroll
