@@ -610,12 +610,19 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
           if (++acc == 2) { acc = 0; aphase ^= 1; }
-          if (a.done_cnt && ew == C::EPI && lane == 0) {
-            // this unit's MMAs are complete, so its e-tiles and statistics have been
-            // read: the unit that completes the batch publishes the chunk epoch
-            const int bb = b1 * a.B2 + b2;
-            if (ptx::atom_add_acqrel_gpu(a.done_cnt + bb, 1) == tpb - 1) ptx::st_release_gpu(a.done_epoch + bb, a.epoch + 1);
-          }
+          // chunk-loop overlap: once this unit has read its e-tiles / statistics (its
+          // MMAs completed) and stored its rows or partials, and the four output warps
+          // are past their stores, the unit that completes the batch publishes the
+          // chunk epoch (release, cumulative over the barrier).  Every unit counts.
+          auto publish = [&]() {
+            if (!a.done_cnt) return;
+            asm volatile("bar.sync 2, 128;" ::: "memory");
+            if (ew == C::EPI && lane == 0) {
+              const int bb = b1 * a.B2 + b2;
+              if (ptx::atom_add_acqrel_gpu(a.done_cnt + bb, 1) == tpb - 1)
+                ptx::st_release_gpu(a.done_epoch + bb, a.epoch + 1);
+            }
+          };
           if (ng > 1) {
             float* mine = a.skpart + (static_cast<long long>(unit0 + g) * BM + r) * BN;
 #pragma unroll
@@ -628,7 +635,10 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
             asm volatile("bar.sync 1, 128;" ::: "memory");
             const int old = *sk_old;
             asm volatile("bar.sync 1, 128;" ::: "memory");  // sk_old reusable
-            if (old != ng - 1) continue;
+            if (old != ng - 1) {
+              publish();
+              continue;
+            }
             __threadfence();
             const float4* base = reinterpret_cast<const float4*>(a.skpart + (static_cast<long long>(unit0) * BM + r) * BN);
 #pragma unroll
@@ -667,6 +677,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
                 if (8 * q < a.N - n) o[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
             }
           }
+          publish();
           if (a.trace && ew == C::EPI && lane == 0) {
             unsigned long long tnow;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
