@@ -91,21 +91,22 @@ struct Cfg {
   // f2 scores (MODE 1): 16 epilogue warps (one 64-column slab each at BN = 256,
   // <= 112 registers) with a single 4 KB bf16 staging box per warp; K = head dim
   // is one or two k-blocks, so two smem stages suffice
-  static constexpr int EPI = (MODE == 1 || MODE == 3) ? 16 : EPI_WARPS;
+  static constexpr int EPI = (MODE == 1 || MODE == 3 || MODE == 4) ? 16 : EPI_WARPS;
   // f2 PV (MODE 2): the EPI warps transform A tiles; XEPI more warps (one per
   // TMEM lane quarter) run the output epilogue so the transform never stalls
   static constexpr int XEPI = MODE == 2 ? 4 : 0;
   static constexpr int THREADS = 64 + 32 * (EPI + XEPI);
   // f2 PV (MODE 2) stages no output in smem: its ring is 8 deep (one CTA must keep
   // ~8 x 24 KB of A/B tiles in flight to stream at full speed when few CTAs remain)
-  static constexpr int EPI_BYTES = (MODE == 1 || MODE == 3) ? EPI * 4096 : MODE == 2 ? 0 : EPI_WARPS * 32 * PITCH * 4;
-  static constexpr int STAGES = (MODE == 1 || MODE == 3) ? 2 : MODE == 2 ? 8 : (BN >= 256 ? 3 : (BN >= 128 ? 4 : 5));
+  static constexpr int EPI_BYTES = (MODE == 1 || MODE == 3 || MODE == 4) ? EPI * 4096 : MODE == 2 ? 0 : EPI_WARPS * 32 * PITCH * 4;
+  static constexpr int STAGES = (MODE == 1 || MODE == 3 || MODE == 4) ? 2 : MODE == 2 ? 8 : (BN >= 256 ? 3 : (BN >= 128 ? 4 : 5));
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  // MODE 4 (paired 64-row tiles): each stage holds the B tiles of both tiles of a pair
+  static constexpr int B_BYTES = (MODE == 4 ? 2 : 1) * BN * BK * 2;
   static constexpr int SW = BN >= 64 ? 64 : 32;  // epilogue slab width (columns)
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
   static constexpr int SMEM = 1024 /*align slack*/ + STAGES * (A_BYTES + B_BYTES) + EPI_BYTES + 512 /*barriers*/ +
-                              (MAX_MT + 1) * 4 + 16 + (MODE == 3 ? 16 * 8 + 8 : 0) /*bias-box barriers*/;
+                              (MODE == 4 ? 0 : (MAX_MT + 1) * 4 + 16 + (MODE == 3 ? 16 * 8 + 8 : 0));
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
@@ -272,7 +273,8 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
   int* uq_slot = reinterpret_cast<int*>(tempty + 27);
   int* prefix = reinterpret_cast<int*>(tempty + 29);  // ends at 2 * STAGES + 31 words <= 512 bytes
   // MODE 1 bias boxes: one mbarrier per epilogue warp, after the prefix table
-  uint64_t* bbar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(prefix + MAX_MT + 2) + 7) & ~uintptr_t(7));
+  uint64_t* bbar = MODE == 4 ? reinterpret_cast<uint64_t*>(prefix)
+                             : reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(prefix + MAX_MT + 2) + 7) & ~uintptr_t(7));
   static_assert(C::STAGES <= 8, "barrier block layout");
 
   const int warp = threadIdx.x >> 5;
@@ -332,7 +334,8 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
       tpb = a.MT * a.skng;
     }
   }
-  const int total = tpb * a.B1 * a.B2;
+  // MODE 4 work unit = (pair of flattened batches 2p, 2p+1; n-tile)
+  const int total = MODE == 4 ? ((a.B1 * a.B2 + 1) / 2) * a.NT : tpb * a.B1 * a.B2;
 #ifdef AC_DEBUG_HANG
   if (blockIdx.x == 0 && threadIdx.x == 0)
     printf("gemm_tc<%d,%d> enter grid %d M %d N %d K %d B1 %d B2 %d total %d tpb %d etile %p\n", BN, MODE, gridDim.x, a.M,
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&a.ta);
     ptx::prefetch_tmap(&a.tb);
-    if (MODE == 3) ptx::prefetch_tmap(&a.tadd);
+    if (MODE == 3 || MODE == 4) ptx::prefetch_tmap(&a.tadd);
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -352,7 +355,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
       ptx::mbar_init(&tempty[s], MODE == 2 ? C::XEPI : C::EPI);
     }
     for (int s = 0; s < C::STAGES; ++s) ptx::mbar_init(&ready[s], 32 * C::EPI);
-    if (MODE == 3)
+    if (MODE == 3 || MODE == 4)
       for (int w = 0; w < C::EPI; ++w) ptx::mbar_init(&bbar[w], 1);
     for (int s = 0; s < 4; ++s) {
       ptx::mbar_init(&uq_full[s], 1);
@@ -405,7 +408,29 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
     }
   };
 
-  if (warp == 0) {
+  if (MODE == 4 && warp == 0) {
+    // ------------------------------------------------------------ TMA producer, MODE 4:
+    // two 64-row A tiles (box rows 64) and their two B tiles per stage
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const int Bt = a.B1 * a.B2;
+      for (int i = 0, t = produce(0); t < total; t = produce(++i)) {
+        const int pb = t / a.NT, nt = t - pb * a.NT;
+        const int nb = 2 * pb + 1 < Bt ? 2 : 1;
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        ptx::mbar_expect_tx(&full[stage], nb * (C::A_BYTES / 2 + C::B_BYTES / 2));
+        for (int q = 0; q < nb; ++q) {
+          const int bb = 2 * pb + q, b1 = bb / a.B2, b2 = bb - (bb / a.B2) * a.B2;
+          ptx::tma_load_4d(sA + stage * C::A_BYTES + q * (C::A_BYTES / 2), &a.ta, &full[stage], 0, 0,
+                           a.a_b1 ? b1 : 0, a.a_b2 ? b2 : 0);
+          ptx::tma_load_4d(sB + stage * C::B_BYTES + q * (C::B_BYTES / 2), &a.tb, &full[stage], 0, nt * BN,
+                           a.b_b1 ? b1 : 0, a.b_b2 ? b2 : 0);
+        }
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       int stage = 0;
@@ -452,6 +477,38 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
+    }
+  } else if (MODE == 4 && warp == 1) {
+    // ------------------------------------------------------------ MMA issuer, MODE 4: two
+    // M = 64 MMAs per k-step; their accumulators interleave in TMEM (lanes 0-15 and
+    // 16-31 of every 32-lane subpartition), so all four epilogue quarters get rows
+    constexpr uint32_t IDESC64 = ptx::idesc_bf16(64, BN);
+    const int Bt = a.B1 * a.B2;
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, aphase = 0;
+    for (int i = 0, t = take(0); t < total; t = take(++i)) {
+      const int pb = t / a.NT;
+      const int nb = 2 * pb + 1 < Bt ? 2 : 1;
+      ptx::mbar_wait(&tempty[acc], aphase ^ 1);
+      ptx::tc_fence_after();
+      ptx::mbar_wait(&full[stage], phase);
+      ptx::tc_fence_after();
+      if (lane == 0) {
+        const uint32_t d = tmem_base + acc * BN;
+        for (int q = 0; q < nb; ++q) {
+          const uint32_t sa = ptx::smem_u32(sA + stage * C::A_BYTES + q * (C::A_BYTES / 2));
+          const uint32_t sb = ptx::smem_u32(sB + stage * C::B_BYTES + q * (C::B_BYTES / 2));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            ptx::mma_bf16(d + (static_cast<uint32_t>(16 * q) << 16), ptx::sdesc_sw128(sa + k * 32),
+                          ptx::sdesc_sw128(sb + k * 32), IDESC64, k ? 1u : 0u);
+        }
+        ptx::mma_commit(&empty[stage]);
+        ptx::mma_commit(&tfull[acc]);
+      }
+      __syncwarp();
+      if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -685,6 +742,125 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
           }
         }
       }
+    } else if constexpr (MODE == 4) {
+      // ---- paired f2 triangle scores for short chunks (M <= 64, R20): thread =
+      // (row quarter*16 + lane%16) of the pair's first tile (lanes 0-15) or second
+      // tile (lanes 16-31); one 64-column slab per warp.  Bias boxes [16 rows x 64]
+      // per tile of the pair land in the warp's staging box, e is packed into it and
+      // leaves as two 2 KB bulk stores (16 e-tile rows per tile).
+      constexpr float L2E = 1.4426950408889634f;
+      const int ew = warp - 2;
+      const int quarter = warp & 3;
+      const int c = ew >> 2;
+      const int sel = lane >> 4;
+      const int Bt = a.B1 * a.B2;
+      uint8_t* sb = reinterpret_cast<uint8_t*>(sEpi) + ew * 4096;
+      const float sc = a.ep.scale * L2E;
+      int acc = 0;
+      uint32_t aphase = 0, bph = 0;
+      for (int i = 0, t = take(0); t < total; t = take(++i)) {
+        const int pb = t / a.NT, nt = t - pb * a.NT;
+        const int nb = 2 * pb + 1 < Bt ? 2 : 1;
+        const int bb = 2 * pb + sel;
+        const int n0 = nt * BN + c * 64;
+        const int m = quarter * 16 + (lane & 15);
+        const bool live = quarter * 16 < a.M;  // warp-uniform
+        const bool mvalid = live && bb < Bt && m < a.M;
+        ptx::mbar_wait(&tfull[acc], aphase);
+        ptx::tc_fence_after();
+        if (live) {
+          if (lane == 0) {
+            ptx::bulk_wait_read<0>();  // the previous e store has read the staging box
+            ptx::mbar_expect_tx(&bbar[ew], nb * 2048);
+            for (int q = 0; q < nb; ++q) {
+              const int qb = 2 * pb + q, q1 = qb / a.B2, q2 = qb - (qb / a.B2) * a.B2;
+              ptx::tma_load_4d(sb + q * 2048, &a.tadd, &bbar[ew], n0, quarter * 16, a.ep.add_sb1 ? q1 : 0,
+                               a.ep.add_sb2 ? q2 : 0);
+            }
+          }
+          __syncwarp();
+          ptx::mbar_wait(&bbar[ew], bph);
+          bph ^= 1;
+          long long lim = a.N - 1 - n0;
+          const uint32_t ta = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c * 64;
+          uint32_t r[32];
+          auto load_x = [&](int hh) {
+            ptx::tmem_ld32(ta + hh * 32, r);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint32_t addr = ptx::smem_u32(sb + lane * 128 + (((hh * 4 + q) ^ (lane & 7)) * 16));
+              uint32_t w[4];
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                           : "r"(addr));
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 bf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+                r[8 * q + 2 * e] = __float_as_uint(fmaf(__uint_as_float(r[8 * q + 2 * e]), sc, bf.x * L2E));
+                r[8 * q + 2 * e + 1] = __float_as_uint(fmaf(__uint_as_float(r[8 * q + 2 * e + 1]), sc, bf.y * L2E));
+              }
+            }
+          };
+          float mx = -CUDART_INF_F;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            load_x(hh);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (hh * 32 + j <= lim) mx = fmaxf(mx, __uint_as_float(r[j]));
+          }
+          const float mref = mx == -CUDART_INF_F ? 0.f : mx;
+          float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            load_x(hh);
+            if (hh == 1) {
+              ptx::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            }
+            uint32_t pk[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float e0 = hh * 32 + 2 * j <= lim ? ptx::ex2(__uint_as_float(r[2 * j]) - mref) : 0.f;
+              const float e1 = hh * 32 + 2 * j + 1 <= lim ? ptx::ex2(__uint_as_float(r[2 * j + 1]) - mref) : 0.f;
+              l0 += e0;
+              l1 += e1;
+              __nv_bfloat162 h = __floats2bfloat162_rn(e0, e1);
+              pk[j] = *reinterpret_cast<uint32_t*>(&h);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int ch = hh * 4 + q;
+              const uint32_t addr = ptx::smem_u32(sb + lane * 128 + ((ch ^ (lane & 7)) * 16));
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[4 * q]),
+                           "r"(pk[4 * q + 1]), "r"(pk[4 * q + 2]), "r"(pk[4 * q + 3])
+                           : "memory");
+            }
+          }
+          if (mvalid && n0 < a.N)
+            a.ep.stats[static_cast<long long>(bb) * a.ep.stats_sb1 + static_cast<long long>(n0 / 64) * a.ep.stats_ss + m] =
+                make_float2(mx, l0 + l1);
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && n0 < a.N) {
+            for (int q = 0; q < nb; ++q) {
+              char* dst = a.etile + ((static_cast<long long>(2 * pb + q) * a.MT) * a.e_nkb + n0 / 64) * 16384 +
+                          quarter * 2048;
+              ptx::bulk_store(dst, sb + q * 2048, 2048);
+            }
+            ptx::bulk_commit();
+          }
+        } else {
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+        }
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+      if (lane == 0) ptx::bulk_wait_read<0>();
+      __syncwarp();
     } else {
     TileWalk walk;
     int dep_ok_b = -1;  // MODE 1 / 3: last batch whose predecessor PV is known finished
@@ -1189,11 +1365,11 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   GemmArgs a;
   memset(&a, 0, sizeof(a));
   if (!(MODE == 2 && p.etile) &&
-      !make_map(&a.ta, p.A, p.K, p.a_rows_total ? p.a_rows_total : p.M, p.B1, p.B2, BM))
+      !make_map(&a.ta, p.A, p.K, p.a_rows_total ? p.a_rows_total : p.M, p.B1, p.B2, MODE == 4 ? 64 : BM))
     return cudaErrorInvalidValue;
   a.etile = static_cast<char*>(p.etile);
   a.sched = MODE == 2 ? p.sched : nullptr;
-  a.e_nkb = (MODE == 1 || MODE == 3) ? (p.N + 63) / 64 : (p.K + 63) / 64;
+  a.e_nkb = (MODE == 1 || MODE == 3 || MODE == 4) ? (p.N + 63) / 64 : (p.K + 63) / 64;
   if (p.etile && (reinterpret_cast<uintptr_t>(p.etile) & 127)) return cudaErrorInvalidValue;
   if (!make_map(&a.tb, p.B, p.K, p.b_rows_total ? p.b_rows_total : p.N, p.B1, p.B2, BN)) return cudaErrorInvalidValue;
   a.ep = p.ep;
@@ -1234,7 +1410,7 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
       a.lean = (!e.add && !e.bias && !e.gate && !e.res && e.act == ACT_NONE) ? 1 : 0;
     }
   }
-  if (MODE == 3 && p.ep.add && p.ep.add_sn == 1) {
+  if ((MODE == 3 || MODE == 4) && p.ep.add && p.ep.add_sn == 1) {
     // bias map {N, M, B1, B2} (a batch dim the bias does not vary over gets extent 1)
     const Epilogue& e = p.ep;
     EncodeTiledFn enc = get_encode();
@@ -1246,7 +1422,7 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
                              static_cast<cuuint64_t>(e.add_sb2 ? e.add_sb2 * 2 : big)};
     bool ok = enc && (reinterpret_cast<uintptr_t>(e.add) & 15) == 0;
     for (int i = 0; i < 3; ++i) ok = ok && strides[i] % 16 == 0 && strides[i] > 0;
-    cuuint32_t box[4] = {64, 32, 1, 1};
+    cuuint32_t box[4] = {64, MODE == 4 ? 16u : 32u, 1, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     if (ok)
       ok = enc(&a.tadd, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(e.add), dims, strides, box, es,
@@ -1260,8 +1436,9 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   // 64-wide tile with an n-contiguous aligned output
   // (MODE 1 may add an n-contiguous bias tensor, the AlphaFold triangle bias)
   if (MODE == 1 && !(a.tma_store && a.lean && p.ep.scale > 0.f)) return cudaErrorInvalidValue;
-  if (MODE == 3) {
+  if (MODE == 3 || MODE == 4) {
     const Epilogue& e = p.ep;
+    if (MODE == 4 && !(p.M <= 64 && p.K <= BK && p.etile)) return cudaErrorInvalidValue;
     const bool only_add = !e.bias && !e.gate && !e.res && e.act == ACT_NONE && !e.causal && e.add;
     if (!(a.tma_store && a.add_tma && only_add && p.ep.scale > 0.f)) return cudaErrorInvalidValue;
   }
@@ -1294,7 +1471,7 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   a.ks = (MODE == 0 && BN == 64 && a.vec && p.ksplit > 1) ? (p.ksplit > 8 ? 8 : p.ksplit) : 1;
   if (a.ks > 1) a.tma_store = 0;
   const int sms = num_sms();
-  int grid = a.total_tiles_dense * a.ks * (MODE == 2 ? a.skng : 1);
+  int grid = MODE == 4 ? ((p.B1 * p.B2 + 1) / 2) * a.NT : a.total_tiles_dense * a.ks * (MODE == 2 ? a.skng : 1);
   int cap = (sms / a.ks) * a.ks;
   {
     static int dbg = -1, dgrid = -1;
@@ -1392,6 +1569,8 @@ cudaError_t gemm_tc(const GemmProblem& p, cudaStream_t s, int bn_hint) {
     }
   }
   if (p.fuse_stats) return p.N <= 32 ? launch<32, 2>(p, s) : bn == 64 ? launch<64, 2>(p, s) : cudaErrorInvalidValue;
+  if (p.ep.stats && p.ep.add && p.M <= 64 && p.etile && p.K <= 64 && getenv("AC_NO_PAIR") == nullptr)
+    return launch<256, 4>(p, s);  // short chunks: paired 64-row tiles
   if (p.ep.stats && p.ep.add) {
     switch (bn) {
       case 64: return launch<64, 3>(p, s);
