@@ -80,6 +80,7 @@ struct alignas(64) GemmArgs {
   int* done_epoch;
   int epoch, dep_epoch;
   int* tsched;  // MODE 1 / 3 dynamic tile counter
+  int pair;     // MODE 2, BN = 32, M <= 64: work units are pairs of batches (two M = 64 MMAs)
 };
 
 // epilogue staging: per epilogue warp a [32 rows][PITCH] fp32 slab; PITCH = 68
@@ -102,7 +103,10 @@ struct Cfg {
   static constexpr int STAGES = (MODE == 1 || MODE == 3 || MODE == 4) ? 2 : MODE == 2 ? 8 : (BN >= 256 ? 3 : (BN >= 128 ? 4 : 5));
   static constexpr int A_BYTES = BM * BK * 2;
   // MODE 4 (paired 64-row tiles): each stage holds the B tiles of both tiles of a pair
-  static constexpr int B_BYTES = (MODE == 4 ? 2 : 1) * BN * BK * 2;
+  // MODE 4 (paired 64-row tiles) and the BN = 32 PV (pairs when M <= 64): each stage
+  // holds the B tiles of both tiles of a pair
+  static constexpr int B_TILE = BN * BK * 2;
+  static constexpr int B_BYTES = (MODE == 4 || (MODE == 2 && BN == 32) ? 2 : 1) * B_TILE;
   static constexpr int SW = BN >= 64 ? 64 : 32;  // epilogue slab width (columns)
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
   static constexpr int SMEM = 1024 /*align slack*/ + STAGES * (A_BYTES + B_BYTES) + EPI_BYTES + 512 /*barriers*/ +
@@ -213,8 +217,9 @@ struct TileWalk {
 __device__ __forceinline__ void decode_unit(const GemmArgs& a, const int* prefix, int upb, int u, int& b1, int& b2,
                                             int& mt, int& kbn, int& klo, int& khi, int& g, int& ng, int& tile,
                                             int& unit0) {
-  const int b = u / upb;
-  const int v = u - b * upb;
+  const int pu = u / upb;
+  const int v = u - pu * upb;
+  const int b = a.pair ? 2 * pu : pu;  // pairs: the pair's first batch
   b1 = b / a.B2;
   b2 = b - b1 * a.B2;
   int r;
@@ -335,7 +340,8 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
     }
   }
   // MODE 4 work unit = (pair of flattened batches 2p, 2p+1; n-tile)
-  const int total = MODE == 4 ? ((a.B1 * a.B2 + 1) / 2) * a.NT : tpb * a.B1 * a.B2;
+  const int total = MODE == 4 ? ((a.B1 * a.B2 + 1) / 2) * a.NT
+                                : (MODE == 2 && a.pair ? tpb * ((a.B1 * a.B2 + 1) / 2) : tpb * a.B1 * a.B2);
 #ifdef AC_DEBUG_HANG
   if (blockIdx.x == 0 && threadIdx.x == 0)
     printf("gemm_tc<%d,%d> enter grid %d M %d N %d K %d B1 %d B2 %d total %d tpb %d etile %p\n", BN, MODE, gridDim.x, a.M,
@@ -466,14 +472,24 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
           const int rows = a.M - mt * BM;
           if (rows < BM) ebytes = ((rows + 31) / 32) * 4096;
         }
+        // pairs: rows 0..63 of the second batch's e-tile go to the stage's upper half,
+        // its V^T tile to the second B slot
+        const bool two = MODE == 2 && a.pair && b1 * a.B2 + b2 + 1 < a.B1 * a.B2;
+        const int pb1 = two ? (b1 * a.B2 + b2 + 1) / a.B2 : 0, pb2 = two ? (b1 * a.B2 + b2 + 1) - pb1 * a.B2 : 0;
         for (int kb = klo; kb < khi; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          ptx::mbar_expect_tx(&full[stage], ebytes + C::B_BYTES);
+          ptx::mbar_expect_tx(&full[stage], (two ? 2 : 1) * (ebytes + C::B_TILE));
           if (MODE == 2 && esrc)
             ptx::bulk_load(sA + stage * C::A_BYTES, esrc + static_cast<long long>(kb) * 16384, ebytes, &full[stage]);
           else
             ptx::tma_load_4d(sA + stage * C::A_BYTES, &a.ta, &full[stage], kb * BK, mt * BM, ac2, ac3);
           ptx::tma_load_4d(sB + stage * C::B_BYTES, &a.tb, &full[stage], kb * BK, nt * BN, bc2, bc3);
+          if (two) {
+            ptx::bulk_load(sA + stage * C::A_BYTES + 8192,
+                           esrc + (static_cast<long long>(a.MT) * a.e_nkb + kb) * 16384, ebytes, &full[stage]);
+            ptx::tma_load_4d(sB + stage * C::B_BYTES + C::B_TILE, &a.tb, &full[stage], kb * BK, nt * BN,
+                             a.b_b1 ? pb1 : 0, a.b_b2 ? pb2 : 0);
+          }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -538,11 +554,23 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
         if (lane == 0) {
           const uint32_t sa = ptx::smem_u32(sA + stage * C::A_BYTES);
           const uint32_t sb = ptx::smem_u32(sB + stage * C::B_BYTES);
+          if (MODE == 2 && a.pair) {
+            // two M = 64 MMAs; their accumulators interleave in TMEM (lanes 0-15 / 16-31
+            // of every subpartition)
+            constexpr uint32_t IDESC64 = ptx::idesc_bf16(64, BN);
+            const int np = b1 * a.B2 + b2 + 1 < a.B1 * a.B2 ? 2 : 1;
+            for (int q = 0; q < np; ++q)
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            if (MODE != 2 || !(a.dbg & 4))
-              ptx::mma_bf16(d, ptx::sdesc_sw128(sa + k * 32), ptx::sdesc_sw128(sb + k * 32), IDESC,
-                            (kb != klo || k != 0) ? 1u : 0u);
+              for (int k = 0; k < BK / 16; ++k)
+                ptx::mma_bf16(d + (static_cast<uint32_t>(16 * q) << 16), ptx::sdesc_sw128(sa + q * 8192 + k * 32),
+                              ptx::sdesc_sw128(sb + q * C::B_TILE + k * 32), IDESC64, (kb != klo || k != 0) ? 1u : 0u);
+          } else {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              if (MODE != 2 || !(a.dbg & 4))
+                ptx::mma_bf16(d, ptx::sdesc_sw128(sa + k * 32), ptx::sdesc_sw128(sb + k * 32), IDESC,
+                              (kb != klo || k != 0) ? 1u : 0u);
+            }
           }
           ptx::mma_commit(&empty[stage]);  // slot free once these MMAs have read smem
         }
@@ -584,10 +612,14 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
         for (int i = 0, t = take(0); t < total; t = take(++i)) {
           int b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0;
           decode_unit(a, prefix, tpb, t, b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0);
-          const int m = mt * BM + r;
-          const bool mv = m < a.M;
-          const bool dead = mt * BM + quarter * 32 >= a.M;  // warp-uniform: rows never loaded
-          const long long bb = static_cast<long long>(b1) * a.B2 + b2;
+          // pairs: stage rows 0-63 = first batch, 64-127 = second batch (rows 0-63 each)
+          const int sel = a.pair ? r >> 6 : 0;
+          const int m = a.pair ? (r & 63) : mt * BM + r;
+          const long long bb = static_cast<long long>(b1) * a.B2 + b2 + sel;
+          const bool bok = bb < static_cast<long long>(a.B1) * a.B2;
+          const bool mv = m < a.M && bok;
+          const bool dead = a.pair ? ((quarter & 1) * 32 >= a.M || !bok)    // warp-uniform: rows never loaded
+                                   : mt * BM + quarter * 32 >= a.M;
           const float* fp = reinterpret_cast<const float*>(a.fstats + bb * a.fst_sb1 + (mv ? m : 0));
           const long long fs = 2 * a.fst_ss;
           const float2 rs = mv ? __ldg(a.frow + bb * a.M + m) : make_float2(0.f, 0.f);
@@ -645,8 +677,15 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
         for (int i = 0, t = take(0); t < total; t = take(++i)) {
           int b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0;
           decode_unit(a, prefix, tpb, t, b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0);
-          const int m = mt * BM + r;
-          const bool mv = m < a.M;
+          // pairs: TMEM lanes 0-15 of each subpartition hold the first batch's rows
+          // quarter*16.., lanes 16-31 the second batch's
+          const int m = a.pair ? quarter * 16 + (lane & 15) : mt * BM + r;
+          if (a.pair && lane >= 16) {
+            const int nb = b1 * a.B2 + b2 + 1;
+            b1 = nb / a.B2;
+            b2 = nb - b1 * a.B2;
+          }
+          const bool mv = m < a.M && b1 < a.B1;
           ptx::mbar_wait(&tfull[acc], aphase);
           ptx::tc_fence_after();
           if (a.trace && ew == C::EPI && lane == 0) {
@@ -1471,7 +1510,9 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   a.ks = (MODE == 0 && BN == 64 && a.vec && p.ksplit > 1) ? (p.ksplit > 8 ? 8 : p.ksplit) : 1;
   if (a.ks > 1) a.tma_store = 0;
   const int sms = num_sms();
-  int grid = MODE == 4 ? ((p.B1 * p.B2 + 1) / 2) * a.NT : a.total_tiles_dense * a.ks * (MODE == 2 ? a.skng : 1);
+  a.pair = (MODE == 2 && BN == 32 && p.etile && p.M <= 64 && a.skng == 1 && !p.causal_k && !getenv("AC_NO_PAIR")) ? 1 : 0;
+  int grid = MODE == 4 ? ((p.B1 * p.B2 + 1) / 2) * a.NT
+                       : (a.pair ? (p.B1 * p.B2 + 1) / 2 : a.total_tiles_dense) * a.ks * (MODE == 2 ? a.skng : 1);
   int cap = (sms / a.ks) * a.ks;
   {
     static int dbg = -1, dgrid = -1;
