@@ -34,12 +34,12 @@ constexpr int FA_BM = 128;   // query rows per tile
 constexpr int FA_BN = 128;   // keys per block
 constexpr int FA_DH = 64;    // head dim (one 128-byte swizzle row)
 constexpr int FA_STG = 3;    // K/V ring depth
-constexpr int FA_THREADS = 192;
+constexpr int FA_THREADS = 320;  // producer, MMA, 8 softmax warps
 constexpr int Q_BYTES = FA_BM * FA_DH * 2;        // 16 KB
 constexpr int K_BYTES = FA_BN * FA_DH * 2;        // 16 KB
 constexpr int V_BYTES = FA_DH * FA_BN * 2;        // 16 KB (two 64-key boxes of 8 KB)
 constexpr int P_BYTES = FA_BM * FA_BN * 2;        // 32 KB (two 64-key k-blocks of 16 KB)
-constexpr int FA_SMEM = 1024 + Q_BYTES + FA_STG * (K_BYTES + V_BYTES) + 2 * P_BYTES + 256;
+constexpr int FA_SMEM = 1024 + Q_BYTES + FA_STG * (K_BYTES + V_BYTES) + 2 * P_BYTES + 256 + 2 * 2 * 128 * 4 + 128 * 4 * 2;
 
 struct alignas(64) FaArgs {
   CUtensorMap tq, tk, tv;
@@ -69,6 +69,10 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
   uint64_t* p_full = s_full + 4;            // [2]
   uint64_t* o_done = s_full + 6;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_full + 7);
+  // softmax row halves exchange their block maxima ([block parity][half][row]) and,
+  // at the end, their partial sums ([half][row])
+  float* xmax = reinterpret_cast<float*>(bar + 32);
+  float* xsum = xmax + 2 * 2 * 128;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = a.H * a.MT;
@@ -84,8 +88,8 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&s_full[b], 1);
-      ptx::mbar_init(&s_free[b], 4);
-      ptx::mbar_init(&p_full[b], 4);
+      ptx::mbar_init(&s_free[b], 8);
+      ptx::mbar_init(&p_full[b], 8);
     }
     ptx::mbar_init(o_done, 1);
     ptx::fence_barrier_init();
@@ -189,50 +193,58 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
       }
     }
   } else {
-    // softmax warps: thread = query row r of the tile (TMEM lane quarter = warp % 4)
+    // softmax warps: thread = (query row r of the tile, half of the 128-key block);
+    // warps w and w + 4 share TMEM lane quarter w % 4 and split each row's keys
+    const int sw = warp - 2;
     const int quarter = warp & 3;
+    const int hf = sw >> 2;  // keys hf*64 .. hf*64+63 of every block; O columns hf*32..
     const int r = quarter * 32 + lane;
     const uint32_t lrow = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t nbar = 1 + quarter;  // named barrier of the two warps of a quarter
     int sidx = 0;
     int pv = 0;  // PV completions awaited so far (o_done phase)
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       int head, mt, nkb;
       tile(t, head, mt, nkb);
       const long long qg = a.row_off + static_cast<long long>(mt) * FA_BM + r;  // global query row
-      float m = -CUDART_INF_F, l = 0.f;
+      float m = -CUDART_INF_F, l = 0.f;  // l: this half's partial sum (same rescales as the other)
       for (int j = 0; j < nkb; ++j) {
         const int b = sidx & 1;
         ptx::mbar_wait(&s_full[b], (sidx >> 1) & 1);
         ptx::tc_fence_after();
-        uint32_t s[128];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) ptx::tmem_ld32(tmem + lrow + b * FA_BN + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]));
+        uint32_t s[64];
+        ptx::tmem_ld32(tmem + lrow + b * FA_BN + hf * 64, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+        ptx::tmem_ld32(tmem + lrow + b * FA_BN + hf * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
         ptx::tmem_ld_wait();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&s_free[b]);
         // mask: causal keys past the row, keys past Nk
-        const long long k0 = static_cast<long long>(j) * FA_BN;
-        long long lim = a.Nk - 1 - k0;  // last valid column of this block
+        const long long k0 = static_cast<long long>(j) * FA_BN + hf * 64;
+        long long lim = a.Nk - 1 - k0;  // last valid column of this half-block
         if (a.causal && qg - k0 < lim) lim = qg - k0;
         float mb = -CUDART_INF_F;
-        if (lim >= FA_BN - 1) {
+        if (lim >= 63) {
 #pragma unroll
-          for (int c = 0; c < 128; ++c) mb = fmaxf(mb, __uint_as_float(s[c]));
+          for (int c = 0; c < 64; ++c) mb = fmaxf(mb, __uint_as_float(s[c]));
         } else {
 #pragma unroll
-          for (int c = 0; c < 128; ++c) {
+          for (int c = 0; c < 64; ++c) {
             if (c > lim) s[c] = __float_as_uint(-CUDART_INF_F);
             mb = fmaxf(mb, __uint_as_float(s[c]));
           }
         }
+        // row max over both halves (slots double-buffered by block parity)
+        xmax[((j & 1) * 2 + hf) * 128 + r] = mb;
+        asm volatile("bar.sync %0, 64;" ::"r"(nbar) : "memory");
+        mb = fmaxf(mb, xmax[((j & 1) * 2 + (hf ^ 1)) * 128 + r]);
         const float m_new = fmaxf(m, mb * a.cl);
         const float mref = m_new == -CUDART_INF_F ? 0.f : m_new;
         const float alpha = m == -CUDART_INF_F ? 0.f : ptx::ex2(m - mref);
         float ls = 0.f;
-        uint32_t pk[64];
+        uint32_t pk[32];
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
+        for (int c = 0; c < 32; ++c) {
           const float e0 = ptx::ex2(fmaf(__uint_as_float(s[2 * c]), a.cl, -mref));
           const float e1 = ptx::ex2(fmaf(__uint_as_float(s[2 * c + 1]), a.cl, -mref));
           ls += e0 + e1;
@@ -247,20 +259,17 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
           ++pv;
           ptx::tc_fence_after();
           uint32_t o[32];
+          ptx::tmem_ld32(tmem + lrow + 256 + hf * 32, o);
+          ptx::tmem_ld_wait();
 #pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
-            ptx::tmem_ld32(tmem + lrow + 256 + h2 * 32, o);
-            ptx::tmem_ld_wait();
-#pragma unroll
-            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
-            ptx::tmem_st32(tmem + lrow + 256 + h2 * 32, o);
-          }
+          for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
+          ptx::tmem_st32(tmem + lrow + 256 + hf * 32, o);
           ptx::tmem_st_wait();
         }
-        uint8_t* pb = sP + b * P_BYTES + r * 128;
+        uint8_t* pb = sP + b * P_BYTES + hf * (P_BYTES / 2) + r * 128;  // k-block hf of P_j
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {  // 16 chunks of 8 keys: k-block c / 8, chunk c % 8
-          const uint32_t addr = ptx::smem_u32(pb + (c >> 3) * (P_BYTES / 2) + (((c & 7) ^ (r & 7)) * 16));
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t addr = ptx::smem_u32(pb + ((c ^ (r & 7)) * 16));
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[4 * c]), "r"(pk[4 * c + 1]),
                        "r"(pk[4 * c + 2]), "r"(pk[4 * c + 3])
                        : "memory");
@@ -271,22 +280,25 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
         if (lane == 0) ptx::mbar_arrive(&p_full[b]);
         ++sidx;
       }
-      // epilogue: wait for the last PV, o = O / l
+      // epilogue: wait for the last PV; l = sum of both halves; o = O / l
+      xsum[hf * 128 + r] = l;
       ptx::mbar_wait(o_done, pv & 1);
       ++pv;
       ptx::tc_fence_after();
-      uint32_t o[64];
-      ptx::tmem_ld32(tmem + lrow + 256, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
-      ptx::tmem_ld32(tmem + lrow + 256 + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
+      uint32_t o[32];
+      ptx::tmem_ld32(tmem + lrow + 256 + hf * 32, o);
       ptx::tmem_ld_wait();
       ptx::tc_fence_before();
+      asm volatile("bar.sync %0, 64;" ::"r"(nbar) : "memory");
+      const float lt = l + xsum[(hf ^ 1) * 128 + r];
+      asm volatile("bar.sync %0, 64;" ::"r"(nbar) : "memory");  // xsum reusable by the next tile
       const int mrow = mt * FA_BM + r;
       if (mrow < a.M) {
-        const float inv = l > 0.f ? 1.f / l : 0.f;
+        const float inv = lt > 0.f ? 1.f / lt : 0.f;
         uint4* dst = reinterpret_cast<uint4*>(a.out + static_cast<long long>(mrow) * a.o_srow +
-                                              static_cast<long long>(head) * a.o_sh);
+                                              static_cast<long long>(head) * a.o_sh + hf * 32);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < 4; ++c) {
           uint32_t w[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
