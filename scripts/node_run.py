@@ -15,7 +15,12 @@ cfg = sys.argv[1]
 cg, doc = bench.c_graph(cfg)
 prof0, _ = api.estimate_memory(cg)
 budget = int(bench.DEFAULT_BUDGET.get(cfg, 0.2) * prof0.peak_bytes)
-plan = api.plan_parse(cg, "autochunk-plan 1\nregion s=scores e=pv n=8 dims=0\n") if cfg == "tiny" else api.ac_plan(cg, budget)
+if len(sys.argv) > 2 and sys.argv[2] == "unchunked":
+    plan = api.plan_parse(cg, "autochunk-plan 1\n")
+elif cfg == "tiny":
+    plan = api.plan_parse(cg, "autochunk-plan 1\nregion s=scores e=pv n=8 dims=0\n")
+else:
+    plan = api.ac_plan(cg, budget)
 _, dev = bench.device_inputs(doc, torch)
 TD = {"bf16": torch.bfloat16, "f32": torch.float32}
 outs = {o: torch.empty(doc.tensors[o][1], dtype=TD[doc.tensors[o][0]], device="cuda") for o in doc.outputs}

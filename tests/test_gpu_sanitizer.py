@@ -40,6 +40,15 @@ for og, txt in [
      "autochunk-plan 1\nregion s=proj_q e=ffn2 n=4 dims=0\n"),
     (workloads.tri_attn_pair(48, 128, 4, 32, "bf16", name="af"),
      "autochunk-plan 1\nregion s=row_scores e=row_pv n=4 dims=0\n"),
+    # short row chunks of the triangle chains: paired 64-row scores / PV (M = 40, ragged keys)
+    (workloads.tri_attn_pair(80, 128, 4, 32, "bf16", name="af2"),
+     "autochunk-plan 1\nregion s=row_scores e=row_pv n=2 dims=1\nregion s=col_scores e=col_pv n=3 dims=0\n"),
+    # fused attention (NEXT f1), ragged rows / keys, causal chunks
+    (workloads.block("transformer_fa", 200, 256, 4, 512, True, "bf16", name="fa"),
+     "autochunk-plan 1\nregion s=attn e=ffn2 n=3 dims=0\n"),
+    # 3-block stack with the chunk-loop overlap (PDL launches, epochs)
+    (workloads.transformer(512, 256, 4, 512, True, "bf16", name="st", layers=2),
+     "autochunk-plan 1\nregion s=L0_scores e=L0_pv n=4 dims=0\nregion s=L1_scores e=L1_pv n=2 dims=0\n"),
 ]:
     cg = gu.c_graph(og)
     vals, dev = gu.make_values(og, 0)
