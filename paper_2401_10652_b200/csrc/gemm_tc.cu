@@ -30,6 +30,13 @@ namespace ac {
 
 namespace {
 
+// f2 PV: post-scale (default: e tiles straight to the tensor core, f_slab applied to
+// each k-block's product in registers) or the pre-scale transform of e in shared
+// memory (AC_PV_POSTSCALE=0 at build time)
+#ifndef AC_PV_POSTSCALE
+#define AC_PV_POSTSCALE 1
+#endif
+
 // f2 scores: exponentials as packed bf16x2 ex2 (one instruction per pair) instead
 // of fp32 ex2 + pack.  Measured slower on B200 (GPT scores 0.94 -> 1.04 ms), so off.
 #ifndef AC_EX2_PACKED
@@ -81,6 +88,7 @@ struct alignas(64) GemmArgs {
   int epoch, dep_epoch;
   int* tsched;  // MODE 1 / 3 dynamic tile counter
   int pair;     // MODE 2, BN = 32, M <= 64: work units are pairs of batches (two M = 64 MMAs)
+  int postscale;  // MODE 2: e tiles straight to the MMA (one TMEM buffer per k-block), f applied after
 };
 
 // epilogue staging: per epilogue warp a [32 rows][PITCH] fp32 slab; PITCH = 68
@@ -92,10 +100,11 @@ struct Cfg {
   // f2 scores (MODE 1): 16 epilogue warps (one 64-column slab each at BN = 256,
   // <= 112 registers) with a single 4 KB bf16 staging box per warp; K = head dim
   // is one or two k-blocks, so two smem stages suffice
-  static constexpr int EPI = (MODE == 1 || MODE == 3 || MODE == 4) ? 16 : EPI_WARPS;
+  static constexpr bool PS = MODE == 2 && AC_PV_POSTSCALE;  // post-scale PV: 4 scale/output warps
+  static constexpr int EPI = (MODE == 1 || MODE == 3 || MODE == 4) ? 16 : PS ? 4 : EPI_WARPS;
   // f2 PV (MODE 2): the EPI warps transform A tiles; XEPI more warps (one per
   // TMEM lane quarter) run the output epilogue so the transform never stalls
-  static constexpr int XEPI = MODE == 2 ? 4 : 0;
+  static constexpr int XEPI = MODE == 2 && !PS ? 4 : 0;
   static constexpr int THREADS = 64 + 32 * (EPI + XEPI);
   // f2 PV (MODE 2) stages no output in smem: its ring is 8 deep (one CTA must keep
   // ~8 x 24 KB of A/B tiles in flight to stream at full speed when few CTAs remain)
@@ -108,9 +117,11 @@ struct Cfg {
   static constexpr int B_TILE = BN * BK * 2;
   static constexpr int B_BYTES = (MODE == 4 || (MODE == 2 && BN == 32) ? 2 : 1) * B_TILE;
   static constexpr int SW = BN >= 64 ? 64 : 32;  // epilogue slab width (columns)
-  static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
+  // MODE 2 post-scale PV: 8 per-k-block accumulator buffers of BN columns
+  static constexpr int TMEM_COLS = MODE == 2 ? (8 * BN <= 256 ? 256 : 512)
+                                             : (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
   static constexpr int SMEM = 1024 /*align slack*/ + STAGES * (A_BYTES + B_BYTES) + EPI_BYTES + 512 /*barriers*/ +
-                              (MODE == 4 ? 0 : (MAX_MT + 1) * 4 + 16 + (MODE == 3 ? 16 * 8 + 8 : 0));
+                              (MODE == 4 ? 0 : (MAX_MT + 1) * 4 + 16 + (MODE == 3 || MODE == 2 ? 16 * 8 + 8 : 0));
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
@@ -358,11 +369,13 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], MODE == 2 ? C::XEPI : C::EPI);
+      ptx::mbar_init(&tempty[s], MODE == 2 ? (C::XEPI ? C::XEPI : 1) : C::EPI);
     }
     for (int s = 0; s < C::STAGES; ++s) ptx::mbar_init(&ready[s], 32 * C::EPI);
     if (MODE == 3 || MODE == 4)
       for (int w = 0; w < C::EPI; ++w) ptx::mbar_init(&bbar[w], 1);
+    if (MODE == 2)  // post-scale PV: kfull[8] (MMA commit), kempty[8] (4 scale warps)
+      for (int w = 0; w < 16; ++w) ptx::mbar_init(&bbar[w], w < 8 ? 1 : 4);
     for (int s = 0; s < 4; ++s) {
       ptx::mbar_init(&uq_full[s], 1);
       ptx::mbar_init(&uq_empty[s], 1 + C::EPI + C::XEPI);
@@ -533,6 +546,8 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
     uint32_t phase = 0;
     int acc = 0;
     uint32_t aphase = 0;
+    int kbuf = 0;          // MODE 2 post-scale: next per-k-block TMEM buffer
+    uint32_t kphase = 0;
     TileWalk walk;
     for (int i = 0, t = take(0); t < total; t = take(++i)) {
       int b1, b2, mt, nt = 0, kbn, klo, khi;
@@ -544,6 +559,41 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
         walk.get(a, b1, b2, mt, nt, kbn);
         klo = kbn * static_cast<int>(crank) / ks;
         khi = kbn * (static_cast<int>(crank) + 1) / ks;
+      }
+      if (MODE == 2 && a.postscale) {
+        // post-scale PV: every k-block gets its own TMEM buffer (kb-th of 8, round
+        // robin), accumulate = 0; the scale warps fold f_slab * (e V) into registers
+        uint64_t* kfull = bbar;
+        uint64_t* kempty = bbar + 8;
+        const int np = a.pair && b1 * a.B2 + b2 + 1 < a.B1 * a.B2 ? 2 : 1;
+        for (int kb = klo; kb < khi; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::mbar_wait(&kempty[kbuf], kphase ^ 1);
+          ptx::tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sa = ptx::smem_u32(sA + stage * C::A_BYTES);
+            const uint32_t sb = ptx::smem_u32(sB + stage * C::B_BYTES);
+            const uint32_t dk = tmem_base + kbuf * BN;
+            if (a.pair) {
+              constexpr uint32_t IDESC64 = ptx::idesc_bf16(64, BN);
+              for (int q = 0; q < np; ++q)
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k)
+                  ptx::mma_bf16(dk + (static_cast<uint32_t>(16 * q) << 16), ptx::sdesc_sw128(sa + q * 8192 + k * 32),
+                                ptx::sdesc_sw128(sb + q * C::B_TILE + k * 32), IDESC64, k ? 1u : 0u);
+            } else {
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k)
+                ptx::mma_bf16(dk, ptx::sdesc_sw128(sa + k * 32), ptx::sdesc_sw128(sb + k * 32), IDESC, k ? 1u : 0u);
+            }
+            ptx::mma_commit(&empty[stage]);
+            ptx::mma_commit(&kfull[kbuf]);
+          }
+          __syncwarp();
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          if (++kbuf == 8) { kbuf = 0; kphase ^= 1; }
+        }
+        continue;
       }
       ptx::mbar_wait(&tempty[acc], aphase ^ 1);
       ptx::tc_fence_after();
@@ -600,7 +650,134 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
     bool bias_pending = false;  // MODE 3: this warp's next bias box is already in flight
     uint32_t pf_phase = 0, pe_phase = 0;  // split-K barrier phases
     if constexpr (MODE == 2) {
-      if (ew < C::EPI) {
+      if (a.postscale) {
+        if (ew < 4) {
+          // ---- post-scale f2 PV (default): the e tiles went to the tensor core
+          // unscaled, one k-block (= one 64-key slab) per TMEM buffer; thread = output
+          // row: O += f_slab * (e_slab V_slab) in fp32 registers with
+          // f_slab = 2^(m2_slab - M) / L (R19), then the output epilogue / split-K
+          uint64_t* kfull = bbar;
+          uint64_t* kempty = bbar + 8;
+          const bool lead = ew == 0;
+          const int r = quarter * 32 + lane;
+          int* sk_old = prefix + MAX_MT + 1;
+          int kbuf = 0;
+          uint32_t kphase = 0;
+          for (int i = 0, t = take(0); t < total; t = take(++i)) {
+            int b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0;
+            decode_unit(a, prefix, tpb, t, b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0);
+            // pairs: TMEM lanes 0-15 of each subpartition = the first batch's rows
+            // quarter*16.., lanes 16-31 the second batch's
+            const int m = a.pair ? quarter * 16 + (lane & 15) : mt * BM + r;
+            if (a.pair && lane >= 16) {
+              const int nb = b1 * a.B2 + b2 + 1;
+              b1 = nb / a.B2;
+              b2 = nb - b1 * a.B2;
+            }
+            const bool mv = m < a.M && b1 < a.B1;
+            const long long bb = static_cast<long long>(b1) * a.B2 + b2;
+            const float* fp = reinterpret_cast<const float*>(a.fstats + (mv ? bb * a.fst_sb1 + m : 0));
+            const long long fs = 2 * a.fst_ss;
+            const float2 rs = mv ? __ldg(a.frow + bb * a.M + m) : make_float2(0.f, 0.f);
+            float accv[BN];
+#pragma unroll
+            for (int c = 0; c < BN; ++c) accv[c] = 0.f;
+            float fr[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) fr[j] = (mv && klo + j < khi) ? __ldg(fp + (klo + j) * fs) : -CUDART_INF_F;
+            for (int kb0 = klo; kb0 < khi; kb0 += 8) {
+              float nx[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) nx[j] = (mv && kb0 + 8 + j < khi) ? __ldg(fp + (kb0 + 8 + j) * fs) : -CUDART_INF_F;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                if (kb0 + j < khi) {
+                  const float f = ptx::ex2(fr[j] - rs.x) * rs.y;  // empty slab: m2 = -inf, f = 0
+                  ptx::mbar_wait(&kfull[kbuf], kphase);
+                  ptx::tc_fence_after();
+#pragma unroll
+                  for (int hh = 0; hh < BN / 32; ++hh) {
+                    uint32_t v[32];
+                    ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + kbuf * BN + hh * 32, v);
+                    ptx::tmem_ld_wait();
+                    if (mv) {
+#pragma unroll
+                      for (int c = 0; c < 32; ++c) accv[hh * 32 + c] = fmaf(f, __uint_as_float(v[c]), accv[hh * 32 + c]);
+                    }
+                  }
+                  ptx::tc_fence_before();
+                  __syncwarp();
+                  if (lane == 0) ptx::mbar_arrive(&kempty[kbuf]);
+                  if (++kbuf == 8) { kbuf = 0; kphase ^= 1; }
+                }
+              }
+#pragma unroll
+              for (int j = 0; j < 8; ++j) fr[j] = nx[j];
+            }
+            auto publish = [&]() {
+              if (!a.done_cnt) return;
+              asm volatile("bar.sync 2, 128;" ::: "memory");
+              if (lead && lane == 0) {
+                if (ptx::atom_add_acqrel_gpu(a.done_cnt + bb, 1) == tpb - 1)
+                  ptx::st_release_gpu(a.done_epoch + bb, a.epoch + 1);
+              }
+            };
+            if (ng > 1) {
+              float* mine = a.skpart + (static_cast<long long>(unit0 + g) * BM + r) * BN;
+#pragma unroll
+              for (int q = 0; q < BN / 4; ++q)
+                reinterpret_cast<float4*>(mine)[q] = make_float4(accv[4 * q], accv[4 * q + 1], accv[4 * q + 2], accv[4 * q + 3]);
+              __threadfence();
+              asm volatile("bar.sync 1, 128;" ::: "memory");
+              if (lead && lane == 0) *sk_old = atomicAdd(a.skcnt + tile, 1);
+              asm volatile("bar.sync 1, 128;" ::: "memory");
+              const int old = *sk_old;
+              asm volatile("bar.sync 1, 128;" ::: "memory");  // sk_old reusable
+              if (old != ng - 1) {
+                publish();
+                continue;
+              }
+              __threadfence();
+              const float4* base = reinterpret_cast<const float4*>(a.skpart + (static_cast<long long>(unit0) * BM + r) * BN);
+#pragma unroll
+              for (int q = 0; q < BN / 4; ++q) {
+                const float4 w = __ldcg(base + q);
+                accv[4 * q] = w.x; accv[4 * q + 1] = w.y; accv[4 * q + 2] = w.z; accv[4 * q + 3] = w.w;
+              }
+              for (int gg = 1; gg < ng; ++gg) {
+                const float4* pp = base + static_cast<long long>(gg) * BM * BN / 4;
+#pragma unroll
+                for (int q = 0; q < BN / 4; ++q) {
+                  const float4 w = __ldcg(pp + q);
+                  accv[4 * q] += w.x; accv[4 * q + 1] += w.y; accv[4 * q + 2] += w.z; accv[4 * q + 3] += w.w;
+                }
+              }
+              if (lead && lane == 0) a.skcnt[tile] = 0;  // ready for the next launch
+            }
+            if (mv) {
+#pragma unroll
+              for (int hh = 0; hh < BN / 32; ++hh) {
+                const int n = hh * 32;
+                if (n >= a.N) break;
+                uint32_t pk[16];
+                epilogue_row32(a.ep, b1, b2, m, n, true, *reinterpret_cast<const uint32_t(*)[32]>(&accv[hh * 32]), pk,
+                               a.N - n);
+                uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.ep.out) +
+                                                    static_cast<long long>(b1) * a.ep.out_sb1 +
+                                                    static_cast<long long>(b2) * a.ep.out_sb2 +
+                                                    static_cast<long long>(m) * a.ep.out_sm + n);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                  if (8 * q < a.N - n) o[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+              }
+            }
+            publish();
+          }
+        } else {
+          for (int i = 0, t = take(0); t < total; t = take(++i)) {
+          }  // the other warps only keep the unit queue moving
+        }
+      } else if (ew < C::EPI) {
         // ---- f2 PV transform warps: thread = A-tile row (TMEM lane quarter x
         // lane), half = which four of the row's eight 16-byte chunks.  Rescale the
         // stored e = 2^(x - m2_slab) in place to P = e * f_slab (f_slab left in the
@@ -1511,6 +1688,7 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   if (a.ks > 1) a.tma_store = 0;
   const int sms = num_sms();
   a.pair = (MODE == 2 && BN == 32 && p.etile && p.M <= 64 && a.skng == 1 && !p.causal_k && !getenv("AC_NO_PAIR")) ? 1 : 0;
+  a.postscale = C::PS ? 1 : 0;
   int grid = MODE == 4 ? ((p.B1 * p.B2 + 1) / 2) * a.NT
                        : (a.pair ? (p.B1 * p.B2 + 1) / 2 : a.total_tiles_dense) * a.ks * (MODE == 2 ? a.skng : 1);
   int cap = (sms / a.ks) * a.ks;
