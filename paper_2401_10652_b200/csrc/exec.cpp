@@ -292,7 +292,12 @@ Arena build_arena(const Graph& g, const Plan& plan) {
   if (overlap_enabled()) {
     for (const Chain& c : fused_chains(g, plan)) {
       const int r = region_index(plan, c.scores);
-      if (r < 0 || g.nodes[c.scores].kind != "attn_scores") continue;  // (triangle chains: no overlap yet)
+      if (r < 0) continue;
+      // triangle chains: measured slower with the overlap (AF 15.8 -> 18.1 ms: the
+      // paired short-chunk scores lose more to dynamic tiles than the overlap saves),
+      // so only on request (AC_OVERLAP_TRI=1)
+      if (g.nodes[c.scores].kind == "tri_scores" && !(getenv("AC_OVERLAP_TRI") && getenv("AC_OVERLAP_TRI")[0] == '1'))
+        continue;
       // the region must be exactly the chain, so that in the chunk loop the PV of
       // chunk k is the launch right before the scores of chunk k + 1 (whose inputs
       // then all predate the region)
@@ -655,6 +660,7 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         p.etile = out.p;
         ep.stats_ss = p.M;
         ep.stats_sb1 = static_cast<int64_t>(p.M) * ns;
+        chain_overlap(e, i, cx, p);
       }
     } else if (k == "tri_pv") {
       const bool fz = e->fuse_role[i] == 3;
@@ -691,6 +697,7 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
           p.sk_part = reinterpret_cast<float*>(in(0).p + L.part);
           p.sk_cnt = reinterpret_cast<int*>(in(0).p + L.cnt) + 1;
         }
+        chain_overlap(e, i, cx, p);
       }
     } else {
       return unsup("no GPU kernel for this kind");

@@ -717,9 +717,11 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
             auto publish = [&]() {
               if (!a.done_cnt) return;
               asm volatile("bar.sync 2, 128;" ::: "memory");
-              if (lead && lane == 0) {
-                if (ptx::atom_add_acqrel_gpu(a.done_cnt + bb, 1) == tpb - 1)
-                  ptx::st_release_gpu(a.done_epoch + bb, a.epoch + 1);
+              if (lead && lane == 0) {  // (lane 0: the pair's first batch; pairs count both)
+                const int nq = a.pair && bb + 1 < static_cast<long long>(a.B1) * a.B2 ? 2 : 1;
+                for (int q = 0; q < nq; ++q)
+                  if (ptx::atom_add_acqrel_gpu(a.done_cnt + bb + q, 1) == tpb - 1)
+                    ptx::st_release_gpu(a.done_epoch + bb + q, a.epoch + 1);
               }
             };
             if (ng > 1) {
@@ -974,6 +976,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
       const float sc = a.ep.scale * L2E;
       int acc = 0;
       uint32_t aphase = 0, bph = 0;
+      int dep_ok_pb = -1;  // last pair whose predecessor PV is known finished
       for (int i = 0, t = take(0); t < total; t = take(++i)) {
         const int pb = t / a.NT, nt = t - pb * a.NT;
         const int nb = 2 * pb + 1 < Bt ? 2 : 1;
@@ -1054,6 +1057,16 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
                            "r"(pk[4 * q + 1]), "r"(pk[4 * q + 2]), "r"(pk[4 * q + 3])
                            : "memory");
             }
+          }
+          if (a.done_epoch && pb != dep_ok_pb) {
+            // chunk-loop overlap: the previous chunk's PV must be done with both batches
+            if (lane == 0) {
+              for (int q = 0; q < nb; ++q)
+                while (ptx::ld_acquire_gpu(a.done_epoch + 2 * pb + q) < a.dep_epoch) __nanosleep(128);
+              ptx::fence_proxy_async_global();
+            }
+            __syncwarp();
+            dep_ok_pb = pb;
           }
           if (mvalid && n0 < a.N)
             a.ep.stats[static_cast<long long>(bb) * a.ep.stats_sb1 + static_cast<long long>(n0 / 64) * a.ep.stats_ss + m] =
@@ -1678,7 +1691,7 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   a.done_epoch = (MODE == 2 && p.done_cnt) || (MODE != 2 && MODE != 0) ? p.done_epoch : nullptr;
   a.epoch = p.epoch;
   a.dep_epoch = p.dep_epoch;
-  a.tsched = (MODE == 1 || MODE == 3) ? p.tsched : nullptr;
+  a.tsched = (MODE == 1 || MODE == 3 || MODE == 4) ? p.tsched : nullptr;
   a.fstats = p.fuse_stats;
   a.fst_sb1 = p.fuse_sb1;
   a.fst_ss = p.fuse_ss;

@@ -274,3 +274,13 @@ def test_fused_attention_regime_plan():
     rows = blocks.sample_rows(16384, 1024, 24)
     ref = blocks.transformer_rows(workloads.config("gpt"), vals, rows)
     assert gu.rel_err(got["y"][torch.from_numpy(rows).cuda()], ref["y"]) < 2e-2
+
+
+def test_af_chunk_overlap_opt_in(monkeypatch):
+    """The chunk-loop overlap on the triangle chains (AC_OVERLAP_TRI=1: paired
+    short-chunk scores with dynamic tiles waiting on per-batch epochs of the previous
+    chunk's PV) keeps the results: vs the oracle and bitwise equal to unchunked."""
+    monkeypatch.setenv("AC_OVERLAP_TRI", "1")
+    og = workloads.tri_attn_pair(192, 128, 4, 32, "bf16", name="af_ov")
+    _check_all_plans(og, ["autochunk-plan 1\nregion s=row_scores e=row_pv n=4 dims=1\n"
+                          "region s=col_scores e=col_pv n=6 dims=0\n"], seed=9)
