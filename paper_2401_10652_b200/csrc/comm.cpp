@@ -76,27 +76,43 @@ int comm_world(const ac_comm* c) { return c ? c->world : 1; }
 ac_status comm_gather_slabs(const ac_comm* c, void* y, const std::vector<int64_t>& shape, int d, int esz, int64_t E,
                             int64_t L, int64_t n, cudaStream_t s) {
   if (!c || c->world == 1) return AC_OK;
-  for (int i = 0; i < d; ++i)
-    if (shape[i] != 1) return set_error(AC_ERR_UNSUPPORTED, "multi-GPU gather needs contiguous Y^c slabs (dim 0)");
-  int64_t inner = esz;
+  // Y^c chunked along dim d: every outer index (dims < d) holds one contiguous run of
+  // each owner's rows; the owner broadcasts each run (one run per owner when d = 0,
+  // e.g. attention rows; one per outer index otherwise, e.g. the AlphaFold j chunks
+  // of o[i, j, h, c]), in groups of at most 512 operations
+  int64_t inner = esz, outer = 1;
   for (size_t i = d + 1; i < shape.size(); ++i) inner *= shape[i];
+  for (int i = 0; i < d; ++i) outer *= shape[i];
+  const int64_t ext = shape[d] * inner;  // bytes per outer index
   const Nccl* nc = nccl();
   if (!nc) return set_error(AC_ERR_NCCL, "libnccl not available");
-  ac_status st = nccl_status(nc->GroupStart(), "ncclGroupStart");
-  if (st != AC_OK) return st;
-  for (int q = 0; q < c->world; ++q) {
-    const int64_t a = std::min(E, chunk_begin(q, n, c->world) * L);
-    const int64_t b = std::min(E, chunk_begin(q + 1, n, c->world) * L);
-    if (b <= a) continue;
-    char* p = static_cast<char*>(y) + a * inner;
-    st = nccl_status(nc->Broadcast(p, p, static_cast<size_t>((b - a) * inner), /*ncclUint8*/ 1, q, c->comm, s),
-                     "ncclBroadcast");
-    if (st != AC_OK) {
-      nc->GroupEnd();
-      return st;
+  int in_group = 0;
+  ac_status st = AC_OK;
+  for (int64_t o = 0; o < outer && st == AC_OK; ++o) {
+    for (int q = 0; q < c->world; ++q) {
+      const int64_t a = std::min(E, chunk_begin(q, n, c->world) * L);
+      const int64_t b = std::min(E, chunk_begin(q + 1, n, c->world) * L);
+      if (b <= a) continue;
+      if (in_group == 0) {
+        st = nccl_status(nc->GroupStart(), "ncclGroupStart");
+        if (st != AC_OK) return st;
+      }
+      char* p = static_cast<char*>(y) + o * ext + a * inner;
+      st = nccl_status(nc->Broadcast(p, p, static_cast<size_t>((b - a) * inner), /*ncclUint8*/ 1, q, c->comm, s),
+                       "ncclBroadcast");
+      if (st != AC_OK) break;
+      if (++in_group == 512) {
+        st = nccl_status(nc->GroupEnd(), "ncclGroupEnd");
+        in_group = 0;
+        if (st != AC_OK) return st;
+      }
     }
   }
-  return nccl_status(nc->GroupEnd(), "ncclGroupEnd");
+  if (in_group) {
+    ac_status e2 = nccl_status(nc->GroupEnd(), "ncclGroupEnd");
+    if (st == AC_OK) st = e2;
+  }
+  return st;
 }
 
 }  // namespace ac

@@ -84,3 +84,74 @@ def test_two_rank_chunk_split_equals_single_rank(n_chunks):
     assert all(ranges[i][1] == ranges[i + 1][0] for i in range(len(ranges) - 1))  # no gap/overlap
     for rank, y, _ in res:
         assert np.array_equal(y, ref), rank
+
+
+def _tri_row_graph(N=12, cz=8, H=2, c=4):
+    """Triangle attention around the starting node up to its gated output o[i, j, h, c]
+    (the region output whose chunks run along dim 1, j)."""
+    from oracle import workloads
+    B = Builder("mr_af", "f64")
+    B.input("z", (N, N, cz))
+    workloads._tri_weights(B, "row_", cz, H, c)
+    B.op("layernorm", ["z", "row_ln_g", "row_ln_b"], "zn", nid="ln", naxes=1, eps=1e-5)
+    B.op("linear", ["zn", "row_wb"], "bias", nid="proj_b", kin=1, out=[H], act="none", trans=1, swap=0, bias=0, res=0)
+    for nm, w, tr in (("q", "row_wq", 0), ("k", "row_wk", 0), ("vt", "row_wv", 1)):
+        B.op("linear", ["zn", w], nm, nid="proj_" + nm, kin=1, out=[H, c], act="none", trans=tr, swap=0, bias=0,
+             res=0)
+    B.op("linear", ["zn", "row_wg", "row_bg"], "g", nid="proj_g", kin=1, out=[H, c], act="sigmoid", trans=0, swap=0,
+         bias=1, res=0)
+    B.op("tri_scores", ["q", "k", "bias"], "s", nid="scores", scale=0.5, ending=0)
+    B.op("softmax", ["s"], "p", nid="softmax", dim=3)
+    B.op("tri_pv", ["p", "vt", "g"], "o", nid="pv", ending=0)
+    B.output("o")
+    return B.build()
+
+
+def _worker_dim1(rank, world, port, n_chunks, result_q):
+    """AlphaFold pattern: the region output o[i, j, h, c] is chunked along dim 1 (j);
+    owners broadcast one run per outer index i (comm_gather_slabs for d > 0)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2401_10652_b200 import api
+    g = _tri_row_graph()
+    cplan = api.plan_parse(api.graph_parse(og_graph.serialize(g)),
+                           f"autochunk-plan 1\nregion s=scores e=pv n={n_chunks} dims=1\n")
+    regions = select.user_plan(g, [("scores", "pv", n_chunks, (1,))]).regions
+    vals = {t: s.value for t, s in synth.make_inputs(g.input_specs(), 5).items()}
+    ranges = [cplan.rank_chunks(0, q, world) for q in range(world)]
+    c0, c1, L, E = ranges[rank]
+    with ops.exact_order():
+        mine = executor.run_chunked(g, vals, regions, chunk_ranges={0: (c0, c1)})["o"]
+    y = torch.from_numpy(np.ascontiguousarray(mine))
+    for o in range(y.shape[0]):                         # one run per outer index
+        for q, (a, b, _, _) in enumerate(ranges):
+            lo, hi = min(E, a * L), min(E, b * L)
+            if hi > lo:
+                run = y[o, lo:hi].clone()
+                dist.broadcast(run, src=q)
+                y[o, lo:hi] = run
+    result_q.put((rank, y.numpy(), None))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_chunks", [4, 3])
+def test_two_rank_dim1_chunks_equal_single_rank(n_chunks):
+    """SURVEY §8(e) AlphaFold: chunks along dim 1 exchanged per outer index."""
+    pytest.importorskip("paper_2401_10652_b200.api")
+    world = 2
+    port = 29700 + n_chunks + (os.getpid() % 1000)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_dim1, args=(r, world, port, n_chunks, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = _tri_row_graph()
+    vals = {t: s.value for t, s in synth.make_inputs(g.input_specs(), 5).items()}
+    with ops.exact_order():
+        ref = executor.run(g, vals)["o"]
+    for rank, y, _ in res:
+        assert np.array_equal(y, ref), rank
