@@ -706,6 +706,10 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
     err = gemm(e->dt, p, s);
   }
   e->stats.launches += 1;
+  if (err == cudaErrorInvalidValue)  // a kernel refused the operand layout (e.g. TMA needs 16-byte rows)
+    return set_error(AC_ERR_UNSUPPORTED, "node " + n.id + " (" + k +
+                                             "): no kernel for this shape / stride / alignment (bf16 rows must be "
+                                             "multiples of 8 elements for the tensor-core paths)");
   return cuda_status(err, ("node " + n.id).c_str());
 }
 

@@ -163,6 +163,59 @@ cudaError_t launch_softmax(const void* s, void* p, int64_t rows, int64_t ncols, 
   return cudaGetLastError();
 }
 
+__device__ __forceinline__ float sc_to_f(float v) { return v; }
+__device__ __forceinline__ float sc_to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T>
+__device__ __forceinline__ T sc_from_f(float v);
+template <>
+__device__ __forceinline__ float sc_from_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 sc_from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// Scalar fallback for rows the vector kernels cannot take (row length or stride
+// not a multiple of the 16-byte vector, e.g. a 9-token sequence): one warp per row,
+// three strided passes (max, sum, normalise); same masking and rounding as above.
+template <typename T>
+__global__ void __launch_bounds__(256) softmax_scalar_kernel(const T* __restrict__ s, T* __restrict__ p, int64_t rows,
+                                                             int64_t ncols, int64_t ld, int causal, int64_t row_off,
+                                                             int64_t group, int64_t gstride, int64_t ldo,
+                                                             int64_t gstrideo) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int64_t roff = group > 0 ? (r / group) * gstride + (r % group) * ld : r * ld;
+  const int64_t rofo = group > 0 ? (r / group) * gstrideo + (r % group) * ldo : r * ldo;
+  const T* srow = s + roff;
+  T* prow = p + rofo;
+  int64_t valid = ncols;
+  if (causal) {
+    const int64_t R = row_off + (group > 0 ? r % group : r);
+    valid = R + 1 < ncols ? R + 1 : ncols;
+  }
+  constexpr float L2E = 1.4426950408889634f;
+  float mx = -CUDART_INF_F;
+  for (int64_t c = lane; c < valid; c += 32) mx = fmaxf(mx, sc_to_f(srow[c]));
+  mx = warp_max(mx);
+  const float mxl = mx * L2E;
+  float sum = 0.f;
+  for (int64_t c = lane; c < valid; c += 32) sum += exp2f(fmaf(sc_to_f(srow[c]), L2E, -mxl));
+  sum = warp_sum(sum);
+  const float inv = 1.f / sum;
+  for (int64_t c = lane; c < ncols; c += 32)
+    prow[c] = sc_from_f<T>(c < valid ? exp2f(fmaf(sc_to_f(srow[c]), L2E, -mxl)) * inv : 0.f);
+}
+
+template <typename T>
+cudaError_t launch_softmax_scalar(const void* s, void* p, int64_t rows, int64_t ncols, int64_t ld, int causal,
+                                  int64_t row_off, int64_t group, int64_t gstride, int64_t ldo, int64_t gstrideo,
+                                  cudaStream_t st) {
+  const int64_t blocks = (rows + 7) / 8;
+  if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
+  softmax_scalar_kernel<T><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+      static_cast<const T*>(s), static_cast<T*>(p), rows, ncols, ld, causal, row_off, group, gstride, ldo, gstrideo);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- pipelined bf16 softmax
 // Persistent CTAs; each row is brought into shared memory with ONE bulk TMA copy
 // (cp.async.bulk, mbarrier completion) issued NBUF-1 rows ahead, so HBM reads of
@@ -699,11 +752,15 @@ cudaError_t softmax_rows(const void* s_in, void* p_out, int64_t rows, int64_t nc
                          int64_t ldo, int64_t gstrideo, int causal, int64_t row_off, int64_t group, int dtype,
                          cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
+  auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
   if (dtype == 1) {
-    if (ld % 8 || ldo % 8 || ncols % 8) return cudaErrorInvalidValue;
+    if (ld % 8 || ldo % 8 || ncols % 8 || gstride % 8 || gstrideo % 8 || !al(s_in) || !al(p_out))
+      return launch_softmax_scalar<__nv_bfloat16>(s_in, p_out, rows, ncols, ld, causal, row_off, group, gstride, ldo,
+                                                  gstrideo, st);
     return softmax_dispatch<__nv_bfloat16>(s_in, p_out, rows, ncols, ld, causal, row_off, group, gstride, ldo, gstrideo, st);
   }
-  if (ld % 4 || ldo % 4 || ncols % 4) return cudaErrorInvalidValue;
+  if (ld % 4 || ldo % 4 || ncols % 4 || gstride % 4 || gstrideo % 4 || !al(s_in) || !al(p_out))
+    return launch_softmax_scalar<float>(s_in, p_out, rows, ncols, ld, causal, row_off, group, gstride, ldo, gstrideo, st);
   return softmax_dispatch<float>(s_in, p_out, rows, ncols, ld, causal, row_off, group, gstride, ldo, gstrideo, st);
 }
 

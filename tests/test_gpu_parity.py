@@ -284,3 +284,52 @@ def test_af_chunk_overlap_opt_in(monkeypatch):
     og = workloads.tri_attn_pair(192, 128, 4, 32, "bf16", name="af_ov")
     _check_all_plans(og, ["autochunk-plan 1\nregion s=row_scores e=row_pv n=4 dims=1\n"
                           "region s=col_scores e=col_pv n=6 dims=0\n"], seed=9)
+
+
+@pytest.mark.parametrize("kind", ["transformer", "transformer_fa"])
+def test_degenerate_sizes(kind):
+    """Degenerate cases: the smallest aligned bf16 sequence (8 tokens)
+    with chunk_len 1 (n = extent) on the attention region and on the whole block (K / V
+    projections hoisted), and a ragged n = 3 FFN region; sequences that break the
+    16-byte row alignment of the bf16 tensor-core operands (9 tokens) are refused with
+    AC_ERR_UNSUPPORTED, never run wrong."""
+    from paper_2401_10652_b200 import api, _lib
+    gu = _gu()
+    og = workloads.block(kind, 8, 256, 4, 512, True, "bf16", name="deg")
+    attn = ("scores", "pv") if kind == "transformer" else ("attn", "proj_o")
+    _check_all_plans(og, ["autochunk-plan 1\nregion s=%s e=%s n=8 dims=0\n" % attn,
+                          "autochunk-plan 1\nregion s=proj_q e=ffn2 n=8 dims=0\n",
+                          "autochunk-plan 1\nregion s=ln2 e=ffn2 n=3 dims=0\n"], seed=2)
+    og9 = workloads.block(kind, 9, 256, 4, 512, True, "bf16", name="deg9")
+    cg = gu.c_graph(og9)
+    vals, dev = gu.make_values(og9, 2)
+    with pytest.raises(_lib.ACError) as ei:
+        gu.run(cg, gu.empty_plan(cg), og9, dev)
+    assert ei.value.status == _lib.AC_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("N", [1, 9])
+def test_degenerate_sizes_fp32(N):
+    """fp32 (SIMT) path at 1 and 9 tokens, chunk_len 1 plans: vs the oracle (1e-4) and
+    chunked == unchunked bitwise."""
+    og = workloads.block("transformer", N, 64, 2, 128, True, "f32", name="deg32")
+    plans = [] if N == 1 else ["autochunk-plan 1\nregion s=scores e=pv n=9 dims=0\n",
+                               "autochunk-plan 1\nregion s=proj_q e=ffn2 n=9 dims=0\n"]
+    _check_all_plans(og, plans, seed=2)
+
+
+def test_single_key_attention_is_v():
+    """Closed form: with one token the attention output is v itself,
+    so the block output is x + (a Wv + bv) Wo + bo."""
+    gu = _gu()
+    og = workloads.block("attn_only", 1, 64, 2, 0, True, "f32", name="one")
+    cg = gu.c_graph(og)
+    vals, dev = gu.make_values(og, 1)
+    got, _ = gu.run(cg, gu.empty_plan(cg), og, dev)
+    torch.cuda.synchronize()
+    x = vals["x"]
+    mu, var = x.mean(-1, keepdims=True), x.var(-1, keepdims=True)
+    a = (x - mu) / np.sqrt(var + 1e-5) * vals["ln1_g"] + vals["ln1_b"]
+    v = a @ vals["wv"].T + vals["bv"]
+    ref = x + v @ vals["wo"].T + vals["bo"]
+    assert gu.rel_err(got["x1"], ref) < 1e-4
