@@ -1062,7 +1062,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
             // chunk-loop overlap: the previous chunk's PV must be done with both batches
             if (lane == 0) {
               for (int q = 0; q < nb; ++q)
-                while (ptx::ld_acquire_gpu(a.done_epoch + 2 * pb + q) < a.dep_epoch) __nanosleep(128);
+                ptx::wait_geq_gpu(a.done_epoch + 2 * pb + q, a.dep_epoch);
               ptx::fence_proxy_async_global();
             }
             __syncwarp();
@@ -1326,7 +1326,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
             const int bb = b1 * a.B2 + b2;
             if (bb != dep_ok_b) {
               if (lane == 0) {
-                while (ptx::ld_acquire_gpu(a.done_epoch + bb) < a.dep_epoch) __nanosleep(128);
+                ptx::wait_geq_gpu(a.done_epoch + bb, a.dep_epoch);
                 ptx::fence_proxy_async_global();
               }
               __syncwarp();

@@ -252,6 +252,19 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// Spin until *p >= target: relaxed polls (an acquire per poll emits an L1 invalidate),
+// then one acquire load (a gpu-scope fence would also wait for this thread's
+// outstanding bulk stores)
+__device__ __forceinline__ void wait_geq_gpu(const int* p, int target) {
+  while (ld_relaxed_gpu(p) < target) __nanosleep(128);
+  (void)ld_acquire_gpu(p);
+}
 __device__ __forceinline__ void st_release_gpu(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
