@@ -404,7 +404,9 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(cons
     if (uq) {
       const int sl = i & 3;
       int* sc = MODE == 2 ? a.sched : a.tsched;
-      int u = sc ? atomicAdd(sc, 1) : cid + i * ncl;
+      // dynamic: the first unit of every CTA is its own index (no atomic round trip at
+      // the start of a launch), later ones come from the counter offset by the grid
+      int u = !sc || i == 0 ? cid + i * ncl : ncl + atomicAdd(sc, 1);
       if (u > total) u = total;
       ptx::mbar_wait(&uq_empty[sl], ((i >> 2) & 1) ^ 1);
       *reinterpret_cast<volatile int*>(&uq_slot[sl]) = u;
