@@ -67,8 +67,8 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
   uint64_t* s_full = bar + 2 + 2 * FA_STG;  // [2]
   uint64_t* s_free = s_full + 2;            // [2]
   uint64_t* p_full = s_full + 4;            // [2]
-  uint64_t* o_done = s_full + 6;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_full + 7);
+  uint64_t* pv_done = s_full + 6;           // [2]: PV of block q commits to pv_done[q & 1]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_full + 8);
   // softmax row halves exchange their block maxima ([block parity][half][row]) and,
   // at the end, their partial sums ([half][row])
   float* xmax = reinterpret_cast<float*>(bar + 32);
@@ -91,7 +91,8 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
       ptx::mbar_init(&s_free[b], 8);
       ptx::mbar_init(&p_full[b], 8);
     }
-    ptx::mbar_init(o_done, 1);
+    ptx::mbar_init(&pv_done[0], 1);
+    ptx::mbar_init(&pv_done[1], 1);
     ptx::fence_barrier_init();
   }
   if (warp == 1) ptx::tmem_alloc<512>(tmem_holder);
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
                             ptx::sdesc_sw128(vb + kb * (V_BYTES / 2) + kk * 32), IDO, (j > 1 || k) ? 1u : 0u);
             }
             ptx::mma_commit(&kv_empty[pst]);
-            ptx::mma_commit(o_done);
+            ptx::mma_commit(&pv_done[pidx & 1]);
           }
           __syncwarp();
           pidx = sidx;
@@ -202,7 +203,6 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
     const uint32_t lrow = static_cast<uint32_t>(quarter * 32) << 16;
     const uint32_t nbar = 1 + quarter;  // named barrier of the two warps of a quarter
     int sidx = 0;
-    int pv = 0;  // PV completions awaited so far (o_done phase)
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       int head, mt, nkb;
       tile(t, head, mt, nkb);
@@ -253,10 +253,17 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
         }
         l = l * alpha + ls;
         m = m_new;
-        if (j >= 1) {
-          // PV_{j-1} done: O may be rescaled and P buffer b (last read by PV_{j-2}) rewritten
-          ptx::mbar_wait(o_done, pv & 1);
-          ++pv;
+        // O needs rescaling only when some row's max moved (alpha != 1; skipping a
+        // multiply by 1.0 is exact): then PV_{j-1} must be complete; otherwise only
+        // PV_{j-2} (the last reader of P buffer b) is awaited, so the exponentials of
+        // block j overlap PV_{j-1}
+        const bool resc = j >= 1 && __any_sync(0xffffffffu, alpha != 1.f);
+        if (resc) {
+          ptx::mbar_wait(&pv_done[(sidx - 1) & 1], ((sidx - 1) >> 1) & 1);
+        } else if (sidx >= 2) {
+          ptx::mbar_wait(&pv_done[sidx & 1], ((sidx - 2) >> 1) & 1);
+        }
+        if (resc) {
           ptx::tc_fence_after();
           uint32_t o[32];
           ptx::tmem_ld32(tmem + lrow + 256 + hf * 32, o);
@@ -282,8 +289,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
       }
       // epilogue: wait for the last PV; l = sum of both halves; o = O / l
       xsum[hf * 128 + r] = l;
-      ptx::mbar_wait(o_done, pv & 1);
-      ++pv;
+      ptx::mbar_wait(&pv_done[(sidx - 1) & 1], ((sidx - 1) >> 1) & 1);
       ptx::tc_fence_after();
       uint32_t o[32];
       ptx::tmem_ld32(tmem + lrow + 256 + hf * 32, o);
