@@ -72,6 +72,8 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
     defs = []
     if os.environ.get("AC_DEBUG_HANG"):
         defs.append("-DAC_DEBUG_HANG=1")
+    if os.environ.get("AC_PV_POSTSCALE") is not None:  # experiments: PV variant at build time
+        defs.append("-DAC_PV_POSTSCALE=" + os.environ["AC_PV_POSTSCALE"])
     if ninc:
         inc.append("-I" + ninc)
         defs.append("-DAC_HAVE_NCCL_H=1")
