@@ -50,6 +50,7 @@ struct alignas(64) FaArgs {
   int causal;
   long long row_off;
   float cl;  // scale * log2(e)
+  int pdl;
 };
 
 __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_constant__ FaArgs a) {
@@ -100,6 +101,10 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;  // S buffers at columns 0 / 128, O at 256
+  if (a.pdl) {  // chunk loop: the prologue overlapped the previous kernel; now wait for its results
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+  }
 
   // work tile t -> (head, m-tile, key blocks); causal: heaviest (last) m-tiles first
   auto tile = [&](int t, int& head, int& mt, int& nkb) {
@@ -391,6 +396,20 @@ cudaError_t attn_fused(const AttnFusedProblem& p, cudaStream_t s) {
   a.cl = p.scale * 1.4426950408889634f;
   const long long tiles = static_cast<long long>(a.H) * a.MT;
   const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
+  a.pdl = p.pdl;
+  if (p.pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(FA_THREADS);
+    cfg.dynamicSmemBytes = FA_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, attn_fused_kernel, a);
+  }
   attn_fused_kernel<<<grid, FA_THREADS, FA_SMEM, s>>>(a);
   return cudaGetLastError();
 }

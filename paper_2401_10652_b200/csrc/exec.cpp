@@ -104,6 +104,11 @@ bool pv_splitk(bool causal, int64_t nk) {
 // Chunk-loop overlap of fused chains (programmatic dependent launch + per-batch
 // epochs): the next chunk's scores start on SMs the PV's tail frees.
 // AC_OVERLAP=0 disables it (every launch then waits for the previous one).
+bool pdl_enabled() {
+  const char* v = getenv("AC_PDL");
+  return !(v && v[0] == '0');
+}
+
 bool overlap_enabled() {
   const char* v = getenv("AC_OVERLAP");
   return !(v && v[0] == '0');
@@ -354,6 +359,7 @@ int64_t extent(const View& v, int a, int b) {
 
 struct NodeCtx {
   int chunk = -1;       // index of the chunk within this rank's chunk loop (-1: none)
+  int pdl = 0;          // launch early (programmatic dependent launch), kernel waits in-kernel
   int64_t row_off = 0;  // global query-row offset of this view (causal)
   int64_t col_off = 0;
   bool fast = false;    // aligned causal chain: skip masked tiles / keys
@@ -380,6 +386,7 @@ void chain_overlap(const ac_exec* e, int node, const NodeCtx& cx, GemmProblem& p
   p.done_epoch = c;
   if (e->fuse_role[node] == 1) {
     p.pdl = k > 0 ? 1 : 0;
+    p.pdl_wait = 0;  // ordered by the per-batch epochs instead (the PV of chunk k - 1 is still draining)
     p.dep_epoch = k;
     p.tsched = c + B + k;
   } else {
@@ -423,7 +430,7 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
     const int64_t C = extent(x, x.nd - na, x.nd);
     if (collapse(x, 0, x.nd) != 1 || collapse(out, 0, out.nd) != 1) return unsup("non-contiguous rows");
     err = layernorm(x.p, in(1).p, in(2).p, out.p, extent(x, 0, x.nd - na), static_cast<int>(C),
-                    static_cast<float>(n.af("eps", 1e-5)), dtc, s);
+                    static_cast<float>(n.af("eps", 1e-5)), dtc, s, cx.pdl);
   } else if (k == "softmax" && e->fuse_role[i] == 2) {
     // fused chain: the softmax node only combines the slab statistics the scores
     // step left in P's buffer into per-slab factors; the PV applies them
@@ -434,7 +441,7 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
     err = softmax_stats_combine(reinterpret_cast<float2*>(out.p), B, M, static_cast<int>(ns),
                                 M * ns, M, cx.fast ? 1 : 0, cx.row_off,
                                 reinterpret_cast<float2*>(out.p + L.rowst), reinterpret_cast<int*>(out.p + L.cnt),
-                                L.ncnt, s, cx.chunk >= 0 && e->arena.ctrl_off[e->fuse_head[i]] >= 0 ? 1 : 0);
+                                L.ncnt, s, cx.pdl || (cx.chunk >= 0 && e->arena.ctrl_off[e->fuse_head[i]] >= 0) ? 1 : 0);
   } else if (k == "softmax") {
     const View& x = in(0);
     if (n.ai("dim") != x.nd - 1 || x.st[x.nd - 1] != 1) return unsup("softmax over a non-last dim");
@@ -464,10 +471,12 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
     p.scale = static_cast<float>(n.af("scale", 1.0));
     p.causal = static_cast<int>(n.ai("causal"));
     p.row_off = cx.row_off;
+    p.pdl = cx.pdl;
     if (p.dh != 64) return unsup("fused attention kernel takes head dim 64");
     err = attn_fused(p, s);
   } else {
     GemmProblem p;
+    p.pdl = p.pdl_wait = cx.pdl;  // (chain_overlap may override for the f2 chains)
     Epilogue& ep = p.ep;
     ep.out = out.p;
     if (k == "linear") {
@@ -968,6 +977,8 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
           return set_error(AC_ERR_CUDA, "cudaMemsetAsync (chunk-loop control block) failed");
       }
     }
+    bool first_launch = true;
+    const bool loop_pdl = pdl_enabled();
     for (int64_t c = c0; c < c1; ++c) {
       const int64_t off = c * L;
       const int64_t len = std::min(L, R.extent - off);
@@ -1008,6 +1019,10 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
         NodeCtx cx;
         cx.fast = e->causal_fast[j] != 0;
         cx.chunk = static_cast<int>(c - c0);
+        // every launch of the chunk loop but the first may start during its
+        // predecessor's tail (it waits in-kernel before touching data); AC_PDL=0 off
+        cx.pdl = loop_pdl && !first_launch ? 1 : 0;
+        first_launch = false;
         const int d = R.dim_of(nj.output);
         if (d >= 0 && d == e->chain_rows_dim[j]) cx.row_off = off;
         ac_status st = launch_node(e, j, *use, cx, s);

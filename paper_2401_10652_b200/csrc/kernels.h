@@ -124,6 +124,7 @@ struct AttnFusedProblem {
   float scale = 1.f;
   int causal = 0;
   int64_t row_off = 0;
+  int pdl = 0;  // programmatic dependent launch (chunk loop): wait for the predecessor in-kernel
 };
 cudaError_t attn_fused(const AttnFusedProblem& p, cudaStream_t s);
 
@@ -136,7 +137,7 @@ cudaError_t gemm_f32(const GemmProblem& p, cudaStream_t s);
 // Row ops.  dtype: 0 = fp32, 1 = bf16.
 // LayerNorm over the last C elements of `rows` rows (row stride = C).
 cudaError_t layernorm(const void* x, const void* gamma, const void* beta, void* y, int64_t rows,
-                      int C, float eps, int dtype, cudaStream_t s);
+                      int C, float eps, int dtype, cudaStream_t s, int pdl = 0);
 // Row softmax: rows of `ncols` values with row stride `ld` (elements).  With
 // causal, row r is query row R = row_off + (r % group) (rows of several heads
 // are stacked); it reads columns <= R and writes columns [0, ceil128(R+1)) with

@@ -593,7 +593,11 @@ cudaError_t softmax_dispatch(const void* s, void* p, int64_t rows, int64_t ncols
 template <typename T, int VPT>
 __global__ void __launch_bounds__(256) layernorm_kernel(const T* __restrict__ x, const T* __restrict__ g,
                                                         const T* __restrict__ b, T* __restrict__ y, int64_t rows,
-                                                        int C, float eps) {
+                                                        int C, float eps, int pdl) {
+  if (pdl) {  // chunk loop: launched early (programmatic dependent launch); wait for the input
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
   constexpr int VN = Vec<T>::N;
   const int lane = threadIdx.x & 31;
   const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
@@ -649,7 +653,7 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const T* __restrict__ x,
 
 template <typename T>
 cudaError_t layernorm_dispatch(const void* x, const void* g, const void* b, void* y, int64_t rows, int C,
-                               float eps, cudaStream_t st) {
+                               float eps, cudaStream_t st, int pdl) {
   constexpr int VN = Vec<T>::N;
   if (C % VN != 0) return cudaErrorInvalidValue;
   const int nv = C / VN;
@@ -660,12 +664,23 @@ cudaError_t layernorm_dispatch(const void* x, const void* g, const void* b, void
   auto G = static_cast<const T*>(g);
   auto B = static_cast<const T*>(b);
   auto Y = static_cast<T*>(y);
-  if (nv <= 32) layernorm_kernel<T, 1><<<gb, 256, 0, st>>>(X, G, B, Y, rows, C, eps);
-  else if (nv <= 64) layernorm_kernel<T, 2><<<gb, 256, 0, st>>>(X, G, B, Y, rows, C, eps);
-  else if (nv <= 128) layernorm_kernel<T, 4><<<gb, 256, 0, st>>>(X, G, B, Y, rows, C, eps);
-  else if (nv <= 256) layernorm_kernel<T, 8><<<gb, 256, 0, st>>>(X, G, B, Y, rows, C, eps);
-  else if (nv <= 512) layernorm_kernel<T, 16><<<gb, 256, 0, st>>>(X, G, B, Y, rows, C, eps);
-  else return cudaErrorInvalidValue;
+  void (*kern)(const T*, const T*, const T*, T*, int64_t, int, float, int) =
+      nv <= 32 ? layernorm_kernel<T, 1> : nv <= 64 ? layernorm_kernel<T, 2> : nv <= 128 ? layernorm_kernel<T, 4>
+      : nv <= 256 ? layernorm_kernel<T, 8> : nv <= 512 ? layernorm_kernel<T, 16> : nullptr;
+  if (!kern) return cudaErrorInvalidValue;
+  if (pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(gb);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, X, G, B, Y, rows, C, eps, 1);
+  }
+  kern<<<gb, 256, 0, st>>>(X, G, B, Y, rows, C, eps, 0);
   return cudaGetLastError();
 }
 
@@ -765,10 +780,10 @@ cudaError_t softmax_rows(const void* s_in, void* p_out, int64_t rows, int64_t nc
 }
 
 cudaError_t layernorm(const void* x, const void* gamma, const void* beta, void* y, int64_t rows, int C, float eps,
-                      int dtype, cudaStream_t st) {
+                      int dtype, cudaStream_t st, int pdl) {
   if (rows <= 0) return cudaSuccess;
-  if (dtype == 1) return layernorm_dispatch<__nv_bfloat16>(x, gamma, beta, y, rows, C, eps, st);
-  return layernorm_dispatch<float>(x, gamma, beta, y, rows, C, eps, st);
+  if (dtype == 1) return layernorm_dispatch<__nv_bfloat16>(x, gamma, beta, y, rows, C, eps, st, pdl);
+  return layernorm_dispatch<float>(x, gamma, beta, y, rows, C, eps, st, pdl);
 }
 
 }  // namespace ac
