@@ -101,7 +101,12 @@ struct Cfg {
   // <= 112 registers) with a single 4 KB bf16 staging box per warp; K = head dim
   // is one or two k-blocks, so two smem stages suffice
   static constexpr bool PS = MODE == 2 && AC_PV_POSTSCALE;  // post-scale PV: 4 scale/output warps
-  static constexpr int EPI = (MODE == 1 || MODE == 3 || MODE == 4) ? 16 : PS ? 4 : EPI_WARPS;
+  // f2 scores at BN = 128: 8 epilogue warps (one 64-column slab each) and two CTAs
+  // per SM, whose tiles run out of phase (one CTA's max pass beside the other's
+  // exponentials)
+  static constexpr bool DUAL = MODE == 1 && BN == 128;
+  static constexpr int EPI = DUAL ? 8 : (MODE == 1 || MODE == 3 || MODE == 4) ? 16 : PS ? 4 : EPI_WARPS;
+  static constexpr int MINB = DUAL ? 2 : 1;
   // f2 PV (MODE 2): the EPI warps transform A tiles; XEPI more warps (one per
   // TMEM lane quarter) run the output epilogue so the transform never stalls
   static constexpr int XEPI = MODE == 2 && !PS ? 4 : 0;
@@ -266,7 +271,7 @@ __device__ __forceinline__ void decode_unit(const GemmArgs& a, const int* prefix
 // lean TMA-store epilogue only); 2 f2 PV (A tile e rescaled to P in shared
 // memory by all epilogue warps, which also run the output epilogue)
 template <int BN, int MODE>
-__global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1) gemm_tc_kernel(const __grid_constant__ GemmArgs a) {
+__global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) gemm_tc_kernel(const __grid_constant__ GemmArgs a) {
   using C = Cfg<BN, MODE>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1706,7 +1711,7 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   a.postscale = C::PS ? 1 : 0;
   int grid = MODE == 4 ? ((p.B1 * p.B2 + 1) / 2) * a.NT
                        : (a.pair ? (p.B1 * p.B2 + 1) / 2 : a.total_tiles_dense) * a.ks * (MODE == 2 ? a.skng : 1);
-  int cap = (sms / a.ks) * a.ks;
+  int cap = C::DUAL ? 2 * sms : (sms / a.ks) * a.ks;
   {
     static int dbg = -1, dgrid = -1;
     if (dbg < 0) {
@@ -1814,6 +1819,8 @@ cudaError_t gemm_tc(const GemmProblem& p, cudaStream_t s, int bn_hint) {
     }
   }
   if (p.ep.stats) {
+    static const int sbn = getenv("AC_SCORES_BN") ? atoi(getenv("AC_SCORES_BN")) : 0;  // experiments
+    if (sbn && p.N > 128) bn = sbn;
     switch (bn) {
       case 64: return launch<64, 1>(p, s);
       case 128: return launch<128, 1>(p, s);
