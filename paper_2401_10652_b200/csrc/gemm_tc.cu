@@ -1255,63 +1255,29 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
           };
           uint32_t r[32];
           float mx = -CUDART_INF_F;
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            load_x(hh, r);
-            float q0 = -CUDART_INF_F, q1 = -CUDART_INF_F, q2 = -CUDART_INF_F, q3 = -CUDART_INF_F;
-            if (lim >= hh * 32 + 31) {
-#pragma unroll
-              for (int j = 0; j < 32; j += 4) {
-                q0 = fmaxf(q0, __uint_as_float(r[j])); q1 = fmaxf(q1, __uint_as_float(r[j + 1]));
-                q2 = fmaxf(q2, __uint_as_float(r[j + 2])); q3 = fmaxf(q3, __uint_as_float(r[j + 3]));
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (hh * 32 + j <= lim) q0 = fmaxf(q0, __uint_as_float(r[j]));
-            }
-            mx = fmaxf(mx, fmaxf(fmaxf(q0, q1), fmaxf(q2, q3)));
-          }
-          const float m2 = mx * cl;
-          const float mref = mx == -CUDART_INF_F ? 0.f : m2;
           float l0 = 0.f, l1 = 0.f;
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            load_x(hh, r);
-            if (hh == 1 && last) {
-              ptx::tc_fence_before();
-              __syncwarp();
-              if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-            }
+          float m2;
+          // exponentials of the 32 columns hh*32.. in r against reference mref, packed into
+          // the staging box (chunks hh*4..hh*4+3 of this thread's row)
+          auto emit = [&](int hh, float mref, float& s0, float& s1) {
             uint32_t pk[16];
             if (lim >= hh * 32 + 31) {
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
-#if AC_EX2_PACKED
-                // one MUFU op per pair: e = 2^bf16(x - m2) on bf16x2 (reading R19);
-                // the slab sum adds the stored (rounded) e
-                const __nv_bfloat162 dh = __floats2bfloat162_rn(fmaf(__uint_as_float(r[2 * j]), cl, -mref),
-                                                                fmaf(__uint_as_float(r[2 * j + 1]), cl, -mref));
-                const uint32_t e = ptx::ex2_bf16x2(*reinterpret_cast<const uint32_t*>(&dh));
-                l0 += __uint_as_float(e << 16);
-                l1 += __uint_as_float(e & 0xffff0000u);
-                pk[j] = e;
-#else
                 const float e0 = ptx::ex2(fmaf(__uint_as_float(r[2 * j]), cl, -mref));
                 const float e1 = ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), cl, -mref));
-                l0 += e0;
-                l1 += e1;
+                s0 += e0;
+                s1 += e1;
                 __nv_bfloat162 h = __floats2bfloat162_rn(e0, e1);
                 pk[j] = *reinterpret_cast<uint32_t*>(&h);
-#endif
               }
             } else {
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
                 const float e0 = hh * 32 + 2 * j <= lim ? ptx::ex2(fmaf(__uint_as_float(r[2 * j]), cl, -mref)) : 0.f;
                 const float e1 = hh * 32 + 2 * j + 1 <= lim ? ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), cl, -mref)) : 0.f;
-                l0 += e0;
-                l1 += e1;
+                s0 += e0;
+                s1 += e1;
                 __nv_bfloat162 h = __floats2bfloat162_rn(e0, e1);
                 pk[j] = *reinterpret_cast<uint32_t*>(&h);
               }
@@ -1325,6 +1291,75 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
               asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[4 * q]),
                            "r"(pk[4 * q + 1]), "r"(pk[4 * q + 2]), "r"(pk[4 * q + 3])
                            : "memory");
+            }
+          };
+          auto slab_max = [&](int hh) {
+            float q0 = -CUDART_INF_F, q1 = -CUDART_INF_F, q2 = -CUDART_INF_F, q3 = -CUDART_INF_F;
+            if (lim >= hh * 32 + 31) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                q0 = fmaxf(q0, __uint_as_float(r[j])); q1 = fmaxf(q1, __uint_as_float(r[j + 1]));
+                q2 = fmaxf(q2, __uint_as_float(r[j + 2])); q3 = fmaxf(q3, __uint_as_float(r[j + 3]));
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (hh * 32 + j <= lim) q0 = fmaxf(q0, __uint_as_float(r[j]));
+            }
+            mx = fmaxf(mx, fmaxf(fmaxf(q0, q1), fmaxf(q2, q3)));
+          };
+          if constexpr (!BIASED) {
+            // one TMEM pass (reading R19): the slab's reference is its first score x0
+            // (column 0 is valid whenever any column is: masks are suffixes), so the
+            // exponentials start before the slab max is known; a row whose max exceeds
+            // x0 by more than 96 (log2 units) is redone against its max (the TMEM
+            // reload is warp-collective, the decision per row: results depend only on
+            // the row's own data)
+            load_x(0, r);
+            float mref = lim >= 0 ? __uint_as_float(r[0]) * cl : 0.f;
+            slab_max(0);
+            emit(0, mref, l0, l1);
+            load_x(1, r);
+            slab_max(1);
+            const bool redo = lim >= 0 && mx * cl - mref > 96.f;
+            const bool any_redo = __any_sync(0xffffffffu, redo);
+            if (!any_redo && last) {
+              ptx::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            }
+            if (redo) {
+              mref = mx * cl;
+              l0 = l1 = 0.f;
+            }
+            emit(1, mref, l0, l1);
+            if (any_redo) {
+              load_x(0, r);
+              if (last) {
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+              }
+              if (redo) emit(0, mref, l0, l1);
+            }
+            m2 = lim >= 0 ? mref : -CUDART_INF_F;
+          } else {
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              load_x(hh, r);
+              slab_max(hh);
+            }
+            m2 = mx * cl;
+            const float mref = mx == -CUDART_INF_F ? 0.f : m2;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              load_x(hh, r);
+              if (hh == 1 && last) {
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+              }
+              emit(hh, mref, l0, l1);
             }
           }
           if (a.done_epoch) {
