@@ -333,3 +333,39 @@ def test_single_key_attention_is_v():
     v = a @ vals["wv"].T + vals["bv"]
     ref = x + v @ vals["wo"].T + vals["bo"]
     assert gu.rel_err(got["x1"], ref) < 1e-4
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_f2_large_logit_range(causal):
+    """f2 scores take each 64-key slab's first score as its exponent reference and
+    redo a row against the slab max when the max exceeds it by more than 96 (log2
+    units).  Wq scaled by 64 (exact in bf16) spreads the logits over hundreds of units
+    so both paths run: vs the oracle on the same values, chunked == unchunked bitwise.
+    At this logit scale the bf16 rounding of q and k alone moves logits by whole
+    units and decides near-ties, so the reference takes q, k, vT and o rounded where
+    the GPU stores them (the oracle's mirror mode, reading R17) while S stays exact,
+    as in the fused chain (reading R19)."""
+    gu = _gu()
+    og = workloads.block("attn_only", 640, 256, 4, 0, causal, "bf16", name="wide")
+    vals, dev = gu.make_values(og, 4)
+    vals["wq"] = vals["wq"] * 64.0
+    dev["wq"] = (dev["wq"].float() * 64.0).bfloat16()
+    cg = gu.c_graph(og)
+    from paper_2401_10652_b200 import api
+    mir = executor.run(og, vals, mirror=True, keep_all=True)
+    q, k, vt = mir["q"], mir["k"], mir["vt"]                     # [N,h,dh], [N,h,dh], [h,dh,N]
+    sc = np.einsum("ihd,jhd->hij", q, k) / 8.0
+    if causal:
+        sc = np.where(np.triu(np.ones(sc.shape[1:], bool), 1)[None], -np.inf, sc)
+    p = np.exp(sc - sc.max(-1, keepdims=True))
+    p /= p.sum(-1, keepdims=True)
+    o = np.einsum("hij,hdj->ihd", p, vt).reshape(q.shape[0], -1)
+    o = torch.from_numpy(o).bfloat16().double().numpy()          # O stored in bf16
+    ref = vals["x"] + o @ vals["wo"].T + vals["bo"]
+    base, _ = gu.run(cg, gu.empty_plan(cg), og, dev)
+    torch.cuda.synchronize()
+    assert gu.rel_err(base["x1"], ref) < 2e-2
+    for n in (5, 2):
+        got, _ = gu.run(cg, api.plan_parse(cg, "autochunk-plan 1\nregion s=scores e=pv n=%d dims=0\n" % n), og, dev)
+        torch.cuda.synchronize()
+        assert torch.equal(got["x1"], base["x1"]), n
