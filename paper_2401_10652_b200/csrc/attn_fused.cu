@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -31,15 +32,25 @@ namespace ac {
 namespace {
 
 constexpr int FA_BM = 128;   // query rows per tile
-constexpr int FA_BN = 128;   // keys per block
+// Key block BNK = 128 (one CTA per SM) or 64 (two CTAs per SM, whose softmax and
+// MMA phases interleave; chosen when the launch has at least two tiles per SM)
+template <int BNK>
+struct FaCfg {
+  static constexpr int BN = BNK;        // keys per block
+  static constexpr int HK = BNK / 2;    // keys per softmax half-row
+  static constexpr int MINB = BNK == 64 ? 2 : 1;
+  static constexpr int OCOL = 2 * BNK;  // TMEM column of the O accumulator (after two S buffers)
+  static constexpr int TMEM = OCOL + 64 <= 256 ? 256 : 512;
+  static constexpr int K_BYTES = BNK * 64 * 2;
+  static constexpr int V_BYTES = 64 * BNK * 2;   // 64-key boxes of 8 KB
+  static constexpr int P_BYTES = 128 * BNK * 2;  // 64-key k-blocks of 16 KB
+  static constexpr int SMEM = 1024 + 128 * 64 * 2 + 3 * (K_BYTES + V_BYTES) + 2 * P_BYTES + 256 + 2 * 2 * 128 * 4 +
+                              128 * 4 * 2;
+};
 constexpr int FA_DH = 64;    // head dim (one 128-byte swizzle row)
 constexpr int FA_STG = 3;    // K/V ring depth
 constexpr int FA_THREADS = 320;  // producer, MMA, 8 softmax warps
 constexpr int Q_BYTES = FA_BM * FA_DH * 2;        // 16 KB
-constexpr int K_BYTES = FA_BN * FA_DH * 2;        // 16 KB
-constexpr int V_BYTES = FA_DH * FA_BN * 2;        // 16 KB (two 64-key boxes of 8 KB)
-constexpr int P_BYTES = FA_BM * FA_BN * 2;        // 32 KB (two 64-key k-blocks of 16 KB)
-constexpr int FA_SMEM = 1024 + Q_BYTES + FA_STG * (K_BYTES + V_BYTES) + 2 * P_BYTES + 256 + 2 * 2 * 128 * 4 + 128 * 4 * 2;
 
 struct alignas(64) FaArgs {
   CUtensorMap tq, tk, tv;
@@ -53,7 +64,11 @@ struct alignas(64) FaArgs {
   int pdl;
 };
 
-__global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_constant__ FaArgs a) {
+template <int BNK>
+__global__ void __launch_bounds__(FA_THREADS, FaCfg<BNK>::MINB) attn_fused_kernel(const __grid_constant__ FaArgs a) {
+  using CF = FaCfg<BNK>;
+  constexpr int FA_BN = CF::BN, HK = CF::HK, OCOL = CF::OCOL, FA_TMEM = CF::TMEM;
+  constexpr int K_BYTES = CF::K_BYTES, V_BYTES = CF::V_BYTES, P_BYTES = CF::P_BYTES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -96,7 +111,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
     ptx::mbar_init(&pv_done[1], 1);
     ptx::fence_barrier_init();
   }
-  if (warp == 1) ptx::tmem_alloc<512>(tmem_holder);
+  if (warp == 1) ptx::tmem_alloc<FA_TMEM>(tmem_holder);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -134,8 +149,8 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
           ptx::mbar_wait(&kv_empty[st], ph ^ 1);
           ptx::mbar_expect_tx(&kv_full[st], K_BYTES + V_BYTES);
           ptx::tma_load_4d(sK + st * K_BYTES, &a.tk, &kv_full[st], 0, j * FA_BN, head, 0);
-          ptx::tma_load_4d(sV + st * V_BYTES, &a.tv, &kv_full[st], j * FA_BN, 0, head, 0);
-          ptx::tma_load_4d(sV + st * V_BYTES + V_BYTES / 2, &a.tv, &kv_full[st], j * FA_BN + 64, 0, head, 0);
+          for (int vb = 0; vb < FA_BN / 64; ++vb)
+            ptx::tma_load_4d(sV + st * V_BYTES + vb * 8192, &a.tv, &kv_full[st], j * FA_BN + vb * 64, 0, head, 0);
           if (++st == FA_STG) { st = 0; ph ^= 1; }
         }
       }
@@ -181,8 +196,8 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
 #pragma unroll
             for (int k = 0; k < FA_BN / 16; ++k) {
               const int kb = k >> 2, kk = k & 3;
-              ptx::mma_bf16(tmem + 256, ptx::sdesc_sw128(pa + kb * (P_BYTES / 2) + kk * 32),
-                            ptx::sdesc_sw128(vb + kb * (V_BYTES / 2) + kk * 32), IDO, (j > 1 || k) ? 1u : 0u);
+              ptx::mma_bf16(tmem + OCOL, ptx::sdesc_sw128(pa + kb * 16384 + kk * 32),
+                            ptx::sdesc_sw128(vb + kb * 8192 + kk * 32), IDO, (j > 1 || k) ? 1u : 0u);
             }
             ptx::mma_commit(&kv_empty[pst]);
             ptx::mma_commit(&pv_done[pidx & 1]);
@@ -217,24 +232,25 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
         const int b = sidx & 1;
         ptx::mbar_wait(&s_full[b], (sidx >> 1) & 1);
         ptx::tc_fence_after();
-        uint32_t s[64];
-        ptx::tmem_ld32(tmem + lrow + b * FA_BN + hf * 64, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-        ptx::tmem_ld32(tmem + lrow + b * FA_BN + hf * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+        uint32_t s[HK];
+#pragma unroll
+        for (int c = 0; c < HK / 32; ++c)
+          ptx::tmem_ld32(tmem + lrow + b * FA_BN + hf * HK + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]));
         ptx::tmem_ld_wait();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&s_free[b]);
         // mask: causal keys past the row, keys past Nk
-        const long long k0 = static_cast<long long>(j) * FA_BN + hf * 64;
+        const long long k0 = static_cast<long long>(j) * FA_BN + hf * HK;
         long long lim = a.Nk - 1 - k0;  // last valid column of this half-block
         if (a.causal && qg - k0 < lim) lim = qg - k0;
         float mb = -CUDART_INF_F;
-        if (lim >= 63) {
+        if (lim >= HK - 1) {
 #pragma unroll
-          for (int c = 0; c < 64; ++c) mb = fmaxf(mb, __uint_as_float(s[c]));
+          for (int c = 0; c < HK; ++c) mb = fmaxf(mb, __uint_as_float(s[c]));
         } else {
 #pragma unroll
-          for (int c = 0; c < 64; ++c) {
+          for (int c = 0; c < HK; ++c) {
             if (c > lim) s[c] = __float_as_uint(-CUDART_INF_F);
             mb = fmaxf(mb, __uint_as_float(s[c]));
           }
@@ -247,9 +263,9 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
         const float mref = m_new == -CUDART_INF_F ? 0.f : m_new;
         const float alpha = m == -CUDART_INF_F ? 0.f : ptx::ex2(m - mref);
         float ls = 0.f;
-        uint32_t pk[32];
+        uint32_t pk[HK / 2];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
+        for (int c = 0; c < HK / 2; ++c) {
           const float e0 = ptx::ex2(fmaf(__uint_as_float(s[2 * c]), a.cl, -mref));
           const float e1 = ptx::ex2(fmaf(__uint_as_float(s[2 * c + 1]), a.cl, -mref));
           ls += e0 + e1;
@@ -271,17 +287,20 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
         if (resc) {
           ptx::tc_fence_after();
           uint32_t o[32];
-          ptx::tmem_ld32(tmem + lrow + 256 + hf * 32, o);
+          ptx::tmem_ld32(tmem + lrow + OCOL + hf * 32, o);
           ptx::tmem_ld_wait();
 #pragma unroll
           for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
-          ptx::tmem_st32(tmem + lrow + 256 + hf * 32, o);
+          ptx::tmem_st32(tmem + lrow + OCOL + hf * 32, o);
           ptx::tmem_st_wait();
         }
-        uint8_t* pb = sP + b * P_BYTES + hf * (P_BYTES / 2) + r * 128;  // k-block hf of P_j
+        // this half's keys: k-block (hf*HK)/64 of P_j, 16-byte chunks from ((hf*HK)%64)/8
+        uint8_t* pb = sP + b * P_BYTES + ((hf * HK) / 64) * 16384 + r * 128;
+        constexpr int CH0 = 0;
+        const int ch0 = ((hf * HK) % 64) / 8 + CH0;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t addr = ptx::smem_u32(pb + ((c ^ (r & 7)) * 16));
+        for (int c = 0; c < HK / 8; ++c) {
+          const uint32_t addr = ptx::smem_u32(pb + (((ch0 + c) ^ (r & 7)) * 16));
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[4 * c]), "r"(pk[4 * c + 1]),
                        "r"(pk[4 * c + 2]), "r"(pk[4 * c + 3])
                        : "memory");
@@ -297,7 +316,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
       ptx::mbar_wait(&pv_done[(sidx - 1) & 1], ((sidx - 1) >> 1) & 1);
       ptx::tc_fence_after();
       uint32_t o[32];
-      ptx::tmem_ld32(tmem + lrow + 256 + hf * 32, o);
+      ptx::tmem_ld32(tmem + lrow + OCOL + hf * 32, o);
       ptx::tmem_ld_wait();
       ptx::tc_fence_before();
       asm volatile("bar.sync %0, 64;" ::"r"(nbar) : "memory");
@@ -326,7 +345,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1) attn_fused_kernel(const __grid_
   __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<512>(tmem);
+    ptx::tmem_dealloc<FA_TMEM>(tmem);
   }
 }
 
@@ -365,22 +384,43 @@ bool map3(CUtensorMap* m, const void* p, long long inner, long long rows, long l
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+template <int BNK>
+cudaError_t attn_fused_launch(const AttnFusedProblem& p, cudaStream_t s, FaArgs& a, long long tiles) {
+  using CF = FaCfg<BNK>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fused_kernel<BNK>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (!map3(&a.tk, p.k, FA_DH, p.Nk, p.H, p.k_srow, p.k_sh, BNK)) return cudaErrorInvalidValue;
+  const int grid = static_cast<int>(tiles < CF::MINB * num_sms() ? tiles : CF::MINB * num_sms());
+  if (p.pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(FA_THREADS);
+    cfg.dynamicSmemBytes = CF::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, attn_fused_kernel<BNK>, a);
+  }
+  attn_fused_kernel<BNK><<<grid, FA_THREADS, CF::SMEM, s>>>(a);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t attn_fused(const AttnFusedProblem& p, cudaStream_t s) {
   if (p.M <= 0 || p.Nk <= 0 || p.H <= 0) return cudaSuccess;
   if (p.dh != FA_DH) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
   FaArgs a;
   memset(&a, 0, sizeof(a));
   // q [M, H, dh] / k [Nk, H, dh]: inner dh; vt [H, dh, Nk]: inner keys, rows dh
   if (!map3(&a.tq, p.q, FA_DH, p.M, p.H, p.q_srow, p.q_sh, FA_BM) ||
-      !map3(&a.tk, p.k, FA_DH, p.Nk, p.H, p.k_srow, p.k_sh, FA_BN) ||
       !map3(&a.tv, p.vt, p.Nk, FA_DH, p.H, p.v_sdh, p.v_sh, FA_DH))
     return cudaErrorInvalidValue;
   if ((reinterpret_cast<uintptr_t>(p.out) & 15) || p.o_srow % 8 || p.o_sh % 8) return cudaErrorInvalidValue;
@@ -394,24 +434,12 @@ cudaError_t attn_fused(const AttnFusedProblem& p, cudaStream_t s) {
   a.causal = p.causal;
   a.row_off = p.row_off;
   a.cl = p.scale * 1.4426950408889634f;
-  const long long tiles = static_cast<long long>(a.H) * a.MT;
-  const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
   a.pdl = p.pdl;
-  if (p.pdl) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(FA_THREADS);
-    cfg.dynamicSmemBytes = FA_SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute la[1];
-    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    la[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = la;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, attn_fused_kernel, a);
-  }
-  attn_fused_kernel<<<grid, FA_THREADS, FA_SMEM, s>>>(a);
-  return cudaGetLastError();
+  const long long tiles = static_cast<long long>(a.H) * a.MT;
+  // two CTAs per SM (64-key blocks) only when the launch can fill them
+  static const int force = getenv("AC_FA_BN") ? atoi(getenv("AC_FA_BN")) : 0;  // experiments
+  const bool dual = force ? force == 64 : tiles >= 2 * num_sms();
+  return dual ? attn_fused_launch<64>(p, s, a, tiles) : attn_fused_launch<128>(p, s, a, tiles);
 }
 
 }  // namespace ac
