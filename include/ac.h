@@ -202,7 +202,15 @@ void ac_exec_free(ac_exec* e);
  * output (fully overwritten).  Asynchronous and stream-ordered; buffers must
  * stay valid until the stream completes.  With a communicator, each rank runs
  * its contiguous share of every region's chunks and the region outputs are
- * all-gathered.  Errors: AC_ERR_BIND, AC_ERR_CUDA, AC_ERR_NCCL. */
+ * all-gathered (NCCL broadcasts from each slab's owner).
+ * Inside a region's chunk loop the kernels are programmatic dependent launches
+ * (each waits in-kernel for its predecessor; AC_PDL=0 disables), and the chunks
+ * of a fused attention chain overlap through per-head epochs kept in a control
+ * block at the end of the workspace (AC_OVERLAP=0 disables).  Results do not
+ * depend on either, nor on the chunking: chunked == unchunked bitwise.
+ * Errors: AC_ERR_BIND, AC_ERR_CUDA, AC_ERR_NCCL; AC_ERR_UNSUPPORTED when a kernel
+ * cannot take an operand layout (bf16 rows for the tensor-core paths must be
+ * multiples of 8 elements, the fused attention kernel needs head dim 64). */
 ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_tensor* outputs, int32_t n_out,
                  void* stream);
 
