@@ -473,7 +473,19 @@ def main():
                 "share_of_step": round(ms / total_k, 4), "peak_source": peak_src,
                 "timing": "per-launch CUDA events on the launch stream in a profiled pass right after the timed "
                           "steps (the events serialise the overlapped chunk loop, so they stay out of value)"}
-        shares = {k: {"kind": v[0], "ms_per_step": round(v[1] / kp, 4), "launches_per_step": v[2] / kp}
+        def stage_roof(node, ms_step):
+            if ms_step <= 0 or doc.node(node)[1] == "softmax":
+                return None  # (bf16 chains: the node is the f2 statistics combine, not a softmax pass)
+            b, w = algorithmic(doc, node)
+            if b == "hbm":
+                return {"bound": "hbm", "achieved_gbs": round(w / (ms_step / 1e3) / 1e9, 1),
+                        "frac": round(w / (ms_step / 1e3) / 1e9 / peaks["hbm_gbs"], 4)}
+            tf = w / (ms_step / 1e3) / 1e12
+            return {"bound": "tensor", "achieved_tflops": round(tf, 1),
+                    "frac": round(tf / peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]), 4)}
+
+        shares = {k: {"kind": v[0], "ms_per_step": round(v[1] / kp, 4), "launches_per_step": v[2] / kp,
+                      "roofline": stage_roof(k, v[1] / kp)}
                   for k, v in sorted(kt.items(), key=lambda kv: -kv[1][1])}
         shares["_profiled_ms_per_step"] = round(prof_ms / kp, 4)
 

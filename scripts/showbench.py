@@ -17,4 +17,6 @@ for fn in sys.argv[1:]:
             if not isinstance(v, dict):
                 print(f"   {k} {v}")
                 continue
-            print(f"   {k:14s} {v['ms_per_step']:8.4f}  unchunked {us.get(k, float('nan')):8.4f}  x{v['launches_per_step']:.0f}")
+            rf = (v.get("roofline") or {}).get("frac")
+            print(f"   {k:14s} {v['ms_per_step']:8.4f}  unchunked {us.get(k, float('nan')):8.4f}  x{v['launches_per_step']:.0f}"
+                  f"  roof {rf}")
