@@ -369,3 +369,57 @@ def test_f2_large_logit_range(causal):
         got, _ = gu.run(cg, api.plan_parse(cg, "autochunk-plan 1\nregion s=scores e=pv n=%d dims=0\n" % n), og, dev)
         torch.cuda.synchronize()
         assert torch.equal(got["x1"], base["x1"]), n
+
+
+@pytest.mark.parametrize("name,rows_per_chunk", [("unet", 2048), ("vit", 8192)])
+def test_full_size_sampled_rows(name, rows_per_chunk):
+    """BASELINE configs at full size (UNet 16384 tokens h=10, ViT-L 65536 tokens) under
+    the plan ac_plan picks at 20 % - the launch configuration bench.py times - sampled
+    rows (first, last, every chunk boundary +-1, random) vs the fp64 oracle."""
+    gu = _gu()
+    from paper_2401_10652_b200 import api
+    og = workloads.config(name)
+    cg = gu.c_graph(og)
+    budget = int(0.2 * memory.profile(og).peak_bytes)
+    plan = api.ac_plan(cg, budget)
+    assert plan.feasible
+    vals, dev = gu.make_values(og, 0)
+    got, ex = gu.run(cg, plan, og, dev)
+    torch.cuda.synchronize()
+    N = og.tensors["x"].shape[0]
+    rows = blocks.sample_rows(N, rows_per_chunk, 16)
+    ref = blocks.transformer_rows(og, vals, rows)
+    out = og.outputs[0]
+    assert gu.rel_err(got[out][torch.from_numpy(rows).cuda()], ref[out]) < 2e-2
+    assert ex.stats().planned_peak < budget
+
+
+@pytest.mark.parametrize("ending", [0, 1])
+def test_af_full_size_sampled_pairs(ending):
+    """One AlphaFold triangle attention (starting node, Alg. 13, or ending node,
+    Alg. 14) at N_res = 1024, c_z = 128, H = 4, c = 32 under ac_plan at 20 % (the
+    short query-dim chunks of the bench's AF config: paired 64-row kernels), sampled
+    (i, j) pairs incl. chunk boundaries vs the fp64 oracle."""
+    gu = _gu()
+    from oracle.graph import Builder
+    from paper_2401_10652_b200 import api
+    N, cz, H, c = 1024, 128, 4, 32
+    B = Builder("af_one", "bf16")
+    B.input("z", (N, N, cz))
+    workloads._tri_weights(B, "t_", cz, H, c)
+    workloads._tri_attention(B, "z", "t_", N, cz, H, c, ending, "zo")
+    B.output("zo")
+    og = B.build()
+    cg = gu.c_graph(og)
+    budget = int(0.2 * memory.profile(og).peak_bytes)
+    plan = api.ac_plan(cg, budget)
+    assert plan.feasible and plan.num_regions >= 1
+    vals, dev = gu.make_values(og, 0)
+    got, _ = gu.run(cg, plan, og, dev)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(1)
+    pairs = [(0, 0), (N - 1, N - 1), (63, 64), (64, 63), (511, 512)] + \
+        [tuple(int(x) for x in rng.integers(0, N, 2)) for _ in range(11)]
+    ref = blocks.tri_attention_pairs(og, vals, "t_", pairs, bool(ending))
+    g_pairs = torch.stack([got["zo"][i, j] for i, j in pairs])
+    assert gu.rel_err(g_pairs, ref) < 2e-2

@@ -244,3 +244,23 @@ def test_fused_attention_chunked_is_exact(causal):
             plan = select.user_plan(g, spec)
             got = executor.run_chunked(g, v, plan.regions)
             np.testing.assert_array_equal(got[g.outputs[0]], base[g.outputs[0]])
+
+
+@pytest.mark.parametrize("ending", [0, 1])
+def test_tri_attention_pair_sampler_equals_full_run(ending):
+    """The sampled-pair oracle for one triangle attention equals the full executor
+    run at those pairs (fp64), so it can check full-size GPU runs."""
+    from oracle import blocks
+    from oracle.graph import Builder
+    N, cz, H, c = 12, 8, 2, 4
+    B = Builder("tri1", "f64")
+    B.input("z", (N, N, cz))
+    workloads._tri_weights(B, "t_", cz, H, c)
+    workloads._tri_attention(B, "z", "t_", N, cz, H, c, ending, "zo")
+    B.output("zo")
+    g = B.build()
+    v = _values(g, 2)
+    full = executor.run(g, v)["zo"]
+    pairs = [(0, 0), (3, 7), (11, 2), (5, 11)]
+    got = blocks.tri_attention_pairs(g, v, "t_", pairs, bool(ending))
+    np.testing.assert_allclose(got, np.stack([full[i, j] for i, j in pairs]), rtol=0, atol=1e-12)
