@@ -393,9 +393,15 @@ def main():
         comm = api.Comm(uid[0], rank, world, local)
     samples, dev = device_inputs(doc, torch)
     s = torch.cuda.current_stream()
+    # device allocator evidence: everything torch holds for one run minus the weights
+    # (parameter memory, excluded from activation by Eq. 1) - inputs, outputs, workspace
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats()
+    weights_bytes = sum(dev[w[0]].numel() * dev[w[0]].element_size() for w in doc.weights)
     ws = torch.empty(max(plan.workspace_bytes(), 16), dtype=torch.uint8, device="cuda")
     TD = {"bf16": torch.bfloat16, "f32": torch.float32}
     outs = {o: torch.empty(doc.tensors[o][1], dtype=TD[doc.tensors[o][0]], device="cuda") for o in doc.outputs}
+    activation_alloc = torch.cuda.memory_allocated() - weights_bytes  # inputs + outputs + workspace
     ins = {t: dev[t] for t in doc.order}
     ex = api.Exec(plan, ws, comm)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
@@ -650,7 +656,11 @@ def main():
         "peak_activation_bytes": {"planned": profp.peak_bytes, "unchunked": prof0.peak_bytes,
                                   "reduction": round(1 - profp.peak_bytes / prof0.peak_bytes, 4),
                                   "budget": budget, "arena_bytes": st.workspace_high_water,
-                                  "arena_plus_caller": st.workspace_high_water + caller},
+                                  "arena_plus_caller": st.workspace_high_water + caller,
+                                  "torch_allocated_activation": activation_alloc,
+                                  "note": "torch_allocated_activation = device bytes torch holds for inputs, "
+                                          "outputs and the ac_run workspace (weights excluded, Eq. 1); it must "
+                                          "not exceed planned (the f2 chains keep P as statistics only)"},
         "unchunked": unchunked, "roofline": roof, "stages": shares, "cpu_baseline": cpu, "e2e": e2e,
         **({"chunk_sweep": sweep} if sweep else {}),
         **({"ablation": ablation} if ablation else {}),
