@@ -73,6 +73,7 @@ struct ac_exec {
   // fused softmax chains (f2): per node 0 none, 1 scores (writes stats), 2 softmax
   // (not launched), 3 PV (normalises S in smem); fuse_s / fuse_p: the chain's S and P tensors
   std::vector<char> fuse_role;
+  std::vector<char> fuse_online;  // non-split chain: the PV folds (M, 1/L) itself, no combine launch
   std::vector<int> fuse_s, fuse_p;
   std::vector<char> fuse_split;        // per node of a fused chain: PV fixed split-K on
   std::vector<int> fuse_head;          // per node of a fused chain: its scores node
@@ -99,6 +100,13 @@ bool pv_splitk(bool causal, int64_t nk) {
   const char* v = getenv("AC_PV_SPLITK");
   if (v && (v[0] == '0' || v[0] == '1')) return v[0] == '1';
   return !causal && nk >= 4096;  // short rows: one unit per tile is cheaper
+}
+
+// AC_PV_ONLINE=0: keep the separate statistics-combine launch for non-split chains too (the PV then folds
+// each row's (M, 1/L) online from the slab statistics; split-K chains always combine)
+bool pv_online_enabled() {
+  const char* v = getenv("AC_PV_ONLINE");
+  return !(v && v[0] == '0');
 }
 
 // Chunk-loop overlap of fused chains (programmatic dependent launch + per-batch
@@ -416,6 +424,7 @@ ac_status launch_node(const ac_exec* e, int i, const std::vector<View>& V, const
 ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, const NodeCtx& cx, cudaStream_t s) {
   const Graph& g = *e->g;
   const Node& n = g.nodes[i];
+  if (e->fuse_role[i] == 2 && e->fuse_online[i]) return AC_OK;  // folded into the PV (no launch)
   const int dtc = e->dt == DT::BF16 ? 1 : 0;
   auto in = [&](int k) -> const View& { return V[n.inputs[k]]; };
   const View& out = V[n.output];
@@ -600,6 +609,8 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         ep.stats_ss = p.M;
         ep.stats_sb1 = static_cast<int64_t>(p.M) * ns;
         chain_overlap(e, i, cx, p);
+        if (e->fuse_online[i])  // no combine step to reset the PV's unit counter
+          p.zero_word = reinterpret_cast<int*>(V[e->fuse_p[i]].p + f2_layout(p.B1, p.M, p.N, false).cnt);
       }
     } else if (k == "attn_pv") {
       // fused chain: A is the raw scores S, normalised in shared memory with the
@@ -627,6 +638,7 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         p.etile = pp.p;
         p.sched = reinterpret_cast<int*>(in(0).p + L.cnt);
         p.fuse_rowst = reinterpret_cast<const float2*>(in(0).p + L.rowst);
+        p.pv_rowstats = e->fuse_online[i];
         if (L.ncnt > 1) {
           p.sk_gk = static_cast<int>(sk_gk(p.K));
           p.sk_part = reinterpret_cast<float*>(in(0).p + L.part);
@@ -670,6 +682,9 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         ep.stats_ss = p.M;
         ep.stats_sb1 = static_cast<int64_t>(p.M) * ns;
         chain_overlap(e, i, cx, p);
+        if (e->fuse_online[i])
+          p.zero_word = reinterpret_cast<int*>(V[e->fuse_p[i]].p +
+                                               f2_layout(static_cast<int64_t>(p.B1) * p.B2, p.M, p.N, false).cnt);
       }
     } else if (k == "tri_pv") {
       const bool fz = e->fuse_role[i] == 3;
@@ -701,6 +716,7 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         p.etile = pp.p;
         p.sched = reinterpret_cast<int*>(in(0).p + L.cnt);
         p.fuse_rowst = reinterpret_cast<const float2*>(in(0).p + L.rowst);
+        p.pv_rowstats = e->fuse_online[i];
         if (L.ncnt > 1) {
           p.sk_gk = static_cast<int>(sk_gk(p.K));
           p.sk_part = reinterpret_cast<float*>(in(0).p + L.part);
@@ -819,6 +835,7 @@ ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_
   }
   for (int i = 0; i < S; ++i) e->chain_rows_dim[i] = rows_dim(g.nodes[i]);
   e->fuse_role.assign(S, 0);
+  e->fuse_online.assign(S, 0);
   e->fuse_s.assign(S, -1);
   e->fuse_p.assign(S, -1);
   e->fuse_split.assign(S, 0);
@@ -835,6 +852,7 @@ ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_
         e->fuse_s[node] = s_t;
         e->fuse_p[node] = p_t;
         e->fuse_split[node] = split ? 1 : 0;
+        e->fuse_online[node] = !split && pv_online_enabled() ? 1 : 0;
         e->fuse_head[node] = c.scores;
       }
     }

@@ -89,6 +89,8 @@ struct alignas(64) GemmArgs {
   int* tsched;  // MODE 1 / 3 dynamic tile counter
   int pair;     // MODE 2, BN = 32, M <= 64: work units are pairs of batches (two M = 64 MMAs)
   int postscale;  // MODE 2: e tiles straight to the MMA (one TMEM buffer per k-block), f applied after
+  int pv_rowstats;  // MODE 2: fold each row's (M, 1/L) from the slab statistics in-kernel (no combine step)
+  int* zero_word;   // MODE 1 / 3 / 4: zeroed at kernel start (the PV's unit counter when no combine runs)
 };
 
 // epilogue staging: per epilogue warp a [32 rows][PITCH] fp32 slab; PITCH = 68
@@ -402,6 +404,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
   // next kernel of the chunk loop be scheduled as SMs free up
   if (a.pdl_wait) ptx::griddep_wait();
   ptx::griddep_launch();
+  if ((MODE == 1 || MODE == 3 || MODE == 4) && a.zero_word && blockIdx.x == 0 && threadIdx.x == 0) *a.zero_word = 0;
   // unit sequence of this CTA: i-th unit (static round-robin, or the MODE 2 queue)
   // unit queue in use: MODE 2 always, MODE 1 / 3 with dynamic tiles
   const bool uq = MODE == 2 || (MODE != 0 && a.tsched != nullptr);
@@ -685,21 +688,42 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
             const long long bb = static_cast<long long>(b1) * a.B2 + b2;
             const float* fp = reinterpret_cast<const float*>(a.fstats + (mv ? bb * a.fst_sb1 + m : 0));
             const long long fs = 2 * a.fst_ss;
-            const float2 rs = mv ? __ldg(a.frow + bb * a.M + m) : make_float2(0.f, 0.f);
+            // pv_rowstats: the row's softmax normalisation (R19) is folded here, online in
+            // slab order (running max Mr, running sum Lr, O rescaled when Mr rises, 1/L at
+            // the end); otherwise (M, 1/L) come from the combine step
+            const bool online = a.pv_rowstats != 0;
+            const float2 rs = (mv && !online) ? __ldg(a.frow + bb * a.M + m) : make_float2(0.f, 0.f);
+            float Mr = -CUDART_INF_F, Lr = 0.f;
             float accv[BN];
 #pragma unroll
             for (int c = 0; c < BN; ++c) accv[c] = 0.f;
-            float fr[8];
+            const float2 nost = make_float2(-CUDART_INF_F, 0.f);
+            float2 fr[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) fr[j] = (mv && klo + j < khi) ? __ldg(fp + (klo + j) * fs) : -CUDART_INF_F;
+            for (int j = 0; j < 8; ++j)
+              fr[j] = (mv && klo + j < khi) ? __ldg(reinterpret_cast<const float2*>(fp + (klo + j) * fs)) : nost;
             for (int kb0 = klo; kb0 < khi; kb0 += 8) {
-              float nx[8];
+              float2 nx[8];
 #pragma unroll
-              for (int j = 0; j < 8; ++j) nx[j] = (mv && kb0 + 8 + j < khi) ? __ldg(fp + (kb0 + 8 + j) * fs) : -CUDART_INF_F;
+              for (int j = 0; j < 8; ++j)
+                nx[j] = (mv && kb0 + 8 + j < khi) ? __ldg(reinterpret_cast<const float2*>(fp + (kb0 + 8 + j) * fs)) : nost;
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 if (kb0 + j < khi) {
-                  const float f = ptx::ex2(fr[j] - rs.x) * rs.y;  // empty slab: m2 = -inf, f = 0
+                  float f;
+                  if (online) {
+                    if (fr[j].x > Mr) {
+                      const float cr = ptx::ex2(Mr - fr[j].x);  // first slab: 2^-inf = 0, O and L are 0
+                      Lr *= cr;
+#pragma unroll
+                      for (int c = 0; c < BN; ++c) accv[c] *= cr;
+                      Mr = fr[j].x;
+                    }
+                    f = fr[j].x == -CUDART_INF_F ? 0.f : ptx::ex2(fr[j].x - Mr);
+                    Lr = fmaf(fr[j].y, f, Lr);
+                  } else {
+                    f = ptx::ex2(fr[j].x - rs.x) * rs.y;  // empty slab: m2 = -inf, f = 0
+                  }
                   ptx::mbar_wait(&kfull[kbuf], kphase);
                   ptx::tc_fence_after();
 #pragma unroll
@@ -720,6 +744,11 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
               }
 #pragma unroll
               for (int j = 0; j < 8; ++j) fr[j] = nx[j];
+            }
+            if (online) {
+              const float il = Lr > 0.f ? 1.f / Lr : 0.f;
+#pragma unroll
+              for (int c = 0; c < BN; ++c) accv[c] *= il;
             }
             auto publish = [&]() {
               if (!a.done_cnt) return;
@@ -1726,6 +1755,7 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
     }
     a.skng = (kbn + a.skgk - 1) / a.skgk;
     if (a.skng > 1 && !a.skcnt) return cudaErrorInvalidValue;
+    if (p.pv_rowstats && a.skgk < kbn) return cudaErrorInvalidValue;  // the online fold needs whole rows
     if (p.causal_k && a.MT > MAX_MT) return cudaErrorInvalidValue;
   }
   a.pdl_wait = p.pdl_wait;
@@ -1738,12 +1768,15 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   a.fst_sb1 = p.fuse_sb1;
   a.fst_ss = p.fuse_ss;
   a.frow = p.fuse_rowst;
-  if (MODE == 2 && !a.frow) return cudaErrorInvalidValue;
+  if (MODE == 2 && !a.frow && !p.pv_rowstats) return cudaErrorInvalidValue;
   a.ks = (MODE == 0 && BN == 64 && a.vec && p.ksplit > 1) ? (p.ksplit > 8 ? 8 : p.ksplit) : 1;
   if (a.ks > 1) a.tma_store = 0;
   const int sms = num_sms();
   a.pair = (MODE == 2 && BN == 32 && p.etile && p.M <= 64 && a.skng == 1 && !p.causal_k && !getenv("AC_NO_PAIR")) ? 1 : 0;
   a.postscale = C::PS ? 1 : 0;
+  a.pv_rowstats = (MODE == 2 && C::PS && p.pv_rowstats) ? 1 : 0;
+  if (MODE == 2 && p.pv_rowstats && !a.pv_rowstats) return cudaErrorInvalidValue;
+  a.zero_word = (MODE == 1 || MODE == 3 || MODE == 4) ? p.zero_word : nullptr;
   int grid = MODE == 4 ? ((p.B1 * p.B2 + 1) / 2) * a.NT
                        : (a.pair ? (p.B1 * p.B2 + 1) / 2 : a.total_tiles_dense) * a.ks * (MODE == 2 ? a.skng : 1);
   int cap = C::DUAL ? 2 * sms : (sms / a.ks) * a.ks;

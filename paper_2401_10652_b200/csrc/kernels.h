@@ -108,6 +108,10 @@ struct GemmProblem {
   int epoch = 0;
   int dep_epoch = 0;
   int* tsched = nullptr;
+  // f2 without a combine step: the PV folds each row's (M, 1/L) from the slab
+  // statistics itself (pv_rowstats); the scores zero the PV's unit counter (zero_word)
+  int pv_rowstats = 0;
+  int* zero_word = nullptr;
 };
 
 // NEXT f1: fused attention o = softmax(q k^T * scale) v, no N x N tensor (attn_fused.cu).
