@@ -1867,12 +1867,14 @@ cudaError_t gemm_tc(const GemmProblem& p, cudaStream_t s, int bn_hint) {
   if (bn == 0) {
     bn = p.N <= 32 ? 32 : p.N <= 64 ? 64 : p.N <= 128 ? 128 : 256;
     if (!p.ep.stats && !p.fuse_stats) {
-      // short-M GEMMs (a row chunk of a linear): narrower tiles until the grid covers
-      // the SMs (M = 1024, N = 1024: 32 tiles at BN = 256, 128 at BN = 64)
+      // short-M GEMMs (a row chunk of a linear): BN = 128 when BN = 256 leaves most SMs
+      // idle, never narrower (a 128x64 tile halves the MMA width and measured slower in
+      // every row-chunk shape: M = 2048, N = 1024, K = 4096: 25 us at 128, 42 us at 64;
+      // scripts/gemm_bench.py)
       auto tiles = [&](int b) {
         return static_cast<long long>((p.M + 127) / 128) * ((p.N + b - 1) / b) * p.B1 * p.B2;
       };
-      while (bn > 64 && tiles(bn) < num_sms()) bn /= 2;
+      if (bn == 256 && tiles(256) < num_sms() * 3 / 4) bn = 128;
     }
   }
   if (p.fuse_stats) return p.N <= 32 ? launch<32, 2>(p, s) : bn == 64 ? launch<64, 2>(p, s) : cudaErrorInvalidValue;

@@ -27,7 +27,11 @@ def main():
     only = sys.argv[1:]  # name bn act: one configuration, 2 launches (for ncu)
     shapes = [("ffn1", 16384, 4096, 1024, 1, True), ("ffn2", 16384, 1024, 4096, 0, False),
               ("proj", 16384, 1024, 1024, 0, False), ("qkv", 16384, 3072, 1024, 0, False),
-              ("af_proj", 1 << 20, 128, 128, 0, False)]
+              ("af_proj", 1 << 20, 128, 128, 0, False),
+              # row chunks of the fused-attention block's FFN / output projection
+              ("ffn1_c", 1024, 4096, 1024, 1, True), ("ffn2_c", 1024, 1024, 4096, 0, False),
+              ("proj_c", 1024, 1024, 1024, 0, False), ("ffn1_c2", 2048, 4096, 1024, 1, True),
+              ("ffn2_c2", 2048, 1024, 4096, 0, False)]
     for name, M, N, Kd, act, bias in shapes:
         if only and name != only[0]:
             continue
@@ -44,7 +48,7 @@ def main():
             return
         tc = t_ms(lambda: torch.matmul(a, w.t()))
         res = [f"{name:8s} M={M} N={N} K={Kd}: cuBLAS {tc*1e3:7.1f} us {fl/tc/1e9:6.0f} TF/s"]
-        for bn in (128, 256):
+        for bn in ((0, 64, 128, 256) if M <= 4096 else (128, 256)):
             if bn > N:
                 continue
             for aa in sorted({0, act}):
@@ -54,6 +58,15 @@ def main():
                     res.append(f"   ours bn={bn} act={aa}: {t*1e3:7.1f} us {fl/t/1e9:6.0f} TF/s")
                 except Exception as e:
                     res.append(f"   ours bn={bn} act={aa}: {e}")
+        for ks in ((2, 4) if M <= 4096 else ()):
+            for bn in (64,):
+                f = lambda: K.gemm(a, Kd, w, Kd, out, M, N, Kd, out_s=(0, 0, N, 1), act=act, bias=bb if act else None,
+                                   bn=bn, ksplit=ks)
+                try:
+                    t = t_ms(f)
+                    res.append(f"   ours bn={bn} ksplit={ks} act={act}: {t*1e3:7.1f} us {fl/t/1e9:6.0f} TF/s")
+                except Exception as e:
+                    res.append(f"   ours bn={bn} ksplit={ks}: {e}")
         if act:
             ref = torch.nn.functional.gelu(torch.matmul(a.float(), w.float().t()) + bb.float())
             K.gemm(a, Kd, w, Kd, out, M, N, Kd, out_s=(0, 0, N, 1), act=act, bias=bb, bn=256)
