@@ -710,6 +710,14 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 if (kb0 + j < khi) {
+                  // the slab's e V product: all BN columns in flight while f is formed
+                  ptx::mbar_wait(&kfull[kbuf], kphase);
+                  ptx::tc_fence_after();
+                  uint32_t v[BN];
+#pragma unroll
+                  for (int hh = 0; hh < BN / 32; ++hh)
+                    ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + kbuf * BN + hh * 32,
+                                   *reinterpret_cast<uint32_t(*)[32]>(&v[hh * 32]));
                   float f;
                   if (online) {
                     if (fr[j].x > Mr) {
@@ -724,17 +732,12 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
                   } else {
                     f = ptx::ex2(fr[j].x - rs.x) * rs.y;  // empty slab: m2 = -inf, f = 0
                   }
-                  ptx::mbar_wait(&kfull[kbuf], kphase);
-                  ptx::tc_fence_after();
+                  ptx::tmem_ld_wait();
 #pragma unroll
-                  for (int hh = 0; hh < BN / 32; ++hh) {
-                    uint32_t v[32];
-                    ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + kbuf * BN + hh * 32, v);
-                    ptx::tmem_ld_wait();
-                    if (mv) {
+                  for (int c = 0; c < BN; ++c) asm volatile("" : "+r"(v[c]));  // uses stay after the wait
+                  if (mv) {
 #pragma unroll
-                      for (int c = 0; c < 32; ++c) accv[hh * 32 + c] = fmaf(f, __uint_as_float(v[c]), accv[hh * 32 + c]);
-                    }
+                    for (int c = 0; c < BN; ++c) accv[c] = fmaf(f, __uint_as_float(v[c]), accv[c]);
                   }
                   ptx::tc_fence_before();
                   __syncwarp();
