@@ -109,6 +109,27 @@ bool pv_online_enabled() {
   return !(v && v[0] == '0');
 }
 
+// Control block of an overlapped chain (B batches, n chunks), ints:
+//   [0, B)                  PV -> next scores: per-batch epochs
+//   [B, B + n)              scores tile counters per chunk
+//   [B + n, B + 2n)         PV unit counters per chunk
+//   [B + 2n, +nB)           PV per-batch unit counts per chunk
+//   [.., +B)                scores -> PV of the same chunk: per-batch epochs (AC_CONC)
+//   [.., +nB)               scores per-batch warp-slab counts per chunk (AC_CONC)
+int64_t ctrl_ints(int64_t B, int64_t n) { return 2 * B + 2 * n + 2 * n * B; }
+
+// AC_CONC=1: the PV of a chunk runs beside its scores (per-batch completion flags
+// instead of a grid dependency), the scores grid capped at AC_CONC_S CTAs (default
+// 112) so the PV has SMs meanwhile; e-tiles are then read soon after they are written
+bool conc_enabled() {
+  const char* v = getenv("AC_CONC");
+  return v && v[0] == '1';
+}
+int conc_scores_ctas() {
+  const char* v = getenv("AC_CONC_S");
+  return v ? atoi(v) : 112;
+}
+
 // Chunk-loop overlap of fused chains (programmatic dependent launch + per-batch
 // epochs): the next chunk's scores start on SMs the PV's tail frees.
 // AC_OVERLAP=0 disables it (every launch then waits for the previous one).
@@ -322,7 +343,7 @@ Arena build_arena(const Graph& g, const Plan& plan) {
       A.ctrl_off[c.scores] = A.size;
       A.ctrl_b[c.scores] = B;
       A.ctrl_n[c.scores] = n;
-      A.size += ((B + 2 * n + n * B) * 4 + 255) / 256 * 256;
+      A.size += (ctrl_ints(B, n) * 4 + 255) / 256 * 256;
     }
   }
   return A;
@@ -384,6 +405,11 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
 // that PV has published epoch k for it; tiles are taken dynamically.  The PV waits
 // for its combine (PDL + griddepcontrol.wait), takes units from its own per-chunk
 // counter and publishes its epochs.
+bool g_kind_is(const ac_exec* e, int node, const char* k1, const char* k2) {
+  const std::string& k = e->g->nodes[node].kind;
+  return k == k1 || k == k2;
+}
+
 void chain_overlap(const ac_exec* e, int node, const NodeCtx& cx, GemmProblem& p) {
   const int h = e->fuse_head[node];
   const int64_t off = h >= 0 ? e->arena.ctrl_off[h] : -1;
@@ -392,17 +418,32 @@ void chain_overlap(const ac_exec* e, int node, const NodeCtx& cx, GemmProblem& p
   int* c = reinterpret_cast<int*>(e->ws + off);
   const int k = cx.chunk;
   p.done_epoch = c;
+  const bool conc = conc_enabled() && e->fuse_online[node] && g_kind_is(e, node, "attn_scores", "attn_pv");
+  int* sdone = c + B + 2 * n + n * B;
   if (e->fuse_role[node] == 1) {
     p.pdl = k > 0 ? 1 : 0;
     p.pdl_wait = 0;  // ordered by the per-batch epochs instead (the PV of chunk k - 1 is still draining)
     p.dep_epoch = k;
     p.tsched = c + B + k;
+    if (conc) {
+      p.pub_epoch = sdone;
+      p.pub_cnt = sdone + B + static_cast<int64_t>(k) * B;
+      p.epoch = k;
+      p.max_ctas = conc_scores_ctas();
+    }
   } else {
     p.pdl = 1;
-    p.pdl_wait = 1;
+    p.pdl_wait = conc ? 0 : 1;  // concurrent: per-batch flags of this chunk's scores instead
     p.sched = c + B + n + k;
     p.done_cnt = c + B + 2 * n + static_cast<int64_t>(k) * B;
     p.epoch = k;
+    if (conc) {
+      p.wait_epoch = sdone;
+      // AC_CONC_P: PV grid (default: the SMs the scores leave free, so the next chunk's
+      // scores take their SMs back as soon as this chunk's scores end)
+      const char* v = getenv("AC_CONC_P");
+      p.max_ctas = v ? atoi(v) : std::max(1, num_sms() - conc_scores_ctas());
+    }
   }
 }
 
@@ -991,7 +1032,7 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
       const int64_t co = e->arena.ctrl_off[j];
       if (co >= 0) {
         const int64_t B = e->arena.ctrl_b[j], nn = e->arena.ctrl_n[j];
-        if (cudaMemsetAsync(e->ws + co, 0, (B + 2 * nn + nn * B) * 4, s) != cudaSuccess)
+        if (cudaMemsetAsync(e->ws + co, 0, ctrl_ints(B, nn) * 4, s) != cudaSuccess)
           return set_error(AC_ERR_CUDA, "cudaMemsetAsync (chunk-loop control block) failed");
       }
     }

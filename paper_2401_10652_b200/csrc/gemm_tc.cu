@@ -91,6 +91,12 @@ struct alignas(64) GemmArgs {
   int postscale;  // MODE 2: e tiles straight to the MMA (one TMEM buffer per k-block), f applied after
   int pv_rowstats;  // MODE 2: fold each row's (M, 1/L) from the slab statistics in-kernel (no combine step)
   int* zero_word;   // MODE 1 / 3 / 4: zeroed at kernel start (the PV's unit counter when no combine runs)
+  // concurrent scores / PV of one chunk (AC_CONC): the scores count finished warp-slabs
+  // per batch (pub_cnt) and release pub_epoch[b] = epoch + 1 when batch b is complete;
+  // the PV waits for wait_epoch[b] >= epoch + 1 before reading batch b
+  int* pub_cnt;
+  int* pub_epoch;
+  int* wait_epoch;
 };
 
 // epilogue staging: per epilogue warp a [32 rows][PITCH] fp32 slab; PITCH = 68
@@ -465,11 +471,21 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
       int stage = 0;
       uint32_t phase = 0;
       TileWalk walk;
+      int ok_b = -1;  // concurrent scores: last batch known complete
       for (int i = 0, t = produce(0); t < total; t = produce(++i)) {
         int b1, b2, mt, nt = 0, kbn, klo, khi;
         if constexpr (MODE == 2) {
           int g, ng, tile, unit0;
           decode_unit(a, prefix, tpb, t, b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0);
+          const int bb = b1 * a.B2 + b2;
+          if (a.wait_epoch && bb != ok_b) {
+            // the scores of this chunk run beside this kernel: batch bb's e-tiles and
+            // statistics are complete once they publish epoch + 1 for it
+            ptx::wait_geq_gpu(a.wait_epoch + bb, a.epoch + 1);
+            if (a.pair && bb + 1 < a.B1 * a.B2) ptx::wait_geq_gpu(a.wait_epoch + bb + 1, a.epoch + 1);
+            ptx::fence_proxy_async_global();
+            ok_b = bb;
+          }
         } else {
           walk.next(a, prefix, tpb, t, ncl);
           walk.get(a, b1, b2, mt, nt, kbn);
@@ -658,6 +674,11 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
     uint32_t aphase = 0;
     uint32_t bphase = 0;  // MODE 3 bias-box barrier phase
     bool bias_pending = false;  // MODE 3: this warp's next bias box is already in flight
+    int pend_b = -1;  // MODE 1, concurrent PV: batch of this warp's last unpublished slab (lane 0)
+    auto pub = [&](int b) {  // one lane: count a finished warp-slab of batch b (4 quarters x NSLAB per tile)
+      ptx::fence_proxy_async_global();
+      if (ptx::atom_add_acqrel_gpu(a.pub_cnt + b, 1) == 4 * NSLAB * tpb - 1) ptx::st_release_gpu(a.pub_epoch + b, a.epoch + 1);
+    };
     uint32_t pf_phase = 0, pe_phase = 0;  // split-K barrier phases
     if constexpr (MODE == 2) {
       if (a.postscale) {
@@ -688,6 +709,13 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
             const long long bb = static_cast<long long>(b1) * a.B2 + b2;
             const float* fp = reinterpret_cast<const float*>(a.fstats + (mv ? bb * a.fst_sb1 + m : 0));
             const long long fs = 2 * a.fst_ss;
+            const bool conc = a.wait_epoch != nullptr;
+            if (conc && mv) ptx::wait_geq_gpu(a.wait_epoch + bb, a.epoch + 1);  // statistics complete
+            // (concurrent: written during this kernel, so through L2, not the read-only path)
+            auto ldst = [&](long long off) -> float2 {
+              const float2* q = reinterpret_cast<const float2*>(fp + off);
+              return conc ? __ldcg(q) : __ldg(q);
+            };
             // pv_rowstats: the row's softmax normalisation (R19) is folded here, online in
             // slab order (running max Mr, running sum Lr, O rescaled when Mr rises, 1/L at
             // the end); otherwise (M, 1/L) come from the combine step
@@ -701,12 +729,12 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
             float2 fr[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j)
-              fr[j] = (mv && klo + j < khi) ? __ldg(reinterpret_cast<const float2*>(fp + (klo + j) * fs)) : nost;
+              fr[j] = (mv && klo + j < khi) ? ldst((klo + j) * fs) : nost;
             for (int kb0 = klo; kb0 < khi; kb0 += 8) {
               float2 nx[8];
 #pragma unroll
               for (int j = 0; j < 8; ++j)
-                nx[j] = (mv && kb0 + 8 + j < khi) ? __ldg(reinterpret_cast<const float2*>(fp + (kb0 + 8 + j) * fs)) : nost;
+                nx[j] = (mv && kb0 + 8 + j < khi) ? ldst((kb0 + 8 + j) * fs) : nost;
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 if (kb0 + j < khi) {
@@ -714,9 +742,10 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
                   ptx::mbar_wait(&kfull[kbuf], kphase);
                   ptx::tc_fence_after();
                   uint32_t v[BN];
+                  const bool skipld = a.dbg & 8;  // experiment: consumer cost without the TMEM reads
 #pragma unroll
                   for (int hh = 0; hh < BN / 32; ++hh)
-                    ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + kbuf * BN + hh * 32,
+                    if (!skipld) ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + kbuf * BN + hh * 32,
                                    *reinterpret_cast<uint32_t(*)[32]>(&v[hh * 32]));
                   float f;
                   if (online) {
@@ -732,10 +761,10 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
                   } else {
                     f = ptx::ex2(fr[j].x - rs.x) * rs.y;  // empty slab: m2 = -inf, f = 0
                   }
-                  ptx::tmem_ld_wait();
+                  if (!skipld) ptx::tmem_ld_wait();
 #pragma unroll
                   for (int c = 0; c < BN; ++c) asm volatile("" : "+r"(v[c]));  // uses stay after the wait
-                  if (mv) {
+                  if (mv && !skipld) {
 #pragma unroll
                     for (int c = 0; c < BN; ++c) accv[c] = fmaf(f, __uint_as_float(v[c]), accv[c]);
                   }
@@ -1233,6 +1262,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
               __syncwarp();
               if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
             }
+            if (MODE == 1 && a.pub_cnt && lane == 0) pub(b1 * a.B2 + b2);
             continue;
           }
           // ---- f2 scores, one 64-column slab: x = acc * scale * log2(e) (fp32,
@@ -1241,6 +1271,14 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
           // e = bf16(2^(x - m2)), statistics (m2, fp32 sum of e).  Two TMEM passes
           // (max, then exponentials) keep 32 accumulators live at a time.
           constexpr float L2E = 1.4426950408889634f;
+          if (MODE == 1 && a.pub_cnt && pend_b >= 0) {
+            // concurrent PV: this warp's previous slab is published once its store landed
+            if (lane == 0) {
+              ptx::bulk_wait<0>();
+              pub(pend_b);
+            }
+            pend_b = -1;
+          }
           if (lane == 0) {
             if (!BIASED || !bias_pending) ptx::bulk_wait_read<0>();  // previous store has read the staging box
             if (BIASED && !bias_pending) {
@@ -1410,6 +1448,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
           if (mvalid && n0 < a.N)
             a.ep.stats[static_cast<long long>(b1 * a.B2 + b2) * a.ep.stats_sb1 +
                        static_cast<long long>(n0 / 64) * a.ep.stats_ss + m] = make_float2(m2, l0 + l1);
+          if (MODE == 1 && a.pub_cnt) __threadfence();  // statistics visible before the slab is published
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -1422,6 +1461,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
               ptx::tma_store_4d(&a.tout, sb, n0, m0, b1, b2);
             }
             ptx::bulk_commit();
+            if (MODE == 1 && a.pub_cnt) pend_b = b1 * a.B2 + b2;
             if constexpr (BIASED) {
               // prefetch the bias box of this warp's slab in the CTA's next tile (same
               // slab index c) as soon as the store has read the staging box, so its L2
@@ -1602,6 +1642,10 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
       if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
     }
+    if (MODE == 1 && a.pub_cnt && pend_b >= 0 && lane == 0) {
+      ptx::bulk_wait<0>();
+      pub(pend_b);
+    }
     if (lane == 0) ptx::bulk_wait_read<0>();  // staging buffers must outlive the TMA stores' reads
     __syncwarp();
   }
@@ -1780,6 +1824,11 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   a.pv_rowstats = (MODE == 2 && C::PS && p.pv_rowstats) ? 1 : 0;
   if (MODE == 2 && p.pv_rowstats && !a.pv_rowstats) return cudaErrorInvalidValue;
   a.zero_word = (MODE == 1 || MODE == 3 || MODE == 4) ? p.zero_word : nullptr;
+  a.pub_cnt = MODE == 1 ? p.pub_cnt : nullptr;
+  a.pub_epoch = MODE == 1 ? p.pub_epoch : nullptr;
+  if (MODE == 1 && a.pub_cnt && !a.tsched) return cudaErrorInvalidValue;  // batch-major dynamic tiles only
+  a.wait_epoch = MODE == 2 ? p.wait_epoch : nullptr;
+  if (MODE == 2 && a.wait_epoch && !a.pv_rowstats) return cudaErrorInvalidValue;
   int grid = MODE == 4 ? ((p.B1 * p.B2 + 1) / 2) * a.NT
                        : (a.pair ? (p.B1 * p.B2 + 1) / 2 : a.total_tiles_dense) * a.ks * (MODE == 2 ? a.skng : 1);
   int cap = C::DUAL ? 2 * sms : (sms / a.ks) * a.ks;
@@ -1807,6 +1856,7 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
     }
   }
   if (grid > cap) grid = cap;
+  if (p.max_ctas > 0 && grid > p.max_ctas) grid = p.max_ctas;  // concurrent scores leave SMs to the PV
   if (grid < a.ks) grid = a.ks;
   if (a.ks == 1 && p.pdl) {
     cudaLaunchConfig_t cfg = {};

@@ -112,6 +112,14 @@ struct GemmProblem {
   // statistics itself (pv_rowstats); the scores zero the PV's unit counter (zero_word)
   int pv_rowstats = 0;
   int* zero_word = nullptr;
+  // concurrent scores / PV of one chunk (AC_CONC=1): the scores publish per-batch
+  // completion (pub_cnt, pub_epoch = epoch + 1), the PV waits on it (wait_epoch)
+  // instead of on the whole scores grid; max_ctas caps the scores grid so the PV
+  // has SMs to run on meanwhile
+  int* pub_cnt = nullptr;
+  int* pub_epoch = nullptr;
+  int* wait_epoch = nullptr;
+  int max_ctas = 0;
 };
 
 // NEXT f1: fused attention o = softmax(q k^T * scale) v, no N x N tensor (attn_fused.cu).

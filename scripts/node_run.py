@@ -1,5 +1,5 @@
 """Exactly one ac_run of a bench config (for ncu captures: every kernel of one
-step, nothing else of ours).  Usage: python scripts/node_run.py CONFIG"""
+step, nothing else of ours).  Usage: python scripts/node_run.py CONFIG [unchunked | n=N]"""
 import json
 import os
 import sys
@@ -17,6 +17,8 @@ prof0, _ = api.estimate_memory(cg)
 budget = int(bench.DEFAULT_BUDGET.get(cfg, 0.2) * prof0.peak_bytes)
 if len(sys.argv) > 2 and sys.argv[2] == "unchunked":
     plan = api.plan_parse(cg, "autochunk-plan 1\n")
+elif len(sys.argv) > 2 and sys.argv[2].startswith("n="):  # forced region chunk count
+    plan = api.plan_parse(cg, f"autochunk-plan 1\nregion s=scores e=pv {sys.argv[2]} dims=0\n")
 elif cfg == "tiny":
     plan = api.plan_parse(cg, "autochunk-plan 1\nregion s=scores e=pv n=8 dims=0\n")
 else:

@@ -290,6 +290,21 @@ def test_af_chunk_overlap_opt_in(monkeypatch):
                           "region s=col_scores e=col_pv n=6 dims=0\n"], seed=9)
 
 
+@pytest.mark.parametrize("causal", [True, False])
+def test_concurrent_scores_pv(monkeypatch, causal):
+    """AC_CONC=1: the PV of each chunk runs beside its scores, reading a head once the
+    scores published it complete (per-batch flags instead of a grid dependency), the
+    scores grid capped so the PV has SMs.  Same arithmetic: vs the oracle and bitwise
+    equal to unchunked; also with a scores grid of one CTA (the PV waits the longest)."""
+    monkeypatch.setenv("AC_CONC", "1")
+    og = workloads.block("attn_only", 2048 + 320, 256, 4, 0, causal, "bf16", name="conc")
+    plans = ["autochunk-plan 1\nregion s=scores e=pv n=4 dims=0\n",
+             "autochunk-plan 1\nregion s=scores e=pv n=3 dims=0\n"]
+    _check_all_plans(og, plans, seed=13)
+    monkeypatch.setenv("AC_CONC_S", "1")
+    _check_all_plans(og, plans[:1], seed=13)
+
+
 @pytest.mark.parametrize("kind", ["transformer", "transformer_fa"])
 def test_degenerate_sizes(kind):
     """Degenerate cases: the smallest aligned bf16 sequence (8 tokens)
