@@ -433,7 +433,7 @@ void chain_overlap(const ac_exec* e, int node, const NodeCtx& cx, GemmProblem& p
     }
   } else {
     p.pdl = 1;
-    p.pdl_wait = conc ? 0 : 1;  // concurrent: per-batch flags of this chunk's scores instead
+    p.pdl_wait = conc && !getenv("AC_CONC_GRIDWAIT") ? 0 : 1;  // concurrent: per-batch flags of this chunk's scores instead
     p.sched = c + B + n + k;
     p.done_cnt = c + B + 2 * n + static_cast<int64_t>(k) * B;
     p.epoch = k;

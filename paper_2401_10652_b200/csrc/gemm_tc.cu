@@ -674,10 +674,39 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
     uint32_t aphase = 0;
     uint32_t bphase = 0;  // MODE 3 bias-box barrier phase
     bool bias_pending = false;  // MODE 3: this warp's next bias box is already in flight
-    int pend_b = -1;  // MODE 1, concurrent PV: batch of this warp's last unpublished slab (lane 0)
-    auto pub = [&](int b) {  // one lane: count a finished warp-slab of batch b (4 quarters x NSLAB per tile)
+    // MODE 1, concurrent PV (lane 0): this warp's finished slabs of the current batch are
+    // counted locally (tiles are batch-major); when the warp moves to another batch the
+    // count is deferred and added to the batch's total once a later store has been
+    // issued and the deferred ones have landed (bulk wait_group 1, normally already
+    // true), or at exit; the add that completes a batch (4 quarters x NSLAB slabs per
+    // tile) releases its epoch
+    int cur_b = -1, cur_n = 0, def_b = -1, def_n = 0, def_after = 0;
+    auto pub_add = [&](int b, int n) {
       ptx::fence_proxy_async_global();
-      if (ptx::atom_add_acqrel_gpu(a.pub_cnt + b, 1) == 4 * NSLAB * tpb - 1) ptx::st_release_gpu(a.pub_epoch + b, a.epoch + 1);
+      if (ptx::atom_add_acqrel_gpu(a.pub_cnt + b, n) + n == 4 * NSLAB * tpb) ptx::st_release_gpu(a.pub_epoch + b, a.epoch + 1);
+    };
+    auto pub_slab = [&](int b) {  // lane 0, before the slab's own work
+      if (def_b >= 0 && def_after > 0) {
+        ptx::bulk_wait<1>();
+        pub_add(def_b, def_n);
+        def_b = -1;
+      }
+      if (b != cur_b) {
+        if (def_b >= 0) {
+          ptx::bulk_wait<0>();
+          pub_add(def_b, def_n);
+        }
+        def_b = cur_b;
+        def_n = cur_n;
+        def_after = 0;
+        cur_b = b;
+        cur_n = 0;
+      }
+    };
+    auto pub_flush = [&]() {
+      ptx::bulk_wait<0>();
+      if (def_b >= 0) pub_add(def_b, def_n);
+      if (cur_b >= 0) pub_add(cur_b, cur_n);
     };
     uint32_t pf_phase = 0, pe_phase = 0;  // split-K barrier phases
     if constexpr (MODE == 2) {
@@ -1262,7 +1291,10 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
               __syncwarp();
               if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
             }
-            if (MODE == 1 && a.pub_cnt && lane == 0) pub(b1 * a.B2 + b2);
+            if (MODE == 1 && a.pub_cnt && lane == 0) {
+              pub_slab(b1 * a.B2 + b2);
+              ++cur_n;
+            }
             continue;
           }
           // ---- f2 scores, one 64-column slab: x = acc * scale * log2(e) (fp32,
@@ -1271,14 +1303,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
           // e = bf16(2^(x - m2)), statistics (m2, fp32 sum of e).  Two TMEM passes
           // (max, then exponentials) keep 32 accumulators live at a time.
           constexpr float L2E = 1.4426950408889634f;
-          if (MODE == 1 && a.pub_cnt && pend_b >= 0) {
-            // concurrent PV: this warp's previous slab is published once its store landed
-            if (lane == 0) {
-              ptx::bulk_wait<0>();
-              pub(pend_b);
-            }
-            pend_b = -1;
-          }
+          if (MODE == 1 && a.pub_cnt && lane == 0) pub_slab(b1 * a.B2 + b2);
           if (lane == 0) {
             if (!BIASED || !bias_pending) ptx::bulk_wait_read<0>();  // previous store has read the staging box
             if (BIASED && !bias_pending) {
@@ -1448,7 +1473,6 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
           if (mvalid && n0 < a.N)
             a.ep.stats[static_cast<long long>(b1 * a.B2 + b2) * a.ep.stats_sb1 +
                        static_cast<long long>(n0 / 64) * a.ep.stats_ss + m] = make_float2(m2, l0 + l1);
-          if (MODE == 1 && a.pub_cnt) __threadfence();  // statistics visible before the slab is published
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -1461,7 +1485,10 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
               ptx::tma_store_4d(&a.tout, sb, n0, m0, b1, b2);
             }
             ptx::bulk_commit();
-            if (MODE == 1 && a.pub_cnt) pend_b = b1 * a.B2 + b2;
+            if (MODE == 1 && a.pub_cnt) {  // (lane 0)
+              ++cur_n;
+              ++def_after;
+            }
             if constexpr (BIASED) {
               // prefetch the bias box of this warp's slab in the CTA's next tile (same
               // slab index c) as soon as the store has read the staging box, so its L2
@@ -1642,10 +1669,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
       if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
     }
-    if (MODE == 1 && a.pub_cnt && pend_b >= 0 && lane == 0) {
-      ptx::bulk_wait<0>();
-      pub(pend_b);
-    }
+    if (MODE == 1 && a.pub_cnt && lane == 0) pub_flush();
     if (lane == 0) ptx::bulk_wait_read<0>();  // staging buffers must outlive the TMA stores' reads
     __syncwarp();
   }
