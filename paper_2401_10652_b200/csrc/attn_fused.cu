@@ -64,7 +64,24 @@ struct alignas(64) FaArgs {
   int pdl;
 };
 
-template <int BNK>
+// 2^x on the FMA / ALU pipes (x <= 0, the softmax exponent): x = j + f with j the
+// nearest integer, f in [-0.5, 0.5]; 2^f by a degree-3 polynomial (relative error
+// 2.1e-4, below half a bf16 ulp of P); 2^j added to the exponent field.  x < -126
+// (masked keys: -inf) gives 0.  Opt-in (AC_FA_POLY=1) for a fixed quarter of the
+// columns, so that the MUFU unit carries three quarters of the exponentials.
+__device__ __forceinline__ float ex2_poly(float x) {
+  const float xc = fmaxf(x, -126.f);
+  const float t = xc + 12582912.f;  // 1.5 * 2^23: round to nearest integer in the low bits
+  const int j = __float_as_int(t) - 0x4B400000;
+  const float f = xc - (t - 12582912.f);
+  float p = fmaf(f, 0.05484806f, 0.24180646f);
+  p = fmaf(f, p, 0.69324815f);
+  p = fmaf(f, p, 0.99998868f);
+  const float r = __int_as_float(__float_as_int(p) + (j << 23));
+  return x < -126.f ? 0.f : r;
+}
+
+template <int BNK, bool POLY>
 __global__ void __launch_bounds__(FA_THREADS, FaCfg<BNK>::MINB) attn_fused_kernel(const __grid_constant__ FaArgs a) {
   using CF = FaCfg<BNK>;
   constexpr int FA_BN = CF::BN, HK = CF::HK, OCOL = CF::OCOL, FA_TMEM = CF::TMEM;
@@ -266,8 +283,13 @@ __global__ void __launch_bounds__(FA_THREADS, FaCfg<BNK>::MINB) attn_fused_kerne
         uint32_t pk[HK / 2];
 #pragma unroll
         for (int c = 0; c < HK / 2; ++c) {
-          const float e0 = ptx::ex2(fmaf(__uint_as_float(s[2 * c]), a.cl, -mref));
-          const float e1 = ptx::ex2(fmaf(__uint_as_float(s[2 * c + 1]), a.cl, -mref));
+          const float x0 = fmaf(__uint_as_float(s[2 * c]), a.cl, -mref);
+          const float x1 = fmaf(__uint_as_float(s[2 * c + 1]), a.cl, -mref);
+          // (columns 8q+6, 8q+7 of every 8 on the FMA pipe: the choice depends on the
+          // column only, so chunked == unchunked stays bitwise)
+          const bool pc = POLY && (c & 3) == 3;
+          const float e0 = pc ? ex2_poly(x0) : ptx::ex2(x0);
+          const float e1 = pc ? ex2_poly(x1) : ptx::ex2(x1);
           ls += e0 + e1;
           __nv_bfloat162 h = __floats2bfloat162_rn(e0, e1);
           pk[c] = *reinterpret_cast<uint32_t*>(&h);
@@ -384,12 +406,12 @@ bool map3(CUtensorMap* m, const void* p, long long inner, long long rows, long l
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BNK>
+template <int BNK, bool POLY>
 cudaError_t attn_fused_launch(const AttnFusedProblem& p, cudaStream_t s, FaArgs& a, long long tiles) {
   using CF = FaCfg<BNK>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fused_kernel<BNK>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(attn_fused_kernel<BNK, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -406,9 +428,9 @@ cudaError_t attn_fused_launch(const AttnFusedProblem& p, cudaStream_t s, FaArgs&
     la[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = la;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, attn_fused_kernel<BNK>, a);
+    return cudaLaunchKernelEx(&cfg, attn_fused_kernel<BNK, POLY>, a);
   }
-  attn_fused_kernel<BNK><<<grid, FA_THREADS, CF::SMEM, s>>>(a);
+  attn_fused_kernel<BNK, POLY><<<grid, FA_THREADS, CF::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -439,7 +461,11 @@ cudaError_t attn_fused(const AttnFusedProblem& p, cudaStream_t s) {
   // two CTAs per SM (64-key blocks) only when the launch can fill them
   static const int force = getenv("AC_FA_BN") ? atoi(getenv("AC_FA_BN")) : 0;  // experiments
   const bool dual = force ? force == 64 : tiles >= 2 * num_sms();
-  return dual ? attn_fused_launch<64>(p, s, a, tiles) : attn_fused_launch<128>(p, s, a, tiles);
+  // AC_FA_POLY=1: a quarter of the exponentials on the FMA pipe (measured slower: the
+  // kernel is not MUFU-bound — unchunked GPT attention 0.98 -> 1.11 ms, chunked equal)
+  static const bool poly = getenv("AC_FA_POLY") && getenv("AC_FA_POLY")[0] == '1';
+  if (poly) return dual ? attn_fused_launch<64, true>(p, s, a, tiles) : attn_fused_launch<128, true>(p, s, a, tiles);
+  return dual ? attn_fused_launch<64, false>(p, s, a, tiles) : attn_fused_launch<128, false>(p, s, a, tiles);
 }
 
 }  // namespace ac
