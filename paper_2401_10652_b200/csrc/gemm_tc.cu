@@ -76,7 +76,8 @@ struct alignas(64) GemmArgs {
   int skgk, skng;
   float* skpart;
   int* skcnt;
-  int dbg;  // experiments (AC_DBG): bit0 = MODE 2 transform skipped
+  int dbg;  // experiments (AC_DBG): bit0 = MODE 2 transform skipped, 8 = post-scale TMEM reads skipped,
+            // 16 / 32 = no L2 evict-first hint on the e-tile loads / stores
   int* sched;  // MODE 2: zero-initialised work counter for dynamic unit scheduling (null = round-robin)
   unsigned long long* trace;  // debug (AC_TRACE): per unit {cta, t_load0, t_tfull, t_done}
   char* etile;  // f2 pre-swizzled e tiles (GemmProblem::etile), null = tensor path
@@ -472,6 +473,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
       uint32_t phase = 0;
       TileWalk walk;
       int ok_b = -1;  // concurrent scores: last batch known complete
+      const uint64_t epol = ptx::policy_evict_first();
       for (int i = 0, t = produce(0); t < total; t = produce(++i)) {
         int b1, b2, mt, nt = 0, kbn, klo, khi;
         if constexpr (MODE == 2) {
@@ -518,8 +520,13 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
         for (int kb = klo; kb < khi; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::mbar_expect_tx(&full[stage], (two ? 2 : 1) * (ebytes + C::B_TILE));
-          if (MODE == 2 && esrc)
-            ptx::bulk_load(sA + stage * C::A_BYTES, esrc + static_cast<long long>(kb) * 16384, ebytes, &full[stage]);
+          if (MODE == 2 && esrc) {
+            if (!(a.dbg & 16))  // e-tiles are read once: L2 evict-first (AC_DBG bit 16 turns it off)
+              ptx::bulk_load_hint(sA + stage * C::A_BYTES, esrc + static_cast<long long>(kb) * 16384, ebytes,
+                                  &full[stage], epol);
+            else
+              ptx::bulk_load(sA + stage * C::A_BYTES, esrc + static_cast<long long>(kb) * 16384, ebytes, &full[stage]);
+          }
           else
             ptx::tma_load_4d(sA + stage * C::A_BYTES, &a.ta, &full[stage], kb * BK, mt * BM, ac2, ac3);
           ptx::tma_load_4d(sB + stage * C::B_BYTES, &a.tb, &full[stage], kb * BK, nt * BN, bc2, bc3);
@@ -1480,7 +1487,12 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
               // (slabs past N would land in the next tile row: not stored)
               char* dst = a.etile + ((static_cast<long long>(b1 * a.B2 + b2) * a.MT + mt) * a.e_nkb + n0 / 64) * 16384 +
                           quarter * 4096;
-              if (n0 < a.N && m0 < a.M) ptx::bulk_store(dst, sb, 4096);  // quarters past M: never read
+              if (n0 < a.N && m0 < a.M) {  // quarters past M: never read
+                if (!(a.dbg & 32))  // e-tiles: L2 evict-first (AC_DBG bit 32 turns it off)
+                  ptx::bulk_store_hint(dst, sb, 4096, ptx::policy_evict_first());
+                else
+                  ptx::bulk_store(dst, sb, 4096);
+              }
             } else {
               ptx::tma_store_4d(&a.tout, sb, n0, m0, b1, b2);
             }
