@@ -46,7 +46,7 @@ struct Arena {
   // the tensors: per scores node, offset (-1 none), batches B, chunks n.  Layout in
   // ints: [epoch: B][tile counters: n][PV unit counters: n][PV done counts: n x B]
   std::vector<int64_t> ctrl_off;
-  std::vector<int64_t> ctrl_b, ctrl_n;
+  std::vector<int64_t> ctrl_b, ctrl_n, ctrl_mt;
 };
 
 struct View {
@@ -116,7 +116,10 @@ bool pv_online_enabled() {
 //   [B + 2n, +nB)           PV per-batch unit counts per chunk
 //   [.., +B)                scores -> PV of the same chunk: per-batch epochs (AC_CONC)
 //   [.., +nB)               scores per-batch warp-slab counts per chunk (AC_CONC)
-int64_t ctrl_ints(int64_t B, int64_t n) { return 2 * B + 2 * n + 2 * n * B; }
+//   [.., +B * mt)           split-K tile counters of the PV (mt = 128-row tiles of a chunk;
+//                           the last unit of a tile resets its counter, so one zeroing
+//                           per region serves every chunk)
+int64_t ctrl_ints(int64_t B, int64_t n, int64_t mt) { return 2 * B + 2 * n + 2 * n * B + B * mt; }
 
 // AC_CONC=1: the PV of a chunk runs beside its scores (per-batch completion flags
 // instead of a grid dependency), the scores grid capped at AC_CONC_S CTAs (default
@@ -206,7 +209,7 @@ std::vector<Chain> fused_chains(const Graph& g, const Plan& plan) {
 constexpr int SK_NG = 4;
 int64_t sk_gk(int64_t nk) { return ((nk + 63) / 64 + SK_NG - 1) / SK_NG; }
 struct F2Layout {
-  int64_t stats = 0, rowst = 0, part = 0, cnt = 0, total = 0;
+  int64_t stats = 0, rowst = 0, part = 0, cnt = 0, ml = 0, total = 0;
   int64_t ncnt = 0;
 };
 // S of a fused chain is stored as pre-swizzled e-tiles (GemmProblem::etile):
@@ -222,7 +225,8 @@ F2Layout f2_layout(int64_t B1, int64_t M, int64_t nk, bool split) {
   L.part = L.rowst + al(B1 * M * 8);
   L.cnt = L.part + (ng > 1 ? al(B1 * mt * ng * 128 * 64 * 4) : 0);
   L.ncnt = 1 + (ng > 1 ? B1 * mt : 0);  // [0]: dynamic unit counter, then one per tile
-  L.total = L.cnt + al(L.ncnt * 4);
+  L.ml = L.cnt + al(L.ncnt * 4);         // split + online fold: (max, sum) per (unit, row)
+  L.total = L.ml + (ng > 1 ? al(B1 * mt * ng * 128 * 8) : 0);
   return L;
 }
 
@@ -323,6 +327,7 @@ Arena build_arena(const Graph& g, const Plan& plan) {
   A.ctrl_off.assign(S, -1);
   A.ctrl_b.assign(S, 0);
   A.ctrl_n.assign(S, 0);
+  A.ctrl_mt.assign(S, 0);
   if (overlap_enabled()) {
     for (const Chain& c : fused_chains(g, plan)) {
       const int r = region_index(plan, c.scores);
@@ -343,7 +348,8 @@ Arena build_arena(const Graph& g, const Plan& plan) {
       A.ctrl_off[c.scores] = A.size;
       A.ctrl_b[c.scores] = B;
       A.ctrl_n[c.scores] = n;
-      A.size += (ctrl_ints(B, n) * 4 + 255) / 256 * 256;
+      A.ctrl_mt[c.scores] = (plan.regions[r].chunk_len() + 127) / 128;
+      A.size += (ctrl_ints(B, n, A.ctrl_mt[c.scores]) * 4 + 255) / 256 * 256;
     }
   }
   return A;
@@ -405,6 +411,12 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
 // that PV has published epoch k for it; tiles are taken dynamically.  The PV waits
 // for its combine (PDL + griddepcontrol.wait), takes units from its own per-chunk
 // counter and publishes its epochs.
+// the chain of this node runs with a chunk-loop control block in this launch
+bool chain_ctrl(const ac_exec* e, int node, const NodeCtx& cx) {
+  const int h = e->fuse_head[node];
+  return h >= 0 && e->arena.ctrl_off[h] >= 0 && cx.chunk >= 0;
+}
+
 bool g_kind_is(const ac_exec* e, int node, const char* k1, const char* k2) {
   const std::string& k = e->g->nodes[node].kind;
   return k == k1 || k == k2;
@@ -437,6 +449,7 @@ void chain_overlap(const ac_exec* e, int node, const NodeCtx& cx, GemmProblem& p
     p.sched = c + B + n + k;
     p.done_cnt = c + B + 2 * n + static_cast<int64_t>(k) * B;
     p.epoch = k;
+    if (p.sk_cnt) p.sk_cnt = c + 2 * B + 2 * n + 2 * n * B;  // (the P buffer's move with the chunk length)
     if (conc) {
       p.wait_epoch = sdone;
       // AC_CONC_P: PV grid (default: the SMs the scores leave free, so the next chunk's
@@ -650,8 +663,11 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         ep.stats_ss = p.M;
         ep.stats_sb1 = static_cast<int64_t>(p.M) * ns;
         chain_overlap(e, i, cx, p);
-        if (e->fuse_online[i])  // no combine step to reset the PV's unit counter
-          p.zero_word = reinterpret_cast<int*>(V[e->fuse_p[i]].p + f2_layout(p.B1, p.M, p.N, false).cnt);
+        if (e->fuse_online[i]) {  // no combine step to reset the PV's counters
+          const F2Layout L = f2_layout(p.B1, p.M, p.N, e->fuse_split[i] != 0);
+          p.zero_word = reinterpret_cast<int*>(V[e->fuse_p[i]].p + L.cnt);
+          p.zero_n = chain_ctrl(e, i, cx) ? 1 : static_cast<int>(L.ncnt);  // (overlap: split counters in the control block)
+        }
       }
     } else if (k == "attn_pv") {
       // fused chain: A is the raw scores S, normalised in shared memory with the
@@ -684,6 +700,7 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
           p.sk_gk = static_cast<int>(sk_gk(p.K));
           p.sk_part = reinterpret_cast<float*>(in(0).p + L.part);
           p.sk_cnt = reinterpret_cast<int*>(in(0).p + L.cnt) + 1;
+          if (p.pv_rowstats) p.sk_ml = in(0).p + L.ml;
         }
         chain_overlap(e, i, cx, p);
       }
@@ -723,9 +740,11 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         ep.stats_ss = p.M;
         ep.stats_sb1 = static_cast<int64_t>(p.M) * ns;
         chain_overlap(e, i, cx, p);
-        if (e->fuse_online[i])
-          p.zero_word = reinterpret_cast<int*>(V[e->fuse_p[i]].p +
-                                               f2_layout(static_cast<int64_t>(p.B1) * p.B2, p.M, p.N, false).cnt);
+        if (e->fuse_online[i]) {
+          const F2Layout L = f2_layout(static_cast<int64_t>(p.B1) * p.B2, p.M, p.N, e->fuse_split[i] != 0);
+          p.zero_word = reinterpret_cast<int*>(V[e->fuse_p[i]].p + L.cnt);
+          p.zero_n = chain_ctrl(e, i, cx) ? 1 : static_cast<int>(L.ncnt);
+        }
       }
     } else if (k == "tri_pv") {
       const bool fz = e->fuse_role[i] == 3;
@@ -762,6 +781,7 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
           p.sk_gk = static_cast<int>(sk_gk(p.K));
           p.sk_part = reinterpret_cast<float*>(in(0).p + L.part);
           p.sk_cnt = reinterpret_cast<int*>(in(0).p + L.cnt) + 1;
+          if (p.pv_rowstats) p.sk_ml = in(0).p + L.ml;
         }
         chain_overlap(e, i, cx, p);
       }
@@ -893,7 +913,7 @@ ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_
         e->fuse_s[node] = s_t;
         e->fuse_p[node] = p_t;
         e->fuse_split[node] = split ? 1 : 0;
-        e->fuse_online[node] = !split && pv_online_enabled() ? 1 : 0;
+        e->fuse_online[node] = pv_online_enabled() ? 1 : 0;
         e->fuse_head[node] = c.scores;
       }
     }
@@ -1032,7 +1052,7 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
       const int64_t co = e->arena.ctrl_off[j];
       if (co >= 0) {
         const int64_t B = e->arena.ctrl_b[j], nn = e->arena.ctrl_n[j];
-        if (cudaMemsetAsync(e->ws + co, 0, ctrl_ints(B, nn) * 4, s) != cudaSuccess)
+        if (cudaMemsetAsync(e->ws + co, 0, ctrl_ints(B, nn, e->arena.ctrl_mt[j]) * 4, s) != cudaSuccess)
           return set_error(AC_ERR_CUDA, "cudaMemsetAsync (chunk-loop control block) failed");
       }
     }

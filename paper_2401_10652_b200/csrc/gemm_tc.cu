@@ -76,6 +76,7 @@ struct alignas(64) GemmArgs {
   int skgk, skng;
   float* skpart;
   int* skcnt;
+  float2* skml;  // online fold with split-K: per (unit, row) the granule's running (max, sum)
   int dbg;  // experiments (AC_DBG): bit0 = MODE 2 transform skipped, 8 = post-scale TMEM reads skipped,
             // 16 / 32 = no L2 evict-first hint on the e-tile loads / stores
   int* sched;  // MODE 2: zero-initialised work counter for dynamic unit scheduling (null = round-robin)
@@ -91,7 +92,8 @@ struct alignas(64) GemmArgs {
   int pair;     // MODE 2, BN = 32, M <= 64: work units are pairs of batches (two M = 64 MMAs)
   int postscale;  // MODE 2: e tiles straight to the MMA (one TMEM buffer per k-block), f applied after
   int pv_rowstats;  // MODE 2: fold each row's (M, 1/L) from the slab statistics in-kernel (no combine step)
-  int* zero_word;   // MODE 1 / 3 / 4: zeroed at kernel start (the PV's unit counter when no combine runs)
+  int* zero_word;   // MODE 1 / 3 / 4: zero_n words zeroed at kernel start (the PV's counters when no combine runs)
+  int zero_n;
   // concurrent scores / PV of one chunk (AC_CONC): the scores count finished warp-slabs
   // per batch (pub_cnt) and release pub_epoch[b] = epoch + 1 when batch b is complete;
   // the PV waits for wait_epoch[b] >= epoch + 1 before reading batch b
@@ -411,7 +413,8 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
   // next kernel of the chunk loop be scheduled as SMs free up
   if (a.pdl_wait) ptx::griddep_wait();
   ptx::griddep_launch();
-  if ((MODE == 1 || MODE == 3 || MODE == 4) && a.zero_word && blockIdx.x == 0 && threadIdx.x == 0) *a.zero_word = 0;
+  if ((MODE == 1 || MODE == 3 || MODE == 4) && a.zero_word && blockIdx.x == 0)
+    for (int z = threadIdx.x; z < a.zero_n; z += C::THREADS) a.zero_word[z] = 0;
   // unit sequence of this CTA: i-th unit (static round-robin, or the MODE 2 queue)
   // unit queue in use: MODE 2 always, MODE 1 / 3 with dynamic tiles
   const bool uq = MODE == 2 || (MODE != 0 && a.tsched != nullptr);
@@ -813,7 +816,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
 #pragma unroll
               for (int j = 0; j < 8; ++j) fr[j] = nx[j];
             }
-            if (online) {
+            if (online && ng == 1) {
               const float il = Lr > 0.f ? 1.f / Lr : 0.f;
 #pragma unroll
               for (int c = 0; c < BN; ++c) accv[c] *= il;
@@ -833,6 +836,8 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
 #pragma unroll
               for (int q = 0; q < BN / 4; ++q)
                 reinterpret_cast<float4*>(mine)[q] = make_float4(accv[4 * q], accv[4 * q + 1], accv[4 * q + 2], accv[4 * q + 3]);
+              // online: this granule's O is relative to its own running max; keep (Mr, Lr)
+              if (online) a.skml[static_cast<long long>(unit0 + g) * BM + r] = make_float2(Mr, Lr);
               __threadfence();
               asm volatile("bar.sync 1, 128;" ::: "memory");
               if (lead && lane == 0) *sk_old = atomicAdd(a.skcnt + tile, 1);
@@ -845,17 +850,44 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
               }
               __threadfence();
               const float4* base = reinterpret_cast<const float4*>(a.skpart + (static_cast<long long>(unit0) * BM + r) * BN);
+              if (online) {
+                // merge the granules in order: M = max M_g, O = sum 2^(M_g - M) O_g,
+                // L = sum 2^(M_g - M) L_g, o = O / L (granules of masked keys only: M_g = -inf)
+                const float2* ml = a.skml + static_cast<long long>(unit0) * BM + r;
+                float Mt = -CUDART_INF_F;
+                for (int gg = 0; gg < ng; ++gg) Mt = fmaxf(Mt, __ldcg(ml + static_cast<long long>(gg) * BM).x);
 #pragma unroll
-              for (int q = 0; q < BN / 4; ++q) {
-                const float4 w = __ldcg(base + q);
-                accv[4 * q] = w.x; accv[4 * q + 1] = w.y; accv[4 * q + 2] = w.z; accv[4 * q + 3] = w.w;
-              }
-              for (int gg = 1; gg < ng; ++gg) {
-                const float4* pp = base + static_cast<long long>(gg) * BM * BN / 4;
+                for (int c = 0; c < BN; ++c) accv[c] = 0.f;
+                float Lt = 0.f;
+                for (int gg = 0; gg < ng; ++gg) {
+                  const float2 mg = __ldcg(ml + static_cast<long long>(gg) * BM);
+                  if (mg.x == -CUDART_INF_F) continue;
+                  const float w = ptx::ex2(mg.x - Mt);
+                  Lt = fmaf(mg.y, w, Lt);
+                  const float4* pp = base + static_cast<long long>(gg) * BM * BN / 4;
+#pragma unroll
+                  for (int q = 0; q < BN / 4; ++q) {
+                    const float4 v4 = __ldcg(pp + q);
+                    accv[4 * q] = fmaf(w, v4.x, accv[4 * q]); accv[4 * q + 1] = fmaf(w, v4.y, accv[4 * q + 1]);
+                    accv[4 * q + 2] = fmaf(w, v4.z, accv[4 * q + 2]); accv[4 * q + 3] = fmaf(w, v4.w, accv[4 * q + 3]);
+                  }
+                }
+                const float il = Lt > 0.f ? 1.f / Lt : 0.f;
+#pragma unroll
+                for (int c = 0; c < BN; ++c) accv[c] *= il;
+              } else {
 #pragma unroll
                 for (int q = 0; q < BN / 4; ++q) {
-                  const float4 w = __ldcg(pp + q);
-                  accv[4 * q] += w.x; accv[4 * q + 1] += w.y; accv[4 * q + 2] += w.z; accv[4 * q + 3] += w.w;
+                  const float4 w = __ldcg(base + q);
+                  accv[4 * q] = w.x; accv[4 * q + 1] = w.y; accv[4 * q + 2] = w.z; accv[4 * q + 3] = w.w;
+                }
+                for (int gg = 1; gg < ng; ++gg) {
+                  const float4* pp = base + static_cast<long long>(gg) * BM * BN / 4;
+#pragma unroll
+                  for (int q = 0; q < BN / 4; ++q) {
+                    const float4 w = __ldcg(pp + q);
+                    accv[4 * q] += w.x; accv[4 * q + 1] += w.y; accv[4 * q + 2] += w.z; accv[4 * q + 3] += w.w;
+                  }
                 }
               }
               if (lead && lane == 0) a.skcnt[tile] = 0;  // ready for the next launch
@@ -1833,12 +1865,13 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
       a.skgk = p.sk_gk;
       a.skpart = p.sk_part;
       a.skcnt = p.sk_cnt;
+      a.skml = static_cast<float2*>(p.sk_ml);
     } else {
       a.skgk = kbn;  // one unit per tile
     }
     a.skng = (kbn + a.skgk - 1) / a.skgk;
     if (a.skng > 1 && !a.skcnt) return cudaErrorInvalidValue;
-    if (p.pv_rowstats && a.skgk < kbn) return cudaErrorInvalidValue;  // the online fold needs whole rows
+    if (p.pv_rowstats && a.skgk < kbn && !p.sk_ml) return cudaErrorInvalidValue;  // split online fold: (M, L) per granule
     if (p.causal_k && a.MT > MAX_MT) return cudaErrorInvalidValue;
   }
   a.pdl_wait = p.pdl_wait;
@@ -1860,6 +1893,7 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   a.pv_rowstats = (MODE == 2 && C::PS && p.pv_rowstats) ? 1 : 0;
   if (MODE == 2 && p.pv_rowstats && !a.pv_rowstats) return cudaErrorInvalidValue;
   a.zero_word = (MODE == 1 || MODE == 3 || MODE == 4) ? p.zero_word : nullptr;
+  a.zero_n = p.zero_n;
   a.pub_cnt = MODE == 1 ? p.pub_cnt : nullptr;
   a.pub_epoch = MODE == 1 ? p.pub_epoch : nullptr;
   if (MODE == 1 && a.pub_cnt && !a.tsched) return cudaErrorInvalidValue;  // batch-major dynamic tiles only

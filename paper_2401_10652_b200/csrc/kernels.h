@@ -83,6 +83,7 @@ struct GemmProblem {
   int sk_gk = 0;
   float* sk_part = nullptr;
   int* sk_cnt = nullptr;
+  void* sk_ml = nullptr;  // float2 per (unit, row): online fold with split-K
   // f2 e-tiles: e = 2^(x - m2) stored as pre-swizzled 16 KB tiles, tile
   // (b1, mt, kb) = the 128-row x 64-key block exactly as the 128B-swizzled UMMA
   // operand sits in shared memory, at etile + ((b1 * MT + mt) * NKB + kb) * 16384
@@ -112,6 +113,7 @@ struct GemmProblem {
   // statistics itself (pv_rowstats); the scores zero the PV's unit counter (zero_word)
   int pv_rowstats = 0;
   int* zero_word = nullptr;
+  int zero_n = 1;  // words zeroed from zero_word
   // concurrent scores / PV of one chunk (AC_CONC=1): the scores publish per-batch
   // completion (pub_cnt, pub_epoch = epoch + 1), the PV waits on it (wait_epoch)
   // instead of on the whole scores grid; max_ctas caps the scores grid so the PV

@@ -171,12 +171,16 @@ def test_fused_softmax_pv_vs_unfused(monkeypatch, causal, online):
     assert gu.rel_err(y1, y0.double().cpu().numpy()) < 1e-2
 
 
+@pytest.mark.parametrize("online", ["1", "0"])
 @pytest.mark.parametrize("split", ["0", "1"])
-def test_fused_pv_split_k_chunk_invariant(monkeypatch, split):
+def test_fused_pv_split_k_chunk_invariant(monkeypatch, split, online):
     """Fixed split-K of the fused PV (AC_PV_SPLITK=1 forces it on, 0 off; keys cut
     into 4 granules at fixed positions): bf16 tolerance vs the oracle and chunked ==
-    unchunked bitwise, causal and not."""
+    unchunked bitwise, causal and not; online=1 (default): each granule folds its own
+    (max, sum) and the tile's last unit merges them in granule order (no combine
+    launch), online=0: the statistics combine runs first."""
     monkeypatch.setenv("AC_PV_SPLITK", split)
+    monkeypatch.setenv("AC_PV_ONLINE", online)
     for causal in (True, False):
         og = workloads.block("attn_only", 2048 + 320, 256, 4, 0, causal, "bf16", name="pv_split")
         _check_all_plans(og, ["autochunk-plan 1\nregion s=scores e=pv n=4 dims=0\n",
