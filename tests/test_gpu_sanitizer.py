@@ -55,6 +55,20 @@ for og, txt in [
     for t in [txt, "autochunk-plan 1\n"]:
         gu.run(cg, api.plan_parse(cg, t), og, dev)
         torch.cuda.synchronize()
+# forced PV split-K with the online fold (granule partials + (max, sum), counters in the
+# control block under the overlap), then the opt-in concurrent scores / PV
+import os
+for env in ({"AC_PV_SPLITK": "1"}, {"AC_CONC": "1", "AC_CONC_S": "8"}):
+    os.environ.update(env)
+    for causal in (False, True):
+        og = workloads.block("attn_only", 640 + 96, 256, 4, 0, causal, "bf16", name="sk")
+        cg = gu.c_graph(og)
+        vals, dev = gu.make_values(og, 1)
+        for t in ["autochunk-plan 1\nregion s=scores e=pv n=3 dims=0\n", "autochunk-plan 1\n"]:
+            gu.run(cg, api.plan_parse(cg, t), og, dev)
+            torch.cuda.synchronize()
+    for k in env:
+        del os.environ[k]
 print("SANITIZER-RUN-OK")
 """
 
