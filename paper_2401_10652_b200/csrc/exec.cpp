@@ -461,6 +461,7 @@ void chain_overlap(const ac_exec* e, int node, const NodeCtx& cx, GemmProblem& p
 }
 
 ac_status launch_node(const ac_exec* e, int i, const std::vector<View>& V, const NodeCtx& cx, cudaStream_t s) {
+  if (e->fuse_role[i] == 2 && e->fuse_online[i]) return AC_OK;  // folded into the PV: no launch, no timing entry
   if (!e->profiling) return launch_node_impl(e, i, V, cx, s);
   const size_t k = e->ev_node.size();
   while (e->ev_pool.size() < 2 * (k + 1)) {
