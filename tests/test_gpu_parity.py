@@ -294,6 +294,20 @@ def test_af_chunk_overlap_opt_in(monkeypatch):
                           "region s=col_scores e=col_pv n=6 dims=0\n"], seed=9)
 
 
+def test_causal_chunk_overlap_opt_in(monkeypatch):
+    """The chunk-loop overlap on causal attention chains (AC_OVERLAP_CAUSAL=1: dynamic
+    scores tiles of chunk k+1 waiting on per-head epochs of chunk k's PV, PDL launches;
+    off by default for causal chains) keeps the results: vs the oracle and bitwise
+    equal to unchunked, also on a 2-block stack."""
+    monkeypatch.setenv("AC_OVERLAP_CAUSAL", "1")
+    og = workloads.block("attn_only", 2048 + 320, 256, 4, 0, True, "bf16", name="ovc")
+    _check_all_plans(og, ["autochunk-plan 1\nregion s=scores e=pv n=4 dims=0\n",
+                          "autochunk-plan 1\nregion s=scores e=pv n=3 dims=0\n"], seed=17)
+    og = workloads.transformer(512, 256, 4, 512, True, "bf16", name="ovs", layers=2)
+    _check_all_plans(og, ["autochunk-plan 1\nregion s=L0_scores e=L0_pv n=4 dims=0\n"
+                          "region s=L1_scores e=L1_pv n=2 dims=0\n"], seed=17)
+
+
 @pytest.mark.parametrize("causal", [True, False])
 def test_concurrent_scores_pv(monkeypatch, causal):
     """AC_CONC=1: the PV of each chunk runs beside its scores, reading a head once the
@@ -301,6 +315,7 @@ def test_concurrent_scores_pv(monkeypatch, causal):
     scores grid capped so the PV has SMs.  Same arithmetic: vs the oracle and bitwise
     equal to unchunked; also with a scores grid of one CTA (the PV waits the longest)."""
     monkeypatch.setenv("AC_CONC", "1")
+    monkeypatch.setenv("AC_OVERLAP_CAUSAL", "1")  # (the concurrency rides on the overlap's control block)
     og = workloads.block("attn_only", 2048 + 320, 256, 4, 0, causal, "bf16", name="conc")
     plans = ["autochunk-plan 1\nregion s=scores e=pv n=4 dims=0\n",
              "autochunk-plan 1\nregion s=scores e=pv n=3 dims=0\n"]
