@@ -294,6 +294,39 @@ def test_af_chunk_overlap_opt_in(monkeypatch):
                           "region s=col_scores e=col_pv n=6 dims=0\n"], seed=9)
 
 
+def test_ac_run_cuda_graph_capture():
+    """ac_run is stream-ordered with no host synchronisation, so a chunked run can be
+    captured into a CUDA graph and replayed: the replay reproduces the direct run
+    bitwise (f2 chain with the chunk-loop overlap on a non-causal block, and a causal
+    block in stream order)."""
+    gu = _gu()
+    from paper_2401_10652_b200 import api
+    for causal in (False, True):
+        og = workloads.block("attn_only", 2048 + 320, 256, 4, 0, causal, "bf16", name="cg")
+        cg = gu.c_graph(og)
+        vals, dev = gu.make_values(og, 19)
+        plan = api.plan_parse(cg, "autochunk-plan 1\nregion s=scores e=pv n=4 dims=0\n")
+        got, ex = gu.run(cg, plan, og, dev)
+        torch.cuda.synchronize()
+        ws = torch.empty(max(plan.workspace_bytes(), 16), dtype=torch.uint8, device="cuda")
+        ex2 = api.Exec(plan, ws)
+        ins = {t: dev[t] for t in og.inputs + og.weights}
+        outs = {o: torch.empty_like(got[o]) for o in og.outputs}
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            ex2.run(ins, outs, stream=s)  # warm-up (function attributes, tensor maps)
+        s.synchronize()
+        for o in outs:
+            outs[o].zero_()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            ex2.run(ins, outs, stream=s)
+        g.replay()
+        torch.cuda.synchronize()
+        for o in og.outputs:
+            assert torch.equal(outs[o], got[o]), (causal, o)
+
+
 def test_causal_chunk_overlap_opt_in(monkeypatch):
     """The chunk-loop overlap on causal attention chains (AC_OVERLAP_CAUSAL=1: dynamic
     scores tiles of chunk k+1 waiting on per-head epochs of chunk k's PV, PDL launches;
