@@ -1029,6 +1029,10 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
 
   const int S = static_cast<int>(g.nodes.size());
   int i = 0;
+  // launches outside chunk loops (GEMMs, LayerNorm, fused attention) after a kernel of
+  // this run overlap their prologue with its tail too (AC_PDL=0 off)
+  const bool run_pdl = pdl_enabled() && !(getenv("AC_PDL_OUTSIDE") && getenv("AC_PDL_OUTSIDE")[0] == '0');
+  int prev_kernel = 0;  // 1: the previous stream operation of this run was one of our kernels
   while (i < S) {
     const Node& n = g.nodes[i];
     if (n.source()) {
@@ -1039,6 +1043,12 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
     if (r < 0 || e->plan.regions[r].n <= 1) {
       NodeCtx cx;
       cx.fast = e->causal_fast[i] != 0;
+      const std::string& kd = n.kind;
+      cx.pdl = run_pdl && prev_kernel && e->fuse_role[i] == 0 &&
+                       (kd == "linear" || kd == "layernorm" || kd == "attn_fused")
+                   ? 1
+                   : 0;
+      prev_kernel = 1;
       ac_status st = launch_node(e, i, full, cx, s);
       if (st != AC_OK) return st;
       ++i;
