@@ -1124,8 +1124,15 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
         cx.pdl = loop_pdl && !first_launch ? 1 : 0;
         // (causal f2 chains without the overlap run in plain stream order, see build_arena)
         if (e->fuse_head[j] >= 0 && e->arena.ctrl_off[e->fuse_head[j]] < 0 && causal_chain(g, e->fuse_head[j]) &&
-            !(getenv("AC_OVERLAP_CAUSAL") && getenv("AC_OVERLAP_CAUSAL")[0] == '1'))
-          cx.pdl = 0;
+            !(getenv("AC_OVERLAP_CAUSAL") && getenv("AC_OVERLAP_CAUSAL")[0] == '1')) {
+          // AC_PDL_CHAIN: bit 1 = PDL on the chain's scores, bit 2 = on its PV.  Default 1:
+          // the scores' prologue overlaps the previous PV's tail (GPT 2.605 -> 2.599 ms), a
+          // PDL-launched PV measured slower (both: 2.615 ms)
+          const char* pc = getenv("AC_PDL_CHAIN");
+          const int bits = pc ? atoi(pc) : 1;
+          const int role = e->fuse_role[j];
+          if (!((role == 1 && (bits & 1)) || (role == 3 && (bits & 2)))) cx.pdl = 0;
+        }
         first_launch = false;
         const int d = R.dim_of(nj.output);
         if (d >= 0 && d == e->chain_rows_dim[j]) cx.row_off = off;
