@@ -418,9 +418,9 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
 
 // Chunk-loop overlap of a fused chain (Arena::ctrl_*): scores of chunk k > 0 start
 // while the PV of chunk k - 1 drains (PDL, no grid wait) and write batch b only once
-// that PV has published epoch k for it; tiles are taken dynamically.  The PV waits
-// for its combine (PDL + griddepcontrol.wait), takes units from its own per-chunk
-// counter and publishes its epochs.
+// that PV has published epoch k for it; tiles are taken dynamically.  The PV follows
+// its scores in stream order, takes units from its own per-chunk counter and
+// publishes its epochs.
 // the chain of this node runs with a chunk-loop control block in this launch
 bool chain_ctrl(const ac_exec* e, int node, const NodeCtx& cx) {
   const int h = e->fuse_head[node];
@@ -454,7 +454,10 @@ void chain_overlap(const ac_exec* e, int node, const NodeCtx& cx, GemmProblem& p
       p.max_ctas = conc_scores_ctas();
     }
   } else {
-    p.pdl = 1;
+    // the PV itself is launched in plain stream order (a PDL-launched PV measured slower:
+    // UNet 2.803 -> 2.781 ms without; AC_OVPV_PDL=1 restores it); it still triggers the
+    // next chunk's scores early.  Concurrent mode needs PDL (no grid dependency).
+    p.pdl = conc || (getenv("AC_OVPV_PDL") && getenv("AC_OVPV_PDL")[0] == '1') ? 1 : 0;
     p.pdl_wait = conc && !getenv("AC_CONC_GRIDWAIT") ? 0 : 1;  // concurrent: per-batch flags of this chunk's scores instead
     p.sched = c + B + n + k;
     p.done_cnt = c + B + 2 * n + static_cast<int64_t>(k) * B;
