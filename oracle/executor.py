@@ -168,6 +168,19 @@ def _tracked_region(g, r, env, tr, per_step, esz, wset, last, mirror, contiguity
                 per_step[k] = max(per_step[k], tr.total())
                 continue
             nd = g.nodes[k]
+            if nd.output not in r.dims:
+                # off the flow, not hoisted (graph optimisation off): the node is
+                # recomputed whole in every chunk from whole inputs; its output is a
+                # full-size interior tensor (Eq. 2 term (v), R6)
+                out = _eval(g, k, [local[t] if t in local else env[t] for t in nd.inputs], None, mirror)
+                local[nd.output] = out
+                tr.alloc(("slice", nd.output), out.size * esz[nd.output])
+                per_step[k] = max(per_step[k], tr.total())
+                for t in set(nd.inputs) | {nd.output}:
+                    if t in local and ilast.get(t, k) <= k:
+                        del local[t]
+                        tr.free(("slice", t))
+                continue
             res = ops.propagate(nd.kind, nd.attrs, [g.tensors[t].shape for t in nd.inputs],
                                 g.tensors[nd.output].shape, r.dims[nd.output])
             vals = []

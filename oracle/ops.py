@@ -299,8 +299,12 @@ def shape(kind: str, attrs: dict, ins) -> tuple:
 
 
 def flops(kind: str, attrs: dict, ins, out) -> int:
-    """FLOP model: SPEC S:76 for primitives; fused kinds = their contraction
-    (2 per multiply-add) + one per element for each fused epilogue op."""
+    """FLOP model: SPEC S:76 for primitives; a fused kind counts the sum over
+    its SPEC-primitive decomposition (S:76 conventions, as SPEC's attention
+    corpus writes the scale as a `mul` node): the contraction
+    (2 per multiply-add) + one per output element for each elementwise
+    epilogue op (scale, causal mask add, bias add, activation, gate, residual).
+    Pinned by tests/test_oracle_flops.py, which builds each decomposition."""
     ne = prod(out)
     if kind in SOURCE or kind in ("transpose", "reshape", "concat", "slice"):
         return 0
@@ -323,17 +327,18 @@ def flops(kind: str, attrs: dict, ins, out) -> int:
         O = prod(attrs["out"])
         extra = int(attrs.get("bias", 0)) + int(attrs.get("act", "none") != "none") + int(attrs.get("res", 0))
         return 2 * R * K * O + R * O * extra
-    if kind == "attn_scores":
+    if kind == "attn_scores":     # matmul + scale mul (+ causal mask add)
         q = ins[0]
-        return 2 * ne * q[2]
+        return 2 * ne * q[2] + ne * (1 + int(attrs.get("causal", 0)))
     if kind == "attn_pv":
         p = ins[0]
         return 2 * prod(p) * out[2]
-    if kind == "attn_fused":
+    if kind == "attn_fused":      # the unfused chain: scores + softmax (5/elem) + PV
         q, k = ins[0], ins[1]
-        return 4 * q[1] * q[0] * k[0] * q[2]   # QK^T + PV of the unfused chain
-    if kind == "tri_scores":
-        return 2 * ne * ins[0][3] + ne
+        ns = q[1] * q[0] * k[0]
+        return 4 * ns * q[2] + ns * (1 + int(attrs.get("causal", 0))) + 5 * ns
+    if kind == "tri_scores":      # matmul + scale mul + bias add
+        return 2 * ne * ins[0][3] + 2 * ne
     if kind == "tri_pv":
         p = ins[0]
         return 2 * prod(p) * out[3] + ne

@@ -1104,6 +1104,17 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
         // consumers taking a region input whole keep the full view
         std::vector<View> VV;
         const std::vector<View>* use = &V;
+        if (R.dim_of(nj.output) < 0) {
+          // off the flow and not hoisted (graph optimisation off, AC_FLAG_NO_HOIST):
+          // recomputed whole every chunk from whole inputs (the search never
+          // lets such a node read a chunked interior tensor)
+          NodeCtx cx;
+          cx.fast = e->causal_fast[j] != 0;
+          first_launch = false;
+          ac_status st = launch_node(e, j, full, cx, s);
+          if (st != AC_OK) return st;
+          continue;
+        }
         auto res_dims = [&]() {
           std::vector<std::vector<int64_t>> in;
           for (int t : nj.inputs) in.push_back(g.tensors[t].shape);

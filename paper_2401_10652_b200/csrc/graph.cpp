@@ -286,10 +286,15 @@ int64_t op_flops(const std::string& k, const Node& n, const std::vector<Shape>& 
     int64_t extra = n.ai("bias") + (n.as("act", "none") != "none" ? 1 : 0) + n.ai("res");
     return 2 * R * K * O + R * O * extra;
   }
-  if (k == "attn_scores") return 2 * ne * in[0][2];
+  // fused kinds: the sum over their SPEC-primitive decomposition, i.e. the
+  // contraction + one flop per output element for each elementwise epilogue op
+  if (k == "attn_scores") return 2 * ne * in[0][2] + ne * (1 + n.ai("causal"));
   if (k == "attn_pv") return 2 * prod(in[0]) * out[2];
-  if (k == "attn_fused") return 4 * in[0][1] * in[0][0] * in[1][0] * in[0][2];
-  if (k == "tri_scores") return 2 * ne * in[0][3] + ne;
+  if (k == "attn_fused") {
+    int64_t ns = in[0][1] * in[0][0] * in[1][0];
+    return 4 * ns * in[0][2] + ns * (1 + n.ai("causal")) + 5 * ns;
+  }
+  if (k == "tri_scores") return 2 * ne * in[0][3] + 2 * ne;
   if (k == "tri_pv") return 2 * prod(in[0]) * out[3] + ne;
   fail("unknown op kind " + k);
 }

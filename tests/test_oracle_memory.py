@@ -119,17 +119,18 @@ def test_estimate_equals_tracked_chunked_run(mk, contig):
             if len(outs) != 1:
                 continue
             for d in range(len(g.tensors[outs[0]].shape)):
-                r = search.candidate_for(g, s, e, (d,), prod=prod)
-                if r is None:
-                    continue
-                for n in sorted({2, 3, r.extent}):
-                    if n > r.extent:
+                for hz in (True, False):   # graph optimisation on / off (Table 1)
+                    r = search.candidate_for(g, s, e, (d,), prod=prod, hoist=hz)
+                    if r is None:
                         continue
-                    rr = r.with_n(n)
-                    _, per = executor.tracked_run(g, v, [rr], contiguity=contig)
-                    est = memory.estimate_with_plan(g, [rr], contiguity=contig)
-                    assert per == est.per_step, (s, e, d, n)
-                    checked += 1
+                    for n in sorted({2, 3, r.extent}):
+                        if n > r.extent:
+                            continue
+                        rr = r.with_n(n)
+                        _, per = executor.tracked_run(g, v, [rr], contiguity=contig)
+                        est = memory.estimate_with_plan(g, [rr], contiguity=contig)
+                        assert per == est.per_step, (s, e, d, n, hz)
+                        checked += 1
         if checked > 60:
             break
     assert checked > 0

@@ -63,10 +63,24 @@ def test_attention_finds_query_dim_not_softmax_dim():
 def _bf_legal(g, s, e, outs, assign, vals, full):
     """Is there a slicing of the region inputs (one dim per input, each consumer
     edge taking the slice or the whole tensor) whose two chunks concatenate to the
-    unchunked outputs exactly (fp64, exact reduction order)?"""
+    unchunked outputs exactly (fp64, exact reduction order)?
+
+    Position-dependent kinds (the causal mask of attn_scores / attn_fused) need the
+    global index of a slice: for each such node every hypothesis "output dim d of
+    this chunk starts at the chunk's offset" (or none) is tried, so legality is
+    decided by execution alone, never by the propagate tables under test."""
     E = g.tensors[outs[0]].shape[assign[0]]
     if any(g.tensors[y].shape[d] != E for y, d in zip(outs, assign)) or E < 2:
         return False
+    pos = [i for i in range(s, e + 1) if g.nodes[i].attrs.get("causal", 0)]
+    ctx_opts = [[None] + [d for d, x in enumerate(g.tensors[g.nodes[i].output].shape) if x == E] for i in pos]
+    for csel in itertools.product(*ctx_opts):
+        if _bf_legal_ctx(g, s, e, outs, assign, vals, full, E, dict(zip(pos, csel))):
+            return True
+    return False
+
+
+def _bf_legal_ctx(g, s, e, outs, assign, vals, full, E, ctxdim):
     produced = {g.nodes[i].output for i in range(s, e + 1)}
     ins = [t for t in memory.region_io(g, s, e)[0] if t not in g.weights]
     dim_opts = [[None] + [d for d, x in enumerate(g.tensors[t].shape) if x == E] for t in ins]
@@ -95,7 +109,9 @@ def _bf_legal(g, s, e, outs, assign, vals, full):
                                 vv.append(vals[t][tuple(idx)])
                             else:
                                 vv.append(vals[t])
-                        loc[nd.output] = ops.evaluate(nd.kind, nd.attrs, vv)
+                        cd = ctxdim.get(i)
+                        ctx = None if cd is None else {"dim": cd, "offset": off}
+                        loc[nd.output] = ops.evaluate(nd.kind, nd.attrs, vv, ctx)
                 except (ValueError, IndexError):
                     ok = False
                     break
@@ -119,10 +135,22 @@ def _bf_legal(g, s, e, outs, assign, vals, full):
 
 CORPUS = [("mlp", 8, 4), ("attention", 8, 4), ("transformer2", 6, 4), ("alphafold_like_2d", 4, 3)]
 
+# every fused kind: linear with bias / act / residual / trans (vᵀ) and
+# swap (ending-node bias, vᵀ), attn_scores causal and not, attn_pv, attn_fused (f1),
+# tri_scores / tri_pv for the starting and the ending node; extents chosen distinct
+# where the block allows (N=5 gives a ragged 3+2 split)
+FUSED = {
+    "gpt": lambda: workloads.block("transformer", 5, 4, 2, 8, True, "f64"),
+    "vit": lambda: workloads.block("transformer", 5, 4, 2, 8, False, "f64"),
+    "fa_causal": lambda: workloads.block("transformer_fa", 5, 4, 2, 8, True, "f64"),
+    "fa": lambda: workloads.block("attn_only_fa", 5, 4, 2, 0, False, "f64"),
+    "af": lambda: workloads.tri_attn_pair(4, 3, 2, 5, "f64"),
+}
 
-@pytest.mark.parametrize("name,seq,d", CORPUS)
+
+@pytest.mark.parametrize("name,seq,d", CORPUS + [(k, 0, 0) for k in FUSED])
 def test_search_complete_and_sound_vs_brute_force(name, seq, d):
-    g = workloads.corpus(name, seq, d, "f64")
+    g = FUSED[name]() if name in FUSED else workloads.corpus(name, seq, d, "f64")
     vals = _values(g, 11)
     from oracle import executor
     with ops.exact_order():
@@ -130,7 +158,7 @@ def test_search_complete_and_sound_vs_brute_force(name, seq, d):
         prod = g.producer_index()
         sources = [i for i, n in enumerate(g.nodes) if n.kind in ("input", "weight")]
         W = 4
-        npass = nfilt = 0
+        npass = nfilt = nlegal = 0
         for p in range(len(g.nodes)):
             if p in sources:
                 continue
@@ -149,7 +177,18 @@ def test_search_complete_and_sound_vs_brute_force(name, seq, d):
                     npass += 1
                     if got:
                         assert f                              # no false negatives (AC-8)
+                        # the flow map the search emits (propagate rows, X^c dims, the
+                        # causal offsets it implies) executed chunk by chunk must give
+                        # the unchunked graph outputs bit for bit (Eq. 5)
+                        for hz in (False, True):
+                            r = search.candidate_for(g, s, e, assign, hoist=hz)
+                            assert r is not None
+                            ch = executor.run_chunked(g, vals, [r.with_n(2)])
+                            for o in g.outputs:
+                                assert np.array_equal(ch[o], full[o]), (name, s, e, assign, hz, o)
+                        nlegal += 1
         assert npass > 0 and nfilt <= npass
+        assert nlegal > 0
 
 
 def test_rule4_holds_and_window_monotone():
