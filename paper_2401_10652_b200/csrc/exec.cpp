@@ -46,7 +46,7 @@ struct Arena {
   // the tensors: per scores node, offset (-1 none), batches B, chunks n.  Layout in
   // ints: [epoch: B][tile counters: n][PV unit counters: n][PV done counts: n x B]
   std::vector<int64_t> ctrl_off;
-  std::vector<int64_t> ctrl_b, ctrl_n, ctrl_mt;
+  std::vector<int64_t> ctrl_b, ctrl_n, ctrl_mt;  // ctrl_mt: split-K tile counters per launch
 };
 
 struct View {
@@ -116,10 +116,12 @@ bool pv_online_enabled() {
 //   [B + 2n, +nB)           PV per-batch unit counts per chunk
 //   [.., +B)                scores -> PV of the same chunk: per-batch epochs (AC_CONC)
 //   [.., +nB)               scores per-batch warp-slab counts per chunk (AC_CONC)
-//   [.., +B * mt)           split-K tile counters of the PV (mt = 128-row tiles of a chunk;
+//   [.., +sk)               split-K tile counters of the PV, one per (batch, 128-row tile)
+//                           of ONE launch (sk = B_launch * ceil(M_launch / 128) from the
+//                           chunk-reduced S shape: a heads cut shrinks B, a rows cut M);
 //                           the last unit of a tile resets its counter, so one zeroing
-//                           per region serves every chunk)
-int64_t ctrl_ints(int64_t B, int64_t n, int64_t mt) { return 2 * B + 2 * n + 2 * n * B + B * mt; }
+//                           per region serves every chunk
+int64_t ctrl_ints(int64_t B, int64_t n, int64_t sk) { return 2 * B + 2 * n + 2 * n * B + sk; }
 
 // AC_CONC=1: the PV of a chunk runs beside its scores (per-batch completion flags
 // instead of a grid dependency), the scores grid capped at AC_CONC_S CTAs (default
@@ -351,14 +353,21 @@ Arena build_arena(const Graph& g, const Plan& plan) {
       // chunk k is the launch right before the scores of chunk k + 1 (whose inputs
       // then all predate the region)
       if (plan.regions[r].start != c.scores || plan.regions[r].end != c.pv) continue;
-      const std::vector<int64_t>& sh = g.tensors[g.nodes[c.scores].output].shape;
-      int64_t B = 1;
-      for (size_t d = 0; d + 2 < sh.size(); ++d) B *= sh[d];
+      const int s_t = g.nodes[c.scores].output;
+      const std::vector<int64_t>& sh = g.tensors[s_t].shape;
+      std::vector<int64_t> shc = sh;  // one launch's S: the chunk dim reduced to the chunk length
+      const int dch = plan.regions[r].dim_of(s_t);
+      if (dch >= 0) shc[dch] = plan.regions[r].chunk_len();
+      int64_t B = 1, Bl = 1;
+      for (size_t d = 0; d + 2 < sh.size(); ++d) {
+        B *= sh[d];
+        Bl *= shc[d];
+      }
       const int64_t n = plan.regions[r].n;
       A.ctrl_off[c.scores] = A.size;
       A.ctrl_b[c.scores] = B;
       A.ctrl_n[c.scores] = n;
-      A.ctrl_mt[c.scores] = (plan.regions[r].chunk_len() + 127) / 128;
+      A.ctrl_mt[c.scores] = Bl * ((shc[shc.size() - 2] + 127) / 128);
       A.size += (ctrl_ints(B, n, A.ctrl_mt[c.scores]) * 4 + 255) / 256 * 256;
     }
   }
@@ -869,6 +878,9 @@ ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_
   for (auto& t : g.tensors)
     if (t.dtype != e->dt || t.dtype == DT::F64)
       return set_error(AC_ERR_UNSUPPORTED, "GPU executor needs one dtype (f32 or bf16) for every tensor");
+  for (auto& t : g.tensors)  // ac_tensor carries shape[6] / stride[6] (ac.h)
+    if (t.shape.size() > 6)
+      return set_error(AC_ERR_UNSUPPORTED, "tensor " + t.id + " has rank > 6 (the executor's view limit)");
   for (auto& n : g.nodes)
     if (!n.source() && !gpu_kind(n.kind))
       return set_error(AC_ERR_UNSUPPORTED, "no GPU kernel for node " + n.id + " (" + n.kind + ")");
@@ -995,6 +1007,7 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
     const int t = it->second;
     const TensorMeta& tm = g.tensors[t];
     if (!is_caller(g, t)) return set_error(AC_ERR_BIND, "tensor " + tm.id + " is not a graph input/weight/output");
+    if (at.ndim < 0 || at.ndim > 6) return set_error(AC_ERR_BIND, "rank of " + tm.id + " outside [0, 6]");
     if (at.dtype != static_cast<int>(tm.dtype)) return set_error(AC_ERR_BIND, "dtype mismatch for " + tm.id);
     if (at.ndim != static_cast<int>(tm.shape.size())) return set_error(AC_ERR_BIND, "rank mismatch for " + tm.id);
     auto st = tm.strides();

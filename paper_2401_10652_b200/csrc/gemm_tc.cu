@@ -780,6 +780,11 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
                   // the slab's e V product: all BN columns in flight while f is formed
                   ptx::mbar_wait(&kfull[kbuf], kphase);
                   ptx::tc_fence_after();
+                  if (a.trace && lead && lane == 0 && kb0 == klo && j == 0) {
+                    unsigned long long tnow;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+                    a.trace[4 * t + 2] = tnow;
+                  }
                   uint32_t v[BN];
                   const bool skipld = a.dbg & 8;  // experiment: consumer cost without the TMEM reads
 #pragma unroll
@@ -815,6 +820,11 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
               }
 #pragma unroll
               for (int j = 0; j < 8; ++j) fr[j] = nx[j];
+            }
+            if (a.trace && lead && lane == 0) {  // end of the unit's slab stream
+              unsigned long long tnow;
+              asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+              a.trace[4 * t + 3] = tnow;
             }
             if (online && ng == 1) {
               const float il = Lr > 0.f ? 1.f / Lr : 0.f;

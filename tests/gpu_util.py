@@ -26,15 +26,35 @@ def c_graph(og):
     return api.graph_parse(__import__("oracle.graph", fromlist=["serialize"]).serialize(og))
 
 
-def run(cg, plan, og, dev, stream=None, ws=None):
-    """Run `plan` once; returns ({output id: tensor}, exec)."""
+GUARD = 1 << 16   # workspace canary: bytes of 0xA5 on both sides of the ac_run workspace
+CANARY = 0xA5
+
+
+def run(cg, plan, og, dev, stream=None, ws=None, canary=True):
+    """Run `plan` once; returns ({output id: tensor}, exec).  With canary=True
+    (the default when the caller passes no workspace) the workspace is carved
+    out of a larger buffer whose guard bytes on both sides must be untouched
+    after the run: every GPU test then checks that ac_run stays inside
+    ac_plan_workspace_bytes (SURVEY §5 workspace canary)."""
     nbytes = plan.workspace_bytes()
+    guarded = None
     if ws is None or ws.numel() < nbytes:
-        ws = torch.empty(max(nbytes, 16), dtype=torch.uint8, device="cuda")
+        if canary:
+            guarded = torch.full((GUARD + max(nbytes, 16) + GUARD,), CANARY, dtype=torch.uint8, device="cuda")
+            ws = guarded[GUARD:GUARD + max(nbytes, 16)]
+        else:
+            ws = torch.empty(max(nbytes, 16), dtype=torch.uint8, device="cuda")
     outs = {o: torch.empty(og.tensors[o].shape, dtype=TORCH_DT[og.tensors[o].dtype], device="cuda")
             for o in og.outputs}
     ex = api.Exec(plan, ws)
     ex.run({t: dev[t] for t in og.inputs + og.weights}, outs, stream)
+    if guarded is not None:
+        torch.cuda.synchronize()
+        n = ws.numel()
+        head, tail = guarded[:GUARD], guarded[GUARD + n:]
+        assert bool((head == CANARY).all()) and bool((tail == CANARY).all()), \
+            "ac_run wrote outside its workspace (canary overwritten)"
+        ex.canary_buffer = guarded   # keep the parent alive with the exec
     return outs, ex
 
 

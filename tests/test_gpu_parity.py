@@ -103,6 +103,17 @@ def test_small_unet_bf16():
                           "autochunk-plan 1\nregion s=scores e=pv n=8 dims=0\n"])
 
 
+@pytest.mark.parametrize("plan", ["region s=scores e=pv n=4 dims=1", "region s=scores e=pv n=2 dims=1",
+                                  "region s=scores e=pv n=4 dims=0"])
+def test_heads_cut_splitk_overlap_bf16(plan):
+    """Non-causal rows of >= 4096 keys: the f2 PV runs split-K and the chunk loop
+    overlaps (both default); a heads cut shrinks each launch's batch count, which
+    the overlap control block's split-K counters must follow.
+    The gpu_util canary checks the run stays inside its workspace."""
+    og = workloads.block("attn_only", 4096, 256, 4, 0, False, "bf16", name="unet_heads")
+    _check_all_plans(og, ["autochunk-plan 1\n" + plan + "\n"])
+
+
 def test_small_af_bf16():
     og = workloads.tri_attn_pair(64, 128, 4, 32, "bf16", name="af_small")
     plan = select.select(og, int(0.2 * memory.profile(og).peak_bytes))
@@ -494,3 +505,23 @@ def test_af_full_size_sampled_pairs(ending):
     ref = blocks.tri_attention_pairs(og, vals, "t_", pairs, bool(ending))
     g_pairs = torch.stack([got["zo"][i, j] for i, j in pairs])
     assert gu.rel_err(g_pairs, ref) < 2e-2
+
+
+def test_rank_above_six_refused():
+    """ac_tensor / the executor's views carry at most 6 dims (ac.h): a rank-7 graph
+    is refused at ac_exec_create with AC_ERR_UNSUPPORTED."""
+    from oracle.graph import Builder
+    from paper_2401_10652_b200 import _lib
+    gu = _gu()
+    B = Builder("rank7", "bf16")
+    B.input("x", (1, 1, 1, 1, 1, 2, 64))
+    B.weight("g", (64,), "ln_gamma", 64)
+    B.weight("b", (64,), "ln_beta", 64)
+    B.op("layernorm", ["x", "g", "b"], "y", naxes=1, eps=1e-5)
+    B.output("y")
+    og = B.build()
+    cg = gu.c_graph(og)
+    vals, dev = gu.make_values(og, 0)
+    with pytest.raises(_lib.ACError) as ei:
+        gu.run(cg, gu.empty_plan(cg), og, dev)
+    assert ei.value.status == _lib.AC_ERR_UNSUPPORTED
