@@ -58,9 +58,26 @@ struct View {
 
 }  // namespace ac
 
+// Executor policy switches, read from the environment when a plan's workspace is
+// sized or an executor is created (never per launch; ac_exec keeps its copy).  Defaults are the measured-best settings; the switches
+// exist for A/B measurement and for the tests that compare the unfused path.
+//   AC_FUSE_SOFTMAX=0   run scores -> softmax -> PV chains unfused (P materialised)
+//   AC_PV_SPLITK=0|1    force the fused PV's fixed split-K off / on (default: auto)
+//   AC_OVERLAP=0        no chunk-loop overlap at all
+//   AC_OVERLAP_CAUSAL=0|1, AC_OVERLAP_TRI=0|1   overlap for causal / triangle chains
+//   AC_PDL=0            no programmatic dependent launches
+struct ExecOptions {
+  bool fuse_softmax = true;
+  int pv_splitk = -1;
+  bool overlap = true;
+  bool overlap_causal = true;
+  bool overlap_tri = false;
+  bool pdl = true;
+};
 struct ac_exec {
   std::shared_ptr<const Graph> g;
   Plan plan;
+  ExecOptions opt;
   Arena arena;
   char* ws = nullptr;
   int64_t ws_bytes = 0;
@@ -73,10 +90,10 @@ struct ac_exec {
   // fused softmax chains (f2): per node 0 none, 1 scores (writes stats), 2 softmax
   // (not launched), 3 PV (normalises S in smem); fuse_s / fuse_p: the chain's S and P tensors
   std::vector<char> fuse_role;
-  std::vector<char> fuse_online;  // non-split chain: the PV folds (M, 1/L) itself, no combine launch
   std::vector<int> fuse_s, fuse_p;
   std::vector<char> fuse_split;        // per node of a fused chain: PV fixed split-K on
-  std::vector<int> fuse_head;          // per node of a fused chain: its scores node
+  std::vector<int> fuse_head;
+  std::vector<int64_t> fuse_balloc, fuse_malloc;  // allocated batches / rows of the chain's S (layout of P)          // per node of a fused chain: its scores node
   mutable ac_run_stats stats{};
   // profiling: event pairs per launch of the last run
   bool profiling = false;
@@ -91,22 +108,28 @@ namespace {
 
 bool is_caller(const Graph& g, int t) { return g.is_input[t] || g.is_weight[t] || g.is_output[t]; }
 
-// Fixed split-K of the fused PV: on for non-causal chains (uniform tiles, where
-// quarter-tile units taken dynamically shorten the last wave: UNet PV 1.70 -> 1.39 ms),
-// off for causal ones (heaviest-first whole tiles already balance; the partials
-// cost more than they save).  The choice depends only on the graph, never on the
-// chunking, so chunked == unchunked bitwise either way.  AC_PV_SPLITK=0/1 forces it.
-bool pv_splitk(bool causal, int64_t nk) {
-  const char* v = getenv("AC_PV_SPLITK");
-  if (v && (v[0] == '0' || v[0] == '1')) return v[0] == '1';
-  return !causal && nk >= 4096;  // short rows: one unit per tile is cheaper
+ExecOptions read_options() {
+  ExecOptions r;
+  auto flag = [](const char* name, int def) {
+    const char* v = getenv(name);
+    return (v && (v[0] == '0' || v[0] == '1')) ? v[0] - '0' : def;
+  };
+  r.fuse_softmax = flag("AC_FUSE_SOFTMAX", 1) != 0;
+  r.pv_splitk = flag("AC_PV_SPLITK", -1);
+  r.overlap = flag("AC_OVERLAP", 1) != 0;
+  r.overlap_causal = flag("AC_OVERLAP_CAUSAL", 1) != 0;
+  r.overlap_tri = flag("AC_OVERLAP_TRI", 0) != 0;
+  r.pdl = flag("AC_PDL", 1) != 0;
+  return r;
 }
 
-// AC_PV_ONLINE=0: keep the separate statistics-combine launch for non-split chains too (the PV then folds
-// each row's (M, 1/L) online from the slab statistics; split-K chains always combine)
-bool pv_online_enabled() {
-  const char* v = getenv("AC_PV_ONLINE");
-  return !(v && v[0] == '0');
+// Fixed split-K of the fused PV (key granules at fixed positions, so chunked ==
+// unchunked bitwise either way): on for non-causal chains of >= 4096 keys (uniform
+// tiles: quarter-tile units taken dynamically shorten the last wave), off for causal
+// ones (heaviest-first whole tiles).  AC_PV_SPLITK=0/1 forces it.
+bool pv_splitk(const ExecOptions& o, bool causal, int64_t nk) {
+  if (o.pv_splitk >= 0) return o.pv_splitk == 1;
+  return !causal && nk >= 4096;
 }
 
 // Control block of an overlapped chain (B batches, n chunks), ints:
@@ -114,42 +137,15 @@ bool pv_online_enabled() {
 //   [B, B + n)              scores tile counters per chunk
 //   [B + n, B + 2n)         PV unit counters per chunk
 //   [B + 2n, +nB)           PV per-batch unit counts per chunk
-//   [.., +B)                scores -> PV of the same chunk: per-batch epochs (AC_CONC)
-//   [.., +nB)               scores per-batch warp-slab counts per chunk (AC_CONC)
 //   [.., +sk)               split-K tile counters of the PV, one per (batch, 128-row tile)
 //                           of ONE launch (sk = B_launch * ceil(M_launch / 128) from the
 //                           chunk-reduced S shape: a heads cut shrinks B, a rows cut M);
 //                           the last unit of a tile resets its counter, so one zeroing
 //                           per region serves every chunk
-int64_t ctrl_ints(int64_t B, int64_t n, int64_t sk) { return 2 * B + 2 * n + 2 * n * B + sk; }
+int64_t ctrl_ints(int64_t B, int64_t n, int64_t sk) { return B + 2 * n + n * B + sk; }
 
-// AC_CONC=1: the PV of a chunk runs beside its scores (per-batch completion flags
-// instead of a grid dependency), the scores grid capped at AC_CONC_S CTAs (default
-// 112) so the PV has SMs meanwhile; e-tiles are then read soon after they are written
-bool conc_enabled() {
-  const char* v = getenv("AC_CONC");
-  return v && v[0] == '1';
-}
-int conc_scores_ctas() {
-  const char* v = getenv("AC_CONC_S");
-  return v ? atoi(v) : 112;
-}
-
-// Chunk-loop overlap of fused chains (programmatic dependent launch + per-batch
-// epochs): the next chunk's scores start on SMs the PV's tail frees.
-// AC_OVERLAP=0 disables it (every launch then waits for the previous one).
 bool causal_chain(const Graph& g, int scores) {
   return g.nodes[scores].kind == "attn_scores" && g.nodes[scores].ai("causal") != 0;
-}
-
-bool pdl_enabled() {
-  const char* v = getenv("AC_PDL");
-  return !(v && v[0] == '0');
-}
-
-bool overlap_enabled() {
-  const char* v = getenv("AC_OVERLAP");
-  return !(v && v[0] == '0');
 }
 
 int region_index(const Plan& plan, int node) {
@@ -167,10 +163,9 @@ int region_index(const Plan& plan, int node) {
 struct Chain {
   int scores, softmax, pv;
 };
-std::vector<Chain> fused_chains(const Graph& g, const Plan& plan) {
+std::vector<Chain> fused_chains(const Graph& g, const Plan& plan, const ExecOptions& o) {
   std::vector<Chain> out;
-  const char* env = getenv("AC_FUSE_SOFTMAX");
-  if (env && env[0] == '0') return out;
+  if (!o.fuse_softmax) return out;
   for (int i = 0; i < static_cast<int>(g.nodes.size()); ++i) {
     const Node& n = g.nodes[i];
     // attn_scores [H, M, nk] -> softmax -> attn_pv, or the AlphaFold triangle chain
@@ -215,7 +210,7 @@ std::vector<Chain> fused_chains(const Graph& g, const Plan& plan) {
 constexpr int SK_NG = 4;
 int64_t sk_gk(int64_t nk) { return ((nk + 63) / 64 + SK_NG - 1) / SK_NG; }
 struct F2Layout {
-  int64_t stats = 0, rowst = 0, part = 0, cnt = 0, ml = 0, total = 0;
+  int64_t stats = 0, part = 0, cnt = 0, ml = 0, total = 0;
   int64_t ncnt = 0;
 };
 // S of a fused chain is stored as pre-swizzled e-tiles (GemmProblem::etile):
@@ -227,8 +222,7 @@ F2Layout f2_layout(int64_t B1, int64_t M, int64_t nk, bool split) {
   const int64_t ns = (nk + 63) / 64, mt = (M + 127) / 128, ng = split ? (ns + sk_gk(nk) - 1) / sk_gk(nk) : 1;
   auto al = [](int64_t v) { return (v + 255) / 256 * 256; };
   L.stats = 0;
-  L.rowst = al(B1 * ns * M * 8);
-  L.part = L.rowst + al(B1 * M * 8);
+  L.part = al(B1 * ns * M * 8);
   L.cnt = L.part + (ng > 1 ? al(B1 * mt * ng * 128 * 64 * 4) : 0);
   L.ncnt = 1 + (ng > 1 ? B1 * mt : 0);  // [0]: dynamic unit counter, then one per tile
   L.ml = L.cnt + al(L.ncnt * 4);         // split + online fold: (max, sum) per (unit, row)
@@ -236,7 +230,7 @@ F2Layout f2_layout(int64_t B1, int64_t M, int64_t nk, bool split) {
   return L;
 }
 
-Arena build_arena(const Graph& g, const Plan& plan) {
+Arena build_arena(const Graph& g, const Plan& plan, const ExecOptions& o) {
   const int T = static_cast<int>(g.tensors.size());
   const int S = static_cast<int>(g.nodes.size());
   Arena A;
@@ -285,7 +279,7 @@ Arena build_arena(const Graph& g, const Plan& plan) {
   }
   // fused chains: S stays live until the PV reads it; P's buffer shrinks to the
   // softmax statistics (float2 per row and 64-key slab), written by the scores step
-  for (const Chain& c : fused_chains(g, plan)) {
+  for (const Chain& c : fused_chains(g, plan, o)) {
     const int s_t = g.nodes[c.scores].output, p_t = g.nodes[c.softmax].output;
     std::vector<int64_t> sh = g.tensors[p_t].shape;  // [(B1,) H, M, nk], chunk-reduced inside a region
     const int r = region_index(plan, c.softmax);
@@ -297,7 +291,7 @@ Arena build_arena(const Graph& g, const Plan& plan) {
     int64_t B = 1;
     for (size_t d = 0; d + 2 < sh.size(); ++d) B *= sh[d];
     const int64_t M = sh[sh.size() - 2], nk = sh.back();
-    bytes[p_t] = f2_layout(B, M, nk, pv_splitk(g.nodes[c.scores].ai("causal") != 0, nk)).total;
+    bytes[p_t] = f2_layout(B, M, nk, pv_splitk(o, g.nodes[c.scores].ai("causal") != 0, nk)).total;
     bytes[s_t] = etile_bytes(B, M, nk);
     birth[p_t] = std::min(birth[p_t], c.scores);
     death[s_t] = std::max(death[s_t], c.pv);
@@ -334,21 +328,15 @@ Arena build_arena(const Graph& g, const Plan& plan) {
   A.ctrl_b.assign(S, 0);
   A.ctrl_n.assign(S, 0);
   A.ctrl_mt.assign(S, 0);
-  if (overlap_enabled()) {
-    for (const Chain& c : fused_chains(g, plan)) {
+  if (o.overlap) {
+    for (const Chain& c : fused_chains(g, plan, o)) {
       const int r = region_index(plan, c.scores);
       if (r < 0) continue;
       // triangle chains: measured slower with the overlap (AF 15.8 -> 18.1 ms: the
       // paired short-chunk scores lose more to dynamic tiles than the overlap saves),
       // so only on request (AC_OVERLAP_TRI=1)
-      if (g.nodes[c.scores].kind == "tri_scores" && !(getenv("AC_OVERLAP_TRI") && getenv("AC_OVERLAP_TRI")[0] == '1'))
-        continue;
-      // causal chains: heaviest-first whole tiles leave the PV little tail to fill, and
-      // the overlap (with the chain's programmatic launches) measured 1.3 % slower than
-      // plain stream order (GPT 2.649 vs 2.614 ms; UNet, non-causal, gains 7 %), so
-      // only on request (AC_OVERLAP_CAUSAL=1)
-      if (causal_chain(g, c.scores) && !(getenv("AC_OVERLAP_CAUSAL") && getenv("AC_OVERLAP_CAUSAL")[0] == '1'))
-        continue;
+      if (g.nodes[c.scores].kind == "tri_scores" && !o.overlap_tri) continue;
+      if (causal_chain(g, c.scores) && !o.overlap_causal) continue;
       // the region must be exactly the chain, so that in the chunk loop the PV of
       // chunk k is the launch right before the scores of chunk k + 1 (whose inputs
       // then all predate the region)
@@ -436,11 +424,6 @@ bool chain_ctrl(const ac_exec* e, int node, const NodeCtx& cx) {
   return h >= 0 && e->arena.ctrl_off[h] >= 0 && cx.chunk >= 0;
 }
 
-bool g_kind_is(const ac_exec* e, int node, const char* k1, const char* k2) {
-  const std::string& k = e->g->nodes[node].kind;
-  return k == k1 || k == k2;
-}
-
 void chain_overlap(const ac_exec* e, int node, const NodeCtx& cx, GemmProblem& p) {
   const int h = e->fuse_head[node];
   const int64_t off = h >= 0 ? e->arena.ctrl_off[h] : -1;
@@ -449,41 +432,25 @@ void chain_overlap(const ac_exec* e, int node, const NodeCtx& cx, GemmProblem& p
   int* c = reinterpret_cast<int*>(e->ws + off);
   const int k = cx.chunk;
   p.done_epoch = c;
-  const bool conc = conc_enabled() && e->fuse_online[node] && g_kind_is(e, node, "attn_scores", "attn_pv");
-  int* sdone = c + B + 2 * n + n * B;
   if (e->fuse_role[node] == 1) {
     p.pdl = k > 0 ? 1 : 0;
     p.pdl_wait = 0;  // ordered by the per-batch epochs instead (the PV of chunk k - 1 is still draining)
     p.dep_epoch = k;
     p.tsched = c + B + k;
-    if (conc) {
-      p.pub_epoch = sdone;
-      p.pub_cnt = sdone + B + static_cast<int64_t>(k) * B;
-      p.epoch = k;
-      p.max_ctas = conc_scores_ctas();
-    }
   } else {
-    // the PV itself is launched in plain stream order (a PDL-launched PV measured slower:
-    // UNet 2.803 -> 2.781 ms without; AC_OVPV_PDL=1 restores it); it still triggers the
-    // next chunk's scores early.  Concurrent mode needs PDL (no grid dependency).
-    p.pdl = conc || (getenv("AC_OVPV_PDL") && getenv("AC_OVPV_PDL")[0] == '1') ? 1 : 0;
-    p.pdl_wait = conc && !getenv("AC_CONC_GRIDWAIT") ? 0 : 1;  // concurrent: per-batch flags of this chunk's scores instead
+    // the PV itself is launched in plain stream order (a PDL-launched PV measured
+    // slower: UNet 2.803 vs 2.781 ms); it still triggers the next chunk's scores early
+    p.pdl = 0;
+    p.pdl_wait = 1;
     p.sched = c + B + n + k;
     p.done_cnt = c + B + 2 * n + static_cast<int64_t>(k) * B;
     p.epoch = k;
-    if (p.sk_cnt) p.sk_cnt = c + 2 * B + 2 * n + 2 * n * B;  // (the P buffer's move with the chunk length)
-    if (conc) {
-      p.wait_epoch = sdone;
-      // AC_CONC_P: PV grid (default: the SMs the scores leave free, so the next chunk's
-      // scores take their SMs back as soon as this chunk's scores end)
-      const char* v = getenv("AC_CONC_P");
-      p.max_ctas = v ? atoi(v) : std::max(1, num_sms() - conc_scores_ctas());
-    }
+    if (p.sk_cnt) p.sk_cnt = c + B + 2 * n + n * B;  // (the P buffer's move with the chunk length)
   }
 }
 
 ac_status launch_node(const ac_exec* e, int i, const std::vector<View>& V, const NodeCtx& cx, cudaStream_t s) {
-  if (e->fuse_role[i] == 2 && e->fuse_online[i]) return AC_OK;  // folded into the PV: no launch, no timing entry
+  if (e->fuse_role[i] == 2) return AC_OK;  // folded into the PV: no launch, no timing entry
   if (!e->profiling) return launch_node_impl(e, i, V, cx, s);
   const size_t k = e->ev_node.size();
   while (e->ev_pool.size() < 2 * (k + 1)) {
@@ -501,7 +468,7 @@ ac_status launch_node(const ac_exec* e, int i, const std::vector<View>& V, const
 ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, const NodeCtx& cx, cudaStream_t s) {
   const Graph& g = *e->g;
   const Node& n = g.nodes[i];
-  if (e->fuse_role[i] == 2 && e->fuse_online[i]) return AC_OK;  // folded into the PV (no launch)
+  if (e->fuse_role[i] == 2) return AC_OK;  // folded into the PV (no launch)
   const int dtc = e->dt == DT::BF16 ? 1 : 0;
   auto in = [&](int k) -> const View& { return V[n.inputs[k]]; };
   const View& out = V[n.output];
@@ -517,17 +484,6 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
     if (collapse(x, 0, x.nd) != 1 || collapse(out, 0, out.nd) != 1) return unsup("non-contiguous rows");
     err = layernorm(x.p, in(1).p, in(2).p, out.p, extent(x, 0, x.nd - na), static_cast<int>(C),
                     static_cast<float>(n.af("eps", 1e-5)), dtc, s, cx.pdl);
-  } else if (k == "softmax" && e->fuse_role[i] == 2) {
-    // fused chain: the softmax node only combines the slab statistics the scores
-    // step left in P's buffer into per-slab factors; the PV applies them
-    const View& x = in(0);  // S view [(B1,) H, M, Nk] of this launch
-    const int64_t B = extent(x, 0, x.nd - 2), M = x.sh[x.nd - 2], nk = x.sh[x.nd - 1];
-    const int64_t ns = (nk + 63) / 64;
-    const F2Layout L = f2_layout(B, M, nk, e->fuse_split[i] != 0);
-    err = softmax_stats_combine(reinterpret_cast<float2*>(out.p), B, M, static_cast<int>(ns),
-                                M * ns, M, cx.fast ? 1 : 0, cx.row_off,
-                                reinterpret_cast<float2*>(out.p + L.rowst), reinterpret_cast<int*>(out.p + L.cnt),
-                                L.ncnt, s, cx.pdl || (cx.chunk >= 0 && e->arena.ctrl_off[e->fuse_head[i]] >= 0) ? 1 : 0);
   } else if (k == "softmax") {
     const View& x = in(0);
     if (n.ai("dim") != x.nd - 1 || x.st[x.nd - 1] != 1) return unsup("softmax over a non-last dim");
@@ -683,14 +639,13 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         const int64_t ns = (p.N + 63) / 64;
         ep.stats = reinterpret_cast<float2*>(V[e->fuse_p[i]].p);
         p.etile = out.p;
-        ep.stats_ss = p.M;
-        ep.stats_sb1 = static_cast<int64_t>(p.M) * ns;
+        ep.stats_ss = e->fuse_malloc[i];
+        ep.stats_sb1 = e->fuse_malloc[i] * ns;
         chain_overlap(e, i, cx, p);
-        if (e->fuse_online[i]) {  // no combine step to reset the PV's counters
-          const F2Layout L = f2_layout(p.B1, p.M, p.N, e->fuse_split[i] != 0);
-          p.zero_word = reinterpret_cast<int*>(V[e->fuse_p[i]].p + L.cnt);
-          p.zero_n = chain_ctrl(e, i, cx) ? 1 : static_cast<int>(L.ncnt);  // (overlap: split counters in the control block)
-        }
+        // the scores reset the PV's counters (overlap: its split counters are in the control block)
+        const F2Layout L = f2_layout(e->fuse_balloc[i], e->fuse_malloc[i], p.N, e->fuse_split[i] != 0);
+        p.zero_word = reinterpret_cast<int*>(V[e->fuse_p[i]].p + L.cnt);
+        p.zero_n = chain_ctrl(e, i, cx) ? 1 : static_cast<int>(L.ncnt);
       }
     } else if (k == "attn_pv") {
       // fused chain: A is the raw scores S, normalised in shared memory with the
@@ -712,18 +667,16 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
       if (fz) {
         const int64_t ns = (p.K + 63) / 64;
         p.fuse_stats = reinterpret_cast<const float2*>(in(0).p);
-        p.fuse_ss = p.M;
-        p.fuse_sb1 = static_cast<int64_t>(p.M) * ns;
-        const F2Layout L = f2_layout(p.B1, p.M, p.K, e->fuse_split[i] != 0);
+        p.fuse_ss = e->fuse_malloc[i];
+        p.fuse_sb1 = e->fuse_malloc[i] * ns;
+        const F2Layout L = f2_layout(e->fuse_balloc[i], e->fuse_malloc[i], p.K, e->fuse_split[i] != 0);
         p.etile = pp.p;
         p.sched = reinterpret_cast<int*>(in(0).p + L.cnt);
-        p.fuse_rowst = reinterpret_cast<const float2*>(in(0).p + L.rowst);
-        p.pv_rowstats = e->fuse_online[i];
         if (L.ncnt > 1) {
           p.sk_gk = static_cast<int>(sk_gk(p.K));
           p.sk_part = reinterpret_cast<float*>(in(0).p + L.part);
           p.sk_cnt = reinterpret_cast<int*>(in(0).p + L.cnt) + 1;
-          if (p.pv_rowstats) p.sk_ml = in(0).p + L.ml;
+          p.sk_ml = in(0).p + L.ml;
         }
         chain_overlap(e, i, cx, p);
       }
@@ -760,14 +713,12 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         const int64_t ns = (p.N + 63) / 64;
         ep.stats = reinterpret_cast<float2*>(V[e->fuse_p[i]].p);
         p.etile = out.p;
-        ep.stats_ss = p.M;
-        ep.stats_sb1 = static_cast<int64_t>(p.M) * ns;
+        ep.stats_ss = e->fuse_malloc[i];
+        ep.stats_sb1 = e->fuse_malloc[i] * ns;
         chain_overlap(e, i, cx, p);
-        if (e->fuse_online[i]) {
-          const F2Layout L = f2_layout(static_cast<int64_t>(p.B1) * p.B2, p.M, p.N, e->fuse_split[i] != 0);
-          p.zero_word = reinterpret_cast<int*>(V[e->fuse_p[i]].p + L.cnt);
-          p.zero_n = chain_ctrl(e, i, cx) ? 1 : static_cast<int>(L.ncnt);
-        }
+        const F2Layout L = f2_layout(e->fuse_balloc[i], e->fuse_malloc[i], p.N, e->fuse_split[i] != 0);
+        p.zero_word = reinterpret_cast<int*>(V[e->fuse_p[i]].p + L.cnt);
+        p.zero_n = chain_ctrl(e, i, cx) ? 1 : static_cast<int>(L.ncnt);
       }
     } else if (k == "tri_pv") {
       const bool fz = e->fuse_role[i] == 3;
@@ -793,18 +744,16 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
       if (fz) {
         const int64_t Bt = static_cast<int64_t>(p.B1) * p.B2, ns = (p.K + 63) / 64;
         p.fuse_stats = reinterpret_cast<const float2*>(in(0).p);
-        p.fuse_ss = p.M;
-        p.fuse_sb1 = static_cast<int64_t>(p.M) * ns;
-        const F2Layout L = f2_layout(Bt, p.M, p.K, e->fuse_split[i] != 0);
+        p.fuse_ss = e->fuse_malloc[i];
+        p.fuse_sb1 = e->fuse_malloc[i] * ns;
+        const F2Layout L = f2_layout(e->fuse_balloc[i], e->fuse_malloc[i], p.K, e->fuse_split[i] != 0);
         p.etile = pp.p;
         p.sched = reinterpret_cast<int*>(in(0).p + L.cnt);
-        p.fuse_rowst = reinterpret_cast<const float2*>(in(0).p + L.rowst);
-        p.pv_rowstats = e->fuse_online[i];
         if (L.ncnt > 1) {
           p.sk_gk = static_cast<int>(sk_gk(p.K));
           p.sk_part = reinterpret_cast<float*>(in(0).p + L.part);
           p.sk_cnt = reinterpret_cast<int*>(in(0).p + L.cnt) + 1;
-          if (p.pv_rowstats) p.sk_ml = in(0).p + L.ml;
+          p.sk_ml = in(0).p + L.ml;
         }
         chain_overlap(e, i, cx, p);
       }
@@ -838,7 +787,7 @@ int64_t ac_plan_workspace_bytes(const ac_chunk_plan* p, int32_t rank, int32_t wo
     set_error(AC_ERR_ARG, "ac_plan_workspace_bytes: bad arguments");
     return -1;
   }
-  return build_arena(*p->g, p->plan).size;
+  return build_arena(*p->g, p->plan, read_options()).size;
 }
 
 ac_status ac_plan_rank_chunks(const ac_chunk_plan* p, int32_t region, int32_t rank, int32_t world, int64_t* c0,
@@ -862,7 +811,8 @@ ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_
   std::unique_ptr<ac_exec> e(new ac_exec);
   e->g = plan->g;
   e->plan = plan->plan;
-  e->arena = build_arena(g, plan->plan);
+  e->opt = read_options();
+  e->arena = build_arena(g, plan->plan, e->opt);
   if (ws_bytes < e->arena.size || (e->arena.size > 0 && !workspace))
     return set_error(AC_ERR_WORKSPACE, "workspace of " + std::to_string(ws_bytes) + " bytes < required " +
                                            std::to_string(e->arena.size));
@@ -922,25 +872,40 @@ ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_
   }
   for (int i = 0; i < S; ++i) e->chain_rows_dim[i] = rows_dim(g.nodes[i]);
   e->fuse_role.assign(S, 0);
-  e->fuse_online.assign(S, 0);
   e->fuse_s.assign(S, -1);
   e->fuse_p.assign(S, -1);
   e->fuse_split.assign(S, 0);
   e->fuse_head.assign(S, -1);
+  e->fuse_balloc.assign(S, 0);
+  e->fuse_malloc.assign(S, 0);
   if (e->dt == DT::BF16) {
-    for (const Chain& c : fused_chains(g, e->plan)) {
+    for (const Chain& c : fused_chains(g, e->plan, e->opt)) {
       e->fuse_role[c.scores] = 1;
       e->fuse_role[c.softmax] = 2;
       e->fuse_role[c.pv] = 3;
       const int s_t = g.nodes[c.scores].output, p_t = g.nodes[c.softmax].output;
       const bool split =
-          pv_splitk(g.nodes[c.scores].ai("causal") != 0, g.tensors[g.nodes[c.softmax].output].shape.back());
+          pv_splitk(e->opt, g.nodes[c.scores].ai("causal") != 0, g.tensors[g.nodes[c.softmax].output].shape.back());
+      // the P buffer's layout (slab statistics, partials, counters) is fixed by the
+      // ALLOCATED batch count and rows (the chunk-reduced S shape), not by each
+      // launch's: a ragged last chunk then never shifts batch b's statistics onto
+      // batch b-1's, which the previous chunk's PV may still be reading under the
+      // chunk-loop overlap (per-batch epochs)
+      std::vector<int64_t> sh = g.tensors[s_t].shape;
+      const int r = region_index(e->plan, c.scores);
+      if (r >= 0) {
+        const int d = e->plan.regions[r].dim_of(s_t);
+        if (d >= 0) sh[d] = e->plan.regions[r].chunk_len();
+      }
+      int64_t Ba = 1;
+      for (size_t d = 0; d + 2 < sh.size(); ++d) Ba *= sh[d];
       for (int node : {c.scores, c.softmax, c.pv}) {
         e->fuse_s[node] = s_t;
         e->fuse_p[node] = p_t;
         e->fuse_split[node] = split ? 1 : 0;
-        e->fuse_online[node] = pv_online_enabled() ? 1 : 0;
         e->fuse_head[node] = c.scores;
+        e->fuse_balloc[node] = Ba;
+        e->fuse_malloc[node] = sh[sh.size() - 2];
       }
     }
   }
@@ -1047,7 +1012,7 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
   int i = 0;
   // launches outside chunk loops (GEMMs, LayerNorm, fused attention) after a kernel of
   // this run overlap their prologue with its tail too (AC_PDL=0 off)
-  const bool run_pdl = pdl_enabled() && !(getenv("AC_PDL_OUTSIDE") && getenv("AC_PDL_OUTSIDE")[0] == '0');
+  const bool run_pdl = e->opt.pdl;
   int prev_kernel = 0;  // 1: the previous stream operation of this run was one of our kernels
   while (i < S) {
     const Node& n = g.nodes[i];
@@ -1094,7 +1059,7 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
       }
     }
     bool first_launch = true;
-    const bool loop_pdl = pdl_enabled();
+    const bool loop_pdl = e->opt.pdl;
     for (int64_t c = c0; c < c1; ++c) {
       const int64_t off = c * L;
       const int64_t len = std::min(L, R.extent - off);
@@ -1149,17 +1114,11 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
         // every launch of the chunk loop but the first may start during its
         // predecessor's tail (it waits in-kernel before touching data); AC_PDL=0 off
         cx.pdl = loop_pdl && !first_launch ? 1 : 0;
-        // (causal f2 chains without the overlap run in plain stream order, see build_arena)
+        // causal f2 chains without the overlap: PDL on the chain's scores only (their
+        // prologue overlaps the previous PV's tail; a PDL-launched PV measured slower)
         if (e->fuse_head[j] >= 0 && e->arena.ctrl_off[e->fuse_head[j]] < 0 && causal_chain(g, e->fuse_head[j]) &&
-            !(getenv("AC_OVERLAP_CAUSAL") && getenv("AC_OVERLAP_CAUSAL")[0] == '1')) {
-          // AC_PDL_CHAIN: bit 1 = PDL on the chain's scores, bit 2 = on its PV.  Default 1:
-          // the scores' prologue overlaps the previous PV's tail (GPT 2.605 -> 2.599 ms), a
-          // PDL-launched PV measured slower (both: 2.615 ms)
-          const char* pc = getenv("AC_PDL_CHAIN");
-          const int bits = pc ? atoi(pc) : 1;
-          const int role = e->fuse_role[j];
-          if (!((role == 1 && (bits & 1)) || (role == 3 && (bits & 2)))) cx.pdl = 0;
-        }
+            e->fuse_role[j] != 1)
+          cx.pdl = 0;
         first_launch = false;
         const int d = R.dim_of(nj.output);
         if (d >= 0 && d == e->chain_rows_dim[j]) cx.row_off = off;

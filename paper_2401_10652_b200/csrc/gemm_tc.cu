@@ -30,13 +30,6 @@ namespace ac {
 
 namespace {
 
-// f2 PV: post-scale (default: e tiles straight to the tensor core, f_slab applied to
-// each k-block's product in registers) or the pre-scale transform of e in shared
-// memory (AC_PV_POSTSCALE=0 at build time)
-#ifndef AC_PV_POSTSCALE
-#define AC_PV_POSTSCALE 1
-#endif
-
 // f2 scores: exponentials as packed bf16x2 ex2 (one instruction per pair) instead
 // of fp32 ex2 + pack.  Measured slower on B200 (GPT scores 0.94 -> 1.04 ms), so off.
 #ifndef AC_EX2_PACKED
@@ -68,7 +61,6 @@ struct alignas(64) GemmArgs {
   int lean; // TMA-store epilogue without aux tensors / activation (scale and causal only)
   int fuse; // fused softmax-normalised A operand (PV of the f2 path)
   const float2* fstats;
-  const float2* frow;  // MODE 2: (M, 1/L) per (b1, row)
   long long fst_sb1, fst_ss;
   // MODE 2 fixed split-K: K cut into granules of skgk k-blocks at fixed key
   // positions; one work unit per (tile, granule); multi-granule tiles leave fp32
@@ -76,9 +68,7 @@ struct alignas(64) GemmArgs {
   int skgk, skng;
   float* skpart;
   int* skcnt;
-  float2* skml;  // online fold with split-K: per (unit, row) the granule's running (max, sum)
-  int dbg;  // experiments (AC_DBG): bit0 = MODE 2 transform skipped, 8 = post-scale TMEM reads skipped,
-            // 16 / 32 = no L2 evict-first hint on the e-tile loads / stores
+  float2* skml;  // split-K: per (unit, row) the granule's running (max, sum)
   int* sched;  // MODE 2: zero-initialised work counter for dynamic unit scheduling (null = round-robin)
   unsigned long long* trace;  // debug (AC_TRACE): per unit {cta, t_load0, t_tfull, t_done}
   char* etile;  // f2 pre-swizzled e tiles (GemmProblem::etile), null = tensor path
@@ -90,16 +80,8 @@ struct alignas(64) GemmArgs {
   int epoch, dep_epoch;
   int* tsched;  // MODE 1 / 3 dynamic tile counter
   int pair;     // MODE 2, BN = 32, M <= 64: work units are pairs of batches (two M = 64 MMAs)
-  int postscale;  // MODE 2: e tiles straight to the MMA (one TMEM buffer per k-block), f applied after
-  int pv_rowstats;  // MODE 2: fold each row's (M, 1/L) from the slab statistics in-kernel (no combine step)
-  int* zero_word;   // MODE 1 / 3 / 4: zero_n words zeroed at kernel start (the PV's counters when no combine runs)
+  int* zero_word;   // MODE 1 / 3 / 4: zero_n words zeroed at kernel start (the PV's counters)
   int zero_n;
-  // concurrent scores / PV of one chunk (AC_CONC): the scores count finished warp-slabs
-  // per batch (pub_cnt) and release pub_epoch[b] = epoch + 1 when batch b is complete;
-  // the PV waits for wait_epoch[b] >= epoch + 1 before reading batch b
-  int* pub_cnt;
-  int* pub_epoch;
-  int* wait_epoch;
 };
 
 // epilogue staging: per epilogue warp a [32 rows][PITCH] fp32 slab; PITCH = 68
@@ -111,17 +93,20 @@ struct Cfg {
   // f2 scores (MODE 1): 16 epilogue warps (one 64-column slab each at BN = 256,
   // <= 112 registers) with a single 4 KB bf16 staging box per warp; K = head dim
   // is one or two k-blocks, so two smem stages suffice
-  static constexpr bool PS = MODE == 2 && AC_PV_POSTSCALE;  // post-scale PV: 4 scale/output warps
   // f2 scores at BN = 128: 8 epilogue warps (one 64-column slab each) and two CTAs
   // per SM, whose tiles run out of phase (one CTA's max pass beside the other's
   // exponentials)
   static constexpr bool DUAL = MODE == 1 && BN == 128;
-  static constexpr int EPI = DUAL ? 8 : (MODE == 1 || MODE == 3 || MODE == 4) ? 16 : PS ? 4 : EPI_WARPS;
+  static constexpr int EPI = DUAL ? 8 : (MODE == 1 || MODE == 3 || MODE == 4) ? 16 : MODE == 2 ? 4 : EPI_WARPS;
   static constexpr int MINB = DUAL ? 2 : 1;
-  // f2 PV (MODE 2): the EPI warps transform A tiles; XEPI more warps (one per
-  // TMEM lane quarter) run the output epilogue so the transform never stalls
-  static constexpr int XEPI = MODE == 2 && !PS ? 4 : 0;
+  // f2 PV (MODE 2): producer, MMA, EPI = 4 scale warps (one per TMEM lane quarter)
+  // and XEPI = 4 finish warps that take each unit's end (output epilogue, split-K
+  // partials and merge) off them: 320 threads, <= 204 registers each
+  static constexpr int XEPI = MODE == 2 ? 4 : 0;
   static constexpr int THREADS = 64 + 32 * (EPI + XEPI);
+  // MODE 2: KBUF per-k-block TMEM accumulators of BN columns + one BN-column staging
+  // buffer for the hand-over to the finish warps
+  static constexpr int KBUF = MODE == 2 && BN == 64 ? 7 : 8;
   // f2 PV (MODE 2) stages no output in smem: its ring is 8 deep (one CTA must keep
   // ~8 x 24 KB of A/B tiles in flight to stream at full speed when few CTAs remain)
   static constexpr int EPI_BYTES = (MODE == 1 || MODE == 3 || MODE == 4) ? EPI * 4096 : MODE == 2 ? 0 : EPI_WARPS * 32 * PITCH * 4;
@@ -133,11 +118,10 @@ struct Cfg {
   static constexpr int B_TILE = BN * BK * 2;
   static constexpr int B_BYTES = (MODE == 4 || (MODE == 2 && BN == 32) ? 2 : 1) * B_TILE;
   static constexpr int SW = BN >= 64 ? 64 : 32;  // epilogue slab width (columns)
-  // MODE 2 post-scale PV: 8 per-k-block accumulator buffers of BN columns
-  static constexpr int TMEM_COLS = MODE == 2 ? (8 * BN <= 256 ? 256 : 512)
+  static constexpr int TMEM_COLS = MODE == 2 ? 512
                                              : (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
   static constexpr int SMEM = 1024 /*align slack*/ + STAGES * (A_BYTES + B_BYTES) + EPI_BYTES + 512 /*barriers*/ +
-                              (MODE == 4 ? 0 : (MAX_MT + 1) * 4 + 16 + (MODE == 3 || MODE == 2 ? 16 * 8 + 8 : 0));
+                              (MODE == 4 ? 0 : (MAX_MT + 1) * 4 + 16 + (MODE == 3 ? 16 * 8 + 8 : MODE == 2 ? 18 * 8 + 8 + 128 * 8 : 0));
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
@@ -278,6 +262,26 @@ __device__ __forceinline__ void decode_unit(const GemmArgs& a, const int* prefix
   unit0 = u - g;
 }
 
+// one MODE 2 work unit as seen by the thread owning TMEM lane (quarter, lane): its
+// output row m (pairs: lanes 0-15 the pair's first batch, 16-31 its second) and batch
+struct PvUnit {
+  int b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0, m;
+  bool mv;
+  long long bb;
+};
+__device__ __forceinline__ void pv_unit(const GemmArgs& a, const int* prefix, int upb, int t, int quarter, int lane,
+                                        PvUnit& u) {
+  decode_unit(a, prefix, upb, t, u.b1, u.b2, u.mt, u.kbn, u.klo, u.khi, u.g, u.ng, u.tile, u.unit0);
+  u.m = a.pair ? quarter * 16 + (lane & 15) : u.mt * BM + quarter * 32 + lane;
+  if (a.pair && lane >= 16) {
+    const int nb = u.b1 * a.B2 + u.b2 + 1;
+    u.b1 = nb / a.B2;
+    u.b2 = nb - u.b1 * a.B2;
+  }
+  u.mv = u.m < a.M && u.b1 < a.B1;
+  u.bb = static_cast<long long>(u.b1) * a.B2 + u.b2;
+}
+
 // MODE: 0 generic; 1 f2 scores (QK^T -> e = exp(s - m_slab) + slab statistics,
 // lean TMA-store epilogue only); 2 f2 PV (A tile e rescaled to P in shared
 // memory by all epilogue warps, which also run the output epilogue)
@@ -390,8 +394,8 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
     for (int s = 0; s < C::STAGES; ++s) ptx::mbar_init(&ready[s], 32 * C::EPI);
     if (MODE == 3 || MODE == 4)
       for (int w = 0; w < C::EPI; ++w) ptx::mbar_init(&bbar[w], 1);
-    if (MODE == 2)  // post-scale PV: kfull[8] (MMA commit), kempty[8] (4 scale warps)
-      for (int w = 0; w < 16; ++w) ptx::mbar_init(&bbar[w], w < 8 ? 1 : 4);
+    if (MODE == 2)  // PV: kfull[8] (MMA commit), kempty[8] (4 scale warps), sfull, sempty (4 warps each)
+      for (int w = 0; w < 18; ++w) ptx::mbar_init(&bbar[w], w < 8 ? 1 : 4);
     for (int s = 0; s < 4; ++s) {
       ptx::mbar_init(&uq_full[s], 1);
       ptx::mbar_init(&uq_empty[s], 1 + C::EPI + C::XEPI);
@@ -413,6 +417,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
   // next kernel of the chunk loop be scheduled as SMs free up
   if (a.pdl_wait) ptx::griddep_wait();
   ptx::griddep_launch();
+
   if ((MODE == 1 || MODE == 3 || MODE == 4) && a.zero_word && blockIdx.x == 0)
     for (int z = threadIdx.x; z < a.zero_n; z += C::THREADS) a.zero_word[z] = 0;
   // unit sequence of this CTA: i-th unit (static round-robin, or the MODE 2 queue)
@@ -475,22 +480,12 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
       int stage = 0;
       uint32_t phase = 0;
       TileWalk walk;
-      int ok_b = -1;  // concurrent scores: last batch known complete
       const uint64_t epol = ptx::policy_evict_first();
       for (int i = 0, t = produce(0); t < total; t = produce(++i)) {
         int b1, b2, mt, nt = 0, kbn, klo, khi;
         if constexpr (MODE == 2) {
           int g, ng, tile, unit0;
           decode_unit(a, prefix, tpb, t, b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0);
-          const int bb = b1 * a.B2 + b2;
-          if (a.wait_epoch && bb != ok_b) {
-            // the scores of this chunk run beside this kernel: batch bb's e-tiles and
-            // statistics are complete once they publish epoch + 1 for it
-            ptx::wait_geq_gpu(a.wait_epoch + bb, a.epoch + 1);
-            if (a.pair && bb + 1 < a.B1 * a.B2) ptx::wait_geq_gpu(a.wait_epoch + bb + 1, a.epoch + 1);
-            ptx::fence_proxy_async_global();
-            ok_b = bb;
-          }
         } else {
           walk.next(a, prefix, tpb, t, ncl);
           walk.get(a, b1, b2, mt, nt, kbn);
@@ -524,11 +519,9 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::mbar_expect_tx(&full[stage], (two ? 2 : 1) * (ebytes + C::B_TILE));
           if (MODE == 2 && esrc) {
-            if (!(a.dbg & 16))  // e-tiles are read once: L2 evict-first (AC_DBG bit 16 turns it off)
-              ptx::bulk_load_hint(sA + stage * C::A_BYTES, esrc + static_cast<long long>(kb) * 16384, ebytes,
-                                  &full[stage], epol);
-            else
-              ptx::bulk_load(sA + stage * C::A_BYTES, esrc + static_cast<long long>(kb) * 16384, ebytes, &full[stage]);
+            // e-tiles are read once: L2 evict-first
+            ptx::bulk_load_hint(sA + stage * C::A_BYTES, esrc + static_cast<long long>(kb) * 16384, ebytes,
+                                &full[stage], epol);
           }
           else
             ptx::tma_load_4d(sA + stage * C::A_BYTES, &a.ta, &full[stage], kb * BK, mt * BM, ac2, ac3);
@@ -596,7 +589,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
         klo = kbn * static_cast<int>(crank) / ks;
         khi = kbn * (static_cast<int>(crank) + 1) / ks;
       }
-      if (MODE == 2 && a.postscale) {
+      if constexpr (MODE == 2) {
         // post-scale PV: every k-block gets its own TMEM buffer (kb-th of 8, round
         // robin), accumulate = 0; the scale warps fold f_slab * (e V) into registers
         uint64_t* kfull = bbar;
@@ -627,7 +620,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
           }
           __syncwarp();
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
-          if (++kbuf == 8) { kbuf = 0; kphase ^= 1; }
+          if (++kbuf == C::KBUF) { kbuf = 0; kphase ^= 1; }
         }
         continue;
       }
@@ -653,8 +646,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
           } else {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
-              if (MODE != 2 || !(a.dbg & 4))
-                ptx::mma_bf16(d, ptx::sdesc_sw128(sa + k * 32), ptx::sdesc_sw128(sb + k * 32), IDESC,
+              ptx::mma_bf16(d, ptx::sdesc_sw128(sa + k * 32), ptx::sdesc_sw128(sb + k * 32), IDESC,
                               (kb != klo || k != 0) ? 1u : 0u);
             }
           }
@@ -684,426 +676,239 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
     uint32_t aphase = 0;
     uint32_t bphase = 0;  // MODE 3 bias-box barrier phase
     bool bias_pending = false;  // MODE 3: this warp's next bias box is already in flight
-    // MODE 1, concurrent PV (lane 0): this warp's finished slabs of the current batch are
-    // counted locally (tiles are batch-major); when the warp moves to another batch the
-    // count is deferred and added to the batch's total once a later store has been
-    // issued and the deferred ones have landed (bulk wait_group 1, normally already
-    // true), or at exit; the add that completes a batch (4 quarters x NSLAB slabs per
-    // tile) releases its epoch
-    int cur_b = -1, cur_n = 0, def_b = -1, def_n = 0, def_after = 0;
-    auto pub_add = [&](int b, int n) {
-      ptx::fence_proxy_async_global();
-      if (ptx::atom_add_acqrel_gpu(a.pub_cnt + b, n) + n == 4 * NSLAB * tpb) ptx::st_release_gpu(a.pub_epoch + b, a.epoch + 1);
-    };
-    auto pub_slab = [&](int b) {  // lane 0, before the slab's own work
-      if (def_b >= 0 && def_after > 0) {
-        ptx::bulk_wait<1>();
-        pub_add(def_b, def_n);
-        def_b = -1;
-      }
-      if (b != cur_b) {
-        if (def_b >= 0) {
-          ptx::bulk_wait<0>();
-          pub_add(def_b, def_n);
-        }
-        def_b = cur_b;
-        def_n = cur_n;
-        def_after = 0;
-        cur_b = b;
-        cur_n = 0;
-      }
-    };
-    auto pub_flush = [&]() {
-      ptx::bulk_wait<0>();
-      if (def_b >= 0) pub_add(def_b, def_n);
-      if (cur_b >= 0) pub_add(cur_b, cur_n);
-    };
     uint32_t pf_phase = 0, pe_phase = 0;  // split-K barrier phases
     if constexpr (MODE == 2) {
-      if (a.postscale) {
-        if (ew < 4) {
-          // ---- post-scale f2 PV (default): the e tiles went to the tensor core
-          // unscaled, one k-block (= one 64-key slab) per TMEM buffer; thread = output
-          // row: O += f_slab * (e_slab V_slab) in fp32 registers with
-          // f_slab = 2^(m2_slab - M) / L (R19), then the output epilogue / split-K
-          uint64_t* kfull = bbar;
-          uint64_t* kempty = bbar + 8;
-          const bool lead = ew == 0;
-          const int r = quarter * 32 + lane;
-          int* sk_old = prefix + MAX_MT + 1;
-          int kbuf = 0;
-          uint32_t kphase = 0;
-          for (int i = 0, t = take(0); t < total; t = take(++i)) {
-            int b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0;
-            decode_unit(a, prefix, tpb, t, b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0);
-            // pairs: TMEM lanes 0-15 of each subpartition = the first batch's rows
-            // quarter*16.., lanes 16-31 the second batch's
-            const int m = a.pair ? quarter * 16 + (lane & 15) : mt * BM + r;
-            if (a.pair && lane >= 16) {
-              const int nb = b1 * a.B2 + b2 + 1;
-              b1 = nb / a.B2;
-              b2 = nb - b1 * a.B2;
-            }
-            const bool mv = m < a.M && b1 < a.B1;
-            const long long bb = static_cast<long long>(b1) * a.B2 + b2;
-            const float* fp = reinterpret_cast<const float*>(a.fstats + (mv ? bb * a.fst_sb1 + m : 0));
-            const long long fs = 2 * a.fst_ss;
-            const bool conc = a.wait_epoch != nullptr;
-            if (conc && mv) ptx::wait_geq_gpu(a.wait_epoch + bb, a.epoch + 1);  // statistics complete
-            // (concurrent: written during this kernel, so through L2, not the read-only path)
-            auto ldst = [&](long long off) -> float2 {
-              const float2* q = reinterpret_cast<const float2*>(fp + off);
-              return conc ? __ldcg(q) : __ldg(q);
-            };
-            // pv_rowstats: the row's softmax normalisation (R19) is folded here, online in
-            // slab order (running max Mr, running sum Lr, O rescaled when Mr rises, 1/L at
-            // the end); otherwise (M, 1/L) come from the combine step
-            const bool online = a.pv_rowstats != 0;
-            const float2 rs = (mv && !online) ? __ldg(a.frow + bb * a.M + m) : make_float2(0.f, 0.f);
-            float Mr = -CUDART_INF_F, Lr = 0.f;
-            float accv[BN];
-#pragma unroll
-            for (int c = 0; c < BN; ++c) accv[c] = 0.f;
-            const float2 nost = make_float2(-CUDART_INF_F, 0.f);
-            float2 fr[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              fr[j] = (mv && klo + j < khi) ? ldst((klo + j) * fs) : nost;
-            for (int kb0 = klo; kb0 < khi; kb0 += 8) {
-              float2 nx[8];
-#pragma unroll
-              for (int j = 0; j < 8; ++j)
-                nx[j] = (mv && kb0 + 8 + j < khi) ? ldst((kb0 + 8 + j) * fs) : nost;
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                if (kb0 + j < khi) {
-                  // the slab's e V product: all BN columns in flight while f is formed
-                  ptx::mbar_wait(&kfull[kbuf], kphase);
-                  ptx::tc_fence_after();
-                  if (a.trace && lead && lane == 0 && kb0 == klo && j == 0) {
-                    unsigned long long tnow;
-                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
-                    a.trace[4 * t + 2] = tnow;
-                  }
-                  uint32_t v[BN];
-                  const bool skipld = a.dbg & 8;  // experiment: consumer cost without the TMEM reads
-#pragma unroll
-                  for (int hh = 0; hh < BN / 32; ++hh)
-                    if (!skipld) ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + kbuf * BN + hh * 32,
-                                   *reinterpret_cast<uint32_t(*)[32]>(&v[hh * 32]));
-                  float f;
-                  if (online) {
-                    if (fr[j].x > Mr) {
-                      const float cr = ptx::ex2(Mr - fr[j].x);  // first slab: 2^-inf = 0, O and L are 0
-                      Lr *= cr;
-#pragma unroll
-                      for (int c = 0; c < BN; ++c) accv[c] *= cr;
-                      Mr = fr[j].x;
-                    }
-                    f = fr[j].x == -CUDART_INF_F ? 0.f : ptx::ex2(fr[j].x - Mr);
-                    Lr = fmaf(fr[j].y, f, Lr);
-                  } else {
-                    f = ptx::ex2(fr[j].x - rs.x) * rs.y;  // empty slab: m2 = -inf, f = 0
-                  }
-                  if (!skipld) ptx::tmem_ld_wait();
-#pragma unroll
-                  for (int c = 0; c < BN; ++c) asm volatile("" : "+r"(v[c]));  // uses stay after the wait
-                  if (mv && !skipld) {
-#pragma unroll
-                    for (int c = 0; c < BN; ++c) accv[c] = fmaf(f, __uint_as_float(v[c]), accv[c]);
-                  }
-                  ptx::tc_fence_before();
-                  __syncwarp();
-                  if (lane == 0) ptx::mbar_arrive(&kempty[kbuf]);
-                  if (++kbuf == 8) { kbuf = 0; kphase ^= 1; }
-                }
-              }
-#pragma unroll
-              for (int j = 0; j < 8; ++j) fr[j] = nx[j];
-            }
-            if (a.trace && lead && lane == 0) {  // end of the unit's slab stream
-              unsigned long long tnow;
-              asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
-              a.trace[4 * t + 3] = tnow;
-            }
-            if (online && ng == 1) {
-              const float il = Lr > 0.f ? 1.f / Lr : 0.f;
-#pragma unroll
-              for (int c = 0; c < BN; ++c) accv[c] *= il;
-            }
-            auto publish = [&]() {
-              if (!a.done_cnt) return;
-              asm volatile("bar.sync 2, 128;" ::: "memory");
-              if (lead && lane == 0) {  // (lane 0: the pair's first batch; pairs count both)
-                const int nq = a.pair && bb + 1 < static_cast<long long>(a.B1) * a.B2 ? 2 : 1;
-                for (int q = 0; q < nq; ++q)
-                  if (ptx::atom_add_acqrel_gpu(a.done_cnt + bb + q, 1) == tpb - 1)
-                    ptx::st_release_gpu(a.done_epoch + bb + q, a.epoch + 1);
-              }
-            };
-            if (ng > 1) {
-              float* mine = a.skpart + (static_cast<long long>(unit0 + g) * BM + r) * BN;
-#pragma unroll
-              for (int q = 0; q < BN / 4; ++q)
-                reinterpret_cast<float4*>(mine)[q] = make_float4(accv[4 * q], accv[4 * q + 1], accv[4 * q + 2], accv[4 * q + 3]);
-              // online: this granule's O is relative to its own running max; keep (Mr, Lr)
-              if (online) a.skml[static_cast<long long>(unit0 + g) * BM + r] = make_float2(Mr, Lr);
-              __threadfence();
-              asm volatile("bar.sync 1, 128;" ::: "memory");
-              if (lead && lane == 0) *sk_old = atomicAdd(a.skcnt + tile, 1);
-              asm volatile("bar.sync 1, 128;" ::: "memory");
-              const int old = *sk_old;
-              asm volatile("bar.sync 1, 128;" ::: "memory");  // sk_old reusable
-              if (old != ng - 1) {
-                publish();
-                continue;
-              }
-              __threadfence();
-              const float4* base = reinterpret_cast<const float4*>(a.skpart + (static_cast<long long>(unit0) * BM + r) * BN);
-              if (online) {
-                // merge the granules in order: M = max M_g, O = sum 2^(M_g - M) O_g,
-                // L = sum 2^(M_g - M) L_g, o = O / L (granules of masked keys only: M_g = -inf)
-                const float2* ml = a.skml + static_cast<long long>(unit0) * BM + r;
-                float Mt = -CUDART_INF_F;
-                for (int gg = 0; gg < ng; ++gg) Mt = fmaxf(Mt, __ldcg(ml + static_cast<long long>(gg) * BM).x);
-#pragma unroll
-                for (int c = 0; c < BN; ++c) accv[c] = 0.f;
-                float Lt = 0.f;
-                for (int gg = 0; gg < ng; ++gg) {
-                  const float2 mg = __ldcg(ml + static_cast<long long>(gg) * BM);
-                  if (mg.x == -CUDART_INF_F) continue;
-                  const float w = ptx::ex2(mg.x - Mt);
-                  Lt = fmaf(mg.y, w, Lt);
-                  const float4* pp = base + static_cast<long long>(gg) * BM * BN / 4;
-#pragma unroll
-                  for (int q = 0; q < BN / 4; ++q) {
-                    const float4 v4 = __ldcg(pp + q);
-                    accv[4 * q] = fmaf(w, v4.x, accv[4 * q]); accv[4 * q + 1] = fmaf(w, v4.y, accv[4 * q + 1]);
-                    accv[4 * q + 2] = fmaf(w, v4.z, accv[4 * q + 2]); accv[4 * q + 3] = fmaf(w, v4.w, accv[4 * q + 3]);
-                  }
-                }
-                const float il = Lt > 0.f ? 1.f / Lt : 0.f;
-#pragma unroll
-                for (int c = 0; c < BN; ++c) accv[c] *= il;
-              } else {
-#pragma unroll
-                for (int q = 0; q < BN / 4; ++q) {
-                  const float4 w = __ldcg(base + q);
-                  accv[4 * q] = w.x; accv[4 * q + 1] = w.y; accv[4 * q + 2] = w.z; accv[4 * q + 3] = w.w;
-                }
-                for (int gg = 1; gg < ng; ++gg) {
-                  const float4* pp = base + static_cast<long long>(gg) * BM * BN / 4;
-#pragma unroll
-                  for (int q = 0; q < BN / 4; ++q) {
-                    const float4 w = __ldcg(pp + q);
-                    accv[4 * q] += w.x; accv[4 * q + 1] += w.y; accv[4 * q + 2] += w.z; accv[4 * q + 3] += w.w;
-                  }
-                }
-              }
-              if (lead && lane == 0) a.skcnt[tile] = 0;  // ready for the next launch
-            }
-            if (mv) {
-#pragma unroll
-              for (int hh = 0; hh < BN / 32; ++hh) {
-                const int n = hh * 32;
-                if (n >= a.N) break;
-                uint32_t pk[16];
-                epilogue_row32(a.ep, b1, b2, m, n, true, *reinterpret_cast<const uint32_t(*)[32]>(&accv[hh * 32]), pk,
-                               a.N - n);
-                uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.ep.out) +
-                                                    static_cast<long long>(b1) * a.ep.out_sb1 +
-                                                    static_cast<long long>(b2) * a.ep.out_sb2 +
-                                                    static_cast<long long>(m) * a.ep.out_sm + n);
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                  if (8 * q < a.N - n) o[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-              }
-            }
-            publish();
-          }
-        } else {
-          for (int i = 0, t = take(0); t < total; t = take(++i)) {
-          }  // the other warps only keep the unit queue moving
-        }
-      } else if (ew < C::EPI) {
-        // ---- f2 PV transform warps: thread = A-tile row (TMEM lane quarter x
-        // lane), half = which four of the row's eight 16-byte chunks.  Rescale the
-        // stored e = 2^(x - m2_slab) in place to P = e * f_slab (f_slab left in the
-        // statistics by the combine step, prefetched 8 slabs ahead); keys >= K are
-        // TMA zero-fill (e = 0), rows past M get f = 0.
+      // ---- f2 PV (post-scale, R19).  Warps 2-5 ("scale", thread = output row of
+      // TMEM lane quarter warp % 4): every 64-key slab's product e_slab V_slab lands in
+      // its own TMEM buffer (KBUF round robin); O += f_slab (e_slab V_slab) in fp32
+      // registers, f_slab = 2^(m2_slab - M_run) against the row's running max (O and L
+      // rescaled when it rises).  At a unit's end they hand (O, M_run, L) over through
+      // a TMEM staging buffer + shared memory and go straight on with the next unit,
+      // whose first statistics they already prefetched during the last slab block.
+      // Warps 6-9 ("finish") run the unit end: o = O / L and the output epilogue, or,
+      // split-K, the fp32 partial + (M, L) of the granule and, for the unit that
+      // completes the tile, the in-order merge of its granules.
+      uint64_t* kfull = bbar;
+      uint64_t* kempty = bbar + 8;
+      uint64_t* sfull = bbar + 16;   // staging written (4 scale warps)
+      uint64_t* sempty = bbar + 17;  // staging read (4 finish warps)
+      float2* sml = reinterpret_cast<float2*>(bbar + 18);  // (M_run, L) per row
+      const uint32_t tstg = tmem_base + C::KBUF * BN;        // staging columns
+      const float2 nost = make_float2(-CUDART_INF_F, 0.f);
+      auto unit = [&](int t, PvUnit& u) { pv_unit(a, prefix, tpb, t, quarter, lane, u); };
+      // slab kb's (m2, l) of the thread's row (float2 index b * sb1 + kb * ss + m)
+      auto ldst = [&](const PvUnit& u, int kb) -> float2 {
+        return __ldg(a.fstats + u.bb * a.fst_sb1 + static_cast<long long>(kb) * a.fst_ss + u.m);
+      };
+      if (warp < 6) {
+        const bool lead = warp == 2;
+        constexpr int PF = 4;  // slab statistics prefetched PF slabs ahead (next unit's included)
         const int r = quarter * 32 + lane;
-        int st = 0;
-        uint32_t ph = 0;
-        for (int i = 0, t = take(0); t < total; t = take(++i)) {
-          int b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0;
-          decode_unit(a, prefix, tpb, t, b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0);
-          // pairs: stage rows 0-63 = first batch, 64-127 = second batch (rows 0-63 each)
-          const int sel = a.pair ? r >> 6 : 0;
-          const int m = a.pair ? (r & 63) : mt * BM + r;
-          const long long bb = static_cast<long long>(b1) * a.B2 + b2 + sel;
-          const bool bok = bb < static_cast<long long>(a.B1) * a.B2;
-          const bool mv = m < a.M && bok;
-          const bool dead = a.pair ? ((quarter & 1) * 32 >= a.M || !bok)    // warp-uniform: rows never loaded
-                                   : mt * BM + quarter * 32 >= a.M;
-          const float* fp = reinterpret_cast<const float*>(a.fstats + bb * a.fst_sb1 + (mv ? m : 0));
-          const long long fs = 2 * a.fst_ss;
-          const float2 rs = mv ? __ldg(a.frow + bb * a.M + m) : make_float2(0.f, 0.f);
-          float fr[8];
+        int kbuf = 0;
+        uint32_t kphase = 0, sphase = 0;
+        int i = 0;
+        int t = take(0);
+        PvUnit u;
+        float2 fr[PF];
+        if (t < total) unit(t, u);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) fr[j] = (mv && klo + j < khi) ? __ldg(fp + (klo + j) * fs) : -CUDART_INF_F;
-          for (int kb0 = klo; kb0 < khi; kb0 += 8) {
-            float nx[8];
+        for (int j = 0; j < PF; ++j) fr[j] = (t < total && u.mv && u.klo + j < u.khi) ? ldst(u, u.klo + j) : nost;
+        while (t < total) {
+          float Mr = -CUDART_INF_F, Lr = 0.f;
+          float accv[BN];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) nx[j] = (mv && kb0 + 8 + j < khi) ? __ldg(fp + (kb0 + 8 + j) * fs) : -CUDART_INF_F;
+          for (int c = 0; c < BN; ++c) accv[c] = 0.f;
+          int tn = -1;
+          PvUnit un;
+          for (int kb0 = u.klo; kb0 < u.khi; kb0 += PF) {
+            float2 nx[PF];
+            if (kb0 + PF < u.khi) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              if (kb0 + j < khi) {
-                // f = 2^(m2_slab - M) / L (an empty slab has m2 = -inf: f = 0)
-                const __nv_bfloat162 f2 = __float2bfloat162_rn(ptx::ex2(fr[j] - rs.x) * rs.y);
-                ptx::mbar_wait(&full[st], ph);
-                uint8_t* row = sA + st * C::A_BYTES + r * 128;
+              for (int j = 0; j < PF; ++j) nx[j] = (u.mv && kb0 + PF + j < u.khi) ? ldst(u, kb0 + PF + j) : nost;
+            } else {
+              // last block of this unit: take the next unit now and prefetch its first
+              // statistics behind this block's slabs
+              tn = take(++i);
+              if (tn < total) unit(tn, un);
 #pragma unroll
-                for (int q4 = 0; q4 < ((a.dbg & 1) || dead ? 0 : 4); ++q4) {
-                  // same factor for every element: walk physical chunks in swizzled
-                  // order so 8 consecutive rows hit all 32 banks
-                  const int ch = half * 4 + q4;
-                  const uint32_t addr = ptx::smem_u32(row + ((ch ^ (r & 7)) * 16));
-                  uint32_t w0, w1, w2, w3;
-                  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                               : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
-                               : "r"(addr));
-                  uint32_t w[4] = {w0, w1, w2, w3};
+              for (int j = 0; j < PF; ++j) nx[j] = (tn < total && un.mv && un.klo + j < un.khi) ? ldst(un, un.klo + j) : nost;
+            }
 #pragma unroll
-                  for (int q = 0; q < 4; ++q) {  // P = bf16(e * bf16(f)): one packed multiply per pair
-                    __nv_bfloat162 h = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&w[q]), f2);
-                    w[q] = *reinterpret_cast<uint32_t*>(&h);
-                  }
-                  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(w[0]), "r"(w[1]),
-                               "r"(w[2]), "r"(w[3])
-                               : "memory");
+            for (int j = 0; j < PF; ++j) {
+              if (kb0 + j < u.khi) {
+                ptx::mbar_wait(&kfull[kbuf], kphase);
+                ptx::tc_fence_after();
+                if (a.trace && lead && lane == 0 && kb0 == u.klo && j == 0) {
+                  unsigned long long tnow;
+                  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+                  a.trace[4 * t + 2] = tnow;
                 }
-                if (!(a.dbg & 2)) ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
-                ptx::mbar_arrive(&ready[st]);
-                if (++st == C::STAGES) { st = 0; ph ^= 1; }
+                // the slab's e V product, 32 columns per TMEM load (the first load in
+                // flight while f is formed; 32 live registers keep the warp under 168)
+                const uint32_t tk = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + kbuf * BN;
+                uint32_t v[32];
+                ptx::tmem_ld32(tk, v);
+                if (fr[j].x > Mr) {
+                  const float cr = ptx::ex2(Mr - fr[j].x);  // first slab: 2^-inf = 0, O and L are 0
+                  Lr *= cr;
+#pragma unroll
+                  for (int c = 0; c < BN; ++c) accv[c] *= cr;
+                  Mr = fr[j].x;
+                }
+                const float f = fr[j].x == -CUDART_INF_F ? 0.f : ptx::ex2(fr[j].x - Mr);
+                Lr = fmaf(fr[j].y, f, Lr);
+#pragma unroll
+                for (int hh = 0; hh < BN / 32; ++hh) {
+                  if (hh > 0) ptx::tmem_ld32(tk + hh * 32, v);
+                  ptx::tmem_ld_wait();
+#pragma unroll
+                  for (int c = 0; c < 32; ++c) asm volatile("" : "+r"(v[c]));  // uses stay after the wait
+                  if (u.mv) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) accv[hh * 32 + c] = fmaf(f, __uint_as_float(v[c]), accv[hh * 32 + c]);
+                  }
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&kempty[kbuf]);
+                if (++kbuf == C::KBUF) { kbuf = 0; kphase ^= 1; }
               }
             }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) fr[j] = nx[j];
+            for (int j = 0; j < PF; ++j) fr[j] = nx[j];
           }
-        }
-      } else {
-        // ---- f2 PV output warps (one per TMEM lane quarter, all 64 columns): the
-        // unit's accumulator -> bf16 output (single-granule tile) or an fp32
-        // partial; the unit that completes a multi-granule tile sums the partials
-        // in granule order (fixed split-K, the same arithmetic however the units
-        // were scheduled or the rows chunked)
-        const int r = quarter * 32 + lane;
-        int* sk_old = prefix + MAX_MT + 1;  // counter value seen by this CTA (broadcast)
-        for (int i = 0, t = take(0); t < total; t = take(++i)) {
-          int b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0;
-          decode_unit(a, prefix, tpb, t, b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0);
-          // pairs: TMEM lanes 0-15 of each subpartition hold the first batch's rows
-          // quarter*16.., lanes 16-31 the second batch's
-          const int m = a.pair ? quarter * 16 + (lane & 15) : mt * BM + r;
-          if (a.pair && lane >= 16) {
-            const int nb = b1 * a.B2 + b2 + 1;
-            b1 = nb / a.B2;
-            b2 = nb - b1 * a.B2;
+          if (tn < 0) {  // (a unit without slabs: nothing was prefetched)
+            tn = take(++i);
+            if (tn < total) unit(tn, un);
+#pragma unroll
+            for (int j = 0; j < PF; ++j) fr[j] = (tn < total && un.mv && un.klo + j < un.khi) ? ldst(un, un.klo + j) : nost;
           }
-          const bool mv = m < a.M && b1 < a.B1;
-          ptx::mbar_wait(&tfull[acc], aphase);
-          ptx::tc_fence_after();
-          if (a.trace && ew == C::EPI && lane == 0) {
+          if (a.trace && lead && lane == 0) {  // end of the unit's slab stream
             unsigned long long tnow;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
-            a.trace[4 * t + 2] = tnow;
+            a.trace[4 * t + 3] = tnow;
           }
-          uint32_t rr[64];
-          {
-            uint32_t (&lo)[32] = *reinterpret_cast<uint32_t(*)[32]>(&rr[0]);
-            uint32_t (&hi)[32] = *reinterpret_cast<uint32_t(*)[32]>(&rr[32]);
-            const uint32_t tb = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
-            ptx::tmem_ld32(tb, lo);
-            if constexpr (BN > 32) ptx::tmem_ld32(tb + 32, hi);
-          }
-          ptx::tmem_ld_wait();
+          // hand over: O -> TMEM staging, (M_run, L) -> shared memory
+          ptx::mbar_wait(sempty, sphase ^ 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int hh = 0; hh < BN / 32; ++hh)
+            ptx::tmem_st32(tstg + (static_cast<uint32_t>(quarter * 32) << 16) + hh * 32,
+                           *reinterpret_cast<const uint32_t(*)[32]>(&accv[hh * 32]));
+          sml[r] = make_float2(Mr, Lr);
+          ptx::tmem_st_wait();
           ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-          if (++acc == 2) { acc = 0; aphase ^= 1; }
-          // chunk-loop overlap: once this unit has read its e-tiles / statistics (its
-          // MMAs completed) and stored its rows or partials, and the four output warps
-          // are past their stores, the unit that completes the batch publishes the
-          // chunk epoch (release, cumulative over the barrier).  Every unit counts.
+          if (lane == 0) ptx::mbar_arrive(sfull);
+          sphase ^= 1;
+          t = tn;
+          u = un;
+        }
+      } else {
+        const bool lead = warp == 6;
+        const int r = quarter * 32 + lane;
+        int* sk_old = prefix + MAX_MT + 1;  // counter value seen by this CTA (broadcast)
+        uint32_t sphase = 0;
+        for (int i = 0, t = take(0); t < total; t = take(++i)) {
+          PvUnit u;
+          unit(t, u);
+          ptx::mbar_wait(sfull, sphase);
+          ptx::tc_fence_after();
+          float accv[BN];
+#pragma unroll
+          for (int hh = 0; hh < BN / 32; ++hh)
+            ptx::tmem_ld32(tstg + (static_cast<uint32_t>(quarter * 32) << 16) + hh * 32,
+                           *reinterpret_cast<uint32_t(*)[32]>(&accv[hh * 32]));
+          const float2 ml = sml[r];
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < BN; ++c) asm volatile("" : "+f"(accv[c]));
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(sempty);
+          sphase ^= 1;
+          const float Mr = ml.x, Lr = ml.y;
+          const long long bb = u.bb;
+          // chunk-loop overlap: once this unit's rows or partials are stored (and the
+          // four finish warps are past their stores) the unit that completes the batch
+          // publishes the chunk epoch (release, cumulative over the barrier)
           auto publish = [&]() {
             if (!a.done_cnt) return;
             asm volatile("bar.sync 2, 128;" ::: "memory");
-            if (ew == C::EPI && lane == 0) {
-              const int bb = b1 * a.B2 + b2;
-              if (ptx::atom_add_acqrel_gpu(a.done_cnt + bb, 1) == tpb - 1)
-                ptx::st_release_gpu(a.done_epoch + bb, a.epoch + 1);
+            if (lead && lane == 0) {  // (lane 0: the pair's first batch; pairs count both)
+              const int nq = a.pair && bb + 1 < static_cast<long long>(a.B1) * a.B2 ? 2 : 1;
+              for (int q = 0; q < nq; ++q)
+                if (ptx::atom_add_acqrel_gpu(a.done_cnt + bb + q, 1) == tpb - 1)
+                  ptx::st_release_gpu(a.done_epoch + bb + q, a.epoch + 1);
             }
           };
-          if (ng > 1) {
-            float* mine = a.skpart + (static_cast<long long>(unit0 + g) * BM + r) * BN;
+          if (u.ng == 1) {
+            const float il = Lr > 0.f ? 1.f / Lr : 0.f;
 #pragma unroll
-            for (int q = 0; q < 16; ++q)
-              reinterpret_cast<float4*>(mine)[q] = make_float4(__uint_as_float(rr[4 * q]), __uint_as_float(rr[4 * q + 1]),
-                                                               __uint_as_float(rr[4 * q + 2]), __uint_as_float(rr[4 * q + 3]));
+            for (int c = 0; c < BN; ++c) accv[c] *= il;
+          } else {
+            float* mine = a.skpart + (static_cast<long long>(u.unit0 + u.g) * BM + r) * BN;
+#pragma unroll
+            for (int q = 0; q < BN / 4; ++q)
+              reinterpret_cast<float4*>(mine)[q] = make_float4(accv[4 * q], accv[4 * q + 1], accv[4 * q + 2], accv[4 * q + 3]);
+            // this granule's O is relative to its own running max: keep (M, L) beside it
+            a.skml[static_cast<long long>(u.unit0 + u.g) * BM + r] = make_float2(Mr, Lr);
             __threadfence();
             asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (ew == C::EPI && lane == 0) *sk_old = atomicAdd(a.skcnt + tile, 1);
+            if (lead && lane == 0) *sk_old = atomicAdd(a.skcnt + u.tile, 1);
             asm volatile("bar.sync 1, 128;" ::: "memory");
             const int old = *sk_old;
             asm volatile("bar.sync 1, 128;" ::: "memory");  // sk_old reusable
-            if (old != ng - 1) {
+            if (old != u.ng - 1) {
               publish();
               continue;
             }
             __threadfence();
-            const float4* base = reinterpret_cast<const float4*>(a.skpart + (static_cast<long long>(unit0) * BM + r) * BN);
+            // merge the granules in order: M = max M_g, O = sum 2^(M_g - M) O_g,
+            // L = sum 2^(M_g - M) L_g, o = O / L (granules of masked keys only: M_g = -inf)
+            const float4* base = reinterpret_cast<const float4*>(a.skpart + (static_cast<long long>(u.unit0) * BM + r) * BN);
+            const float2* mlp = a.skml + static_cast<long long>(u.unit0) * BM + r;
+            float Mt = -CUDART_INF_F;
+            for (int gg = 0; gg < u.ng; ++gg) Mt = fmaxf(Mt, __ldcg(mlp + static_cast<long long>(gg) * BM).x);
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              const float4 v = __ldcg(base + q);
-              rr[4 * q] = __float_as_uint(v.x); rr[4 * q + 1] = __float_as_uint(v.y);
-              rr[4 * q + 2] = __float_as_uint(v.z); rr[4 * q + 3] = __float_as_uint(v.w);
-            }
-            for (int gg = 1; gg < ng; ++gg) {
+            for (int c = 0; c < BN; ++c) accv[c] = 0.f;
+            float Lt = 0.f;
+            for (int gg = 0; gg < u.ng; ++gg) {
+              const float2 mg = __ldcg(mlp + static_cast<long long>(gg) * BM);
+              if (mg.x == -CUDART_INF_F) continue;
+              const float w = ptx::ex2(mg.x - Mt);
+              Lt = fmaf(mg.y, w, Lt);
               const float4* pp = base + static_cast<long long>(gg) * BM * BN / 4;
 #pragma unroll
-              for (int q = 0; q < 16; ++q) {
-                const float4 v = __ldcg(pp + q);
-                rr[4 * q] = __float_as_uint(__uint_as_float(rr[4 * q]) + v.x);
-                rr[4 * q + 1] = __float_as_uint(__uint_as_float(rr[4 * q + 1]) + v.y);
-                rr[4 * q + 2] = __float_as_uint(__uint_as_float(rr[4 * q + 2]) + v.z);
-                rr[4 * q + 3] = __float_as_uint(__uint_as_float(rr[4 * q + 3]) + v.w);
+              for (int q = 0; q < BN / 4; ++q) {
+                const float4 v4 = __ldcg(pp + q);
+                accv[4 * q] = fmaf(w, v4.x, accv[4 * q]); accv[4 * q + 1] = fmaf(w, v4.y, accv[4 * q + 1]);
+                accv[4 * q + 2] = fmaf(w, v4.z, accv[4 * q + 2]); accv[4 * q + 3] = fmaf(w, v4.w, accv[4 * q + 3]);
               }
             }
-            if (ew == C::EPI && lane == 0) a.skcnt[tile] = 0;  // ready for the next launch
+            const float il = Lt > 0.f ? 1.f / Lt : 0.f;
+#pragma unroll
+            for (int c = 0; c < BN; ++c) accv[c] *= il;
+            if (lead && lane == 0) a.skcnt[u.tile] = 0;  // ready for the next launch
           }
-          if (mv) {
+          if (u.mv) {
 #pragma unroll
             for (int hh = 0; hh < BN / 32; ++hh) {
               const int n = hh * 32;
               if (n >= a.N) break;
               uint32_t pk[16];
-              epilogue_row32(a.ep, b1, b2, m, n, true, *reinterpret_cast<const uint32_t(*)[32]>(&rr[hh * 32]), pk,
-                             a.N - n);
+              epilogue_row32(a.ep, u.b1, u.b2, u.m, n, true, *reinterpret_cast<const uint32_t(*)[32]>(&accv[hh * 32]),
+                             pk, a.N - n);
               uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.ep.out) +
-                                                  static_cast<long long>(b1) * a.ep.out_sb1 +
-                                                  static_cast<long long>(b2) * a.ep.out_sb2 +
-                                                  static_cast<long long>(m) * a.ep.out_sm + n);
+                                                  static_cast<long long>(u.b1) * a.ep.out_sb1 +
+                                                  static_cast<long long>(u.b2) * a.ep.out_sb2 +
+                                                  static_cast<long long>(u.m) * a.ep.out_sm + n);
 #pragma unroll
               for (int q = 0; q < 4; ++q)
                 if (8 * q < a.N - n) o[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
             }
           }
           publish();
-          if (a.trace && ew == C::EPI && lane == 0) {
-            unsigned long long tnow;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
-            a.trace[4 * t + 3] = tnow;
-          }
         }
       }
     } else if constexpr (MODE == 4) {
@@ -1340,10 +1145,6 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
               __syncwarp();
               if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
             }
-            if (MODE == 1 && a.pub_cnt && lane == 0) {
-              pub_slab(b1 * a.B2 + b2);
-              ++cur_n;
-            }
             continue;
           }
           // ---- f2 scores, one 64-column slab: x = acc * scale * log2(e) (fp32,
@@ -1352,7 +1153,6 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
           // e = bf16(2^(x - m2)), statistics (m2, fp32 sum of e).  Two TMEM passes
           // (max, then exponentials) keep 32 accumulators live at a time.
           constexpr float L2E = 1.4426950408889634f;
-          if (MODE == 1 && a.pub_cnt && lane == 0) pub_slab(b1 * a.B2 + b2);
           if (lane == 0) {
             if (!BIASED || !bias_pending) ptx::bulk_wait_read<0>();  // previous store has read the staging box
             if (BIASED && !bias_pending) {
@@ -1530,19 +1330,12 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
               char* dst = a.etile + ((static_cast<long long>(b1 * a.B2 + b2) * a.MT + mt) * a.e_nkb + n0 / 64) * 16384 +
                           quarter * 4096;
               if (n0 < a.N && m0 < a.M) {  // quarters past M: never read
-                if (!(a.dbg & 32))  // e-tiles: L2 evict-first (AC_DBG bit 32 turns it off)
-                  ptx::bulk_store_hint(dst, sb, 4096, ptx::policy_evict_first());
-                else
-                  ptx::bulk_store(dst, sb, 4096);
+                ptx::bulk_store_hint(dst, sb, 4096, ptx::policy_evict_first());  // e-tiles: L2 evict-first
               }
             } else {
               ptx::tma_store_4d(&a.tout, sb, n0, m0, b1, b2);
             }
             ptx::bulk_commit();
-            if (MODE == 1 && a.pub_cnt) {  // (lane 0)
-              ++cur_n;
-              ++def_after;
-            }
             if constexpr (BIASED) {
               // prefetch the bias box of this warp's slab in the CTA's next tile (same
               // slab index c) as soon as the store has read the staging box, so its L2
@@ -1723,7 +1516,6 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
       if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
     }
-    if (MODE == 1 && a.pub_cnt && lane == 0) pub_flush();
     if (lane == 0) ptx::bulk_wait_read<0>();  // staging buffers must outlive the TMA stores' reads
     __syncwarp();
   }
@@ -1881,7 +1673,7 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
     }
     a.skng = (kbn + a.skgk - 1) / a.skgk;
     if (a.skng > 1 && !a.skcnt) return cudaErrorInvalidValue;
-    if (p.pv_rowstats && a.skgk < kbn && !p.sk_ml) return cudaErrorInvalidValue;  // split online fold: (M, L) per granule
+    if (a.skgk < kbn && !p.sk_ml) return cudaErrorInvalidValue;  // split online fold: (M, L) per granule
     if (p.causal_k && a.MT > MAX_MT) return cudaErrorInvalidValue;
   }
   a.pdl_wait = p.pdl_wait;
@@ -1893,36 +1685,15 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   a.fstats = p.fuse_stats;
   a.fst_sb1 = p.fuse_sb1;
   a.fst_ss = p.fuse_ss;
-  a.frow = p.fuse_rowst;
-  if (MODE == 2 && !a.frow && !p.pv_rowstats) return cudaErrorInvalidValue;
   a.ks = (MODE == 0 && BN == 64 && a.vec && p.ksplit > 1) ? (p.ksplit > 8 ? 8 : p.ksplit) : 1;
   if (a.ks > 1) a.tma_store = 0;
   const int sms = num_sms();
-  a.pair = (MODE == 2 && BN == 32 && p.etile && p.M <= 64 && a.skng == 1 && !p.causal_k && !getenv("AC_NO_PAIR")) ? 1 : 0;
-  a.postscale = C::PS ? 1 : 0;
-  a.pv_rowstats = (MODE == 2 && C::PS && p.pv_rowstats) ? 1 : 0;
-  if (MODE == 2 && p.pv_rowstats && !a.pv_rowstats) return cudaErrorInvalidValue;
+  a.pair = (MODE == 2 && BN == 32 && p.etile && p.M <= 64 && a.skng == 1 && !p.causal_k) ? 1 : 0;
   a.zero_word = (MODE == 1 || MODE == 3 || MODE == 4) ? p.zero_word : nullptr;
   a.zero_n = p.zero_n;
-  a.pub_cnt = MODE == 1 ? p.pub_cnt : nullptr;
-  a.pub_epoch = MODE == 1 ? p.pub_epoch : nullptr;
-  if (MODE == 1 && a.pub_cnt && !a.tsched) return cudaErrorInvalidValue;  // batch-major dynamic tiles only
-  a.wait_epoch = MODE == 2 ? p.wait_epoch : nullptr;
-  if (MODE == 2 && a.wait_epoch && !a.pv_rowstats) return cudaErrorInvalidValue;
   int grid = MODE == 4 ? ((p.B1 * p.B2 + 1) / 2) * a.NT
                        : (a.pair ? (p.B1 * p.B2 + 1) / 2 : a.total_tiles_dense) * a.ks * (MODE == 2 ? a.skng : 1);
   int cap = C::DUAL ? 2 * sms : (sms / a.ks) * a.ks;
-  {
-    static int dbg = -1, dgrid = -1;
-    if (dbg < 0) {
-      const char* v = getenv("AC_DBG");
-      dbg = v ? atoi(v) : 0;
-      v = getenv("AC_DBG_GRID");
-      dgrid = v ? atoi(v) : 0;
-    }
-    a.dbg = dbg;
-    if (MODE == 2 && dgrid > 0 && dgrid < cap) cap = dgrid;
-  }
   static int trace_on = -1;
   static unsigned long long* trace_buf = nullptr;
   static int trace_launch = 0;
@@ -1936,7 +1707,6 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
     }
   }
   if (grid > cap) grid = cap;
-  if (p.max_ctas > 0 && grid > p.max_ctas) grid = p.max_ctas;  // concurrent scores leave SMs to the PV
   if (grid < a.ks) grid = a.ks;
   if (a.ks == 1 && p.pdl) {
     cudaLaunchConfig_t cfg = {};
@@ -2011,7 +1781,7 @@ cudaError_t gemm_tc(const GemmProblem& p, cudaStream_t s, int bn_hint) {
     }
   }
   if (p.fuse_stats) return p.N <= 32 ? launch<32, 2>(p, s) : bn == 64 ? launch<64, 2>(p, s) : cudaErrorInvalidValue;
-  if (p.ep.stats && p.ep.add && p.M <= 64 && p.etile && p.K <= 64 && getenv("AC_NO_PAIR") == nullptr)
+  if (p.ep.stats && p.ep.add && p.M <= 64 && p.etile && p.K <= 64)
     return launch<256, 4>(p, s);  // short chunks: paired 64-row tiles
   if (p.ep.stats && p.ep.add) {
     switch (bn) {
@@ -2022,8 +1792,6 @@ cudaError_t gemm_tc(const GemmProblem& p, cudaStream_t s, int bn_hint) {
     }
   }
   if (p.ep.stats) {
-    static const int sbn = getenv("AC_SCORES_BN") ? atoi(getenv("AC_SCORES_BN")) : 0;  // experiments
-    if (sbn && p.N > 128) bn = sbn;
     switch (bn) {
       case 64: return launch<64, 1>(p, s);
       case 128: return launch<128, 1>(p, s);

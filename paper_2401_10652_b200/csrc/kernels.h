@@ -67,13 +67,12 @@ struct GemmProblem {
   // the split depends only on the tile's K range, never on the chunking)
   int ksplit = 1;
   // fused softmax-normalised PV (NEXT f2): A holds e = 2^(x - m2_slab) written by
-  // the QK^T epilogue (Epilogue::stats, same layout in fuse_stats); fuse_rowst
-  // holds (M, 1/L) per (b1, row) (softmax_stats_combine); each 128 x 64 A tile
-  // (one slab) is rescaled in shared memory to P = e * 2^(m2_slab - M) / L before
-  // the MMA reads it, so P is never written to HBM.  BN = 64 only.
+  // the QK^T epilogue (Epilogue::stats, the slab statistics (m2, l) in fuse_stats);
+  // each 64-key slab's product e V lands in its own TMEM buffer and is folded into
+  // the row's output with f = 2^(m2_slab - M_run) against the running max (online,
+  // in slab order), o = O / L at the end, so P is never written.  BN = 32 / 64.
   const float2* fuse_stats = nullptr;
   int64_t fuse_sb1 = 0, fuse_ss = 0;
-  const float2* fuse_rowst = nullptr;
   // fixed split-K of the fused PV (SURVEY H-g): the key range is cut into
   // granules of sk_gk k-blocks at fixed key positions (0 = off); one work unit
   // per (tile, granule) balances the waves, multi-granule tiles leave fp32 partials
@@ -109,19 +108,9 @@ struct GemmProblem {
   int epoch = 0;
   int dep_epoch = 0;
   int* tsched = nullptr;
-  // f2 without a combine step: the PV folds each row's (M, 1/L) from the slab
-  // statistics itself (pv_rowstats); the scores zero the PV's unit counter (zero_word)
-  int pv_rowstats = 0;
+  // the scores zero the PV's unit counter (and split-K tile counters) at start
   int* zero_word = nullptr;
   int zero_n = 1;  // words zeroed from zero_word
-  // concurrent scores / PV of one chunk (AC_CONC=1): the scores publish per-batch
-  // completion (pub_cnt, pub_epoch = epoch + 1), the PV waits on it (wait_epoch)
-  // instead of on the whole scores grid; max_ctas caps the scores grid so the PV
-  // has SMs to run on meanwhile
-  int* pub_cnt = nullptr;
-  int* pub_epoch = nullptr;
-  int* wait_epoch = nullptr;
-  int max_ctas = 0;
 };
 
 // NEXT f1: fused attention o = softmax(q k^T * scale) v, no N x N tensor (attn_fused.cu).
@@ -161,16 +150,6 @@ cudaError_t layernorm(const void* x, const void* gamma, const void* beta, void* 
 cudaError_t softmax_rows(const void* s_in, void* p_out, int64_t rows, int64_t ncols, int64_t ld, int64_t gstride,
                          int64_t ldo, int64_t gstrideo, int causal, int64_t row_off, int64_t group, int dtype,
                          cudaStream_t s);
-
-// f2 statistics combine (the softmax node of a fused chain), log2 domain: for each of the
-// B1 x M rows, fold the slab statistics (m2_s, l_s) at stats[b1*sb1 + s*ss + m]
-// into the row's (M, L) and write rowst[b1*M + m] = (M, 1/L) (1/L = 0 for an
-// empty row).  causal: only the slabs below the row's 128-row tile end
-// (row_off + (m/128 + 1)*128) are read - the causal PV reads no others.
-// Also zeroes zero[0 .. nzero) (the PV's unit counter and split-K tile counters).
-cudaError_t softmax_stats_combine(float2* stats, int64_t B1, int64_t M, int ns, int64_t sb1, int64_t ss, int causal,
-                                  int64_t row_off, float2* rowst, int* zero, int64_t nzero, cudaStream_t s,
-                                  int pdl = 0);
 
 int num_sms();
 

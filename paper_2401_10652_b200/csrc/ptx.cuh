@@ -269,6 +269,12 @@ __device__ __forceinline__ uint32_t ex2_bf16x2(uint32_t x) {
 // ---------------------------------------------------------------- grid dependencies
 // programmatic dependent launch: wait for the preceding grid (complete + visible) /
 // let the following grid be scheduled now
+// register rebalancing between warpgroups (all four warps of a warpgroup execute it)
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
+
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {

@@ -684,84 +684,7 @@ cudaError_t layernorm_dispatch(const void* x, const void* g, const void* b, void
   return cudaGetLastError();
 }
 
-// f2 statistics combine: 32 rows x 8 slab groups per 256-thread block.  The
-// slab statistics are in the log2 domain (m2 = max of s*log2(e), l = sum of
-// 2^(x - m2)).  Thread (g, r) folds slabs s = g, g+8, ... of row r online, the 8
-// partials meet in shared memory in a fixed order and the row's (M, 1/L) is
-// written to rowst (one pass over the slab statistics, which stay as they are).
-__global__ void __launch_bounds__(256) stats_combine_kernel(float2* __restrict__ st, int64_t B1, int64_t M, int ns,
-                                                           int64_t sb1, int64_t ss, int causal, int64_t row_off,
-                                                           float2* __restrict__ rowst, int* __restrict__ zero,
-                                                           int64_t nzero, int pdl) {
-  __shared__ float2 part[8][33];
-  if (pdl) {  // chunk-loop overlap: the scores step must be complete and visible
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  }
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x; i < nzero; i += static_cast<int64_t>(gridDim.x) * 256)
-    zero[i] = 0;  // split-K tile counters of the PV that follows
-  const int r = threadIdx.x & 31, g = threadIdx.x >> 5;
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * 32 + r;
-  const bool valid = row < B1 * M;
-  const int64_t b1 = valid ? row / M : 0, m = valid ? row - b1 * M : 0;
-  int lim = ns;
-  if (causal) {  // slabs the causal PV tile of this row reads (its 128-row tile's key end)
-    const int64_t kend = row_off + (m / 128 + 1) * 128;
-    const int64_t sl = (kend + 63) / 64;
-    if (sl < lim) lim = static_cast<int>(sl);
-  }
-  float2* p = st + b1 * sb1 + m;
-  float mx = -INFINITY, l = 0.f;
-  if (valid)
-    for (int s = g; s < lim; s += 8) {
-      const float2 v = p[s * ss];
-      if (v.x == -INFINITY) continue;
-      if (v.x > mx) {
-        l = l * ex2f(mx - v.x) + v.y;
-        mx = v.x;
-      } else {
-        l += v.y * ex2f(v.x - mx);
-      }
-    }
-  part[g][r] = make_float2(mx, l);
-  __syncthreads();
-  float M_ = -INFINITY;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) M_ = fmaxf(M_, part[q][r].x);
-  float L = 0.f;
-  if (M_ != -INFINITY) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (part[q][r].x != -INFINITY) L += part[q][r].y * ex2f(part[q][r].x - M_);
-  }
-  if (!valid || g != 0) return;
-  // the PV forms f_s = 2^(m2_s - M) / L itself from (M, 1/L)
-  rowst[b1 * M + m] = make_float2(M_ == -INFINITY ? 0.f : M_, L > 0.f ? 1.f / L : 0.f);
-}
-
 }  // namespace
-
-cudaError_t softmax_stats_combine(float2* stats, int64_t B1, int64_t M, int ns, int64_t sb1, int64_t ss, int causal,
-                                  int64_t row_off, float2* rowst, int* zero, int64_t nzero, cudaStream_t st, int pdl) {
-  if (B1 * M <= 0) return cudaSuccess;
-  const int64_t blocks = (B1 * M + 31) / 32;
-  if (pdl) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(blocks));
-    cfg.blockDim = dim3(256);
-    cfg.stream = st;
-    cudaLaunchAttribute la[1];
-    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    la[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = la;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, stats_combine_kernel, stats, B1, M, ns, sb1, ss, causal, row_off, rowst, zero,
-                              nzero, 1);
-  }
-  stats_combine_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(stats, B1, M, ns, sb1, ss, causal, row_off,
-                                                                      rowst, zero, nzero, 0);
-  return cudaGetLastError();
-}
 
 cudaError_t softmax_rows(const void* s_in, void* p_out, int64_t rows, int64_t ncols, int64_t ld, int64_t gstride,
                          int64_t ldo, int64_t gstrideo, int causal, int64_t row_off, int64_t group, int dtype,

@@ -151,15 +151,11 @@ def test_gpt_full_size_sampled_rows():
 
 
 @pytest.mark.parametrize("causal", [True, False])
-@pytest.mark.parametrize("online", ["1", "0"])
-def test_fused_softmax_pv_vs_unfused(monkeypatch, causal, online):
+def test_fused_softmax_pv_vs_unfused(monkeypatch, causal):
     """NEXT f2: scores -> softmax -> PV with the normalisation folded into the PV
     operand path (AC_FUSE_SOFTMAX=1, default) against the three-kernel path
     (AC_FUSE_SOFTMAX=0): both within the bf16 tolerance of the oracle, smaller
-    workspace.  online=1 (default): the PV folds each row's (M, 1/L) itself, one
-    launch fewer per chunk; online=0: the softmax launch becomes the statistics
-    combine, same launch count."""
-    monkeypatch.setenv("AC_PV_ONLINE", online)
+    workspace, one launch fewer per chunk (the PV folds each row's (M, 1/L) itself)."""
     gu = _gu()
     from paper_2401_10652_b200 import api
     og = workloads.block("transformer", 1024 + 96, 256, 4, 1024, causal, "bf16", name="gpt_small")
@@ -176,22 +172,19 @@ def test_fused_softmax_pv_vs_unfused(monkeypatch, causal, online):
         res[flag] = (got["y"], ex.stats(), plan.workspace_bytes())
         assert gu.rel_err(got["y"], ref["y"]) < TOL["bf16"], flag
     (y0, s0, w0), (y1, s1, w1) = res["0"], res["1"]
-    assert s1.launches == s0.launches - (4 if online == "1" else 0)
+    assert s1.launches == s0.launches - 4
     assert w1 < w0
     # same bf16 P rounding point, different exp/sum order: close, not bitwise
     assert gu.rel_err(y1, y0.double().cpu().numpy()) < 1e-2
 
 
-@pytest.mark.parametrize("online", ["1", "0"])
 @pytest.mark.parametrize("split", ["0", "1"])
-def test_fused_pv_split_k_chunk_invariant(monkeypatch, split, online):
+def test_fused_pv_split_k_chunk_invariant(monkeypatch, split):
     """Fixed split-K of the fused PV (AC_PV_SPLITK=1 forces it on, 0 off; keys cut
     into 4 granules at fixed positions): bf16 tolerance vs the oracle and chunked ==
-    unchunked bitwise, causal and not; online=1 (default): each granule folds its own
-    (max, sum) and the tile's last unit merges them in granule order (no combine
-    launch), online=0: the statistics combine runs first."""
+    unchunked bitwise, causal and not; each granule folds its own (max, sum) and the
+    tile's last unit (a finish warp group) merges them in granule order."""
     monkeypatch.setenv("AC_PV_SPLITK", split)
-    monkeypatch.setenv("AC_PV_ONLINE", online)
     for causal in (True, False):
         og = workloads.block("attn_only", 2048 + 320, 256, 4, 0, causal, "bf16", name="pv_split")
         _check_all_plans(og, ["autochunk-plan 1\nregion s=scores e=pv n=4 dims=0\n",
@@ -338,34 +331,19 @@ def test_ac_run_cuda_graph_capture():
             assert torch.equal(outs[o], got[o]), (causal, o)
 
 
-def test_causal_chunk_overlap_opt_in(monkeypatch):
-    """The chunk-loop overlap on causal attention chains (AC_OVERLAP_CAUSAL=1: dynamic
-    scores tiles of chunk k+1 waiting on per-head epochs of chunk k's PV, PDL launches;
-    off by default for causal chains) keeps the results: vs the oracle and bitwise
-    equal to unchunked, also on a 2-block stack."""
-    monkeypatch.setenv("AC_OVERLAP_CAUSAL", "1")
+@pytest.mark.parametrize("ov", ["0", "1"])
+def test_causal_chunk_overlap(monkeypatch, ov):
+    """The chunk-loop overlap on causal attention chains (dynamic scores tiles of chunk
+    k+1 waiting on per-head epochs of chunk k's PV, PDL launches; on by default,
+    AC_OVERLAP_CAUSAL=0 off) keeps the results: vs the oracle and bitwise equal to
+    unchunked, also on a 2-block stack."""
+    monkeypatch.setenv("AC_OVERLAP_CAUSAL", ov)
     og = workloads.block("attn_only", 2048 + 320, 256, 4, 0, True, "bf16", name="ovc")
     _check_all_plans(og, ["autochunk-plan 1\nregion s=scores e=pv n=4 dims=0\n",
                           "autochunk-plan 1\nregion s=scores e=pv n=3 dims=0\n"], seed=17)
     og = workloads.transformer(512, 256, 4, 512, True, "bf16", name="ovs", layers=2)
     _check_all_plans(og, ["autochunk-plan 1\nregion s=L0_scores e=L0_pv n=4 dims=0\n"
                           "region s=L1_scores e=L1_pv n=2 dims=0\n"], seed=17)
-
-
-@pytest.mark.parametrize("causal", [True, False])
-def test_concurrent_scores_pv(monkeypatch, causal):
-    """AC_CONC=1: the PV of each chunk runs beside its scores, reading a head once the
-    scores published it complete (per-batch flags instead of a grid dependency), the
-    scores grid capped so the PV has SMs.  Same arithmetic: vs the oracle and bitwise
-    equal to unchunked; also with a scores grid of one CTA (the PV waits the longest)."""
-    monkeypatch.setenv("AC_CONC", "1")
-    monkeypatch.setenv("AC_OVERLAP_CAUSAL", "1")  # (the concurrency rides on the overlap's control block)
-    og = workloads.block("attn_only", 2048 + 320, 256, 4, 0, causal, "bf16", name="conc")
-    plans = ["autochunk-plan 1\nregion s=scores e=pv n=4 dims=0\n",
-             "autochunk-plan 1\nregion s=scores e=pv n=3 dims=0\n"]
-    _check_all_plans(og, plans, seed=13)
-    monkeypatch.setenv("AC_CONC_S", "1")
-    _check_all_plans(og, plans[:1], seed=13)
 
 
 @pytest.mark.parametrize("kind", ["transformer", "transformer_fa"])

@@ -56,10 +56,9 @@ for og, txt in [
         gu.run(cg, api.plan_parse(cg, t), og, dev)
         torch.cuda.synchronize()
 # forced PV split-K with the online fold (granule partials + (max, sum), counters in the
-# control block under the overlap), then the opt-in concurrent scores / PV
+# control block under the overlap), and causal chains without the overlap
 import os
-for env in ({"AC_PV_SPLITK": "1"}, {"AC_CONC": "1", "AC_CONC_S": "8", "AC_OVERLAP_CAUSAL": "1"},
-            {"AC_OVERLAP_CAUSAL": "1"}):
+for env in ({"AC_PV_SPLITK": "1"}, {"AC_OVERLAP_CAUSAL": "0"}):
     os.environ.update(env)
     for causal in (False, True):
         og = workloads.block("attn_only", 640 + 96, 256, 4, 0, causal, "bf16", name="sk")
