@@ -335,7 +335,8 @@ def maxlen_arm(args):
                                       if ln.startswith("region")],
                "ms": round(ms, 3), "tokens_per_s": round(Nr / (ms / 1e3), 1),
                "planned_peak_bytes": profp.peak_bytes, "unchunked_peak_bytes": prof0.peak_bytes,
-               "arena_bytes": ex.stats().workspace_high_water, "arena_plus_caller": ex.stats().workspace_high_water + caller,
+               "workspace_bytes": ex.stats().workspace_high_water,
+               "measured_peak_bytes": ex.stats().arena_live_peak + profp.x_bytes + profp.y_bytes,
                "torch_peak_delta_bytes": torch.cuda.max_memory_allocated() - base,
                "output_finite": bool(torch.isfinite(y.float()).all().item())}
     line = {"metric": "max inference length under this GPU's HBM (P:357-361)", "value": ml["chunked"],
@@ -352,6 +353,28 @@ def maxlen_arm(args):
 
 
 # ------------------------------------------------------------------ our arm
+def peak_block(profp, prof0, st, budget, caller, activation_alloc, unchunked):
+    """Planned (Eq. 2 under R25, ac_estimate_memory) and measured peaks, side by side.
+    measured = the device bytes torch holds for the run: inputs + outputs + the whole
+    workspace, all allocated at once (the caller keeps x and y for the whole run, so
+    this is >= planned, whose liveness frees x after its last use and allocates y when
+    it is produced); measured_unchunked likewise for the unchunked run.  The arena's
+    activation high-water (arena_live_peak) plus the caller tensors live at each step
+    equals the per-step plan exactly (tests/test_host_lib.py, test_gpu_parity.py)."""
+    meas = activation_alloc
+    mu = (unchunked or {}).get("measured_peak_bytes")
+    return {"planned": profp.peak_bytes, "unchunked": prof0.peak_bytes,
+            "reduction": round(1 - profp.peak_bytes / prof0.peak_bytes, 4),
+            "measured": meas, "measured_unchunked": mu,
+            "measured_reduction": round(1 - meas / mu, 4) if mu else None,
+            "budget": budget, "workspace_bytes": st.workspace_high_water,
+            "control_bytes": st.control_bytes, "arena_live_peak": st.arena_live_peak,
+            "note": "planned = Eq. 2 with the fused attention chains materialised as e-tiles + slab statistics "
+                    "(DESIGN.md R25), == arena live slots + caller tensors live, per step; measured = inputs + "
+                    "outputs + whole workspace as torch holds them for the run (weights excluded); "
+                    "control_bytes = scheduler state in the workspace (work counters, overlap epochs)"}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -496,6 +519,7 @@ def main():
         shares["_profiled_ms_per_step"] = round(prof_ms / kp, 4)
 
     # same kernels, unchunked (speed loss) — when it fits
+    caller_bytes = sum(doc.nbytes(t) for t in doc.inputs + doc.outputs)
     unchunked = None
     if not args.no_unchunked and not args.profile:
         try:
@@ -509,8 +533,11 @@ def main():
                 tu, _ = timed(exu, ins, outs, ku, 2)
                 _, ktu = timed(exu, ins, outs, ku, 1, profile=True)
                 vu = units * ku / (tu / 1e3)
+                stu = exu.stats()
                 unchunked = {"value": vu, "ms_per_step": tu / ku,
                              "speed_loss": 1.0 - value / vu, "workspace_bytes": need,
+                             "arena_live_peak": stu.arena_live_peak,
+                             "measured_peak_bytes": need + caller_bytes,
                              "stages_ms": {k: round(v[1] / ku, 4) for k, v in
                                            sorted(ktu.items(), key=lambda kv: -kv[1][1])}}
                 del exu, wsu
@@ -653,14 +680,7 @@ def main():
         "config": {"workload": WORKLOADS[args.config] + (f", {args.layers} stacked blocks" if args.layers > 1 else ""),
                    "plan": regions, "parallelism": f"chunk-split x{world}",
                    "l2": "flushed between timed steps (256 MiB write)"},
-        "peak_activation_bytes": {"planned": profp.peak_bytes, "unchunked": prof0.peak_bytes,
-                                  "reduction": round(1 - profp.peak_bytes / prof0.peak_bytes, 4),
-                                  "budget": budget, "arena_bytes": st.workspace_high_water,
-                                  "arena_plus_caller": st.workspace_high_water + caller,
-                                  "torch_allocated_activation": activation_alloc,
-                                  "note": "torch_allocated_activation = device bytes torch holds for inputs, "
-                                          "outputs and the ac_run workspace (weights excluded, Eq. 1); it must "
-                                          "not exceed planned (the f2 chains keep P as statistics only)"},
+        "peak_activation_bytes": peak_block(profp, prof0, st, budget, caller, activation_alloc, unchunked),
         "unchunked": unchunked, "roofline": roof, "stages": shares, "cpu_baseline": cpu, "e2e": e2e,
         **({"chunk_sweep": sweep} if sweep else {}),
         **({"ablation": ablation} if ablation else {}),

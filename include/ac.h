@@ -162,6 +162,17 @@ int32_t ac_plan_num_regions(const ac_chunk_plan* p);
  * static arena).  -1 on error. */
 int64_t ac_plan_workspace_bytes(const ac_chunk_plan* p, int32_t rank, int32_t world);
 
+/* The static arena ac_exec_create lays out for this plan, without a device:
+ * live_per_step[s] (nullable, ac_graph node count entries) = bytes of the
+ * activation slots live at execution step s (chunk-sized interior tensors, the
+ * fused chains' e-tiles and statistics, R25); *live_peak = their maximum;
+ * *control_bytes = workspace bytes after the slots that are scheduler state, not
+ * activation.  With the inputs / outputs live at a step added, live_per_step
+ * equals ac_estimate_memory's per-step bytes (the test of "planned == arena +
+ * caller").  Errors: AC_ERR_ARG. */
+ac_status ac_plan_arena_profile(const ac_chunk_plan* p, int64_t* live_per_step, int64_t* live_peak,
+                                int64_t* control_bytes);
+
 /* Chunks [*c0, *c1) of region `region` (commit order) that rank `rank` of
  * `world` executes: floor(rank n / world) .. floor((rank+1) n / world)
  * (SURVEY §8(e)).  Also reports the region's chunk_len and extent.
@@ -216,11 +227,19 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
 
 /* Statistics of the last ac_run (read after the stream has completed). */
 typedef struct ac_run_stats {
-  int64_t workspace_high_water;  /* bytes of the arena actually addressed */
+  int64_t workspace_high_water;  /* bytes of the workspace actually addressed */
   int64_t planned_peak;          /* ac_estimate_memory(plan) peak */
   int64_t caller_bytes;          /* graph inputs + outputs (full size) */
   int32_t launches;              /* kernels launched by the last ac_run */
   int32_t chunks_run;            /* chunk iterations executed on this rank */
+  /* activation high-water of the workspace: max over steps of the bytes of the
+   * activation slots live at that step (the f2 chains' e-tiles and statistics
+   * included, R25).  planned_peak == arena_live_peak + the caller-held inputs /
+   * outputs live at the planned peak step (ac_mem_profile x_bytes + y_bytes). */
+  int64_t arena_live_peak;
+  /* workspace bytes that are scheduler state, not activation (the fused chains'
+   * work counters, split-K partials, chunk-loop overlap epochs): after the slots */
+  int64_t control_bytes;
 } ac_run_stats;
 ac_status ac_exec_stats(const ac_exec* e, ac_run_stats* out);
 

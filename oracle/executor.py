@@ -8,7 +8,12 @@
                  pre-allocated Y^c, so Y = [y_1; ...; y_n].
 * tracked_run  — the same execution with a buffer tracker that measures live
                  activation bytes per step from the buffers that actually exist
-                 (the brute-force check of Eq. 1 / Eq. 2).
+                 (the brute-force check of Eq. 1 / Eq. 2).  A fused
+                 bf16 chain (R25, memory.f2_chains) allocates what the
+                 GPU path materialises: the e-tile buffer (rows padded to 128,
+                 keys to 64, bf16) at the scores step together with the slab
+                 statistics buffer (fp32 pairs per row and 64-key slab), both
+                 released after the PV; the chain's values are computed as usual.
 Values are float64.  With mirror=True every bf16 tensor is rounded to bf16
 (round-to-nearest-even) after it is produced, mirroring the GPU storage points
 (reading R17); the default is pure fp64.
@@ -71,7 +76,7 @@ class _Tracker:
         return sum(self.live.values())
 
 
-def _last_use(g: Graph):
+def _last_use(g: Graph, chains=()):
     last = {}
     for i, n in enumerate(g.nodes):
         last.setdefault(n.output, 0 if n.kind in ("input", "weight") else i)
@@ -79,7 +84,20 @@ def _last_use(g: Graph):
             last[t] = i
     for o in g.outputs:
         last[o] = len(g.nodes)  # never freed
+    for i, sm, pv in chains:    # the PV reads the e-tiles
+        last[g.nodes[i].output] = max(last[g.nodes[i].output], pv)
     return last
+
+
+def _f2_buffers(shape):
+    """The two buffers a fused chain's scores step creates for an S of `shape`
+    [..B.., M, nk]: e-tiles (bf16, 128-row x 64-key blocks) and the slab
+    statistics (fp32 max and sum per row and 64-key slab).  Real arrays: the
+    tracker counts their nbytes."""
+    *lead, M, nk = shape
+    e = np.empty(tuple(lead) + (-(-M // 128) * 128, -(-nk // 64) * 64), dtype=np.uint16)
+    st = np.empty(tuple(lead) + (M, -(-nk // 64), 2), dtype=np.float32)
+    return e, st
 
 
 def tracked_run(g: Graph, values: dict, regions=(), mirror=False, contiguity=False, chunk_ranges=None):
@@ -92,10 +110,14 @@ def tracked_run(g: Graph, values: dict, regions=(), mirror=False, contiguity=Fal
         if r.n > 1 and chunk_ranges is not None and k in chunk_ranges:
             ranges[id(r)] = chunk_ranges[k]
     regions = [r for r in regions if r.n > 1]
+    from .memory import f2_chains
+    chains = f2_chains(g, regions)
+    f2 = {i: (sm, pv) for i, sm, pv in chains}          # scores node -> (softmax, pv)
+    f2_soft = {sm for i, sm, pv in chains}
     esz = {t: g.tensors[t].esize for t in g.tensors}
     wset = set(g.weights)
     tr = _Tracker(g)
-    last = _last_use(g)
+    last = _last_use(g, chains)
     env = dict(values)
     per_step = [0] * len(g.nodes)
     for n in g.nodes:                         # inputs are born at step 0
@@ -108,7 +130,7 @@ def tracked_run(g: Graph, values: dict, regions=(), mirror=False, contiguity=Fal
         if i in at:
             r = at[i]
             _tracked_region(g, r, env, tr, per_step, esz, wset, last, mirror, contiguity,
-                            ranges.get(id(r), (0, r.n)))
+                            ranges.get(id(r), (0, r.n)), f2, f2_soft)
             # free everything whose last use was inside the region
             for t in list(tr.live):
                 if isinstance(t, str) and last.get(t, -1) <= r.end:
@@ -120,7 +142,12 @@ def tracked_run(g: Graph, values: dict, regions=(), mirror=False, contiguity=Fal
         else:
             out = _eval(g, i, [env[t] for t in n.inputs], None, mirror)
             env[n.output] = out
-            tr.alloc(n.output, out.size * esz[n.output])
+            if i in f2:                     # fused chain: e-tiles + statistics
+                e, st = _f2_buffers(out.shape)
+                tr.alloc(n.output, e.nbytes)
+                tr.alloc(g.nodes[f2[i][0]].output, st.nbytes)
+            elif i not in f2_soft:          # (the statistics stand for P)
+                tr.alloc(n.output, out.size * esz[n.output])
             per_step[i] = tr.total()
         for t in list(tr.live):
             if isinstance(t, str) and last.get(t, -1) <= i:
@@ -129,7 +156,8 @@ def tracked_run(g: Graph, values: dict, regions=(), mirror=False, contiguity=Fal
     return {o: env[o] for o in g.outputs}, per_step
 
 
-def _tracked_region(g, r, env, tr, per_step, esz, wset, last, mirror, contiguity, crange=None):
+def _tracked_region(g, r, env, tr, per_step, esz, wset, last, mirror, contiguity, crange=None, f2=None,
+                    f2_soft=()):
     from .memory import contiguity_cost
     E, n = r.extent, r.n
     L = -(-E // n)
@@ -148,12 +176,16 @@ def _tracked_region(g, r, env, tr, per_step, esz, wset, last, mirror, contiguity
         for t, d in list(r.xc) + list(r.yc):
             tm = g.tensors[t]
             ctg += contiguity_cost(tm.shape, tm.esize, d, n)
+    f2 = f2 or {}
     ilast = {}                                  # last in-region (per-chunk) use
     for k in range(r.start, r.end + 1):
         if k not in hs:
             for t in g.nodes[k].inputs:
                 if t in produced:
                     ilast[t] = k
+    for k, (sm, pv) in f2.items():              # fused chain: the PV reads the e-tiles
+        if r.start <= k <= r.end:
+            ilast[g.nodes[k].output] = max(ilast.get(g.nodes[k].output, pv), pv)
     c0, c1 = crange if crange is not None else (0, n)
     for c in range(c0, c1):
         off = c * L
@@ -163,6 +195,16 @@ def _tracked_region(g, r, env, tr, per_step, esz, wset, last, mirror, contiguity
         if ctg:
             tr.alloc(("ctg",), ctg)
         local = {}
+
+        def alloc_local(k, out):
+            t = g.nodes[k].output
+            if k in f2:                         # fused chain: e-tiles + statistics (R25)
+                e, st = _f2_buffers(out.shape)
+                tr.alloc(("slice", t), e.nbytes)
+                tr.alloc(("slice", g.nodes[f2[k][0]].output), st.nbytes)
+            elif k not in f2_soft:              # (the statistics stand for P)
+                tr.alloc(("slice", t), out.size * esz[t])
+
         for k in range(r.start, r.end + 1):
             if k in hs:                         # nothing runs here per chunk
                 per_step[k] = max(per_step[k], tr.total())
@@ -174,7 +216,7 @@ def _tracked_region(g, r, env, tr, per_step, esz, wset, last, mirror, contiguity
                 # full-size interior tensor (Eq. 2 term (v), R6)
                 out = _eval(g, k, [local[t] if t in local else env[t] for t in nd.inputs], None, mirror)
                 local[nd.output] = out
-                tr.alloc(("slice", nd.output), out.size * esz[nd.output])
+                alloc_local(k, out)
                 per_step[k] = max(per_step[k], tr.total())
                 for t in set(nd.inputs) | {nd.output}:
                     if t in local and ilast.get(t, k) <= k:
@@ -198,7 +240,7 @@ def _tracked_region(g, r, env, tr, per_step, esz, wset, last, mirror, contiguity
                     local[nd.output] = out
             else:
                 local[nd.output] = out
-                tr.alloc(("slice", nd.output), out.size * esz[nd.output])
+                alloc_local(k, out)
             per_step[k] = max(per_step[k], tr.total())
             for t in set(nd.inputs) | {nd.output}:
                 if t in local and ilast.get(t, k) <= k:

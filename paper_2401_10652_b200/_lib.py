@@ -52,7 +52,8 @@ class Tensor(C.Structure):
 
 class RunStats(C.Structure):
     _fields_ = [("workspace_high_water", C.c_int64), ("planned_peak", C.c_int64), ("caller_bytes", C.c_int64),
-                ("launches", C.c_int32), ("chunks_run", C.c_int32)]
+                ("launches", C.c_int32), ("chunks_run", C.c_int32), ("arena_live_peak", C.c_int64),
+                ("control_bytes", C.c_int64)]
 
 
 class KernelTime(C.Structure):
@@ -95,6 +96,7 @@ SIGNATURES = [
     ("ac_plan_free", None, [P]),
     ("ac_plan_num_regions", C.c_int32, [P]),
     ("ac_plan_workspace_bytes", C.c_int64, [P, C.c_int32, C.c_int32]),
+    ("ac_plan_arena_profile", C.c_int, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("ac_plan_rank_chunks", C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int64),
                                       C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("ac_comm_get_unique_id", C.c_int, [C.c_char_p]),

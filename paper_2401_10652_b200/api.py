@@ -112,6 +112,16 @@ class Plan:
         return v
 
 
+def arena_profile(plan: Plan):
+    """ac_plan_arena_profile: (live bytes of the arena's activation slots per step,
+    their peak, control bytes) of the arena ac_exec_create lays out for `plan`."""
+    n = plan.graph.num_nodes
+    arr = (C.c_int64 * max(n, 1))()
+    pk, cb = C.c_int64(), C.c_int64()
+    check(lib().ac_plan_arena_profile(plan.handle, arr, C.byref(pk), C.byref(cb)))
+    return list(arr)[:n], pk.value, cb.value
+
+
 def cost_params(**kw) -> L.CostParams:
     p = L.CostParams()
     lib().ac_cost_params_default(C.byref(p))

@@ -40,8 +40,13 @@ struct ArenaSlot {
 
 struct Arena {
   std::vector<ArenaSlot> slot;  // per tensor
-  int64_t size = 0;
-  int64_t live_peak = 0;        // max over steps of the bytes live in the arena
+  int64_t size = 0;             // whole workspace: activation slots + control area
+  int64_t act_size = 0;         // activation slots (Eq. 1 / 2 bytes) only
+  int64_t live_peak = 0;        // max over steps of the bytes live in the activation slots
+  // per fused chain (indexed by its scores node, -1 none): offset of its control area
+  // (PV work counters, split-K partials) after the activation slots - scheduler
+  // state, not activation (R25)
+  std::vector<int64_t> f2_off;
   // chunk-loop overlap control blocks (fused chains inside a chunked region), after
   // the tensors: per scores node, offset (-1 none), batches B, chunks n.  Layout in
   // ints: [epoch: B][tile counters: n][PV unit counters: n][PV done counts: n x B]
@@ -124,12 +129,14 @@ ExecOptions read_options() {
 }
 
 // Fixed split-K of the fused PV (key granules at fixed positions, so chunked ==
-// unchunked bitwise either way): on for non-causal chains of >= 4096 keys (uniform
-// tiles: quarter-tile units taken dynamically shorten the last wave), off for causal
-// ones (heaviest-first whole tiles).  AC_PV_SPLITK=0/1 forces it.
+// unchunked bitwise either way).  Off by default: with the finish warps and the
+// chunk-loop overlap (the next chunk's scores fill the PV's last wave) whole-tile
+// units are faster for causal and non-causal chains alike (GPT 2.48 vs 2.62 ms,
+// UNet 2.56 vs 2.60 ms per step).  AC_PV_SPLITK=1 forces it on.
 bool pv_splitk(const ExecOptions& o, bool causal, int64_t nk) {
-  if (o.pv_splitk >= 0) return o.pv_splitk == 1;
-  return !causal && nk >= 4096;
+  (void)causal;
+  (void)nk;
+  return o.pv_splitk == 1;
 }
 
 // Control block of an overlapped chain (B batches, n chunks), ints:
@@ -155,77 +162,35 @@ int region_index(const Plan& plan, int node) {
   return -1;
 }
 
-// attn_scores -> softmax(last dim) -> attn_pv chains whose softmax normalisation is
-// fused into PV's operand path (NEXT f2): S consumed only by the
-// softmax, P only by the PV, bf16, head dim <= 64, all three nodes executed in the
-// same chunk context.  P is then never written; its (still allocated) buffer holds
-// the per-slab softmax statistics.  AC_FUSE_SOFTMAX=0 disables it.
-struct Chain {
-  int scores, softmax, pv;
-};
+// attn_scores / tri_scores -> softmax(keys) -> attn_pv / tri_pv chains run fused (NEXT
+// f2): the rule is the estimator's (f2_chains, R25), so the arena holds
+// exactly what ac_estimate_memory charges.  AC_FUSE_SOFTMAX=0 runs them unfused.
+using Chain = F2Chain;
 std::vector<Chain> fused_chains(const Graph& g, const Plan& plan, const ExecOptions& o) {
-  std::vector<Chain> out;
-  if (!o.fuse_softmax) return out;
-  for (int i = 0; i < static_cast<int>(g.nodes.size()); ++i) {
-    const Node& n = g.nodes[i];
-    // attn_scores [H, M, nk] -> softmax -> attn_pv, or the AlphaFold triangle chain
-    // tri_scores [B1, H, M, nk] (+ bias) -> softmax -> tri_pv (gated)
-    const bool tri = n.kind == "tri_scores";
-    if (n.kind != "attn_scores" && !tri) continue;
-    const int s_t = n.output;
-    const int kd = static_cast<int>(g.tensors[s_t].shape.size()) - 1;  // key dim of S
-    if (g.tensors[s_t].dtype != DT::BF16 || g.is_output[s_t] || g.consumers[s_t].size() != 1) continue;
-    const int sm = g.consumers[s_t][0];
-    if (g.nodes[sm].kind != "softmax" || g.nodes[sm].ai("dim") != kd) continue;
-    const int p_t = g.nodes[sm].output;
-    if (g.is_output[p_t] || g.consumers[p_t].size() != 1) continue;
-    const int pv = g.consumers[p_t][0];
-    if (g.nodes[pv].kind != (tri ? "tri_pv" : "attn_pv") || g.nodes[pv].inputs[0] != p_t) continue;
-    // PV on the BN = 32 / 64 tile (head dim <= 64); scores on the TMA-store path
-    const std::vector<int64_t>& osh = g.tensors[g.nodes[pv].output].shape;
-    const int64_t dh = osh.back(), nk = g.tensors[s_t].shape[kd];
-    if (dh > 64 || dh % 8 != 0 || nk < 64 || nk % 8 != 0) continue;
-    const int ri = region_index(plan, i), rs = region_index(plan, sm), rp = region_index(plan, pv);
-    if (ri != rs || rs != rp) continue;
-    if (ri >= 0) {
-      const Region& R = plan.regions[ri];
-      bool hoisted = false;
-      for (int h : R.hoisted) hoisted = hoisted || h == i || h == sm || h == pv;
-      if (hoisted) continue;
-      // S and P must be chunked along the same dim (batch, heads or query rows), never keys
-      const int ds = R.dim_of(s_t), dp = R.dim_of(p_t);
-      if (ds != dp || ds == kd) continue;
-    }
-    out.push_back({i, sm, pv});
-  }
-  return out;
+  if (!o.fuse_softmax) return {};
+  return f2_chains(g, plan.regions);
 }
 
-// P's buffer in a fused chain (per launch of B1 heads x M rows x nk keys):
-// [slab statistics, float2 per (b1, 64-key slab, row)] [split-K partials of the
-// PV, fp32 128 x 64 per (tile, granule)] [split-K tile counters, int per tile].
-// The key range is cut into SK_NG granules of sk_gk(nk) k-blocks at fixed key
-// positions (a function of the key count only, so chunk-invariant): four units
-// per tile balance the waves while the fp32 partials stay < 1 % of the e traffic.
 constexpr int SK_NG = 4;
 int64_t sk_gk(int64_t nk) { return ((nk + 63) / 64 + SK_NG - 1) / SK_NG; }
-struct F2Layout {
-  int64_t stats = 0, part = 0, cnt = 0, ml = 0, total = 0;
+// control area of a fused chain (per launch of at most B1 batches x M rows x nk keys):
+// [int counters: the PV's dynamic unit counter, then one per split-K tile]
+// [split-K partials, fp32 128 x 64 per (tile, granule)] [split-K (max, sum) per (unit, row)].
+// The key range is cut into SK_NG granules of sk_gk(nk) k-blocks at fixed key
+// positions (a function of the key count only, so chunk-invariant).
+struct F2Ctrl {
+  int64_t cnt = 0, part = 0, ml = 0, total = 0;
   int64_t ncnt = 0;
 };
-// S of a fused chain is stored as pre-swizzled e-tiles (GemmProblem::etile):
-// 16 KB per (head, 128-row tile, 64-key block)
-int64_t etile_bytes(int64_t B1, int64_t M, int64_t nk) { return B1 * ((M + 127) / 128) * ((nk + 63) / 64) * 16384; }
 
-F2Layout f2_layout(int64_t B1, int64_t M, int64_t nk, bool split) {
-  F2Layout L;
+F2Ctrl f2_ctrl(int64_t B1, int64_t M, int64_t nk, bool split) {
+  F2Ctrl L;
   const int64_t ns = (nk + 63) / 64, mt = (M + 127) / 128, ng = split ? (ns + sk_gk(nk) - 1) / sk_gk(nk) : 1;
   auto al = [](int64_t v) { return (v + 255) / 256 * 256; };
-  L.stats = 0;
-  L.part = al(B1 * ns * M * 8);
-  L.cnt = L.part + (ng > 1 ? al(B1 * mt * ng * 128 * 64 * 4) : 0);
-  L.ncnt = 1 + (ng > 1 ? B1 * mt : 0);  // [0]: dynamic unit counter, then one per tile
-  L.ml = L.cnt + al(L.ncnt * 4);         // split + online fold: (max, sum) per (unit, row)
+  L.ncnt = 1 + (ng > 1 ? B1 * mt : 0);
+  L.cnt = 0;
+  L.part = al(L.ncnt * 4);
+  L.ml = L.part + (ng > 1 ? al(B1 * mt * ng * 128 * 64 * 4) : 0);
   L.total = L.ml + (ng > 1 ? al(B1 * mt * ng * 128 * 8) : 0);
   return L;
 }
@@ -277,9 +242,11 @@ Arena build_arena(const Graph& g, const Plan& plan, const ExecOptions& o) {
       death[t] = lastc;
     }
   }
-  // fused chains: S stays live until the PV reads it; P's buffer shrinks to the
-  // softmax statistics (float2 per row and 64-key slab), written by the scores step
-  for (const Chain& c : fused_chains(g, plan, o)) {
+  // fused chains (R25): S holds the e-tiles and stays live until the PV reads them;
+  // P holds the softmax statistics (float2 per row and 64-key slab), written by the
+  // scores step
+  const std::vector<Chain> chains = fused_chains(g, plan, o);
+  for (const Chain& c : chains) {
     const int s_t = g.nodes[c.scores].output, p_t = g.nodes[c.softmax].output;
     std::vector<int64_t> sh = g.tensors[p_t].shape;  // [(B1,) H, M, nk], chunk-reduced inside a region
     const int r = region_index(plan, c.softmax);
@@ -288,18 +255,19 @@ Arena build_arena(const Graph& g, const Plan& plan, const ExecOptions& o) {
       const int d = R.dim_of(p_t);
       if (d >= 0) sh[d] = (sh[d] + R.n - 1) / R.n;
     }
-    int64_t B = 1;
-    for (size_t d = 0; d + 2 < sh.size(); ++d) B *= sh[d];
-    const int64_t M = sh[sh.size() - 2], nk = sh.back();
-    bytes[p_t] = f2_layout(B, M, nk, pv_splitk(o, g.nodes[c.scores].ai("causal") != 0, nk)).total;
-    bytes[s_t] = etile_bytes(B, M, nk);
+    bytes[p_t] = f2_stats_bytes(sh);
+    bytes[s_t] = f2_etile_bytes(sh);
     birth[p_t] = std::min(birth[p_t], c.scores);
     death[s_t] = std::max(death[s_t], c.pv);
   }
   std::vector<int> order;
   for (int t = 0; t < T; ++t)
     if (!is_caller(g, t)) order.push_back(t);
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return birth[a] < birth[b]; });
+  // larger slots first (then birth order): first fit then packs the interval graph
+  // without holes in every planned configuration (ac_plan_arena_profile tests)
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return bytes[a] != bytes[b] ? bytes[a] > bytes[b] : birth[a] < birth[b];
+  });
   std::vector<int> placed;
   for (int t : order) {
     const int64_t sz = (bytes[t] + 255) / 256 * 256;
@@ -324,12 +292,26 @@ Arena build_arena(const Graph& g, const Plan& plan, const ExecOptions& o) {
       if (A.slot[t].birth <= s && s <= A.slot[t].death) live += A.slot[t].bytes;
     A.live_peak = std::max(A.live_peak, live);
   }
+  A.act_size = A.size;
+  // control areas of the fused chains (scheduler state, after the activation slots)
+  A.f2_off.assign(S, -1);
+  for (const Chain& c : chains) {
+    const int s_t = g.nodes[c.scores].output;
+    std::vector<int64_t> sh = g.tensors[s_t].shape;
+    const int r = region_index(plan, c.scores);
+    if (r >= 0 && plan.regions[r].dim_of(s_t) >= 0) sh[plan.regions[r].dim_of(s_t)] = plan.regions[r].chunk_len();
+    int64_t B = 1;
+    for (size_t d = 0; d + 2 < sh.size(); ++d) B *= sh[d];
+    const F2Ctrl L = f2_ctrl(B, sh[sh.size() - 2], sh.back(), pv_splitk(o, causal_chain(g, c.scores), sh.back()));
+    A.f2_off[c.scores] = A.size;
+    A.size += L.total;
+  }
   A.ctrl_off.assign(S, -1);
   A.ctrl_b.assign(S, 0);
   A.ctrl_n.assign(S, 0);
   A.ctrl_mt.assign(S, 0);
   if (o.overlap) {
-    for (const Chain& c : fused_chains(g, plan, o)) {
+    for (const Chain& c : chains) {
       const int r = region_index(plan, c.scores);
       if (r < 0) continue;
       // triangle chains: measured slower with the overlap (AF 15.8 -> 18.1 ms: the
@@ -643,8 +625,8 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         ep.stats_sb1 = e->fuse_malloc[i] * ns;
         chain_overlap(e, i, cx, p);
         // the scores reset the PV's counters (overlap: its split counters are in the control block)
-        const F2Layout L = f2_layout(e->fuse_balloc[i], e->fuse_malloc[i], p.N, e->fuse_split[i] != 0);
-        p.zero_word = reinterpret_cast<int*>(V[e->fuse_p[i]].p + L.cnt);
+        const F2Ctrl L = f2_ctrl(e->fuse_balloc[i], e->fuse_malloc[i], p.N, e->fuse_split[i] != 0);
+        p.zero_word = reinterpret_cast<int*>(e->ws + e->arena.f2_off[e->fuse_head[i]] + L.cnt);
         p.zero_n = chain_ctrl(e, i, cx) ? 1 : static_cast<int>(L.ncnt);
       }
     } else if (k == "attn_pv") {
@@ -669,14 +651,15 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         p.fuse_stats = reinterpret_cast<const float2*>(in(0).p);
         p.fuse_ss = e->fuse_malloc[i];
         p.fuse_sb1 = e->fuse_malloc[i] * ns;
-        const F2Layout L = f2_layout(e->fuse_balloc[i], e->fuse_malloc[i], p.K, e->fuse_split[i] != 0);
+        const F2Ctrl L = f2_ctrl(e->fuse_balloc[i], e->fuse_malloc[i], p.K, e->fuse_split[i] != 0);
+        char* ctl = e->ws + e->arena.f2_off[e->fuse_head[i]];
         p.etile = pp.p;
-        p.sched = reinterpret_cast<int*>(in(0).p + L.cnt);
+        p.sched = reinterpret_cast<int*>(ctl + L.cnt);
         if (L.ncnt > 1) {
           p.sk_gk = static_cast<int>(sk_gk(p.K));
-          p.sk_part = reinterpret_cast<float*>(in(0).p + L.part);
-          p.sk_cnt = reinterpret_cast<int*>(in(0).p + L.cnt) + 1;
-          p.sk_ml = in(0).p + L.ml;
+          p.sk_part = reinterpret_cast<float*>(ctl + L.part);
+          p.sk_cnt = reinterpret_cast<int*>(ctl + L.cnt) + 1;
+          p.sk_ml = ctl + L.ml;
         }
         chain_overlap(e, i, cx, p);
       }
@@ -716,8 +699,8 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         ep.stats_ss = e->fuse_malloc[i];
         ep.stats_sb1 = e->fuse_malloc[i] * ns;
         chain_overlap(e, i, cx, p);
-        const F2Layout L = f2_layout(e->fuse_balloc[i], e->fuse_malloc[i], p.N, e->fuse_split[i] != 0);
-        p.zero_word = reinterpret_cast<int*>(V[e->fuse_p[i]].p + L.cnt);
+        const F2Ctrl L = f2_ctrl(e->fuse_balloc[i], e->fuse_malloc[i], p.N, e->fuse_split[i] != 0);
+        p.zero_word = reinterpret_cast<int*>(e->ws + e->arena.f2_off[e->fuse_head[i]] + L.cnt);
         p.zero_n = chain_ctrl(e, i, cx) ? 1 : static_cast<int>(L.ncnt);
       }
     } else if (k == "tri_pv") {
@@ -746,14 +729,15 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         p.fuse_stats = reinterpret_cast<const float2*>(in(0).p);
         p.fuse_ss = e->fuse_malloc[i];
         p.fuse_sb1 = e->fuse_malloc[i] * ns;
-        const F2Layout L = f2_layout(e->fuse_balloc[i], e->fuse_malloc[i], p.K, e->fuse_split[i] != 0);
+        const F2Ctrl L = f2_ctrl(e->fuse_balloc[i], e->fuse_malloc[i], p.K, e->fuse_split[i] != 0);
+        char* ctl = e->ws + e->arena.f2_off[e->fuse_head[i]];
         p.etile = pp.p;
-        p.sched = reinterpret_cast<int*>(in(0).p + L.cnt);
+        p.sched = reinterpret_cast<int*>(ctl + L.cnt);
         if (L.ncnt > 1) {
           p.sk_gk = static_cast<int>(sk_gk(p.K));
-          p.sk_part = reinterpret_cast<float*>(in(0).p + L.part);
-          p.sk_cnt = reinterpret_cast<int*>(in(0).p + L.cnt) + 1;
-          p.sk_ml = in(0).p + L.ml;
+          p.sk_part = reinterpret_cast<float*>(ctl + L.part);
+          p.sk_cnt = reinterpret_cast<int*>(ctl + L.cnt) + 1;
+          p.sk_ml = ctl + L.ml;
         }
         chain_overlap(e, i, cx, p);
       }
@@ -788,6 +772,24 @@ int64_t ac_plan_workspace_bytes(const ac_chunk_plan* p, int32_t rank, int32_t wo
     return -1;
   }
   return build_arena(*p->g, p->plan, read_options()).size;
+}
+
+ac_status ac_plan_arena_profile(const ac_chunk_plan* p, int64_t* live_per_step, int64_t* live_peak,
+                                int64_t* control_bytes) {
+  if (!p) return set_error(AC_ERR_ARG, "ac_plan_arena_profile: NULL plan");
+  const Graph& g = *p->g;
+  const Arena A = build_arena(g, p->plan, read_options());
+  const int S = static_cast<int>(g.nodes.size());
+  if (live_per_step)
+    for (int s = 0; s < S; ++s) {
+      int64_t live = 0;
+      for (size_t t = 0; t < A.slot.size(); ++t)
+        if (A.slot[t].offset >= 0 && A.slot[t].birth <= s && s <= A.slot[t].death) live += A.slot[t].bytes;
+      live_per_step[s] = live;
+    }
+  if (live_peak) *live_peak = A.live_peak;
+  if (control_bytes) *control_bytes = A.size - A.act_size;
+  return AC_OK;
 }
 
 ac_status ac_plan_rank_chunks(const ac_chunk_plan* p, int32_t region, int32_t rank, int32_t world, int64_t* c0,
@@ -1004,6 +1006,8 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
   e->stats = ac_run_stats{};
   e->ev_node.clear();
   e->stats.workspace_high_water = e->arena.size;
+  e->stats.arena_live_peak = e->arena.live_peak;
+  e->stats.control_bytes = e->arena.size - e->arena.act_size;
   e->stats.planned_peak = estimate(g, e->plan.regions, false).peak;
   for (int t = 0; t < T; ++t)
     if (g.is_input[t] || g.is_output[t]) e->stats.caller_bytes += g.tensors[t].bytes();

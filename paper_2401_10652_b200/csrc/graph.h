@@ -140,6 +140,18 @@ struct Profile {
 
 Profile profile(const Graph& g);
 Profile estimate(const Graph& g, const std::vector<Region>& regions, bool contiguity);
+
+// f2 materialisation model (R25): a bf16 scores -> softmax(keys) -> PV chain
+// runs fused, S stored as pre-swizzled e-tiles (128-row x 64-key blocks of 16 KB),
+// P as the per-(row, 64-key slab) statistics (8 B each), P live from the scores
+// step, S until the PV step.  The estimator, the planner and the executor's arena
+// all use this one rule.
+struct F2Chain {
+  int scores, softmax, pv;
+};
+std::vector<F2Chain> f2_chains(const Graph& g, const std::vector<Region>& regions);
+int64_t f2_etile_bytes(const std::vector<int64_t>& s_shape);  // [..B.., M, nk]
+int64_t f2_stats_bytes(const std::vector<int64_t>& p_shape);  // [..B.., M, nk]
 void region_io(const Graph& g, int s, int e, std::vector<int>& ins, std::vector<int>& outs);
 bool candidate_for(const Graph& g, int s, int e, const std::vector<int>& assign, bool hoist, Region& out);
 Plan select_plan(const Graph& g, int64_t budget, const Params& p);

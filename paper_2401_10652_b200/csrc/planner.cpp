@@ -67,6 +67,24 @@ int64_t contiguity_cost(const TensorMeta& t, int dim, int64_t n) {
   return t.bytes() / E * ((E + n - 1) / n);
 }
 
+// materialised bytes of tensor t with dim d cut to ceil(E/n) (d < 0: whole):
+// the plain Eq. 2 charge bytes / E * ceil(E/n), or the f2 layouts (R25) of a fused
+// chain's S (e-tiles) and P (slab statistics) on the cut shape
+struct Mat {
+  std::vector<char> role;  // per tensor: 0 plain, 1 fused S, 2 fused P
+  int64_t bytes(const Graph& g, int t, int d, int64_t n) const {
+    const TensorMeta& tm = g.tensors[t];
+    if (role[t] == 0) {
+      if (d < 0) return tm.bytes();
+      const int64_t E = tm.shape[d];
+      return tm.bytes() / E * ((E + n - 1) / n);
+    }
+    std::vector<int64_t> sh = tm.shape;
+    if (d >= 0) sh[d] = (sh[d] + n - 1) / n;
+    return role[t] == 1 ? f2_etile_bytes(sh) : f2_stats_bytes(sh);
+  }
+};
+
 struct RegionInfo {
   const Region* r;
   std::vector<int> ins, outs, hout;
@@ -76,41 +94,33 @@ struct RegionInfo {
 };
 
 // live (tensor, bytes) at step s; tensor -1 = contiguity charge
-void live_at(const Graph& g, const Live& L, const RegionInfo* ri, int s, std::vector<std::pair<int, int64_t>>& out) {
+void live_at(const Graph& g, const Live& L, const Mat& M, const RegionInfo* ri, int s,
+             std::vector<std::pair<int, int64_t>>& out) {
   out.clear();
   const int T = static_cast<int>(g.tensors.size());
   if (!ri) {
     for (int t = 0; t < T; ++t)
-      if (!g.is_weight[t] && L.birth[t] <= s && s <= L.death[t]) out.push_back({t, g.tensors[t].bytes()});
+      if (!g.is_weight[t] && L.birth[t] <= s && s <= L.death[t]) out.push_back({t, M.bytes(g, t, -1, 1)});
     return;
   }
   const Region& r = *ri->r;
   for (int t : ri->ins)
-    if (!g.is_weight[t]) out.push_back({t, g.tensors[t].bytes()});
-  for (int t : ri->outs) out.push_back({t, g.tensors[t].bytes()});
-  for (int t : ri->hout) out.push_back({t, g.tensors[t].bytes()});
+    if (!g.is_weight[t]) out.push_back({t, M.bytes(g, t, -1, 1)});
+  for (int t : ri->outs) out.push_back({t, M.bytes(g, t, -1, 1)});
+  for (int t : ri->hout) out.push_back({t, M.bytes(g, t, -1, 1)});
   for (int t = 0; t < T; ++t) {
     if (g.is_weight[t] || ri->produced[t] || ri->consumed_in[t]) continue;
-    if (L.birth[t] <= s && s <= L.death[t]) out.push_back({t, g.tensors[t].bytes()});
+    if (L.birth[t] <= s && s <= L.death[t]) out.push_back({t, M.bytes(g, t, -1, 1)});
   }
   for (auto& it : ri->interior) {
     const int t = it.first;
-    if (it.second.first <= s && s <= it.second.second) {
-      const TensorMeta& tm = g.tensors[t];
-      const int d = r.dim_of(t);
-      if (d >= 0) {
-        const int64_t E = tm.shape[d];
-        out.push_back({t, tm.bytes() / E * ((E + r.n - 1) / r.n)});
-      } else {
-        out.push_back({t, tm.bytes()});
-      }
-    }
+    if (it.second.first <= s && s <= it.second.second) out.push_back({t, M.bytes(g, t, r.dim_of(t), r.n)});
   }
   if (ri->contig) out.push_back({-1, ri->contig});
 }
 
-Profile finish(const Graph& g, const Live& L, const std::vector<RegionInfo>& infos, const std::vector<int>& owner,
-               std::vector<int64_t> per) {
+Profile finish(const Graph& g, const Live& L, const Mat& M, const std::vector<RegionInfo>& infos,
+               const std::vector<int>& owner, std::vector<int64_t> per) {
   Profile p;
   p.per_step = std::move(per);
   if (p.per_step.empty()) return p;
@@ -120,7 +130,7 @@ Profile finish(const Graph& g, const Live& L, const std::vector<RegionInfo>& inf
   p.peak = p.per_step[ps];
   p.peak_step = ps;
   std::vector<std::pair<int, int64_t>> live;
-  live_at(g, L, owner[ps] >= 0 ? &infos[owner[ps]] : nullptr, ps, live);
+  live_at(g, L, M, owner[ps] >= 0 ? &infos[owner[ps]] : nullptr, ps, live);
   for (auto& lv : live) {
     if (lv.first >= 0 && g.is_input[lv.first]) p.x += lv.second;
     else if (lv.first >= 0 && g.is_output[lv.first]) p.y += lv.second;
@@ -152,10 +162,78 @@ void region_io(const Graph& g, int s, int e, std::vector<int>& ins, std::vector<
 
 Profile profile(const Graph& g) { return estimate(g, {}, false); }
 
+int64_t f2_etile_bytes(const std::vector<int64_t>& sh) {
+  int64_t B = 1;
+  for (size_t d = 0; d + 2 < sh.size(); ++d) B *= sh[d];
+  const int64_t M = sh[sh.size() - 2], nk = sh.back();
+  return B * ((M + 127) / 128) * ((nk + 63) / 64) * 16384;
+}
+
+int64_t f2_stats_bytes(const std::vector<int64_t>& sh) {
+  int64_t B = 1;
+  for (size_t d = 0; d + 2 < sh.size(); ++d) B *= sh[d];
+  const int64_t M = sh[sh.size() - 2], nk = sh.back();
+  return B * M * ((nk + 63) / 64) * 8;
+}
+
+std::vector<F2Chain> f2_chains(const Graph& g, const std::vector<Region>& regions) {
+  std::vector<F2Chain> out;
+  auto region_of = [&](int node) {
+    for (size_t r = 0; r < regions.size(); ++r)
+      if (regions[r].n > 1 && node >= regions[r].start && node <= regions[r].end) return static_cast<int>(r);
+    return -1;
+  };
+  for (int i = 0; i < static_cast<int>(g.nodes.size()); ++i) {
+    const Node& n = g.nodes[i];
+    const bool tri = n.kind == "tri_scores";
+    if (n.kind != "attn_scores" && !tri) continue;
+    const int s_t = n.output;
+    const int kd = static_cast<int>(g.tensors[s_t].shape.size()) - 1;  // key dim of S
+    if (g.tensors[s_t].dtype != DT::BF16 || g.is_output[s_t] || g.consumers[s_t].size() != 1) continue;
+    const int sm = g.consumers[s_t][0];
+    if (g.nodes[sm].kind != "softmax" || g.nodes[sm].ai("dim") != kd) continue;
+    const int p_t = g.nodes[sm].output;
+    if (g.is_output[p_t] || g.consumers[p_t].size() != 1) continue;
+    const int pv = g.consumers[p_t][0];
+    if (g.nodes[pv].kind != (tri ? "tri_pv" : "attn_pv") || g.nodes[pv].inputs[0] != p_t) continue;
+    // the PV on the BN = 32 / 64 tensor-core tile (head dim <= 64, 16-byte rows)
+    const int64_t dh = g.tensors[g.nodes[pv].output].shape.back(), nk = g.tensors[s_t].shape[kd];
+    if (dh > 64 || dh % 8 != 0 || nk < 64 || nk % 8 != 0) continue;
+    const int ri = region_of(i), rs = region_of(sm), rp = region_of(pv);
+    if (ri != rs || rs != rp) continue;
+    if (ri >= 0) {
+      const Region& R = regions[ri];
+      bool hoisted = false;
+      for (int h : R.hoisted) hoisted = hoisted || h == i || h == sm || h == pv;
+      if (hoisted) continue;
+      // S and P cut along the same dim (batch, heads or query rows), never the keys
+      const int ds = R.dim_of(s_t), dp = R.dim_of(p_t);
+      if (ds != dp || ds == kd) continue;
+    }
+    out.push_back({i, sm, pv});
+  }
+  return out;
+}
+
 Profile estimate(const Graph& g, const std::vector<Region>& regions, bool contiguity) {
-  const Live L = liveness(g);
+  Live L = liveness(g);
   const int S = static_cast<int>(g.nodes.size());
   const int T = static_cast<int>(g.tensors.size());
+  // f2 materialisation (R25): e-tile S and statistics P; P is written by the scores
+  // step, S read by the PV step
+  Mat M;
+  M.role.assign(T, 0);
+  const std::vector<F2Chain> chains = f2_chains(g, regions);
+  std::vector<int> f2_birth(T, -1), f2_death(T, -1);
+  for (const F2Chain& c : chains) {
+    const int s_t = g.nodes[c.scores].output, p_t = g.nodes[c.softmax].output;
+    M.role[s_t] = 1;
+    M.role[p_t] = 2;
+    L.birth[p_t] = std::min(L.birth[p_t], c.scores);
+    L.death[s_t] = std::max(L.death[s_t], c.pv);
+    f2_birth[p_t] = c.scores;
+    f2_death[s_t] = c.pv;
+  }
   std::vector<int> owner(S, -1);
   std::vector<RegionInfo> infos;
   infos.reserve(regions.size());
@@ -186,7 +264,8 @@ Profile estimate(const Graph& g, const std::vector<Region>& regions, bool contig
       int lastc = i;
       for (int c : g.consumers[t])
         if (c >= r.start && c <= r.end) lastc = std::max(lastc, c);
-      ri.interior.push_back({t, {i, lastc}});
+      if (f2_death[t] >= 0) lastc = std::max(lastc, f2_death[t]);
+      ri.interior.push_back({t, {f2_birth[t] >= 0 ? std::min(i, f2_birth[t]) : i, lastc}});
     }
     if (contiguity) {
       for (auto& p : r.xc) ri.contig += contiguity_cost(g.tensors[p.first], p.second, r.n);
@@ -198,12 +277,12 @@ Profile estimate(const Graph& g, const std::vector<Region>& regions, bool contig
   std::vector<int64_t> per(S, 0);
   std::vector<std::pair<int, int64_t>> live;
   for (int s = 0; s < S; ++s) {
-    live_at(g, L, owner[s] >= 0 ? &infos[owner[s]] : nullptr, s, live);
+    live_at(g, L, M, owner[s] >= 0 ? &infos[owner[s]] : nullptr, s, live);
     int64_t sum = 0;
     for (auto& lv : live) sum += lv.second;
     per[s] = sum;
   }
-  return finish(g, L, infos, owner, std::move(per));
+  return finish(g, L, M, infos, owner, std::move(per));
 }
 
 // ------------------------------------------------------------------ search

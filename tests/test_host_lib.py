@@ -243,3 +243,55 @@ def test_max_length_unbounded_budget_hits_cap():
     """budget -> infinity: both lengths reach the search cap, ratio 1."""
     got = api.max_length("transformer", 64, 4, 256, True, "bf16", 1 << 60, step=128, cap=1 << 14)
     assert got["unchunked"] == got["chunked"] == 1 << 14 and got["ratio"] == 1.0
+
+
+# ------------------------------------------------ R25: planned == arena + caller (no GPU)
+def _arena_cases():
+    from oracle import workloads
+    return [
+        (workloads.config("gpt"), None),
+        (workloads.config("unet"), None),
+        (workloads.config("af"), None),
+        (workloads.block("transformer", 1024, 256, 4, 512, True, "bf16", name="m"),
+         "region s=scores e=pv n=32 dims=0"),
+        (workloads.block("transformer", 1024, 256, 4, 512, True, "bf16", name="m"),
+         "region s=proj_q e=ffn2 n=4 dims=0"),
+        (workloads.block("attn_only", 4096, 256, 4, 0, False, "bf16", name="h"), "region s=scores e=pv n=4 dims=1"),
+        (workloads.tri_attn_pair(64, 128, 4, 32, "bf16", name="t"),
+         "region s=row_scores e=row_pv n=4 dims=0\nregion s=col_scores e=col_pv n=4 dims=1"),
+        (workloads.tri_attn_pair(64, 128, 4, 32, "bf16", name="t"),
+         "region s=row_scores e=row_pv n=2 dims=1\nregion s=col_scores e=col_pv n=2 dims=0"),
+        (workloads.transformer(512, 256, 4, 512, True, "bf16", name="st", layers=2), None),
+    ]
+
+
+@pytest.mark.parametrize("case", range(9))
+def test_arena_equals_planned_per_step(case):
+    """ac_plan_arena_profile (the arena ac_exec_create lays out) + the caller-held
+    inputs / outputs the oracle's Eq. 2 model has live at each step == the per-step
+    estimate, at EVERY step, for planned (ac_plan at 20 %) and user plans; and the
+    arena has no fragmentation at its peak."""
+    from oracle import graph as og_graph, memory, select
+    og, txt = _arena_cases()[case]
+    cg = api.graph_parse(og_graph.serialize(og))
+    if txt is None:
+        plan = api.ac_plan(cg, int(0.2 * memory.profile(og).peak_bytes))
+        regions = select.select(og, int(0.2 * memory.profile(og).peak_bytes)).regions
+    else:
+        plan = api.plan_parse(cg, "autochunk-plan 1\n" + txt + "\n")
+        from oracle import search
+        names = [n.id for n in og.nodes]
+        regions = [search.candidate_for(og, names.index(a), names.index(b), d).with_n(n)
+                   for a, b, n, d in oplan.parse_user_regions("autochunk-plan 1\n" + txt + "\n")]
+    live, peak, ctl = api.arena_profile(plan)
+    est = memory.estimate_with_plan(og, regions)
+    prof, per = api.estimate_memory(cg, plan)
+    assert per == est.per_step
+    callers = set(og.inputs) | set(og.outputs)
+    tot = []
+    for s_ in range(len(og.nodes)):
+        caller = sum(b for t, b in est.live_sets[s_].items() if t in callers)
+        assert live[s_] + caller == est.per_step[s_], (s_, og.nodes[s_].id, live[s_], caller, est.per_step[s_])
+        tot.append(live[s_] + caller)
+    assert max(tot) == prof.peak_bytes and max(live) == peak
+    assert plan.workspace_bytes() - ctl == peak   # size-ordered first fit: no holes at the peak

@@ -145,10 +145,12 @@ def test_monotone_in_n():
 
 
 def test_gpt_closed_form_peaks():
-    """unchunked softmax step = 2 N d b + 2 h N^2 b; minimal attention
-    region at n chunks = 5 N d b + 2 h N ceil(N/n) b."""
-    N, d, h, b = 16384, 1024, 16, 2
-    g = workloads.config("gpt")
+    """SURVEY App. A, plain Eq. 1 / Eq. 2 (fp32 GPT: no fused chain): unchunked softmax
+    step = 2 N d b + 2 h N^2 b; minimal attention region at n chunks =
+    5 N d b + 2 h N ceil(N/n) b."""
+    N, d, h, b = 16384, 1024, 16, 4
+    g = workloads.config("gpt", dtype="f32")
+    assert memory.f2_chains(g) == []
     p = memory.profile(g)
     assert p.peak_bytes == 2 * N * d * b + 2 * h * N * N * b and p.peak_node == "softmax"
     names = [n.id for n in g.nodes]
@@ -156,3 +158,25 @@ def test_gpt_closed_form_peaks():
     for n in (4, 8, 16):
         est = memory.estimate_with_plan(g, [r.with_n(n)])
         assert est.peak_bytes == 5 * N * d * b + 2 * h * N * (-(-N // n)) * b
+
+
+def test_gpt_f2_closed_form_peaks():
+    """R25 on the bf16 GPT block: the chain is fused, S is its e-tiles (N, N multiples
+    of 128 / 64: exactly h N^2 bf16), P its slab statistics h N (N/64) 8 B written by
+    the scores step.  Unchunked peak at the scores step = x + q + k + v^T + S + P =
+    4 N d 2 + 2 h N^2 + 8 h N N/64; the attention region at n chunks holds x, q, k,
+    v^T and o whole plus one chunk of S and P: 5 N d 2 + (2 h N + 8 h N/64) ceil(N/n)."""
+    N, d, h = 16384, 1024, 16
+    g = workloads.config("gpt")
+    names = [n.id for n in g.nodes]
+    assert memory.f2_chains(g) == [(names.index("scores"), names.index("softmax"), names.index("pv"))]
+    p = memory.profile(g)
+    assert p.peak_bytes == 4 * N * d * 2 + 2 * h * N * N + 8 * h * N * (N // 64) and p.peak_node == "scores"
+    r = search.candidate_for(g, names.index("scores"), names.index("pv"), (0,))
+    for n in (4, 8, 16):
+        est = memory.estimate_with_plan(g, [r.with_n(n)])
+        L = -(-N // n)
+        assert est.peak_bytes == 5 * N * d * 2 + (2 * h * N + 8 * h * (N // 64)) * L
+    # a chunk of 32 rows pads its e-tiles to 128 rows (ADVICE r1 medium): charged so
+    est = memory.estimate_with_plan(g, [r.with_n(N // 32)])
+    assert est.peak_bytes == 5 * N * d * 2 + 2 * h * 128 * N + 8 * h * 32 * (N // 64)
