@@ -31,8 +31,11 @@ WORKLOADS = {
            "budget = 20% of unchunked activation (BASELINE.json configs[1])",
     "vit": "ViT-Large encoder block, 65536 tokens, hidden 1024, 16 heads, FFN 4096, bf16, budget 20%",
     "unet": "UNet self-attention, 16384 tokens, hidden 640, 10 heads, bf16, budget 20%",
-    "af": "AlphaFold triangle attention pair (rows then columns), N_res 1024, c_z 128, 4 heads, c 32, bf16, "
-          "budget 20% (tokens = pair positions N_res^2)",
+    "af": "AlphaFold Evoformer pair stack (triangle multiplication outgoing / incoming, triangle attention "
+          "starting / ending node, pair transition), N_res 1024, c_z 128, 4 heads, c 32, bf16, budget 20% "
+          "(BASELINE.json configs[3]; tokens = pair positions N_res^2)",
+    "af_attn": "AlphaFold triangle attention pair (rows then columns), N_res 1024, c_z 128, 4 heads, c 32, bf16, "
+               "budget 20% (tokens = pair positions N_res^2)",
     "tiny": "tiny attention+MLP block, seq 256, hidden 64, 2 heads, fp32, chunk 32 along seq",
     "gpt_fa": "GPT-style decoder block with fused attention (NEXT f1, P:350-351), seq 16384, hidden 1024, "
               "16 heads, FFN 4096, causal, bf16, budget 90% of its unchunked activation",
@@ -127,7 +130,8 @@ BLOCKS = {
     "tiny": ("transformer", 256, 64, 2, 256, False, "f32"),
     "gpt": ("transformer", 16384, 1024, 16, 4096, True, "bf16"),
     "vit": ("transformer", 65536, 1024, 16, 4096, False, "bf16"),
-    "af": ("tri_attn_pair", 1024, 128, 4, 32, False, "bf16"),
+    "af": ("evoformer_pair", 1024, 128, 4, 32, False, "bf16"),
+    "af_attn": ("tri_attn_pair", 1024, 128, 4, 32, False, "bf16"),
     "unet": ("attn_only", 16384, 640, 10, 0, False, "bf16"),
     "gpt_fa": ("transformer_fa", 16384, 1024, 16, 4096, True, "bf16"),
 }
@@ -149,7 +153,7 @@ def oracle_graph(name, layers=1):
 
 def tokens_per_step(name, doc):
     shp = doc.tensors[doc.inputs[0]][1]
-    return shp[0] * shp[1] if name == "af" else shp[0]
+    return shp[0] * shp[1] if name in ("af", "af_attn") else shp[0]
 
 
 def device_inputs(doc, torch):
@@ -163,6 +167,26 @@ def device_inputs(doc, torch):
         else:
             dev[t] = torch.from_numpy(np.ascontiguousarray(s.storage)).cuda()
     return samples, dev
+
+
+def device_inputs_gpu(doc, torch, seed=0):
+    """Inputs of the synth recipe's distributions, drawn on the device
+    with torch's generator: for capacity runs at lengths whose host-side fp64 copies
+    would not fit in host memory (no oracle comparison is made on them)."""
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(seed)
+    TD = {"bf16": torch.bfloat16, "f32": torch.float32}
+    dev = {}
+    for t, kind, dt, shp, role, fan in doc.input_specs():
+        v = torch.randn(shp, generator=gen, device="cuda", dtype=torch.float32)
+        if role == "matrix":
+            v *= 1.0 / max(fan, 1) ** 0.5
+        elif role in ("bias", "ln_beta"):
+            v *= 0.02
+        elif role == "ln_gamma":
+            v = 1.0 + 0.02 * v
+        dev[t] = v.to(TD[dt])
+    return dev
 
 
 # ------------------------------------------------------------------ roofline bookkeeping
@@ -210,7 +234,10 @@ def algorithmic(doc, node_id):
         Nk = doc.tensors[ins[1]][1][0]
         pairs = N * (N + 1) // 2 if attrs.get("causal") == "1" else N * Nk
         return "tensor", 4 * h * dh * pairs
-    if kind in ("tri_scores", "tri_pv", "layernorm"):
+    if kind == "tri_mul":        # batched GEMM over channels: 2 C I J K
+        C_, I, K = doc.tensors[ins[0]][1]
+        return "tensor", 2 * C_ * I * K * doc.tensors[ins[1]][1][1]
+    if kind in ("tri_scores", "tri_pv", "layernorm", "ln_cfirst"):
         return "hbm", sum(B(t) for t in ins) + B(out)
     return "hbm", B(out)
 
@@ -231,16 +258,18 @@ def cpu_baseline(name, og, samples, budget_s=20.0):
         return {"value": len(rows) / dt, "unit": "tokens/s", "cores": cores, "kind": "oracle",
                 "sample": f"{len(rows)} output rows of the {name} block incl. LN1/K/V of all {N} rows "
                           f"(fp64 numpy, {dt:.1f} s)"}
-    if name == "af":
+    if name in ("af", "af_attn"):
         from oracle import workloads
-        small = workloads.tri_attn_pair(128, 128, 4, 32, "bf16", name="af_sample")
+        mk = workloads.evoformer_pair if name == "af" else workloads.tri_attn_pair
+        small = mk(128, 128, 4, 32, "bf16", name="af_sample")
         import synth
         v = {t: s.value for t, s in synth.make_inputs(small.input_specs(), 0).items()}
         t0 = time.perf_counter()
         executor.run(small, v)
         dt = time.perf_counter() - t0
         return {"value": 128 * 128 / dt, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                "sample": f"full AF triangle-attention pair at N_res=128 (fp64 numpy, {dt:.1f} s)"}
+                "sample": f"the full {small.name} block at N_res=128 (fp64 numpy, {dt:.1f} s); the work per pair "
+                          f"grows with N_res, so this overstates the oracle's rate at 1024"}
     return None
 
 
@@ -263,15 +292,16 @@ def reference_arm(args):
     for k in range(args.warmup + args.steps):
         rows = (np.arange(R) * (N // R) + k) % N
         t0 = time.perf_counter()
-        if args.config == "af":
+        if args.config in ("af", "af_attn"):
             from oracle import executor, workloads
-            small = workloads.tri_attn_pair(64, 128, 4, 32, "bf16", name="af_sample")
+            mk = workloads.evoformer_pair if args.config == "af" else workloads.tri_attn_pair
+            small = mk(64, 128, 4, 32, "bf16", name="af_sample")
             executor.run(small, {t: s.value for t, s in synth.make_inputs(small.input_specs(), 0).items()})
         else:
             blocks.transformer_rows(og, vals, rows)
         if k >= args.warmup:
             times.append(time.perf_counter() - t0)
-    units = 64 * 64 if args.config == "af" else R
+    units = 64 * 64 if args.config in ("af", "af_attn") else R
     tot = sum(times)
     value = units * len(times) / tot
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
@@ -300,19 +330,20 @@ def maxlen_arm(args):
     wbytes = sum(doc0.nbytes(w[0]) for w in doc0.weights)
     free, total = torch.cuda.mem_get_info()
     budget = free - wbytes - (2 << 30)
-    step = 64 if kind == "tri_attn_pair" else 128
-    cap = (1 << 15) if kind == "tri_attn_pair" else (1 << 23)
+    pair = kind in ("tri_attn_pair", "evoformer_pair")
+    step = 64 if pair else 128
+    cap = (1 << 15) if pair else (1 << 23)
     t0 = time.perf_counter()
     ml = api.max_length(kind, d, h, f, causal, dt, budget, layers=args.layers, step=step, cap=cap)
     t_search = time.perf_counter() - t0
     run = None
     Nr = min(args.maxlen_run, ml["chunked"]) if ml["chunked"] else 0
-    if Nr and kind != "tri_attn_pair":
+    if Nr:
         cg, doc = c_graph(args.config, args.layers, N=Nr)
         prof0, _ = api.estimate_memory(cg)
         plan = api.ac_plan(cg, budget)
         profp, _ = api.estimate_memory(cg, plan)
-        _, dev = device_inputs(doc, torch)
+        dev = device_inputs_gpu(doc, torch)   # (host-free: the capacity run checks finiteness only)
         TD = {"bf16": torch.bfloat16, "f32": torch.float32}
         outs = {o: torch.empty(doc.tensors[o][1], dtype=TD[doc.tensors[o][0]], device="cuda") for o in doc.outputs}
         torch.cuda.synchronize()
@@ -336,16 +367,22 @@ def maxlen_arm(args):
                "ms": round(ms, 3), "tokens_per_s": round(Nr / (ms / 1e3), 1),
                "planned_peak_bytes": profp.peak_bytes, "unchunked_peak_bytes": prof0.peak_bytes,
                "workspace_bytes": ex.stats().workspace_high_water,
-               "measured_peak_bytes": ex.stats().arena_live_peak + profp.x_bytes + profp.y_bytes,
+               "arena_live_peak": ex.stats().arena_live_peak,
                "torch_peak_delta_bytes": torch.cuda.max_memory_allocated() - base,
                "output_finite": bool(torch.isfinite(y.float()).all().item())}
     line = {"metric": "max inference length under this GPU's HBM (P:357-361)", "value": ml["chunked"],
-            "unit": "tokens" if kind != "tri_attn_pair" else "residues", "n_gpus": 1,
+            "unit": "tokens" if not pair else "residues", "n_gpus": 1,
             "higher_is_better": True, "dtype": dt, "data": "synthetic",
             "config": {"workload": WORKLOADS[args.config] + (f", {args.layers} stacked blocks" if args.layers > 1 else ""),
                        "activation_budget_bytes": budget, "hbm_free_bytes": free, "weights_bytes": wbytes,
                        "length_step": step, "search_cap": cap},
-            "unchunked_max": ml["unchunked"], "ratio": ml["ratio"], "plan_at_max": ml["plan"],
+            "unchunked_max": ml["unchunked"], "ratio": ml["ratio"],
+            # the paper's 2D models (ViT, UNet images; AlphaFold pair representation) extend a
+            # side length: tokens grow with its square for ViT / UNet, residues are the side
+            "side_ratio": (ml["ratio"] ** 0.5 if args.config in ("vit", "unet") else ml["ratio"])
+            if ml["ratio"] else None,
+            "dims": 1 if args.config in ("gpt", "gpt_fa", "tiny") else 2,
+            "plan_at_max": ml["plan"],
             "search_s": round(t_search, 2), "run": run,
             "paper": {"claim": "11.7x (1D) / 3.2x avg (2D) max-length extension", "hardware": "A100 80GB (P:336)"}}
     print(json.dumps(line))

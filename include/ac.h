@@ -65,14 +65,17 @@ typedef enum ac_block_kind {
   AC_BLOCK_ATTN_ONLY = 1,     /* pre-LN attention + residual only (UNet self-attention) */
   AC_BLOCK_TRI_ATTN_PAIR = 2, /* AlphaFold triangle attention, starting then ending node */
   AC_BLOCK_TRANSFORMER_FA = 3, /* transformer with attention as one fused kernel (NEXT f1) */
-  AC_BLOCK_ATTN_ONLY_FA = 4    /* attn_only with the fused attention kernel */
+  AC_BLOCK_ATTN_ONLY_FA = 4,   /* attn_only with the fused attention kernel */
+  AC_BLOCK_EVOFORMER_PAIR = 5  /* AlphaFold Evoformer pair stack (AF2 Alg. 6 l. 13-17): triangle
+                                  multiplication outgoing / incoming (c = 128), triangle attention
+                                  starting / ending node, pair transition (n = 4) (NEXT f3) */
 } ac_block_kind;
 
 typedef enum ac_dtype { AC_F32 = 0, AC_BF16 = 1, AC_F64 = 2 } ac_dtype;
 
 /* Workload templates of BASELINE.json (the SPEC cmd_corpus analog).
  * transformer/attn_only: N tokens, d model width, h heads, f FFN width.
- * tri_attn_pair: N residues, d = c_z, h = heads, f = per-head width c. */
+ * tri_attn_pair, evoformer_pair: N residues, d = c_z, h = heads, f = per-head width c. */
 typedef struct ac_block_desc {
   int32_t kind;      /* ac_block_kind */
   int64_t N, d, h, f;
@@ -145,6 +148,15 @@ void ac_cost_params_default(ac_cost_params* p);
  * AC_OK: feasible plan.  AC_ERR_BUDGET: *out holds the best-effort plan.
  * Errors: AC_ERR_ARG. */
 ac_status ac_plan(const ac_graph* g, int64_t mem_budget_bytes, const ac_cost_params* params, ac_chunk_plan** out);
+
+/* Max inference length (the paper's 1D / 2D length extension; SPEC
+ * cmd_maxlen S:478-486): the largest multiple of `step` (<= cap) of the block's
+ * sequence length N (residues for the pair blocks) whose unchunked Eq. 1 peak
+ * (*unchunked), resp. whose ac_plan peak under `params` (*chunked), is strictly
+ * below `budget` activation bytes.  Doubling then bisection; 0 when even
+ * `step` does not fit.  Errors: AC_ERR_ARG, AC_ERR_GRAPH. */
+ac_status ac_max_length(const ac_block_desc* desc, int64_t budget, int64_t step, int64_t cap,
+                        const ac_cost_params* params, int64_t* unchunked, int64_t* chunked);
 
 /* User-fixed plan: "autochunk-plan 1" followed by lines
  *   region s=<node id> e=<node id> n=<chunks> dims=<d,...>

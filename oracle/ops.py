@@ -122,7 +122,7 @@ REDUCE = ("reduce_sum", "reduce_mean", "reduce_max")
 SOURCE = ("input", "weight")
 ALL_KINDS = SOURCE + ("matmul",) + ELEMENTWISE2 + UNARY + ("softmax", "layernorm") + REDUCE + (
     "transpose", "reshape", "concat", "slice",
-    "linear", "attn_scores", "attn_pv", "tri_scores", "tri_pv", "attn_fused")
+    "linear", "attn_scores", "attn_pv", "tri_scores", "tri_pv", "attn_fused", "tri_mul", "ln_cfirst")
 
 # attribute schema: name -> type tag ("int", "float", "ints", "str", "ranges")
 ATTR_SCHEMA = {
@@ -134,7 +134,8 @@ ATTR_SCHEMA = {
     "concat": {"dim": "int"},
     "slice": {"ranges": "ranges"},
     "linear": {"kin": "int", "out": "ints", "act": "str", "trans": "int", "swap": "int",
-               "bias": "int", "res": "int"},
+               "bias": "int", "res": "int", "gate": "int"},
+    "ln_cfirst": {"eps": "float"},
     "attn_scores": {"scale": "float", "causal": "int"},
     "attn_fused": {"scale": "float", "causal": "int"},
     "tri_scores": {"scale": "float", "ending": "int"},
@@ -142,7 +143,8 @@ ATTR_SCHEMA = {
 }
 
 ARITY = {"matmul": (2, 2), "softmax": (1, 1), "layernorm": (3, 3), "transpose": (1, 1),
-         "reshape": (1, 1), "concat": (1, 64), "slice": (1, 1), "linear": (2, 4),
+         "reshape": (1, 1), "concat": (1, 64), "slice": (1, 1), "linear": (2, 5),
+         "tri_mul": (2, 2), "ln_cfirst": (3, 3),
          "attn_scores": (2, 2), "attn_pv": (2, 2), "tri_scores": (3, 3), "tri_pv": (3, 3),
          "attn_fused": (3, 3)}
 for _k in ELEMENTWISE2:
@@ -152,7 +154,7 @@ for _k in UNARY + REDUCE:
 
 
 def linear_arity(attrs) -> int:
-    return 2 + int(attrs.get("bias", 0)) + int(attrs.get("res", 0))
+    return 2 + int(attrs.get("bias", 0)) + int(attrs.get("gate", 0)) + int(attrs.get("res", 0))
 
 
 def _linear_rows(attrs, a_shape):
@@ -247,6 +249,10 @@ def shape(kind: str, attrs: dict, ins) -> tuple:
             if ins[i] != (prod(out),):
                 raise ValueError("linear bias shape mismatch")
             i += 1
+        if attrs.get("gate", 0):   # elementwise gate in the output's layout
+            if ins[i] != res:
+                raise ValueError("linear gate shape mismatch")
+            i += 1
         if attrs.get("res", 0):
             if ins[i] != res:
                 raise ValueError("linear residual shape mismatch")
@@ -283,6 +289,19 @@ def shape(kind: str, attrs: dict, ins) -> tuple:
         if (k[0], k[2], k[3]) != (I, H, c) or b != (H, J, k[1]):
             raise ValueError("tri_scores shape mismatch")
         return (I, H, J, k[1])
+    if kind == "tri_mul":
+        # AF2 Alg. 11 / 12 line 4, channel-major: x[c, i, j] = sum_k a[c, i, k] b[c, j, k]
+        a, b = ins
+        if len(a) != 3 or len(b) != 3 or a[0] != b[0] or a[2] != b[2]:
+            raise ValueError("tri_mul shape mismatch")
+        return (a[0], a[1], b[1])
+    if kind == "ln_cfirst":
+        # LayerNorm over the leading (channel) dim, written channel-last:
+        # y[i, j, :] = LN(x[:, i, j]) (AF2 Alg. 11 line 4, the LN of the product)
+        x, gm, bt = ins
+        if len(x) != 3 or gm != (x[0],) or bt != gm:
+            raise ValueError("ln_cfirst shape mismatch")
+        return (x[1], x[2], x[0])
     if kind == "tri_pv":
         p, vt, g = ins
         if len(p) != 4 or len(vt) != 4 or len(g) != 4:
@@ -325,7 +344,8 @@ def flops(kind: str, attrs: dict, ins, out) -> int:
         R = prod(a[: len(a) - kin])
         K = prod(a[len(a) - kin:])
         O = prod(attrs["out"])
-        extra = int(attrs.get("bias", 0)) + int(attrs.get("act", "none") != "none") + int(attrs.get("res", 0))
+        extra = (int(attrs.get("bias", 0)) + int(attrs.get("act", "none") != "none") + int(attrs.get("gate", 0))
+                 + int(attrs.get("res", 0)))
         return 2 * R * K * O + R * O * extra
     if kind == "attn_scores":     # matmul + scale mul (+ causal mask add)
         q = ins[0]
@@ -342,6 +362,11 @@ def flops(kind: str, attrs: dict, ins, out) -> int:
     if kind == "tri_pv":
         p = ins[0]
         return 2 * prod(p) * out[3] + ne
+    if kind == "tri_mul":         # a batched matmul over channels
+        a = ins[0]
+        return 2 * prod(a) * out[2]
+    if kind == "ln_cfirst":       # transpose (0) + layernorm (8 / element)
+        return 8 * ne
     raise ValueError(kind)
 
 
@@ -406,6 +431,8 @@ def propagate(kind: str, attrs: dict, ins, out, d: int):
         res = [ad, NC]
         if attrs.get("bias", 0):
             res.append(NC)
+        if attrs.get("gate", 0):
+            res.append(d)
         if attrs.get("res", 0):
             res.append(d)
         return res
@@ -415,6 +442,10 @@ def propagate(kind: str, attrs: dict, ins, out, d: int):
         return [[1, NC], [0, 0], [NC, 1]][d]
     if kind == "attn_fused":
         return [[0, NC, NC], [1, 1, 0], [NC, NC, 1]][d]
+    if kind == "tri_mul":
+        return [[0, 0], [1, NC], [NC, 1]][d]
+    if kind == "ln_cfirst":
+        return [[1, NC, NC], [2, NC, NC], [BREAK, BREAK, BREAK]][d]
     if kind == "tri_scores":
         if attrs.get("ending", 0):
             return [[1, 1, NC], [2, 2, 0], [0, NC, 1], [NC, 0, 2]][d]
@@ -514,6 +545,12 @@ def evaluate(kind: str, attrs: dict, vals, ctx=None) -> np.ndarray:
         Q = np.transpose(q, (0, 2, 1, 3))       # [I,H,J,c]
         Kk = np.transpose(k, (0, 2, 1, 3))      # [I,H,K,c]
         return _bdot(Q, Kk) * sc + b[None]
+    if kind == "tri_mul":
+        a, b = vals
+        return _bdot(a, b)                       # [C, I, K] x [C, J, K] -> [C, I, J]
+    if kind == "ln_cfirst":
+        x, gm, bt = vals
+        return _layernorm(np.moveaxis(x, 0, -1), gm, bt, 1, attrs["eps"])
     if kind == "tri_pv":
         p, vt, g = vals
         V = np.transpose(vt, (2, 0, 1, 3))      # [I|J, H, c, K]
@@ -551,6 +588,9 @@ def _linear(attrs, vals):
     if attrs.get("trans", 0):
         nr = len(rows)
         y = np.ascontiguousarray(np.transpose(y, tuple(range(nr, nr + len(out))) + tuple(range(nr))))
+    if attrs.get("gate", 0):
+        y = y * vals[i]
+        i += 1
     if attrs.get("res", 0):
         y = y + vals[i]
     return y

@@ -128,12 +128,84 @@ def tri_attn_pair(N, cz=128, H=4, c=32, dtype="bf16", name="af_pair", layers=1) 
     return B.build()
 
 
+def _tri_mul(B: Builder, z: str, pre: str, cz: int, cm: int, incoming: int, out: str, eps=1e-5):
+    """Triangular multiplicative update, AF2 supplement Alg. 11 (outgoing edges,
+    x_ij = sum_k a_ik b_jk) / Alg. 12 (incoming, x_ij = sum_k a_ki b_jk):
+    zn = LN(z); a = sigmoid(Linear(zn)) * Linear(zn); b likewise; g = sigmoid(Linear(zn));
+    z + g * Linear(LN(x)).  a and b are written channel-major [c, i, k] ([c, j, k])
+    so the product is a batched K-major GEMM; the incoming edges read z transposed
+    (`swap`), so both updates share one kind (tri_mul)."""
+    P = (lambda s_: pre + s_)
+    for nm, shp, role, fan in (("ln_g", (cz,), "ln_gamma", cz), ("ln_b", (cz,), "ln_beta", cz),
+                               ("wag", (cm, cz), "matrix", cz), ("bag", (cm,), "bias", cz),
+                               ("wa", (cm, cz), "matrix", cz), ("ba", (cm,), "bias", cz),
+                               ("wbg", (cm, cz), "matrix", cz), ("bbg", (cm,), "bias", cz),
+                               ("wb", (cm, cz), "matrix", cz), ("bb", (cm,), "bias", cz),
+                               ("wg", (cz, cz), "matrix", cz), ("bg", (cz,), "bias", cz),
+                               ("lnx_g", (cm,), "ln_gamma", cm), ("lnx_b", (cm,), "ln_beta", cm),
+                               ("wo", (cz, cm), "matrix", cm), ("bo", (cz,), "bias", cm)):
+        B.weight(P(nm), shp, role, fan)
+    B.op("layernorm", [z, P("ln_g"), P("ln_b")], P("zn"), nid=P("ln"), naxes=1, eps=eps)
+    sw = int(incoming)
+    B.op("linear", [P("zn"), P("wag"), P("bag")], P("ag"), nid=P("proj_ag"), kin=1, out=[cm], act="sigmoid",
+         trans=1, swap=sw, bias=1, res=0)
+    B.op("linear", [P("zn"), P("wa"), P("ba"), P("ag")], P("a"), nid=P("proj_a"), kin=1, out=[cm], act="none",
+         trans=1, swap=sw, bias=1, res=0, gate=1)
+    B.op("linear", [P("zn"), P("wbg"), P("bbg")], P("bgt"), nid=P("proj_bg"), kin=1, out=[cm], act="sigmoid",
+         trans=1, swap=sw, bias=1, res=0)
+    B.op("linear", [P("zn"), P("wb"), P("bb"), P("bgt")], P("b"), nid=P("proj_b"), kin=1, out=[cm], act="none",
+         trans=1, swap=sw, bias=1, res=0, gate=1)
+    B.op("linear", [P("zn"), P("wg"), P("bg")], P("g"), nid=P("proj_g"), kin=1, out=[cz], act="sigmoid",
+         trans=0, swap=0, bias=1, res=0)
+    B.op("tri_mul", [P("a"), P("b")], P("x"), nid=P("mul"))
+    B.op("ln_cfirst", [P("x"), P("lnx_g"), P("lnx_b")], P("xn"), nid=P("lnx"), eps=eps)
+    B.op("linear", [P("xn"), P("wo"), P("bo"), P("g"), z], out, nid=P("proj_o"), kin=1, out=[cz], act="none",
+         trans=0, swap=0, bias=1, res=1, gate=1)
+
+
+def _transition(B: Builder, z: str, pre: str, cz: int, nf: int, out: str, eps=1e-5):
+    """Pair transition, AF2 Alg. 15: z + Linear(relu(Linear(LN(z)))), hidden n * c_z."""
+    P = (lambda s_: pre + s_)
+    for nm, shp, role, fan in (("ln_g", (cz,), "ln_gamma", cz), ("ln_b", (cz,), "ln_beta", cz),
+                               ("w1", (nf * cz, cz), "matrix", cz), ("b1", (nf * cz,), "bias", cz),
+                               ("w2", (cz, nf * cz), "matrix", nf * cz), ("b2", (cz,), "bias", nf * cz)):
+        B.weight(P(nm), shp, role, fan)
+    B.op("layernorm", [z, P("ln_g"), P("ln_b")], P("zn"), nid=P("ln"), naxes=1, eps=eps)
+    B.op("linear", [P("zn"), P("w1"), P("b1")], P("h"), nid=P("ffn1"), kin=1, out=[nf * cz], act="relu",
+         trans=0, swap=0, bias=1, res=0)
+    B.op("linear", [P("h"), P("w2"), P("b2"), z], out, nid=P("ffn2"), kin=1, out=[cz], act="none",
+         trans=0, swap=0, bias=1, res=1)
+
+
+def evoformer_pair(N, cz=128, H=4, c=32, dtype="bf16", name="evoformer_pair", layers=1, cm=128, nf=4) -> Graph:
+    """The Evoformer pair stack (AF2 Alg. 6 lines 13-17, dropout at inference =
+    identity): z += TriangleMultiplicationOutgoing(z); z += ...Incoming(z);
+    z += TriangleAttentionStartingNode(z); z += ...EndingNode(z); z += PairTransition(z);
+    `layers` such stacks in sequence."""
+    B = Builder(name, dtype)
+    B.input("z", (N, N, cz))
+    z = "z"
+    for i in range(max(1, layers)):
+        p = _prefix(layers, i)
+        _tri_mul(B, z, p + "mo_", cz, cm, 0, p + "z1")
+        _tri_mul(B, p + "z1", p + "mi_", cz, cm, 1, p + "z2")
+        _tri_weights(B, p + "row_", cz, H, c)
+        _tri_weights(B, p + "col_", cz, H, c)
+        _tri_attention(B, p + "z2", p + "row_", N, cz, H, c, 0, p + "z3")
+        _tri_attention(B, p + "z3", p + "col_", N, cz, H, c, 1, p + "z4")
+        _transition(B, p + "z4", p + "tr_", cz, nf, p + "z5")
+        z = p + "z5"
+    B.output(z)
+    return B.build()
+
+
 CONFIGS = {
     # BASELINE.json configs[0..4] (DESIGN.md §Workloads)
     "tiny": dict(kind="transformer", N=256, d=64, h=2, f=256, causal=False, dtype="f32"),
     "gpt": dict(kind="transformer", N=16384, d=1024, h=16, f=4096, causal=True, dtype="bf16"),
     "vit": dict(kind="transformer", N=65536, d=1024, h=16, f=4096, causal=False, dtype="bf16"),
-    "af": dict(kind="tri_attn_pair", N=1024, d=128, h=4, f=32, causal=False, dtype="bf16"),
+    "af": dict(kind="evoformer_pair", N=1024, d=128, h=4, f=32, causal=False, dtype="bf16"),
+    "af_attn": dict(kind="tri_attn_pair", N=1024, d=128, h=4, f=32, causal=False, dtype="bf16"),
     "unet": dict(kind="attn_only", N=16384, d=640, h=10, f=0, causal=False, dtype="bf16"),
     "unet_h8": dict(kind="attn_only", N=16384, d=640, h=8, f=0, causal=False, dtype="bf16"),
     # NEXT f1: the GPT block with a fused attention kernel (the paper's second regime)
@@ -152,6 +224,8 @@ def block(kind, N, d, h, f=0, causal=False, dtype="bf16", name=None, layers=1) -
         return transformer(N, d, h, 0, causal, dtype, True, name or "attn_only_fa", layers=layers, fused=True)
     if kind == "tri_attn_pair":
         return tri_attn_pair(N, d, h, f, dtype, name or "af_pair", layers=layers)
+    if kind == "evoformer_pair":
+        return evoformer_pair(N, d, h, f, dtype, name or "evoformer_pair", layers=layers)
     raise ValueError(kind)
 
 

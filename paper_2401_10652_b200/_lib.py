@@ -17,7 +17,7 @@ STATUS_NAMES = ["AC_OK", "AC_ERR_ARG", "AC_ERR_GRAPH", "AC_ERR_BUDGET", "AC_ERR_
                 "AC_ERR_BIND", "AC_ERR_CUDA", "AC_ERR_NCCL", "AC_ERR_WORKSPACE"]
 AC_F32, AC_BF16, AC_F64 = 0, 1, 2
 AC_BLOCK_TRANSFORMER, AC_BLOCK_ATTN_ONLY, AC_BLOCK_TRI_ATTN_PAIR = 0, 1, 2
-AC_BLOCK_TRANSFORMER_FA, AC_BLOCK_ATTN_ONLY_FA = 3, 4
+AC_BLOCK_TRANSFORMER_FA, AC_BLOCK_ATTN_ONLY_FA, AC_BLOCK_EVOFORMER_PAIR = 3, 4, 5
 AC_FLAG_NO_HOIST, AC_FLAG_NO_DENSITY, AC_FLAG_NO_STRIDE, AC_FLAG_NO_NODES, AC_FLAG_NO_FLOPS, \
     AC_FLAG_CONTIGUITY = 1, 2, 4, 8, 16, 32
 
@@ -96,6 +96,8 @@ SIGNATURES = [
     ("ac_plan_free", None, [P]),
     ("ac_plan_num_regions", C.c_int32, [P]),
     ("ac_plan_workspace_bytes", C.c_int64, [P, C.c_int32, C.c_int32]),
+    ("ac_max_length", C.c_int, [C.POINTER(BlockDesc), C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
+                                C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("ac_plan_arena_profile", C.c_int, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("ac_plan_rank_chunks", C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int64),
                                       C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),

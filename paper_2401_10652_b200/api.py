@@ -18,7 +18,7 @@ from ._lib import check, lib
 DTYPES = {"f32": L.AC_F32, "bf16": L.AC_BF16, "f64": L.AC_F64}
 KINDS = {"transformer": L.AC_BLOCK_TRANSFORMER, "attn_only": L.AC_BLOCK_ATTN_ONLY,
          "tri_attn_pair": L.AC_BLOCK_TRI_ATTN_PAIR, "transformer_fa": L.AC_BLOCK_TRANSFORMER_FA,
-         "attn_only_fa": L.AC_BLOCK_ATTN_ONLY_FA}
+         "attn_only_fa": L.AC_BLOCK_ATTN_ONLY_FA, "evoformer_pair": L.AC_BLOCK_EVOFORMER_PAIR}
 
 
 class Graph:
@@ -250,44 +250,17 @@ class Exec:
 
 def max_length(kind: str, d: int, h: int, f: int, causal: bool, dtype: str, budget: int, layers: int = 1,
                step: int = 128, cap: int = 1 << 22, params: L.CostParams | None = None) -> dict:
-    """Largest sequence length (multiple of `step`, <= cap) whose unchunked Eq. 1 peak
-    (ac_estimate_memory) and whose ac_plan peak fit `budget` activation bytes, strict
-     - SPEC cmd_maxlen, the paper's max-inference-length extension
-    (P:357-361).  Returns {"unchunked", "chunked", "ratio", "plan"} (plan: ac_plan's
-    regions at the chunked maximum)."""
-    def graph(N):
-        return graph_block(kind, N, d, h, f, causal, dtype, name="maxlen", layers=layers)
-
-    def fits_unchunked(N):
-        prof, _ = estimate_memory(graph(N))
-        return prof.peak_bytes < budget
-
-    def fits_chunked(N):
-        return ac_plan(graph(N), budget, params).feasible
-
-    def largest(fits):
-        if not fits(step):
-            return 0
-        lo, hi = 1, 2  # fits(lo * step) holds; grow hi until it fails or passes the cap
-        while hi * step <= cap and fits(hi * step):
-            lo, hi = hi, 2 * hi
-        if hi * step > cap:
-            top = cap // step
-            if fits(top * step):
-                return top * step
-            hi = top
-        while hi - lo > 1:
-            mid = (lo + hi) // 2
-            if fits(mid * step):
-                lo = mid
-            else:
-                hi = mid
-        return lo * step
-
-    nu = largest(fits_unchunked)
-    nc = largest(fits_chunked)
+    """ac_max_length (the search runs in the library): the largest length, a multiple
+    of `step` <= cap, whose unchunked Eq. 1 peak and whose ac_plan peak fit `budget`
+    activation bytes (SPEC cmd_maxlen S:478-486).  Returns {"unchunked",
+    "chunked", "ratio", "plan"} (plan: ac_plan's regions at the chunked maximum)."""
+    desc = L.BlockDesc(KINDS[kind], 1, d, h, f, int(causal), DTYPES[dtype], 1e-5, None, int(layers))
+    nu, nc = C.c_int64(), C.c_int64()
+    check(lib().ac_max_length(C.byref(desc), budget, step, cap, C.byref(params) if params else None,
+                              C.byref(nu), C.byref(nc)))
     plan = None
-    if nc:
-        p = ac_plan(graph(nc), budget, params)
+    if nc.value:
+        p = ac_plan(graph_block(kind, nc.value, d, h, f, causal, dtype, name="maxlen", layers=layers), budget, params)
         plan = [ln.split(" flow=")[0] for ln in p.serialize().splitlines() if ln.startswith("region")]
-    return {"unchunked": nu, "chunked": nc, "ratio": (nc / nu) if nu else None, "plan": plan}
+    return {"unchunked": nu.value, "chunked": nc.value, "ratio": (nc.value / nu.value) if nu.value else None,
+            "plan": plan}

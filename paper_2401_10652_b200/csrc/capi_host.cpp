@@ -155,6 +155,51 @@ ac_status ac_plan_serialize(const ac_chunk_plan* p, char* buf, size_t cap, size_
   return copy_out(serialize_plan(p->plan, *p->g), buf, cap, len);
 }
 
+ac_status ac_max_length(const ac_block_desc* d, int64_t budget, int64_t step, int64_t cap,
+                        const ac_cost_params* params, int64_t* unchunked, int64_t* chunked) {
+  if (!d || !unchunked || !chunked || step < 1 || cap < step || budget < 0)
+    return set_error(AC_ERR_ARG, "ac_max_length: bad arguments");
+  *unchunked = *chunked = 0;
+  const Params pp = to_params(params);
+  try {
+    auto graph = [&](int64_t N) {
+      BlockDesc b{d->kind, N, d->d, d->h, d->f, d->causal, static_cast<DT>(d->dtype),
+                  d->ln_eps > 0 ? d->ln_eps : 1e-5, "maxlen", d->layers > 1 ? d->layers : 1};
+      return build_block(b);
+    };
+    // strict feasibility: the unchunked Eq. 1 peak, resp. ac_plan's Eq. 2 peak, below the budget
+    auto fits_unchunked = [&](int64_t N) { return profile(graph(N)).peak < budget; };
+    auto fits_chunked = [&](int64_t N) { return select_plan(graph(N), budget, pp).feasible; };
+    // largest multiple of step <= cap that fits: doubling, then bisection (SPEC cmd_maxlen)
+    auto largest = [&](auto fits) -> int64_t {
+      if (!fits(step)) return 0;
+      int64_t lo = 1, hi = 2;
+      while (hi * step <= cap && fits(hi * step)) {
+        lo = hi;
+        hi *= 2;
+      }
+      if (hi * step > cap) {
+        const int64_t top = cap / step;
+        if (fits(top * step)) return top * step;
+        hi = top;
+      }
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) / 2;
+        if (fits(mid * step)) lo = mid;
+        else hi = mid;
+      }
+      return lo * step;
+    };
+    *unchunked = largest(fits_unchunked);
+    *chunked = largest(fits_chunked);
+    return AC_OK;
+  } catch (GraphError& e) {
+    return set_error(AC_ERR_GRAPH, e.msg);
+  } catch (std::bad_alloc&) {
+    return set_error(AC_ERR_ARG, "ac_max_length: out of host memory");
+  }
+}
+
 void ac_plan_free(ac_chunk_plan* p) { delete p; }
 
 int32_t ac_plan_num_regions(const ac_chunk_plan* p) { return p ? static_cast<int32_t>(p->plan.regions.size()) : -1; }

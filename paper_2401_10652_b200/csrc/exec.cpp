@@ -346,8 +346,7 @@ Arena build_arena(const Graph& g, const Plan& plan, const ExecOptions& o) {
 
 bool gpu_kind(const std::string& k) {
   return k == "layernorm" || k == "linear" || k == "attn_scores" || k == "softmax" || k == "attn_pv" ||
-         k == "attn_fused" ||
-         k == "tri_scores" || k == "tri_pv";
+         k == "attn_fused" || k == "tri_scores" || k == "tri_pv" || k == "tri_mul" || k == "ln_cfirst";
 }
 
 View full_view(const TensorMeta& tm, void* p) {
@@ -463,9 +462,24 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
     const View& x = in(0);
     const int na = static_cast<int>(n.ai("naxes"));
     const int64_t C = extent(x, x.nd - na, x.nd);
-    if (collapse(x, 0, x.nd) != 1 || collapse(out, 0, out.nd) != 1) return unsup("non-contiguous rows");
+    int64_t group = 0, gx = 0, gy = 0;
+    if (collapse(x, 0, x.nd) != 1 || collapse(out, 0, out.nd) != 1) {
+      // a view cut along a middle dim: groups of contiguous rows along dim 0
+      if (x.nd - na < 2 || collapse(x, 1, x.nd) != 1 || collapse(out, 1, out.nd) != 1)
+        return unsup("non-contiguous rows");
+      group = extent(x, 1, x.nd - na);
+      gx = x.st[0];
+      gy = out.st[0];
+    }
     err = layernorm(x.p, in(1).p, in(2).p, out.p, extent(x, 0, x.nd - na), static_cast<int>(C),
-                    static_cast<float>(n.af("eps", 1e-5)), dtc, s, cx.pdl);
+                    static_cast<float>(n.af("eps", 1e-5)), dtc, s, cx.pdl, group, gx, gy);
+  } else if (k == "ln_cfirst") {
+    // x [C, I, J] (j contiguous) -> y [I, J, C] (c contiguous); views may be cut along i or j
+    const View& x = in(0);
+    if (x.st[2] != 1 || out.st[2] != 1) return unsup("ln_cfirst needs j-contiguous input, c-contiguous output");
+    err = layernorm_cfirst(x.p, x.st[0], x.st[1], in(1).p, in(2).p, out.p, out.st[0], out.st[1],
+                           static_cast<int>(x.sh[0]), x.sh[1], x.sh[2], static_cast<float>(n.af("eps", 1e-5)), dtc, s,
+                           cx.pdl);
   } else if (k == "softmax") {
     const View& x = in(0);
     if (n.ai("dim") != x.nd - 1 || x.st[x.nd - 1] != 1) return unsup("softmax over a non-last dim");
@@ -516,7 +530,9 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
       int ia = 2;
       const void* bias = nullptr;
       if (n.ai("bias")) bias = in(ia++).p;
+      const View* gatev = n.ai("gate") ? &in(ia++) : nullptr;  // elementwise, in the output's layout
       const View* resv = n.ai("res") ? &in(ia) : nullptr;
+      ep.gate = gatev ? gatev->p : nullptr;
       ep.bias = bias;
       ep.res = resv ? resv->p : nullptr;
       const std::string act = n.as("act", "none");
@@ -542,6 +558,11 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
             ep.res_sn = collapse(*resv, 2, resv->nd);
             if (ep.res_sn < 0) return unsup("residual not collapsible");
           }
+          if (gatev) {
+            ep.gate_sb1 = gatev->st[0]; ep.gate_sm = gatev->st[1];
+            ep.gate_sn = collapse(*gatev, 2, gatev->nd);
+            if (ep.gate_sn < 0) return unsup("gate not collapsible");
+          }
           goto launch;
         }
         if (sa < 0 || so < 0 || sf != 1) return unsup("rows not collapsible");
@@ -557,6 +578,11 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
           ep.res_sm = collapse(*resv, 0, nrows);
           ep.res_sn = collapse(*resv, nrows, resv->nd);
           if (ep.res_sm < 0 || ep.res_sn < 0) return unsup("residual not collapsible");
+        }
+        if (gatev) {
+          ep.gate_sm = collapse(*gatev, 0, nrows);
+          ep.gate_sn = collapse(*gatev, nrows, gatev->nd);
+          if (ep.gate_sm < 0 || ep.gate_sn < 0) return unsup("gate not collapsible");
         }
       } else if (!swap) {
         const int64_t sa = collapse(a, 0, nrows), sf = collapse(out, 0, nout), so = collapse(out, nout, out.nd);
@@ -574,6 +600,11 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
           ep.res_sm = collapse(*resv, 0, nout);
           ep.res_sn = collapse(*resv, nout, resv->nd);
           if (ep.res_sm < 0 || ep.res_sn < 0) return unsup("residual not collapsible");
+        }
+        if (gatev) {
+          ep.gate_sm = collapse(*gatev, 0, nout);
+          ep.gate_sn = collapse(*gatev, nout, gatev->nd);
+          if (ep.gate_sm < 0 || ep.gate_sn < 0) return unsup("gate not collapsible");
         }
       } else {
         if (nrows != 2) return unsup("swap needs two row dims");
@@ -597,6 +628,12 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
           ep.res_sb1 = resv->st[nout];
           ep.res_sn = resv->st[nout + 1];
           if (ep.res_sm < 0) return unsup("residual not collapsible");
+        }
+        if (gatev) {
+          ep.gate_sm = collapse(*gatev, 0, nout);
+          ep.gate_sb1 = gatev->st[nout];
+          ep.gate_sn = gatev->st[nout + 1];
+          if (ep.gate_sm < 0) return unsup("gate not collapsible");
         }
       }
     } else if (k == "attn_scores") {
@@ -665,6 +702,17 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
       }
       // Cluster split-K (ac_gemm_desc.ksplit) exists but measured slower than one
       // CTA per tile for these shapes (DSMEM reduction latency), so it stays off.
+    } else if (k == "tri_mul") {
+      // x[c, i, j] = sum_k a[c, i, k] b[c, j, k]: batch = channels, both operands K-major
+      const View &a = in(0), &b = in(1);
+      if (a.st[2] != 1 || b.st[2] != 1 || out.st[2] != 1) return unsup("tri_mul needs k- and j-contiguous rows");
+      p.B1 = static_cast<int>(a.sh[0]);
+      p.M = static_cast<int>(a.sh[1]);
+      p.N = static_cast<int>(b.sh[1]);
+      p.K = static_cast<int>(a.sh[2]);
+      p.A.p = a.p; p.A.srow = a.st[1]; p.A.sb1 = a.st[0]; p.A.use_b1 = 1;
+      p.B.p = b.p; p.B.srow = b.st[1]; p.B.sb1 = b.st[0]; p.B.use_b1 = 1;
+      ep.out_sb1 = out.st[0]; ep.out_sm = out.st[1]; ep.out_sn = 1;
     } else if (k == "tri_scores") {
       const View &q = in(0), &kk = in(1), &b = in(2);
       const bool end = n.ai("ending") != 0;
@@ -1030,7 +1078,8 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
       cx.fast = e->causal_fast[i] != 0;
       const std::string& kd = n.kind;
       cx.pdl = run_pdl && prev_kernel && e->fuse_role[i] == 0 &&
-                       (kd == "linear" || kd == "layernorm" || kd == "attn_fused")
+                       (kd == "linear" || kd == "layernorm" || kd == "attn_fused" || kd == "tri_mul" ||
+                        kd == "ln_cfirst")
                    ? 1
                    : 0;
       prev_kernel = 1;

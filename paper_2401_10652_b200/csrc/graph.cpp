@@ -77,7 +77,8 @@ const std::map<std::string, std::map<std::string, Attr::Kind>>& schema() {
       {"slice", {{"ranges", Attr::RANGES}}},
       {"linear",
        {{"kin", Attr::INT}, {"out", Attr::INTS}, {"act", Attr::STR}, {"trans", Attr::INT}, {"swap", Attr::INT},
-        {"bias", Attr::INT}, {"res", Attr::INT}}},
+        {"bias", Attr::INT}, {"res", Attr::INT}, {"gate", Attr::INT}}},
+      {"ln_cfirst", {{"eps", Attr::FLOAT}}},
       {"attn_scores", {{"scale", Attr::FLOAT}, {"causal", Attr::INT}}},
       {"attn_fused", {{"scale", Attr::FLOAT}, {"causal", Attr::INT}}},
       {"tri_scores", {{"scale", Attr::FLOAT}, {"ending", Attr::INT}}},
@@ -90,19 +91,19 @@ const std::set<std::string>& kinds() {
   static const std::set<std::string> k = {"matmul", "add", "sub", "mul", "div", "relu", "gelu", "exp", "sigmoid",
                                           "softmax", "layernorm", "reduce_sum", "reduce_mean", "reduce_max",
                                           "transpose", "reshape", "concat", "slice", "linear", "attn_scores",
-                                          "attn_pv", "tri_scores", "tri_pv", "attn_fused"};
+                                          "attn_pv", "tri_scores", "tri_pv", "attn_fused", "tri_mul", "ln_cfirst"};
   return k;
 }
 
 std::pair<int, int> arity(const Node& n) {
   const std::string& k = n.kind;
   if (k == "linear") {
-    int a = 2 + static_cast<int>(n.ai("bias")) + static_cast<int>(n.ai("res"));
+    int a = 2 + static_cast<int>(n.ai("bias")) + static_cast<int>(n.ai("gate")) + static_cast<int>(n.ai("res"));
     return {a, a};
   }
   if (k == "concat") return {1, 64};
-  if (k == "layernorm" || k == "tri_scores" || k == "tri_pv" || k == "attn_fused") return {3, 3};
-  if (k == "matmul" || is_elem2(k) || k == "attn_scores" || k == "attn_pv") return {2, 2};
+  if (k == "layernorm" || k == "tri_scores" || k == "tri_pv" || k == "attn_fused" || k == "ln_cfirst") return {3, 3};
+  if (k == "matmul" || is_elem2(k) || k == "attn_scores" || k == "attn_pv" || k == "tri_mul") return {2, 2};
   return {1, 1};
 }
 
@@ -222,10 +223,24 @@ Shape op_shape(const std::string& k, const Node& n, const std::vector<Shape>& in
       if (in[i] != Shape{prod(out)}) fail("linear bias shape mismatch");
       ++i;
     }
+    if (n.ai("gate")) {  // elementwise gate in the output's layout
+      if (in[i] != res) fail("linear gate shape mismatch");
+      ++i;
+    }
     if (n.ai("res") && in[i] != res) fail("linear residual shape mismatch");
     std::string act = n.as("act", "none");
     if (act != "none" && act != "gelu" && act != "sigmoid" && act != "relu") fail("linear act");
     return res;
+  }
+  if (k == "tri_mul") {  // AF2 Alg. 11 / 12 line 4, channel-major: x[c,i,j] = sum_k a[c,i,k] b[c,j,k]
+    const Shape &a = in[0], &b = in[1];
+    if (a.size() != 3 || b.size() != 3 || a[0] != b[0] || a[2] != b[2]) fail("tri_mul shape mismatch");
+    return {a[0], a[1], b[1]};
+  }
+  if (k == "ln_cfirst") {  // LayerNorm over the leading channel dim, written channel-last
+    const Shape& x = in[0];
+    if (x.size() != 3 || in[1] != Shape{x[0]} || in[2] != in[1]) fail("ln_cfirst shape mismatch");
+    return {x[1], x[2], x[0]};
   }
   if (k == "attn_scores") {
     const Shape &q = in[0], &kk = in[1];
@@ -283,7 +298,7 @@ int64_t op_flops(const std::string& k, const Node& n, const std::vector<Shape>& 
     const Shape& a = in[0];
     int64_t kin = n.ai("kin");
     int64_t R = prod(a, 0, a.size() - kin), K = prod(a, a.size() - kin), O = prod(n.av("out"));
-    int64_t extra = n.ai("bias") + (n.as("act", "none") != "none" ? 1 : 0) + n.ai("res");
+    int64_t extra = n.ai("bias") + (n.as("act", "none") != "none" ? 1 : 0) + n.ai("gate") + n.ai("res");
     return 2 * R * K * O + R * O * extra;
   }
   // fused kinds: the sum over their SPEC-primitive decomposition, i.e. the
@@ -296,6 +311,8 @@ int64_t op_flops(const std::string& k, const Node& n, const std::vector<Shape>& 
   }
   if (k == "tri_scores") return 2 * ne * in[0][3] + 2 * ne;
   if (k == "tri_pv") return 2 * prod(in[0]) * out[3] + ne;
+  if (k == "tri_mul") return 2 * prod(in[0]) * out[2];  // batched matmul over channels
+  if (k == "ln_cfirst") return 8 * ne;                   // transpose + layernorm
   fail("unknown op kind " + k);
 }
 
@@ -348,8 +365,17 @@ std::vector<int> op_propagate(const std::string& k, const Node& n, const std::ve
     if (n.ai("swap") && rd < 2) ad = 1 - rd;
     std::vector<int> res = {ad, NC};
     if (n.ai("bias")) res.push_back(NC);
+    if (n.ai("gate")) res.push_back(d);
     if (n.ai("res")) res.push_back(d);
     return res;
+  }
+  if (k == "tri_mul") {
+    static const int t[3][2] = {{0, 0}, {1, NC}, {NC, 1}};
+    return {t[d][0], t[d][1]};
+  }
+  if (k == "ln_cfirst") {
+    if (d == 2) return {BRK, BRK, BRK};
+    return {d + 1, NC, NC};
   }
   if (k == "attn_scores") {
     static const int t[3][2] = {{1, 1}, {0, NC}, {NC, 0}};
@@ -758,10 +784,11 @@ struct GB {
     g.nodes.push_back(n);
   }
   void linear(const std::string& nid, const std::vector<std::string>& ins, const std::string& out, int64_t kin,
-              const Shape& o, const std::string& act, int trans, int swap, int bias, int res) {
-    op(nid, "linear", ins, out,
-       {{"kin", I(kin)}, {"out", V(o)}, {"act", S(act)}, {"trans", I(trans)}, {"swap", I(swap)}, {"bias", I(bias)},
-        {"res", I(res)}});
+              const Shape& o, const std::string& act, int trans, int swap, int bias, int res, int gate = 0) {
+    std::map<std::string, Attr> at = {{"kin", I(kin)},     {"out", V(o)},       {"act", S(act)}, {"trans", I(trans)},
+                                      {"swap", I(swap)},   {"bias", I(bias)},   {"res", I(res)}};
+    if (gate) at["gate"] = I(1);  // (the attribute is written only when set)
+    op(nid, "linear", ins, out, at);
   }
 };
 
@@ -792,6 +819,51 @@ void tri_attention(GB& b, const std::string& z, const std::string& pre, int64_t 
   b.op(pre + "softmax", "softmax", {pre + "s"}, pre + "p", {{"dim", GB::I(3)}});
   b.op(pre + "pv", "tri_pv", {pre + "p", pre + "vt", pre + "g"}, pre + "o", {{"ending", GB::I(ending)}});
   b.linear(pre + "proj_o", {pre + "o", pre + "wo", pre + "bo", z}, out, 2, {cz}, "none", 0, 0, 1, 1);
+}
+
+// Triangular multiplicative update (AF2 supplement Alg. 11 outgoing / Alg. 12
+// incoming): a, b gated, channel-major [c, i, k] so x = tri_mul(a, b) is a batched
+// K-major GEMM; incoming edges read z transposed (swap).  Then LN over the channels
+// (ln_cfirst, written channel-last) and the gated output projection + residual.
+void tri_mul_block(GB& b, const std::string& z, const std::string& pre, int64_t cz, int64_t cm, int incoming,
+                   const std::string& out, double eps) {
+  auto P = [&](const std::string& s) { return pre + s; };
+  b.weight(P("ln_g"), {cz}, "ln_gamma", cz);
+  b.weight(P("ln_b"), {cz}, "ln_beta", cz);
+  for (const char* nm : {"ag", "a", "bg", "b"}) {
+    b.weight(P(std::string("w") + nm), {cm, cz}, "matrix", cz);
+    b.weight(P(std::string("b") + nm), {cm}, "bias", cz);
+  }
+  b.weight(P("wg"), {cz, cz}, "matrix", cz);
+  b.weight(P("bg"), {cz}, "bias", cz);
+  b.weight(P("lnx_g"), {cm}, "ln_gamma", cm);
+  b.weight(P("lnx_b"), {cm}, "ln_beta", cm);
+  b.weight(P("wo"), {cz, cm}, "matrix", cm);
+  b.weight(P("bo"), {cz}, "bias", cm);
+  b.op(P("ln"), "layernorm", {z, P("ln_g"), P("ln_b")}, P("zn"), {{"naxes", GB::I(1)}, {"eps", GB::F(eps)}});
+  b.linear(P("proj_ag"), {P("zn"), P("wag"), P("bag")}, P("ag"), 1, {cm}, "sigmoid", 1, incoming, 1, 0);
+  b.linear(P("proj_a"), {P("zn"), P("wa"), P("ba"), P("ag")}, P("a"), 1, {cm}, "none", 1, incoming, 1, 0, 1);
+  b.linear(P("proj_bg"), {P("zn"), P("wbg"), P("bbg")}, P("bgt"), 1, {cm}, "sigmoid", 1, incoming, 1, 0);
+  b.linear(P("proj_b"), {P("zn"), P("wb"), P("bb"), P("bgt")}, P("b"), 1, {cm}, "none", 1, incoming, 1, 0, 1);
+  b.linear(P("proj_g"), {P("zn"), P("wg"), P("bg")}, P("g"), 1, {cz}, "sigmoid", 0, 0, 1, 0);
+  b.op(P("mul"), "tri_mul", {P("a"), P("b")}, P("x"), {});
+  b.op(P("lnx"), "ln_cfirst", {P("x"), P("lnx_g"), P("lnx_b")}, P("xn"), {{"eps", GB::F(eps)}});
+  b.linear(P("proj_o"), {P("xn"), P("wo"), P("bo"), P("g"), z}, out, 1, {cz}, "none", 0, 0, 1, 1, 1);
+}
+
+// Pair transition (AF2 Alg. 15): z + Linear(relu(Linear(LN(z)))), hidden nf * c_z.
+void transition_block(GB& b, const std::string& z, const std::string& pre, int64_t cz, int64_t nf,
+                      const std::string& out, double eps) {
+  auto P = [&](const std::string& s) { return pre + s; };
+  b.weight(P("ln_g"), {cz}, "ln_gamma", cz);
+  b.weight(P("ln_b"), {cz}, "ln_beta", cz);
+  b.weight(P("w1"), {nf * cz, cz}, "matrix", cz);
+  b.weight(P("b1"), {nf * cz}, "bias", cz);
+  b.weight(P("w2"), {cz, nf * cz}, "matrix", nf * cz);
+  b.weight(P("b2"), {cz}, "bias", nf * cz);
+  b.op(P("ln"), "layernorm", {z, P("ln_g"), P("ln_b")}, P("zn"), {{"naxes", GB::I(1)}, {"eps", GB::F(eps)}});
+  b.linear(P("ffn1"), {P("zn"), P("w1"), P("b1")}, P("h"), 1, {nf * cz}, "relu", 0, 0, 1, 0);
+  b.linear(P("ffn2"), {P("h"), P("w2"), P("b2"), z}, out, 1, {cz}, "none", 0, 0, 1, 1);
 }
 
 // One pre-LN transformer block reading `xin`, every other id
@@ -866,6 +938,26 @@ Graph build_block(const BlockDesc& d) {
       tri_attention(b, z, p + "row_", cz, H, c, 0, p + "z1", eps);
       tri_attention(b, p + "z1", p + "col_", cz, H, c, 1, p + "z2", eps);
       z = p + "z2";
+    }
+    b.g.outputs.push_back(b.g.tindex[z]);
+  } else if (d.kind == 5) {
+    // the Evoformer pair stack (AF2 Alg. 6 lines 13-17): triangle multiplication
+    // outgoing / incoming (c = 128), triangle attention starting / ending node,
+    // pair transition (n = 4)
+    b.g.name = d.name.empty() ? "evoformer_pair" : d.name;
+    const int64_t N = d.N, cz = d.d, H = d.h, c = d.f, cm = 128, nf = 4;
+    b.input("z", {N, N, cz});
+    std::string z = "z";
+    for (int i = 0; i < L; ++i) {
+      const std::string p = pre(i);
+      tri_mul_block(b, z, p + "mo_", cz, cm, 0, p + "z1", eps);
+      tri_mul_block(b, p + "z1", p + "mi_", cz, cm, 1, p + "z2", eps);
+      tri_weights(b, p + "row_", cz, H, c);
+      tri_weights(b, p + "col_", cz, H, c);
+      tri_attention(b, p + "z2", p + "row_", cz, H, c, 0, p + "z3", eps);
+      tri_attention(b, p + "z3", p + "col_", cz, H, c, 1, p + "z4", eps);
+      transition_block(b, p + "z4", p + "tr_", cz, nf, p + "z5", eps);
+      z = p + "z5";
     }
     b.g.outputs.push_back(b.g.tindex[z]);
   } else {

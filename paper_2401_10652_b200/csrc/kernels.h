@@ -139,8 +139,16 @@ cudaError_t gemm_f32(const GemmProblem& p, cudaStream_t s);
 
 // Row ops.  dtype: 0 = fp32, 1 = bf16.
 // LayerNorm over the last C elements of `rows` rows (row stride = C).
+// rows: `group` contiguous rows per group, groups gx / gy elements apart in x / y
+// (group <= 0: all rows contiguous)
 cudaError_t layernorm(const void* x, const void* gamma, const void* beta, void* y, int64_t rows,
-                      int C, float eps, int dtype, cudaStream_t s, int pdl = 0);
+                      int C, float eps, int dtype, cudaStream_t s, int pdl = 0, int64_t group = 0, int64_t gx = 0,
+                      int64_t gy = 0);
+// ln_cfirst: x [C, I, J] (element strides xs_c, xs_i; j contiguous) -> y [I, J, C]
+// (strides ys_i, ys_j; c contiguous), LayerNorm over c with fp32 two-pass statistics.
+cudaError_t layernorm_cfirst(const void* x, int64_t xs_c, int64_t xs_i, const void* gamma, const void* beta, void* y,
+                             int64_t ys_i, int64_t ys_j, int C, int64_t I, int64_t J, float eps, int dtype,
+                             cudaStream_t s, int pdl = 0);
 // Row softmax: rows of `ncols` values with row stride `ld` (elements).  With
 // causal, row r is query row R = row_off + (r % group) (rows of several heads
 // are stacked); it reads columns <= R and writes columns [0, ceil128(R+1)) with

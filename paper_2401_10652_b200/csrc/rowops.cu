@@ -593,7 +593,8 @@ cudaError_t softmax_dispatch(const void* s, void* p, int64_t rows, int64_t ncols
 template <typename T, int VPT>
 __global__ void __launch_bounds__(256) layernorm_kernel(const T* __restrict__ x, const T* __restrict__ g,
                                                         const T* __restrict__ b, T* __restrict__ y, int64_t rows,
-                                                        int C, float eps, int pdl) {
+                                                        int C, float eps, int pdl, int64_t group, int64_t gx,
+                                                        int64_t gy) {
   if (pdl) {  // chunk loop: launched early (programmatic dependent launch); wait for the input
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -602,8 +603,11 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const T* __restrict__ x,
   const int lane = threadIdx.x & 31;
   const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   if (r >= rows) return;
-  const T* xr = x + r * C;
-  T* yr = y + r * C;
+  // rows in groups of `group` contiguous rows, groups gx / gy elements apart (a view
+  // cut along a middle dim, e.g. a column chunk of the pair representation)
+  const int64_t gi = r / group, ri = r - gi * group;
+  const T* xr = x + gi * gx + ri * C;
+  T* yr = y + gi * gy + ri * C;
   const int nv = C / VN;
   float f[VPT][VN];
   float sum = 0.f;
@@ -653,7 +657,7 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const T* __restrict__ x,
 
 template <typename T>
 cudaError_t layernorm_dispatch(const void* x, const void* g, const void* b, void* y, int64_t rows, int C,
-                               float eps, cudaStream_t st, int pdl) {
+                               float eps, cudaStream_t st, int pdl, int64_t group, int64_t gx, int64_t gy) {
   constexpr int VN = Vec<T>::N;
   if (C % VN != 0) return cudaErrorInvalidValue;
   const int nv = C / VN;
@@ -664,7 +668,8 @@ cudaError_t layernorm_dispatch(const void* x, const void* g, const void* b, void
   auto G = static_cast<const T*>(g);
   auto B = static_cast<const T*>(b);
   auto Y = static_cast<T*>(y);
-  void (*kern)(const T*, const T*, const T*, T*, int64_t, int, float, int) =
+  if (group <= 0 || gx % VN || gy % VN) return cudaErrorInvalidValue;
+  void (*kern)(const T*, const T*, const T*, T*, int64_t, int, float, int, int64_t, int64_t, int64_t) =
       nv <= 32 ? layernorm_kernel<T, 1> : nv <= 64 ? layernorm_kernel<T, 2> : nv <= 128 ? layernorm_kernel<T, 4>
       : nv <= 256 ? layernorm_kernel<T, 8> : nv <= 512 ? layernorm_kernel<T, 16> : nullptr;
   if (!kern) return cudaErrorInvalidValue;
@@ -678,13 +683,116 @@ cudaError_t layernorm_dispatch(const void* x, const void* g, const void* b, void
     la[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = la;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, X, G, B, Y, rows, C, eps, 1);
+    return cudaLaunchKernelEx(&cfg, kern, X, G, B, Y, rows, C, eps, 1, group, gx, gy);
   }
-  kern<<<gb, 256, 0, st>>>(X, G, B, Y, rows, C, eps, 0);
+  kern<<<gb, 256, 0, st>>>(X, G, B, Y, rows, C, eps, 0, group, gx, gy);
   return cudaGetLastError();
 }
 
+// LayerNorm over the leading (channel) dim of x [C, I, J] written channel-last,
+// y[i, j, :] = gamma * (x[:, i, j] - mu) / sqrt(var + eps) + beta (ln_cfirst, AF2
+// Alg. 11 line 4: the LN of the triangle product, whose GEMM leaves it channel-major).
+// One CTA per (i, 64 j): the [C x 64] tile is read coalesced along j into shared
+// memory (fp32, pitch 65), four threads per column fold its mean and then its
+// variance (two passes, fp32), and the normalised tile leaves coalesced along c in
+// 16-byte vectors.  HBM-bound: one read and one write of x.
+template <typename T>
+__global__ void __launch_bounds__(256) ln_cfirst_kernel(const T* __restrict__ x, int64_t xs_c, int64_t xs_i,
+                                                         const T* __restrict__ g, const T* __restrict__ b,
+                                                         T* __restrict__ y, int64_t ys_i, int64_t ys_j, int C,
+                                                         int64_t J, float eps, int pdl) {
+  extern __shared__ float lsm[];  // [C][65] values, then mu[64], rstd[64]
+  float* mu = lsm + C * 65;
+  float* rs = mu + 64;
+  if (pdl) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
+  const int64_t i = blockIdx.y;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * 64;
+  const int jn = static_cast<int>(J - j0 < 64 ? J - j0 : 64);
+  for (int idx = threadIdx.x; idx < C * 64; idx += 256) {
+    const int c = idx >> 6, jj = idx & 63;
+    lsm[c * 65 + jj] = jj < jn ? static_cast<float>(x[c * xs_c + i * xs_i + j0 + jj]) : 0.f;
+  }
+  __syncthreads();
+  {
+    const int col = threadIdx.x >> 2, part = threadIdx.x & 3;
+    float s = 0.f;
+    for (int c = part; c < C; c += 4) s += lsm[c * 65 + col];
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    const float m = s / static_cast<float>(C);
+    float q = 0.f;
+    for (int c = part; c < C; c += 4) {
+      const float d = lsm[c * 65 + col] - m;
+      q += d * d;
+    }
+    q += __shfl_xor_sync(0xffffffffu, q, 1);
+    q += __shfl_xor_sync(0xffffffffu, q, 2);
+    if (part == 0) {
+      mu[col] = m;
+      rs[col] = 1.f / sqrtf(q / static_cast<float>(C) + eps);
+    }
+  }
+  __syncthreads();
+  constexpr int VN = Vec<T>::N;
+  const int cv = C / VN;
+  for (int idx = threadIdx.x; idx < jn * cv; idx += 256) {
+    const int jj = idx / cv, c0 = (idx - jj * cv) * VN;
+    Vec<T> gv, bv, o;
+    gv.raw = *reinterpret_cast<const uint4*>(g + c0);
+    bv.raw = *reinterpret_cast<const uint4*>(b + c0);
+    float gf[VN], bf[VN], of[VN];
+    gv.to_float(gf);
+    bv.to_float(bf);
+#pragma unroll
+    for (int e = 0; e < VN; ++e) of[e] = (lsm[(c0 + e) * 65 + jj] - mu[jj]) * rs[jj] * gf[e] + bf[e];
+    o.from_float(of);
+    *reinterpret_cast<uint4*>(y + i * ys_i + (j0 + jj) * ys_j + c0) = o.raw;
+  }
+}
+
 }  // namespace
+
+cudaError_t layernorm_cfirst(const void* x, int64_t xs_c, int64_t xs_i, const void* gamma, const void* beta, void* y,
+                             int64_t ys_i, int64_t ys_j, int C, int64_t I, int64_t J, float eps, int dtype,
+                             cudaStream_t st, int pdl) {
+  if (I <= 0 || J <= 0) return cudaSuccess;
+  const int VN = dtype == 1 ? 8 : 4;
+  auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  if (C % VN || C > 1024 || ys_j % VN || ys_i % VN || !al(y) || !al(gamma) || !al(beta)) return cudaErrorInvalidValue;
+  const size_t smem = (static_cast<size_t>(C) * 65 + 128) * 4;
+  dim3 grid(static_cast<unsigned>((J + 63) / 64), static_cast<unsigned>(I));
+  auto launch = [&](auto kern, auto* X, auto* G, auto* B, auto* Y) -> cudaError_t {
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+    }
+    if (pdl) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = grid;
+      cfg.blockDim = dim3(256);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute la[1];
+      la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      la[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = la;
+      cfg.numAttrs = 1;
+      return cudaLaunchKernelEx(&cfg, kern, X, xs_c, xs_i, G, B, Y, ys_i, ys_j, C, J, eps, 1);
+    }
+    kern<<<grid, 256, smem, st>>>(X, xs_c, xs_i, G, B, Y, ys_i, ys_j, C, J, eps, 0);
+    return cudaGetLastError();
+  };
+  if (dtype == 1) {
+    using T = __nv_bfloat16;
+    return launch(ln_cfirst_kernel<T>, static_cast<const T*>(x), static_cast<const T*>(gamma),
+                  static_cast<const T*>(beta), static_cast<T*>(y));
+  }
+  return launch(ln_cfirst_kernel<float>, static_cast<const float*>(x), static_cast<const float*>(gamma),
+                static_cast<const float*>(beta), static_cast<float*>(y));
+}
 
 cudaError_t softmax_rows(const void* s_in, void* p_out, int64_t rows, int64_t ncols, int64_t ld, int64_t gstride,
                          int64_t ldo, int64_t gstrideo, int causal, int64_t row_off, int64_t group, int dtype,
@@ -703,10 +811,14 @@ cudaError_t softmax_rows(const void* s_in, void* p_out, int64_t rows, int64_t nc
 }
 
 cudaError_t layernorm(const void* x, const void* gamma, const void* beta, void* y, int64_t rows, int C, float eps,
-                      int dtype, cudaStream_t st, int pdl) {
+                      int dtype, cudaStream_t st, int pdl, int64_t group, int64_t gx, int64_t gy) {
   if (rows <= 0) return cudaSuccess;
-  if (dtype == 1) return layernorm_dispatch<__nv_bfloat16>(x, gamma, beta, y, rows, C, eps, st, pdl);
-  return layernorm_dispatch<float>(x, gamma, beta, y, rows, C, eps, st, pdl);
+  if (group <= 0) {  // contiguous rows
+    group = rows;
+    gx = gy = 0;
+  }
+  if (dtype == 1) return layernorm_dispatch<__nv_bfloat16>(x, gamma, beta, y, rows, C, eps, st, pdl, group, gx, gy);
+  return layernorm_dispatch<float>(x, gamma, beta, y, rows, C, eps, st, pdl, group, gx, gy);
 }
 
 }  // namespace ac

@@ -546,3 +546,22 @@ def test_rank_above_six_refused():
     with pytest.raises(_lib.ACError) as ei:
         gu.run(cg, gu.empty_plan(cg), og, dev)
     assert ei.value.status == _lib.AC_ERR_UNSUPPORTED
+
+
+def test_evoformer_pair_stack_bf16():
+    """NEXT f3: the full Evoformer pair stack (triangle multiplication outgoing /
+    incoming: gated channel-major projections, the tri_mul GEMM over channels, the
+    channel LayerNorm written channel-last, the gated output projection; triangle
+    attention starting / ending node; pair transition) vs the fp64 oracle, chunked
+    == unchunked bitwise, with regions cutting each kind of node along rows (i) and
+    columns (j)."""
+    og = workloads.evoformer_pair(64, 128, 4, 32, "bf16", name="evo_small")
+    _check_all_plans(og, [
+        "autochunk-plan 1\nregion s=mo_mul e=mo_proj_o n=4 dims=0\n",
+        "autochunk-plan 1\nregion s=mo_proj_ag e=mo_proj_o n=2 dims=0\n",
+        "autochunk-plan 1\nregion s=mi_proj_bg e=mi_proj_o n=2 dims=1\n",
+        "autochunk-plan 1\nregion s=mi_mul e=mi_lnx n=4 dims=1\n",
+        "autochunk-plan 1\nregion s=tr_ln e=tr_ffn2 n=4 dims=0\n",
+        "autochunk-plan 1\nregion s=row_scores e=row_pv n=4 dims=0\nregion s=col_scores e=col_pv n=4 dims=1\n"
+        "region s=tr_ln e=tr_ffn2 n=2 dims=1\n",
+    ], seed=9)

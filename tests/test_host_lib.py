@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol(root):
     assert declared <= bound, declared - bound
 
 
-CONFIGS = ["tiny", "gpt", "vit", "af", "unet", "unet_h8", "gpt_fa"]
+CONFIGS = ["tiny", "gpt", "vit", "af", "af_attn", "unet", "unet_h8", "gpt_fa"]
 
 
 def _c_graph(name):

@@ -56,10 +56,11 @@ def _check(Bp, prim_out, kind, attrs, fused_ins, extra=None):
     assert f_fused == _prim_flops(g), (kind, attrs, f_fused, _prim_flops(g))
 
 
-@pytest.mark.parametrize("bias,act,res,trans,swap", [
-    (0, "none", 0, 0, 0), (1, "none", 0, 0, 0), (1, "gelu", 0, 0, 0), (1, "none", 1, 0, 0),
-    (1, "sigmoid", 0, 0, 0), (0, "none", 0, 1, 0), (0, "none", 0, 1, 1), (1, "relu", 1, 0, 0)])
-def test_linear_flops_equal_primitive_sum(bias, act, res, trans, swap):
+@pytest.mark.parametrize("bias,act,res,trans,swap,gate", [
+    (0, "none", 0, 0, 0, 0), (1, "none", 0, 0, 0, 0), (1, "gelu", 0, 0, 0, 0), (1, "none", 1, 0, 0, 0),
+    (1, "sigmoid", 0, 0, 0, 0), (0, "none", 0, 1, 0, 0), (0, "none", 0, 1, 1, 0), (1, "relu", 1, 0, 0, 0),
+    (1, "none", 0, 1, 1, 1), (1, "none", 1, 0, 0, 1)])
+def test_linear_flops_equal_primitive_sum(bias, act, res, trans, swap, gate):
     I, J, K, O1, O2 = 3, 5, 4, 2, 3
     two_d = bool(swap)              # swap is defined on 2-row-dim inputs (AlphaFold pairs)
     B = Builder("lin", "f64")
@@ -76,10 +77,14 @@ def test_linear_flops_equal_primitive_sum(bias, act, res, trans, swap):
     full = tuple(rows) + tuple(out)
     if trans:
         full = tuple(out) + tuple(rows)
+    if gate:
+        B.input("gt", full)
+        ins.append("gt")
     if res:
         B.input("r", full)
         ins.append("r")
-    # primitives: [swap transpose] → reshape [R, K] → matmul with Wᵀ → (+ b) → act → reshape → [transpose] → (+ r)
+    # primitives: [swap transpose] → reshape [R, K] → matmul with Wᵀ → (+ b) → act → reshape → [transpose]
+    # → (* gate) → (+ r)
     a = "a"
     if swap:
         a = B.op("transpose", ["a"], "a_sw", perm=[1, 0, 2])
@@ -95,9 +100,13 @@ def test_linear_flops_equal_primitive_sum(bias, act, res, trans, swap):
     if trans:
         nr, no = len(rows), len(out)
         cur = B.op("transpose", [cur], "y1", perm=list(range(nr, nr + no)) + list(range(nr)))
+    if gate:
+        cur = B.op("mul", [cur, "gt"], "yg")
     if res:
         cur = B.op("add", [cur, "r"], "y2")
     attrs = dict(kin=1, out=out, act=act, trans=trans, swap=swap, bias=bias, res=res)
+    if gate:
+        attrs["gate"] = 1
     _check(B, cur, "linear", attrs, ins)
 
 
@@ -196,3 +205,26 @@ def test_tri_pv_flops_equal_primitive_sum(ending):
     B.op("transpose", ["oh"], "o0", perm=[2, 0, 1, 3] if ending else [0, 2, 1, 3])
     o = B.op("mul", ["o0", "g"], "o")
     _check(B, o, "tri_pv", dict(ending=ending), ["p", "vt", "g"])
+
+
+def test_tri_mul_flops_equal_primitive_sum():
+    """tri_mul = batched matmul over channels: a [C, I, K] x (b [C, J, K])^T."""
+    C_, I, K = 3, 4, 5
+    B = Builder("tm", "f64")
+    B.input("a", (C_, I, K))
+    B.input("b", (C_, I + 1, K))
+    B.op("transpose", ["b"], "bt", perm=[0, 2, 1])
+    x = B.op("matmul", ["a", "bt"], "x")
+    _check(B, x, "tri_mul", {}, ["a", "b"])
+
+
+def test_ln_cfirst_flops_equal_primitive_sum():
+    """ln_cfirst = transpose (channel first -> last) + layernorm over the channels."""
+    C_, I, J = 5, 3, 4
+    B = Builder("lc", "f64")
+    B.input("x", (C_, I, J))
+    B.weight("gm", (C_,), "ln_gamma")
+    B.weight("bt", (C_,), "ln_beta")
+    B.op("transpose", ["x"], "xt", perm=[1, 2, 0])
+    y = B.op("layernorm", ["xt", "gm", "bt"], "y", naxes=1, eps=1e-5)
+    _check(B, y, "ln_cfirst", {"eps": 1e-5}, ["x", "gm", "bt"])

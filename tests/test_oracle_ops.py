@@ -264,3 +264,46 @@ def test_tri_attention_pair_sampler_equals_full_run(ending):
     pairs = [(0, 0), (3, 7), (11, 2), (5, 11)]
     got = blocks.tri_attention_pairs(g, v, "t_", pairs, bool(ending))
     np.testing.assert_allclose(got, np.stack([full[i, j] for i, j in pairs]), rtol=0, atol=1e-12)
+
+
+# ----------------------------------------- Evoformer pair stack (NEXT f3), AF2 Alg. 6/11/12/15
+def _torch_tri_mul(z, W, incoming):
+    """AF2 Alg. 11 (outgoing) / Alg. 12 (incoming) via torch einsum, fp64."""
+    T = {k: torch.from_numpy(np.asarray(a, dtype=np.float64)) for k, a in W.items()}
+    z = torch.from_numpy(z)
+    cz = z.shape[-1]
+    zn = F.layer_norm(z, (cz,), T["ln_g"], T["ln_b"], eps=1e-5)
+    a = torch.sigmoid(F.linear(zn, T["wag"], T["bag"])) * F.linear(zn, T["wa"], T["ba"])
+    b = torch.sigmoid(F.linear(zn, T["wbg"], T["bbg"])) * F.linear(zn, T["wb"], T["bb"])
+    g = torch.sigmoid(F.linear(zn, T["wg"], T["bg"]))
+    x = torch.einsum("kic,kjc->ijc", a, b) if incoming else torch.einsum("ikc,jkc->ijc", a, b)
+    xn = F.layer_norm(x, (x.shape[-1],), T["lnx_g"], T["lnx_b"], eps=1e-5)
+    return (z + g * F.linear(xn, T["wo"], T["bo"])).numpy()
+
+
+def _torch_transition(z, W):
+    """AF2 Alg. 15 (pair transition, n = 4): z + Linear(relu(Linear(LN(z))))."""
+    T = {k: torch.from_numpy(np.asarray(a, dtype=np.float64)) for k, a in W.items()}
+    z = torch.from_numpy(z)
+    zn = F.layer_norm(z, (z.shape[-1],), T["ln_g"], T["ln_b"], eps=1e-5)
+    return (z + F.linear(torch.relu(F.linear(zn, T["w1"], T["b1"])), T["w2"], T["b2"])).numpy()
+
+
+def test_evoformer_pair_stack_matches_af2_algorithms():
+    """Every update of the pair stack (AF2 Alg. 6 lines 13-17) against its algorithm
+    written with torch (einsum / nn.functional), on the previous update's output."""
+    N, cz, H, c, cm = 10, 16, 2, 8, 12
+    g = workloads.evoformer_pair(N, cz, H, c, "f64", cm=cm)
+    v = _values(g, 4)
+    env = executor.run(g, v, keep_all=True)
+    pick = lambda pre: {k[len(pre):]: v[k] for k in v if k.startswith(pre)}  # noqa: E731
+    z1 = _torch_tri_mul(v["z"], pick("mo_"), incoming=False)
+    np.testing.assert_allclose(env["z1"], z1, rtol=0, atol=1e-12)
+    z2 = _torch_tri_mul(env["z1"], pick("mi_"), incoming=True)
+    np.testing.assert_allclose(env["z2"], z2, rtol=0, atol=1e-12)
+    z3 = _torch_tri_attention(env["z2"], pick("row_"), ending=False)
+    np.testing.assert_allclose(env["z3"], z3, rtol=0, atol=1e-12)
+    z4 = _torch_tri_attention(env["z3"], pick("col_"), ending=True)
+    np.testing.assert_allclose(env["z4"], z4, rtol=0, atol=1e-12)
+    z5 = _torch_transition(env["z4"], pick("tr_"))
+    np.testing.assert_allclose(env["z5"], z5, rtol=0, atol=1e-12)

@@ -145,7 +145,20 @@ FUSED = {
     "fa_causal": lambda: workloads.block("transformer_fa", 5, 4, 2, 8, True, "f64"),
     "fa": lambda: workloads.block("attn_only_fa", 5, 4, 2, 0, False, "f64"),
     "af": lambda: workloads.tri_attn_pair(4, 3, 2, 5, "f64"),
+    "evo_mul": lambda: _evo_mul_graph(),
 }
+
+
+def _evo_mul_graph():
+    """Triangle multiplication outgoing + incoming + pair transition (the f3 kinds:
+    gated channel-major linear, tri_mul, ln_cfirst, relu FFN) on a 4 x 4 pair rep."""
+    B = Builder("evo_mul", "f64")
+    B.input("z", (4, 4, 3))
+    workloads._tri_mul(B, "z", "mo_", 3, 5, 0, "z1")
+    workloads._tri_mul(B, "z1", "mi_", 3, 5, 1, "z2")
+    workloads._transition(B, "z2", "tr_", 3, 2, "z3")
+    B.output("z3")
+    return B.build()
 
 
 @pytest.mark.parametrize("name,seq,d", CORPUS + [(k, 0, 0) for k in FUSED])
