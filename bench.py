@@ -80,48 +80,57 @@ def load_peaks():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled every 5 ms through NVML
+    while the timed regions run (nvidia-smi per sample is too slow for 2.5 ms steps)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4))
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period: float = 0.005):
         self.index = index
+        self.period = period
         self.samples = []
         self._stop = threading.Event()
         self._t = None
+        self._nv = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self._nv = None
 
     def _run(self):
+        nv = self._nv
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.samples.append((float(sm), int(rs)))
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(self.period)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
         return self
 
     def __exit__(self, *a):
         self._stop.set()
-        self._t.join(timeout=10)
+        if self._t:
+            self._t.join(timeout=10)
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
-        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = sorted(x[0] for x in self.samples)
+        reasons = sorted({nm for _, r in self.samples for nm, bit in self.REASONS if r & bit})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.max_mhz, "sm_min_mhz": sm[0], "reasons": reasons,
+                "samples": len(self.samples), "source": "NVML, 5 ms period, over the timed and profiled passes"}
 
 
 # ------------------------------------------------------------------ workload
@@ -244,7 +253,9 @@ def algorithmic(doc, node_id):
 
 def cpu_baseline(name, og, samples, budget_s=20.0):
     """The oracle as it stands on this host: sampled output rows of the block
-    (K/V of all rows + R query rows), rows/s."""
+    (K/V of all rows + R query rows), rows/s, with the full-block time extrapolated
+    from a 1-row and an R-row run (precompute + N x per-row).  Returns (line, rows,
+    oracle values at those rows) so the GPU output can be compared with them."""
     import numpy as np
     from oracle import blocks, executor
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
@@ -253,11 +264,20 @@ def cpu_baseline(name, og, samples, budget_s=20.0):
         N = og.tensors["x"].shape[0]
         rows = np.arange(0, N, max(1, N // 32))[:32]
         t0 = time.perf_counter()
-        blocks.transformer_rows(og, vals, rows)
+        blocks.transformer_rows(og, vals, rows[:1])
+        t1 = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        ref = blocks.transformer_rows(og, vals, rows)
         dt = time.perf_counter() - t0
-        return {"value": len(rows) / dt, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                "sample": f"{len(rows)} output rows of the {name} block incl. LN1/K/V of all {N} rows "
-                          f"(fp64 numpy, {dt:.1f} s)"}
+        per_row = max(dt - t1, 1e-9) / (len(rows) - 1)
+        pre = max(t1 - per_row, 0.0)
+        return ({"value": len(rows) / dt, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                 "sample": f"{len(rows)} output rows of the {name} block incl. LN1/K/V of all {N} rows "
+                           f"(fp64 numpy, {dt:.1f} s)",
+                 "extrapolated_block_s": round(pre + N * per_row, 1),
+                 "extrapolation": f"precompute {pre:.2f} s (LN1, K, V of all rows) + N x {per_row * 1e3:.1f} ms "
+                                  f"per row, from a 1-row and a {len(rows)}-row run"},
+                rows, ref)
     if name in ("af", "af_attn"):
         from oracle import workloads
         mk = workloads.evoformer_pair if name == "af" else workloads.tri_attn_pair
@@ -267,10 +287,49 @@ def cpu_baseline(name, og, samples, budget_s=20.0):
         t0 = time.perf_counter()
         executor.run(small, v)
         dt = time.perf_counter() - t0
-        return {"value": 128 * 128 / dt, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                "sample": f"the full {small.name} block at N_res=128 (fp64 numpy, {dt:.1f} s); the work per pair "
-                          f"grows with N_res, so this overstates the oracle's rate at 1024"}
-    return None
+        return ({"value": 128 * 128 / dt, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                 "sample": f"the full {small.name} block at N_res=128 (fp64 numpy, {dt:.1f} s); the work per pair "
+                           f"grows with N_res, so this overstates the oracle's rate at 1024",
+                 "extrapolated_block_s": round(dt * (1024 / 128) ** 3, 1),
+                 "extrapolation": "x (1024/128)^3: the triangle updates and attentions are cubic in N_res"},
+                None, None)
+    return None, None, None
+
+
+def error_vs_oracle(doc, outs, rows, ref):
+    """Elementwise and normwise error of the GPU block output at the oracle's sampled
+    rows (fp64, the same seeded inputs): max |g - r|, normwise ||g - r||_inf / ||r||_inf
+    (R18, the tolerance metric), and the elementwise relative error |g - r| / |r| over
+    elements with |r| >= 1e-2 ||r||_inf (max and 99.9th percentile)."""
+    import numpy as np
+    if rows is None:
+        return None
+    key = "y" if "y" in ref else "x1"
+    g = outs[doc.outputs[0]][rows].double().cpu().numpy()
+    r = ref[key]
+    d = np.abs(g - r)
+    big = np.abs(r) >= 1e-2 * np.abs(r).max()
+    el = d[big] / np.abs(r[big])
+    return {"rows": len(rows), "tensor": doc.outputs[0], "max_abs": float(d.max()),
+            "normwise_rel": float(d.max() / np.abs(r).max()),
+            "elementwise_rel_max": float(el.max()), "elementwise_rel_p999": float(np.quantile(el, 0.999)),
+            "tolerance": 2e-2 if doc.tensors[doc.outputs[0]][0] == "bf16" else 1e-4}
+
+
+def planner_timing(name, cg, budget):
+    """ac_plan (C++) vs the oracle's planner (Alg. 1 + Eq. 8-11 in numpy-free Python)
+    on the config graph at the bench budget (the search-cost claim)."""
+    from oracle import graph as og_graph, plan as oplan, select
+    from paper_2401_10652_b200 import api
+    og = oracle_graph(name)
+    t0 = time.perf_counter()
+    cp = api.ac_plan(cg, budget)
+    t_c = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    op = select.select(og, budget)
+    t_o = time.perf_counter() - t0
+    return {"ac_plan_ms": round(t_c * 1e3, 2), "oracle_plan_ms": round(t_o * 1e3, 1),
+            "plans_identical": oplan.serialize(op, og) == cp.serialize(), "nodes": len(og.nodes)}
 
 
 # ------------------------------------------------------------------ reference arm
@@ -412,8 +471,27 @@ def peak_block(profp, prof0, st, budget, caller, activation_alloc, unchunked):
                     "control_bytes = scheduler state in the workspace (work counters, overlap epochs)"}
 
 
+def self_launch(args):
+    """--gpus N > 1 without a torchrun environment: relaunch this command as N ranks
+    (torch.distributed.run on this node, rendezvous on 127.0.0.1)."""
+    import socket
+    import torch
+    if args.impl == "ours" and torch.cuda.device_count() < args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but only {torch.cuda.device_count()} "
+                                                     f"CUDA devices are visible"}))
+        return 1
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     if args.impl == "reference":
         return reference_arm(args)
     import torch
@@ -423,6 +501,8 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        print(f"bench: WORLD_SIZE={world} overrides --gpus {args.gpus}", file=sys.stderr)
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
@@ -500,14 +580,14 @@ def main():
 
     peaks, peak_src = load_peaks()
     units = tokens_per_step(args.config, doc)
-    with ClockSampler(local) as clk:
-        tot_ms, _ = timed(ex, ins, outs, args.steps, args.warmup)
+    clk = ClockSampler(local)
+    clk.__enter__()
+    tot_ms, _ = timed(ex, ins, outs, args.steps, args.warmup)
     st = ex.stats()
     # per-stage device times from a separate profiled pass (per-launch events
     # serialise the chunk loop's overlapped launches, so they stay out of `value`)
     kp = max(2, min(args.steps, 5))
     prof_ms, kt = timed(ex, ins, outs, kp, 1, profile=True)
-    clocks = clk.summary()
     value = units * args.steps / (tot_ms / 1e3)
     ms_step = tot_ms / args.steps
 
@@ -572,6 +652,8 @@ def main():
                 vu = units * ku / (tu / 1e3)
                 stu = exu.stats()
                 unchunked = {"value": vu, "ms_per_step": tu / ku,
+                             **({"note": f"the empty plan on every rank (replicated work at {world} ranks)"}
+                                if world > 1 else {}),
                              "speed_loss": 1.0 - value / vu, "workspace_bytes": need,
                              "arena_live_peak": stu.arena_live_peak,
                              "measured_peak_bytes": need + caller_bytes,
@@ -583,6 +665,8 @@ def main():
         except Exception as e:  # pragma: no cover
             unchunked = {"error": str(e)}
         torch.cuda.empty_cache()
+    clk.__exit__()
+    clocks = clk.summary()
 
     # end to end: pinned host input -> device, ac_run, output -> pinned host, every
     # step.  Pipelined as a serving loop would run it: step k's H2D (copy stream)
@@ -689,6 +773,27 @@ def main():
                 ablation.append({"budget_frac": frac, "toggle": name, "plan": txt.splitlines(),
                                  "feasible": bool(feas), "planned_peak_frac": round(pfrac, 4),
                                  "tokens_per_s": round(tps, 1)})
+        # "No graph optimization" where it bites: a forced region holding the K / V
+        # projections (off the row flow), hoisted vs recomputed in every chunk (opt=0)
+        if args.config in ("gpt", "vit", "unet", "gpt_fa"):
+            n_f = 8
+            s0, e0 = "proj_q", ("attn" if args.config == "gpt_fa" else "pv")
+            for opt in ("", " opt=0"):
+                txt = f"region s={s0} e={e0} n={n_f} dims=0{opt}"
+                fp = api.plan_parse(cg, "autochunk-plan 1\n" + txt + "\n")
+                pr_, _ = api.estimate_memory(cg, fp)
+                wsa = torch.empty(max(fp.workspace_bytes(), 16), dtype=torch.uint8, device="cuda")
+                exa = api.Exec(fp, wsa, comm)
+                ka = max(3, args.steps // 2)
+                ta, _ = timed(exa, ins, outs, ka, 2)
+                del exa, wsa
+                ablation.append({"budget_frac": None, "toggle": "forced region, graph optimization " +
+                                 ("off" if opt else "on"), "plan": [txt], "feasible": None,
+                                 "planned_peak_frac": round(pr_.peak_bytes / prof0.peak_bytes, 4),
+                                 "tokens_per_s": round(units * ka / (ta / 1e3), 1)})
+            on, off = ablation[-2]["tokens_per_s"], ablation[-1]["tokens_per_s"]
+            ablation[-1]["speed_vs_all"] = round(off / on, 4)
+            ablation[-2]["speed_vs_all"] = 1.0
         for frac in (0.2, 0.1, 0.05):
             ref = [a["tokens_per_s"] for a in ablation if a["budget_frac"] == frac and a["toggle"] == "all strategies"][0]
             for a in ablation:
@@ -698,14 +803,23 @@ def main():
 
     if rank != 0:
         return 0
-    cpu = None
+    cpu, err, ptime = None, None, None
     if not args.no_cpu and not args.profile:
         try:
             base_cfg = "gpt" if args.config == "gpt_fa" else args.config   # same block maths, unfused ids
-            cpu = (cpu_baseline(base_cfg, oracle_graph(base_cfg), samples) if args.layers == 1 else
-                   {"note": "oracle row sampler covers one block; stacks are parity-tested in tests/"})
+            if args.layers == 1:
+                cpu, rows, ref = cpu_baseline(base_cfg, oracle_graph(base_cfg), samples)
+                # the timed runs left the block output of the last step in `outs`
+                err = error_vs_oracle(doc, outs, rows, ref)
+            else:
+                cpu = {"note": "oracle row sampler covers one block; stacks are parity-tested in tests/"}
         except Exception as e:  # pragma: no cover
             cpu = {"error": str(e)}
+        if args.config not in ("tiny",) and args.layers == 1 and not args.plan:
+            try:
+                ptime = planner_timing(args.config, cg, budget)
+            except Exception as e:  # pragma: no cover
+                ptime = {"error": str(e)}
     plan_txt = plan.serialize().splitlines()
     regions = [ln.split(" flow=")[0] for ln in plan_txt if ln.startswith("region")]
     caller = sum(doc.nbytes(t) for t in doc.inputs + doc.outputs)
@@ -715,10 +829,13 @@ def main():
         "vs_baseline": None, "dtype": doc.tensors[doc.inputs[0]][0],
         "data": "synthetic (seeded PCG64, DESIGN.md §4)",
         "config": {"workload": WORKLOADS[args.config] + (f", {args.layers} stacked blocks" if args.layers > 1 else ""),
-                   "plan": regions, "parallelism": f"chunk-split x{world}",
+                   "plan": regions, "parallelism": f"chunk-split x{world}" + (
+                       " (zigzag / round-robin chunk shares, row-partitioned post-region nodes, NCCL all-gather)"
+                       if world > 1 else ""),
                    "l2": "flushed between timed steps (256 MiB write)"},
         "peak_activation_bytes": peak_block(profp, prof0, st, budget, caller, activation_alloc, unchunked),
         "unchunked": unchunked, "roofline": roof, "stages": shares, "cpu_baseline": cpu, "e2e": e2e,
+        "error_vs_oracle": err, "planner_timing": ptime,
         **({"chunk_sweep": sweep} if sweep else {}),
         **({"ablation": ablation} if ablation else {}),
         "gpu_launches": st.launches * args.steps, "clocks": clocks,

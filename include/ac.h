@@ -159,8 +159,9 @@ ac_status ac_max_length(const ac_block_desc* desc, int64_t budget, int64_t step,
                         const ac_cost_params* params, int64_t* unchunked, int64_t* chunked);
 
 /* User-fixed plan: "autochunk-plan 1" followed by lines
- *   region s=<node id> e=<node id> n=<chunks> dims=<d,...>
- * (one output dim per region output).  The library re-derives the flow, X^c,
+ *   region s=<node id> e=<node id> n=<chunks> dims=<d,...> [opt=0]
+ * (one output dim per region output; opt=0 turns graph optimisation - hoisting,
+ * P:247, Table 1's "No graph optimization" - off for the region).  The library re-derives the flow, X^c,
  * X^nc, Y^c and hoisting exactly as the search would.  Errors: AC_ERR_PLAN. */
 ac_status ac_plan_parse(const ac_graph* g, const char* doc, size_t len, ac_chunk_plan** out);
 
@@ -185,20 +186,79 @@ int64_t ac_plan_workspace_bytes(const ac_chunk_plan* p, int32_t rank, int32_t wo
 ac_status ac_plan_arena_profile(const ac_chunk_plan* p, int64_t* live_per_step, int64_t* live_peak,
                                 int64_t* control_bytes);
 
-/* Chunks [*c0, *c1) of region `region` (commit order) that rank `rank` of
- * `world` executes: floor(rank n / world) .. floor((rank+1) n / world)
- * (SURVEY §8(e)).  Also reports the region's chunk_len and extent.
- * Errors: AC_ERR_ARG. */
-ac_status ac_plan_rank_chunks(const ac_chunk_plan* p, int32_t region, int32_t rank, int32_t world, int64_t* c0,
-                              int64_t* c1, int64_t* chunk_len, int64_t* extent);
+/* ------------------------------------------------------------------ multi-GPU share */
+
+/* The chunks of region `region` (commit order) that rank `rank` of `world` runs
+ * (chunks along the chunk dim are independent, Eq. 4 P:166-169,
+ * P:99-102).  On world > 1 the plan's n may be refined to a multiple n_eff
+ * (equal chunks, never longer than the plan's, so the arena still holds them):
+ * regions with a causal attention are dealt in ZIGZAG groups of 2W chunks (rank r
+ * owns g*2W + r and g*2W + 2W-1-r, equal causal work per rank), others in
+ * ROUND-ROBIN groups of W (rank r owns g*W + r); when no refinement gives equal
+ * chunks in whole groups, contiguous blocks [floor(r n / W), floor((r+1) n / W)).
+ * Writes up to `cap` chunk indices (ascending) to `chunks` and their count to
+ * *n_chunks; *n_eff, *chunk_len (length of chunk c: rows [c L, min(E, (c+1) L))),
+ * *extent (E) are nullable.  world = 1: every chunk of the plan.  Errors: AC_ERR_ARG. */
+ac_status ac_plan_rank_chunks(const ac_chunk_plan* p, int32_t region, int32_t rank, int32_t world,
+                              int64_t* chunks, int32_t cap, int32_t* n_chunks, int64_t* n_eff, int64_t* chunk_len,
+                              int64_t* extent);
+
+/* One exchange of a rank's schedule: makes a tensor that ranks computed in parts
+ * (a region output, or a row-partitioned node's output) complete on every rank. */
+typedef enum ac_exchange_kind {
+  AC_X_ALLGATHER = 0,     /* in-place all-gather of W equal chunks c_first .. c_first+W-1; rank q's
+                             chunk is c_first + q */
+  AC_X_ALLGATHER_REV = 1, /* the same on the rank-reversed communicator: rank q's chunk is
+                             c_first + W-1-q (second half of a zigzag group) */
+  AC_X_BCAST = 2          /* broadcast of `run_bytes` at byte `offset` from rank `root` */
+} ac_exchange_kind;
+
+typedef struct ac_exchange_op {
+  int32_t kind;         /* ac_exchange_kind */
+  int32_t before_node;  /* node whose launch needs the result; ac_graph_num_nodes = after the last node */
+  int32_t region;       /* region whose chunk share partitions the tensor */
+  int32_t eager;        /* 1: issued inside the region's chunk loop on a communication stream, once the
+                           rank's chunks of `group` are done (the consumer waits at region end) */
+  int64_t group;        /* ownership group of an all-gather (-1 for broadcasts) */
+  int64_t c_first;      /* all-gather: first chunk */
+  int32_t dim;          /* chunk dim of the tensor */
+  int32_t root;         /* broadcast: owner rank */
+  int64_t outer;        /* product of the extents before `dim`; > 1: every chunk is `outer` runs,
+                           packed through a staging buffer in the workspace for the all-gather */
+  int64_t run_bytes;    /* all-gather: bytes of one chunk per outer index; broadcast: bytes */
+  int64_t ext_bytes;    /* bytes per outer index (extent of `dim` x inner) */
+  int64_t offset;       /* broadcast: byte offset in the tensor */
+  char tensor[48];      /* tensor id */
+} ac_exchange_op;
+
+/* The rank's schedule beyond the regions: node_region[i] (nullable,
+ * one entry per node) = the region whose chunk share node i outside every region
+ * runs on (its rows [c L, (c+1) L) of the rank's chunks c, output dim node_dim[i]),
+ * or -1 when the node runs whole: row-local nodes after a region (out-projection,
+ * LayerNorm, FFN) and nodes feeding only a region's chunked input (the Q
+ * projection) run on the rank's rows only.  ops (up to `cap`, *n_ops = total): the
+ * exchanges in issue order.  ac_run follows exactly this schedule; the multi-rank
+ * CPU tests replay it.  Errors: AC_ERR_ARG. */
+ac_status ac_plan_rank_schedule(const ac_chunk_plan* p, int32_t rank, int32_t world, int32_t* node_region,
+                                int32_t* node_dim, ac_exchange_op* ops, int32_t cap, int32_t* n_ops);
 
 /* ------------------------------------------------------------------ multi-GPU */
 
 /* NCCL bootstrap: rank 0 calls ac_comm_get_unique_id, the 128
  * bytes are broadcast by the caller (torch.distributed), every rank calls
- * ac_comm_init on its device.  Errors: AC_ERR_NCCL, AC_ERR_ARG. */
+ * ac_comm_init on its device (collective: it also splits the rank-reversed
+ * communicator of the zigzag all-gathers).  Errors: AC_ERR_NCCL, AC_ERR_ARG. */
 ac_status ac_comm_get_unique_id(uint8_t unique_id[128]);
 ac_status ac_comm_init(const uint8_t unique_id[128], int32_t rank, int32_t world, int32_t device, ac_comm** out);
+/* In-process transport for tests on ONE device: comms[0..world-1] are the ranks of
+ * one group, each to be driven by its own host thread (ac_run on its own stream).
+ * Every collective is a host barrier plus device-to-device copies ordered by CUDA
+ * events - the data movement of the NCCL collective, not its speed.
+ * Errors: AC_ERR_ARG, AC_ERR_CUDA. */
+ac_status ac_comm_init_local(int32_t world, ac_comm** comms);
+/* Non-blocking health check: AC_ERR_NCCL with the message when an earlier
+ * collective failed asynchronously (ncclCommGetAsyncError).  ac_run calls it first. */
+ac_status ac_comm_check(const ac_comm* c);
 void ac_comm_free(ac_comm* c);
 
 /* ------------------------------------------------------------------ execution */
@@ -224,8 +284,10 @@ void ac_exec_free(ac_exec* e);
  * inputs: every graph input and weight, by tensor id; outputs: every graph
  * output (fully overwritten).  Asynchronous and stream-ordered; buffers must
  * stay valid until the stream completes.  With a communicator, each rank runs
- * its contiguous share of every region's chunks and the region outputs are
- * all-gathered (NCCL broadcasts from each slab's owner).
+ * its share of every region's chunks and of the row-local nodes around them and
+ * issues the exchanges of ac_plan_rank_schedule (NCCL all-gathers in place; region
+ * outputs group by group on an internal communication stream overlapping the
+ * chunk loop); every rank's outputs equal the single-GPU outputs bitwise.
  * Inside a region's chunk loop the kernels are programmatic dependent launches
  * (each waits in-kernel for its predecessor; AC_PDL=0 disables), and the chunks
  * of a fused attention chain overlap through per-head epochs kept in a control
@@ -252,6 +314,7 @@ typedef struct ac_run_stats {
   /* workspace bytes that are scheduler state, not activation (the fused chains'
    * work counters, split-K partials, chunk-loop overlap epochs): after the slots */
   int64_t control_bytes;
+  int32_t exchanges;             /* collectives issued by the last ac_run (world > 1) */
 } ac_run_stats;
 ac_status ac_exec_stats(const ac_exec* e, ac_run_stats* out);
 

@@ -98,8 +98,8 @@ def serialize(plan: Plan, g) -> str:
 
 
 def parse_user_regions(text: str):
-    """Parse the region records of a plan document: [(start_id, end_id, n, dims|None)].
-    Only s/e/n/dims are read; the library re-derives flows (SURVEY §8(b) ac_plan_parse)."""
+    """Parse the region records of a plan document: [(start_id, end_id, n, dims|None[, hoist])].
+    Only s/e/n/dims/opt are read; the library re-derives flows (SURVEY §8(b) ac_plan_parse)."""
     lines = [ln.strip() for ln in text.splitlines() if ln.strip()]
     if not lines or lines[0] != "autochunk-plan 1":
         raise ValueError("plan parse error: missing header")
@@ -114,5 +114,7 @@ def parse_user_regions(text: str):
             dims = tuple(int(x) for x in kv["dims"].split(","))
         elif "yc" in kv:
             dims = tuple(int(x.rsplit(":", 1)[1]) for x in kv["yc"].split(","))
-        out.append((kv["s"], kv["e"], int(kv["n"]), dims))
+        # opt=0: graph optimisation (hoisting) off for this region (Table 1's
+        # "No graph optimization" on a user-fixed region)
+        out.append((kv["s"], kv["e"], int(kv["n"]), dims) + ((False,) if kv.get("opt") == "0" else ()))
     return out

@@ -190,16 +190,18 @@ def exhaustive(g: Graph, budget: int, p: CostParams, max_passes: int = 3):
 
 def user_plan(g: Graph, specs, p: CostParams = None) -> Plan:
     """A user-fixed plan (ac_plan_parse): specs = [(start_node_id, end_node_id, n,
-    dims)].  Flows, X^c / X^nc / Y^c and hoisting are derived as the search does."""
+    dims[, hoist])].  Flows, X^c / X^nc / Y^c and hoisting are derived as the search does."""
     from .search import candidate_for
     p = p or CostParams()
     names = [n.id for n in g.nodes]
     regions = []
-    for s_id, e_id, n, dims in specs:
+    for spec in specs:
+        s_id, e_id, n, dims = spec[:4]
+        hoist = spec[4] if len(spec) > 4 else True     # False: opt=0, no graph optimisation (P:247)
         s, e = names.index(s_id), names.index(e_id)
         if any(g.nodes[i].kind in ("input", "weight") for i in range(s, e + 1)):
             raise ValueError("illegal region: contains an input/weight node")
-        r = candidate_for(g, s, e, tuple(dims), hoist=True)
+        r = candidate_for(g, s, e, tuple(dims), hoist=hoist)
         if r is None:
             raise ValueError("illegal region: no legal chunk flow for these dims")
         if not 1 <= n <= r.extent:

@@ -53,7 +53,14 @@ class Tensor(C.Structure):
 class RunStats(C.Structure):
     _fields_ = [("workspace_high_water", C.c_int64), ("planned_peak", C.c_int64), ("caller_bytes", C.c_int64),
                 ("launches", C.c_int32), ("chunks_run", C.c_int32), ("arena_live_peak", C.c_int64),
-                ("control_bytes", C.c_int64)]
+                ("control_bytes", C.c_int64), ("exchanges", C.c_int32)]
+
+
+class ExchangeOp(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("before_node", C.c_int32), ("region", C.c_int32), ("eager", C.c_int32),
+                ("group", C.c_int64), ("c_first", C.c_int64), ("dim", C.c_int32), ("root", C.c_int32),
+                ("outer", C.c_int64), ("run_bytes", C.c_int64), ("ext_bytes", C.c_int64), ("offset", C.c_int64),
+                ("tensor", C.c_char * 48)]
 
 
 class KernelTime(C.Structure):
@@ -99,10 +106,15 @@ SIGNATURES = [
     ("ac_max_length", C.c_int, [C.POINTER(BlockDesc), C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
                                 C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("ac_plan_arena_profile", C.c_int, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
-    ("ac_plan_rank_chunks", C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int64),
-                                      C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("ac_plan_rank_chunks", C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.c_int32,
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_int64)]),
+    ("ac_plan_rank_schedule", C.c_int, [P, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                        C.POINTER(ExchangeOp), C.c_int32, C.POINTER(C.c_int32)]),
     ("ac_comm_get_unique_id", C.c_int, [C.c_char_p]),
     ("ac_comm_init", C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(P)]),
+    ("ac_comm_init_local", C.c_int, [C.c_int32, C.POINTER(P)]),
+    ("ac_comm_check", C.c_int, [P]),
     ("ac_comm_free", None, [P]),
     ("ac_exec_create", C.c_int, [P, P, C.c_int64, P, C.POINTER(P)]),
     ("ac_exec_free", None, [P]),

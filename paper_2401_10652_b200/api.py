@@ -99,11 +99,27 @@ class Plan:
         return lib().ac_plan_num_regions(self._h)
 
     def rank_chunks(self, region: int, rank: int, world: int):
-        """(c0, c1, chunk_len, extent): the chunks of `region` that `rank` runs."""
-        a, b, ln, ext = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
-        check(lib().ac_plan_rank_chunks(self._h, region, rank, world, C.byref(a), C.byref(b), C.byref(ln),
-                                        C.byref(ext)))
-        return a.value, b.value, ln.value, ext.value
+        """ac_plan_rank_chunks: (chunks, n_eff, chunk_len, extent) - the chunks of
+        `region` that `rank` of `world` runs."""
+        cnt, ne, ln, ext = C.c_int32(), C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().ac_plan_rank_chunks(self._h, region, rank, world, None, 0, C.byref(cnt), None, None, None))
+        arr = (C.c_int64 * max(cnt.value, 1))()
+        check(lib().ac_plan_rank_chunks(self._h, region, rank, world, arr, cnt.value, C.byref(cnt), C.byref(ne),
+                                        C.byref(ln), C.byref(ext)))
+        return list(arr)[: cnt.value], ne.value, ln.value, ext.value
+
+    def rank_schedule(self, rank: int, world: int):
+        """ac_plan_rank_schedule: (node_region, node_dim, ops) - per node the region
+        share it runs on (-1 whole) and its output dim, and the exchanges as dicts."""
+        nn = self.graph.num_nodes
+        nr, nd = (C.c_int32 * max(nn, 1))(), (C.c_int32 * max(nn, 1))()
+        cnt = C.c_int32()
+        check(lib().ac_plan_rank_schedule(self._h, rank, world, nr, nd, None, 0, C.byref(cnt)))
+        ops = (L.ExchangeOp * max(cnt.value, 1))()
+        check(lib().ac_plan_rank_schedule(self._h, rank, world, nr, nd, ops, cnt.value, C.byref(cnt)))
+        out = [{f: (getattr(o, f).decode() if f == "tensor" else getattr(o, f)) for f, _ in L.ExchangeOp._fields_}
+               for o in ops[: cnt.value]]
+        return list(nr)[:nn], list(nd)[:nn], out
 
     def workspace_bytes(self, rank: int = 0, world: int = 1) -> int:
         v = lib().ac_plan_workspace_bytes(self._h, rank, world)
@@ -157,10 +173,14 @@ def estimate_memory(g: Graph, plan: Plan | None = None):
 class Comm:
     """NCCL communicator (ac_comm_*); `unique_id` is broadcast by the caller."""
 
-    def __init__(self, unique_id: bytes, rank: int, world: int, device: int):
-        out = C.c_void_p()
-        check(lib().ac_comm_init(unique_id, rank, world, device, C.byref(out)))
-        self._h = out
+    def __init__(self, unique_id: bytes | None, rank: int, world: int, device: int, handle=None):
+        if handle is not None:
+            self._h = C.c_void_p(handle)
+        else:
+            out = C.c_void_p()
+            check(lib().ac_comm_init(unique_id, rank, world, device, C.byref(out)))
+            self._h = out
+        self.rank, self.world = rank, world
 
     @staticmethod
     def unique_id() -> bytes:
@@ -168,13 +188,26 @@ class Comm:
         check(lib().ac_comm_get_unique_id(buf))
         return buf.raw
 
+    @staticmethod
+    def local(world: int) -> list:
+        """ac_comm_init_local: `world` in-process ranks on the current device (tests)."""
+        arr = (C.c_void_p * world)()
+        check(lib().ac_comm_init_local(world, arr))
+        return [Comm(None, r, world, 0, handle=arr[r]) for r in range(world)]
+
+    def check(self):
+        check(lib().ac_comm_check(self._h))
+
     @property
     def handle(self):
         return self._h
 
     def __del__(self):
         if getattr(self, "_h", None) and self._h.value:
-            lib().ac_comm_free(self._h)
+            try:
+                lib().ac_comm_free(self._h)
+            except TypeError:  # interpreter shutdown
+                pass
             self._h = None
 
 

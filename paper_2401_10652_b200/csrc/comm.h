@@ -1,9 +1,10 @@
-// NCCL communicator for the multi-GPU chunk split.
+// Communicators for the multi-GPU chunk split: NCCL over
+// NVLink (libnccl resolved at run time), or an in-process emulation of the same
+// collectives on one device (ac_comm_init_local, for tests on a single GPU).
 #pragma once
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <vector>
 
 #include "../../include/ac.h"
 
@@ -12,14 +13,19 @@ namespace ac {
 int comm_rank(const ac_comm* c);
 int comm_world(const ac_comm* c);
 
-// Each rank owns chunks [floor(q n / W), floor((q+1) n / W)) of a region; make
-// every rank's copy of the Y^c tensor complete by broadcasting each owner's
-// slab (dim d, chunk length L, extent E).  Slabs must be contiguous (d == 0 or
-// all leading extents 1).
-ac_status comm_gather_slabs(const ac_comm* c, void* y, const std::vector<int64_t>& shape, int d, int esz,
-                            int64_t E, int64_t L, int64_t n, cudaStream_t s);
+// Non-blocking health check (ncclCommGetAsyncError on both communicators).
+ac_status comm_check(const ac_comm* c);
 
-// Partition arithmetic shared with the CPU tests: first chunk of rank q.
-inline int64_t chunk_begin(int64_t q, int64_t n, int64_t W) { return q * n / W; }
+// Brackets a batch of collectives (ncclGroupStart / ncclGroupEnd; no-op emulated).
+ac_status comm_group_start(const ac_comm* c);
+ac_status comm_group_end(const ac_comm* c);
+
+// In-place all-gather of `bytes` per rank: rank q's segment sits at position
+// xop_pos(kind, q, W) of buf (kind X_ALLGATHER: the communicator's rank order,
+// X_ALLGATHER_REV: the rank-reversed communicator, ncclCommSplit key W-1-q).
+ac_status comm_allgather(const ac_comm* c, int kind, void* buf, int64_t bytes, cudaStream_t s);
+
+// In-place broadcast of `bytes` from rank `root`.
+ac_status comm_bcast(const ac_comm* c, void* buf, int64_t bytes, int root, cudaStream_t s);
 
 }  // namespace ac

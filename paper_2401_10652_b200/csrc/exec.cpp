@@ -12,8 +12,11 @@
 //   narrowed along their chunk dim (pointer offset, same strides; TMA reads the
 //   strided slice, so no contiguity copy, R5), interior tensors are the scratch
 //   buffer narrowed to the chunk's length.  Y^c slices are written in place.
-// * Multi-GPU (§8(e)): rank r runs chunks [floor(r n / W), floor((r+1) n / W))
-//   and the Y^c slabs are exchanged with NCCL broadcasts from their owners.
+// * Multi-GPU (§8(e), partition.h): rank r runs its share of every region's chunks
+//   (zigzag / round-robin groups), the row-local nodes around a region on its
+//   rows only, and the exchanges of its RankSchedule: in-place all-gathers where a
+//   tensor is needed whole, region outputs group by group on a communication
+//   stream while the chunk loop goes on.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -27,6 +30,7 @@
 #include "errors.h"
 #include "handles.h"
 #include "kernels.h"
+#include "partition.h"
 
 using namespace ac;
 
@@ -52,6 +56,7 @@ struct Arena {
   // ints: [epoch: B][tile counters: n][PV unit counters: n][PV done counts: n x B]
   std::vector<int64_t> ctrl_off;
   std::vector<int64_t> ctrl_b, ctrl_n, ctrl_mt;  // ctrl_mt: split-K tile counters per launch
+  int64_t staging_off = -1;                      // multi-GPU packed all-gathers (RankSchedule::staging)
 };
 
 struct View {
@@ -88,6 +93,9 @@ struct ac_exec {
   int64_t ws_bytes = 0;
   const ac_comm* comm = nullptr;
   int rank = 0, world = 1;
+  RankSchedule sched;                  // this rank's chunks, row-partitioned nodes, exchanges
+  cudaStream_t comm_s = nullptr;       // eager region-output gathers (world > 1)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DT dt = DT::BF16;
   std::vector<int> region_of;          // node -> region index or -1
   std::vector<char> causal_fast;       // per node: member of an aligned causal chain
@@ -106,6 +114,9 @@ struct ac_exec {
   mutable std::vector<int> ev_node;    // node of launch k (events 2k, 2k+1)
   ~ac_exec() {
     for (auto ev : ev_pool) cudaEventDestroy(ev);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (comm_s) cudaStreamDestroy(comm_s);
   }
 };
 
@@ -195,7 +206,7 @@ F2Ctrl f2_ctrl(int64_t B1, int64_t M, int64_t nk, bool split) {
   return L;
 }
 
-Arena build_arena(const Graph& g, const Plan& plan, const ExecOptions& o) {
+Arena build_arena(const Graph& g, const Plan& plan, const ExecOptions& o, int world = 1) {
   const int T = static_cast<int>(g.tensors.size());
   const int S = static_cast<int>(g.nodes.size());
   Arena A;
@@ -333,12 +344,22 @@ Arena build_arena(const Graph& g, const Plan& plan, const ExecOptions& o) {
         B *= sh[d];
         Bl *= shc[d];
       }
-      const int64_t n = plan.regions[r].n;
+      // chunks this chain's loop may run on one rank (<= the plan's n, or its refinement
+      // on `world` ranks, partition.h)
+      Own own;
+      const int64_t n = std::max(plan.regions[r].n, share_n(g, plan.regions[r], world, &own));
       A.ctrl_off[c.scores] = A.size;
       A.ctrl_b[c.scores] = B;
       A.ctrl_n[c.scores] = n;
       A.ctrl_mt[c.scores] = Bl * ((shc[shc.size() - 2] + 127) / 128);
       A.size += (ctrl_ints(B, n, A.ctrl_mt[c.scores]) * 4 + 255) / 256 * 256;
+    }
+  }
+  if (world > 1) {
+    const int64_t st = rank_schedule(g, plan, 0, world).staging;
+    if (st > 0) {
+      A.staging_off = A.size;
+      A.size += (st + 255) / 256 * 256;
     }
   }
   return A;
@@ -819,7 +840,7 @@ int64_t ac_plan_workspace_bytes(const ac_chunk_plan* p, int32_t rank, int32_t wo
     set_error(AC_ERR_ARG, "ac_plan_workspace_bytes: bad arguments");
     return -1;
   }
-  return build_arena(*p->g, p->plan, read_options()).size;
+  return build_arena(*p->g, p->plan, read_options(), world).size;
 }
 
 ac_status ac_plan_arena_profile(const ac_chunk_plan* p, int64_t* live_per_step, int64_t* live_peak,
@@ -840,16 +861,51 @@ ac_status ac_plan_arena_profile(const ac_chunk_plan* p, int64_t* live_per_step, 
   return AC_OK;
 }
 
-ac_status ac_plan_rank_chunks(const ac_chunk_plan* p, int32_t region, int32_t rank, int32_t world, int64_t* c0,
-                              int64_t* c1, int64_t* chunk_len, int64_t* extent) {
-  if (!p || !c0 || !c1 || world < 1 || rank < 0 || rank >= world || region < 0 ||
+ac_status ac_plan_rank_chunks(const ac_chunk_plan* p, int32_t region, int32_t rank, int32_t world,
+                              int64_t* chunks, int32_t cap, int32_t* n_chunks, int64_t* n_eff, int64_t* chunk_len,
+                              int64_t* extent) {
+  if (!p || !n_chunks || world < 1 || rank < 0 || rank >= world || region < 0 || cap < 0 ||
       region >= static_cast<int32_t>(p->plan.regions.size()))
     return set_error(AC_ERR_ARG, "ac_plan_rank_chunks: bad arguments");
-  const Region& R = p->plan.regions[region];
-  *c0 = chunk_begin(rank, R.n, world);
-  *c1 = chunk_begin(rank + 1, R.n, world);
-  if (chunk_len) *chunk_len = R.chunk_len();
-  if (extent) *extent = R.extent;
+  const RankSchedule rs = rank_schedule(*p->g, p->plan, rank, world);
+  const RegionShare& sh = rs.reg[region];
+  *n_chunks = static_cast<int32_t>(sh.chunks.size());
+  for (int32_t k = 0; k < cap && k < *n_chunks; ++k) chunks[k] = sh.chunks[k];
+  if (n_eff) *n_eff = sh.n;
+  if (chunk_len) *chunk_len = sh.L;
+  if (extent) *extent = sh.E;
+  return AC_OK;
+}
+
+ac_status ac_plan_rank_schedule(const ac_chunk_plan* p, int32_t rank, int32_t world, int32_t* node_region,
+                                int32_t* node_dim, ac_exchange_op* ops, int32_t cap, int32_t* n_ops) {
+  if (!p || !n_ops || world < 1 || rank < 0 || rank >= world || cap < 0)
+    return set_error(AC_ERR_ARG, "ac_plan_rank_schedule: bad arguments");
+  const Graph& g = *p->g;
+  const RankSchedule rs = rank_schedule(g, p->plan, rank, world);
+  for (size_t i = 0; i < g.nodes.size(); ++i) {
+    if (node_region) node_region[i] = rs.node_region[i];
+    if (node_dim) node_dim[i] = rs.node_dim[i];
+  }
+  *n_ops = static_cast<int32_t>(rs.ops.size());
+  for (int32_t k = 0; k < cap && k < *n_ops; ++k) {
+    const XOp& x = rs.ops[k];
+    ac_exchange_op& o = ops[k];
+    memset(&o, 0, sizeof(o));
+    o.kind = x.kind;
+    o.before_node = x.before;
+    o.region = x.region;
+    o.eager = x.eager;
+    o.group = x.group;
+    o.c_first = x.c_first;
+    o.dim = x.dim;
+    o.root = x.root;
+    o.outer = x.outer;
+    o.run_bytes = x.run;
+    o.ext_bytes = x.ext;
+    o.offset = x.offset;
+    strncpy(o.tensor, g.tensors[x.tensor].id.c_str(), sizeof(o.tensor) - 1);
+  }
   return AC_OK;
 }
 
@@ -862,16 +918,23 @@ ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_
   e->g = plan->g;
   e->plan = plan->plan;
   e->opt = read_options();
-  e->arena = build_arena(g, plan->plan, e->opt);
+  e->comm = comm;
+  if (comm) {
+    e->rank = comm_rank(comm);
+    e->world = comm_world(comm);
+  }
+  e->arena = build_arena(g, plan->plan, e->opt, e->world);
   if (ws_bytes < e->arena.size || (e->arena.size > 0 && !workspace))
     return set_error(AC_ERR_WORKSPACE, "workspace of " + std::to_string(ws_bytes) + " bytes < required " +
                                            std::to_string(e->arena.size));
   e->ws = static_cast<char*>(workspace);
   e->ws_bytes = ws_bytes;
-  e->comm = comm;
-  if (comm) {
-    e->rank = comm_rank(comm);
-    e->world = comm_world(comm);
+  e->sched = rank_schedule(g, plan->plan, e->rank, e->world);
+  if (e->world > 1) {
+    if (cudaStreamCreateWithFlags(&e->comm_s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess)
+      return set_error(AC_ERR_CUDA, "communication stream / events");
   }
   // one element type for the whole graph (f32 -> SIMT path, bf16 -> tcgen05 path)
   e->dt = g.tensors.empty() ? DT::BF16 : g.tensors[0].dtype;
@@ -1061,6 +1124,71 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
     if (g.is_input[t] || g.is_output[t]) e->stats.caller_bytes += g.tensors[t].bytes();
 
   const int S = static_cast<int>(g.nodes.size());
+  const RankSchedule& rs = e->sched;
+  if (e->world > 1) {
+    ac_status st = comm_check(e->comm);  // a failed collective of an earlier run surfaces here
+    if (st != AC_OK) return st;
+  }
+  // exchanges of the rank schedule (partition.h): the ops needed by node `before`
+  // (S: the graph outputs at the end), issued on stream `st_` in schedule order;
+  // consecutive broadcasts are batched in one NCCL group
+  auto issue = [&](const XOp& x, cudaStream_t st_) -> ac_status {
+    char* base = full[x.tensor].p;
+    if (x.kind == X_BCAST) return comm_bcast(e->comm, base + x.offset, x.run, x.root, st_);
+    if (x.outer == 1) return comm_allgather(e->comm, x.kind, base + x.c_first * x.run, x.run, st_);
+    // chunk dim not outermost: pack this rank's chunk (one run per outer index) into
+    // the staging buffer [W][outer][run], gather it, unpack the peers' chunks
+    char* stg = e->ws + e->arena.staging_off;
+    const int W = e->world, pos = xop_pos(x.kind, e->rank, W);
+    const int64_t cnt = x.outer * x.run;
+    if (cudaMemcpy2DAsync(stg + pos * cnt, x.run, base + (x.c_first + pos) * x.run, x.ext, x.run, x.outer,
+                          cudaMemcpyDeviceToDevice, st_) != cudaSuccess)
+      return set_error(AC_ERR_CUDA, "staging pack");
+    ac_status r = comm_allgather(e->comm, x.kind, stg, cnt, st_);
+    if (r != AC_OK) return r;
+    for (int q = 0; q < W; ++q) {
+      const int pq = xop_pos(x.kind, q, W);
+      if (pq == pos) continue;
+      if (cudaMemcpy2DAsync(base + (x.c_first + pq) * x.run, x.ext, stg + pq * cnt, x.run, x.run, x.outer,
+                            cudaMemcpyDeviceToDevice, st_) != cudaSuccess)
+        return set_error(AC_ERR_CUDA, "staging unpack");
+    }
+    return AC_OK;
+  };
+  auto issue_list = [&](const std::vector<const XOp*>& xs, cudaStream_t st_) -> ac_status {
+    for (size_t k = 0; k < xs.size();) {
+      if (xs[k]->kind != X_BCAST) {
+        ac_status r = issue(*xs[k++], st_);
+        if (r != AC_OK) return r;
+        continue;
+      }
+      ac_status r = comm_group_start(e->comm);
+      for (int m = 0; r == AC_OK && k < xs.size() && xs[k]->kind == X_BCAST && m < 512; ++m) r = issue(*xs[k++], st_);
+      ac_status r2 = comm_group_end(e->comm);
+      if (r != AC_OK) return r;
+      if (r2 != AC_OK) return r2;
+    }
+    return AC_OK;
+  };
+  auto issue_before = [&](int before) -> ac_status {
+    std::vector<const XOp*> xs;
+    for (const XOp& x : rs.ops)
+      if (!x.eager && x.before == before) xs.push_back(&x);
+    if (xs.empty()) return AC_OK;
+    e->stats.exchanges += static_cast<int32_t>(xs.size());
+    return issue_list(xs, s);
+  };
+  // the rank's rows of a partitioned node's share: owned chunks merged into ranges
+  auto owned_rows = [&](const RegionShare& sh) {
+    std::vector<std::pair<int64_t, int64_t>> rows;
+    for (int64_t c : sh.chunks) {
+      const int64_t a = c * sh.L, b = std::min(sh.E, (c + 1) * sh.L);
+      if (b <= a) continue;
+      if (!rows.empty() && rows.back().second == a) rows.back().second = b;
+      else rows.push_back({a, b});
+    }
+    return rows;
+  };
   int i = 0;
   // launches outside chunk loops (GEMMs, LayerNorm, fused attention) after a kernel of
   // this run overlap their prologue with its tail too (AC_PDL=0 off)
@@ -1072,32 +1200,55 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
       ++i;
       continue;
     }
+    if (e->world > 1) {
+      const int32_t before = e->stats.exchanges;
+      ac_status st = issue_before(i);
+      if (st != AC_OK) return st;
+      if (e->stats.exchanges != before) prev_kernel = 0;
+    }
     const int r = e->region_of[i];
     if (r < 0 || e->plan.regions[r].n <= 1) {
       NodeCtx cx;
       cx.fast = e->causal_fast[i] != 0;
       const std::string& kd = n.kind;
-      cx.pdl = run_pdl && prev_kernel && e->fuse_role[i] == 0 &&
-                       (kd == "linear" || kd == "layernorm" || kd == "attn_fused" || kd == "tri_mul" ||
-                        kd == "ln_cfirst")
-                   ? 1
-                   : 0;
+      const bool pdl_kind = run_pdl && e->fuse_role[i] == 0 &&
+                            (kd == "linear" || kd == "layernorm" || kd == "attn_fused" || kd == "tri_mul" ||
+                             kd == "ln_cfirst");
+      cx.pdl = pdl_kind && prev_kernel ? 1 : 0;
       prev_kernel = 1;
-      ac_status st = launch_node(e, i, full, cx, s);
-      if (st != AC_OK) return st;
+      if (rs.node_region[i] >= 0) {
+        // row-partitioned (multi-GPU): this rank's rows of the region share only
+        const int d = rs.node_dim[i];
+        std::vector<std::vector<int64_t>> in;
+        for (int t : n.inputs) in.push_back(g.tensors[t].shape);
+        const std::vector<int> res = op_propagate(n.kind, n, in, g.tensors[n.output].shape, d);
+        for (auto& ab : owned_rows(rs.reg[rs.node_region[i]])) {
+          std::vector<View> V = full;
+          for (size_t q = 0; q < n.inputs.size(); ++q)
+            if (res[q] >= 0) V[n.inputs[q]] = narrow(full[n.inputs[q]], res[q], ab.first, ab.second - ab.first, esz);
+          V[n.output] = narrow(full[n.output], d, ab.first, ab.second - ab.first, esz);
+          NodeCtx c2 = cx;
+          if (d == e->chain_rows_dim[i]) c2.row_off = ab.first;
+          ac_status st = launch_node(e, i, V, c2, s);
+          if (st != AC_OK) return st;
+          cx.pdl = pdl_kind ? 1 : 0;  // the next range follows this launch
+        }
+      } else {
+        ac_status st = launch_node(e, i, full, cx, s);
+        if (st != AC_OK) return st;
+      }
       ++i;
       continue;
     }
     const Region& R = e->plan.regions[r];
+    const RegionShare& sh = rs.reg[r];
     for (int h : R.hoisted) {
       NodeCtx cx;
       cx.fast = e->causal_fast[h] != 0;
       ac_status st = launch_node(e, h, full, cx, s);
       if (st != AC_OK) return st;
     }
-    const int64_t L = R.chunk_len();
-    const int64_t c0 = chunk_begin(e->rank, R.n, e->world);
-    const int64_t c1 = chunk_begin(e->rank + 1, R.n, e->world);
+    const int64_t L = sh.L;
     std::set<int> hs(R.hoisted.begin(), R.hoisted.end());
     std::set<int> ycs;
     for (auto& y : R.yc) ycs.insert(y.first);
@@ -1111,9 +1262,15 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
           return set_error(AC_ERR_CUDA, "cudaMemsetAsync (chunk-loop control block) failed");
       }
     }
+    // eager exchanges of this region's outputs, per ownership group
+    std::vector<const XOp*> eager;
+    for (const XOp& x : rs.ops)
+      if (x.eager && x.region == r) eager.push_back(&x);
+    bool forked = false;
     bool first_launch = true;
     const bool loop_pdl = e->opt.pdl;
-    for (int64_t c = c0; c < c1; ++c) {
+    for (size_t ci = 0; ci < sh.chunks.size(); ++ci) {
+      const int64_t c = sh.chunks[ci];
       const int64_t off = c * L;
       const int64_t len = std::min(L, R.extent - off);
       if (len <= 0) break;
@@ -1163,7 +1320,7 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
         }
         NodeCtx cx;
         cx.fast = e->causal_fast[j] != 0;
-        cx.chunk = static_cast<int>(c - c0);
+        cx.chunk = static_cast<int>(ci);
         // every launch of the chunk loop but the first may start during its
         // predecessor's tail (it waits in-kernel before touching data); AC_PDL=0 off
         cx.pdl = loop_pdl && !first_launch ? 1 : 0;
@@ -1179,15 +1336,35 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
         if (st != AC_OK) return st;
       }
       e->stats.chunks_run += 1;
-    }
-    if (e->world > 1) {
-      for (auto& y : R.yc) {
-        ac_status st = comm_gather_slabs(e->comm, full[y.first].p, g.tensors[y.first].shape, y.second, esz,
-                                         R.extent, L, R.n, s);
-        if (st != AC_OK) return st;
+      // the rank's last chunk of an ownership group: that group's region outputs are
+      // complete here, so their all-gathers start on the communication stream while
+      // the next group's chunks run
+      if (!eager.empty() && sh.group > 0 &&
+          (ci + 1 == sh.chunks.size() || sh.chunks[ci + 1] / sh.group != c / sh.group)) {
+        std::vector<const XOp*> xs;
+        for (const XOp* x : eager)
+          if (x->group == c / sh.group) xs.push_back(x);
+        if (!xs.empty()) {
+          if (cudaEventRecord(e->ev_fork, s) != cudaSuccess ||
+              cudaStreamWaitEvent(e->comm_s, e->ev_fork, 0) != cudaSuccess)
+            return set_error(AC_ERR_CUDA, "fork to the communication stream");
+          ac_status st = issue_list(xs, e->comm_s);
+          if (st != AC_OK) return st;
+          e->stats.exchanges += static_cast<int32_t>(xs.size());
+          forked = true;
+        }
       }
     }
+    if (forked) {
+      if (cudaEventRecord(e->ev_join, e->comm_s) != cudaSuccess || cudaStreamWaitEvent(s, e->ev_join, 0) != cudaSuccess)
+        return set_error(AC_ERR_CUDA, "join of the communication stream");
+      prev_kernel = 0;
+    }
     i = R.end + 1;
+  }
+  if (e->world > 1) {
+    ac_status st = issue_before(S);
+    if (st != AC_OK) return st;
   }
   return cuda_status(cudaGetLastError(), "ac_run");
 }

@@ -765,7 +765,9 @@ Plan parse_user_plan(const Graph& g, const std::string& text) {
     for (int i = s; i <= e; ++i)
       if (g.nodes[i].source()) throw GraphError{"illegal region: contains an input/weight node"};
     Region r;
-    if (!candidate_for(g, s, e, dims, true, r)) throw GraphError{"illegal region: no legal chunk flow for these dims"};
+    // opt=0: graph optimisation (hoisting) off for this region
+    const bool hoist = !(kv.count("opt") && kv["opt"] == "0");
+    if (!candidate_for(g, s, e, dims, hoist, r)) throw GraphError{"illegal region: no legal chunk flow for these dims"};
     if (n < 1 || n > r.extent) throw GraphError{"chunk count n outside [1, extent]"};
     r.n = n;
     for (auto& o : plan.regions)

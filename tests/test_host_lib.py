@@ -167,6 +167,13 @@ def test_user_plan_parse_matches_oracle():
     p = api.plan_parse(cg, whole)
     ref = select.user_plan(g, [("proj_q", "ffn2", 8, (0,))])
     assert p.serialize() == oplan.serialize(ref, g)
+    # opt=0: graph optimisation off for the region (K / V projections recomputed per chunk)
+    for txt in ("autochunk-plan 1\nregion s=proj_q e=pv n=8 dims=0 opt=0\n",
+                "autochunk-plan 1\nregion s=proj_q e=ffn2 n=4 dims=0 opt=0\n"):
+        p = api.plan_parse(cg, txt)
+        ref = select.user_plan(g, oplan.parse_user_regions(txt))
+        assert p.serialize() == oplan.serialize(ref, g)
+        assert "hoist=- " in p.serialize()
     # the canonical text of an ac_plan result parses back to the same plan
     full = api.ac_plan(cg, int(0.2 * memory.profile(g).peak_bytes))
     again = api.plan_parse(cg, full.serialize())
