@@ -63,7 +63,8 @@ def parse():
     ap.add_argument("--maxlen", action="store_true",
                     help="NEXT f3: max sequence length whose unchunked / ac_plan peak fits this GPU's free HBM "
                          "(api.max_length), then run the chunked plan at --maxlen-run tokens")
-    ap.add_argument("--maxlen-run", type=int, default=262144)
+    ap.add_argument("--maxlen-run", type=int, default=0,
+                    help="length of the capacity run (0: the chunked maximum itself)")
     ap.add_argument("--ablation", action="store_true",
                     help="also run the paper's Table 1 toggles (P:319-332): ac_plan with each cost term / "
                          "graph optimisation switched off, at 20/10/5 %% budgets; every distinct plan timed")
@@ -187,14 +188,15 @@ def device_inputs_gpu(doc, torch, seed=0):
     TD = {"bf16": torch.bfloat16, "f32": torch.float32}
     dev = {}
     for t, kind, dt, shp, role, fan in doc.input_specs():
-        v = torch.randn(shp, generator=gen, device="cuda", dtype=torch.float32)
+        v = torch.randn(shp, generator=gen, device="cuda", dtype=TD[dt])   # (no fp32 temporaries)
         if role == "matrix":
             v *= 1.0 / max(fan, 1) ** 0.5
         elif role in ("bias", "ln_beta"):
             v *= 0.02
         elif role == "ln_gamma":
-            v = 1.0 + 0.02 * v
-        dev[t] = v.to(TD[dt])
+            v.mul_(0.02).add_(1.0)
+        dev[t] = v
+    torch.cuda.empty_cache()
     return dev
 
 
@@ -396,11 +398,22 @@ def maxlen_arm(args):
     ml = api.max_length(kind, d, h, f, causal, dt, budget, layers=args.layers, step=step, cap=cap)
     t_search = time.perf_counter() - t0
     run = None
-    Nr = min(args.maxlen_run, ml["chunked"]) if ml["chunked"] else 0
-    if Nr:
+    Nr = min(args.maxlen_run or ml["chunked"], ml["chunked"]) if ml["chunked"] else 0
+    fit_note = None
+    while Nr:
+        # the caller holds the inputs and outputs for the whole run (the plan's liveness
+        # frees x after its last use and allocates y when produced), so the capacity run
+        # may need up to x + y more than the planned peak: step down until it fits
         cg, doc = c_graph(args.config, args.layers, N=Nr)
-        prof0, _ = api.estimate_memory(cg)
         plan = api.ac_plan(cg, budget)
+        need = plan.workspace_bytes() + sum(doc.nbytes(t) for t in doc.inputs + doc.outputs) + wbytes
+        if need < free - (1 << 30):
+            break
+        fit_note = (f"executed below the planner's maximum: workspace + caller-held inputs / outputs "
+                    f"at {ml['chunked']} exceed the free HBM")
+        Nr -= step * max(1, (Nr // 50) // step)
+    if Nr:
+        prof0, _ = api.estimate_memory(cg)
         profp, _ = api.estimate_memory(cg, plan)
         dev = device_inputs_gpu(doc, torch)   # (host-free: the capacity run checks finiteness only)
         TD = {"bf16": torch.bfloat16, "f32": torch.float32}
@@ -411,7 +424,8 @@ def maxlen_arm(args):
         ws = torch.empty(max(plan.workspace_bytes(), 16), dtype=torch.uint8, device="cuda")
         ex = api.Exec(plan, ws)
         ins = {t: dev[t] for t in doc.order}
-        ex.run(ins, outs)
+        if Nr <= 4 * N0:     # (a capacity run at the maximum is timed once: it runs for seconds)
+            ex.run(ins, outs)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
@@ -428,7 +442,8 @@ def maxlen_arm(args):
                "workspace_bytes": ex.stats().workspace_high_water,
                "arena_live_peak": ex.stats().arena_live_peak,
                "torch_peak_delta_bytes": torch.cuda.max_memory_allocated() - base,
-               "output_finite": bool(torch.isfinite(y.float()).all().item())}
+               "output_finite": all(bool(torch.isfinite(c).all().item()) for c in y.view(-1).split(1 << 26)),
+               **({"note": fit_note} if fit_note else {})}
     line = {"metric": "max inference length under this GPU's HBM (P:357-361)", "value": ml["chunked"],
             "unit": "tokens" if not pair else "residues", "n_gpus": 1,
             "higher_is_better": True, "dtype": dt, "data": "synthetic",
@@ -728,20 +743,30 @@ def main():
                "d2h_bytes_per_step": hy.numel() * hy.element_size(),
                "pipelined": "H2D / D2H on two copy streams overlapping the neighbouring steps' ac_run"}
 
-    # chunk-length sweep of the attention region (BASELINE.json configs[4]: UNet 64..4096)
+    # chunk-size sweep of the plan's regions (BASELINE.json configs[4]: UNet chunk
+    # length 64..4096; the same for GPT / ViT; AlphaFold: n = 4..128 on both attentions)
     sweep = None
     if args.sweep and not args.profile:
         sweep = []
-        N = doc.tensors[doc.inputs[0]][1][0]
-        for L in (64, 128, 256, 512, 1024, 2048, 4096):
-            n = -(-N // L)
-            sp = api.plan_parse(cg, f"autochunk-plan 1\nregion s=scores e=pv n={n} dims=0\n")
+        base_regions = [dict(x.split("=", 1) for x in ln.split()[1:]) for ln in plan.serialize().splitlines()
+                        if ln.startswith("region")]
+        pair = args.config in ("af", "af_attn")
+        ladder = (4, 8, 16, 32, 64, 128) if pair else \
+            [-(-int(base_regions[0]["ext"]) // L) for L in (64, 128, 256, 512, 1024, 2048, 4096)] if base_regions else []
+        for n in ladder:
+            txt = "autochunk-plan 1\n" + "".join(f"region s={r['s']} e={r['e']} n={n} yc={r['yc']}\n"
+                                                 for r in base_regions)
+            sp = api.plan_parse(cg, txt)
             pr, _ = api.estimate_memory(cg, sp)
             wss = torch.empty(max(sp.workspace_bytes(), 16), dtype=torch.uint8, device="cuda")
             exs = api.Exec(sp, wss, comm)
-            ts, _ = timed(exs, ins, outs, max(2, args.steps // 2), 1)
-            sweep.append({"chunk_len": L, "n": n, "tokens_per_s": units * max(2, args.steps // 2) / (ts / 1e3),
-                          "planned_peak": pr.peak_bytes, "peak_frac": pr.peak_bytes / prof0.peak_bytes})
+            ks = max(2, args.steps // 2)
+            ts, _ = timed(exs, ins, outs, ks, 1)
+            sweep.append({"n": n, "chunk_len": -(-int(base_regions[0]["ext"]) // n),
+                          "tokens_per_s": round(units * ks / (ts / 1e3), 1), "planned_peak": pr.peak_bytes,
+                          "peak_frac": round(pr.peak_bytes / prof0.peak_bytes, 4),
+                          "speed_vs_unchunked": round(units * ks / (ts / 1e3) / unchunked["value"], 4)
+                          if unchunked and unchunked.get("value") else None})
             del exs, wss
         torch.cuda.empty_cache()
 

@@ -1,20 +1,27 @@
 // NEXT f1: fused (memory-efficient) attention for sm_100a, o = softmax(q k^T * scale) v
 // with no N x N tensor in HBM (the "fused attention kernel" regime of the paper,
-// P:350-351; the graph node kind attn_fused).  One CTA per SM, persistent over
-// (head, 128-row query tile) work tiles, causal tiles heaviest first.
+// P:350-351; the graph node kind attn_fused).  One CTA per SM, persistent over work
+// units of NT query tiles (128 rows each, the same head, adjacent rows), causal units
+// heaviest first.
 //
-//   warp 0     : TMA producer - Q tile once per work tile, K / V^T blocks of 128
-//                keys through a 3-stage ring (128B swizzle)
-//   warp 1     : TMEM allocator + MMA issuer: S_j = Q K_j^T into one of two TMEM
-//                S buffers (M=128, N=128, K=64), O += P_j V_j (M=128, N=64, K=128)
-//                into the TMEM O accumulator; order S_0, S_1, PV_0, S_2, PV_1, ...
-//   warps 2..5 : softmax, thread = query row: online max / sum in the log2 domain
-//                (x = s * scale * log2 e), P_j = 2^(x - m) rounded to bf16 into a
-//                shared-memory A operand (128B-swizzled, two 64-key k-blocks), the
-//                O accumulator rescaled by 2^(m_old - m_new) in TMEM before PV_j,
-//                and at the end o = O / l stored as bf16.
-// Same arithmetic whatever chunk a query row falls in (the key loop and its order
-// depend only on the global row), so chunked == unchunked bitwise.
+//   warp 0       : TMA producer - the unit's Q tiles once, K / V^T blocks of 128 keys
+//                  through a 3-stage ring shared by the NT tiles (128B swizzle)
+//   warp 1       : TMEM allocator + MMA issuer.  Jobs (tile t, key block j) in the
+//                  order j-major, t-minor; S = Q_t K_j^T (M=128, N=128, K=64) into one
+//                  of two TMEM slots (NT = 2: the tile's own slot, the two tiles' softmax
+//                  and MMA phases ping-pong; NT = 1: alternating slots, so S_{j+1} runs
+//                  during softmax_j); O_t += P V_j (M=128, N=64, K=128) with P read from
+//                  TMEM (the slot's first 64 columns, bf16 pairs) - issued right before
+//                  the slot's next S, so the tensor core's in-order execution keeps the
+//                  slot's WAR order
+//   warps 2, 3   : idle (NT = 2: registers handed to the softmax warpgroups)
+//   warpgroup 1+t: softmax of tile t, thread = query row over all 128 keys of a block:
+//                  max, lazy online reference (moves only when the block max exceeds
+//                  it by FA_LAZY log2 units, so most blocks need no O rescale),
+//                  P = bf16(2^(x - m)) stored to TMEM, l += sum; O rescaled in TMEM when
+//                  the reference moved; at the end o = O / l stored as bf16.
+// Same arithmetic whatever chunk a query row falls in (the key loop, its order and the
+// reference sequence depend only on the global row), so chunked == unchunked bitwise.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -31,84 +38,87 @@ namespace ac {
 
 namespace {
 
-constexpr int FA_BM = 128;   // query rows per tile
-// Key block BNK = 128 (one CTA per SM) or 64 (two CTAs per SM, whose softmax and
-// MMA phases interleave; chosen when the launch has at least two tiles per SM)
-template <int BNK>
+constexpr int FA_BM = 128;       // query rows per tile
+constexpr int FA_BN = 128;       // keys per block
+constexpr int FA_DH = 64;        // head dim (one 128-byte swizzle row)
+constexpr int FA_STG = 3;        // K/V ring depth
+constexpr float FA_LAZY = 8.f;   // reference-update threshold of the online softmax (log2 units)
+constexpr int Q_BYTES = FA_BM * FA_DH * 2;   // 16 KB
+constexpr int K_BYTES = FA_BN * FA_DH * 2;   // 16 KB
+constexpr int V_BYTES = FA_DH * FA_BN * 2;   // 16 KB: two 64-key boxes of 8 KB
+constexpr int O_COL = 256;                   // TMEM: slots at columns 0 / 128, O_t at 256 + 64 t
+
+template <int NT>
 struct FaCfg {
-  static constexpr int BN = BNK;        // keys per block
-  static constexpr int HK = BNK / 2;    // keys per softmax half-row
-  static constexpr int MINB = BNK == 64 ? 2 : 1;
-  static constexpr int OCOL = 2 * BNK;  // TMEM column of the O accumulator (after two S buffers)
-  static constexpr int TMEM = OCOL + 64 <= 256 ? 256 : 512;
-  static constexpr int K_BYTES = BNK * 64 * 2;
-  static constexpr int V_BYTES = 64 * BNK * 2;   // 64-key boxes of 8 KB
-  static constexpr int P_BYTES = 128 * BNK * 2;  // 64-key k-blocks of 16 KB
-  static constexpr int SMEM = 1024 + 128 * 64 * 2 + 3 * (K_BYTES + V_BYTES) + 2 * P_BYTES + 256 + 2 * 2 * 128 * 4 +
-                              128 * 4 * 2;
+  static constexpr int THREADS = 128 * (1 + NT);
+  static constexpr int SMEM = 1024 + NT * Q_BYTES + FA_STG * (K_BYTES + V_BYTES) + 256;
 };
-constexpr int FA_DH = 64;    // head dim (one 128-byte swizzle row)
-constexpr int FA_STG = 3;    // K/V ring depth
-constexpr int FA_THREADS = 320;  // producer, MMA, 8 softmax warps
-constexpr int Q_BYTES = FA_BM * FA_DH * 2;        // 16 KB
 
 struct alignas(64) FaArgs {
   CUtensorMap tq, tk, tv;
   __nv_bfloat16* out;
   long long o_srow, o_sh;
   int M, Nk, H;
-  int MT;
+  int MT;        // 128-row tiles
+  int NP;        // units per head (ceil(MT / NT))
   int causal;
   long long row_off;
-  float cl;  // scale * log2(e)
+  float cl;      // scale * log2(e)
   int pdl;
 };
 
-// 2^x on the FMA / ALU pipes (x <= 0, the softmax exponent): x = j + f with j the
-// nearest integer, f in [-0.5, 0.5]; 2^f by a degree-3 polynomial (relative error
-// 2.1e-4, below half a bf16 ulp of P); 2^j added to the exponent field.  x < -126
-// (masked keys: -inf) gives 0.  Opt-in (AC_FA_POLY=1) for a fixed quarter of the
-// columns, so that the MUFU unit carries three quarters of the exponentials.
-__device__ __forceinline__ float ex2_poly(float x) {
-  const float xc = fmaxf(x, -126.f);
-  const float t = xc + 12582912.f;  // 1.5 * 2^23: round to nearest integer in the low bits
-  const int j = __float_as_int(t) - 0x4B400000;
-  const float f = xc - (t - 12582912.f);
-  float p = fmaf(f, 0.05484806f, 0.24180646f);
-  p = fmaf(f, p, 0.69324815f);
-  p = fmaf(f, p, 0.99998868f);
-  const float r = __int_as_float(__float_as_int(p) + (j << 23));
-  return x < -126.f ? 0.f : r;
+// key blocks of query tile mt (0 for a tile past the rows)
+__device__ __forceinline__ int fa_nkb(const FaArgs& a, int mt) {
+  if (mt >= a.MT) return 0;
+  long long kend = a.Nk;
+  if (a.causal) {
+    const long long e = a.row_off + static_cast<long long>(mt + 1) * FA_BM;
+    if (e < kend) kend = e;
+  }
+  return static_cast<int>((kend + FA_BN - 1) / FA_BN);
 }
 
-template <int BNK, bool POLY>
-__global__ void __launch_bounds__(FA_THREADS, FaCfg<BNK>::MINB) attn_fused_kernel(const __grid_constant__ FaArgs a) {
-  using CF = FaCfg<BNK>;
-  constexpr int FA_BN = CF::BN, HK = CF::HK, OCOL = CF::OCOL, FA_TMEM = CF::TMEM;
-  constexpr int K_BYTES = CF::K_BYTES, V_BYTES = CF::V_BYTES, P_BYTES = CF::P_BYTES;
+// 16 packed 32-bit columns per thread (tcgen05.st 32x32b.x16)
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+// D(tmem) (+)= A(tmem) * B(smem)^T, kind::f16: A = 128 lanes x K/2 packed bf16 pairs
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+template <int NT>
+__global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const __grid_constant__ FaArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sK = sQ + Q_BYTES;
+  uint8_t* sK = sQ + NT * Q_BYTES;
   uint8_t* sV = sK + FA_STG * K_BYTES;
-  uint8_t* sP = sV + FA_STG * V_BYTES;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 2 * P_BYTES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + FA_STG * V_BYTES);
   uint64_t* q_full = bar;
   uint64_t* q_empty = bar + 1;
   uint64_t* kv_full = bar + 2;              // [FA_STG]
   uint64_t* kv_empty = bar + 2 + FA_STG;    // [FA_STG]
-  uint64_t* s_full = bar + 2 + 2 * FA_STG;  // [2]
-  uint64_t* s_free = s_full + 2;            // [2]
-  uint64_t* p_full = s_full + 4;            // [2]
-  uint64_t* pv_done = s_full + 6;           // [2]: PV of block q commits to pv_done[q & 1]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_full + 8);
-  // softmax row halves exchange their block maxima ([block parity][half][row]) and,
-  // at the end, their partial sums ([half][row])
-  float* xmax = reinterpret_cast<float*>(bar + 32);
-  float* xsum = xmax + 2 * 2 * 128;
+  uint64_t* s_full = kv_empty + FA_STG;     // [2] per slot: S written (MMA commit)
+  uint64_t* p_full = s_full + 2;            // [2] per slot: P stored, O rescaled (4 softmax warps)
+  uint64_t* pv_done = p_full + 2;           // [2] per tile: a PV of the tile completed (MMA commit)
+  uint64_t* o_free = pv_done + 2;           // [2] per tile: the epilogue read O (4 softmax warps)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_free + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int total = a.H * a.MT;
+  const int total = a.H * a.NP;
   if (threadIdx.x == 0) {
     ptx::prefetch_tmap(&a.tq);
     ptx::prefetch_tmap(&a.tk);
@@ -121,236 +131,233 @@ __global__ void __launch_bounds__(FA_THREADS, FaCfg<BNK>::MINB) attn_fused_kerne
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&s_full[b], 1);
-      ptx::mbar_init(&s_free[b], 8);
-      ptx::mbar_init(&p_full[b], 8);
+      ptx::mbar_init(&p_full[b], 4);
+      ptx::mbar_init(&pv_done[b], 1);
+      ptx::mbar_init(&o_free[b], 4);
     }
-    ptx::mbar_init(&pv_done[0], 1);
-    ptx::mbar_init(&pv_done[1], 1);
     ptx::fence_barrier_init();
   }
-  if (warp == 1) ptx::tmem_alloc<FA_TMEM>(tmem_holder);
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_holder);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_holder;  // S buffers at columns 0 / 128, O at 256
+  const uint32_t tmem = *tmem_holder;
   if (a.pdl) {  // chunk loop: the prologue overlapped the previous kernel; now wait for its results
     ptx::griddep_wait();
     ptx::griddep_launch();
   }
-
-  // work tile t -> (head, m-tile, key blocks); causal: heaviest (last) m-tiles first
-  auto tile = [&](int t, int& head, int& mt, int& nkb) {
-    const int r = t / a.H;
-    head = t - r * a.H;
-    mt = a.causal ? a.MT - 1 - r : r;
-    long long kend = a.Nk;
-    if (a.causal) {
-      const long long e = a.row_off + static_cast<long long>(mt + 1) * FA_BM;
-      if (e < kend) kend = e;
-    }
-    nkb = static_cast<int>((kend + FA_BN - 1) / FA_BN);
+  // work unit u -> (head, first tile); causal: heaviest (last) units first
+  auto unit = [&](int u, int& head, int& mt0) {
+    const int r = u / a.H;
+    head = u - r * a.H;
+    mt0 = (a.causal ? a.NP - 1 - r : r) * NT;
   };
 
-  if (warp == 0) {
-    if (lane == 0) {
+  if (warp < 4) {
+    // NT = 2: 384 threads x 168 registers at launch; the softmax warpgroups take the
+    // producer / MMA warpgroup's spare registers (128 x 112 = 256 x 56)
+    if constexpr (NT == 2) ptx::setmaxnreg_dec<56>();
+    if (warp == 0 && lane == 0) {
       int st = 0;
       uint32_t ph = 0, qph = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        int head, mt, nkb;
-        tile(t, head, mt, nkb);
+      for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        int head, mt0;
+        unit(u, head, mt0);
+        int nkb = 0, nq = 0;
+        for (int t = 0; t < NT; ++t) {
+          const int k = fa_nkb(a, mt0 + t);
+          nkb = k > nkb ? k : nkb;
+          nq += k > 0;
+        }
         ptx::mbar_wait(q_empty, qph ^ 1);
         qph ^= 1;
-        ptx::mbar_expect_tx(q_full, Q_BYTES);
-        ptx::tma_load_4d(sQ, &a.tq, q_full, 0, mt * FA_BM, head, 0);
+        ptx::mbar_expect_tx(q_full, nq * Q_BYTES);
+        for (int t = 0; t < nq; ++t) ptx::tma_load_4d(sQ + t * Q_BYTES, &a.tq, q_full, 0, (mt0 + t) * FA_BM, head, 0);
         for (int j = 0; j < nkb; ++j) {
           ptx::mbar_wait(&kv_empty[st], ph ^ 1);
           ptx::mbar_expect_tx(&kv_full[st], K_BYTES + V_BYTES);
           ptx::tma_load_4d(sK + st * K_BYTES, &a.tk, &kv_full[st], 0, j * FA_BN, head, 0);
-          for (int vb = 0; vb < FA_BN / 64; ++vb)
-            ptx::tma_load_4d(sV + st * V_BYTES + vb * 8192, &a.tv, &kv_full[st], j * FA_BN + vb * 64, 0, head, 0);
+          ptx::tma_load_4d(sV + st * V_BYTES, &a.tv, &kv_full[st], j * FA_BN, 0, head, 0);
+          ptx::tma_load_4d(sV + st * V_BYTES + 8192, &a.tv, &kv_full[st], j * FA_BN + 64, 0, head, 0);
           if (++st == FA_STG) { st = 0; ph ^= 1; }
         }
       }
-    }
-  } else if (warp == 1) {
-    constexpr uint32_t IDS = ptx::idesc_bf16(FA_BM, FA_BN);
-    constexpr uint32_t IDO = ptx::idesc_bf16(FA_BM, FA_DH);
-    int st = 0;
-    uint32_t ph = 0, qph = 0;
-    int sidx = 0;  // S blocks issued by this CTA
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      int head, mt, nkb;
-      tile(t, head, mt, nkb);
-      ptx::mbar_wait(q_full, qph);
-      qph ^= 1;
-      ptx::tc_fence_after();
-      int pst = st;          // stage of the pending PV
-      int pidx = sidx;       // block index of the pending PV
-      for (int j = 0; j <= nkb; ++j) {
-        if (j < nkb) {
-          const int b = sidx & 1;
+    } else if (warp == 1) {
+      constexpr uint32_t IDS = ptx::idesc_bf16(FA_BM, FA_BN);
+      constexpr uint32_t IDO = ptx::idesc_bf16(FA_BM, FA_DH);
+      // pending PV per slot (S issued, PV not yet): tile, block, K/V stage, releases the stage
+      int pv_t[2] = {-1, -1}, pv_j[2] = {0, 0}, pv_st[2] = {0, 0}, pv_rel[2] = {0, 0};
+      uint32_t p_use[2] = {0, 0};        // P arrivals consumed per slot
+      uint32_t o_units[2] = {0, 0};      // units of tile t whose first PV was issued
+      int st = 0, gjob = 0;
+      uint32_t ph = 0, qph = 0;
+      auto flush = [&](int x) {          // issue the pending PV of slot x
+        const int t = pv_t[x];
+        if (t < 0) return;
+        ptx::mbar_wait(&p_full[x], p_use[x] & 1);
+        ++p_use[x];
+        if (pv_j[x] == 0 && o_units[t]++ > 0) ptx::mbar_wait(&o_free[t], (o_units[t] - 2) & 1);
+        ptx::tc_fence_after();
+        if (lane == 0) {
+          const uint32_t vb = ptx::smem_u32(sV + pv_st[x] * V_BYTES);
+#pragma unroll
+          for (int k = 0; k < FA_BN / 16; ++k)
+            mma_bf16_ts(tmem + O_COL + t * 64, tmem + x * 128 + k * 8,
+                        ptx::sdesc_sw128(vb + (k >> 2) * 8192 + (k & 3) * 32), IDO, (pv_j[x] > 0 || k) ? 1u : 0u);
+          ptx::mma_commit(&pv_done[t]);
+          if (pv_rel[x]) ptx::mma_commit(&kv_empty[pv_st[x]]);
+        }
+        __syncwarp();
+        pv_t[x] = -1;
+      };
+      for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        int head, mt0;
+        unit(u, head, mt0);
+        int nk[NT], nkb = 0;
+        for (int t = 0; t < NT; ++t) {
+          nk[t] = fa_nkb(a, mt0 + t);
+          nkb = nk[t] > nkb ? nk[t] : nkb;
+        }
+        ptx::mbar_wait(q_full, qph);
+        qph ^= 1;
+        for (int j = 0; j < nkb; ++j) {
           ptx::mbar_wait(&kv_full[st], ph);
-          ptx::mbar_wait(&s_free[b], ((sidx >> 1) & 1) ^ 1);
-          ptx::tc_fence_after();
-          if (lane == 0) {
-            const uint32_t sa = ptx::smem_u32(sQ), sb = ptx::smem_u32(sK + st * K_BYTES);
+          int last_t = 0;
+          for (int t = 0; t < NT; ++t)
+            if (j < nk[t]) last_t = t;
+          for (int t = 0; t < NT; ++t) {
+            if (j >= nk[t]) continue;
+            const int x = NT == 2 ? t : (gjob & 1);
+            flush(x);  // the slot's previous P is consumed before S overwrites it (in-order MMAs)
+            ptx::tc_fence_after();
+            if (lane == 0) {
+              const uint32_t sa = ptx::smem_u32(sQ + t * Q_BYTES), sb = ptx::smem_u32(sK + st * K_BYTES);
 #pragma unroll
-            for (int k = 0; k < FA_DH / 16; ++k)
-              ptx::mma_bf16(tmem + b * FA_BN, ptx::sdesc_sw128(sa + k * 32), ptx::sdesc_sw128(sb + k * 32), IDS,
-                            k ? 1u : 0u);
-            ptx::mma_commit(&s_full[b]);
-            if (j == nkb - 1) ptx::mma_commit(q_empty);  // Q no longer read in this tile
-          }
-          __syncwarp();
-        }
-        if (j >= 1) {
-          // PV of block j - 1 (stage pst, P buffer pidx & 1)
-          const int b = pidx & 1;
-          ptx::mbar_wait(&p_full[b], (pidx >> 1) & 1);
-          ptx::tc_fence_after();
-          if (lane == 0) {
-            const uint32_t pa = ptx::smem_u32(sP + b * P_BYTES), vb = ptx::smem_u32(sV + pst * V_BYTES);
-#pragma unroll
-            for (int k = 0; k < FA_BN / 16; ++k) {
-              const int kb = k >> 2, kk = k & 3;
-              ptx::mma_bf16(tmem + OCOL, ptx::sdesc_sw128(pa + kb * 16384 + kk * 32),
-                            ptx::sdesc_sw128(vb + kb * 8192 + kk * 32), IDO, (j > 1 || k) ? 1u : 0u);
+              for (int k = 0; k < FA_DH / 16; ++k)
+                ptx::mma_bf16(tmem + x * 128, ptx::sdesc_sw128(sa + k * 32), ptx::sdesc_sw128(sb + k * 32), IDS,
+                              k ? 1u : 0u);
+              ptx::mma_commit(&s_full[x]);
+              if (j == nkb - 1 && t == last_t) ptx::mma_commit(q_empty);  // Q no longer read in this unit
             }
-            ptx::mma_commit(&kv_empty[pst]);
-            ptx::mma_commit(&pv_done[pidx & 1]);
+            __syncwarp();
+            pv_t[x] = t;
+            pv_j[x] = j;
+            pv_st[x] = st;
+            pv_rel[x] = t == last_t;
+            ++gjob;
           }
-          __syncwarp();
-          pidx = sidx;
-          pst = st;
-        }
-        if (j < nkb) {
-          if (j == 0) { pidx = sidx; pst = st; }
-          ++sidx;
           if (++st == FA_STG) { st = 0; ph ^= 1; }
         }
       }
+      // drain: oldest pending first (NT = 1: both slots hold the same tile's PVs)
+      if (NT == 1 && pv_t[gjob & 1] >= 0) flush(gjob & 1);
+      flush(0);
+      flush(1);
     }
   } else {
-    // softmax warps: thread = (query row r of the tile, half of the 128-key block);
-    // warps w and w + 4 share TMEM lane quarter w % 4 and split each row's keys
-    const int sw = warp - 2;
+    if constexpr (NT == 2) ptx::setmaxnreg_inc<224>();
+    const int t = (warp - 4) >> 2;          // this warpgroup's tile of the unit
     const int quarter = warp & 3;
-    const int hf = sw >> 2;  // keys hf*64 .. hf*64+63 of every block; O columns hf*32..
     const int r = quarter * 32 + lane;
     const uint32_t lrow = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t nbar = 1 + quarter;  // named barrier of the two warps of a quarter
-    int sidx = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      int head, mt, nkb;
-      tile(t, head, mt, nkb);
+    uint32_t s_use[2] = {0, 0};
+    uint32_t pv_cnt = 0;                    // PVs of this tile awaited so far
+    int gjob = 0;                           // (NT = 1) jobs of this CTA: slot parity
+    for (int u = blockIdx.x; u < total; u += gridDim.x) {
+      int head, mt0;
+      unit(u, head, mt0);
+      const int mt = mt0 + t;
+      const int nkb = fa_nkb(a, mt);
+      if (nkb == 0) continue;
       const long long qg = a.row_off + static_cast<long long>(mt) * FA_BM + r;  // global query row
-      float m = -CUDART_INF_F, l = 0.f;  // l: this half's partial sum (same rescales as the other)
+      float m = -CUDART_INF_F, l = 0.f;
       for (int j = 0; j < nkb; ++j) {
-        const int b = sidx & 1;
-        ptx::mbar_wait(&s_full[b], (sidx >> 1) & 1);
+        const int x = NT == 2 ? t : (gjob & 1);
+        ptx::mbar_wait(&s_full[x], s_use[x] & 1);
+        ++s_use[x];
         ptx::tc_fence_after();
-        uint32_t s[HK];
+        uint32_t sv[128];
 #pragma unroll
-        for (int c = 0; c < HK / 32; ++c)
-          ptx::tmem_ld32(tmem + lrow + b * FA_BN + hf * HK + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]));
+        for (int c = 0; c < 4; ++c)
+          ptx::tmem_ld32(tmem + lrow + x * 128 + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
         ptx::tmem_ld_wait();
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&s_free[b]);
-        // mask: causal keys past the row, keys past Nk
-        const long long k0 = static_cast<long long>(j) * FA_BN + hf * HK;
-        long long lim = a.Nk - 1 - k0;  // last valid column of this half-block
+        // mask: keys past the row (causal) or past Nk
+        const long long k0 = static_cast<long long>(j) * FA_BN;
+        long long lim = a.Nk - 1 - k0;
         if (a.causal && qg - k0 < lim) lim = qg - k0;
-        float mb = -CUDART_INF_F;
-        if (lim >= HK - 1) {
+        if (lim < FA_BN - 1) {
 #pragma unroll
-          for (int c = 0; c < HK; ++c) mb = fmaxf(mb, __uint_as_float(s[c]));
-        } else {
+          for (int c = 0; c < FA_BN; ++c)
+            if (c > lim) sv[c] = __float_as_uint(-CUDART_INF_F);
+        }
+        float m8[8];
 #pragma unroll
-          for (int c = 0; c < HK; ++c) {
-            if (c > lim) s[c] = __float_as_uint(-CUDART_INF_F);
-            mb = fmaxf(mb, __uint_as_float(s[c]));
+        for (int c = 0; c < 8; ++c) m8[c] = __uint_as_float(sv[c]);
+#pragma unroll
+        for (int c = 8; c < FA_BN; ++c) m8[c & 7] = fmaxf(m8[c & 7], __uint_as_float(sv[c]));
+        const float mb = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        const float mx = mb * a.cl;
+        const float m_new = (m == -CUDART_INF_F || mx > m + FA_LAZY) ? fmaxf(m, mx) : m;
+        const float mref = m_new == -CUDART_INF_F ? 0.f : m_new;
+        const float alpha = m == -CUDART_INF_F ? 0.f : (m_new == m ? 1.f : ptx::ex2(m - mref));
+        float l4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {   // 32 keys -> 16 packed columns of P per pass
+          uint32_t pk[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            const float e0 = ptx::ex2(fmaf(__uint_as_float(sv[h * 32 + 2 * c]), a.cl, -mref));
+            const float e1 = ptx::ex2(fmaf(__uint_as_float(sv[h * 32 + 2 * c + 1]), a.cl, -mref));
+            l4[c & 3] += e0 + e1;
+            __nv_bfloat162 hh = __floats2bfloat162_rn(e0, e1);
+            pk[c] = *reinterpret_cast<uint32_t*>(&hh);
+          }
+          tmem_st16(tmem + lrow + x * 128 + h * 16, pk);
+        }
+        l = l * alpha + ((l4[0] + l4[1]) + (l4[2] + l4[3]));
+        m = m_new;
+        if (j >= 1) {
+          // PV_{j-1} of this tile complete (NT = 2: it preceded this S on the tensor core)
+          ptx::mbar_wait(&pv_done[t], pv_cnt & 1);
+          ++pv_cnt;
+          if (__any_sync(0xffffffffu, alpha != 1.f)) {
+            ptx::tc_fence_after();
+            uint32_t o[32];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              ptx::tmem_ld32(tmem + lrow + O_COL + t * 64 + hh * 32, o);
+              ptx::tmem_ld_wait();
+#pragma unroll
+              for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
+              ptx::tmem_st32(tmem + lrow + O_COL + t * 64 + hh * 32, o);
+            }
           }
         }
-        // row max over both halves (slots double-buffered by block parity)
-        xmax[((j & 1) * 2 + hf) * 128 + r] = mb;
-        asm volatile("bar.sync %0, 64;" ::"r"(nbar) : "memory");
-        mb = fmaxf(mb, xmax[((j & 1) * 2 + (hf ^ 1)) * 128 + r]);
-        const float m_new = fmaxf(m, mb * a.cl);
-        const float mref = m_new == -CUDART_INF_F ? 0.f : m_new;
-        const float alpha = m == -CUDART_INF_F ? 0.f : ptx::ex2(m - mref);
-        float ls = 0.f;
-        uint32_t pk[HK / 2];
-#pragma unroll
-        for (int c = 0; c < HK / 2; ++c) {
-          const float x0 = fmaf(__uint_as_float(s[2 * c]), a.cl, -mref);
-          const float x1 = fmaf(__uint_as_float(s[2 * c + 1]), a.cl, -mref);
-          // (columns 8q+6, 8q+7 of every 8 on the FMA pipe: the choice depends on the
-          // column only, so chunked == unchunked stays bitwise)
-          const bool pc = POLY && (c & 3) == 3;
-          const float e0 = pc ? ex2_poly(x0) : ptx::ex2(x0);
-          const float e1 = pc ? ex2_poly(x1) : ptx::ex2(x1);
-          ls += e0 + e1;
-          __nv_bfloat162 h = __floats2bfloat162_rn(e0, e1);
-          pk[c] = *reinterpret_cast<uint32_t*>(&h);
-        }
-        l = l * alpha + ls;
-        m = m_new;
-        // O needs rescaling only when some row's max moved (alpha != 1; skipping a
-        // multiply by 1.0 is exact): then PV_{j-1} must be complete; otherwise only
-        // PV_{j-2} (the last reader of P buffer b) is awaited, so the exponentials of
-        // block j overlap PV_{j-1}
-        const bool resc = j >= 1 && __any_sync(0xffffffffu, alpha != 1.f);
-        if (resc) {
-          ptx::mbar_wait(&pv_done[(sidx - 1) & 1], ((sidx - 1) >> 1) & 1);
-        } else if (sidx >= 2) {
-          ptx::mbar_wait(&pv_done[sidx & 1], ((sidx - 2) >> 1) & 1);
-        }
-        if (resc) {
-          ptx::tc_fence_after();
-          uint32_t o[32];
-          ptx::tmem_ld32(tmem + lrow + OCOL + hf * 32, o);
-          ptx::tmem_ld_wait();
-#pragma unroll
-          for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
-          ptx::tmem_st32(tmem + lrow + OCOL + hf * 32, o);
-          ptx::tmem_st_wait();
-        }
-        // this half's keys: k-block (hf*HK)/64 of P_j, 16-byte chunks from ((hf*HK)%64)/8
-        uint8_t* pb = sP + b * P_BYTES + ((hf * HK) / 64) * 16384 + r * 128;
-        constexpr int CH0 = 0;
-        const int ch0 = ((hf * HK) % 64) / 8 + CH0;
-#pragma unroll
-        for (int c = 0; c < HK / 8; ++c) {
-          const uint32_t addr = ptx::smem_u32(pb + (((ch0 + c) ^ (r & 7)) * 16));
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[4 * c]), "r"(pk[4 * c + 1]),
-                       "r"(pk[4 * c + 2]), "r"(pk[4 * c + 3])
-                       : "memory");
-        }
-        ptx::fence_proxy_async_smem();  // generic-proxy P writes -> visible to the tensor core
+        ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&p_full[b]);
-        ++sidx;
+        if (lane == 0) ptx::mbar_arrive(&p_full[x]);
+        ++gjob;
       }
-      // epilogue: wait for the last PV; l = sum of both halves; o = O / l
-      xsum[hf * 128 + r] = l;
-      ptx::mbar_wait(&pv_done[(sidx - 1) & 1], ((sidx - 1) >> 1) & 1);
+      // epilogue: the tile's last PV, o = O / l
+      ptx::mbar_wait(&pv_done[t], pv_cnt & 1);
+      ++pv_cnt;
       ptx::tc_fence_after();
-      uint32_t o[32];
-      ptx::tmem_ld32(tmem + lrow + OCOL + hf * 32, o);
+      uint32_t o[64];
+      ptx::tmem_ld32(tmem + lrow + O_COL + t * 64, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
+      ptx::tmem_ld32(tmem + lrow + O_COL + t * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
       ptx::tmem_ld_wait();
       ptx::tc_fence_before();
-      asm volatile("bar.sync %0, 64;" ::"r"(nbar) : "memory");
-      const float lt = l + xsum[(hf ^ 1) * 128 + r];
-      asm volatile("bar.sync %0, 64;" ::"r"(nbar) : "memory");  // xsum reusable by the next tile
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&o_free[t]);
       const int mrow = mt * FA_BM + r;
       if (mrow < a.M) {
-        const float inv = lt > 0.f ? 1.f / lt : 0.f;
+        const float inv = l > 0.f ? 1.f / l : 0.f;
         uint4* dst = reinterpret_cast<uint4*>(a.out + static_cast<long long>(mrow) * a.o_srow +
-                                              static_cast<long long>(head) * a.o_sh + hf * 32);
+                                              static_cast<long long>(head) * a.o_sh);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 8; ++c) {
           uint32_t w[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -367,7 +374,7 @@ __global__ void __launch_bounds__(FA_THREADS, FaCfg<BNK>::MINB) attn_fused_kerne
   __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<FA_TMEM>(tmem);
+    ptx::tmem_dealloc<512>(tmem);
   }
 }
 
@@ -406,21 +413,20 @@ bool map3(CUtensorMap* m, const void* p, long long inner, long long rows, long l
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BNK, bool POLY>
-cudaError_t attn_fused_launch(const AttnFusedProblem& p, cudaStream_t s, FaArgs& a, long long tiles) {
-  using CF = FaCfg<BNK>;
+template <int NT>
+cudaError_t attn_fused_launch(cudaStream_t s, FaArgs& a, long long units) {
+  using CF = FaCfg<NT>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fused_kernel<BNK, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(attn_fused_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (!map3(&a.tk, p.k, FA_DH, p.Nk, p.H, p.k_srow, p.k_sh, BNK)) return cudaErrorInvalidValue;
-  const int grid = static_cast<int>(tiles < CF::MINB * num_sms() ? tiles : CF::MINB * num_sms());
-  if (p.pdl) {
+  const int grid = static_cast<int>(units < num_sms() ? units : num_sms());
+  if (a.pdl) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(FA_THREADS);
+    cfg.blockDim = dim3(CF::THREADS);
     cfg.dynamicSmemBytes = CF::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute la[1];
@@ -428,9 +434,9 @@ cudaError_t attn_fused_launch(const AttnFusedProblem& p, cudaStream_t s, FaArgs&
     la[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = la;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, attn_fused_kernel<BNK, POLY>, a);
+    return cudaLaunchKernelEx(&cfg, attn_fused_kernel<NT>, a);
   }
-  attn_fused_kernel<BNK, POLY><<<grid, FA_THREADS, CF::SMEM, s>>>(a);
+  attn_fused_kernel<NT><<<grid, CF::THREADS, CF::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -443,6 +449,7 @@ cudaError_t attn_fused(const AttnFusedProblem& p, cudaStream_t s) {
   memset(&a, 0, sizeof(a));
   // q [M, H, dh] / k [Nk, H, dh]: inner dh; vt [H, dh, Nk]: inner keys, rows dh
   if (!map3(&a.tq, p.q, FA_DH, p.M, p.H, p.q_srow, p.q_sh, FA_BM) ||
+      !map3(&a.tk, p.k, FA_DH, p.Nk, p.H, p.k_srow, p.k_sh, FA_BN) ||
       !map3(&a.tv, p.vt, p.Nk, FA_DH, p.H, p.v_sdh, p.v_sh, FA_DH))
     return cudaErrorInvalidValue;
   if ((reinterpret_cast<uintptr_t>(p.out) & 15) || p.o_srow % 8 || p.o_sh % 8) return cudaErrorInvalidValue;
@@ -458,14 +465,14 @@ cudaError_t attn_fused(const AttnFusedProblem& p, cudaStream_t s) {
   a.cl = p.scale * 1.4426950408889634f;
   a.pdl = p.pdl;
   const long long tiles = static_cast<long long>(a.H) * a.MT;
-  // two CTAs per SM (64-key blocks) only when the launch can fill them
-  static const int force = getenv("AC_FA_BN") ? atoi(getenv("AC_FA_BN")) : 0;  // experiments
-  const bool dual = force ? force == 64 : tiles >= 2 * num_sms();
-  // AC_FA_POLY=1: a quarter of the exponentials on the FMA pipe (measured slower: the
-  // kernel is not MUFU-bound — unchunked GPT attention 0.98 -> 1.11 ms, chunked equal)
-  static const bool poly = getenv("AC_FA_POLY") && getenv("AC_FA_POLY")[0] == '1';
-  if (poly) return dual ? attn_fused_launch<64, true>(p, s, a, tiles) : attn_fused_launch<128, true>(p, s, a, tiles);
-  return dual ? attn_fused_launch<64, false>(p, s, a, tiles) : attn_fused_launch<128, false>(p, s, a, tiles);
+  // two query tiles per CTA (ping-pong) when the launch still fills every SM with
+  // such pairs; otherwise one tile per CTA (short row chunks)
+  if (tiles >= 2LL * num_sms()) {
+    a.NP = (a.MT + 1) / 2;
+    return attn_fused_launch<2>(s, a, static_cast<long long>(a.H) * a.NP);
+  }
+  a.NP = a.MT;
+  return attn_fused_launch<1>(s, a, tiles);
 }
 
 }  // namespace ac

@@ -388,12 +388,17 @@ View narrow(View v, int d, int64_t off, int64_t len, int esz) {
   return v;
 }
 
-// stride of dims [a, b) collapsed into one index; -1 if not collapsible
+// stride of dims [a, b) collapsed into one index; -1 if not collapsible (dims of
+// extent 1 never address anything, so their strides are ignored: a chunk of length 1)
 int64_t collapse(const View& v, int a, int b) {
   if (a >= b) return 1;
-  for (int i = a; i < b - 1; ++i)
-    if (v.st[i] != v.st[i + 1] * v.sh[i + 1]) return -1;
-  return v.st[b - 1];
+  int last = -1;
+  for (int i = b - 1; i >= a; --i) {
+    if (v.sh[i] == 1) continue;
+    if (last >= 0 && v.st[i] != v.st[last] * v.sh[last]) return -1;
+    last = i;
+  }
+  return last >= 0 ? v.st[last] : v.st[b - 1];  // the combined index steps along the innermost non-unit dim
 }
 int64_t extent(const View& v, int a, int b) {
   int64_t e = 1;
@@ -607,6 +612,33 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         }
       } else if (!swap) {
         const int64_t sa = collapse(a, 0, nrows), sf = collapse(out, 0, nout), so = collapse(out, nout, out.nd);
+        if (sa < 0 && nrows == 2 && sf >= 0 && out.st[nout + 1] == 1) {
+          // two row dims that do not collapse (a chunk of the second): batch over the first,
+          // the output [features, r0, r1] written per batch with the r0 stride
+          p.M = static_cast<int>(O);
+          p.N = static_cast<int>(a.sh[1]);
+          p.B1 = static_cast<int>(a.sh[0]);
+          p.K = static_cast<int>(K);
+          p.A = W;
+          p.B.p = a.p; p.B.srow = a.st[1]; p.B.sb1 = a.st[0]; p.B.use_b1 = 1;
+          ep.out_sm = sf;
+          ep.out_sb1 = out.st[nout];
+          ep.out_sn = 1;
+          ep.bias_along_m = 1;
+          if (resv) {
+            ep.res_sm = collapse(*resv, 0, nout);
+            ep.res_sb1 = resv->st[nout];
+            ep.res_sn = resv->st[nout + 1];
+            if (ep.res_sm < 0) return unsup("residual not collapsible");
+          }
+          if (gatev) {
+            ep.gate_sm = collapse(*gatev, 0, nout);
+            ep.gate_sb1 = gatev->st[nout];
+            ep.gate_sn = gatev->st[nout + 1];
+            if (ep.gate_sm < 0) return unsup("gate not collapsible");
+          }
+          goto launch;
+        }
         if (sa < 0 || sf < 0 || so != 1) return unsup("rows not collapsible");
         p.M = static_cast<int>(O);
         p.N = static_cast<int>(extent(a, 0, nrows));

@@ -564,4 +564,9 @@ def test_evoformer_pair_stack_bf16():
         "autochunk-plan 1\nregion s=tr_ln e=tr_ffn2 n=4 dims=0\n",
         "autochunk-plan 1\nregion s=row_scores e=row_pv n=4 dims=0\nregion s=col_scores e=col_pv n=4 dims=1\n"
         "region s=tr_ln e=tr_ffn2 n=2 dims=1\n",
+        # channel-major projections on chunks of the second row dim (batched over the
+        # first), including chunks of length 1 (the Table 1 ablation's best-effort plans)
+        "autochunk-plan 1\nregion s=mo_proj_bg e=mo_proj_b n=4 dims=2\n",
+        "autochunk-plan 1\nregion s=mo_proj_bg e=mo_proj_b n=64 dims=2\n",
+        "autochunk-plan 1\nregion s=row_scores e=row_scores n=64 dims=0\nregion s=row_softmax e=row_pv n=64 dims=0\n",
     ], seed=9)

@@ -1,7 +1,11 @@
-"""compute-sanitizer memcheck over small runs of every kernel path, with the
-PyTorch caching allocator off so each tensor is its own allocation and any
+"""compute-sanitizer over small runs of every kernel path.  memcheck with the
+PyTorch caching allocator off, so each tensor is its own allocation and any
 read or write past a tensor's end is reported (e.g. aux loads of a ragged last
-column tile).  GPU only."""
+column tile); racecheck (shared-memory hazards between the warp roles) and
+synccheck (barrier misuse) over the kernels with warp-specialised pipelines:
+the f2 chain with the chunk-loop overlap (epochs, dynamic tiles), the paired
+triangle chain, the fused attention, a vectorised-epilogue GEMM, and the
+multi-rank executor on an in-process communicator.  GPU only."""
 import os
 import shutil
 import subprocess
@@ -71,6 +75,61 @@ for env in ({"AC_PV_SPLITK": "1"}, {"AC_OVERLAP_CAUSAL": "0"}):
         del os.environ[k]
 print("SANITIZER-RUN-OK")
 """
+
+
+SCRIPT_SYNC = r"""
+import sys, threading
+sys.path[:0] = [%(root)r, %(root)r + "/tests"]
+import torch
+import gpu_util as gu
+from oracle import workloads
+from paper_2401_10652_b200 import api
+
+for og, txt in [
+    (workloads.block("transformer", 512, 256, 4, 512, True, "bf16", name="g"),
+     "autochunk-plan 1\nregion s=scores e=pv n=4 dims=0\n"),
+    (workloads.block("attn_only", 384, 256, 4, 0, False, "bf16", name="u"),
+     "autochunk-plan 1\nregion s=scores e=pv n=3 dims=0\n"),
+    (workloads.tri_attn_pair(48, 128, 4, 32, "bf16", name="af"),
+     "autochunk-plan 1\nregion s=row_scores e=row_pv n=2 dims=1\n"),
+    (workloads.block("transformer_fa", 256, 256, 4, 512, True, "bf16", name="fa"),
+     "autochunk-plan 1\nregion s=attn e=ffn2 n=2 dims=0\n"),
+]:
+    cg = gu.c_graph(og)
+    vals, dev = gu.make_values(og, 0)
+    gu.run(cg, api.plan_parse(cg, txt), og, dev)
+    torch.cuda.synchronize()
+# two in-process ranks (threads) through the multi-rank executor
+og = workloads.block("transformer", 512, 256, 4, 512, True, "bf16", name="mr")
+cg = gu.c_graph(og)
+_, dev = gu.make_values(og, 0)
+plan = api.plan_parse(cg, "autochunk-plan 1\nregion s=scores e=pv n=4 dims=0\n")
+comms = api.Comm.local(2)
+ins = {t: dev[t] for t in og.inputs + og.weights}
+exs, outs = [], []
+for r in range(2):
+    ws = torch.empty(plan.workspace_bytes(r, 2), dtype=torch.uint8, device="cuda")
+    exs.append(api.Exec(plan, ws, comms[r]))
+    outs.append({o: torch.empty(og.tensors[o].shape, dtype=torch.bfloat16, device="cuda") for o in og.outputs})
+st = [torch.cuda.Stream() for _ in range(2)]
+th = [threading.Thread(target=lambda r=r: exs[r].run(ins, outs[r], st[r])) for r in range(2)]
+[t.start() for t in th]
+[t.join() for t in th]
+torch.cuda.synchronize()
+print("SANITIZER-RUN-OK")
+"""
+
+
+@pytest.mark.parametrize("tool", ["racecheck", "synccheck"])
+def test_racecheck_synccheck_clean(tmp_path, tool):
+    san = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(san):
+        pytest.skip("compute-sanitizer not found")
+    script = tmp_path / "run.py"
+    script.write_text(SCRIPT_SYNC % {"root": ROOT})
+    r = subprocess.run([san, "--tool", tool, "--error-exitcode", "3", "--print-limit", "10",
+                        sys.executable, str(script)], capture_output=True, text=True, timeout=1500)
+    assert r.returncode == 0 and "SANITIZER-RUN-OK" in r.stdout, (r.stdout[-3000:], r.stderr[-3000:])
 
 
 def test_memcheck_clean(tmp_path):
