@@ -7,10 +7,10 @@
 //   warp 0       : TMA producer - the unit's Q tiles once, K / V^T blocks of 128 keys
 //                  through a 3-stage ring shared by the NT tiles (128B swizzle)
 //   warp 1       : TMEM allocator + MMA issuer.  Jobs (tile t, key block j) in the
-//                  order j-major, t-minor; S = Q_t K_j^T (M=128, N=128, K=64) into one
-//                  of two TMEM slots (NT = 2: the tile's own slot, the two tiles' softmax
-//                  and MMA phases ping-pong; NT = 1: alternating slots, so S_{j+1} runs
-//                  during softmax_j); O_t += P V_j (M=128, N=64, K=128) with P read from
+//                  order j-major, t-minor; job k: S = Q_t K_j^T (M=128, N=128, K=64) into
+//                  TMEM slot k % 3, so the tensor core runs up to two jobs ahead of the
+//                  softmax warpgroups (NT = 2: the two tiles' softmax phases overlap each
+//                  other and the MMAs); O_t += P V_j (M=128, N=64, K=128) with P read from
 //                  TMEM (the slot's first 64 columns, bf16 pairs) - issued right before
 //                  the slot's next S, so the tensor core's in-order execution keeps the
 //                  slot's WAR order
@@ -46,7 +46,8 @@ constexpr float FA_LAZY = 8.f;   // reference-update threshold of the online sof
 constexpr int Q_BYTES = FA_BM * FA_DH * 2;   // 16 KB
 constexpr int K_BYTES = FA_BN * FA_DH * 2;   // 16 KB
 constexpr int V_BYTES = FA_DH * FA_BN * 2;   // 16 KB: two 64-key boxes of 8 KB
-constexpr int O_COL = 256;                   // TMEM: slots at columns 0 / 128, O_t at 256 + 64 t
+constexpr int FA_SLOTS = 3;                  // TMEM S slots (job k -> slot k % 3)
+constexpr int O_COL = 384;                   // TMEM: slots at columns 0 / 128 / 256, O_t at 384 + 64 t
 
 template <int NT>
 struct FaCfg {
@@ -111,9 +112,9 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
   uint64_t* q_empty = bar + 1;
   uint64_t* kv_full = bar + 2;              // [FA_STG]
   uint64_t* kv_empty = bar + 2 + FA_STG;    // [FA_STG]
-  uint64_t* s_full = kv_empty + FA_STG;     // [2] per slot: S written (MMA commit)
-  uint64_t* p_full = s_full + 2;            // [2] per slot: P stored, O rescaled (4 softmax warps)
-  uint64_t* pv_done = p_full + 2;           // [2] per tile: a PV of the tile completed (MMA commit)
+  uint64_t* s_full = kv_empty + FA_STG;     // [3] per slot: S written (MMA commit)
+  uint64_t* p_full = s_full + FA_SLOTS;     // [3] per slot: P stored, O rescaled (4 softmax warps)
+  uint64_t* pv_done = p_full + FA_SLOTS;    // [2] per tile: a PV of the tile completed (MMA commit)
   uint64_t* o_free = pv_done + 2;           // [2] per tile: the epilogue read O (4 softmax warps)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_free + 2);
 
@@ -129,9 +130,11 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
       ptx::mbar_init(&kv_full[s], 1);
       ptx::mbar_init(&kv_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < FA_SLOTS; ++b) {
       ptx::mbar_init(&s_full[b], 1);
       ptx::mbar_init(&p_full[b], 4);
+    }
+    for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&pv_done[b], 1);
       ptx::mbar_init(&o_free[b], 4);
     }
@@ -185,17 +188,20 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
     } else if (warp == 1) {
       constexpr uint32_t IDS = ptx::idesc_bf16(FA_BM, FA_BN);
       constexpr uint32_t IDO = ptx::idesc_bf16(FA_BM, FA_DH);
-      // pending PV per slot (S issued, PV not yet): tile, block, K/V stage, releases the stage
-      int pv_t[2] = {-1, -1}, pv_j[2] = {0, 0}, pv_st[2] = {0, 0}, pv_rel[2] = {0, 0};
-      uint32_t p_use[2] = {0, 0};        // P arrivals consumed per slot
+      // job k (this CTA's k-th (tile, block)) uses S slot k % 3; its PV is issued right
+      // before S of job k + 3 overwrites the slot (in-order MMAs keep the WAR order), so
+      // the tensor core runs up to two jobs ahead of the softmax warpgroups.
+      // pending PV per slot: tile (-1 none), block, K/V stage, releases the stage, job
+      int pv_t[FA_SLOTS], pv_j[FA_SLOTS], pv_st[FA_SLOTS], pv_rel[FA_SLOTS], pv_k[FA_SLOTS];
+#pragma unroll
+      for (int x = 0; x < FA_SLOTS; ++x) pv_t[x] = -1;
       uint32_t o_units[2] = {0, 0};      // units of tile t whose first PV was issued
       int st = 0, gjob = 0;
       uint32_t ph = 0, qph = 0;
       auto flush = [&](int x) {          // issue the pending PV of slot x
         const int t = pv_t[x];
         if (t < 0) return;
-        ptx::mbar_wait(&p_full[x], p_use[x] & 1);
-        ++p_use[x];
+        ptx::mbar_wait(&p_full[x], (pv_k[x] / FA_SLOTS) & 1);
         if (pv_j[x] == 0 && o_units[t]++ > 0) ptx::mbar_wait(&o_free[t], (o_units[t] - 2) & 1);
         ptx::tc_fence_after();
         if (lane == 0) {
@@ -221,14 +227,20 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
         ptx::mbar_wait(q_full, qph);
         qph ^= 1;
         for (int j = 0; j < nkb; ++j) {
-          ptx::mbar_wait(&kv_full[st], ph);
           int last_t = 0;
           for (int t = 0; t < NT; ++t)
             if (j < nk[t]) last_t = t;
+          bool loaded = false;
           for (int t = 0; t < NT; ++t) {
             if (j >= nk[t]) continue;
-            const int x = NT == 2 ? t : (gjob & 1);
-            flush(x);  // the slot's previous P is consumed before S overwrites it (in-order MMAs)
+            const int x = gjob % FA_SLOTS;
+            // the slot's previous P is consumed before S overwrites it; flushed before
+            // waiting for block j (that PV may be what frees block j's ring stage)
+            flush(x);
+            if (!loaded) {
+              ptx::mbar_wait(&kv_full[st], ph);
+              loaded = true;
+            }
             ptx::tc_fence_after();
             if (lane == 0) {
               const uint32_t sa = ptx::smem_u32(sQ + t * Q_BYTES), sb = ptx::smem_u32(sK + st * K_BYTES);
@@ -244,15 +256,14 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
             pv_j[x] = j;
             pv_st[x] = st;
             pv_rel[x] = t == last_t;
+            pv_k[x] = gjob;
             ++gjob;
           }
           if (++st == FA_STG) { st = 0; ph ^= 1; }
         }
       }
-      // drain: oldest pending first (NT = 1: both slots hold the same tile's PVs)
-      if (NT == 1 && pv_t[gjob & 1] >= 0) flush(gjob & 1);
-      flush(0);
-      flush(1);
+      // drain, oldest job first
+      for (int d = 0; d < FA_SLOTS; ++d) flush((gjob + d) % FA_SLOTS);
     }
   } else {
     if constexpr (NT == 2) ptx::setmaxnreg_inc<224>();
@@ -260,21 +271,27 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;
     const uint32_t lrow = static_cast<uint32_t>(quarter * 32) << 16;
-    uint32_t s_use[2] = {0, 0};
     uint32_t pv_cnt = 0;                    // PVs of this tile awaited so far
-    int gjob = 0;                           // (NT = 1) jobs of this CTA: slot parity
+    int gjob = 0;                           // jobs of this CTA so far (all tiles): slot = job % 3
     for (int u = blockIdx.x; u < total; u += gridDim.x) {
       int head, mt0;
       unit(u, head, mt0);
+      int nk[NT];
+      for (int tt = 0; tt < NT; ++tt) nk[tt] = fa_nkb(a, mt0 + tt);
       const int mt = mt0 + t;
-      const int nkb = fa_nkb(a, mt);
-      if (nkb == 0) continue;
+      const int nkb = nk[t];
+      if (nkb == 0) {
+        for (int tt = 0; tt < NT; ++tt) gjob += nk[tt];
+        continue;
+      }
       const long long qg = a.row_off + static_cast<long long>(mt) * FA_BM + r;  // global query row
       float m = -CUDART_INF_F, l = 0.f;
       for (int j = 0; j < nkb; ++j) {
-        const int x = NT == 2 ? t : (gjob & 1);
-        ptx::mbar_wait(&s_full[x], s_use[x] & 1);
-        ++s_use[x];
+        for (int tt = 0; tt < t; ++tt) gjob += j < nk[tt];       // the other tiles' jobs of block j first
+        const int job = gjob++;
+        for (int tt = t + 1; tt < NT; ++tt) gjob += j < nk[tt];
+        const int x = job % FA_SLOTS;
+        ptx::mbar_wait(&s_full[x], (job / FA_SLOTS) & 1);
         ptx::tc_fence_after();
         uint32_t sv[128];
 #pragma unroll
@@ -338,8 +355,12 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&p_full[x]);
-        ++gjob;
       }
+      // the other tiles' jobs past this tile's last block
+      int nmax = 0;
+      for (int tt = 0; tt < NT; ++tt) nmax = nk[tt] > nmax ? nk[tt] : nmax;
+      for (int j = nkb; j < nmax; ++j)
+        for (int tt = 0; tt < NT; ++tt) gjob += j < nk[tt];
       // epilogue: the tile's last PV, o = O / l
       ptx::mbar_wait(&pv_done[t], pv_cnt & 1);
       ++pv_cnt;

@@ -392,13 +392,14 @@ View narrow(View v, int d, int64_t off, int64_t len, int esz) {
 // extent 1 never address anything, so their strides are ignored: a chunk of length 1)
 int64_t collapse(const View& v, int a, int b) {
   if (a >= b) return 1;
-  int last = -1;
+  int last = -1, inner = -1;
   for (int i = b - 1; i >= a; --i) {
     if (v.sh[i] == 1) continue;
     if (last >= 0 && v.st[i] != v.st[last] * v.sh[last]) return -1;
+    if (inner < 0) inner = i;
     last = i;
   }
-  return last >= 0 ? v.st[last] : v.st[b - 1];  // the combined index steps along the innermost non-unit dim
+  return inner >= 0 ? v.st[inner] : v.st[b - 1];  // the combined index steps along the innermost non-unit dim
 }
 int64_t extent(const View& v, int a, int b) {
   int64_t e = 1;
@@ -639,7 +640,7 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
           }
           goto launch;
         }
-        if (sa < 0 || sf < 0 || so != 1) return unsup("rows not collapsible");
+        if (sa < 0 || sf < 0 || so < 0) return unsup("rows not collapsible");
         p.M = static_cast<int>(O);
         p.N = static_cast<int>(extent(a, 0, nrows));
         p.K = static_cast<int>(K);
@@ -647,7 +648,7 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         p.B.p = a.p;
         p.B.srow = sa;
         ep.out_sm = sf;
-        ep.out_sn = 1;
+        ep.out_sn = so;  // (1 unless the rows are a strided slice, e.g. a chunk of length 1)
         ep.bias_along_m = 1;
         if (resv) {
           ep.res_sm = collapse(*resv, 0, nout);

@@ -795,6 +795,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
           for (int hh = 0; hh < BN / 32; ++hh)
             ptx::tmem_st32(tstg + (static_cast<uint32_t>(quarter * 32) << 16) + hh * 32,
                            *reinterpret_cast<const uint32_t(*)[32]>(&accv[hh * 32]));
+          // racecheck: mbarrier handoff (written after the sempty wait, read after sfull)
           sml[r] = make_float2(Mr, Lr);
           ptx::tmem_st_wait();
           ptx::tc_fence_before();
@@ -819,6 +820,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
           for (int hh = 0; hh < BN / 32; ++hh)
             ptx::tmem_ld32(tstg + (static_cast<uint32_t>(quarter * 32) << 16) + hh * 32,
                            *reinterpret_cast<uint32_t(*)[32]>(&accv[hh * 32]));
+          // racecheck: mbarrier handoff (read after the sfull wait, freed by the sempty arrive)
           const float2 ml = sml[r];
           ptx::tmem_ld_wait();
 #pragma unroll
