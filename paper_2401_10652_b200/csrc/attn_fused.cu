@@ -14,7 +14,7 @@
 //                  TMEM (the slot's first 64 columns, bf16 pairs) - issued right before
 //                  the slot's next S, so the tensor core's in-order execution keeps the
 //                  slot's WAR order
-//   warps 2, 3   : idle (NT = 2: registers handed to the softmax warpgroups)
+//   warp 3       : idle (NT = 2: registers handed to the softmax warpgroups)
 //   warpgroup 1+t: softmax of tile t, thread = query row over all 128 keys of a block:
 //                  max, lazy online reference (moves only when the block max exceeds
 //                  it by FA_LAZY log2 units, so most blocks need no O rescale),
@@ -41,7 +41,8 @@ namespace {
 constexpr int FA_BM = 128;       // query rows per tile
 constexpr int FA_BN = 128;       // keys per block
 constexpr int FA_DH = 64;        // head dim (one 128-byte swizzle row)
-constexpr int FA_STG = 3;        // K/V ring depth
+constexpr int FA_STG = 4;        // K ring and V ring depth (separate rings: K is released by the
+                                 // block's last S, V by its last PV, which runs three jobs later)
 constexpr float FA_LAZY = 8.f;   // reference-update threshold of the online softmax (log2 units)
 constexpr int Q_BYTES = FA_BM * FA_DH * 2;   // 16 KB
 constexpr int K_BYTES = FA_BN * FA_DH * 2;   // 16 KB
@@ -110,9 +111,11 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
   uint64_t* bar = reinterpret_cast<uint64_t*>(sV + FA_STG * V_BYTES);
   uint64_t* q_full = bar;
   uint64_t* q_empty = bar + 1;
-  uint64_t* kv_full = bar + 2;              // [FA_STG]
-  uint64_t* kv_empty = bar + 2 + FA_STG;    // [FA_STG]
-  uint64_t* s_full = kv_empty + FA_STG;     // [3] per slot: S written (MMA commit)
+  uint64_t* k_full = bar + 2;               // [FA_STG]
+  uint64_t* k_empty = k_full + FA_STG;      // [FA_STG]
+  uint64_t* v_full = k_empty + FA_STG;      // [FA_STG]
+  uint64_t* v_empty = v_full + FA_STG;      // [FA_STG]
+  uint64_t* s_full = v_empty + FA_STG;      // [3] per slot: S written (MMA commit)
   uint64_t* p_full = s_full + FA_SLOTS;     // [3] per slot: P stored, O rescaled (4 softmax warps)
   uint64_t* pv_done = p_full + FA_SLOTS;    // [2] per tile: a PV of the tile completed (MMA commit)
   uint64_t* o_free = pv_done + 2;           // [2] per tile: the epilogue read O (4 softmax warps)
@@ -127,8 +130,10 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
     ptx::mbar_init(q_full, 1);
     ptx::mbar_init(q_empty, 1);
     for (int s = 0; s < FA_STG; ++s) {
-      ptx::mbar_init(&kv_full[s], 1);
-      ptx::mbar_init(&kv_empty[s], 1);
+      ptx::mbar_init(&k_full[s], 1);
+      ptx::mbar_init(&k_empty[s], 1);
+      ptx::mbar_init(&v_full[s], 1);
+      ptx::mbar_init(&v_empty[s], 1);
     }
     for (int b = 0; b < FA_SLOTS; ++b) {
       ptx::mbar_init(&s_full[b], 1);
@@ -158,8 +163,8 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
 
   if (warp < 4) {
     // NT = 2: 384 threads x 168 registers at launch; the softmax warpgroups take the
-    // producer / MMA warpgroup's spare registers (128 x 112 = 256 x 56)
-    if constexpr (NT == 2) ptx::setmaxnreg_dec<56>();
+    // producer / MMA warpgroup's spare registers (168 -> 96 there, 168 -> 200 here)
+    if constexpr (NT == 2) ptx::setmaxnreg_dec<96>();
     if (warp == 0 && lane == 0) {
       int st = 0;
       uint32_t ph = 0, qph = 0;
@@ -177,11 +182,28 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
         ptx::mbar_expect_tx(q_full, nq * Q_BYTES);
         for (int t = 0; t < nq; ++t) ptx::tma_load_4d(sQ + t * Q_BYTES, &a.tq, q_full, 0, (mt0 + t) * FA_BM, head, 0);
         for (int j = 0; j < nkb; ++j) {
-          ptx::mbar_wait(&kv_empty[st], ph ^ 1);
-          ptx::mbar_expect_tx(&kv_full[st], K_BYTES + V_BYTES);
-          ptx::tma_load_4d(sK + st * K_BYTES, &a.tk, &kv_full[st], 0, j * FA_BN, head, 0);
-          ptx::tma_load_4d(sV + st * V_BYTES, &a.tv, &kv_full[st], j * FA_BN, 0, head, 0);
-          ptx::tma_load_4d(sV + st * V_BYTES + 8192, &a.tv, &kv_full[st], j * FA_BN + 64, 0, head, 0);
+          ptx::mbar_wait(&k_empty[st], ph ^ 1);
+          ptx::mbar_expect_tx(&k_full[st], K_BYTES);
+          ptx::tma_load_4d(sK + st * K_BYTES, &a.tk, &k_full[st], 0, j * FA_BN, head, 0);
+          if (++st == FA_STG) { st = 0; ph ^= 1; }
+        }
+      }
+    } else if (warp == 2 && lane == 0) {   // V^T blocks, on their own ring
+      int st = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        int head, mt0;
+        unit(u, head, mt0);
+        int nkb = 0;
+        for (int t = 0; t < NT; ++t) {
+          const int k = fa_nkb(a, mt0 + t);
+          nkb = k > nkb ? k : nkb;
+        }
+        for (int j = 0; j < nkb; ++j) {
+          ptx::mbar_wait(&v_empty[st], ph ^ 1);
+          ptx::mbar_expect_tx(&v_full[st], V_BYTES);
+          ptx::tma_load_4d(sV + st * V_BYTES, &a.tv, &v_full[st], j * FA_BN, 0, head, 0);
+          ptx::tma_load_4d(sV + st * V_BYTES + 8192, &a.tv, &v_full[st], j * FA_BN + 64, 0, head, 0);
           if (++st == FA_STG) { st = 0; ph ^= 1; }
         }
       }
@@ -190,83 +212,92 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
       constexpr uint32_t IDO = ptx::idesc_bf16(FA_BM, FA_DH);
       // job k (this CTA's k-th (tile, block)) uses S slot k % 3; its PV is issued right
       // before S of job k + 3 overwrites the slot (in-order MMAs keep the WAR order), so
-      // the tensor core runs up to two jobs ahead of the softmax warpgroups.
-      // pending PV per slot: tile (-1 none), block, K/V stage, releases the stage, job
-      int pv_t[FA_SLOTS], pv_j[FA_SLOTS], pv_st[FA_SLOTS], pv_rel[FA_SLOTS], pv_k[FA_SLOTS];
-#pragma unroll
-      for (int x = 0; x < FA_SLOTS; ++x) pv_t[x] = -1;
-      uint32_t o_units[2] = {0, 0};      // units of tile t whose first PV was issued
-      int st = 0, gjob = 0;
-      uint32_t ph = 0, qph = 0;
-      auto flush = [&](int x) {          // issue the pending PV of slot x
-        const int t = pv_t[x];
-        if (t < 0) return;
-        ptx::mbar_wait(&p_full[x], (pv_k[x] / FA_SLOTS) & 1);
-        if (pv_j[x] == 0 && o_units[t]++ > 0) ptx::mbar_wait(&o_free[t], (o_units[t] - 2) & 1);
+      // the tensor core runs up to two jobs ahead of the softmax warpgroups.  The three
+      // pending PVs (jobs k-3, k-2, k-1) are a register FIFO: no dynamically indexed
+      // arrays (local memory) on this warp's critical path.
+      struct Pend {
+        int t = -1, j = 0, st = 0, rel = 0, x = 0;
+        uint32_t ph = 0, pph = 0;  // V stage phase, P phase of the slot
+      };
+      Pend q0, q1, q2;                    // oldest .. newest
+      uint32_t o_units0 = 0, o_units1 = 0;  // units of tile 0 / 1 whose first PV was issued
+      int st = 0, slot = 0;
+      uint32_t ph = 0, qph = 0, pcnt = 0;  // pcnt: jobs issued (slot use = pcnt / 3)
+      auto flush = [&](const Pend& e) {    // issue a pending PV
+        if (e.t < 0) return;
+        ptx::mbar_wait(&p_full[e.x], e.pph);
+        if (e.j == 0) {
+          uint32_t& ou = e.t ? o_units1 : o_units0;
+          if (ou++ > 0) ptx::mbar_wait(&o_free[e.t], (ou - 2) & 1);
+        }
+        ptx::mbar_wait(&v_full[e.st], e.ph);
         ptx::tc_fence_after();
         if (lane == 0) {
-          const uint32_t vb = ptx::smem_u32(sV + pv_st[x] * V_BYTES);
+          const uint32_t vb = ptx::smem_u32(sV + e.st * V_BYTES);
+          const uint32_t ot = tmem + O_COL + e.t * 64, pt = tmem + e.x * 128;
 #pragma unroll
           for (int k = 0; k < FA_BN / 16; ++k)
-            mma_bf16_ts(tmem + O_COL + t * 64, tmem + x * 128 + k * 8,
-                        ptx::sdesc_sw128(vb + (k >> 2) * 8192 + (k & 3) * 32), IDO, (pv_j[x] > 0 || k) ? 1u : 0u);
-          ptx::mma_commit(&pv_done[t]);
-          if (pv_rel[x]) ptx::mma_commit(&kv_empty[pv_st[x]]);
+            mma_bf16_ts(ot, pt + k * 8, ptx::sdesc_sw128(vb + (k >> 2) * 8192 + (k & 3) * 32), IDO,
+                        (e.j > 0 || k) ? 1u : 0u);
+          ptx::mma_commit(&pv_done[e.t]);
+          if (e.rel) ptx::mma_commit(&v_empty[e.st]);
         }
         __syncwarp();
-        pv_t[x] = -1;
       };
       for (int u = blockIdx.x; u < total; u += gridDim.x) {
         int head, mt0;
         unit(u, head, mt0);
-        int nk[NT], nkb = 0;
-        for (int t = 0; t < NT; ++t) {
-          nk[t] = fa_nkb(a, mt0 + t);
-          nkb = nk[t] > nkb ? nk[t] : nkb;
-        }
+        int nk0 = fa_nkb(a, mt0), nk1 = NT == 2 ? fa_nkb(a, mt0 + 1) : 0;
+        const int nkb = nk0 > nk1 ? nk0 : nk1;
         ptx::mbar_wait(q_full, qph);
         qph ^= 1;
         for (int j = 0; j < nkb; ++j) {
-          int last_t = 0;
-          for (int t = 0; t < NT; ++t)
-            if (j < nk[t]) last_t = t;
+          const int last_t = (NT == 2 && j < nk1) ? 1 : 0;
           bool loaded = false;
+#pragma unroll
           for (int t = 0; t < NT; ++t) {
-            if (j >= nk[t]) continue;
-            const int x = gjob % FA_SLOTS;
+            if (j >= (t ? nk1 : nk0)) continue;
             // the slot's previous P is consumed before S overwrites it; flushed before
-            // waiting for block j (that PV may be what frees block j's ring stage)
-            flush(x);
+            // waiting for block j's K (in-order issue keeps every ring moving)
+            flush(q0);
             if (!loaded) {
-              ptx::mbar_wait(&kv_full[st], ph);
+              ptx::mbar_wait(&k_full[st], ph);
               loaded = true;
             }
             ptx::tc_fence_after();
             if (lane == 0) {
               const uint32_t sa = ptx::smem_u32(sQ + t * Q_BYTES), sb = ptx::smem_u32(sK + st * K_BYTES);
+              const uint32_t dt = tmem + slot * 128;
 #pragma unroll
               for (int k = 0; k < FA_DH / 16; ++k)
-                ptx::mma_bf16(tmem + x * 128, ptx::sdesc_sw128(sa + k * 32), ptx::sdesc_sw128(sb + k * 32), IDS,
-                              k ? 1u : 0u);
-              ptx::mma_commit(&s_full[x]);
+                ptx::mma_bf16(dt, ptx::sdesc_sw128(sa + k * 32), ptx::sdesc_sw128(sb + k * 32), IDS, k ? 1u : 0u);
+              ptx::mma_commit(&s_full[slot]);
+              if (t == last_t) ptx::mma_commit(&k_empty[st]);              // block j's K no longer read
               if (j == nkb - 1 && t == last_t) ptx::mma_commit(q_empty);  // Q no longer read in this unit
             }
             __syncwarp();
-            pv_t[x] = t;
-            pv_j[x] = j;
-            pv_st[x] = st;
-            pv_rel[x] = t == last_t;
-            pv_k[x] = gjob;
-            ++gjob;
+            q0 = q1;
+            q1 = q2;
+            q2.t = t;
+            q2.j = j;
+            q2.st = st;
+            q2.ph = ph;
+            q2.rel = t == last_t;
+            q2.x = slot;
+            q2.pph = (pcnt / FA_SLOTS) & 1;
+            ++pcnt;
+            if (++slot == FA_SLOTS) slot = 0;
           }
           if (++st == FA_STG) { st = 0; ph ^= 1; }
         }
       }
       // drain, oldest job first
-      for (int d = 0; d < FA_SLOTS; ++d) flush((gjob + d) % FA_SLOTS);
+      flush(q0);
+      flush(q1);
+      flush(q2);
     }
   } else {
-    if constexpr (NT == 2) ptx::setmaxnreg_inc<224>();
+    if constexpr (NT == 2) ptx::setmaxnreg_inc<200>();
     const int t = (warp - 4) >> 2;          // this warpgroup's tile of the unit
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;

@@ -568,5 +568,8 @@ def test_evoformer_pair_stack_bf16():
         # first), including chunks of length 1 (the Table 1 ablation's best-effort plans)
         "autochunk-plan 1\nregion s=mo_proj_bg e=mo_proj_b n=4 dims=2\n",
         "autochunk-plan 1\nregion s=mo_proj_bg e=mo_proj_b n=64 dims=2\n",
-        "autochunk-plan 1\nregion s=row_scores e=row_scores n=64 dims=0\nregion s=row_softmax e=row_pv n=64 dims=0\n",
+        # both triangle chains cut across regions (the ablation's best-effort shape): both
+        # run unfused, so the result equals the unfused unchunked run bitwise
+        "autochunk-plan 1\nregion s=row_scores e=row_scores n=64 dims=0\nregion s=row_softmax e=row_pv n=64 dims=0\n"
+        "region s=col_scores e=col_scores n=4 dims=0\nregion s=col_softmax e=col_pv n=4 dims=0\n",
     ], seed=9)
