@@ -58,15 +58,14 @@ def main():
                     res.append(f"   ours bn={bn} act={aa}: {t*1e3:7.1f} us {fl/t/1e9:6.0f} TF/s")
                 except Exception as e:
                     res.append(f"   ours bn={bn} act={aa}: {e}")
-        for ks in ((2, 4) if M <= 4096 else ()):
-            for bn in (64,):
-                f = lambda: K.gemm(a, Kd, w, Kd, out, M, N, Kd, out_s=(0, 0, N, 1), act=act, bias=bb if act else None,
-                                   bn=bn, ksplit=ks)
-                try:
-                    t = t_ms(f)
-                    res.append(f"   ours bn={bn} ksplit={ks} act={act}: {t*1e3:7.1f} us {fl/t/1e9:6.0f} TF/s")
-                except Exception as e:
-                    res.append(f"   ours bn={bn} ksplit={ks}: {e}")
+        for pair in (0, 1):   # BN = 256 as single CTAs / CTA pairs (cta_group::2)
+            f = lambda: K.gemm(a, Kd, w, Kd, out, M, N, Kd, out_s=(0, 0, N, 1), act=act, bias=bb if act else None,
+                               bn=256, cta_pair=pair)
+            try:
+                t = t_ms(f)
+                res.append(f"   ours bn=256 cta_pair={pair} act={act}: {t*1e3:7.1f} us {fl/t/1e9:6.0f} TF/s")
+            except Exception as e:
+                res.append(f"   ours bn=256 cta_pair={pair}: {e}")
         if act:
             ref = torch.nn.functional.gelu(torch.matmul(a.float(), w.float().t()) + bb.float())
             K.gemm(a, Kd, w, Kd, out, M, N, Kd, out_s=(0, 0, N, 1), act=act, bias=bb, bn=256)

@@ -9,10 +9,10 @@ import sys
 
 KIND = {  # kernel template -> node ids it runs in the bench configs
     "gemm_tc_kernel<256, 1>": ["scores"], "gemm_tc_kernel<128, 1>": ["scores"],
-    "gemm_tc_kernel<256, 3>": ["row_scores", "col_scores"],
+    "gemm_tc_kernel<256, 3>": ["row_scores", "col_scores"], "gemm_tc_kernel<256, 4>": ["row_scores", "col_scores"],
     "gemm_tc_kernel<64, 2>": ["pv"], "gemm_tc_kernel<32, 2>": ["row_pv", "col_pv"],
     "stats_combine_kernel": ["softmax", "row_softmax", "col_softmax"],
-    "attn_fused_kernel": ["attn"],
+    "attn_fused_kernel": ["attn"], "attn_fused_kernel<2>": ["attn"], "attn_fused_kernel<1>": ["attn"],
 }
 
 
