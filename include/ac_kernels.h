@@ -41,7 +41,8 @@ typedef struct ac_gemm_desc {
   const void* res;
   void* out; int64_t out_sb1, out_sb2, out_sm, out_sn;
   int32_t bn;                /* tcgen05 N tile (32/64/128/256), 0 = auto */
-  int32_t ksplit;            /* split K over a cluster of this many CTAs (BN = 64 only), <= 1 = off */
+  int32_t cta_pair;          /* BN = 256 plain GEMMs: 1 = run as CTA pairs (cta_group::2, M = 256 per
+                                MMA, bitwise equal to single CTAs); <= 0 single CTAs */
 } ac_gemm_desc;
 
 ac_status ac_kernel_gemm(const ac_gemm_desc* d, void* stream);

@@ -82,7 +82,7 @@ class GemmDesc(C.Structure):
                 ("add_sn", C.c_int64),
                 ("gate", C.c_void_p), ("res", C.c_void_p),
                 ("out", C.c_void_p), ("out_sb1", C.c_int64), ("out_sb2", C.c_int64), ("out_sm", C.c_int64),
-                ("out_sn", C.c_int64), ("bn", C.c_int32), ("ksplit", C.c_int32)]
+                ("out_sn", C.c_int64), ("bn", C.c_int32), ("cta_pair", C.c_int32)]
 
 
 # (name, restype, argtypes) for every symbol declared in include/*.h

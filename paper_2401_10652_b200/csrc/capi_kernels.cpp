@@ -30,7 +30,7 @@ extern "C" ac_status ac_kernel_gemm(const ac_gemm_desc* d, void* stream) {
   e.gate_sm = e.res_sm = d->out_sm;
   e.gate_sn = e.res_sn = d->out_sn;
   cudaError_t err;
-  p.ksplit = d->ksplit > 1 ? d->ksplit : 1;
+  p.cta_pair = d->cta_pair;
   if (d->dtype == 1) err = gemm_tc(p, static_cast<cudaStream_t>(stream), d->bn);
   else if (d->dtype == 0) err = gemm_f32(p, static_cast<cudaStream_t>(stream));
   else return set_error(AC_ERR_ARG, "ac_kernel_gemm: dtype must be AC_F32 or AC_BF16");

@@ -754,8 +754,6 @@ ac_status launch_node_impl(const ac_exec* e, int i, const std::vector<View>& V, 
         }
         chain_overlap(e, i, cx, p);
       }
-      // Cluster split-K (ac_gemm_desc.ksplit) exists but measured slower than one
-      // CTA per tile for these shapes (DSMEM reduction latency), so it stays off.
     } else if (k == "tri_mul") {
       // x[c, i, j] = sum_k a[c, i, k] b[c, j, k]: batch = channels, both operands K-major
       const View &a = in(0), &b = in(1);

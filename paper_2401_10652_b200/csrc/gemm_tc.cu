@@ -57,7 +57,7 @@ struct alignas(64) GemmArgs {
   int tiles_per_batch_dense;
   int total_tiles_dense;
   int vec;  // 1: 8-wide vectorised epilogue (16-byte aux loads / stores) is legal
-  int ks;   // cluster split-K factor (1 = none)
+  int pair2;  // MODE 0, BN = 256: CTA pair (cta_group::2): a cluster of 2 CTAs runs M = 256 MMAs
   int lean; // TMA-store epilogue without aux tensors / activation (scale and causal only)
   int fuse; // fused softmax-normalised A operand (PV of the f2 path)
   const float2* fstats;
@@ -285,8 +285,8 @@ __device__ __forceinline__ void pv_unit(const GemmArgs& a, const int* prefix, in
 // MODE: 0 generic; 1 f2 scores (QK^T -> e = exp(s - m_slab) + slab statistics,
 // lean TMA-store epilogue only); 2 f2 PV (A tile e rescaled to P in shared
 // memory by all epilogue warps, which also run the output epilogue)
-template <int BN, int MODE>
-__global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) gemm_tc_kernel(const __grid_constant__ GemmArgs a) {
+template <int BN, int MODE, bool PAIR>
+__device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
   using C = Cfg<BN, MODE>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -298,8 +298,6 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint64_t* part_full = tempty + 3;   // split-K: leader waits for the other ranks' partials
-  uint64_t* part_empty = tempty + 7;  // split-K: ranks wait for the leader to have read them
   uint64_t* ready = tempty + 11;      // fused softmax: A tile transformed S -> P (<= 8 stages)
   // MODE 2 unit queue: the producer picks the next work unit (dynamically from the
   // sched counter when given, else round-robin) and hands it to the other roles
@@ -315,9 +313,14 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int ks = MODE == 0 ? a.ks : 1;
-  const uint32_t crank = ks > 1 ? ptx::cluster_rank() : 0;
-  const int cid = blockIdx.x / ks, ncl = gridDim.x / ks;
+  // CTA pair (MODE 0, BN = 256): both CTAs of a cluster walk the same tiles (tile rows in
+  // 256-row units); rank r holds rows r * 128 .. +127 of A and of the accumulator and
+  // B rows r * 128 .. +127 of the 256-wide n-tile; the leader (rank 0) issues the MMAs
+  // (a compile-time false outside gemm_tc_pair_kernel: kernels that contain cta_group::2
+  // instructions may only be launched as clusters once any such launch has run)
+  const bool P2 = PAIR && MODE == 0 && BN == 256 && a.pair2 != 0;
+  const uint32_t crank = P2 ? ptx::cluster_rank() : 0;
+  const int cid = P2 ? blockIdx.x / 2 : blockIdx.x, ncl = P2 ? gridDim.x / 2 : gridDim.x;
 
   // --- tile table for causal QK^T: live n-tiles per m-tile, prefix-summed
   int tpb = a.tiles_per_batch_dense;
@@ -389,7 +392,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], MODE == 2 ? (C::XEPI ? C::XEPI : 1) : C::EPI);
+      ptx::mbar_init(&tempty[s], MODE == 2 ? (C::XEPI ? C::XEPI : 1) : (P2 ? 2 : 1) * C::EPI);
     }
     for (int s = 0; s < C::STAGES; ++s) ptx::mbar_init(&ready[s], 32 * C::EPI);
     if (MODE == 3 || MODE == 4)
@@ -400,18 +403,22 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
       ptx::mbar_init(&uq_full[s], 1);
       ptx::mbar_init(&uq_empty[s], 1 + C::EPI + C::XEPI);
     }
-    for (int q = 0; q < 4; ++q) {
-      ptx::mbar_init(&part_full[q], 32 * (ks > 1 ? ks - 1 : 1));
-      ptx::mbar_init(&part_empty[q], 32);
-    }
     ptx::fence_barrier_init();
   }
-  if (warp == 1) ptx::tmem_alloc<C::TMEM_COLS>(tmem_holder);
+  if (warp == 1) {
+    if (P2) ptx::tmem_alloc2<C::TMEM_COLS>(tmem_holder);
+    else ptx::tmem_alloc<C::TMEM_COLS>(tmem_holder);
+  }
   ptx::tc_fence_before();
   __syncthreads();
-  if (ks > 1) ptx::cluster_sync();  // remote barriers initialised before any remote arrive
+  if (P2) ptx::cluster_sync();  // the peer's barriers initialised before any remote arrive / commit
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // an epilogue warp is done with accumulator buffer `acc` (pair: tell the leader's MMA)
+  auto acc_free = [&](int acc_) {
+    if (P2) ptx::mbar_arrive_remote(ptx::map_remote(ptx::smem_u32(&tempty[acc_]), 0));
+    else ptx::mbar_arrive(&tempty[acc_]);
+  };
   // programmatic dependent launch: the prologue above overlapped the previous
   // kernel; wait for its results only when this kernel reads them, and let the
   // next kernel of the chunk loop be scheduled as SMs free up
@@ -489,8 +496,8 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
         } else {
           walk.next(a, prefix, tpb, t, ncl);
           walk.get(a, b1, b2, mt, nt, kbn);
-          klo = kbn * static_cast<int>(crank) / ks;
-          khi = kbn * (static_cast<int>(crank) + 1) / ks;
+          klo = 0;
+          khi = kbn;
         }
         const int ac2 = a.a_b1 ? b1 : 0, ac3 = a.a_b2 ? b2 : 0;
         const int bc2 = a.b_b1 ? b1 : 0, bc3 = a.b_b2 ? b2 : 0;
@@ -515,6 +522,23 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
         // its V^T tile to the second B slot
         const bool two = MODE == 2 && a.pair && b1 * a.B2 + b2 + 1 < a.B1 * a.B2;
         const int pb1 = two ? (b1 * a.B2 + b2 + 1) / a.B2 : 0, pb2 = two ? (b1 * a.B2 + b2 + 1) - pb1 * a.B2 : 0;
+        if (P2) {
+          // pair: this CTA's 128 rows of A and 128 rows of B; both halves' bytes are
+          // counted on the leader's full barrier (its expect_tx covers the pair)
+          // the leader's barrier: this CTA's shared address with the pair's peer bit (bit 24 of
+          // the shared window) cleared - the form the 2-SM TMA expects
+          const uint32_t lead_full = ptx::smem_u32(full) & 0xFEFFFFFFu;
+          for (int kb = klo; kb < khi; ++kb) {
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            if (crank == 0) ptx::mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_TILE / 2));
+            ptx::tma_load_4d_2sm(sA + stage * C::A_BYTES, &a.ta, lead_full + stage * 8, kb * BK,
+                                 (2 * mt + static_cast<int>(crank)) * BM, ac2, ac3);
+            ptx::tma_load_4d_2sm(sB + stage * C::B_BYTES, &a.tb, lead_full + stage * 8, kb * BK,
+                                 nt * BN + static_cast<int>(crank) * (BN / 2), bc2, bc3);
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          }
+          continue;
+        }
         for (int kb = klo; kb < khi; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::mbar_expect_tx(&full[stage], (two ? 2 : 1) * (ebytes + C::B_TILE));
@@ -568,9 +592,12 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
       if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
+  } else if (warp == 1 && P2 && crank != 0) {
+    // the pair's peer issues no MMAs (the leader's cta_group::2 MMAs use its smem halves)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t IDESC = ptx::idesc_bf16(BM, BN);
+    constexpr uint32_t IDESC2 = ptx::idesc_bf16(2 * BM, BN);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -586,8 +613,8 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
       } else {
         walk.next(a, prefix, tpb, t, ncl);
         walk.get(a, b1, b2, mt, nt, kbn);
-        klo = kbn * static_cast<int>(crank) / ks;
-        khi = kbn * (static_cast<int>(crank) + 1) / ks;
+        klo = 0;
+        khi = kbn;
       }
       if constexpr (MODE == 2) {
         // post-scale PV: every k-block gets its own TMEM buffer (kb-th of 8, round
@@ -643,6 +670,11 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
               for (int k = 0; k < BK / 16; ++k)
                 ptx::mma_bf16(d + (static_cast<uint32_t>(16 * q) << 16), ptx::sdesc_sw128(sa + q * 8192 + k * 32),
                               ptx::sdesc_sw128(sb + q * C::B_TILE + k * 32), IDESC64, (kb != klo || k != 0) ? 1u : 0u);
+          } else if (P2) {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              ptx::mma_bf16_2(d, ptx::sdesc_sw128(sa + k * 32), ptx::sdesc_sw128(sb + k * 32), IDESC2,
+                              (kb != klo || k != 0) ? 1u : 0u);
           } else {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
@@ -650,12 +682,16 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
                               (kb != klo || k != 0) ? 1u : 0u);
             }
           }
-          ptx::mma_commit(&empty[stage]);  // slot free once these MMAs have read smem
+          if (P2) ptx::mma_commit2(&empty[stage]);  // both CTAs' slots free
+          else ptx::mma_commit(&empty[stage]);  // slot free once these MMAs have read smem
         }
         __syncwarp();
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
-      if (lane == 0) ptx::mma_commit(&tfull[acc]);  // accumulator ready
+      if (lane == 0) {  // accumulator ready (pair: in both CTAs)
+        if (P2) ptx::mma_commit2(&tfull[acc]);
+        else ptx::mma_commit(&tfull[acc]);
+      }
       __syncwarp();
       if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
@@ -676,7 +712,6 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
     uint32_t aphase = 0;
     uint32_t bphase = 0;  // MODE 3 bias-box barrier phase
     bool bias_pending = false;  // MODE 3: this warp's next bias box is already in flight
-    uint32_t pf_phase = 0, pe_phase = 0;  // split-K barrier phases
     if constexpr (MODE == 2) {
       // ---- f2 PV (post-scale, R19).  Warps 2-5 ("scale", thread = output row of
       // TMEM lane quarter warp % 4): every 64-key slab's product e_slab V_slab lands in
@@ -990,7 +1025,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
             if (hh == 1) {
               ptx::tc_fence_before();
               __syncwarp();
-              if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+              if (lane == 0) acc_free(acc);
             }
             uint32_t pk[16];
 #pragma unroll
@@ -1037,7 +1072,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
         } else {
           ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+          if (lane == 0) acc_free(acc);
         }
         if (++acc == 2) { acc = 0; aphase ^= 1; }
       }
@@ -1055,82 +1090,12 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
       if (half >= NSLAB) {  // narrow tile: nothing for this warp, but keep the tempty count
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+        if (lane == 0) acc_free(acc);
         if (++acc == 2) { acc = 0; aphase ^= 1; }
         continue;
       }
-      const int m0 = mt * BM + quarter * 32;
+      const int m0 = (P2 ? 2 * mt + static_cast<int>(crank) : mt) * BM + quarter * 32;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
-      if constexpr (BN == 64) {
-        if (ks > 1) {
-          // ---- split-K: every rank stages its fp32 partial; the leader (rank 0)
-          // sums rank 0 + 1 + ... + ks-1 through DSMEM and runs the epilogue
-          const int klo = kbn * static_cast<int>(crank) / ks, khi = kbn * (static_cast<int>(crank) + 1) / ks;
-          if (crank != 0) ptx::mbar_wait_cluster(&part_empty[quarter], pe_phase ^ 1);
-          uint32_t r[32], r2[32];
-          if (khi > klo) {
-            ptx::tmem_ld32(tbase, r);
-            ptx::tmem_ld32(tbase + 32, r2);
-            ptx::tmem_ld_wait();
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) r[j] = r2[j] = 0u;
-          }
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-          float4* dst = reinterpret_cast<float4*>(stage + lane * PITCH);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                 __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-            dst[8 + j] = make_float4(__uint_as_float(r2[4 * j]), __uint_as_float(r2[4 * j + 1]),
-                                     __uint_as_float(r2[4 * j + 2]), __uint_as_float(r2[4 * j + 3]));
-          }
-          if (crank != 0) {
-            // every lane publishes its own row (release at cluster scope)
-            ptx::mbar_arrive_remote(ptx::map_remote(ptx::smem_u32(&part_full[quarter]), 0));
-            pe_phase ^= 1;
-          } else {
-            ptx::mbar_wait_cluster(&part_full[quarter], pf_phase);
-            pf_phase ^= 1;
-            __syncwarp();
-            const int rows = min(32, a.M - m0);
-            const int sub = lane / 8, seg = lane % 8;
-            const int n = nt * BN + seg * 8;
-            const bool col_ok = n < a.N;
-            float bias_n[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            if (a.ep.bias && !a.ep.bias_along_m && col_ok)
-              bf16x8_to_f(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.ep.bias) + n), bias_n);
-#pragma unroll 2
-            for (int it = 0; it < 8; ++it) {
-              const int rr = it * 4 + sub;
-              if (rr < rows && col_ok) {
-                Aux8 aux;
-                load_aux8(a.ep, b1, b2, m0 + rr, n, aux);
-                const float* own = stage + rr * PITCH + seg * 8;
-                const float4 u0 = reinterpret_cast<const float4*>(own)[0];
-                const float4 u1 = reinterpret_cast<const float4*>(own)[1];
-                float v8[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
-                const uint32_t la = ptx::smem_u32(own);
-                for (int q = 1; q < ks; ++q) {
-                  const uint32_t ra = ptx::map_remote(la, static_cast<uint32_t>(q));
-                  const float4 w0 = ptx::ld_remote_f4(ra), w1 = ptx::ld_remote_f4(ra + 16);
-                  v8[0] += w0.x; v8[1] += w0.y; v8[2] += w0.z; v8[3] += w0.w;
-                  v8[4] += w1.x; v8[5] += w1.y; v8[6] += w1.z; v8[7] += w1.w;
-                }
-                epilogue8p(a.ep, b1, b2, m0 + rr, n, v8, aux, bias_n);
-              }
-            }
-            // let the other ranks overwrite their staging (each lane releases its reads)
-            for (int q = 1; q < ks; ++q)
-              ptx::mbar_arrive_remote(ptx::map_remote(ptx::smem_u32(&part_empty[quarter]), static_cast<uint32_t>(q)));
-          }
-          __syncwarp();
-          if (++acc == 2) { acc = 0; aphase ^= 1; }
-          continue;
-        }
-      }
 #pragma unroll 1
       for (int c = half; c < NSLAB; c += C::EPI / 4) {
         const bool last = c + C::EPI / 4 >= NSLAB;
@@ -1145,7 +1110,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
             if (last) {
               ptx::tc_fence_before();
               __syncwarp();
-              if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+              if (lane == 0) acc_free(acc);
             }
             continue;
           }
@@ -1272,7 +1237,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
             if (!any_redo && last) {
               ptx::tc_fence_before();
               __syncwarp();
-              if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+              if (lane == 0) acc_free(acc);
             }
             if (redo) {
               mref = mx * cl;
@@ -1284,7 +1249,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
               if (last) {
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+                if (lane == 0) acc_free(acc);
               }
               if (redo) emit(0, mref, l0, l1);
             }
@@ -1303,7 +1268,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
               if (hh == 1 && last) {
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+                if (lane == 0) acc_free(acc);
               }
               emit(hh, mref, l0, l1);
             }
@@ -1382,7 +1347,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
               if (last) {
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+                if (lane == 0) acc_free(acc);
               }
               long long lim = a.ep.causal ? (a.ep.row_off + m - a.ep.col_off - n0) : (1ll << 40);
               if (lim > a.N - 1 - n0) lim = a.N - 1 - n0;  // columns past N: masked (clipped by the store)
@@ -1416,7 +1381,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
               if (hh == 1 && last) {
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+                if (lane == 0) acc_free(acc);
               }
               uint32_t pk[16];
               epilogue_row32(a.ep, b1, b2, m, n0 + hh * 32, mvalid, r, pk, a.N - (n0 + hh * 32));
@@ -1464,7 +1429,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
         if (last) {  // this warp's share of the accumulator is read: release TMEM
           ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+          if (lane == 0) acc_free(acc);
         }
         __syncwarp();
         if (n0 < a.N) {
@@ -1523,14 +1488,29 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) g
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (ks > 1) ptx::cluster_sync();  // the leader has finished reading our staging
+  if (P2) ptx::cluster_sync();  // both CTAs of the pair are done with the paired TMEM
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+    if (P2) ptx::tmem_dealloc2<C::TMEM_COLS>(tmem_base);
+    else ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
   }
 #ifdef AC_DEBUG_HANG
   if (blockIdx.x == 0 && threadIdx.x == 0) printf("gemm_tc<%d,%d> exit\n", BN, MODE);
 #endif
+}
+
+template <int BN, int MODE>
+__global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, Cfg<BN, MODE>::MINB) gemm_tc_kernel(const __grid_constant__ GemmArgs a) {
+  gemm_tc_body<BN, MODE, false>(a);
+}
+
+// the CTA-pair launches of MODE 0 (a.pair2 = 1) get their own function, the only one that
+// contains cta_group::2 instructions: once a kernel with them has run as a cluster of 2,
+// launches of such kernels without that cluster shape fail (cudaErrorInvalidClusterSize;
+// scripts/micro/pair_alloc.cu, cluster_seq.cu)
+template <int BN>
+__global__ void __launch_bounds__(Cfg<BN, 0>::THREADS, 1) gemm_tc_pair_kernel(const __grid_constant__ GemmArgs a) {
+  gemm_tc_body<BN, 0, true>(a);
 }
 
 // ---------------------------------------------------------------- host side
@@ -1579,6 +1559,10 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
+    if constexpr (MODE == 0 && BN == 256) {
+      e = cudaFuncSetAttribute(gemm_tc_pair_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+      if (e != cudaSuccess) return e;
+    }
     attr = true;
   }
   GemmArgs a;
@@ -1687,15 +1671,27 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   a.fstats = p.fuse_stats;
   a.fst_sb1 = p.fuse_sb1;
   a.fst_ss = p.fuse_ss;
-  a.ks = (MODE == 0 && BN == 64 && a.vec && p.ksplit > 1) ? (p.ksplit > 8 ? 8 : p.ksplit) : 1;
-  if (a.ks > 1) a.tma_store = 0;
   const int sms = num_sms();
+  // CTA pair (cta_group::2, M = 256 per MMA): halves each SM's shared-memory operand
+  // traffic per FLOP (B halves).  Bitwise equal to single CTAs, but measured no faster on
+  // the GPT / ViT linears (FFN1 142.6 vs 136.9 us, proj 39.0 vs 33.4 us; scripts/gemm_bench.py):
+  // these GEMMs are bound by the epilogue warps, not by shared-memory bandwidth - so
+  // only on request (ac_gemm_desc.cta_pair = 1)
+  a.pair2 = (MODE == 0 && BN == 256 && a.vec && p.cta_pair > 0) ? 1 : 0;
+  if (a.pair2) {
+    if (!make_map(&a.tb, p.B, p.K, p.b_rows_total ? p.b_rows_total : p.N, p.B1, p.B2, BN / 2))
+      return cudaErrorInvalidValue;
+    a.MT = (p.M + 2 * BM - 1) / (2 * BM);  // tile rows in 256-row units
+    a.tiles_per_batch_dense = a.MT * a.NT;
+    a.total_tiles_dense = a.tiles_per_batch_dense * p.B1 * p.B2;
+  }
   a.pair = (MODE == 2 && BN == 32 && p.etile && p.M <= 64 && a.skng == 1 && !p.causal_k) ? 1 : 0;
   a.zero_word = (MODE == 1 || MODE == 3 || MODE == 4) ? p.zero_word : nullptr;
   a.zero_n = p.zero_n;
+  const int cw = a.pair2 ? 2 : 1;  // CTAs per tile
   int grid = MODE == 4 ? ((p.B1 * p.B2 + 1) / 2) * a.NT
-                       : (a.pair ? (p.B1 * p.B2 + 1) / 2 : a.total_tiles_dense) * a.ks * (MODE == 2 ? a.skng : 1);
-  int cap = C::DUAL ? 2 * sms : (sms / a.ks) * a.ks;
+                       : (a.pair ? (p.B1 * p.B2 + 1) / 2 : a.total_tiles_dense) * cw * (MODE == 2 ? a.skng : 1);
+  int cap = C::DUAL ? 2 * sms : (sms / cw) * cw;
   static int trace_on = -1;
   static unsigned long long* trace_buf = nullptr;
   static int trace_launch = 0;
@@ -1709,48 +1705,60 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
     }
   }
   if (grid > cap) grid = cap;
-  if (grid < a.ks) grid = a.ks;
-  if (a.ks == 1 && p.pdl) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(C::THREADS);
-    cfg.dynamicSmemBytes = C::SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute lattr[1];
-    lattr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    lattr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = lattr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, MODE>, a);
-  }
-  if (a.ks == 1) {
-    gemm_tc_kernel<BN, MODE><<<grid, C::THREADS, C::SMEM, s>>>(a);
-    if (a.trace) {  // debug only: dump {cta, t_load0, t_tfull, t_done} per unit
-      std::vector<unsigned long long> h(trace_units * 4);
-      cudaMemcpy(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost);
-      char fn[256];
-      snprintf(fn, sizeof fn, "%s/trace_%03d.txt", getenv("AC_TRACE"), trace_launch++);
-      if (FILE* f = fopen(fn, "w")) {
-        for (long long u = 0; u < trace_units; ++u)
-          fprintf(f, "%lld %llu %llu %llu %llu\n", u, h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]);
-        fclose(f);
-      }
-    }
-    return cudaGetLastError();
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(C::THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute lattr[1];
-  lattr[0].id = cudaLaunchAttributeClusterDimension;
-  lattr[0].val.clusterDim.x = a.ks;
-  lattr[0].val.clusterDim.y = 1;
-  lattr[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute lattr[2];
+  int na = 0;
+  if (p.pdl) {
+    lattr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    lattr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (a.pair2) {
+    lattr[na].id = cudaLaunchAttributeClusterDimension;
+    lattr[na].val.clusterDim.x = 2;
+    lattr[na].val.clusterDim.y = 1;
+    lattr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = lattr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, MODE>, a);
+  cfg.numAttrs = na;
+  auto kfn = gemm_tc_kernel<BN, MODE>;
+  if constexpr (MODE == 0 && BN == 256)
+    if (a.pair2) kfn = gemm_tc_pair_kernel<BN>;
+  if (a.pair2) {
+    static int diag = 0;
+    int nclu = 0;
+    cudaError_t oe = cudaOccupancyMaxActiveClusters(&nclu, kfn, &cfg);
+    if (oe != cudaSuccess || nclu <= 0) {
+      if (!diag++)
+        fprintf(stderr, "gemm_tc: CTA pair not schedulable (%s, %d clusters, smem %d): single CTAs\n",
+                cudaGetErrorString(oe), nclu, C::SMEM);
+      cudaGetLastError();
+      GemmProblem q = p;
+      q.cta_pair = 0;
+      return launch<BN, MODE>(q, s);
+    }
+  }
+  cudaError_t err = cudaLaunchKernelEx(&cfg, kfn, a);
+  if (err != cudaSuccess && a.pair2)
+    fprintf(stderr, "gemm_tc<%d,%d> pair launch: %s grid %d block %d smem %d attrs %d (cluster %d)\n", BN, MODE,
+            cudaGetErrorString(err), grid, C::THREADS, C::SMEM, na, a.pair2);
+  if (err == cudaSuccess && a.trace) {  // debug only: dump {cta, t_load0, t_tfull, t_done} per unit
+    std::vector<unsigned long long> h(trace_units * 4);
+    cudaMemcpy(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost);
+    char fn[256];
+    snprintf(fn, sizeof fn, "%s/trace_%03d.txt", getenv("AC_TRACE"), trace_launch++);
+    if (FILE* f = fopen(fn, "w")) {
+      for (long long u = 0; u < trace_units; ++u)
+        fprintf(f, "%lld %llu %llu %llu %llu\n", u, h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]);
+      fclose(f);
+    }
+  }
+  return err;
 }
 
 }  // namespace

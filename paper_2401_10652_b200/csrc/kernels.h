@@ -65,7 +65,7 @@ struct GemmProblem {
   // a cluster take contiguous K ranges of the same tile and the leader sums the
   // fp32 partials through distributed shared memory in rank order (deterministic;
   // the split depends only on the tile's K range, never on the chunking)
-  int ksplit = 1;
+  int cta_pair = 0;  // MODE 0, BN = 256: 1 = CTA pair (cta_group::2)
   // fused softmax-normalised PV (NEXT f2): A holds e = 2^(x - m2_slab) written by
   // the QK^T epilogue (Epilogue::stats, the slab statistics (m2, l) in fuse_stats);
   // each 64-key slab's product e V lands in its own TMEM buffer and is folded into

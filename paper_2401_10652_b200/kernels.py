@@ -23,7 +23,7 @@ def _stream(stream):
 def gemm(a, a_srow, b, b_srow, out, M, N, K, B1=1, B2=1, a_sb=(0, 0), a_use=(0, 0), b_sb=(0, 0),
          b_use=(0, 0), out_s=(0, 0, 0, 1), scale=1.0, act=0, causal=0, row_off=0, col_off=0,
          causal_tiles=0, causal_k=0, k_row_off=0, bias=None, bias_along_m=0, add=None,
-         add_s=(0, 0, 0, 0), gate=None, res=None, bn=0, ksplit=1, stream=None):
+         add_s=(0, 0, 0, 0), gate=None, res=None, bn=0, cta_pair=-1, stream=None):
     d = GemmDesc()
     d.dtype = _DT[a.dtype]
     d.M, d.N, d.K, d.B1, d.B2 = M, N, K, B1, B2
@@ -40,7 +40,7 @@ def gemm(a, a_srow, b, b_srow, out, M, N, K, B1=1, B2=1, a_sb=(0, 0), a_use=(0, 
     d.out = out.data_ptr()
     d.out_sb1, d.out_sb2, d.out_sm, d.out_sn = out_s
     d.bn = bn
-    d.ksplit = ksplit
+    d.cta_pair = cta_pair
     check(lib().ac_kernel_gemm(C.byref(d), _stream(stream)))
     return out
 

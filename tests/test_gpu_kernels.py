@@ -89,26 +89,31 @@ def test_gemm_tc_pv_causal_k(K):
     assert _rel(o, ref) < 1e-2
 
 
-@pytest.mark.parametrize("ks,causal", [(2, 0), (4, 0), (4, 1), (8, 1)])
-def test_gemm_tc_cluster_split_k(K, ks, causal):
-    """PV with split-K over a thread-block cluster (DSMEM reduction): equal to the
-    fp32 reference, deterministic run to run, and the causal K loop respected."""
-    torch.manual_seed(7)
-    N, h, dh, rows, row_off = 4096, 3, 64, 640, (1024 if causal else 0)
-    p = torch.rand(h, rows, N, device="cuda")
-    if causal:
-        i = torch.arange(rows, device="cuda")[:, None] + row_off
-        j = torch.arange(N, device="cuda")[None, :]
-        p = torch.where((j <= i)[None], p, torch.zeros_like(p))
-    p = p.bfloat16()
-    vt = torch.randn(h, dh, N, device="cuda").bfloat16()
+@pytest.mark.parametrize("M,N,Kd,act,bias,res", [(4096, 4096, 1024, 1, True, False),
+                                                  (2048 + 128 + 64, 1024, 4096, 0, True, True),
+                                                  (1000, 512, 256, 0, False, False)])
+def test_gemm_tc_cta_pair(K, M, N, Kd, act, bias, res):
+    """CTA pairs (cta_group::2: the leader's M = 256 MMAs over both CTAs' shared-memory
+    halves, multicast commits, the peer's rows written by the peer's epilogue) give the
+    same bits as single CTAs (the K reduction order per element is unchanged, so chunked
+    linears stay bitwise equal to unchunked ones), and match the fp32 reference; ragged
+    M leaves the peer's half partly past the rows."""
+    torch.manual_seed(3)
+    a = torch.randn(M, Kd, device="cuda").bfloat16()
+    w = (torch.randn(N, Kd, device="cuda") / Kd ** 0.5).bfloat16()
+    bv = torch.randn(N, device="cuda").bfloat16() if bias else None
+    rv = torch.randn(M, N, device="cuda").bfloat16() if res else None
     outs = []
-    for _ in range(2):
-        o = torch.empty(rows, h, dh, device="cuda", dtype=torch.bfloat16)
-        K.gemm(p, N, vt, N, o, rows, dh, N, B1=h, a_sb=(rows * N, 0), a_use=(1, 0), b_sb=(dh * N, 0),
-               b_use=(1, 0), out_s=(dh, 0, h * dh, 1), causal_k=causal, k_row_off=row_off, ksplit=ks)
+    for pair in (1, 0):
+        o = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        K.gemm(a, Kd, w, Kd, o, M, N, Kd, out_s=(0, 0, N, 1), bias=bv, act=act, res=rv, bn=256, cta_pair=pair)
         outs.append(o)
-    ref = torch.einsum("hij,hcj->ihc", p.float(), vt.float())
+    torch.cuda.synchronize()
+    ref = a.float() @ w.float().T + (bv.float() if bias else 0)
+    if act == 1:
+        ref = torch.nn.functional.gelu(ref)
+    if res:
+        ref = ref + rv.float()
     assert _rel(outs[0], ref) < 1e-2
     assert torch.equal(outs[0], outs[1])
 
