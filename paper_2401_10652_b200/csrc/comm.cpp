@@ -119,7 +119,7 @@ int comm_rank(const ac_comm* c) { return c ? c->rank : 0; }
 int comm_world(const ac_comm* c) { return c ? c->world : 1; }
 
 ac_status comm_check(const ac_comm* c) {
-  if (!c || c->local || c->world == 1) return AC_OK;
+  if (!c || c->local) return AC_OK;
   const Nccl* nc = nccl();
   if (!nc) return set_error(AC_ERR_NCCL, "libnccl not available");
   for (nccl_comm cm : {c->comm, c->rev}) {

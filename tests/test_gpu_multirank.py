@@ -77,3 +77,27 @@ def test_local_ranks_equal_single_rank(name, world):
                                                   for k in range(plan.num_regions))
         for o in og.outputs:
             assert torch.equal(outs[r][o], ref[o]), (name, world, r, o)
+
+
+def test_nccl_communicator_world1():
+    """The NCCL binding itself on this one-GPU box: unique id, ncclCommInitRank, the
+    rank-reversed ncclCommSplit, ncclCommGetAsyncError (ac_comm_check) and an ac_run
+    through a world-1 communicator (no exchanges) equal to the run without one."""
+    import gpu_util as gu
+    from paper_2401_10652_b200 import api
+    og = workloads.transformer(512, 256, 4, 512, True, "bf16", name="nccl1")
+    cg = gu.c_graph(og)
+    plan = api.plan_parse(cg, "autochunk-plan 1\nregion s=scores e=pv n=4 dims=0\n")
+    _, dev = gu.make_values(og, 0)
+    ref, _ = gu.run(cg, plan, og, dev)
+    comm = api.Comm(api.Comm.unique_id(), 0, 1, torch.cuda.current_device())
+    comm.check()
+    ws = torch.empty(plan.workspace_bytes(0, 1), dtype=torch.uint8, device="cuda")
+    outs = {o: torch.empty_like(ref[o]) for o in og.outputs}
+    ex = api.Exec(plan, ws, comm)
+    ex.run({t: dev[t] for t in og.inputs + og.weights}, outs)
+    torch.cuda.synchronize()
+    comm.check()
+    assert ex.stats().exchanges == 0
+    for o in og.outputs:
+        assert torch.equal(outs[o], ref[o])
