@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libautochunk.so")
+LIB_PATH = os.environ.get("AC_LIB_PATH") or os.path.join(HERE, "libautochunk.so")  # (override: A/B variants)
 
 AC_OK, AC_ERR_ARG, AC_ERR_GRAPH, AC_ERR_BUDGET, AC_ERR_PLAN, AC_ERR_UNSUPPORTED, AC_ERR_BIND, \
     AC_ERR_CUDA, AC_ERR_NCCL, AC_ERR_WORKSPACE = range(10)

@@ -72,8 +72,8 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
     defs = []
     if os.environ.get("AC_DEBUG_HANG"):
         defs.append("-DAC_DEBUG_HANG=1")
-    if os.environ.get("AC_PV_POSTSCALE") is not None:  # experiments: PV variant at build time
-        defs.append("-DAC_PV_POSTSCALE=" + os.environ["AC_PV_POSTSCALE"])
+    for d in os.environ.get("AC_EXTRA_DEFS", "").split():  # experiments: variants at build time
+        defs.append("-D" + d)
     if ninc:
         inc.append("-I" + ninc)
         defs.append("-DAC_HAVE_NCCL_H=1")
@@ -112,10 +112,11 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
     if verbose:
         for l in logs:
             sys.stdout.write(l)
-    tmp = LIB + ".tmp"
+    out = os.environ.get("AC_LIB_OUT", LIB)  # experiments: a variant library beside the default
+    tmp = out + ".tmp"
     _run([NVCC, "-shared", "-o", tmp] + ARCH + objs + ["-lcudart", "-ldl", "-lpthread"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

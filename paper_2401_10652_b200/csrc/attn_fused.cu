@@ -46,9 +46,36 @@ constexpr int FA_STG = 4;        // K ring and V ring depth (separate rings: K i
 constexpr float FA_LAZY = 8.f;   // reference-update threshold of the online softmax (log2 units)
 constexpr int Q_BYTES = FA_BM * FA_DH * 2;   // 16 KB
 constexpr int K_BYTES = FA_BN * FA_DH * 2;   // 16 KB
-constexpr int V_BYTES = FA_DH * FA_BN * 2;   // 16 KB: two 64-key boxes of 8 KB
-constexpr int FA_SLOTS = 3;                  // TMEM S slots (job k -> slot k % 3)
-constexpr int O_COL = 384;                   // TMEM: slots at columns 0 / 128 / 256, O_t at 384 + 64 t
+// V^T per stage: two 64-key boxes, each 64 rows (head dim) of 128 B from TMA plus 16 rows
+// of bf16 ones written once at kernel start, so the PV MMA (N = 80) also accumulates the
+// row sums of P in the output's column 64: l = sum of exactly the bf16 P the MMA used,
+// no per-element additions in the softmax
+constexpr int V_BOX = 64 * 128 + 16 * 128;   // 10 KB
+constexpr int V_BYTES = 2 * V_BOX;
+constexpr int FA_OW = 80;                    // O columns per tile: 64 head dims + 16 (column 64 = l)
+constexpr int FA_OSTR = 96;                  // TMEM column stride between the tiles' O (32-aligned)
+constexpr int FA_SLOTS = 3;                  // barrier slots allocated (NT = 2 uses 2 TMEM S slots)
+
+#ifndef AC_FA_POLY
+#define AC_FA_POLY 0
+#endif
+#ifndef AC_FA_INTPACK
+#define AC_FA_INTPACK 0
+#endif
+// 2^x for x <= 0 on the FMA pipe: x = j + f, j = round(x), 2^f by a degree-4 polynomial
+// (rel. error < 4e-6), 2^j added to the exponent; x < -126 (masked keys) gives 0
+__device__ __forceinline__ float fa_ex2_poly(float x) {
+  const float xc = fmaxf(x, -126.f);
+  const float t = xc + 12582912.f;  // 1.5 * 2^23: round to nearest integer in the low mantissa bits
+  const int j = __float_as_int(t) - 0x4B400000;
+  const float f = xc - (t - 12582912.f);
+  float p = fmaf(f, 1.3333558e-2f, 5.5503349e-2f);
+  p = fmaf(f, p, 2.4022650e-1f);
+  p = fmaf(f, p, 6.9314718e-1f);
+  p = fmaf(f, p, 1.0f);
+  const float r = __int_as_float(__float_as_int(p) + (j << 23));
+  return x < -126.f ? 0.f : r;
+}
 
 template <int NT>
 struct FaCfg {
@@ -80,6 +107,15 @@ __device__ __forceinline__ int fa_nkb(const FaArgs& a, int mt) {
   return static_cast<int>((kend + FA_BN - 1) / FA_BN);
 }
 
+// 16 consecutive 32-bit columns per thread (tcgen05.ld 32x32b.x16)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
 // 16 packed 32-bit columns per thread (tcgen05.st 32x32b.x16)
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
   asm volatile(
@@ -123,6 +159,17 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = a.H * a.NP;
+  // TMEM: SLOTS S slots of 128 columns, then O_t (80 columns) per tile: NT = 2 -> 2 slots
+  // (the two tiles' softmax phases alternate), NT = 1 -> 3 (the tensor core runs ahead)
+  constexpr int SLOTS = NT == 2 ? 2 : 3;
+  constexpr int O_COL = SLOTS * 128;
+  static_assert(O_COL + NT * FA_OSTR <= 512, "TMEM columns");
+  // the ones rows of every V stage (constant; their swizzle is irrelevant)
+  for (int i = threadIdx.x; i < FA_STG * 2 * 512; i += blockDim.x) {
+    const int box = i / 512, w = i % 512;
+    reinterpret_cast<uint32_t*>(sV + box * V_BOX + 8192)[w] = 0x3F803F80u;
+  }
+  ptx::fence_proxy_async_smem();
   if (threadIdx.x == 0) {
     ptx::prefetch_tmap(&a.tq);
     ptx::prefetch_tmap(&a.tk);
@@ -201,15 +248,15 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
         }
         for (int j = 0; j < nkb; ++j) {
           ptx::mbar_wait(&v_empty[st], ph ^ 1);
-          ptx::mbar_expect_tx(&v_full[st], V_BYTES);
+          ptx::mbar_expect_tx(&v_full[st], 2 * 8192);
           ptx::tma_load_4d(sV + st * V_BYTES, &a.tv, &v_full[st], j * FA_BN, 0, head, 0);
-          ptx::tma_load_4d(sV + st * V_BYTES + 8192, &a.tv, &v_full[st], j * FA_BN + 64, 0, head, 0);
+          ptx::tma_load_4d(sV + st * V_BYTES + V_BOX, &a.tv, &v_full[st], j * FA_BN + 64, 0, head, 0);
           if (++st == FA_STG) { st = 0; ph ^= 1; }
         }
       }
     } else if (warp == 1) {
       constexpr uint32_t IDS = ptx::idesc_bf16(FA_BM, FA_BN);
-      constexpr uint32_t IDO = ptx::idesc_bf16(FA_BM, FA_DH);
+      constexpr uint32_t IDO = ptx::idesc_bf16(FA_BM, FA_OW);
       // job k (this CTA's k-th (tile, block)) uses S slot k % 3; its PV is issued right
       // before S of job k + 3 overwrites the slot (in-order MMAs keep the WAR order), so
       // the tensor core runs up to two jobs ahead of the softmax warpgroups.  The three
@@ -234,10 +281,10 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
         ptx::tc_fence_after();
         if (lane == 0) {
           const uint32_t vb = ptx::smem_u32(sV + e.st * V_BYTES);
-          const uint32_t ot = tmem + O_COL + e.t * 64, pt = tmem + e.x * 128;
+          const uint32_t ot = tmem + O_COL + e.t * FA_OSTR, pt = tmem + e.x * 128;
 #pragma unroll
           for (int k = 0; k < FA_BN / 16; ++k)
-            mma_bf16_ts(ot, pt + k * 8, ptx::sdesc_sw128(vb + (k >> 2) * 8192 + (k & 3) * 32), IDO,
+            mma_bf16_ts(ot, pt + k * 8, ptx::sdesc_sw128(vb + (k >> 2) * V_BOX + (k & 3) * 32), IDO,
                         (e.j > 0 || k) ? 1u : 0u);
           ptx::mma_commit(&pv_done[e.t]);
           if (e.rel) ptx::mma_commit(&v_empty[e.st]);
@@ -259,7 +306,9 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
             if (j >= (t ? nk1 : nk0)) continue;
             // the slot's previous P is consumed before S overwrites it; flushed before
             // waiting for block j's K (in-order issue keeps every ring moving)
-            flush(q0);
+            // the oldest pending PV is job k - SLOTS (SLOTS = 2: q1, q2 hold the pending jobs)
+            if constexpr (SLOTS == 3) flush(q0);
+            else flush(q1);
             if (!loaded) {
               ptx::mbar_wait(&k_full[st], ph);
               loaded = true;
@@ -276,7 +325,7 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
               if (j == nkb - 1 && t == last_t) ptx::mma_commit(q_empty);  // Q no longer read in this unit
             }
             __syncwarp();
-            q0 = q1;
+            if constexpr (SLOTS == 3) q0 = q1;
             q1 = q2;
             q2.t = t;
             q2.j = j;
@@ -284,9 +333,9 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
             q2.ph = ph;
             q2.rel = t == last_t;
             q2.x = slot;
-            q2.pph = (pcnt / FA_SLOTS) & 1;
+            q2.pph = (pcnt / SLOTS) & 1;
             ++pcnt;
-            if (++slot == FA_SLOTS) slot = 0;
+            if (++slot == SLOTS) slot = 0;
           }
           if (++st == FA_STG) { st = 0; ph ^= 1; }
         }
@@ -316,13 +365,13 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
         continue;
       }
       const long long qg = a.row_off + static_cast<long long>(mt) * FA_BM + r;  // global query row
-      float m = -CUDART_INF_F, l = 0.f;
+      float m = -CUDART_INF_F;
       for (int j = 0; j < nkb; ++j) {
         for (int tt = 0; tt < t; ++tt) gjob += j < nk[tt];       // the other tiles' jobs of block j first
         const int job = gjob++;
         for (int tt = t + 1; tt < NT; ++tt) gjob += j < nk[tt];
-        const int x = job % FA_SLOTS;
-        ptx::mbar_wait(&s_full[x], (job / FA_SLOTS) & 1);
+        const int x = job % SLOTS;
+        ptx::mbar_wait(&s_full[x], (job / SLOTS) & 1);
         ptx::tc_fence_after();
         uint32_t sv[128];
 #pragma unroll
@@ -349,37 +398,57 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
         const float m_new = (m == -CUDART_INF_F || mx > m + FA_LAZY) ? fmaxf(m, mx) : m;
         const float mref = m_new == -CUDART_INF_F ? 0.f : m_new;
         const float alpha = m == -CUDART_INF_F ? 0.f : (m_new == m ? 1.f : ptx::ex2(m - mref));
-        float l4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int h = 0; h < 4; ++h) {   // 32 keys -> 16 packed columns of P per pass
           uint32_t pk[16];
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
-            const float e0 = ptx::ex2(fmaf(__uint_as_float(sv[h * 32 + 2 * c]), a.cl, -mref));
-            const float e1 = ptx::ex2(fmaf(__uint_as_float(sv[h * 32 + 2 * c + 1]), a.cl, -mref));
-            l4[c & 3] += e0 + e1;
+            const float x0 = fmaf(__uint_as_float(sv[h * 32 + 2 * c]), a.cl, -mref);
+            const float x1 = fmaf(__uint_as_float(sv[h * 32 + 2 * c + 1]), a.cl, -mref);
+#if AC_FA_POLY
+            // (experiment) one pair in AC_FA_POLY+1 on the FMA pipe
+            const bool pc = (c % (AC_FA_POLY + 1)) == AC_FA_POLY;
+            const float e0 = pc ? fa_ex2_poly(x0) : ptx::ex2(x0);
+            const float e1 = pc ? fa_ex2_poly(x1) : ptx::ex2(x1);
+#else
+            const float e0 = ptx::ex2(x0);
+            const float e1 = ptx::ex2(x1);
+#endif
+#if AC_FA_INTPACK
+            // (experiment) round-to-nearest-even bf16 pack on the integer pipe
+            const uint32_t u0 = __float_as_uint(e0), u1 = __float_as_uint(e1);
+            const uint32_t r0 = u0 + 0x7FFFu + ((u0 >> 16) & 1u), r1 = u1 + 0x7FFFu + ((u1 >> 16) & 1u);
+            pk[c] = __byte_perm(r0, r1, 0x7632);
+#else
             __nv_bfloat162 hh = __floats2bfloat162_rn(e0, e1);
             pk[c] = *reinterpret_cast<uint32_t*>(&hh);
+#endif
           }
           tmem_st16(tmem + lrow + x * 128 + h * 16, pk);
         }
-        l = l * alpha + ((l4[0] + l4[1]) + (l4[2] + l4[3]));
         m = m_new;
         if (j >= 1) {
           // PV_{j-1} of this tile complete (NT = 2: it preceded this S on the tensor core)
           ptx::mbar_wait(&pv_done[t], pv_cnt & 1);
           ++pv_cnt;
           if (__any_sync(0xffffffffu, alpha != 1.f)) {
+            // rescale O and its row-sum column (columns 64..79) by 2^(m_old - m_new)
             ptx::tc_fence_after();
+            const uint32_t ob = tmem + lrow + O_COL + t * FA_OSTR;
             uint32_t o[32];
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
-              ptx::tmem_ld32(tmem + lrow + O_COL + t * 64 + hh * 32, o);
+              ptx::tmem_ld32(ob + hh * 32, o);
               ptx::tmem_ld_wait();
 #pragma unroll
               for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
-              ptx::tmem_st32(tmem + lrow + O_COL + t * 64 + hh * 32, o);
+              ptx::tmem_st32(ob + hh * 32, o);
             }
+            tmem_ld16(ob + 64, o);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < 16; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
+            tmem_st16(ob + 64, o);
           }
         }
         ptx::tmem_st_wait();
@@ -396,10 +465,13 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
       ptx::mbar_wait(&pv_done[t], pv_cnt & 1);
       ++pv_cnt;
       ptx::tc_fence_after();
-      uint32_t o[64];
-      ptx::tmem_ld32(tmem + lrow + O_COL + t * 64, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
-      ptx::tmem_ld32(tmem + lrow + O_COL + t * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
+      uint32_t o[64], ls[16];
+      const uint32_t ob = tmem + lrow + O_COL + t * FA_OSTR;
+      ptx::tmem_ld32(ob, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
+      ptx::tmem_ld32(ob + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
+      tmem_ld16(ob + 64, ls);
       ptx::tmem_ld_wait();
+      const float l = __uint_as_float(ls[0]);  // row sum of P (the ones column)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&o_free[t]);

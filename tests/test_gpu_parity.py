@@ -313,6 +313,15 @@ def test_fused_attention_block(N, causal):
     ], seed=4)
 
 
+def test_fused_attention_two_tile_units():
+    """The fused attention's two-tile units (NT = 2, >= 296 tiles: 16 heads x 32 row
+    tiles unchunked) and one-tile units (NT = 1: a 1024-row chunk is 128 tiles) compute
+    every row with the same job order and arithmetic: chunked == unchunked bitwise, and
+    both vs the fp64 oracle."""
+    og = workloads.block("transformer_fa", 4096, 1024, 16, 1024, True, "bf16", name="fa_nt2")
+    _check_all_plans(og, ["autochunk-plan 1\nregion s=attn e=ffn2 n=4 dims=0\n"], seed=6)
+
+
 def test_fused_attention_regime_plan():
     """NEXT f1 at the GPT config: ac_plan under a budget below the fused block's
     unchunked peak chunks the FFN-side intermediates; sampled rows vs the oracle."""
