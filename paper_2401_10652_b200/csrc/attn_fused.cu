@@ -56,27 +56,6 @@ constexpr int FA_OW = 80;                    // O columns per tile: 64 head dims
 constexpr int FA_OSTR = 96;                  // TMEM column stride between the tiles' O (32-aligned)
 constexpr int FA_SLOTS = 3;                  // barrier slots allocated (NT = 2 uses 2 TMEM S slots)
 
-#ifndef AC_FA_POLY
-#define AC_FA_POLY 0
-#endif
-#ifndef AC_FA_INTPACK
-#define AC_FA_INTPACK 0
-#endif
-// 2^x for x <= 0 on the FMA pipe: x = j + f, j = round(x), 2^f by a degree-4 polynomial
-// (rel. error < 4e-6), 2^j added to the exponent; x < -126 (masked keys) gives 0
-__device__ __forceinline__ float fa_ex2_poly(float x) {
-  const float xc = fmaxf(x, -126.f);
-  const float t = xc + 12582912.f;  // 1.5 * 2^23: round to nearest integer in the low mantissa bits
-  const int j = __float_as_int(t) - 0x4B400000;
-  const float f = xc - (t - 12582912.f);
-  float p = fmaf(f, 1.3333558e-2f, 5.5503349e-2f);
-  p = fmaf(f, p, 2.4022650e-1f);
-  p = fmaf(f, p, 6.9314718e-1f);
-  p = fmaf(f, p, 1.0f);
-  const float r = __int_as_float(__float_as_int(p) + (j << 23));
-  return x < -126.f ? 0.f : r;
-}
-
 template <int NT>
 struct FaCfg {
   static constexpr int THREADS = 128 * (1 + NT);
@@ -405,24 +384,10 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
           for (int c = 0; c < 16; ++c) {
             const float x0 = fmaf(__uint_as_float(sv[h * 32 + 2 * c]), a.cl, -mref);
             const float x1 = fmaf(__uint_as_float(sv[h * 32 + 2 * c + 1]), a.cl, -mref);
-#if AC_FA_POLY
-            // (experiment) one pair in AC_FA_POLY+1 on the FMA pipe
-            const bool pc = (c % (AC_FA_POLY + 1)) == AC_FA_POLY;
-            const float e0 = pc ? fa_ex2_poly(x0) : ptx::ex2(x0);
-            const float e1 = pc ? fa_ex2_poly(x1) : ptx::ex2(x1);
-#else
             const float e0 = ptx::ex2(x0);
             const float e1 = ptx::ex2(x1);
-#endif
-#if AC_FA_INTPACK
-            // (experiment) round-to-nearest-even bf16 pack on the integer pipe
-            const uint32_t u0 = __float_as_uint(e0), u1 = __float_as_uint(e1);
-            const uint32_t r0 = u0 + 0x7FFFu + ((u0 >> 16) & 1u), r1 = u1 + 0x7FFFu + ((u1 >> 16) & 1u);
-            pk[c] = __byte_perm(r0, r1, 0x7632);
-#else
             __nv_bfloat162 hh = __floats2bfloat162_rn(e0, e1);
             pk[c] = *reinterpret_cast<uint32_t*>(&hh);
-#endif
           }
           tmem_st16(tmem + lrow + x * 128 + h * 16, pk);
         }
