@@ -377,13 +377,14 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
         const float m_new = (m == -CUDART_INF_F || mx > m + FA_LAZY) ? fmaxf(m, mx) : m;
         const float mref = m_new == -CUDART_INF_F ? 0.f : m_new;
         const float alpha = m == -CUDART_INF_F ? 0.f : (m_new == m ? 1.f : ptx::ex2(m - mref));
+        const uint64_t cl2 = ptx::f32x2_splat(a.cl), nm2 = ptx::f32x2_splat(-mref);
 #pragma unroll
         for (int h = 0; h < 4; ++h) {   // 32 keys -> 16 packed columns of P per pass
           uint32_t pk[16];
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
-            const float x0 = fmaf(__uint_as_float(sv[h * 32 + 2 * c]), a.cl, -mref);
-            const float x1 = fmaf(__uint_as_float(sv[h * 32 + 2 * c + 1]), a.cl, -mref);
+            float x0, x1;  // x = s * cl - m for a key pair in one FFMA2 (same rounding as fmaf)
+            ptx::fma2(sv[h * 32 + 2 * c], sv[h * 32 + 2 * c + 1], cl2, nm2, x0, x1);
             const float e0 = ptx::ex2(x0);
             const float e1 = ptx::ex2(x1);
             __nv_bfloat162 hh = __floats2bfloat162_rn(e0, e1);

@@ -799,8 +799,10 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
 #pragma unroll
                   for (int c = 0; c < 32; ++c) asm volatile("" : "+r"(v[c]));  // uses stay after the wait
                   if (u.mv) {
+                    const uint64_t f2 = ptx::f32x2_splat(f);
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) accv[hh * 32 + c] = fmaf(f, __uint_as_float(v[c]), accv[hh * 32 + c]);
+                    for (int c = 0; c < 32; c += 2)  // FFMA2: same rounding as fmaf(f, v, acc)
+                      ptx::fma2_acc(v[c], v[c + 1], f2, accv[hh * 32 + c], accv[hh * 32 + c + 1]);
                   }
                 }
                 ptx::tc_fence_before();
@@ -1173,10 +1175,18 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
           auto emit = [&](int hh, float mref, float& s0, float& s1) {
             uint32_t pk[16];
             if (lim >= hh * 32 + 31) {
+              const uint64_t cl2 = ptx::f32x2_splat(cl), nm2 = ptx::f32x2_splat(-mref);
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
-                const float e0 = ptx::ex2(fmaf(__uint_as_float(r[2 * j]), cl, -mref));
-                const float e1 = ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), cl, -mref));
+                float x0, x1;
+                if constexpr (!BIASED) {  // one FFMA2 per column pair (same rounding as fmaf)
+                  ptx::fma2(r[2 * j], r[2 * j + 1], cl2, nm2, x0, x1);
+                } else {
+                  x0 = fmaf(__uint_as_float(r[2 * j]), cl, -mref);
+                  x1 = fmaf(__uint_as_float(r[2 * j + 1]), cl, -mref);
+                }
+                const float e0 = ptx::ex2(x0);
+                const float e1 = ptx::ex2(x1);
                 s0 += e0;
                 s1 += e1;
                 __nv_bfloat162 h = __floats2bfloat162_rn(e0, e1);

@@ -296,6 +296,30 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
          (static_cast<uint32_t>(M >> 4) << 24);
 }
 
+// packed fp32 pair FMA (FFMA2): (a0, a1) * (b, b) + (c, c), each lane rounded as fmaf
+__device__ __forceinline__ void fma2(uint32_t a0, uint32_t a1, uint64_t bb, uint64_t cc, float& r0, float& r1) {
+  asm("{\n\t.reg .b64 pa, pr;\n\t"
+      "mov.b64 pa, {%2, %3};\n\t"
+      "fma.rn.f32x2 pr, pa, %4, %5;\n\t"
+      "mov.b64 {%0, %1}, pr;\n}"
+      : "=f"(r0), "=f"(r1)
+      : "r"(a0), "r"(a1), "l"(bb), "l"(cc));
+}
+// packed accumulate (FFMA2): (acc0, acc1) += (v0, v1) * (f, f), each lane rounded as fmaf(f, v, acc)
+__device__ __forceinline__ void fma2_acc(uint32_t v0, uint32_t v1, uint64_t ff, float& acc0, float& acc1) {
+  asm("{\n\t.reg .b64 pv, pc, pr;\n\t"
+      "mov.b64 pv, {%2, %3};\n\t"
+      "mov.b64 pc, {%0, %1};\n\t"
+      "fma.rn.f32x2 pr, pv, %4, pc;\n\t"
+      "mov.b64 {%0, %1}, pr;\n}"
+      : "+f"(acc0), "+f"(acc1)
+      : "r"(v0), "r"(v1), "l"(ff));
+}
+__device__ __forceinline__ uint64_t f32x2_splat(float v) {
+  const uint64_t u = __float_as_uint(v);
+  return u | (u << 32);
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
