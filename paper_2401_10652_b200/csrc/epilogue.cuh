@@ -46,14 +46,68 @@ __device__ __forceinline__ float erf_fast(float z) {
   return copysignf(1.f - erfc, z);
 }
 
+// packed fp32 pairs (FFMA2 / FMUL2: two lanes per instruction, each rounded as the
+// scalar op) for the element-wise epilogue math
+__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_splat(float v) { return f2_pack(v, v); }
+
+// GELU of a pair with erf_fast's arithmetic on packed pairs (the two reciprocals and
+// exponentials stay scalar MUFU ops): half the FMA-pipe instructions of two gelu calls
+__device__ __forceinline__ void gelu_pair(float& x0, float& x1) {
+  const uint64_t x = f2_pack(x0, x1);
+  const uint64_t z = f2_mul(x, f2_splat(0.70710678118654752f));
+  float z0, z1;
+  f2_unpack(z, z0, z1);
+  const uint64_t av = f2_pack(fabsf(z0), fabsf(z1));
+  float d0, d1;
+  f2_unpack(f2_fma(f2_splat(0.3275911f), av, f2_splat(1.f)), d0, d1);
+  const uint64_t t = f2_pack(rcp_approx(d0), rcp_approx(d1));
+  uint64_t p = f2_fma(t, f2_splat(1.061405429f), f2_splat(-1.453152027f));
+  p = f2_fma(t, p, f2_splat(1.421413741f));
+  p = f2_fma(t, p, f2_splat(-0.284496736f));
+  p = f2_fma(t, p, f2_splat(0.254829592f));
+  float q0, q1;
+  f2_unpack(f2_mul(f2_mul(av, av), f2_splat(-1.4426950408889634f)), q0, q1);
+  float ex0, ex1;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ex0) : "f"(q0));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ex1) : "f"(q1));
+  float e0, e1;
+  f2_unpack(f2_mul(f2_mul(t, p), f2_pack(ex0, ex1)), e0, e1);
+  const uint64_t erf = f2_pack(copysignf(1.f - e0, z0), copysignf(1.f - e1, z1));
+  const uint64_t h = f2_mul(x, f2_splat(0.5f));
+  f2_unpack(f2_fma(h, erf, h), x0, x1);  // 0.5 x (1 + erf)
+}
+
 // Activation over an array with the kind test hoisted out of the element loop: a
 // per-element branch puts every element in its own reconvergence region and
 // serialises the otherwise independent erf chains (measured 2x on FFN1).
 template <int NE>
 __device__ __forceinline__ void act_array(int act, float (&x)[NE]) {
   if (act == ACT_GELU) {
+    if constexpr (NE % 2 == 0) {
 #pragma unroll
-    for (int j = 0; j < NE; ++j) x[j] = 0.5f * x[j] * (1.f + erf_fast(x[j] * 0.70710678118654752f));
+      for (int j = 0; j < NE; j += 2) gelu_pair(x[j], x[j + 1]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < NE; ++j) x[j] = 0.5f * x[j] * (1.f + erf_fast(x[j] * 0.70710678118654752f));
+    }
   } else if (act == ACT_SIGMOID) {
 #pragma unroll
     for (int j = 0; j < NE; ++j) x[j] = rcp_approx(1.f + __expf(-x[j]));
