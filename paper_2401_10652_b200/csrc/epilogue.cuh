@@ -67,6 +67,29 @@ __device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
   return r;
 }
 __device__ __forceinline__ uint64_t f2_splat(float v) { return f2_pack(v, v); }
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// x[j] = x[j] * s, x[j] = x[j] + y[j], x[j] = x[j] * y[j] over even-length arrays, two
+// lanes per instruction (bitwise the scalar results)
+template <int NE>
+__device__ __forceinline__ void arr_scale(float (&x)[NE], float sc) {
+  const uint64_t s2 = f2_splat(sc);
+#pragma unroll
+  for (int j = 0; j < NE; j += 2) f2_unpack(f2_mul(f2_pack(x[j], x[j + 1]), s2), x[j], x[j + 1]);
+}
+template <int NE>
+__device__ __forceinline__ void arr_add(float (&x)[NE], const float (&y)[NE]) {
+#pragma unroll
+  for (int j = 0; j < NE; j += 2) f2_unpack(f2_add(f2_pack(x[j], x[j + 1]), f2_pack(y[j], y[j + 1])), x[j], x[j + 1]);
+}
+template <int NE>
+__device__ __forceinline__ void arr_mul(float (&x)[NE], const float (&y)[NE]) {
+#pragma unroll
+  for (int j = 0; j < NE; j += 2) f2_unpack(f2_mul(f2_pack(x[j], x[j + 1]), f2_pack(y[j], y[j + 1])), x[j], x[j + 1]);
+}
 
 // GELU of a pair with erf_fast's arithmetic on packed pairs (the two reciprocals and
 // exponentials stay scalar MUFU ops): half the FMA-pipe instructions of two gelu calls
@@ -263,27 +286,28 @@ __device__ __forceinline__ void load_aux8(const Epilogue& ep, int b1, int b2, in
 __device__ __forceinline__ void epilogue8p(const Epilogue& ep, int b1, int b2, int m, int n, float (&x)[8],
                                            const Aux8& aux, const float (&bias_n)[8]) {
   float a[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) x[i] *= ep.scale;
+  arr_scale(x, ep.scale);
   if (ep.add) {
     bf16x8_to_f(aux.add, a);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] += a[i];
+    arr_add(x, a);
   }
   if (ep.bias) {
+    if (ep.bias_along_m) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] += ep.bias_along_m ? aux.bias_m : bias_n[i];
+      for (int i = 0; i < 8; ++i) a[i] = aux.bias_m;
+      arr_add(x, a);
+    } else {
+      arr_add(x, bias_n);
+    }
   }
   act_array(ep.act, x);
   if (ep.gate) {
     bf16x8_to_f(aux.gate, a);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] *= a[i];
+    arr_mul(x, a);
   }
   if (ep.res) {
     bf16x8_to_f(aux.res, a);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] += a[i];
+    arr_add(x, a);
   }
   if (ep.causal) {
     const int64_t lim = ep.row_off + m - ep.col_off - n;
@@ -323,14 +347,14 @@ __device__ __forceinline__ void epilogue_row32(const Epilogue& ep, int b1, int b
                                                const uint32_t (&r)[32], uint32_t (&pk)[16], int nvalid) {
   float x[32];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(r[j]) * ep.scale;
+  for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(r[j]);
+  arr_scale(x, ep.scale);
   float a[32];
   if (ep.add && mvalid) {
     load32_bf16(static_cast<const __nv_bfloat16*>(ep.add) + static_cast<int64_t>(b1) * ep.add_sb1 +
                     static_cast<int64_t>(b2) * ep.add_sb2 + static_cast<int64_t>(m) * ep.add_sm + n,
                 a, nvalid);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] += a[j];
+    arr_add(x, a);
   }
   if (ep.bias) {
     if (ep.bias_along_m) {
@@ -339,8 +363,7 @@ __device__ __forceinline__ void epilogue_row32(const Epilogue& ep, int b1, int b
       for (int j = 0; j < 32; ++j) x[j] += bm;
     } else {
       load32_bf16(static_cast<const __nv_bfloat16*>(ep.bias) + n, a, nvalid);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) x[j] += a[j];
+      arr_add(x, a);
     }
   }
   act_array(ep.act, x);
@@ -348,15 +371,13 @@ __device__ __forceinline__ void epilogue_row32(const Epilogue& ep, int b1, int b
     load32_bf16(static_cast<const __nv_bfloat16*>(ep.gate) + static_cast<int64_t>(b1) * ep.gate_sb1 +
                     static_cast<int64_t>(b2) * ep.gate_sb2 + static_cast<int64_t>(m) * ep.gate_sm + n,
                 a, nvalid);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] *= a[j];
+    arr_mul(x, a);
   }
   if (ep.res && mvalid) {
     load32_bf16(static_cast<const __nv_bfloat16*>(ep.res) + static_cast<int64_t>(b1) * ep.res_sb1 +
                     static_cast<int64_t>(b2) * ep.res_sb2 + static_cast<int64_t>(m) * ep.res_sm + n,
                 a, nvalid);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] += a[j];
+    arr_add(x, a);
   }
   if (ep.causal) {
     const int64_t lim = ep.row_off + m - ep.col_off - n;  // column n+j masked when j > lim
