@@ -1,27 +1,28 @@
 // NEXT f1: fused (memory-efficient) attention for sm_100a, o = softmax(q k^T * scale) v
 // with no N x N tensor in HBM (the "fused attention kernel" regime of the paper,
-// P:350-351; the graph node kind attn_fused).  One CTA per SM, persistent over work
-// units of NT query tiles (128 rows each, the same head, adjacent rows), causal units
-// heaviest first.
+// P:350-351; the graph node kind attn_fused).  One CTA per SM, persistent over work units
+// = (head, 128-row query tile), causal units heaviest first.  Each tile's key blocks are
+// split into two halves at a position fixed by the tile's own key range (first ceil(n/2)
+// blocks, the rest), one softmax warpgroup per half, merged at the end: a short row chunk
+// (128 tiles < 148 SMs) keeps both warpgroups of every CTA busy, and the arithmetic of a
+// row never depends on the launch, so chunked == unchunked bitwise.
 //
-//   warp 0       : TMA producer - the unit's Q tiles once, K / V^T blocks of 128 keys
-//                  through a 3-stage ring shared by the NT tiles (128B swizzle)
-//   warp 1       : TMEM allocator + MMA issuer.  Jobs (tile t, key block j) in the
-//                  order j-major, t-minor; job k: S = Q_t K_j^T (M=128, N=128, K=64) into
-//                  TMEM slot k % 3, so the tensor core runs up to two jobs ahead of the
-//                  softmax warpgroups (NT = 2: the two tiles' softmax phases overlap each
-//                  other and the MMAs); O_t += P V_j (M=128, N=64, K=128) with P read from
-//                  TMEM (the slot's first 64 columns, bf16 pairs) - issued right before
-//                  the slot's next S, so the tensor core's in-order execution keeps the
-//                  slot's WAR order
-//   warp 3       : idle (NT = 2: registers handed to the softmax warpgroups)
-//   warpgroup 1+t: softmax of tile t, thread = query row over all 128 keys of a block:
-//                  max, lazy online reference (moves only when the block max exceeds
-//                  it by FA_LAZY log2 units, so most blocks need no O rescale),
-//                  P = bf16(2^(x - m)) stored to TMEM, l += sum; O rescaled in TMEM when
-//                  the reference moved; at the end o = O / l stored as bf16.
-// Same arithmetic whatever chunk a query row falls in (the key loop, its order and the
-// reference sequence depend only on the global row), so chunked == unchunked bitwise.
+//   warp 0       : TMA producer - the unit's Q tile once, K blocks of 128 keys through a
+//                  4-stage ring (128B swizzle), one block per job
+//   warp 2       : TMA producer of the V^T blocks (their own 4-stage ring)
+//   warp 1       : TMEM allocator + MMA issuer.  Jobs (half t, block j) in the order
+//                  j-major, t-minor; job k: S = Q K^T (M=128, N=128, K=64) into TMEM slot
+//                  k % 2; O_t += P V (M=128, N=80, K=128) with P read from TMEM (the slot's
+//                  first 64 columns, bf16 pairs), issued right before the slot's next S (the
+//                  tensor core's in-order execution keeps the slot's WAR order); V^T carries
+//                  16 rows of ones, so O_t's column 64 accumulates the row sum of P
+//   warp 3       : idle (its registers go to the softmax warpgroups)
+//   warpgroup 1+t: softmax of half t, thread = query row over all 128 keys of a block:
+//                  max, lazy online reference (moves only when the block max exceeds it by
+//                  FA_LAZY log2 units), P = bf16(2^(x - m)) stored to TMEM, O_t rescaled in
+//                  TMEM when the reference moved.  At the end half 1 hands its reference
+//                  over (shared memory + mbarrier) and half 0 merges:
+//                  o = (a0 O_0 + a1 O_1) / (a0 l_0 + a1 l_1), a_t = 2^(m_t - max(m_0, m_1)).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -41,8 +42,8 @@ namespace {
 constexpr int FA_BM = 128;       // query rows per tile
 constexpr int FA_BN = 128;       // keys per block
 constexpr int FA_DH = 64;        // head dim (one 128-byte swizzle row)
-constexpr int FA_STG = 4;        // K ring and V ring depth (separate rings: K is released by the
-                                 // block's last S, V by its last PV, which runs three jobs later)
+constexpr int FA_STG = 4;        // K ring and V ring depth (separate rings: K is released by its
+                                 // S, V by its PV, which runs two jobs later)
 constexpr float FA_LAZY = 8.f;   // reference-update threshold of the online softmax (log2 units)
 constexpr int Q_BYTES = FA_BM * FA_DH * 2;   // 16 KB
 constexpr int K_BYTES = FA_BN * FA_DH * 2;   // 16 KB
@@ -52,15 +53,12 @@ constexpr int K_BYTES = FA_BN * FA_DH * 2;   // 16 KB
 // no per-element additions in the softmax
 constexpr int V_BOX = 64 * 128 + 16 * 128;   // 10 KB
 constexpr int V_BYTES = 2 * V_BOX;
-constexpr int FA_OW = 80;                    // O columns per tile: 64 head dims + 16 (column 64 = l)
-constexpr int FA_OSTR = 96;                  // TMEM column stride between the tiles' O (32-aligned)
-constexpr int FA_SLOTS = 3;                  // barrier slots allocated (NT = 2 uses 2 TMEM S slots)
-
-template <int NT>
-struct FaCfg {
-  static constexpr int THREADS = 128 * (1 + NT);
-  static constexpr int SMEM = 1024 + NT * Q_BYTES + FA_STG * (K_BYTES + V_BYTES) + 256;
-};
+constexpr int FA_OW = 80;                    // O columns per half: 64 head dims + 16 (column 64 = l)
+constexpr int FA_OSTR = 96;                  // TMEM column stride between the halves' O (32-aligned)
+constexpr int SLOTS = 2;                     // TMEM S slots (job k -> slot k % 2)
+constexpr int O_COL = SLOTS * 128;           // O_0 at 256, O_1 at 352
+constexpr int THREADS = 384;
+constexpr int SMEM = 1024 + Q_BYTES + FA_STG * (K_BYTES + V_BYTES) + 512 + 128 * 4;
 
 struct alignas(64) FaArgs {
   CUtensorMap tq, tk, tv;
@@ -68,16 +66,14 @@ struct alignas(64) FaArgs {
   long long o_srow, o_sh;
   int M, Nk, H;
   int MT;        // 128-row tiles
-  int NP;        // units per head (ceil(MT / NT))
   int causal;
   long long row_off;
   float cl;      // scale * log2(e)
   int pdl;
 };
 
-// key blocks of query tile mt (0 for a tile past the rows)
+// key blocks of query tile mt
 __device__ __forceinline__ int fa_nkb(const FaArgs& a, int mt) {
-  if (mt >= a.MT) return 0;
   long long kend = a.Nk;
   if (a.causal) {
     const long long e = a.row_off + static_cast<long long>(mt + 1) * FA_BM;
@@ -116,12 +112,11 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       : "memory");
 }
 
-template <int NT>
-__global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const __grid_constant__ FaArgs a) {
+__global__ void __launch_bounds__(THREADS, 1) attn_fused_kernel(const __grid_constant__ FaArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sK = sQ + NT * Q_BYTES;
+  uint8_t* sK = sQ + Q_BYTES;
   uint8_t* sV = sK + FA_STG * K_BYTES;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sV + FA_STG * V_BYTES);
   uint64_t* q_full = bar;
@@ -130,19 +125,16 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
   uint64_t* k_empty = k_full + FA_STG;      // [FA_STG]
   uint64_t* v_full = k_empty + FA_STG;      // [FA_STG]
   uint64_t* v_empty = v_full + FA_STG;      // [FA_STG]
-  uint64_t* s_full = v_empty + FA_STG;      // [3] per slot: S written (MMA commit)
-  uint64_t* p_full = s_full + FA_SLOTS;     // [3] per slot: P stored, O rescaled (4 softmax warps)
-  uint64_t* pv_done = p_full + FA_SLOTS;    // [2] per tile: a PV of the tile completed (MMA commit)
-  uint64_t* o_free = pv_done + 2;           // [2] per tile: the epilogue read O (4 softmax warps)
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_free + 2);
+  uint64_t* s_full = v_empty + FA_STG;      // [2] per slot: S written (MMA commit)
+  uint64_t* p_full = s_full + SLOTS;        // [2] per slot: P stored, O rescaled (4 softmax warps)
+  uint64_t* pv_done = p_full + SLOTS;       // [2] per half: a PV of the half completed (MMA commit)
+  uint64_t* o_free = pv_done + 2;           // [2] per half: the merge read O_t (4 warps of half 0)
+  uint64_t* merge_full = o_free + 2;        // half 1's reference is in sm1 (4 warps of half 1)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(merge_full + 1);
+  float* sm1 = reinterpret_cast<float*>(bar + 64);  // [128] half 1's final reference per row
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int total = a.H * a.NP;
-  // TMEM: SLOTS S slots of 128 columns, then O_t (80 columns) per tile: NT = 2 -> 2 slots
-  // (the two tiles' softmax phases alternate), NT = 1 -> 3 (the tensor core runs ahead)
-  constexpr int SLOTS = NT == 2 ? 2 : 3;
-  constexpr int O_COL = SLOTS * 128;
-  static_assert(O_COL + NT * FA_OSTR <= 512, "TMEM columns");
+  const int total = a.H * a.MT;
   // the ones rows of every V stage (constant; their swizzle is irrelevant)
   for (int i = threadIdx.x; i < FA_STG * 2 * 512; i += blockDim.x) {
     const int box = i / 512, w = i % 512;
@@ -161,7 +153,7 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
       ptx::mbar_init(&v_full[s], 1);
       ptx::mbar_init(&v_empty[s], 1);
     }
-    for (int b = 0; b < FA_SLOTS; ++b) {
+    for (int b = 0; b < SLOTS; ++b) {
       ptx::mbar_init(&s_full[b], 1);
       ptx::mbar_init(&p_full[b], 4);
     }
@@ -169,6 +161,7 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
       ptx::mbar_init(&pv_done[b], 1);
       ptx::mbar_init(&o_free[b], 4);
     }
+    ptx::mbar_init(merge_full, 4);
     ptx::fence_barrier_init();
   }
   if (warp == 1) ptx::tmem_alloc<512>(tmem_holder);
@@ -180,75 +173,63 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
     ptx::griddep_wait();
     ptx::griddep_launch();
   }
-  // work unit u -> (head, first tile); causal: heaviest (last) units first
-  auto unit = [&](int u, int& head, int& mt0) {
+  // work unit u -> (head, tile); causal: heaviest (last) tiles first
+  auto unit = [&](int u, int& head, int& mt) {
     const int r = u / a.H;
     head = u - r * a.H;
-    mt0 = (a.causal ? a.NP - 1 - r : r) * NT;
+    mt = a.causal ? a.MT - 1 - r : r;
   };
 
   if (warp < 4) {
-    // NT = 2: 384 threads x 168 registers at launch; the softmax warpgroups take the
-    // producer / MMA warpgroup's spare registers (168 -> 96 there, 168 -> 200 here)
-    if constexpr (NT == 2) ptx::setmaxnreg_dec<96>();
-    if (warp == 0 && lane == 0) {
+    // 384 threads x 168 registers at launch; the softmax warpgroups take this
+    // warpgroup's spare registers (168 -> 96 here, 168 -> 200 there)
+    ptx::setmaxnreg_dec<96>();
+    if ((warp == 0 || warp == 2) && lane == 0) {
+      // warp 0: Q + K blocks, warp 2: V^T blocks, one block per job in job order
+      const bool isk = warp == 0;
       int st = 0;
       uint32_t ph = 0, qph = 0;
       for (int u = blockIdx.x; u < total; u += gridDim.x) {
-        int head, mt0;
-        unit(u, head, mt0);
-        int nkb = 0, nq = 0;
-        for (int t = 0; t < NT; ++t) {
-          const int k = fa_nkb(a, mt0 + t);
-          nkb = k > nkb ? k : nkb;
-          nq += k > 0;
+        int head, mt;
+        unit(u, head, mt);
+        const int nkb = fa_nkb(a, mt), h0 = (nkb + 1) / 2;
+        if (isk) {
+          ptx::mbar_wait(q_empty, qph ^ 1);
+          qph ^= 1;
+          ptx::mbar_expect_tx(q_full, Q_BYTES);
+          ptx::tma_load_4d(sQ, &a.tq, q_full, 0, mt * FA_BM, head, 0);
         }
-        ptx::mbar_wait(q_empty, qph ^ 1);
-        qph ^= 1;
-        ptx::mbar_expect_tx(q_full, nq * Q_BYTES);
-        for (int t = 0; t < nq; ++t) ptx::tma_load_4d(sQ + t * Q_BYTES, &a.tq, q_full, 0, (mt0 + t) * FA_BM, head, 0);
-        for (int j = 0; j < nkb; ++j) {
-          ptx::mbar_wait(&k_empty[st], ph ^ 1);
-          ptx::mbar_expect_tx(&k_full[st], K_BYTES);
-          ptx::tma_load_4d(sK + st * K_BYTES, &a.tk, &k_full[st], 0, j * FA_BN, head, 0);
-          if (++st == FA_STG) { st = 0; ph ^= 1; }
-        }
-      }
-    } else if (warp == 2 && lane == 0) {   // V^T blocks, on their own ring
-      int st = 0;
-      uint32_t ph = 0;
-      for (int u = blockIdx.x; u < total; u += gridDim.x) {
-        int head, mt0;
-        unit(u, head, mt0);
-        int nkb = 0;
-        for (int t = 0; t < NT; ++t) {
-          const int k = fa_nkb(a, mt0 + t);
-          nkb = k > nkb ? k : nkb;
-        }
-        for (int j = 0; j < nkb; ++j) {
-          ptx::mbar_wait(&v_empty[st], ph ^ 1);
-          ptx::mbar_expect_tx(&v_full[st], 2 * 8192);
-          ptx::tma_load_4d(sV + st * V_BYTES, &a.tv, &v_full[st], j * FA_BN, 0, head, 0);
-          ptx::tma_load_4d(sV + st * V_BYTES + V_BOX, &a.tv, &v_full[st], j * FA_BN + 64, 0, head, 0);
-          if (++st == FA_STG) { st = 0; ph ^= 1; }
+        for (int j = 0; j < h0; ++j) {
+          for (int t = 0; t < 2; ++t) {
+            const int blk = 2 * j + t;
+            if (blk >= nkb) continue;
+            if (isk) {
+              ptx::mbar_wait(&k_empty[st], ph ^ 1);
+              ptx::mbar_expect_tx(&k_full[st], K_BYTES);
+              ptx::tma_load_4d(sK + st * K_BYTES, &a.tk, &k_full[st], 0, blk * FA_BN, head, 0);
+            } else {
+              ptx::mbar_wait(&v_empty[st], ph ^ 1);
+              ptx::mbar_expect_tx(&v_full[st], 2 * 8192);
+              ptx::tma_load_4d(sV + st * V_BYTES, &a.tv, &v_full[st], blk * FA_BN, 0, head, 0);
+              ptx::tma_load_4d(sV + st * V_BYTES + V_BOX, &a.tv, &v_full[st], blk * FA_BN + 64, 0, head, 0);
+            }
+            if (++st == FA_STG) { st = 0; ph ^= 1; }
+          }
         }
       }
     } else if (warp == 1) {
       constexpr uint32_t IDS = ptx::idesc_bf16(FA_BM, FA_BN);
       constexpr uint32_t IDO = ptx::idesc_bf16(FA_BM, FA_OW);
-      // job k (this CTA's k-th (tile, block)) uses S slot k % 3; its PV is issued right
-      // before S of job k + 3 overwrites the slot (in-order MMAs keep the WAR order), so
-      // the tensor core runs up to two jobs ahead of the softmax warpgroups.  The three
-      // pending PVs (jobs k-3, k-2, k-1) are a register FIFO: no dynamically indexed
-      // arrays (local memory) on this warp's critical path.
+      // job k uses S slot k % 2; its PV is issued right before S of job k + 2 overwrites the
+      // slot.  The two pending PVs (jobs k-2, k-1) are a register FIFO (no local memory).
       struct Pend {
-        int t = -1, j = 0, st = 0, rel = 0, x = 0;
+        int t = -1, j = 0, st = 0, x = 0;
         uint32_t ph = 0, pph = 0;  // V stage phase, P phase of the slot
       };
-      Pend q0, q1, q2;                    // oldest .. newest
-      uint32_t o_units0 = 0, o_units1 = 0;  // units of tile 0 / 1 whose first PV was issued
+      Pend q1, q2;                        // older, newer
+      uint32_t o_units0 = 0, o_units1 = 0;  // units of half 0 / 1 whose first PV was issued
       int st = 0, slot = 0;
-      uint32_t ph = 0, qph = 0, pcnt = 0;  // pcnt: jobs issued (slot use = pcnt / 3)
+      uint32_t ph = 0, qph = 0, pcnt = 0;
       auto flush = [&](const Pend& e) {    // issue a pending PV
         if (e.t < 0) return;
         ptx::mbar_wait(&p_full[e.x], e.pph);
@@ -266,89 +247,75 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
             mma_bf16_ts(ot, pt + k * 8, ptx::sdesc_sw128(vb + (k >> 2) * V_BOX + (k & 3) * 32), IDO,
                         (e.j > 0 || k) ? 1u : 0u);
           ptx::mma_commit(&pv_done[e.t]);
-          if (e.rel) ptx::mma_commit(&v_empty[e.st]);
+          ptx::mma_commit(&v_empty[e.st]);
         }
         __syncwarp();
       };
       for (int u = blockIdx.x; u < total; u += gridDim.x) {
-        int head, mt0;
-        unit(u, head, mt0);
-        int nk0 = fa_nkb(a, mt0), nk1 = NT == 2 ? fa_nkb(a, mt0 + 1) : 0;
-        const int nkb = nk0 > nk1 ? nk0 : nk1;
+        int head, mt;
+        unit(u, head, mt);
+        const int nkb = fa_nkb(a, mt), h0 = (nkb + 1) / 2;
         ptx::mbar_wait(q_full, qph);
         qph ^= 1;
-        for (int j = 0; j < nkb; ++j) {
-          const int last_t = (NT == 2 && j < nk1) ? 1 : 0;
-          bool loaded = false;
-#pragma unroll
-          for (int t = 0; t < NT; ++t) {
-            if (j >= (t ? nk1 : nk0)) continue;
-            // the slot's previous P is consumed before S overwrites it; flushed before
-            // waiting for block j's K (in-order issue keeps every ring moving)
-            // the oldest pending PV is job k - SLOTS (SLOTS = 2: q1, q2 hold the pending jobs)
-            if constexpr (SLOTS == 3) flush(q0);
-            else flush(q1);
-            if (!loaded) {
-              ptx::mbar_wait(&k_full[st], ph);
-              loaded = true;
-            }
+        for (int j = 0; j < h0; ++j) {
+          for (int t = 0; t < 2; ++t) {
+            const int blk = 2 * j + t;
+            if (blk >= nkb) continue;
+            flush(q1);  // the slot's previous P is consumed before S overwrites it
+            ptx::mbar_wait(&k_full[st], ph);
             ptx::tc_fence_after();
             if (lane == 0) {
-              const uint32_t sa = ptx::smem_u32(sQ + t * Q_BYTES), sb = ptx::smem_u32(sK + st * K_BYTES);
+              const uint32_t sa = ptx::smem_u32(sQ), sb = ptx::smem_u32(sK + st * K_BYTES);
               const uint32_t dt = tmem + slot * 128;
 #pragma unroll
               for (int k = 0; k < FA_DH / 16; ++k)
                 ptx::mma_bf16(dt, ptx::sdesc_sw128(sa + k * 32), ptx::sdesc_sw128(sb + k * 32), IDS, k ? 1u : 0u);
               ptx::mma_commit(&s_full[slot]);
-              if (t == last_t) ptx::mma_commit(&k_empty[st]);              // block j's K no longer read
-              if (j == nkb - 1 && t == last_t) ptx::mma_commit(q_empty);  // Q no longer read in this unit
+              ptx::mma_commit(&k_empty[st]);                  // K read by this S only
+              if (blk == nkb - 1) ptx::mma_commit(q_empty);  // the unit's last S (jobs run in block order)
             }
             __syncwarp();
-            if constexpr (SLOTS == 3) q0 = q1;
             q1 = q2;
             q2.t = t;
             q2.j = j;
             q2.st = st;
             q2.ph = ph;
-            q2.rel = t == last_t;
             q2.x = slot;
             q2.pph = (pcnt / SLOTS) & 1;
             ++pcnt;
             if (++slot == SLOTS) slot = 0;
+            if (++st == FA_STG) { st = 0; ph ^= 1; }
           }
-          if (++st == FA_STG) { st = 0; ph ^= 1; }
         }
       }
-      // drain, oldest job first
-      flush(q0);
       flush(q1);
       flush(q2);
     }
   } else {
-    if constexpr (NT == 2) ptx::setmaxnreg_inc<200>();
-    const int t = (warp - 4) >> 2;          // this warpgroup's tile of the unit
+    ptx::setmaxnreg_inc<200>();
+    const int t = (warp - 4) >> 2;          // this warpgroup's half of each tile's key blocks
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;
     const uint32_t lrow = static_cast<uint32_t>(quarter * 32) << 16;
-    uint32_t pv_cnt = 0;                    // PVs of this tile awaited so far
-    int gjob = 0;                           // jobs of this CTA so far (all tiles): slot = job % 3
+    uint32_t pv_cnt = 0;                    // PVs of this half awaited so far
+    uint32_t merges = 0;                    // units merged (merge_full phase)
+    int gjob = 0;                           // jobs of this CTA so far (both halves): slot = job % 2
     for (int u = blockIdx.x; u < total; u += gridDim.x) {
-      int head, mt0;
-      unit(u, head, mt0);
-      int nk[NT];
-      for (int tt = 0; tt < NT; ++tt) nk[tt] = fa_nkb(a, mt0 + tt);
-      const int mt = mt0 + t;
-      const int nkb = nk[t];
-      if (nkb == 0) {
-        for (int tt = 0; tt < NT; ++tt) gjob += nk[tt];
+      int head, mt;
+      unit(u, head, mt);
+      const int nkb = fa_nkb(a, mt), h0 = (nkb + 1) / 2;
+      const int nk0 = h0, nk1 = nkb - h0;   // even / odd key blocks
+      const int nk = t ? nk1 : nk0;
+      if (nk == 0) {                        // (half 1 of a one-block tile)
+        gjob += nkb;
         continue;
       }
       const long long qg = a.row_off + static_cast<long long>(mt) * FA_BM + r;  // global query row
       float m = -CUDART_INF_F;
-      for (int j = 0; j < nkb; ++j) {
-        for (int tt = 0; tt < t; ++tt) gjob += j < nk[tt];       // the other tiles' jobs of block j first
+      for (int j = 0; j < nk; ++j) {
+        if (t == 1) gjob += 1;                         // half 0's job of block pair j first
         const int job = gjob++;
-        for (int tt = t + 1; tt < NT; ++tt) gjob += j < nk[tt];
+        if (t == 0 && j < nk1) gjob += 1;              // then half 1's
         const int x = job % SLOTS;
         ptx::mbar_wait(&s_full[x], (job / SLOTS) & 1);
         ptx::tc_fence_after();
@@ -358,7 +325,7 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
           ptx::tmem_ld32(tmem + lrow + x * 128 + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
         ptx::tmem_ld_wait();
         // mask: keys past the row (causal) or past Nk
-        const long long k0 = static_cast<long long>(j) * FA_BN;
+        const long long k0 = static_cast<long long>(2 * j + t) * FA_BN;
         long long lim = a.Nk - 1 - k0;
         if (a.causal && qg - k0 < lim) lim = qg - k0;
         if (lim < FA_BN - 1) {
@@ -374,6 +341,10 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
         const float mb = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
                                fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
         const float mx = mb * a.cl;
+        // lazy reference: the running reference m moves only when the block max exceeds
+        // it by more than FA_LAZY (log2 units), so P = 2^(x - m) <= 2^FA_LAZY; O and l
+        // share the reference, so o = O / l is the same softmax.  The sequence of
+        // references depends only on the row's keys, so chunked == unchunked bitwise.
         const float m_new = (m == -CUDART_INF_F || mx > m + FA_LAZY) ? fmaxf(m, mx) : m;
         const float mref = m_new == -CUDART_INF_F ? 0.f : m_new;
         const float alpha = m == -CUDART_INF_F ? 0.f : (m_new == m ? 1.f : ptx::ex2(m - mref));
@@ -394,11 +365,11 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
         }
         m = m_new;
         if (j >= 1) {
-          // PV_{j-1} of this tile complete (NT = 2: it preceded this S on the tensor core)
+          // this half's previous PV complete (it preceded this S on the tensor core)
           ptx::mbar_wait(&pv_done[t], pv_cnt & 1);
           ++pv_cnt;
           if (__any_sync(0xffffffffu, alpha != 1.f)) {
-            // rescale O and its row-sum column (columns 64..79) by 2^(m_old - m_new)
+            // rescale O_t and its row-sum column (columns 64..79) by 2^(m_old - m_new)
             ptx::tc_fence_after();
             const uint32_t ob = tmem + lrow + O_COL + t * FA_OSTR;
             uint32_t o[32];
@@ -422,41 +393,70 @@ __global__ void __launch_bounds__(FaCfg<NT>::THREADS, 1) attn_fused_kernel(const
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&p_full[x]);
       }
-      // the other tiles' jobs past this tile's last block
-      int nmax = 0;
-      for (int tt = 0; tt < NT; ++tt) nmax = nk[tt] > nmax ? nk[tt] : nmax;
-      for (int j = nkb; j < nmax; ++j)
-        for (int tt = 0; tt < NT; ++tt) gjob += j < nk[tt];
-      // epilogue: the tile's last PV, o = O / l
+      if (t == 1) gjob += nk0 - nk1;                   // half 0's jobs past half 1's last block
+      // this half's last PV
       ptx::mbar_wait(&pv_done[t], pv_cnt & 1);
       ++pv_cnt;
+      if (t == 1) {
+        // hand the reference to half 0 (its O_1 stays in TMEM until half 0 read it)
+        sm1[r] = m;
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(merge_full);
+        continue;
+      }
       ptx::tc_fence_after();
-      uint32_t o[64], ls[16];
-      const uint32_t ob = tmem + lrow + O_COL + t * FA_OSTR;
-      ptx::tmem_ld32(ob, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
-      ptx::tmem_ld32(ob + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
-      tmem_ld16(ob + 64, ls);
+      const uint32_t ob0 = tmem + lrow + O_COL, ob1 = ob0 + FA_OSTR;
+      float a0 = 1.f, a1 = 0.f;
+      const bool two = nk1 > 0;
+      if (two) {
+        ptx::mbar_wait(merge_full, merges & 1);
+        ++merges;
+        ptx::tc_fence_after();
+        const float m1 = sm1[r];
+        const float mm = fmaxf(m, m1);
+        a0 = ptx::ex2(m - mm);
+        a1 = ptx::ex2(m1 - mm);
+      }
+      uint32_t l0[16], l1[16];
+      tmem_ld16(ob0 + 64, l0);
+      if (two) tmem_ld16(ob1 + 64, l1);
       ptx::tmem_ld_wait();
-      const float l = __uint_as_float(ls[0]);  // row sum of P (the ones column)
+      const float lt = two ? fmaf(a1, __uint_as_float(l1[0]), a0 * __uint_as_float(l0[0])) : __uint_as_float(l0[0]);
+      const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      const float w0 = a0 * inv, w1 = a1 * inv;
+      const int mrow = mt * FA_BM + r;
+      uint4* dst = reinterpret_cast<uint4*>(a.out + static_cast<long long>(mrow) * a.o_srow +
+                                            static_cast<long long>(head) * a.o_sh);
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t o0[32], o1[32];
+        ptx::tmem_ld32(ob0 + hh * 32, o0);
+        if (two) ptx::tmem_ld32(ob1 + hh * 32, o1);
+        ptx::tmem_ld_wait();
+        if (mrow < a.M) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int k = 8 * c + 2 * e;
+              float y0 = __uint_as_float(o0[k]) * w0, y1 = __uint_as_float(o0[k + 1]) * w0;
+              if (two) {
+                y0 = fmaf(__uint_as_float(o1[k]), w1, y0);
+                y1 = fmaf(__uint_as_float(o1[k + 1]), w1, y1);
+              }
+              __nv_bfloat162 h = __floats2bfloat162_rn(y0, y1);
+              w[e] = *reinterpret_cast<uint32_t*>(&h);
+            }
+            dst[hh * 4 + c] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&o_free[t]);
-      const int mrow = mt * FA_BM + r;
-      if (mrow < a.M) {
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-        uint4* dst = reinterpret_cast<uint4*>(a.out + static_cast<long long>(mrow) * a.o_srow +
-                                              static_cast<long long>(head) * a.o_sh);
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint32_t w[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 2 * e]) * inv,
-                                                     __uint_as_float(o[8 * c + 2 * e + 1]) * inv);
-            w[e] = *reinterpret_cast<uint32_t*>(&h);
-          }
-          dst[c] = make_uint4(w[0], w[1], w[2], w[3]);
-        }
+      if (lane == 0) {
+        ptx::mbar_arrive(&o_free[0]);
+        if (two) ptx::mbar_arrive(&o_free[1]);
       }
     }
   }
@@ -503,31 +503,25 @@ bool map3(CUtensorMap* m, const void* p, long long inner, long long rows, long l
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int NT>
 cudaError_t attn_fused_launch(cudaStream_t s, FaArgs& a, long long units) {
-  using CF = FaCfg<NT>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fused_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(attn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int grid = static_cast<int>(units < num_sms() ? units : num_sms());
-  if (a.pdl) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(CF::THREADS);
-    cfg.dynamicSmemBytes = CF::SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute la[1];
-    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    la[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = la;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, attn_fused_kernel<NT>, a);
-  }
-  attn_fused_kernel<NT><<<grid, CF::THREADS, CF::SMEM, s>>>(a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = la;
+  cfg.numAttrs = a.pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, attn_fused_kernel, a);
 }
 
 }  // namespace
@@ -554,15 +548,7 @@ cudaError_t attn_fused(const AttnFusedProblem& p, cudaStream_t s) {
   a.row_off = p.row_off;
   a.cl = p.scale * 1.4426950408889634f;
   a.pdl = p.pdl;
-  const long long tiles = static_cast<long long>(a.H) * a.MT;
-  // two query tiles per CTA (ping-pong) when the launch still fills every SM with
-  // such pairs; otherwise one tile per CTA (short row chunks)
-  if (tiles >= 2LL * num_sms()) {
-    a.NP = (a.MT + 1) / 2;
-    return attn_fused_launch<2>(s, a, static_cast<long long>(a.H) * a.NP);
-  }
-  a.NP = a.MT;
-  return attn_fused_launch<1>(s, a, tiles);
+  return attn_fused_launch(s, a, static_cast<long long>(a.H) * a.MT);
 }
 
 }  // namespace ac
