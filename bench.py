@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-unchunked", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time direct ac_run launches instead of a captured CUDA graph of one ac_run")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
     ap.add_argument("--sweep", action="store_true", help="also sweep the attention chunk length 64..4096")
     ap.add_argument("--layers", type=int, default=1,
@@ -580,11 +582,25 @@ def main():
     ex = api.Exec(plan, ws, comm)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
 
+    use_graph = not args.no_graph and world == 1
+
     def timed(exe, inputs, outputs, K, W, profile=False, pre=None, post=None):
         for _ in range(W):
             exe.run(inputs, outputs)
         exe.set_profiling(profile)
         torch.cuda.synchronize()
+        graph = None
+        if use_graph and not profile and pre is None and post is None:
+            # one ac_run captured into a CUDA graph and replayed per step (ac_run is
+            # stream-ordered with no host synchronisation; replay is bitwise the direct
+            # run, test_ac_run_cuda_graph_capture): the host's per-launch cost leaves the
+            # timed region, which matters for the launch-bound small configs
+            gs = torch.cuda.Stream()
+            gs.wait_stream(s)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=gs):
+                exe.run(inputs, outputs, stream=gs)
+            torch.cuda.synchronize()
         barrier()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
         kt = {}
@@ -593,7 +609,10 @@ def main():
             evs[k][0].record(s)
             if pre:
                 pre()
-            exe.run(inputs, outputs)
+            if graph is not None:
+                graph.replay()
+            else:
+                exe.run(inputs, outputs)
             if post:
                 post()
             evs[k][1].record(s)
@@ -882,7 +901,9 @@ def main():
                    "plan": regions, "parallelism": f"chunk-split x{world}" + (
                        " (zigzag / round-robin chunk shares, row-partitioned post-region nodes, NCCL all-gather)"
                        if world > 1 else ""),
-                   "l2": "flushed between timed steps (256 MiB write)"},
+                   "l2": "flushed between timed steps (256 MiB write)",
+                   "launch": "one ac_run captured as a CUDA graph, replayed per step" if use_graph else
+                             "direct ac_run launches"},
         "peak_activation_bytes": peak_block(profp, prof0, st, budget, caller, activation_alloc, unchunked),
         "unchunked": unchunked, "roofline": roof, "stages": shares, "cpu_baseline": cpu, "e2e": e2e,
         "error_vs_oracle": err, "planner_timing": ptime,
