@@ -574,7 +574,7 @@ def main():
     torch.cuda.synchronize()
     torch.cuda.reset_peak_memory_stats()
     weights_bytes = sum(dev[w[0]].numel() * dev[w[0]].element_size() for w in doc.weights)
-    ws = torch.empty(max(plan.workspace_bytes(), 16), dtype=torch.uint8, device="cuda")
+    ws = torch.empty(max(plan.workspace_bytes(rank, world), 16), dtype=torch.uint8, device="cuda")
     TD = {"bf16": torch.bfloat16, "f32": torch.float32}
     outs = {o: torch.empty(doc.tensors[o][1], dtype=TD[doc.tensors[o][0]], device="cuda") for o in doc.outputs}
     activation_alloc = torch.cuda.memory_allocated() - weights_bytes  # inputs + outputs + workspace
@@ -698,7 +698,7 @@ def main():
     if not args.no_unchunked and not args.profile:
         try:
             up = api.plan_parse(cg, "autochunk-plan 1\n")
-            need = up.workspace_bytes()
+            need = up.workspace_bytes(rank, world)
             free, _ = torch.cuda.mem_get_info()
             if need + (1 << 30) < free:
                 wsu = torch.empty(need, dtype=torch.uint8, device="cuda")
@@ -802,7 +802,7 @@ def main():
                                                  for r in base_regions)
             sp = api.plan_parse(cg, txt)
             pr, _ = api.estimate_memory(cg, sp)
-            wss = torch.empty(max(sp.workspace_bytes(), 16), dtype=torch.uint8, device="cuda")
+            wss = torch.empty(max(sp.workspace_bytes(rank, world), 16), dtype=torch.uint8, device="cuda")
             exs = api.Exec(sp, wss, comm)
             ks = max(2, args.steps // 2)
             ts, _ = timed(exs, ins, outs, ks, 1)
@@ -832,7 +832,7 @@ def main():
                 txt = "\n".join(ln.split(" flow=")[0] for ln in ap_.serialize().splitlines() if ln.startswith("region"))
                 if txt not in timed_plans:
                     pr_, _ = api.estimate_memory(cg, ap_)
-                    wsa = torch.empty(max(ap_.workspace_bytes(), 16), dtype=torch.uint8, device="cuda")
+                    wsa = torch.empty(max(ap_.workspace_bytes(rank, world), 16), dtype=torch.uint8, device="cuda")
                     exa = api.Exec(ap_, wsa, comm)
                     ka = max(3, args.steps // 2)
                     ta, _ = timed(exa, ins, outs, ka, 2)
@@ -851,7 +851,7 @@ def main():
                 txt = f"region s={s0} e={e0} n={n_f} dims=0{opt}"
                 fp = api.plan_parse(cg, "autochunk-plan 1\n" + txt + "\n")
                 pr_, _ = api.estimate_memory(cg, fp)
-                wsa = torch.empty(max(fp.workspace_bytes(), 16), dtype=torch.uint8, device="cuda")
+                wsa = torch.empty(max(fp.workspace_bytes(rank, world), 16), dtype=torch.uint8, device="cuda")
                 exa = api.Exec(fp, wsa, comm)
                 ka = max(3, args.steps // 2)
                 ta, _ = timed(exa, ins, outs, ka, 2)

@@ -192,6 +192,26 @@ def test_gpt_full_size_sampled_rows():
     assert st.control_bytes < 1 << 20
 
 
+def test_gpt_full_size_whole_block_plan():
+    """The forced whole-block plan at the full GPT size ([proj_q ... ffn2]
+    on 2048-row chunks, K / V hoisted, the N x 4d FFN hidden never exists): sampled rows
+    vs the oracle, and the same bits as the planner's attention-region plan (tiles and
+    row kernels never depend on the chunking)."""
+    gu = _gu()
+    from paper_2401_10652_b200 import api
+    og = workloads.config("gpt")
+    cg = gu.c_graph(og)
+    vals, dev = gu.make_values(og, 0)
+    got, ex = gu.run(cg, api.plan_parse(cg, "autochunk-plan 1\nregion s=proj_q e=ffn2 n=8 dims=0\n"), og, dev)
+    torch.cuda.synchronize()
+    rows = blocks.sample_rows(16384, 2048, 24)
+    ref = blocks.transformer_rows(og, vals, rows)
+    assert gu.rel_err(got["y"][torch.from_numpy(rows).cuda()], ref["y"]) < 2e-2
+    other, _ = gu.run(cg, api.plan_parse(cg, "autochunk-plan 1\nregion s=scores e=pv n=8 dims=0\n"), og, dev)
+    torch.cuda.synchronize()
+    assert torch.equal(got["y"], other["y"])
+
+
 @pytest.mark.parametrize("causal", [True, False])
 def test_fused_softmax_pv_vs_unfused(monkeypatch, causal):
     """NEXT f2: scores -> softmax -> PV with the normalisation folded into the PV
