@@ -399,6 +399,8 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fused_kernel(const __grid_con
       ++pv_cnt;
       if (t == 1) {
         // hand the reference to half 0 (its O_1 stays in TMEM until half 0 read it)
+        // racecheck: mbarrier handoff (released by merge_full; the next tile's write
+        // waits on pv_done, which needs the o_free half 0 gives after reading it)
         sm1[r] = m;
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(merge_full);
@@ -412,6 +414,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fused_kernel(const __grid_con
         ptx::mbar_wait(merge_full, merges & 1);
         ++merges;
         ptx::tc_fence_after();
+        // racecheck: mbarrier handoff (acquired by the merge_full wait)
         const float m1 = sm1[r];
         const float mm = fmaxf(m, m1);
         a0 = ptx::ex2(m - mm);
