@@ -291,8 +291,11 @@ void ac_exec_free(ac_exec* e);
  * Inside a region's chunk loop the kernels are programmatic dependent launches
  * (each waits in-kernel for its predecessor; AC_PDL=0 disables), and the chunks
  * of a fused attention chain overlap through per-head epochs kept in a control
- * block at the end of the workspace (AC_OVERLAP=0 disables).  Results do not
- * depend on either, nor on the chunking: chunked == unchunked bitwise.
+ * block at the end of the workspace (AC_OVERLAP=0 disables).  Chunks of other
+ * regions are pipelined over two streams (the caller's and one the exec owns): a
+ * launch of chunk k waits only for the last launch of chunk k - 1 touching the same
+ * workspace bytes (AC_PIPELINE=0 or AC_OVERLAP=0 disables).  Results do not
+ * depend on any of these, nor on the chunking: chunked == unchunked bitwise.
  * Errors: AC_ERR_BIND, AC_ERR_CUDA, AC_ERR_NCCL; AC_ERR_UNSUPPORTED when a kernel
  * cannot take an operand layout (bf16 rows for the tensor-core paths must be
  * multiples of 8 elements, the fused attention kernel needs head dim 64). */
@@ -315,6 +318,7 @@ typedef struct ac_run_stats {
    * work counters, split-K partials, chunk-loop overlap epochs): after the slots */
   int64_t control_bytes;
   int32_t exchanges;             /* collectives issued by the last ac_run (world > 1) */
+  int32_t pipelined_chunks;      /* chunks run on the executor's second stream (chunk pipelining) */
 } ac_run_stats;
 ac_status ac_exec_stats(const ac_exec* e, ac_run_stats* out);
 

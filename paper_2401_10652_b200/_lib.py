@@ -53,7 +53,7 @@ class Tensor(C.Structure):
 class RunStats(C.Structure):
     _fields_ = [("workspace_high_water", C.c_int64), ("planned_peak", C.c_int64), ("caller_bytes", C.c_int64),
                 ("launches", C.c_int32), ("chunks_run", C.c_int32), ("arena_live_peak", C.c_int64),
-                ("control_bytes", C.c_int64), ("exchanges", C.c_int32)]
+                ("control_bytes", C.c_int64), ("exchanges", C.c_int32), ("pipelined_chunks", C.c_int32)]
 
 
 class ExchangeOp(C.Structure):

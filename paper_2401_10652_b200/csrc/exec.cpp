@@ -76,6 +76,7 @@ struct View {
 //   AC_OVERLAP=0        no chunk-loop overlap at all
 //   AC_OVERLAP_CAUSAL=0|1, AC_OVERLAP_TRI=0|1   overlap for causal / triangle chains
 //   AC_PDL=0            no programmatic dependent launches
+//   AC_PIPELINE=0       no chunk pipelining over two streams (AC_OVERLAP=0 implies it)
 struct ExecOptions {
   bool fuse_softmax = true;
   int pv_splitk = -1;
@@ -83,6 +84,7 @@ struct ExecOptions {
   bool overlap_causal = true;
   bool overlap_tri = false;
   bool pdl = true;
+  bool pipeline = true;
 };
 struct ac_exec {
   std::shared_ptr<const Graph> g;
@@ -96,6 +98,16 @@ struct ac_exec {
   RankSchedule sched;                  // this rank's chunks, row-partitioned nodes, exchanges
   cudaStream_t comm_s = nullptr;       // eager region-output gathers (world > 1)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // chunk pipelining (regions without an overlapped f2 chain): chunk k of a region
+  // runs on stream k mod 2 (the caller's, side_s), and a launch of chunk k waits only
+  // for the last launch of chunk k - 1 that touches the same workspace bytes
+  // (pipe_wait), so chunk k's first kernels fill the SMs chunk k - 1's last ones leave
+  cudaStream_t side_s = nullptr;
+  cudaEvent_t ev_pfork = nullptr, ev_pjoin = nullptr;
+  std::vector<cudaEvent_t> ev_pipe;    // [2][nodes]: after node j of chunks of parity p
+  std::vector<int> pipe_wait;          // per node: node of the previous chunk to wait for (-1 none)
+  std::vector<char> pipe_rec;          // per node: some node of the next chunk waits for it
+  std::vector<char> pipe_region;       // per region: pipelined
   DT dt = DT::BF16;
   std::vector<int> region_of;          // node -> region index or -1
   std::vector<char> causal_fast;       // per node: member of an aligned causal chain
@@ -117,6 +129,10 @@ struct ac_exec {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (comm_s) cudaStreamDestroy(comm_s);
+    for (auto ev : ev_pipe) cudaEventDestroy(ev);
+    if (ev_pfork) cudaEventDestroy(ev_pfork);
+    if (ev_pjoin) cudaEventDestroy(ev_pjoin);
+    if (side_s) cudaStreamDestroy(side_s);
   }
 };
 
@@ -135,6 +151,7 @@ ExecOptions read_options() {
   r.overlap = flag("AC_OVERLAP", 1) != 0;
   r.overlap_causal = flag("AC_OVERLAP_CAUSAL", 1) != 0;
   r.overlap_tri = flag("AC_OVERLAP_TRI", 0) != 0;
+  r.pipeline = r.overlap && flag("AC_PIPELINE", 1) != 0;
   r.pdl = flag("AC_PDL", 1) != 0;
   return r;
 }
@@ -940,6 +957,75 @@ ac_status ac_plan_rank_schedule(const ac_chunk_plan* p, int32_t rank, int32_t wo
   return AC_OK;
 }
 
+// Chunk pipelining (ac_exec::pipe_*).  A launch's workspace accesses are byte ranges:
+// the slots of the region's interior tensors (the chunk scratch every chunk reuses,
+// and the whole tensors of off-flow nodes recomputed per chunk), for an f2 chain the
+// S / P slots and its control area; Y^c slices of different chunks are disjoint and
+// region inputs / hoisted tensors are only read, so neither orders chunks.  Node j of
+// chunk k waits for the last node i of chunk k - 1 with a write of one overlapping a
+// read or write of the other; chunk k - 2 precedes it on its own stream.
+void plan_pipelining(ac_exec* e) {
+  const Graph& g = *e->g;
+  const int S = static_cast<int>(g.nodes.size());
+  e->pipe_wait.assign(S, -1);
+  e->pipe_rec.assign(S, 0);
+  e->pipe_region.assign(e->plan.regions.size(), 0);
+  if (!e->opt.pipeline) return;
+  using Rng = std::pair<int64_t, int64_t>;
+  struct Acc {
+    std::vector<Rng> rd, wr;
+  };
+  auto overlaps = [](const std::vector<Rng>& a, const std::vector<Rng>& b) {
+    for (const Rng& x : a)
+      for (const Rng& y : b)
+        if (x.first < y.second && y.first < x.second) return true;
+    return false;
+  };
+  for (size_t r = 0; r < e->plan.regions.size(); ++r) {
+    const Region& R = e->plan.regions[r];
+    if (R.n <= 1) continue;
+    bool ctrl = false;
+    for (int j = R.start; j <= R.end; ++j) ctrl = ctrl || e->arena.ctrl_off[j] >= 0;
+    if (ctrl) continue;  // the f2 chain overlap orders these chunks itself (one stream)
+    std::set<int> hs(R.hoisted.begin(), R.hoisted.end());
+    std::set<int> ycs;
+    for (auto& y : R.yc) ycs.insert(y.first);
+    std::vector<char> produced(g.tensors.size(), 0);
+    for (int j = R.start; j <= R.end; ++j)
+      if (!hs.count(j)) produced[g.nodes[j].output] = 1;
+    auto add = [&](int t, std::vector<Rng>& v) {
+      if (ycs.count(t) || !produced[t]) return;  // chunk-disjoint slices / read-only here
+      const ArenaSlot& sl = e->arena.slot[t];
+      if (sl.offset >= 0) v.push_back({sl.offset, sl.offset + std::max<int64_t>(sl.bytes, 1)});
+      else v.push_back({-16 * (t + 1), -16 * (t + 1) + 1});  // a caller tensor written whole
+    };
+    std::vector<int> ord;
+    std::vector<Acc> acc(S);
+    for (int j = R.start; j <= R.end; ++j) {
+      if (hs.count(j) || e->fuse_role[j] == 2) continue;
+      ord.push_back(j);
+      const Node& n = g.nodes[j];
+      for (int t : n.inputs) add(t, acc[j].rd);
+      add(n.output, acc[j].wr);
+      if (e->fuse_head[j] >= 0) {  // the chain's S / P slots and control area
+        add(e->fuse_s[j], acc[j].wr);
+        add(e->fuse_p[j], acc[j].wr);
+        const int64_t fo = e->arena.f2_off[e->fuse_head[j]];
+        if (fo >= 0) acc[j].wr.push_back({fo, fo + 1});
+      }
+    }
+    if (ord.size() < 2) continue;
+    for (int j : ord) {
+      for (int i : ord)
+        if (overlaps(acc[i].wr, acc[j].rd) || overlaps(acc[i].wr, acc[j].wr) || overlaps(acc[i].rd, acc[j].wr))
+          e->pipe_wait[j] = i;  // the last one in launch order
+      if (e->pipe_wait[j] >= 0) e->pipe_rec[e->pipe_wait[j]] = 1;
+    }
+    // worth a second stream only if chunk k can start before chunk k - 1 ends
+    e->pipe_region[r] = e->pipe_wait[ord[0]] != ord.back() ? 1 : 0;
+  }
+}
+
 ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_bytes, const ac_comm* comm,
                          ac_exec** out) {
   if (!plan || !out) return set_error(AC_ERR_ARG, "ac_exec_create: NULL argument");
@@ -1052,6 +1138,19 @@ ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_
         e->fuse_malloc[node] = sh[sh.size() - 2];
       }
     }
+  }
+  plan_pipelining(e.get());
+  bool any_pipe = false;
+  for (char p : e->pipe_region) any_pipe = any_pipe || p;
+  if (any_pipe) {
+    if (cudaStreamCreateWithFlags(&e->side_s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_pfork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_pjoin, cudaEventDisableTiming) != cudaSuccess)
+      return set_error(AC_ERR_CUDA, "chunk pipelining stream / events");
+    e->ev_pipe.assign(2 * S, nullptr);
+    for (int k = 0; k < 2 * S; ++k)
+      if (e->pipe_rec[k % S] && cudaEventCreateWithFlags(&e->ev_pipe[k], cudaEventDisableTiming) != cudaSuccess)
+        return set_error(AC_ERR_CUDA, "chunk pipelining events");
   }
   *out = e.release();
   return AC_OK;
@@ -1300,11 +1399,33 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
     bool forked = false;
     bool first_launch = true;
     const bool loop_pdl = e->opt.pdl;
+    // chunk pipelining: odd chunks on the side stream (not while timing launches)
+    const bool pipe = e->pipe_region[r] && !e->profiling && sh.chunks.size() > 1;
+    bool side_fresh = true;  // no kernel of this region on the side stream yet
+    if (pipe && (cudaEventRecord(e->ev_pfork, s) != cudaSuccess || cudaStreamWaitEvent(e->side_s, e->ev_pfork, 0) != cudaSuccess))
+      return set_error(AC_ERR_CUDA, "fork to the chunk pipelining stream");
     for (size_t ci = 0; ci < sh.chunks.size(); ++ci) {
       const int64_t c = sh.chunks[ci];
       const int64_t off = c * L;
       const int64_t len = std::min(L, R.extent - off);
       if (len <= 0) break;
+      cudaStream_t cs = pipe && (ci & 1) ? e->side_s : s;
+      if (pipe && (ci & 1)) e->stats.pipelined_chunks += 1;
+      // before node j of this chunk: the previous chunk's conflicting launch; after it:
+      // the event the next chunk may wait for.  A launch behind a cross-stream wait is
+      // not a programmatic dependent launch.
+      auto pipe_pre = [&](int j) -> ac_status {
+        if (!pipe || ci == 0 || e->pipe_wait[j] < 0) return AC_OK;
+        if (cudaStreamWaitEvent(cs, e->ev_pipe[((ci - 1) & 1) * S + e->pipe_wait[j]], 0) != cudaSuccess)
+          return set_error(AC_ERR_CUDA, "chunk pipelining wait");
+        return AC_OK;
+      };
+      auto pipe_post = [&](int j) -> ac_status {
+        if (!pipe || !e->pipe_rec[j]) return AC_OK;
+        if (cudaEventRecord(e->ev_pipe[(ci & 1) * S + j], cs) != cudaSuccess)
+          return set_error(AC_ERR_CUDA, "chunk pipelining record");
+        return AC_OK;
+      };
       std::vector<View> V = full;
       for (auto& fd : R.dims) {
         const int t = fd.first, d = fd.second;
@@ -1330,7 +1451,9 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
           NodeCtx cx;
           cx.fast = e->causal_fast[j] != 0;
           first_launch = false;
-          ac_status st = launch_node(e, j, full, cx, s);
+          ac_status st = pipe_pre(j);
+          if (st == AC_OK) st = launch_node(e, j, full, cx, cs);
+          if (st == AC_OK) st = pipe_post(j);
           if (st != AC_OK) return st;
           continue;
         }
@@ -1361,9 +1484,13 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
             e->fuse_role[j] != 1)
           cx.pdl = 0;
         first_launch = false;
+        if (pipe && ((ci > 0 && e->pipe_wait[j] >= 0) || (cs == e->side_s && side_fresh))) cx.pdl = 0;
+        if (cs == e->side_s) side_fresh = false;
         const int d = R.dim_of(nj.output);
         if (d >= 0 && d == e->chain_rows_dim[j]) cx.row_off = off;
-        ac_status st = launch_node(e, j, *use, cx, s);
+        ac_status st = pipe_pre(j);
+        if (st == AC_OK) st = launch_node(e, j, *use, cx, cs);
+        if (st == AC_OK) st = pipe_post(j);
         if (st != AC_OK) return st;
       }
       e->stats.chunks_run += 1;
@@ -1376,8 +1503,11 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
         for (const XOp* x : eager)
           if (x->group == c / sh.group) xs.push_back(x);
         if (!xs.empty()) {
-          if (cudaEventRecord(e->ev_fork, s) != cudaSuccess ||
-              cudaStreamWaitEvent(e->comm_s, e->ev_fork, 0) != cudaSuccess)
+          // (pipelined: the group's chunks ran on both streams)
+          if (cudaEventRecord(e->ev_fork, cs) != cudaSuccess ||
+              cudaStreamWaitEvent(e->comm_s, e->ev_fork, 0) != cudaSuccess ||
+              (pipe && (cudaEventRecord(e->ev_pjoin, cs == s ? e->side_s : s) != cudaSuccess ||
+                        cudaStreamWaitEvent(e->comm_s, e->ev_pjoin, 0) != cudaSuccess)))
             return set_error(AC_ERR_CUDA, "fork to the communication stream");
           ac_status st = issue_list(xs, e->comm_s);
           if (st != AC_OK) return st;
@@ -1385,6 +1515,11 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
           forked = true;
         }
       }
+    }
+    if (pipe) {
+      if (cudaEventRecord(e->ev_pjoin, e->side_s) != cudaSuccess || cudaStreamWaitEvent(s, e->ev_pjoin, 0) != cudaSuccess)
+        return set_error(AC_ERR_CUDA, "join of the chunk pipelining stream");
+      prev_kernel = 0;
     }
     if (forked) {
       if (cudaEventRecord(e->ev_join, e->comm_s) != cudaSuccess || cudaStreamWaitEvent(s, e->ev_join, 0) != cudaSuccess)

@@ -24,6 +24,9 @@ CASES = {
                   "region s=proj_q e=ffn2 n=4 dims=0\n"),
     "evo": (lambda: workloads.evoformer_pair(128, 64, 2, 32, "bf16", name="mg_evo", cm=64, nf=2),
             "region s=row_scores e=row_pv n=4 dims=0\nregion s=col_scores e=col_pv n=4 dims=1\n"),
+    # f1 region: chunks pipelined over two streams, region outputs gathered eagerly
+    "gpt_fa": (lambda: workloads.block("transformer_fa", 2048, 256, 4, 1024, True, "bf16", name="mg_fa"),
+               "region s=attn e=ffn2 n=8 dims=0\n"),
     "ragged": (lambda: workloads.transformer(896, 256, 4, 512, False, "bf16", name="mg_rag"),
                "region s=scores e=pv n=3 dims=0\n"),
 }

@@ -360,6 +360,72 @@ def test_fused_attention_regime_plan():
     assert gu.rel_err(got["y"][torch.from_numpy(rows).cuda()], ref["y"]) < 2e-2
 
 
+PIPE_CASES = {
+    # f1 region: chunk k's attention runs beside chunk k-1's FFN (only the o / h
+    # scratch orders them)
+    "gpt_fa": (lambda: workloads.block("transformer_fa", 2048, 256, 4, 1024, True, "bf16", name="pipe_fa"),
+               "autochunk-plan 1\nregion s=attn e=ffn2 n=4 dims=0\n", True),
+    # whole block with its causal f2 chain run without the chunk-loop overlap
+    "gpt_block": (lambda: workloads.transformer(1024, 256, 4, 512, True, "bf16", name="pipe_blk"),
+                  "autochunk-plan 1\nregion s=proj_q e=ffn2 n=4 dims=0\n", None),
+    # triangle attention pair (the triangle chains run without the overlap by default)
+    "af": (lambda: workloads.tri_attn_pair(192, 128, 4, 32, "bf16", name="pipe_af"),
+           "autochunk-plan 1\nregion s=row_scores e=row_pv n=4 dims=1\nregion s=col_scores e=col_pv n=6 dims=0\n",
+           None),
+    # ragged FFN region, odd chunk count
+    "ffn_ragged": (lambda: workloads.block("transformer_fa", 1024 + 96, 256, 4, 1024, True, "bf16", name="pipe_rag"),
+                   "autochunk-plan 1\nregion s=ln2 e=ffn2 n=5 dims=0\n", True),
+}
+
+
+@pytest.mark.parametrize("name", list(PIPE_CASES))
+def test_chunk_pipelining(monkeypatch, name):
+    """Chunk pipelining over two streams (chunk k waits only for the launches of chunk
+    k-1 that touch the same workspace bytes): bitwise equal to the same plan run on
+    one stream (AC_PIPELINE=0), to the unchunked run, also under CUDA graph capture,
+    and the f1 / FFN regions really run their odd chunks on the second stream."""
+    gu = _gu()
+    from paper_2401_10652_b200 import api
+    mk, txt, expect = PIPE_CASES[name]
+    og = mk()
+    cg = gu.c_graph(og)
+    plan = api.plan_parse(cg, txt)
+    _, dev = gu.make_values(og, 11)
+    base, _ = gu.run(cg, gu.empty_plan(cg), og, dev)
+    got, ex = gu.run(cg, plan, og, dev)
+    torch.cuda.synchronize()
+    st = ex.stats()
+    if expect:
+        assert st.pipelined_chunks > 0
+    monkeypatch.setenv("AC_PIPELINE", "0")
+    one, ex1 = gu.run(cg, plan, og, dev)
+    torch.cuda.synchronize()
+    assert ex1.stats().pipelined_chunks == 0
+    monkeypatch.delenv("AC_PIPELINE")
+    for o in og.outputs:
+        assert torch.equal(got[o], one[o]), (name, o)
+        if not torch.equal(got[o], base[o]):
+            assert torch.equal(got[o], _unfused_base(cg, og, dev)[o]), (name, o)
+    # captured: the side stream joins the capture through the fork event
+    ws = torch.empty(max(plan.workspace_bytes(), 16), dtype=torch.uint8, device="cuda")
+    exg = api.Exec(plan, ws)
+    outs = {o: torch.full_like(got[o], float("nan")) for o in og.outputs}
+    ins = {t: dev[t] for t in og.inputs + og.weights}
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    exg.run(ins, outs, s)                     # warm-up (module loads) outside the capture
+    s.synchronize()
+    for o in outs:
+        outs[o].fill_(float("nan"))
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        exg.run(ins, outs, s)
+    graph.replay()
+    torch.cuda.synchronize()
+    for o in og.outputs:
+        assert torch.equal(outs[o], got[o]), (name, "graph", o)
+
+
 def test_af_chunk_overlap_opt_in(monkeypatch):
     """The chunk-loop overlap on the triangle chains (AC_OVERLAP_TRI=1: paired
     short-chunk scores with dynamic tiles waiting on per-batch epochs of the previous
