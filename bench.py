@@ -556,7 +556,10 @@ def main():
         args.budget_frac = DEFAULT_BUDGET.get(args.config, 0.2)
     budget = int(args.budget_frac * prof0.peak_bytes)
     if args.plan:
-        plan = api.plan_parse(cg, args.plan)
+        # full plan text, or region lines separated by ';' (header added)
+        txt = args.plan if args.plan.startswith("autochunk-plan") else \
+            "autochunk-plan 1\n" + "".join(r.strip() + "\n" for r in args.plan.split(";") if r.strip())
+        plan = api.plan_parse(cg, txt)
     elif args.config == "tiny":
         plan = api.plan_parse(cg, "autochunk-plan 1\nregion s=scores e=pv n=8 dims=0\n")
     else:

@@ -322,6 +322,18 @@ typedef struct ac_run_stats {
 } ac_run_stats;
 ac_status ac_exec_stats(const ac_exec* e, ac_run_stats* out);
 
+/* Chunk pipelining of a plan (host only, no CUDA calls): what ac_run does with the
+ * chunk loops of `plan` under the current AC_* switches.  wait[i] (one per graph
+ * node): the node of chunk k - 1 that node i of chunk k waits for in a pipelined
+ * region (the last launch touching a workspace byte range node i also touches, one
+ * of the two writing it), -1 for none; pipelined[r] (one per region): 1 when region
+ * r's chunks alternate between two streams.  Regions whose f2 chain runs the
+ * chunk-loop overlap (per-head epochs) are never pipelined.  Chunk pipelining is the
+ * executor's scheduling of the paper's chunk loop (chunks are independent
+ * computations; only the reused chunk scratch orders them), not a change of the
+ * memory the estimator charges.  Errors: AC_ERR_ARG, AC_ERR_UNSUPPORTED. */
+ac_status ac_plan_chunk_pipeline(const ac_chunk_plan* plan, int32_t* wait, int32_t* pipelined);
+
 /* Per-stage timing: while profiling is on, ac_run brackets every kernel
  * launch with CUDA events on the run stream (a few microseconds of host time
  * per launch, no device synchronisation).  ac_exec_kernel_times synchronises

@@ -120,6 +120,7 @@ SIGNATURES = [
     ("ac_exec_free", None, [P]),
     ("ac_run", C.c_int, [P, C.POINTER(Tensor), C.c_int32, C.POINTER(Tensor), C.c_int32, P]),
     ("ac_exec_stats", C.c_int, [P, C.POINTER(RunStats)]),
+    ("ac_plan_chunk_pipeline", C.c_int, [P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     ("ac_exec_set_profiling", C.c_int, [P, C.c_int32]),
     ("ac_exec_kernel_times", C.c_int, [P, C.POINTER(KernelTime), C.c_int32, C.POINTER(C.c_int32)]),
     ("ac_kernel_gemm", C.c_int, [C.POINTER(GemmDesc), P]),

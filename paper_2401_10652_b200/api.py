@@ -108,6 +108,15 @@ class Plan:
                                         C.byref(ln), C.byref(ext)))
         return list(arr)[: cnt.value], ne.value, ln.value, ext.value
 
+    def chunk_pipeline(self):
+        """ac_plan_chunk_pipeline: (wait, pipelined) - per node the node of the
+        previous chunk it waits for (-1 none), per region whether its chunks alternate
+        between two streams."""
+        nn, nr = self.graph.num_nodes, self.num_regions
+        w, p = (C.c_int32 * max(nn, 1))(), (C.c_int32 * max(nr, 1))()
+        check(lib().ac_plan_chunk_pipeline(self._h, w, p))
+        return list(w)[:nn], list(p)[:nr]
+
     def rank_schedule(self, rank: int, world: int):
         """ac_plan_rank_schedule: (node_region, node_dim, ops) - per node the region
         share it runs on (-1 whole) and its output dim, and the exchanges as dicts."""

@@ -129,7 +129,8 @@ struct ac_exec {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (comm_s) cudaStreamDestroy(comm_s);
-    for (auto ev : ev_pipe) cudaEventDestroy(ev);
+    for (auto ev : ev_pipe)
+      if (ev) cudaEventDestroy(ev);
     if (ev_pfork) cudaEventDestroy(ev_pfork);
     if (ev_pjoin) cudaEventDestroy(ev_pjoin);
     if (side_s) cudaStreamDestroy(side_s);
@@ -239,7 +240,9 @@ Arena build_arena(const Graph& g, const Plan& plan, const ExecOptions& o, int wo
   for (int o : g.outputs) death[o] = S - 1;
   std::vector<int64_t> bytes(T);
   for (int t = 0; t < T; ++t) bytes[t] = g.tensors[t].bytes();
-  for (const Region& r : plan.regions) {
+  std::vector<std::vector<int>> interior(plan.regions.size());  // chunk scratch tensors per region
+  for (size_t ri = 0; ri < plan.regions.size(); ++ri) {
+    const Region& r = plan.regions[ri];
     if (r.n <= 1) continue;
     std::vector<int> ins, outs;
     region_io(g, r.start, r.end, ins, outs);
@@ -268,6 +271,7 @@ Arena build_arena(const Graph& g, const Plan& plan, const ExecOptions& o, int wo
       for (int c : g.consumers[t])
         if (c >= r.start && c <= r.end) lastc = std::max(lastc, c);
       death[t] = lastc;
+      interior[ri].push_back(t);
     }
   }
   // fused chains (R25): S holds the e-tiles and stays live until the PV reads them;
@@ -313,6 +317,42 @@ Arena build_arena(const Graph& g, const Plan& plan, const ExecOptions& o, int wo
     A.slot[t] = ArenaSlot{off, bytes[t], birth[t], death[t]};
     A.size = std::max(A.size, off + sz);
     placed.push_back(t);
+  }
+  // chunk pipelining (ac_exec::pipe_*) orders chunk k's launch after the last launch of
+  // chunk k - 1 that touches the same bytes: move each chunk scratch tensor, within the
+  // arena size first fit found (so Eq. 1 / 2 bytes and the size are unchanged), to the
+  // offset whose other region scratch occupants die earliest in the chunk (GPT with
+  // fused attention: the attention output shares the LN2 output's bytes, not the FFN
+  // hidden's, so chunk k + 1's attention may run beside chunk k's FFN2)
+  auto rsz = [&](int u) { return (A.slot[u].bytes + 255) / 256 * 256; };
+  for (size_t ri = 0; ri < interior.size(); ++ri) {
+    std::set<int> in_r(interior[ri].begin(), interior[ri].end());
+    for (int t : interior[ri]) {
+      const int64_t sz = rsz(t);
+      auto score = [&](int64_t off) -> int {  // -2: not free at this offset
+        int worst = -1;
+        for (int u : placed) {
+          if (u == t) continue;
+          const bool busy_t = !(death[u] < birth[t] || death[t] < birth[u]);
+          const bool ov = A.slot[u].offset < off + sz && off < A.slot[u].offset + rsz(u);
+          if (!ov) continue;
+          if (busy_t) return -2;
+          if (in_r.count(u)) worst = std::max(worst, death[u]);
+        }
+        return worst;
+      };
+      int64_t best = A.slot[t].offset;
+      int bs = score(best);
+      std::vector<int64_t> cand{0};
+      for (int u : placed) cand.push_back(A.slot[u].offset), cand.push_back(A.slot[u].offset + rsz(u));
+      std::sort(cand.begin(), cand.end());
+      for (int64_t off : cand) {
+        if (off + sz > A.size) continue;
+        const int sc = score(off);
+        if (sc != -2 && sc < bs) best = off, bs = sc;
+      }
+      A.slot[t].offset = best;
+    }
   }
   for (int s = 0; s < S; ++s) {
     int64_t live = 0;
@@ -964,7 +1004,7 @@ ac_status ac_plan_rank_schedule(const ac_chunk_plan* p, int32_t rank, int32_t wo
 // region inputs / hoisted tensors are only read, so neither orders chunks.  Node j of
 // chunk k waits for the last node i of chunk k - 1 with a write of one overlapping a
 // read or write of the other; chunk k - 2 precedes it on its own stream.
-void plan_pipelining(ac_exec* e) {
+static void plan_pipelining(ac_exec* e) {
   const Graph& g = *e->g;
   const int S = static_cast<int>(g.nodes.size());
   e->pipe_wait.assign(S, -1);
@@ -1026,6 +1066,8 @@ void plan_pipelining(ac_exec* e) {
   }
 }
 
+static ac_status exec_analyse(ac_exec* e);
+
 ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_bytes, const ac_comm* comm,
                          ac_exec** out) {
   if (!plan || !out) return set_error(AC_ERR_ARG, "ac_exec_create: NULL argument");
@@ -1046,13 +1088,36 @@ ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_
                                            std::to_string(e->arena.size));
   e->ws = static_cast<char*>(workspace);
   e->ws_bytes = ws_bytes;
-  e->sched = rank_schedule(g, plan->plan, e->rank, e->world);
+  ac_status st = exec_analyse(e.get());
+  if (st != AC_OK) return st;
   if (e->world > 1) {
     if (cudaStreamCreateWithFlags(&e->comm_s, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess)
       return set_error(AC_ERR_CUDA, "communication stream / events");
   }
+  const int S = static_cast<int>(g.nodes.size());
+  bool any_pipe = false;
+  for (char p : e->pipe_region) any_pipe = any_pipe || p;
+  if (any_pipe) {
+    if (cudaStreamCreateWithFlags(&e->side_s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_pfork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_pjoin, cudaEventDisableTiming) != cudaSuccess)
+      return set_error(AC_ERR_CUDA, "chunk pipelining stream / events");
+    e->ev_pipe.assign(2 * S, nullptr);
+    for (int k = 0; k < 2 * S; ++k)
+      if (e->pipe_rec[k % S] && cudaEventCreateWithFlags(&e->ev_pipe[k], cudaEventDisableTiming) != cudaSuccess)
+        return set_error(AC_ERR_CUDA, "chunk pipelining events");
+  }
+  *out = e.release();
+  return AC_OK;
+}
+
+// host half of ac_exec_create (no CUDA calls): the rank schedule, dtype / kernel
+// checks, chain detection, fused f2 chains, chunk pipelining
+static ac_status exec_analyse(ac_exec* e) {
+  const Graph& g = *e->g;
+  e->sched = rank_schedule(g, e->plan, e->rank, e->world);
   // one element type for the whole graph (f32 -> SIMT path, bf16 -> tcgen05 path)
   e->dt = g.tensors.empty() ? DT::BF16 : g.tensors[0].dtype;
   for (auto& t : g.tensors)
@@ -1139,20 +1204,21 @@ ac_status ac_exec_create(const ac_chunk_plan* plan, void* workspace, int64_t ws_
       }
     }
   }
-  plan_pipelining(e.get());
-  bool any_pipe = false;
-  for (char p : e->pipe_region) any_pipe = any_pipe || p;
-  if (any_pipe) {
-    if (cudaStreamCreateWithFlags(&e->side_s, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&e->ev_pfork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&e->ev_pjoin, cudaEventDisableTiming) != cudaSuccess)
-      return set_error(AC_ERR_CUDA, "chunk pipelining stream / events");
-    e->ev_pipe.assign(2 * S, nullptr);
-    for (int k = 0; k < 2 * S; ++k)
-      if (e->pipe_rec[k % S] && cudaEventCreateWithFlags(&e->ev_pipe[k], cudaEventDisableTiming) != cudaSuccess)
-        return set_error(AC_ERR_CUDA, "chunk pipelining events");
-  }
-  *out = e.release();
+  plan_pipelining(e);
+  return AC_OK;
+}
+
+ac_status ac_plan_chunk_pipeline(const ac_chunk_plan* plan, int32_t* wait, int32_t* pipelined) {
+  if (!plan || !wait || !pipelined) return set_error(AC_ERR_ARG, "ac_plan_chunk_pipeline: NULL argument");
+  std::unique_ptr<ac_exec> e(new ac_exec);
+  e->g = plan->g;
+  e->plan = plan->plan;
+  e->opt = read_options();
+  e->arena = build_arena(*e->g, plan->plan, e->opt, 1);
+  ac_status st = exec_analyse(e.get());
+  if (st != AC_OK) return st;
+  for (size_t i = 0; i < e->pipe_wait.size(); ++i) wait[i] = e->pipe_wait[i];
+  for (size_t r = 0; r < e->pipe_region.size(); ++r) pipelined[r] = e->pipe_region[r];
   return AC_OK;
 }
 
