@@ -2,7 +2,7 @@
 # chunk pipelining: GPU tests, then A/B against AC_PIPELINE=0 on the configs it touches
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_multirank.py -x -q \
-  -k "pipelining or fused_attention or af_ or whole_block or gpt_fa or evoformer" > gpurun_out/pipe_pytest.log 2>&1
+  -k "pipelining or fused_attention or af_ or whole_block or gpt_fa or gpt_block or evoformer or graph_capture or planned_peak or stacked" > gpurun_out/pipe_pytest.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pipe_pytest.log
 : > gpurun_out/pipe_ab.txt
 for C in gpt_fa gpt_fa_ffn gpt_block; do
