@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--budget-frac", type=float, default=None,
                     help="activation budget as a fraction of the unchunked peak (default 0.2; gpt_fa 0.9)")
     ap.add_argument("--plan", default=None, help="user plan text (ac_plan_parse) instead of ac_plan")
+    ap.add_argument("--normalize", action="store_true",
+                    help="ac_plan with normalised cost features and unit weights (AC_FLAG_NORMALIZE, R27)")
     ap.add_argument("--no-unchunked", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -562,6 +564,10 @@ def main():
         plan = api.plan_parse(cg, txt)
     elif args.config == "tiny":
         plan = api.plan_parse(cg, "autochunk-plan 1\nregion s=scores e=pv n=8 dims=0\n")
+    elif args.normalize:
+        from paper_2401_10652_b200 import _lib as L
+        plan = api.ac_plan(cg, budget, api.cost_params(flags=L.AC_FLAG_NORMALIZE, alpha=1.0, beta=1.0,
+                                                       gamma=-1.0, lam=1.0))
     else:
         plan = api.ac_plan(cg, budget)
     profp, _ = api.estimate_memory(cg, plan)
@@ -904,6 +910,8 @@ def main():
                    "plan": regions, "parallelism": f"chunk-split x{world}" + (
                        " (zigzag / round-robin chunk shares, row-partitioned post-region nodes, NCCL all-gather)"
                        if world > 1 else ""),
+                   **({"cost": "normalised features, unit weights (AC_FLAG_NORMALIZE, R27)"} if args.normalize else {}),
+                   "pipelined_chunks": st.pipelined_chunks,
                    "l2": "flushed between timed steps (256 MiB write)",
                    "launch": "one ac_run captured as a CUDA graph, replayed per step" if use_graph else
                              "direct ac_run launches"},

@@ -127,7 +127,13 @@ enum {
   AC_FLAG_NO_STRIDE = 1 << 2,    /* "No dimension strides" */
   AC_FLAG_NO_NODES = 1 << 3,     /* "No number of nodes" */
   AC_FLAG_NO_FLOPS = 1 << 4,     /* "No flops" */
-  AC_FLAG_CONTIGUITY = 1 << 5    /* charge SPEC contiguity copies */
+  AC_FLAG_CONTIGUITY = 1 << 5,   /* charge SPEC contiguity copies */
+  /* normalised cost features (R27; off by default): Eq. 8/9 with N_node / S_g,
+   * N_flop / F_g, N_density / (F_g / S_g) and N_stride / numel(largest flow tensor),
+   * S_g = the graph's compute nodes, F_g = their FLOPs; meant for O(1) weights
+   * (e.g. alpha = beta = lambda = 1, gamma = -1), where the raw SPEC-scaled features
+   * let the density term swamp the others (SURVEY c.2 #10) */
+  AC_FLAG_NORMALIZE = 1 << 6
 };
 
 /* Cost model Eq. 8-10 and search/selection knobs. */

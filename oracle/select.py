@@ -7,6 +7,10 @@
   with beam search over passes; each pass re-estimates memory, finds the new
   peak node and runs the chunk search (the pass loop of P:153).
 Readings (DESIGN.md R8-R12): gamma < 0, lambda > 0 (SPEC defaults S:368);
+optional normalised features (R27, off by default, SURVEY c.2 #10): N_node / S_g,
+N_flop / F_g, N_density / (F_g / S_g), N_stride / numel(largest flow tensor), with
+S_g the graph's compute nodes and F_g their FLOPs, so that O(1) weights compare
+terms of the same scale (the paper tunes its weights, P:336);
 N_node / N_flop count the nodes executed per chunk (hoisted nodes run once);
 N_stride is the row-major stride of the chunk dim of the largest flow tensor
 (first in BFS order on ties); DP key = sorted set of region intervals; beam 4;
@@ -38,6 +42,7 @@ class CostParams:
     use_density: bool = True
     use_stride: bool = True
     allowed_dims: tuple = None
+    normalize: bool = False
 
 
 def macro_cost(n_node: int, n_flop: int, p: CostParams) -> float:
@@ -52,6 +57,12 @@ def micro_cost(density: float, stride: int, p: CostParams) -> float:
     return c * density + l * float(stride)
 
 
+def graph_scales(g: Graph):
+    """(S_g, F_g) of the normalised features: compute nodes and their FLOPs (>= 1)."""
+    nodes = [i for i, n in enumerate(g.nodes) if n.kind not in ("input", "weight")]
+    return max(len(nodes), 1), max(sum(g.flops(i) for i in nodes), 1)
+
+
 def region_cost(g: Graph, r: Region, p: CostParams) -> Cost:
     hs = set(r.hoisted)
     nodes = [i for i in range(r.start, r.end + 1) if i not in hs]
@@ -64,6 +75,18 @@ def region_cost(g: Graph, r: Region, p: CostParams) -> Cost:
         if b > bigb:
             big, bigb = t, b
     stride = g.tensors[big].strides[r.dims[big]]
+    if p.normalize:
+        sg, fg = graph_scales(g)
+        numel = 1
+        for e in g.tensors[big].shape:
+            numel *= e
+        a = p.alpha if p.use_node else 0.0
+        b = p.beta if p.use_flop else 0.0
+        c = p.gamma if p.use_density else 0.0
+        lm = p.lam if p.use_stride else 0.0
+        ma = a * (float(n_node) / float(sg)) + b * (float(n_flop) / float(fg))
+        mi = c * (density / (float(fg) / float(sg))) + lm * (float(stride) / float(numel))
+        return Cost(n_node, n_flop, density, stride, ma, mi, ma + mi)
     ma = macro_cost(n_node, n_flop, p)
     mi = micro_cost(density, stride, p)
     return Cost(n_node, n_flop, density, stride, ma, mi, ma + mi)

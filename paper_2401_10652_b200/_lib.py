@@ -19,7 +19,7 @@ AC_F32, AC_BF16, AC_F64 = 0, 1, 2
 AC_BLOCK_TRANSFORMER, AC_BLOCK_ATTN_ONLY, AC_BLOCK_TRI_ATTN_PAIR = 0, 1, 2
 AC_BLOCK_TRANSFORMER_FA, AC_BLOCK_ATTN_ONLY_FA, AC_BLOCK_EVOFORMER_PAIR = 3, 4, 5
 AC_FLAG_NO_HOIST, AC_FLAG_NO_DENSITY, AC_FLAG_NO_STRIDE, AC_FLAG_NO_NODES, AC_FLAG_NO_FLOPS, \
-    AC_FLAG_CONTIGUITY = 1, 2, 4, 8, 16, 32
+    AC_FLAG_CONTIGUITY, AC_FLAG_NORMALIZE = 1, 2, 4, 8, 16, 32, 64
 
 
 class ACError(RuntimeError):

@@ -39,6 +39,7 @@ Params to_params(const ac_cost_params* cp) {
   p.use_node = !(cp->flags & AC_FLAG_NO_NODES);
   p.use_flop = !(cp->flags & AC_FLAG_NO_FLOPS);
   p.contiguity = (cp->flags & AC_FLAG_CONTIGUITY) != 0;
+  p.normalize = (cp->flags & AC_FLAG_NORMALIZE) != 0;
   p.allowed_mask = cp->allowed_dims_mask;
   return p;
 }

@@ -128,6 +128,7 @@ struct Params {
   int64_t max_chunks = 4096;
   bool hoist = true, contiguity = false;
   bool use_node = true, use_flop = true, use_density = true, use_stride = true;
+  bool normalize = false;  // AC_FLAG_NORMALIZE (R27)
   uint32_t allowed_mask = 0;
 };
 

@@ -591,6 +591,25 @@ Cost region_cost(const Graph& g, const Region& r, const Params& p) {
   const double b = p.use_flop ? p.beta : 0.0;
   const double gm = p.use_density ? p.gamma : 0.0;
   const double l = p.use_stride ? p.lam : 0.0;
+  if (p.normalize) {
+    // normalised features (R27, AC_FLAG_NORMALIZE): N_node / S_g, N_flop / F_g,
+    // N_density / (F_g / S_g), N_stride / numel(largest flow tensor)
+    int64_t sg = 0, fg = 0;
+    for (int i = 0; i < static_cast<int>(g.nodes.size()); ++i) {
+      if (g.nodes[i].source()) continue;
+      sg += 1;
+      fg += g.flops(i);
+    }
+    sg = std::max<int64_t>(sg, 1);
+    fg = std::max<int64_t>(fg, 1);
+    int64_t numel = 1;
+    for (int64_t e : g.tensors[big].shape) numel *= e;
+    const double dsg = static_cast<double>(sg), dfg = static_cast<double>(fg);
+    c.macro = a * (static_cast<double>(c.n_node) / dsg) + b * (static_cast<double>(c.n_flop) / dfg);
+    c.micro = gm * (c.density / (dfg / dsg)) + l * (static_cast<double>(c.stride) / static_cast<double>(numel));
+    c.total = c.macro + c.micro;
+    return c;
+  }
   c.macro = a * static_cast<double>(c.n_node) + b * static_cast<double>(c.n_flop);
   c.micro = gm * c.density + l * static_cast<double>(c.stride);
   c.total = c.macro + c.micro;

@@ -81,7 +81,9 @@ def test_corpus_plans_bit_exact(frac):
         budget = int(frac * memory.profile(g).peak_bytes)
         for kw, prm in [({}, select.CostParams()), ({"beam": 16}, select.CostParams(beam=16)),
                         ({"flags": _lib.AC_FLAG_NO_HOIST}, select.CostParams(hoist=False)),
-                        ({"flags": _lib.AC_FLAG_CONTIGUITY}, select.CostParams(contiguity=True))]:
+                        ({"flags": _lib.AC_FLAG_CONTIGUITY}, select.CostParams(contiguity=True)),
+                        ({"flags": _lib.AC_FLAG_NORMALIZE, "alpha": 1.0, "beta": 1.0, "gamma": -1.0, "lam": 1.0},
+                         select.CostParams(normalize=True, alpha=1.0, beta=1.0, gamma=-1.0, lam=1.0))]:
             ref = select.select(g, budget, prm)
             got = api.ac_plan(cg, budget, api.cost_params(**kw))
             assert got.serialize() == oplan.serialize(ref, g), (name, kw)
@@ -302,3 +304,15 @@ def test_arena_equals_planned_per_step(case):
         tot.append(live[s_] + caller)
     assert max(tot) == prof.peak_bytes and max(live) == peak
     assert plan.workspace_bytes() - ctl == peak   # size-ordered first fit: no holes at the peak
+
+
+@pytest.mark.parametrize("name,frac", [("gpt_fa", 0.9), ("gpt", 0.2), ("af", 0.2), ("tiny", 0.5)])
+def test_normalized_plans_bit_exact(name, frac):
+    """AC_FLAG_NORMALIZE (R27): the C++ planner and the oracle agree byte for byte
+    (plan text incl. every cost term) at the configs' sizes."""
+    og_g = workloads.config(name)
+    budget = int(frac * memory.profile(og_g).peak_bytes)
+    ref = select.select(og_g, budget, select.CostParams(normalize=True, alpha=1.0, beta=1.0, gamma=-1.0, lam=1.0))
+    got = api.ac_plan(_c_graph(name), budget, api.cost_params(flags=_lib.AC_FLAG_NORMALIZE, alpha=1.0, beta=1.0,
+                                                               gamma=-1.0, lam=1.0))
+    assert got.serialize() == oplan.serialize(ref, og_g)

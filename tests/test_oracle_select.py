@@ -136,3 +136,41 @@ def test_expected_plan_tiny_infeasible():
     g, base, p = _plan("tiny")
     assert not p.feasible and p.regions                         # AC_ERR_BUDGET + best effort
     assert 0.25 < p.peak / base.peak_bytes < 0.3                # floor ~28 %
+
+
+def test_normalized_features_closed_forms():
+    """R27 normalised features (AC_FLAG_NORMALIZE, SURVEY c.2 #10): a region holding
+    every compute node of the graph (nothing hoisted) has N_node / S_g = 1,
+    N_flop / F_g = 1 and N_density / (F_g / S_g) = 1 exactly, and a row-chunked
+    [N, *] flow tensor has N_stride / numel = 1 / N."""
+    g = workloads.corpus("mlp", 32, 8, "f32")
+    spec = [("n_h1", "n_y", 4, (0,), False)]
+    def cost(**kw):
+        p = select.CostParams(normalize=True, **kw)
+        (r,) = select.user_plan(g, spec, p).regions
+        assert r.hoisted == [] or list(r.hoisted) == []
+        return r.cost
+    assert cost(alpha=1.0, beta=0.0, gamma=0.0, lam=0.0).macro == 1.0
+    assert cost(alpha=0.0, beta=1.0, gamma=0.0, lam=0.0).macro == 1.0
+    assert cost(alpha=0.0, beta=0.0, gamma=-1.0, lam=0.0).micro == -1.0
+    assert cost(alpha=0.0, beta=0.0, gamma=0.0, lam=1.0).micro == 1.0 / 32
+    # the raw features are the same numbers either way
+    raw = select.user_plan(g, spec).regions[0].cost
+    nrm = cost(alpha=1.0, beta=1.0, gamma=-1.0, lam=1.0)
+    assert (raw.n_node, raw.n_flop, raw.density, raw.stride) == (nrm.n_node, nrm.n_flop, nrm.density, nrm.stride)
+    # Table-1 toggles still zero their terms
+    p = select.CostParams(normalize=True, alpha=1.0, beta=1.0, gamma=-1.0, lam=1.0, use_node=False,
+                          use_flop=False, use_density=False, use_stride=False)
+    assert select.user_plan(g, spec, p).regions[0].cost.total == 0.0
+
+
+def test_normalized_features_pick_the_ffn_region_for_fused_attention():
+    """GPT with fused attention (NEXT f1) at 90 % of its unchunked peak: the raw SPEC
+    features choose the attention-including region (the density term, ~1e6, swamps
+    the others); normalised features with unit weights choose an FFN-only region."""
+    g = workloads.config("gpt_fa")
+    budget = int(0.9 * memory.profile(g).peak_bytes)
+    raw = select.select(g, budget)
+    assert [g.nodes[r.start].id for r in raw.regions] == ["attn"]
+    nrm = select.select(g, budget, select.CostParams(normalize=True, alpha=1.0, beta=1.0, gamma=-1.0, lam=1.0))
+    assert nrm.feasible and all(g.nodes[r.start].id in ("ln2", "ffn1") for r in nrm.regions)
