@@ -1176,6 +1176,7 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
             uint32_t pk[16];
             if (lim >= hh * 32 + 31) {
               const uint64_t cl2 = ptx::f32x2_splat(cl), nm2 = ptx::f32x2_splat(-mref);
+              uint64_t sp = f2_pack(s0, s1);  // (s0, s1) summed as one FADD2 per pair: same rounding
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
                 float x0, x1;
@@ -1187,11 +1188,11 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
                 }
                 const float e0 = ptx::ex2(x0);
                 const float e1 = ptx::ex2(x1);
-                s0 += e0;
-                s1 += e1;
+                sp = f2_add(sp, f2_pack(e0, e1));
                 __nv_bfloat162 h = __floats2bfloat162_rn(e0, e1);
                 pk[j] = *reinterpret_cast<uint32_t*>(&h);
               }
+              f2_unpack(sp, s0, s1);
             } else {
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
