@@ -18,6 +18,7 @@
 //   tensor is needed whole, region outputs group by group on a communication
 //   stream while the chunk loop goes on.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstring>
@@ -140,6 +141,16 @@ struct ac_exec {
 namespace {
 
 bool is_caller(const Graph& g, int t) { return g.is_input[t] || g.is_weight[t] || g.is_output[t]; }
+
+// NVTX ranges (SURVEY §5 tracing): "ac_run", "region <k> <start>..<end> n=<n>",
+// "chunk <c>" - host-side markers (no-ops without a tool attached) that let
+// `ncu --nvtx --nvtx-include "region 0/chunk 3/"` capture one chunk's kernels
+struct NvtxRange {
+  explicit NvtxRange(const std::string& name) { nvtxRangePushA(name.c_str()); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 ExecOptions read_options() {
   ExecOptions r;
@@ -1270,6 +1281,7 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
   if (!e) return set_error(AC_ERR_ARG, "ac_run: NULL exec");
   const Graph& g = *e->g;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  NvtxRange nv_run("ac_run");
   const int T = static_cast<int>(g.tensors.size());
   const int esz = dt_size(e->dt);
   std::vector<View> full(T);
@@ -1438,6 +1450,8 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
     }
     const Region& R = e->plan.regions[r];
     const RegionShare& sh = rs.reg[r];
+    NvtxRange nv_region("region " + std::to_string(r) + " " + g.nodes[R.start].id + ".." + g.nodes[R.end].id +
+                        " n=" + std::to_string(R.n));
     for (int h : R.hoisted) {
       NodeCtx cx;
       cx.fast = e->causal_fast[h] != 0;
@@ -1476,6 +1490,7 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
       const int64_t len = std::min(L, R.extent - off);
       if (len <= 0) break;
       cudaStream_t cs = pipe && (ci & 1) ? e->side_s : s;
+      NvtxRange nv_chunk("chunk " + std::to_string(c));
       if (pipe && (ci & 1)) e->stats.pipelined_chunks += 1;
       // before node j of this chunk: the previous chunk's conflicting launch; after it:
       // the event the next chunk may wait for.  A launch behind a cross-stream wait is
