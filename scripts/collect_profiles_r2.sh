@@ -2,7 +2,7 @@
 # Copy the outputs of scripts/profile_r2.sh (gpurun_out/r2p_*) into profiles/ (round 2).
 set -e
 cd "$(dirname "$0")/.."
-for c in gpt unet vit af af_attn gpt_fa tiny gpt_l4; do
+for c in gpt unet vit af af_attn gpt_fa gpt_fa_norm tiny gpt_l4; do
   grep -h "^{" gpurun_out/r2p_bench_$c.json | python -c "
 import json,sys
 for l in sys.stdin:

@@ -6,6 +6,7 @@ for C in gpt unet vit af af_attn gpt_fa tiny; do
   timeout 900 python bench.py --config $C --steps 20 --warmup 5 > gpurun_out/r2p_bench_$C.json 2> gpurun_out/r2p_bench_$C.err
 done
 timeout 600 python bench.py --config gpt --layers 4 --no-cpu --no-e2e > gpurun_out/r2p_bench_gpt_l4.json 2> gpurun_out/r2p_l4.err
+timeout 600 python bench.py --config gpt_fa --normalize --steps 20 --warmup 5 > gpurun_out/r2p_bench_gpt_fa_norm.json 2> gpurun_out/r2p_fa_norm.err
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/r2p_reference.json 2> gpurun_out/r2p_reference.err
 for C in gpt unet af gpt_fa; do
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
