@@ -316,3 +316,31 @@ def test_normalized_plans_bit_exact(name, frac):
     got = api.ac_plan(_c_graph(name), budget, api.cost_params(flags=_lib.AC_FLAG_NORMALIZE, alpha=1.0, beta=1.0,
                                                                gamma=-1.0, lam=1.0))
     assert got.serialize() == oplan.serialize(ref, og_g)
+
+
+def test_chunk_pipeline_schedule(monkeypatch):
+    """ac_plan_chunk_pipeline (host only): the fused-attention block's region
+    [attn ... ffn2] is pipelined and chunk k's attention waits only for chunk k-1's
+    out-projection (the arena gives the attention output the LN2 output's bytes, not
+    the FFN hidden's); an f2 region run with the chunk-loop overlap is not pipelined;
+    waits stay inside their region; AC_PIPELINE=0 / AC_OVERLAP=0 turn it off."""
+    from oracle import graph as og_graph
+    def sched(name, txt):
+        g = workloads.config(name)
+        cg = api.graph_parse(og_graph.serialize(g))
+        plan = api.plan_parse(cg, "autochunk-plan 1\n" + txt)
+        w, p = plan.chunk_pipeline()
+        ids = [n.id for n in g.nodes]
+        return {ids[i]: ids[w[i]] for i in range(len(ids)) if w[i] >= 0}, p, ids
+    waits, p, ids = sched("gpt_fa", "region s=attn e=ffn2 n=16 dims=0\n")
+    assert p == [1] and waits["attn"] == "proj_o"
+    assert set(waits) <= set(ids[ids.index("attn"): ids.index("ffn2") + 1])
+    waits, p, _ = sched("gpt", "region s=scores e=pv n=8 dims=0\n")
+    assert p == [0]
+    waits, p, _ = sched("gpt_fa", "region s=ln2 e=ffn2 n=2 dims=0\n")
+    assert p == [1] and waits["ln2"] == "ffn1"
+    monkeypatch.setenv("AC_PIPELINE", "0")
+    assert sched("gpt_fa", "region s=attn e=ffn2 n=16 dims=0\n")[1] == [0]
+    monkeypatch.delenv("AC_PIPELINE")
+    monkeypatch.setenv("AC_OVERLAP", "0")
+    assert sched("gpt_fa", "region s=attn e=ffn2 n=16 dims=0\n")[1] == [0]
