@@ -40,6 +40,11 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, alternating 64-column slabs
 constexpr int MAX_MT = 2048;
+// f2 scores: every F2_POLY_EVERY-th column pair of a full 32-column group takes 2^x from a
+// polynomial on the FMA pipe instead of MUFU (0 = all MUFU)
+#ifndef F2_POLY_EVERY
+#define F2_POLY_EVERY 0
+#endif
 
 struct alignas(64) GemmArgs {
   CUtensorMap ta;
@@ -61,6 +66,7 @@ struct alignas(64) GemmArgs {
   int lean; // TMA-store epilogue without aux tensors / activation (scale and causal only)
   int fuse; // fused softmax-normalised A operand (PV of the f2 path)
   const float2* fstats;
+  int stats_smem;  // MODE 2: slab statistics staged into shared memory by the producer (16-slab ring)
   long long fst_sb1, fst_ss;
   // MODE 2 fixed split-K: K cut into granules of skgk k-blocks at fixed key
   // positions; one work unit per (tile, granule); multi-granule tiles leave fp32
@@ -109,7 +115,9 @@ struct Cfg {
   static constexpr int KBUF = MODE == 2 && BN == 64 ? 7 : 8;
   // f2 PV (MODE 2) stages no output in smem: its ring is 8 deep (one CTA must keep
   // ~8 x 24 KB of A/B tiles in flight to stream at full speed when few CTAs remain)
-  static constexpr int EPI_BYTES = (MODE == 1 || MODE == 3 || MODE == 4) ? EPI * 4096 : MODE == 2 ? 0 : EPI_WARPS * 32 * PITCH * 4;
+  // MODE 2: the statistics ring (SRING slots of 128 rows x (m2, l), 1 KB each)
+  static constexpr int SRING = 16;
+  static constexpr int EPI_BYTES = (MODE == 1 || MODE == 3 || MODE == 4) ? EPI * 4096 : MODE == 2 ? SRING * 1024 : EPI_WARPS * 32 * PITCH * 4;
   static constexpr int STAGES = (MODE == 1 || MODE == 3 || MODE == 4) ? 2 : MODE == 2 ? 8 : (BN >= 256 ? 3 : (BN >= 128 ? 4 : 5));
   static constexpr int A_BYTES = BM * BK * 2;
   // MODE 4 (paired 64-row tiles): each stage holds the B tiles of both tiles of a pair
@@ -121,7 +129,7 @@ struct Cfg {
   static constexpr int TMEM_COLS = MODE == 2 ? 512
                                              : (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
   static constexpr int SMEM = 1024 /*align slack*/ + STAGES * (A_BYTES + B_BYTES) + EPI_BYTES + 512 /*barriers*/ +
-                              (MODE == 4 ? 0 : (MAX_MT + 1) * 4 + 16 + (MODE == 3 ? 16 * 8 + 8 : MODE == 2 ? 18 * 8 + 8 + 128 * 8 : 0));
+                              (MODE == 4 ? 0 : (MAX_MT + 1) * 4 + 16 + (MODE == 3 ? 16 * 8 + 8 : MODE == 2 ? 18 * 8 + 8 + 128 * 8 + 2 * SRING * 8 : 0));
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
@@ -289,7 +297,9 @@ template <int BN, int MODE, bool PAIR>
 __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
   using C = Cfg<BN, MODE>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // aligned by pointer arithmetic on the shared array (an integer round trip would
+  // turn every later access into a generic LD / ST)
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
   float* sEpi = reinterpret_cast<float*>(sB + C::STAGES * C::B_BYTES);
@@ -304,11 +314,14 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
   // through a 4-deep ring (uq_full: 1 arrival, uq_empty: one per consuming warp)
   uint64_t* uq_full = tempty + 19;
   uint64_t* uq_empty = tempty + 23;
+  // slot = 8 ints: the unit, and for MODE 1 / 3 its decoded tile (TileWalk b, r, mt, lo, hi),
+  // so the consuming warps do not each decode it (integer division + binary search)
   int* uq_slot = reinterpret_cast<int*>(tempty + 27);
-  int* prefix = reinterpret_cast<int*>(tempty + 29);  // ends at 2 * STAGES + 31 words <= 512 bytes
+  int* prefix = reinterpret_cast<int*>(tempty + 43);  // 2 * STAGES + 47 words, MODE 2: + 18 + 1 + 128
   // MODE 1 bias boxes: one mbarrier per epilogue warp, after the prefix table
   uint64_t* bbar = MODE == 4 ? reinterpret_cast<uint64_t*>(prefix)
-                             : reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(prefix + MAX_MT + 2) + 7) & ~uintptr_t(7));
+                             : reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(prefix + MAX_MT + 2) +
+                                                         ((8u - (ptx::smem_u32(prefix + MAX_MT + 2) & 7u)) & 7u));
   static_assert(C::STAGES <= 8, "barrier block layout");
 
   const int warp = threadIdx.x >> 5;
@@ -397,8 +410,11 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
     for (int s = 0; s < C::STAGES; ++s) ptx::mbar_init(&ready[s], 32 * C::EPI);
     if (MODE == 3 || MODE == 4)
       for (int w = 0; w < C::EPI; ++w) ptx::mbar_init(&bbar[w], 1);
-    if (MODE == 2)  // PV: kfull[8] (MMA commit), kempty[8] (4 scale warps), sfull, sempty (4 warps each)
+    if (MODE == 2) {  // PV: kfull[8] (MMA commit), kempty[8] (4 scale warps), sfull, sempty (4 warps each)
       for (int w = 0; w < 18; ++w) ptx::mbar_init(&bbar[w], w < 8 ? 1 : 4);
+      // statistics ring: stfull (producer's bulk load), stempty (4 scale warps)
+      for (int w = 0; w < 2 * C::SRING; ++w) ptx::mbar_init(&bbar[18 + 128 + w], w < C::SRING ? 1 : 4);
+    }
     for (int s = 0; s < 4; ++s) {
       ptx::mbar_init(&uq_full[s], 1);
       ptx::mbar_init(&uq_empty[s], 1 + C::EPI + C::XEPI);
@@ -438,8 +454,14 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
       // the start of a launch), later ones come from the counter offset by the grid
       int u = !sc || i == 0 ? cid + i * ncl : ncl + atomicAdd(sc, 1);
       if (u > total) u = total;
+      TileWalk w;
+      if ((MODE == 1 || MODE == 3) && u < total) w.next(a, prefix, tpb, u, ncl);
       ptx::mbar_wait(&uq_empty[sl], ((i >> 2) & 1) ^ 1);
-      *reinterpret_cast<volatile int*>(&uq_slot[sl]) = u;
+      volatile int* q = uq_slot + 8 * sl;
+      q[0] = u;
+      if (MODE == 1 || MODE == 3) {
+        q[1] = w.b; q[2] = w.r; q[3] = w.mt; q[4] = w.lo; q[5] = w.hi;
+      }
       ptx::mbar_arrive(&uq_full[sl]);
       return u;
     } else {
@@ -450,13 +472,30 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
     if (uq) {
       const int sl = i & 3;
       ptx::mbar_wait(&uq_full[sl], (i >> 2) & 1);
-      const int u = *reinterpret_cast<volatile int*>(&uq_slot[sl]);
+      const int u = uq_slot[8 * sl];
       __syncwarp();
       if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(&uq_empty[sl]);
       return u;
     } else {
       return cid + i * ncl;
     }
+  };
+  // MODE 1 / 3 consumers: the next tile, decoded (from the queue slot when tiles are
+  // dynamic, else by the incremental walk)
+  auto take_walk = [&](int i, TileWalk& w) -> int {
+    if ((MODE == 1 || MODE == 3) && uq) {
+      const int sl = i & 3;
+      ptx::mbar_wait(&uq_full[sl], (i >> 2) & 1);
+      const volatile int* q = uq_slot + 8 * sl;
+      const int u = q[0];
+      w.b = q[1]; w.r = q[2]; w.mt = q[3]; w.lo = q[4]; w.hi = q[5];
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(&uq_empty[sl]);
+      return u;
+    }
+    const int t = take(i);
+    if (t < total) w.next(a, prefix, tpb, t, ncl);
+    return t;
   };
 
   if (MODE == 4 && warp == 0) {
@@ -488,6 +527,8 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
       uint32_t phase = 0;
       TileWalk walk;
       const uint64_t epol = ptx::policy_evict_first();
+      int ss = 0;          // MODE 2 statistics ring slot / phase
+      uint32_t sph = 0;
       for (int i = 0, t = produce(0); t < total; t = produce(++i)) {
         int b1, b2, mt, nt = 0, kbn, klo, khi;
         if constexpr (MODE == 2) {
@@ -540,6 +581,18 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
           continue;
         }
         for (int kb = klo; kb < khi; ++kb) {
+          if (MODE == 2 && a.stats_smem) {
+            // the slab's statistics of the tile's rows (< M, an even count) into the ring
+            uint64_t* stfull = bbar + 18 + 128;
+            const int rows = a.M - mt * BM < BM ? a.M - mt * BM : BM;
+            ptx::mbar_wait(&stfull[C::SRING + ss], sph ^ 1);
+            ptx::mbar_expect_tx(&stfull[ss], rows * 8);
+            ptx::bulk_load(reinterpret_cast<uint8_t*>(sEpi) + ss * 1024,
+                           a.fstats + static_cast<long long>(b1 * a.B2 + b2) * a.fst_sb1 +
+                               static_cast<long long>(kb) * a.fst_ss + static_cast<long long>(mt) * BM,
+                           rows * 8, &stfull[ss]);
+            if (++ss == C::SRING) { ss = 0; sph ^= 1; }
+          }
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::mbar_expect_tx(&full[stage], (two ? 2 : 1) * (ebytes + C::B_TILE));
           if (MODE == 2 && esrc) {
@@ -605,13 +658,13 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
     int kbuf = 0;          // MODE 2 post-scale: next per-k-block TMEM buffer
     uint32_t kphase = 0;
     TileWalk walk;
-    for (int i = 0, t = take(0); t < total; t = take(++i)) {
+    for (int i = 0, t = MODE == 2 ? take(0) : take_walk(0, walk); t < total;
+         t = MODE == 2 ? take(++i) : take_walk(++i, walk)) {
       int b1, b2, mt, nt = 0, kbn, klo, khi;
       if constexpr (MODE == 2) {
         int g, ng, tile, unit0;
         decode_unit(a, prefix, tpb, t, b1, b2, mt, kbn, klo, khi, g, ng, tile, unit0);
       } else {
-        walk.next(a, prefix, tpb, t, ncl);
         walk.get(a, b1, b2, mt, nt, kbn);
         klo = 0;
         khi = kbn;
@@ -739,6 +792,13 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
         const bool lead = warp == 2;
         constexpr int PF = 4;  // slab statistics prefetched PF slabs ahead (next unit's included)
         const int r = quarter * 32 + lane;
+        // statistics from the producer's shared-memory ring (no load latency on this warp),
+        // else prefetched from global memory PF slabs ahead
+        const bool sm = a.stats_smem != 0;
+        uint64_t* stfull = bbar + 18 + 128;
+        const float2* sst = reinterpret_cast<const float2*>(sEpi);
+        int ss = 0;
+        uint32_t sph = 0;
         int kbuf = 0;
         uint32_t kphase = 0, sphase = 0;
         int i = 0;
@@ -747,7 +807,7 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
         float2 fr[PF];
         if (t < total) unit(t, u);
 #pragma unroll
-        for (int j = 0; j < PF; ++j) fr[j] = (t < total && u.mv && u.klo + j < u.khi) ? ldst(u, u.klo + j) : nost;
+        for (int j = 0; j < PF; ++j) fr[j] = (!sm && t < total && u.mv && u.klo + j < u.khi) ? ldst(u, u.klo + j) : nost;
         while (t < total) {
           float Mr = -CUDART_INF_F, Lr = 0.f;
           float accv[BN];
@@ -759,14 +819,14 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
             float2 nx[PF];
             if (kb0 + PF < u.khi) {
 #pragma unroll
-              for (int j = 0; j < PF; ++j) nx[j] = (u.mv && kb0 + PF + j < u.khi) ? ldst(u, kb0 + PF + j) : nost;
+              for (int j = 0; j < PF; ++j) nx[j] = (!sm && u.mv && kb0 + PF + j < u.khi) ? ldst(u, kb0 + PF + j) : nost;
             } else {
               // last block of this unit: take the next unit now and prefetch its first
               // statistics behind this block's slabs
               tn = take(++i);
               if (tn < total) unit(tn, un);
 #pragma unroll
-              for (int j = 0; j < PF; ++j) nx[j] = (tn < total && un.mv && un.klo + j < un.khi) ? ldst(un, un.klo + j) : nost;
+              for (int j = 0; j < PF; ++j) nx[j] = (!sm && tn < total && un.mv && un.klo + j < un.khi) ? ldst(un, un.klo + j) : nost;
             }
 #pragma unroll
             for (int j = 0; j < PF; ++j) {
@@ -783,15 +843,27 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
                 const uint32_t tk = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + kbuf * BN;
                 uint32_t v[32];
                 ptx::tmem_ld32(tk, v);
-                if (fr[j].x > Mr) {
-                  const float cr = ptx::ex2(Mr - fr[j].x);  // first slab: 2^-inf = 0, O and L are 0
+                float2 st = fr[j];
+                if (sm) {
+                  ptx::mbar_wait(&stfull[ss], sph);
+                  // racecheck: mbarrier handoff (bulk-loaded before stfull, freed by the stempty arrive)
+                  st = u.mv ? sst[ss * 128 + r] : nost;
+                  __syncwarp();
+                  if (lane == 0) ptx::mbar_arrive(&stfull[C::SRING + ss]);
+                  if (++ss == C::SRING) { ss = 0; sph ^= 1; }
+                }
+                // lazy reference (R19): O and L move to a new running max only when a slab's
+                // m2 exceeds it by more than 8 (f <= 2^8), so a row rescales a few times, not
+                // at every slab whose m2 sets a record (divergent over the warp's 32 rows)
+                if (st.x > Mr + 8.f) {
+                  const float cr = ptx::ex2(Mr - st.x);  // first slab: 2^-inf = 0, O and L are 0
                   Lr *= cr;
 #pragma unroll
                   for (int c = 0; c < BN; ++c) accv[c] *= cr;
-                  Mr = fr[j].x;
+                  Mr = st.x;
                 }
-                const float f = fr[j].x == -CUDART_INF_F ? 0.f : ptx::ex2(fr[j].x - Mr);
-                Lr = fmaf(fr[j].y, f, Lr);
+                const float f = st.x == -CUDART_INF_F ? 0.f : ptx::ex2(st.x - Mr);
+                Lr = fmaf(st.y, f, Lr);
 #pragma unroll
                 for (int hh = 0; hh < BN / 32; ++hh) {
                   if (hh > 0) ptx::tmem_ld32(tk + hh * 32, v);
@@ -1083,9 +1155,8 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
     } else {
     TileWalk walk;
     int dep_ok_b = -1;  // MODE 1 / 3: last batch whose predecessor PV is known finished
-    for (int i = 0, t = take(0); t < total; t = take(++i)) {
+    for (int i = 0, t = take_walk(0, walk); t < total; t = take_walk(++i, walk)) {
       int b1, b2, mt, nt, kbn;
-      walk.next(a, prefix, tpb, t, ncl);
       walk.get(a, b1, b2, mt, nt, kbn);
       ptx::mbar_wait(&tfull[acc], aphase);
       ptx::tc_fence_after();
@@ -1139,8 +1210,9 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
           }
           const int m = m0 + lane;
           const bool mvalid = m < a.M;
-          long long lim = a.ep.causal ? (a.ep.row_off + m - a.ep.col_off - n0) : (1ll << 40);
-          if (lim > a.N - 1 - n0) lim = a.N - 1 - n0;  // columns past N are masked (and clipped by the store)
+          long long lim64 = a.ep.causal ? (a.ep.row_off + m - a.ep.col_off - n0) : (1ll << 40);
+          if (lim64 > a.N - 1 - n0) lim64 = a.N - 1 - n0;  // columns past N are masked (and clipped by the store)
+          const int lim = lim64 < -1 ? -1 : static_cast<int>(lim64);  // only lim < 0 / lim >= j matter
           const uint32_t ta = tbase + c * SW;
           // biased: registers hold x itself after the add (unit multiplier below)
           const float cl = BIASED ? 1.f : a.ep.scale * L2E;
@@ -1186,8 +1258,15 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
                   x0 = fmaf(__uint_as_float(r[2 * j]), cl, -mref);
                   x1 = fmaf(__uint_as_float(r[2 * j + 1]), cl, -mref);
                 }
-                const float e0 = ptx::ex2(x0);
-                const float e1 = ptx::ex2(x1);
+                // one column pair in F2_POLY_EVERY on the FMA pipe (the MUFU pipe saturates
+                // while the warps exponentiate; columns fixed, so chunking changes nothing)
+                float e0, e1;
+                if (F2_POLY_EVERY > 0 && j % (F2_POLY_EVERY > 0 ? F2_POLY_EVERY : 1) == F2_POLY_EVERY - 1) {
+                  ptx::exp2_poly2(x0, x1, e0, e1);
+                } else {
+                  e0 = ptx::ex2(x0);
+                  e1 = ptx::ex2(x1);
+                }
                 sp = f2_add(sp, f2_pack(e0, e1));
                 __nv_bfloat162 h = __floats2bfloat162_rn(e0, e1);
                 pk[j] = *reinterpret_cast<uint32_t*>(&h);
@@ -1233,36 +1312,40 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
           if constexpr (!BIASED) {
             // one TMEM pass (reading R19): the slab's reference is its first score x0
             // (column 0 is valid whenever any column is: masks are suffixes), so the
-            // exponentials start before the slab max is known; a row whose max exceeds
-            // x0 by more than 96 (log2 units) is redone against its max (the TMEM
-            // reload is warp-collective, the decision per row: results depend only on
-            // the row's own data)
+            // exponentials need no slab max; a row whose sum of 2^(x - x0) exceeds 2^96
+            // (its max exceeds x0 by more than 96, or nearly so) is redone against its
+            // max in a second TMEM pass (warp-collective reloads, the decision per row:
+            // results depend only on the row's own data)
             load_x(0, r);
             float mref = lim >= 0 ? __uint_as_float(r[0]) * cl : 0.f;
-            slab_max(0);
             emit(0, mref, l0, l1);
             load_x(1, r);
-            slab_max(1);
-            const bool redo = lim >= 0 && mx * cl - mref > 96.f;
+            emit(1, mref, l0, l1);
+            const bool redo = lim >= 0 && !(l0 + l1 <= 0x1p96f);
             const bool any_redo = __any_sync(0xffffffffu, redo);
             if (!any_redo && last) {
               ptx::tc_fence_before();
               __syncwarp();
               if (lane == 0) acc_free(acc);
             }
-            if (redo) {
-              mref = mx * cl;
-              l0 = l1 = 0.f;
-            }
-            emit(1, mref, l0, l1);
             if (any_redo) {
               load_x(0, r);
+              slab_max(0);
+              load_x(1, r);
+              slab_max(1);
+              if (redo) {
+                mref = mx * cl;
+                l0 = l1 = 0.f;
+              }
+              load_x(0, r);
+              if (redo) emit(0, mref, l0, l1);
+              load_x(1, r);
               if (last) {
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) acc_free(acc);
               }
-              if (redo) emit(0, mref, l0, l1);
+              if (redo) emit(1, mref, l0, l1);
             }
             m2 = lim >= 0 ? mref : -CUDART_INF_F;
           } else {
@@ -1680,6 +1763,11 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
   a.dep_epoch = p.dep_epoch;
   a.tsched = (MODE == 1 || MODE == 3 || MODE == 4) ? p.tsched : nullptr;
   a.fstats = p.fuse_stats;
+  // statistics staged by 16-byte bulk copies: rows of a slab (M, even) at an even float2 offset
+  a.stats_smem = (MODE == 2 && p.etile && p.fuse_stats && !(p.M & 1) && !(p.fuse_ss & 1) && !(p.fuse_sb1 & 1) &&
+                  !(reinterpret_cast<uintptr_t>(p.fuse_stats) & 15))
+                     ? 1
+                     : 0;
   a.fst_sb1 = p.fuse_sb1;
   a.fst_ss = p.fuse_ss;
   const int sms = num_sms();
@@ -1697,6 +1785,7 @@ cudaError_t launch(const GemmProblem& p, cudaStream_t s) {
     a.total_tiles_dense = a.tiles_per_batch_dense * p.B1 * p.B2;
   }
   a.pair = (MODE == 2 && BN == 32 && p.etile && p.M <= 64 && a.skng == 1 && !p.causal_k) ? 1 : 0;
+  if (a.pair) a.stats_smem = 0;  // pairs: two batches' rows per unit, global loads
   a.zero_word = (MODE == 1 || MODE == 3 || MODE == 4) ? p.zero_word : nullptr;
   a.zero_n = p.zero_n;
   const int cw = a.pair2 ? 2 : 1;  // CTAs per tile

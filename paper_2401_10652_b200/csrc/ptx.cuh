@@ -326,6 +326,34 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x for a pair on the FMA pipe (no MUFU): x clamped to >= -126, j = round(x) by the
+// 1.5 * 2^23 shifter, f = x - j in [-0.5, 0.5], 2^f by a degree-3 polynomial (relative error
+// <= 7.5e-5, near-minimax on [-0.5, 0.5]), 2^j added to the exponent field.  For values
+// stored in bf16 (half-ulp 2^-9 = 2e-3) the polynomial is as good as MUFU ex2.approx
+// (FA4's split of the exponentials between MUFU and FMA).  x <= 127 required.
+__device__ __forceinline__ void exp2_poly2(float x0, float x1, float& e0, float& e1) {
+  x0 = fmaxf(x0, -126.f);
+  x1 = fmaxf(x1, -126.f);
+  const uint64_t mg = f32x2_splat(12582912.f), nmg = f32x2_splat(-12582912.f);
+  const uint64_t c0 = f32x2_splat(0.9999280571937561f), c1 = f32x2_splat(0.6932609677314758f),
+                 c2 = f32x2_splat(0.24261115491390228f), c3 = f32x2_splat(0.0551716685295105f);
+  uint32_t t0, t1, p0, p1;
+  asm("{\n\t.reg .b64 px, pt, pj, pf, pp;\n\t"
+      "mov.b64 px, {%4, %5};\n\t"
+      "add.rn.f32x2 pt, px, %6;\n\t"
+      "add.rn.f32x2 pj, pt, %7;\n\t"
+      "sub.rn.f32x2 pf, px, pj;\n\t"
+      "fma.rn.f32x2 pp, pf, %11, %10;\n\t"
+      "fma.rn.f32x2 pp, pp, pf, %9;\n\t"
+      "fma.rn.f32x2 pp, pp, pf, %8;\n\t"
+      "mov.b64 {%0, %1}, pt;\n\t"
+      "mov.b64 {%2, %3}, pp;\n}"
+      : "=r"(t0), "=r"(t1), "=r"(p0), "=r"(p1)
+      : "f"(x0), "f"(x1), "l"(mg), "l"(nmg), "l"(c0), "l"(c1), "l"(c2), "l"(c3));
+  e0 = __uint_as_float(p0 + (t0 << 23));
+  e1 = __uint_as_float(p1 + (t1 << 23));
+}
+
 // 2^x on a bf16x2 pair (one MUFU op for both halves)
 __device__ __forceinline__ uint32_t ex2_bf16x2(uint32_t x) {
   uint32_t y;
