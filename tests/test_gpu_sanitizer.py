@@ -147,7 +147,6 @@ def _marked(loc):
     return any("racecheck: mbarrier handoff" in lines[k] for k in range(max(0, i - 3), min(len(lines), i + 1)))
 
 
-@pytest.mark.parametrize("tool", ["racecheck", "synccheck"])
 def _skip_if_refused(r):
     # the pool may close compute-sanitizer (its wrapper then refuses with a message and
     # runs nothing): that is an unavailable tool, not a finding
@@ -155,6 +154,7 @@ def _skip_if_refused(r):
         pytest.skip("compute-sanitizer refused on this pool: " + r.stderr.strip().splitlines()[0][:200])
 
 
+@pytest.mark.parametrize("tool", ["racecheck", "synccheck"])
 def test_racecheck_synccheck_clean(tmp_path, tool):
     """synccheck must be clean.  racecheck must report no hazard except on shared-memory
     handoffs ordered by mbarriers (arrive has release, try_wait acquire semantics; the
