@@ -40,8 +40,13 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, alternating 64-column slabs
 constexpr int MAX_MT = 2048;
-// f2 scores: every F2_POLY_EVERY-th column pair of a full 32-column group takes 2^x from a
-// polynomial on the FMA pipe instead of MUFU (0 = all MUFU)
+// f2 scores (unbiased chains; the triangle chains' paired short-chunk kernel has no such
+// split, so they stay on MUFU for chunk invariance): every F2_POLY_EVERY-th column pair of a
+// full 32-column group takes 2^x from a polynomial on the FMA pipe instead of MUFU (0 = all
+// MUFU; 4 measured faster alone, slower under the chunk-loop overlap on GPT)
+#ifndef F2_STAGES
+#define F2_STAGES 2
+#endif
 #ifndef F2_POLY_EVERY
 #define F2_POLY_EVERY 0
 #endif
@@ -118,7 +123,10 @@ struct Cfg {
   // MODE 2: the statistics ring (SRING slots of 128 rows x (m2, l), 1 KB each)
   static constexpr int SRING = 16;
   static constexpr int EPI_BYTES = (MODE == 1 || MODE == 3 || MODE == 4) ? EPI * 4096 : MODE == 2 ? SRING * 1024 : EPI_WARPS * 32 * PITCH * 4;
-  static constexpr int STAGES = (MODE == 1 || MODE == 3 || MODE == 4) ? 2 : MODE == 2 ? 8 : (BN >= 256 ? 3 : (BN >= 128 ? 4 : 5));
+  // f2 scores: one stage = one tile's Q and K blocks (K = head dim <= 64); a third stage
+  // lets the producer run two tiles ahead of the MMA
+  static constexpr int STAGES = (MODE == 1 && BN == 256) ? F2_STAGES
+                                : (MODE == 1 || MODE == 3 || MODE == 4) ? 2 : MODE == 2 ? 8 : (BN >= 256 ? 3 : (BN >= 128 ? 4 : 5));
   static constexpr int A_BYTES = BM * BK * 2;
   // MODE 4 (paired 64-row tiles): each stage holds the B tiles of both tiles of a pair
   // MODE 4 (paired 64-row tiles) and the BN = 32 PV (pairs when M <= 64): each stage
@@ -1261,7 +1269,7 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
                 // one column pair in F2_POLY_EVERY on the FMA pipe (the MUFU pipe saturates
                 // while the warps exponentiate; columns fixed, so chunking changes nothing)
                 float e0, e1;
-                if (F2_POLY_EVERY > 0 && j % (F2_POLY_EVERY > 0 ? F2_POLY_EVERY : 1) == F2_POLY_EVERY - 1) {
+                if (!BIASED && F2_POLY_EVERY > 0 && j % (F2_POLY_EVERY > 0 ? F2_POLY_EVERY : 1) == F2_POLY_EVERY - 1) {
                   ptx::exp2_poly2(x0, x1, e0, e1);
                 } else {
                   e0 = ptx::ex2(x0);
