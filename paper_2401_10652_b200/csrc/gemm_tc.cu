@@ -45,7 +45,7 @@ constexpr int MAX_MT = 2048;
 // full 32-column group takes 2^x from a polynomial on the FMA pipe instead of MUFU (0 = all
 // MUFU; 4 measured faster alone, slower under the chunk-loop overlap on GPT)
 #ifndef F2_STAGES
-#define F2_STAGES 2
+#define F2_STAGES 3
 #endif
 #ifndef F2_POLY_EVERY
 #define F2_POLY_EVERY 0
