@@ -1091,24 +1091,38 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
               }
             }
           };
-          float mx = -CUDART_INF_F;
+          // biased redo path: the box holds e by then, so the bias comes from global memory
+          auto load_x_gbias = [&](int hh) {
+            ptx::tmem_ld32(ta + hh * 32, r);
+            ptx::tmem_ld_wait();
+            const int q1 = bb / a.B2, q2 = bb - (bb / a.B2) * a.B2;
+            const __nv_bfloat16* brow = static_cast<const __nv_bfloat16*>(a.ep.add) +
+                                        (a.ep.add_sb1 ? static_cast<long long>(q1) * a.ep.add_sb1 : 0) +
+                                        (a.ep.add_sb2 ? static_cast<long long>(q2) * a.ep.add_sb2 : 0) +
+                                        static_cast<long long>(mvalid ? m : 0) * a.ep.add_sm + n0 + hh * 32;
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            load_x(hh);
+            for (int q = 0; q < 4; ++q) {
+              uint32_t w[4] = {0u, 0u, 0u, 0u};
+              const int n = n0 + hh * 32 + 8 * q;
+              if (mvalid && n + 8 <= a.N) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(brow + 8 * q));
+                w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+              } else if (mvalid) {
+                __nv_bfloat16 h[8];
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (hh * 32 + j <= lim) mx = fmaxf(mx, __uint_as_float(r[j]));
-          }
-          const float mref = mx == -CUDART_INF_F ? 0.f : mx;
-          float l0 = 0.f, l1 = 0.f;
+                for (int e = 0; e < 8; ++e) h[e] = n + e < a.N ? brow[8 * q + e] : __float2bfloat16(0.f);
+                memcpy(w, h, 16);
+              }
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            load_x(hh);
-            if (hh == 1) {
-              ptx::tc_fence_before();
-              __syncwarp();
-              if (lane == 0) acc_free(acc);
+              for (int e = 0; e < 4; ++e) {
+                const float2 bf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+                r[8 * q + 2 * e] = __float_as_uint(fmaf(__uint_as_float(r[8 * q + 2 * e]), sc, bf.x * L2E));
+                r[8 * q + 2 * e + 1] = __float_as_uint(fmaf(__uint_as_float(r[8 * q + 2 * e + 1]), sc, bf.y * L2E));
+              }
             }
+          };
+          float l0 = 0.f, l1 = 0.f;
+          auto emit = [&](int hh, float mref) {
             uint32_t pk[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
@@ -1127,7 +1141,43 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
                            "r"(pk[4 * q + 1]), "r"(pk[4 * q + 2]), "r"(pk[4 * q + 3])
                            : "memory");
             }
+          };
+          // one TMEM pass, reference = the slab's first score x0 (R19, as the 128-row
+          // kernel: same x, same reference, same redo rule, so a row's e and statistics are
+          // bitwise those of the unpaired kernel in any chunking)
+          load_x(0);
+          float mref = lim >= 0 ? __uint_as_float(r[0]) : 0.f;
+          emit(0, mref);
+          load_x(1);
+          emit(1, mref);
+          const bool redo = lim >= 0 && !(l0 + l1 <= 0x1p96f);
+          const bool any_redo = __any_sync(0xffffffffu, redo);
+          if (!any_redo) {
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) acc_free(acc);
+          } else {
+            float mx = -CUDART_INF_F;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              load_x_gbias(hh);
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (hh * 32 + j <= lim) mx = fmaxf(mx, __uint_as_float(r[j]));
+            }
+            if (redo) {
+              mref = mx;
+              l0 = l1 = 0.f;
+            }
+            load_x_gbias(0);
+            if (redo) emit(0, mref);
+            load_x_gbias(1);
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) acc_free(acc);
+            if (redo) emit(1, mref);
           }
+          const float mx = lim >= 0 ? mref : -CUDART_INF_F;
           if (a.done_epoch && pb != dep_ok_pb) {
             // chunk-loop overlap: the previous chunk's PV must be done with both batches
             if (lane == 0) {
@@ -1246,6 +1296,39 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
               }
             }
           };
+          // biased redo path: the staging box already holds this slab's e chunks, so the
+          // bias comes from global memory (L2) - the same bf16 values, the same arithmetic
+          auto load_x_gbias = [&](int hh, uint32_t (&r)[32]) {
+            ptx::tmem_ld32(ta + hh * 32, r);
+            ptx::tmem_ld_wait();
+            if constexpr (BIASED) {
+              const float sc = a.ep.scale * L2E;
+              const __nv_bfloat16* brow = static_cast<const __nv_bfloat16*>(a.ep.add) +
+                                          (a.ep.add_sb1 ? static_cast<long long>(b1) * a.ep.add_sb1 : 0) +
+                                          (a.ep.add_sb2 ? static_cast<long long>(b2) * a.ep.add_sb2 : 0) +
+                                          static_cast<long long>(mvalid ? m : 0) * a.ep.add_sm + n0 + hh * 32;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                uint32_t w[4] = {0u, 0u, 0u, 0u};
+                const int n = n0 + hh * 32 + 8 * q;
+                if (mvalid && n + 8 <= a.N) {
+                  const uint4 v = __ldg(reinterpret_cast<const uint4*>(brow + 8 * q));
+                  w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+                } else if (mvalid) {
+                  __nv_bfloat16 h[8];
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) h[e] = n + e < a.N ? brow[8 * q + e] : __float2bfloat16(0.f);
+                  memcpy(w, h, 16);
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 bf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+                  r[8 * q + 2 * e] = __float_as_uint(fmaf(__uint_as_float(r[8 * q + 2 * e]), sc, bf.x * L2E));
+                  r[8 * q + 2 * e + 1] = __float_as_uint(fmaf(__uint_as_float(r[8 * q + 2 * e + 1]), sc, bf.y * L2E));
+                }
+              }
+            }
+          };
           uint32_t r[32];
           float mx = -CUDART_INF_F;
           float l0 = 0.f, l1 = 0.f;
@@ -1317,8 +1400,8 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
             }
             mx = fmaxf(mx, fmaxf(fmaxf(q0, q1), fmaxf(q2, q3)));
           };
-          if constexpr (!BIASED) {
-            // one TMEM pass (reading R19): the slab's reference is its first score x0
+          {
+            // one TMEM pass (reading R19, plain and biased chains alike): the slab's reference is its first score x0
             // (column 0 is valid whenever any column is: masks are suffixes), so the
             // exponentials need no slab max; a row whose sum of 2^(x - x0) exceeds 2^96
             // (its max exceeds x0 by more than 96, or nearly so) is redone against its
@@ -1337,17 +1420,22 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
               if (lane == 0) acc_free(acc);
             }
             if (any_redo) {
-              load_x(0, r);
+              // (biased: the bias from global memory, the box now holds e)
+              auto reload = [&](int hh) {
+                if constexpr (BIASED) load_x_gbias(hh, r);
+                else load_x(hh, r);
+              };
+              reload(0);
               slab_max(0);
-              load_x(1, r);
+              reload(1);
               slab_max(1);
               if (redo) {
                 mref = mx * cl;
                 l0 = l1 = 0.f;
               }
-              load_x(0, r);
+              reload(0);
               if (redo) emit(0, mref, l0, l1);
-              load_x(1, r);
+              reload(1);
               if (last) {
                 ptx::tc_fence_before();
                 __syncwarp();
@@ -1356,24 +1444,6 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
               if (redo) emit(1, mref, l0, l1);
             }
             m2 = lim >= 0 ? mref : -CUDART_INF_F;
-          } else {
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              load_x(hh, r);
-              slab_max(hh);
-            }
-            m2 = mx * cl;
-            const float mref = mx == -CUDART_INF_F ? 0.f : m2;
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              load_x(hh, r);
-              if (hh == 1 && last) {
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) acc_free(acc);
-              }
-              emit(hh, mref, l0, l1);
-            }
           }
           if (a.done_epoch) {
             // chunk-loop overlap: the previous chunk's PV must have finished reading this

@@ -569,6 +569,32 @@ def test_f2_large_logit_range(causal):
         assert torch.equal(got["x1"], base["x1"]), n
 
 
+def test_af_large_logit_range():
+    """The triangle chains take the same one-pass reference as the plain chains (R19: the
+    slab's first score x = (q.k scale + b) log2 e, a row redone against its max when the
+    slab sum exceeds 2^96, the bias of the redo read from global memory because the staging
+    box already holds e).  Wq and the bias projection scaled by 64 (exact in bf16) spread
+    the logits over hundreds of log2 units so the redo path runs in every launch: the
+    128-row kernel (unchunked, batch-dim chunks) and the paired 64-row kernel (query-dim
+    chunks of 48 rows) must give the same bits, and every output is finite."""
+    gu = _gu()
+    from paper_2401_10652_b200 import api
+    og = workloads.tri_attn_pair(192, 128, 4, 32, "bf16", name="af_wide")
+    cg = gu.c_graph(og)
+    vals, dev = gu.make_values(og, 5)
+    for w in ("row_wq", "col_wq", "row_wb", "col_wb"):
+        dev[w] = (dev[w].float() * 64.0).bfloat16()
+    base, _ = gu.run(cg, gu.empty_plan(cg), og, dev)
+    torch.cuda.synchronize()
+    out = og.outputs[0]
+    assert torch.isfinite(base[out].float()).all()
+    for txt in ("region s=row_scores e=row_pv n=4 dims=1\nregion s=col_scores e=col_pv n=4 dims=0\n",
+                "region s=row_scores e=row_pv n=3 dims=0\nregion s=col_scores e=col_pv n=2 dims=1\n"):
+        got, _ = gu.run(cg, api.plan_parse(cg, "autochunk-plan 1\n" + txt), og, dev)
+        torch.cuda.synchronize()
+        assert torch.equal(got[out], base[out]), txt
+
+
 @pytest.mark.parametrize("name,rows_per_chunk", [("unet", 2048), ("vit", 8192)])
 def test_full_size_sampled_rows(name, rows_per_chunk):
     """BASELINE configs at full size (UNet 16384 tokens h=10, ViT-L 65536 tokens) under
