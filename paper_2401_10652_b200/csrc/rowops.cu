@@ -590,7 +590,18 @@ cudaError_t softmax_dispatch(const void* s, void* p, int64_t rows, int64_t ncols
 
 // ------------------------------------------------------------------ layernorm
 // one warp per row, VPT 16-byte vectors per lane
-template <typename T, int VPT>
+// GS lanes per row (32: a warp per row; 16 / 8 for rows of <= 16 / 8 vectors, e.g. the
+// AlphaFold pair channels c_z = 128: two rows per warp instead of half a warp idle).  The
+// sums are xor butterflies over the GS lanes, bitwise the warp-wide butterfly whose upper
+// lanes would only add zeros.
+template <int GS>
+__device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+  for (int o = GS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T, int VPT, int GS = 32>
 __global__ void __launch_bounds__(256) layernorm_kernel(const T* __restrict__ x, const T* __restrict__ g,
                                                         const T* __restrict__ b, T* __restrict__ y, int64_t rows,
                                                         int C, float eps, int pdl, int64_t group, int64_t gx,
@@ -600,9 +611,12 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const T* __restrict__ x,
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   }
   constexpr int VN = Vec<T>::N;
-  const int lane = threadIdx.x & 31;
-  const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-  if (r >= rows) return;
+  constexpr int RPW = 32 / GS;  // rows per warp
+  const int lane = threadIdx.x & (GS - 1);
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 8 * RPW + (threadIdx.x >> 5) * RPW + ((threadIdx.x & 31) / GS);
+  if (RPW == 1 && r0 >= rows) return;
+  const bool rvalid = r0 < rows;  // (groups of a warp share its shuffles: no early exit)
+  const int64_t r = rvalid ? r0 : rows - 1;
   // rows in groups of `group` contiguous rows, groups gx / gy elements apart (a view
   // cut along a middle dim, e.g. a column chunk of the pair representation)
   const int64_t gi = r / group, ri = r - gi * group;
@@ -613,7 +627,7 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const T* __restrict__ x,
   float sum = 0.f;
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
-    const int vi = i * 32 + lane;
+    const int vi = i * GS + lane;
     if (vi < nv) {
       Vec<T> v;
       v.raw = *reinterpret_cast<const uint4*>(xr + vi * VN);
@@ -622,11 +636,11 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const T* __restrict__ x,
       for (int e = 0; e < VN; ++e) sum += f[i][e];
     }
   }
-  const float mean = warp_sum(sum) / static_cast<float>(C);
+  const float mean = group_sum<GS>(sum) / static_cast<float>(C);
   float sq = 0.f;
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
-    const int vi = i * 32 + lane;
+    const int vi = i * GS + lane;
     if (vi < nv) {
 #pragma unroll
       for (int e = 0; e < VN; ++e) {
@@ -635,12 +649,12 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const T* __restrict__ x,
       }
     }
   }
-  const float var = warp_sum(sq) / static_cast<float>(C);
+  const float var = group_sum<GS>(sq) / static_cast<float>(C);
   const float inv = 1.f / sqrtf(var + eps);
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
-    const int vi = i * 32 + lane;
-    if (vi < nv) {
+    const int vi = i * GS + lane;
+    if (vi < nv && rvalid) {
       Vec<T> gv, bv, o;
       gv.raw = *reinterpret_cast<const uint4*>(g + vi * VN);
       bv.raw = *reinterpret_cast<const uint4*>(b + vi * VN);
@@ -661,7 +675,8 @@ cudaError_t layernorm_dispatch(const void* x, const void* g, const void* b, void
   constexpr int VN = Vec<T>::N;
   if (C % VN != 0) return cudaErrorInvalidValue;
   const int nv = C / VN;
-  const int64_t blocks = (rows + 7) / 8;
+  const int rpb = 8 * (nv <= 8 ? 4 : nv <= 16 ? 2 : 1);  // rows per 256-thread block
+  const int64_t blocks = (rows + rpb - 1) / rpb;
   if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
   const unsigned gb = static_cast<unsigned>(blocks);
   auto X = static_cast<const T*>(x);
@@ -670,7 +685,8 @@ cudaError_t layernorm_dispatch(const void* x, const void* g, const void* b, void
   auto Y = static_cast<T*>(y);
   if (group <= 0 || gx % VN || gy % VN) return cudaErrorInvalidValue;
   void (*kern)(const T*, const T*, const T*, T*, int64_t, int, float, int, int64_t, int64_t, int64_t) =
-      nv <= 32 ? layernorm_kernel<T, 1> : nv <= 64 ? layernorm_kernel<T, 2> : nv <= 128 ? layernorm_kernel<T, 4>
+      nv <= 8 ? layernorm_kernel<T, 1, 8> : nv <= 16 ? layernorm_kernel<T, 1, 16>
+      : nv <= 32 ? layernorm_kernel<T, 1> : nv <= 64 ? layernorm_kernel<T, 2> : nv <= 128 ? layernorm_kernel<T, 4>
       : nv <= 256 ? layernorm_kernel<T, 8> : nv <= 512 ? layernorm_kernel<T, 16> : nullptr;
   if (!kern) return cudaErrorInvalidValue;
   if (pdl) {
@@ -711,9 +727,23 @@ __global__ void __launch_bounds__(256) ln_cfirst_kernel(const T* __restrict__ x,
   const int64_t i = blockIdx.y;
   const int64_t j0 = static_cast<int64_t>(blockIdx.x) * 64;
   const int jn = static_cast<int>(J - j0 < 64 ? J - j0 : 64);
-  for (int idx = threadIdx.x; idx < C * 64; idx += 256) {
-    const int c = idx >> 6, jj = idx & 63;
-    lsm[c * 65 + jj] = jj < jn ? static_cast<float>(x[c * xs_c + i * xs_i + j0 + jj]) : 0.f;
+  constexpr int VL = 16 / sizeof(T);  // elements per 16-byte load
+  if (jn == 64 && (xs_c % VL) == 0 && (xs_i % VL) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    // full tile: 16-byte loads along j (a c-row of the tile is 64 / VL vectors)
+    for (int idx = threadIdx.x; idx < C * (64 / VL); idx += 256) {
+      const int c = idx / (64 / VL), jv = (idx - c * (64 / VL)) * VL;
+      Vec<T> v;
+      v.raw = *reinterpret_cast<const uint4*>(x + c * xs_c + i * xs_i + j0 + jv);
+      float f[VL];
+      v.to_float(f);
+#pragma unroll
+      for (int e = 0; e < VL; ++e) lsm[c * 65 + jv + e] = f[e];
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < C * 64; idx += 256) {
+      const int c = idx >> 6, jj = idx & 63;
+      lsm[c * 65 + jj] = jj < jn ? static_cast<float>(x[c * xs_c + i * xs_i + j0 + jj]) : 0.f;
+    }
   }
   __syncthreads();
   {
