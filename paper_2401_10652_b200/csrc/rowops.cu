@@ -590,10 +590,10 @@ cudaError_t softmax_dispatch(const void* s, void* p, int64_t rows, int64_t ncols
 
 // ------------------------------------------------------------------ layernorm
 // one warp per row, VPT 16-byte vectors per lane
-// GS lanes per row (32: a warp per row; 16 / 8 for rows of <= 16 / 8 vectors, e.g. the
-// AlphaFold pair channels c_z = 128: two rows per warp instead of half a warp idle).  The
-// sums are xor butterflies over the GS lanes, bitwise the warp-wide butterfly whose upper
-// lanes would only add zeros.
+// GS lanes per row (32: a warp per row; 8 lanes for rows of <= 16 vectors, e.g. the
+// AlphaFold pair channels c_z = 128: four rows per warp, two 16-byte loads per lane in
+// flight, instead of a warp per row with half its lanes idle).  The sums are xor
+// butterflies over the GS lanes.
 template <int GS>
 __device__ __forceinline__ float group_sum(float v) {
 #pragma unroll
@@ -675,7 +675,7 @@ cudaError_t layernorm_dispatch(const void* x, const void* g, const void* b, void
   constexpr int VN = Vec<T>::N;
   if (C % VN != 0) return cudaErrorInvalidValue;
   const int nv = C / VN;
-  const int rpb = 8 * (nv <= 8 ? 4 : nv <= 16 ? 2 : 1);  // rows per 256-thread block
+  const int rpb = 8 * (nv <= 16 ? 4 : 1);  // rows per 256-thread block
   const int64_t blocks = (rows + rpb - 1) / rpb;
   if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
   const unsigned gb = static_cast<unsigned>(blocks);
@@ -685,7 +685,7 @@ cudaError_t layernorm_dispatch(const void* x, const void* g, const void* b, void
   auto Y = static_cast<T*>(y);
   if (group <= 0 || gx % VN || gy % VN) return cudaErrorInvalidValue;
   void (*kern)(const T*, const T*, const T*, T*, int64_t, int, float, int, int64_t, int64_t, int64_t) =
-      nv <= 8 ? layernorm_kernel<T, 1, 8> : nv <= 16 ? layernorm_kernel<T, 1, 16>
+      nv <= 8 ? layernorm_kernel<T, 1, 8> : nv <= 16 ? layernorm_kernel<T, 2, 8>
       : nv <= 32 ? layernorm_kernel<T, 1> : nv <= 64 ? layernorm_kernel<T, 2> : nv <= 128 ? layernorm_kernel<T, 4>
       : nv <= 256 ? layernorm_kernel<T, 8> : nv <= 512 ? layernorm_kernel<T, 16> : nullptr;
   if (!kern) return cudaErrorInvalidValue;
