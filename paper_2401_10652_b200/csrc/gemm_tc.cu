@@ -1279,7 +1279,9 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
             ptx::tmem_ld32(ta + hh * 32, r);
             ptx::tmem_ld_wait();
             if constexpr (BIASED) {
-              const float sc = a.ep.scale * L2E;
+              // x = fmaf(acc, scale log2e, b log2e) on packed pairs (FMUL2 + FFMA2: per lane
+              // the scalar roundings of the paired kernel); bf16 -> f32 by bit shifts
+              const uint64_t sc2 = f2_splat(a.ep.scale * L2E), l2e2 = f2_splat(L2E);
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 const uint32_t addr = ptx::smem_u32(sb + lane * 128 + (((hh * 4 + q) ^ (lane & 7)) * 16));
@@ -1289,9 +1291,13 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
                              : "r"(addr));
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                  const float2 bf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
-                  r[8 * q + 2 * e] = __float_as_uint(fmaf(__uint_as_float(r[8 * q + 2 * e]), sc, bf.x * L2E));
-                  r[8 * q + 2 * e + 1] = __float_as_uint(fmaf(__uint_as_float(r[8 * q + 2 * e + 1]), sc, bf.y * L2E));
+                  const uint64_t b2 = f2_pack(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xffff0000u));
+                  const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(r[8 * q + 2 * e]), __uint_as_float(r[8 * q + 2 * e + 1])),
+                                             sc2, f2_mul(b2, l2e2));
+                  float x0, x1;
+                  f2_unpack(x2, x0, x1);
+                  r[8 * q + 2 * e] = __float_as_uint(x0);
+                  r[8 * q + 2 * e + 1] = __float_as_uint(x1);
                 }
               }
             }
@@ -1345,9 +1351,8 @@ __device__ __forceinline__ void gemm_tc_body(const GemmArgs& a) {
                 float x0, x1;
                 if constexpr (!BIASED) {  // one FFMA2 per column pair (same rounding as fmaf)
                   ptx::fma2(r[2 * j], r[2 * j + 1], cl2, nm2, x0, x1);
-                } else {
-                  x0 = fmaf(__uint_as_float(r[2 * j]), cl, -mref);
-                  x1 = fmaf(__uint_as_float(r[2 * j + 1]), cl, -mref);
+                } else {  // x - mref as one FADD2 (= fmaf(x, 1, -mref) per lane)
+                  f2_unpack(f2_add(f2_pack(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])), nm2), x0, x1);
                 }
                 // one column pair in F2_POLY_EVERY on the FMA pipe (the MUFU pipe saturates
                 // while the warps exponentiate; columns fixed, so chunking changes nothing)
