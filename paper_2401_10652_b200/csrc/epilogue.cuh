@@ -23,6 +23,10 @@ __device__ __forceinline__ float from_f<float>(float v) { return v; }
 template <>
 __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
+#ifndef SIGMOID_TANH
+#define SIGMOID_TANH 1
+#endif
+
 // Branch-free erf for the GELU epilogue, Abramowitz & Stegun 7.1.26:
 // erf(a) = 1 - t (a1 + t (a2 + t (a3 + t (a4 + t a5)))) exp(-a^2), t = 1 / (1 + p a),
 // a = |z| (absolute error < 1.5e-7, below the fp32 / bf16 rounding of the GELU
@@ -33,6 +37,16 @@ __device__ __forceinline__ float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// Sigmoid of a value stored in bf16: 0.5 + 0.5 tanh(x / 2) with MUFU tanh.approx (one MUFU
+// op; |error| <= 2.5e-4 absolute, below the bf16 half-ulp of every sigmoid value >= 0.125)
+// instead of ex2 + rcp, two dependent MUFU ops (reading R28).  fp32 outputs keep the
+// precise form (their tolerance is 1e-4).
+__device__ __forceinline__ float sigmoid_bf16(float x) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * x));
+  return fmaf(0.5f, t, 0.5f);
 }
 
 __device__ __forceinline__ float erf_fast(float z) {
@@ -133,16 +147,18 @@ __device__ __forceinline__ void act_array(int act, float (&x)[NE]) {
     }
   } else if (act == ACT_SIGMOID) {
 #pragma unroll
-    for (int j = 0; j < NE; ++j) x[j] = rcp_approx(1.f + __expf(-x[j]));
+    for (int j = 0; j < NE; ++j) x[j] = SIGMOID_TANH ? sigmoid_bf16(x[j]) : rcp_approx(1.f + __expf(-x[j]));
   } else if (act == ACT_RELU) {
 #pragma unroll
     for (int j = 0; j < NE; ++j) x[j] = fmaxf(x[j], 0.f);
   }
 }
 
+template <typename T = float>
 __device__ __forceinline__ float act_apply(int act, float v) {
   if (act == ACT_GELU) return 0.5f * v * (1.f + erf_fast(v * 0.70710678118654752f));
-  if (act == ACT_SIGMOID) return rcp_approx(1.f + __expf(-v));
+  if (act == ACT_SIGMOID)
+    return (SIGMOID_TANH && sizeof(T) == 2) ? sigmoid_bf16(v) : rcp_approx(1.f + __expf(-v));
   if (act == ACT_RELU) return fmaxf(v, 0.f);
   return v;
 }
@@ -156,7 +172,7 @@ __device__ __forceinline__ float epi_value(const Epilogue& ep, int b1, int b2, i
                                                static_cast<int64_t>(b2) * ep.add_sb2 +
                                                static_cast<int64_t>(m) * ep.add_sm + static_cast<int64_t>(n) * ep.add_sn]);
   if (ep.bias) x += to_f<T>(static_cast<const T*>(ep.bias)[ep.bias_along_m ? m : n]);
-  x = act_apply(ep.act, x);
+  x = act_apply<T>(ep.act, x);
   (void)o;
   if (ep.gate)
     x *= to_f<T>(static_cast<const T*>(ep.gate)[static_cast<int64_t>(b1) * ep.gate_sb1 +
