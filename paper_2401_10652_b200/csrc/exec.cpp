@@ -1484,11 +1484,22 @@ ac_status ac_run(const ac_exec* e, const ac_tensor* inputs, int32_t n_in, ac_ten
     bool side_fresh = true;  // no kernel of this region on the side stream yet
     if (pipe && (cudaEventRecord(e->ev_pfork, s) != cudaSuccess || cudaStreamWaitEvent(e->side_s, e->ev_pfork, 0) != cudaSuccess))
       return set_error(AC_ERR_CUDA, "fork to the chunk pipelining stream");
+    // one rank, a causal attention chain, no chunk pipelining: the chunks run last-to-first.
+    // Chunks are independent (Eq. 4), so the order changes no value; the last
+    // causal chunk holds the most keys, and running it first lets the step end on the
+    // smallest chunk's PV tail while the larger tails overlap the next chunk's scores
+    // (GPT 2.238 -> 2.211 ms; a pipelined fused-attention region measured slower reversed)
+    bool rev = e->world <= 1 && !pipe;
+    if (rev) {
+      bool causal = false;
+      for (int j = R.start; j <= R.end; ++j) causal = causal || causal_chain(g, j);
+      rev = causal;
+    }
     for (size_t ci = 0; ci < sh.chunks.size(); ++ci) {
-      const int64_t c = sh.chunks[ci];
+      const int64_t c = sh.chunks[rev ? sh.chunks.size() - 1 - ci : ci];
       const int64_t off = c * L;
       const int64_t len = std::min(L, R.extent - off);
-      if (len <= 0) break;
+      if (len <= 0) continue;
       cudaStream_t cs = pipe && (ci & 1) ? e->side_s : s;
       NvtxRange nv_chunk("chunk " + std::to_string(c));
       if (pipe && (ci & 1)) e->stats.pipelined_chunks += 1;
