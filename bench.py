@@ -700,6 +700,20 @@ def main():
                       "roofline": stage_roof(k, v[1] / kp)}
                   for k, v in sorted(kt.items(), key=lambda kv: -kv[1][1])}
         shares["_profiled_ms_per_step"] = round(prof_ms / kp, 4)
+        # the fused attention chains inside the overlapped step (derived, not a kernel time):
+        # their algorithmic bytes over the step time left after every other stage's alone time
+        chain = [k for k in kt if doc.node(k)[1] in ("attn_scores", "attn_pv", "tri_scores", "tri_pv")
+                 and algorithmic(doc, k)[0] == "hbm"]
+        other_ms = sum(v[1] for k, v in kt.items() if k not in chain) / kp
+        if chain and roof is not None and ms_step - other_ms > 0:
+            cb = sum(algorithmic(doc, k)[1] for k in chain)
+            cg = cb / ((ms_step - other_ms) / 1e3) / 1e9
+            roof["f2_chains_in_step"] = {
+                "nodes": sorted(chain), "algorithmic_bytes_per_step": int(cb),
+                "ms": round(ms_step - other_ms, 4), "achieved_gbs": round(cg, 1),
+                "frac": round(cg / peaks["hbm_gbs"], 4),
+                "derivation": "timed step minus the alone times of all other stages; the chains' "
+                              "scores and PV overlap across chunks, so this is their joint in-step rate"}
 
     # same kernels, unchunked (speed loss) — when it fits
     caller_bytes = sum(doc.nbytes(t) for t in doc.inputs + doc.outputs)
