@@ -12,6 +12,10 @@
 
 #include "kernels.h"
 
+#ifndef LNC_JT
+#define LNC_JT 128
+#endif
+
 namespace ac {
 namespace {
 
@@ -708,58 +712,60 @@ cudaError_t layernorm_dispatch(const void* x, const void* g, const void* b, void
 // LayerNorm over the leading (channel) dim of x [C, I, J] written channel-last,
 // y[i, j, :] = gamma * (x[:, i, j] - mu) / sqrt(var + eps) + beta (ln_cfirst, AF2
 // Alg. 11 line 4: the LN of the triangle product, whose GEMM leaves it channel-major).
-// One CTA per (i, 64 j): the [C x 64] tile is read coalesced along j into shared
-// memory (fp32, pitch 65), four threads per column fold its mean and then its
+// One CTA per (i, JT j): the [C x JT] tile is read coalesced along j into shared
+// memory (fp32, pitch JT + 1), 256 / JT threads per column fold its mean and then its
 // variance (two passes, fp32), and the normalised tile leaves coalesced along c in
 // 16-byte vectors.  HBM-bound: one read and one write of x.
-template <typename T>
+template <typename T, int JT>
 __global__ void __launch_bounds__(256) ln_cfirst_kernel(const T* __restrict__ x, int64_t xs_c, int64_t xs_i,
                                                          const T* __restrict__ g, const T* __restrict__ b,
                                                          T* __restrict__ y, int64_t ys_i, int64_t ys_j, int C,
                                                          int64_t J, float eps, int pdl) {
-  extern __shared__ float lsm[];  // [C][65] values, then mu[64], rstd[64]
-  float* mu = lsm + C * 65;
-  float* rs = mu + 64;
+  constexpr int PT = JT + 1;     // smem pitch (odd: column reads conflict-free)
+  constexpr int TPC = 256 / JT;  // threads per column in the statistics pass
+  extern __shared__ float lsm[];  // [C][JT + 1] values, then mu[JT], rstd[JT]
+  float* mu = lsm + C * PT;
+  float* rs = mu + JT;
   if (pdl) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   }
   const int64_t i = blockIdx.y;
-  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * 64;
-  const int jn = static_cast<int>(J - j0 < 64 ? J - j0 : 64);
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * JT;
+  const int jn = static_cast<int>(J - j0 < JT ? J - j0 : JT);
   constexpr int VL = 16 / sizeof(T);  // elements per 16-byte load
-  if (jn == 64 && (xs_c % VL) == 0 && (xs_i % VL) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+  if (jn == JT && (xs_c % VL) == 0 && (xs_i % VL) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
     // full tile: 16-byte loads along j (a c-row of the tile is 64 / VL vectors)
-    for (int idx = threadIdx.x; idx < C * (64 / VL); idx += 256) {
-      const int c = idx / (64 / VL), jv = (idx - c * (64 / VL)) * VL;
+    for (int idx = threadIdx.x; idx < C * (JT / VL); idx += 256) {
+      const int c = idx / (JT / VL), jv = (idx - c * (JT / VL)) * VL;
       Vec<T> v;
       v.raw = *reinterpret_cast<const uint4*>(x + c * xs_c + i * xs_i + j0 + jv);
       float f[VL];
       v.to_float(f);
 #pragma unroll
-      for (int e = 0; e < VL; ++e) lsm[c * 65 + jv + e] = f[e];
+      for (int e = 0; e < VL; ++e) lsm[c * PT + jv + e] = f[e];
     }
   } else {
-    for (int idx = threadIdx.x; idx < C * 64; idx += 256) {
-      const int c = idx >> 6, jj = idx & 63;
-      lsm[c * 65 + jj] = jj < jn ? static_cast<float>(x[c * xs_c + i * xs_i + j0 + jj]) : 0.f;
+    for (int idx = threadIdx.x; idx < C * JT; idx += 256) {
+      const int c = idx / JT, jj = idx % JT;
+      lsm[c * PT + jj] = jj < jn ? static_cast<float>(x[c * xs_c + i * xs_i + j0 + jj]) : 0.f;
     }
   }
   __syncthreads();
   {
-    const int col = threadIdx.x >> 2, part = threadIdx.x & 3;
+    const int col = threadIdx.x / TPC, part = threadIdx.x % TPC;
     float s = 0.f;
-    for (int c = part; c < C; c += 4) s += lsm[c * 65 + col];
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    for (int c = part; c < C; c += TPC) s += lsm[c * PT + col];
+#pragma unroll
+    for (int o = 1; o < TPC; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     const float m = s / static_cast<float>(C);
     float q = 0.f;
-    for (int c = part; c < C; c += 4) {
-      const float d = lsm[c * 65 + col] - m;
+    for (int c = part; c < C; c += TPC) {
+      const float d = lsm[c * PT + col] - m;
       q += d * d;
     }
-    q += __shfl_xor_sync(0xffffffffu, q, 1);
-    q += __shfl_xor_sync(0xffffffffu, q, 2);
+#pragma unroll
+    for (int o = 1; o < TPC; o <<= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
     if (part == 0) {
       mu[col] = m;
       rs[col] = 1.f / sqrtf(q / static_cast<float>(C) + eps);
@@ -777,7 +783,7 @@ __global__ void __launch_bounds__(256) ln_cfirst_kernel(const T* __restrict__ x,
     gv.to_float(gf);
     bv.to_float(bf);
 #pragma unroll
-    for (int e = 0; e < VN; ++e) of[e] = (lsm[(c0 + e) * 65 + jj] - mu[jj]) * rs[jj] * gf[e] + bf[e];
+    for (int e = 0; e < VN; ++e) of[e] = (lsm[(c0 + e) * PT + jj] - mu[jj]) * rs[jj] * gf[e] + bf[e];
     o.from_float(of);
     *reinterpret_cast<uint4*>(y + i * ys_i + (j0 + jj) * ys_j + c0) = o.raw;
   }
@@ -792,8 +798,13 @@ cudaError_t layernorm_cfirst(const void* x, int64_t xs_c, int64_t xs_i, const vo
   const int VN = dtype == 1 ? 8 : 4;
   auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
   if (C % VN || C > 1024 || ys_j % VN || ys_i % VN || !al(y) || !al(gamma) || !al(beta)) return cudaErrorInvalidValue;
-  const size_t smem = (static_cast<size_t>(C) * 65 + 128) * 4;
-  dim3 grid(static_cast<unsigned>((J + 63) / 64), static_cast<unsigned>(I));
+  // bf16: 128-column j tiles (each block reads 256 contiguous bytes of every channel row,
+  // the rows being a 2 MB page apart for the AlphaFold pair tensor); fp32: 64
+  constexpr int JTB = LNC_JT;
+  const bool wide = dtype == 1 && (static_cast<size_t>(C) * (JTB + 1) + 2 * JTB) * 4 <= 200 * 1024;
+  const int JT = wide ? JTB : 64;
+  const size_t smem = (static_cast<size_t>(C) * (JT + 1) + 2 * JT) * 4;
+  dim3 grid(static_cast<unsigned>((J + JT - 1) / JT), static_cast<unsigned>(I));
   auto launch = [&](auto kern, auto* X, auto* G, auto* B, auto* Y) -> cudaError_t {
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -817,10 +828,13 @@ cudaError_t layernorm_cfirst(const void* x, int64_t xs_c, int64_t xs_i, const vo
   };
   if (dtype == 1) {
     using T = __nv_bfloat16;
-    return launch(ln_cfirst_kernel<T>, static_cast<const T*>(x), static_cast<const T*>(gamma),
+    if (wide)
+      return launch(ln_cfirst_kernel<T, JTB>, static_cast<const T*>(x), static_cast<const T*>(gamma),
+                    static_cast<const T*>(beta), static_cast<T*>(y));
+    return launch(ln_cfirst_kernel<T, 64>, static_cast<const T*>(x), static_cast<const T*>(gamma),
                   static_cast<const T*>(beta), static_cast<T*>(y));
   }
-  return launch(ln_cfirst_kernel<float>, static_cast<const float*>(x), static_cast<const float*>(gamma),
+  return launch(ln_cfirst_kernel<float, 64>, static_cast<const float*>(x), static_cast<const float*>(gamma),
                 static_cast<const float*>(beta), static_cast<float*>(y));
 }
 
