@@ -707,11 +707,11 @@ def main():
         other_ms = sum(v[1] for k, v in kt.items() if k not in chain) / kp
         if chain and roof is not None and ms_step - other_ms > 0:
             cb = sum(algorithmic(doc, k)[1] for k in chain)
-            cg = cb / ((ms_step - other_ms) / 1e3) / 1e9
+            chain_gbs = cb / ((ms_step - other_ms) / 1e3) / 1e9
             roof["f2_chains_in_step"] = {
                 "nodes": sorted(chain), "algorithmic_bytes_per_step": int(cb),
-                "ms": round(ms_step - other_ms, 4), "achieved_gbs": round(cg, 1),
-                "frac": round(cg / peaks["hbm_gbs"], 4),
+                "ms": round(ms_step - other_ms, 4), "achieved_gbs": round(chain_gbs, 1),
+                "frac": round(chain_gbs / peaks["hbm_gbs"], 4),
                 "derivation": "timed step minus the alone times of all other stages; the chains' "
                               "scores and PV overlap across chunks, so this is their joint in-step rate"}
 
